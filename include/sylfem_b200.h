@@ -1,0 +1,166 @@
+/*
+ * sylfem_b200.h — C ABI of the B200-native MO-FEM solve path.
+ *
+ * The reference (`sylfem`, a pure-Python package) has no FFI: its plugin
+ * boundary is the Python API.  These entry points are what a ctypes/cffi
+ * binding of that API binds; each cites the reference
+ * function it replaces (paths relative to /root/reference/pkg/src/sylfem/).
+ *
+ * Conventions
+ *  - Grid matrices are q_y x q_x, row-major (rows follow y, columns follow x,
+ *    operators.py:1-9) with an explicit leading dimension `ld*`.
+ *  - Pointers named *_dev are device pointers; *_host are host pointers.
+ *  - `stream` is a cudaStream_t (may be NULL = legacy default stream).  Calls
+ *    order themselves after prior work on `stream`, and work they leave
+ *    pending is ordered before later work on `stream`.
+ *  - Every function returns SFB_OK (0) or a negative status; the message is
+ *    available from sfb_last_error() (thread-local).  The Python shim maps
+ *    statuses to the reference exception classes and messages.
+ *  - Band storage: a left factor G (q_y x q_y) is stored as gband[i][d] =
+ *    G[i][i + goff + d], d = 0..gw-1; a right factor H (acting as U H) is
+ *    stored by columns: hband[j][e] = H[j + hoff + e][j], e = 0..hw-1.
+ *    Multi-term operators store all terms back to back ([nterms][rows][w]).
+ */
+#ifndef SYLFEM_B200_H
+#define SYLFEM_B200_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (mapped to sylfem exceptions by the Python shim) ---- */
+enum {
+    SFB_OK = 0,
+    SFB_ERR_ARG = -1,          /* bad argument / shape      -> OperatorError  */
+    SFB_ERR_CUDA = -2,         /* CUDA runtime failure      -> SolverError    */
+    SFB_ERR_NOMEM = -3,        /* device allocation failed  -> SolverError    */
+    SFB_ERR_UNSUPPORTED = -4   /* band width / term count beyond the kernels  */
+};
+
+/* MO-PCG stop reasons (solvers.py:415-453) */
+enum {
+    SFB_PCG_RUNNING = 0,
+    SFB_PCG_TOLERANCE = 1,     /* "tolerance"                                 */
+    SFB_PCG_INCREMENT = 2,     /* "increment"                                 */
+    SFB_PCG_INDEFINITE = 3,    /* <L(Q),Q> <= 0   -> OperatorError            */
+    SFB_PCG_NONFINITE = 4,     /* residual not finite -> SolverError          */
+    SFB_PCG_MAX_ITER = 5       /* "max_iter" (report, not an error)           */
+};
+
+/* stopping rule kinds (solvers.py:53-83) */
+enum { SFB_RULE_RESIDUAL = 0, SFB_RULE_INCREMENT = 1 };
+
+/* preconditioner / spectral sandwich kinds (solvers.py:103-150, 211-300) */
+enum {
+    SFB_PRE_IDENTITY = 0,      /* Z = R (copy)                                */
+    SFB_PRE_INVERSE = 1,       /* Z = Linv R RinvT^T    (2 DMMA GEMMs)        */
+    SFB_PRE_SPECTRAL_PROD = 2, /* Z = VL [(VL^T R VR) / (lamL_i lamR_j)] VR^T */
+    SFB_PRE_SPECTRAL_SUM = 3,  /* Z = VL [(VL^T R VR) / (lamL_i + lamR_j)] VR^T (reduced solve) */
+    SFB_PRE_BANDED = 4         /* Z = PL^-1 R PR^-1 by banded Cholesky sweeps */
+};
+
+typedef struct sfb_op sfb_op;
+typedef struct sfb_map sfb_map;
+typedef struct sfb_pre sfb_pre;
+typedef struct sfb_pcg sfb_pcg;
+
+typedef struct {
+    int iterations;       /* completed iterations                        */
+    int stop_reason;      /* SFB_PCG_*                                   */
+    int bad_iter;         /* iteration of INDEFINITE / NONFINITE         */
+    int chunks;           /* graph launches used                         */
+    double res0;          /* |R_0|                                       */
+    double bad_value;     /* <L(Q),Q> at INDEFINITE                      */
+    double device_ms;     /* device time of the iteration loop           */
+} sfb_pcg_result;
+
+/* ---- library ---------------------------------------------------------- */
+int sfb_version(void);
+const char* sfb_last_error(void);
+/* Select the device and warm the driver entry points; reports SM count. */
+int sfb_init(int device, int* sm_count);
+
+/* ---- operator: SylvesterOperator (operators.py:97-138) ----------------- */
+/* Banded term list W = sum_t G_t U H_t.  Bands are uploaded once. */
+int sfb_op_create(int qy, int qx, int nterms,
+                  int gw, int goff, const double* gband_host,
+                  int hw, int hoff, const double* hband_host, sfb_op** out);
+/* Dense term list (factors too wide for the banded kernels). */
+int sfb_op_create_dense(int qy, int qx, int nterms, const double* G_host,
+                        const double* H_host, sfb_op** out);
+/* W = op(U)  (SylvesterOperator.apply, operators.py:124-131). */
+int sfb_op_apply(const sfb_op* op, const double* U_dev, int ldu,
+                 double* W_dev, int ldw, void* stream);
+/* out2_host = { |op(U) - rhs|_F, |rhs|_F }  (solvers.py:293-294). */
+int sfb_op_residual(const sfb_op* op, const double* U_dev, int ldu,
+                    const double* rhs_dev, int ldr, double* out2_host, void* stream);
+int sfb_op_destroy(sfb_op* op);
+
+/* ---- rectangular banded map: the rhs builders (operators.py:206-207,
+ *      228-232, 266-268, 281-282) --------------------------------------- */
+int sfb_map_create(int out_rows, int out_cols, int in_rows, int in_cols,
+                   int gw, int goff, const double* gband_host,
+                   int hw, int hoff, const double* hband_host, sfb_map** out);
+/* out = G F H^T over the full node grid F. */
+int sfb_map_apply(const sfb_map* m, const double* F_dev, int ldf,
+                  double* out_dev, int ldo, void* stream);
+/* IMEX heat rhs (timestepping.py:150-153): W = expand(U) + c F, checked for
+ * blow-up, then out = G W H^T.  U is the interior state placed at full-grid
+ * offset (row_shift, col_shift); F may be NULL.  check2_host (nullable) =
+ * { max|W|, number of non-finite entries }. */
+int sfb_map_apply_heat(const sfb_map* m, const double* U_dev, int ldu,
+                       int row_shift, int col_shift, double c,
+                       const double* F_dev, int ldf, double* out_dev, int ldo,
+                       double* check2_host, void* stream);
+/* IMEX DIB rhs (timestepping.py:201-207, models.py:74-82): species 0 uses
+ * W = U + tau_rho f(U,V), species 1 W = V + tau_rho g(U,V); then
+ * out = G W H^T.  params = {alpha, gamma_k, A1, A2, B, C, D, k2, k3}. */
+int sfb_map_apply_dib(const sfb_map* m, const double* U_dev, const double* V_dev,
+                      int ld, int species, double tau_rho, const double* params_host,
+                      double* out_dev, int ldo, double* check2_host, void* stream);
+int sfb_map_destroy(sfb_map* m);
+
+/* ---- preconditioner / spectral sandwich (solvers.py:103-150, 284-300) -- */
+/* kind SFB_PRE_INVERSE: L = P_L^-1 (q_y x q_y), R = (P_R^-1)^T (q_x x q_x).
+ * kind SFB_PRE_SPECTRAL_*: L = V_L, R = V_R, lamL/lamR eigenvalues.
+ * kind SFB_PRE_BANDED: L/R = banded Cholesky factors, see sfb_pre_create_banded.
+ * Host arrays are row-major and uploaded once. */
+int sfb_pre_create(int qy, int qx, int kind, const double* L_host,
+                   const double* R_host, const double* lamL_host,
+                   const double* lamR_host, sfb_pre** out);
+/* Banded SPD factors: lower Cholesky factors in band storage
+ * lband[i][d] = C_L[i][i - bw + d] (d = 0..bw), same for the right factor. */
+int sfb_pre_create_banded(int qy, int qx, int bwL, const double* lband_host,
+                          int bwR, const double* rband_host, sfb_pre** out);
+/* Z = P^-1 R  (Preconditioner.apply_inverse, solvers.py:134-143), or the
+ * reduced-solve sandwich (solvers.py:292) for SFB_PRE_SPECTRAL_SUM. */
+int sfb_pre_apply(const sfb_pre* p, const double* R_dev, int ldr,
+                  double* Z_dev, int ldz, void* stream);
+/* Y = V_L^T X V_R for the spectral kinds (the forward spectral transform;
+ * used by the closed-form residual, solvers.py:345-348). */
+int sfb_pre_transform(const sfb_pre* p, const double* X_dev, int ldx, double* Y_dev, int ldy, void* stream);
+int sfb_pre_destroy(sfb_pre* p);
+
+/* ---- MO-PCG (solvers.py:365-453) --------------------------------------- */
+int sfb_pcg_create(const sfb_op* op, const sfb_pre* pre, sfb_pcg** out);
+/* Runs the full device-resident loop.  u0_dev may be NULL (U0 = 0).
+ * history_host holds max_iter+1 doubles (|R_s|), increments_host max_iter
+ * (|alpha| |Q|).  iterates_dev (nullable) receives up to n_iterates
+ * contiguous q_y x q_x copies of U_0, U_1, ... (record_iterates). */
+int sfb_pcg_solve(sfb_pcg* s, const double* rhs_dev, int ldr,
+                  const double* u0_dev, int ldu0, double* U_dev, int ldu,
+                  int rule, double value, int max_iter,
+                  double* history_host, double* increments_host,
+                  double* iterates_dev, int n_iterates,
+                  sfb_pcg_result* res, void* stream);
+int sfb_pcg_destroy(sfb_pcg* s);
+
+/* ---- reductions for the IMEX drivers (timestepping.py:89-91, 155, 210-215) */
+/* out4_host = { |A - B|_F (B may be NULL), max|A|, #non-finite(A), |A|_F }. */
+int sfb_diff_norm(const double* A_dev, int lda, const double* B_dev, int ldb,
+                  int rows, int cols, double* out4_host, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SYLFEM_B200_H */

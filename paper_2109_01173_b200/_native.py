@@ -1,0 +1,179 @@
+"""ctypes binding of the sm_100a library (include/sylfem_b200.h).
+
+There is no CPU fallback: if the shared library is missing or no CUDA device
+is visible, every device entry point raises.  PyTorch is used only as the
+device-memory / stream plumbing (tensors are passed to the C ABI as raw
+pointers).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+import numpy as np
+
+from .exceptions import OperatorError, SolverError, SylfemError
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsylfem_b200.so")
+
+# status codes / kinds (mirror include/sylfem_b200.h)
+OK, ERR_ARG, ERR_CUDA, ERR_NOMEM, ERR_UNSUPPORTED = 0, -1, -2, -3, -4
+PCG_RUNNING, PCG_TOLERANCE, PCG_INCREMENT, PCG_INDEFINITE, PCG_NONFINITE, PCG_MAX_ITER = range(6)
+RULE_RESIDUAL, RULE_INCREMENT = 0, 1
+PRE_IDENTITY, PRE_INVERSE, PRE_SPECTRAL_PROD, PRE_SPECTRAL_SUM, PRE_BANDED = range(5)
+
+EXPORTS = [
+    "sfb_version", "sfb_last_error", "sfb_init",
+    "sfb_op_create", "sfb_op_create_dense", "sfb_op_apply", "sfb_op_residual", "sfb_op_destroy",
+    "sfb_map_create", "sfb_map_apply", "sfb_map_apply_heat", "sfb_map_apply_dib", "sfb_map_destroy",
+    "sfb_pre_create", "sfb_pre_create_banded", "sfb_pre_apply", "sfb_pre_transform", "sfb_pre_destroy",
+    "sfb_pcg_create", "sfb_pcg_solve", "sfb_pcg_destroy", "sfb_diff_norm",
+]
+
+
+class PcgResult(C.Structure):
+    _fields_ = [("iterations", C.c_int), ("stop_reason", C.c_int), ("bad_iter", C.c_int),
+                ("chunks", C.c_int), ("res0", C.c_double), ("bad_value", C.c_double),
+                ("device_ms", C.c_double)]
+
+
+_P = C.c_void_p
+_D = C.c_double
+_I = C.c_int
+_DP = C.POINTER(C.c_double)
+
+_SIGS = {
+    "sfb_version": (_I, []),
+    "sfb_last_error": (C.c_char_p, []),
+    "sfb_init": (_I, [_I, C.POINTER(_I)]),
+    "sfb_op_create": (_I, [_I, _I, _I, _I, _I, _P, _I, _I, _P, C.POINTER(_P)]),
+    "sfb_op_create_dense": (_I, [_I, _I, _I, _P, _P, C.POINTER(_P)]),
+    "sfb_op_apply": (_I, [_P, _P, _I, _P, _I, _P]),
+    "sfb_op_residual": (_I, [_P, _P, _I, _P, _I, _DP, _P]),
+    "sfb_op_destroy": (_I, [_P]),
+    "sfb_map_create": (_I, [_I, _I, _I, _I, _I, _I, _P, _I, _I, _P, C.POINTER(_P)]),
+    "sfb_map_apply": (_I, [_P, _P, _I, _P, _I, _P]),
+    "sfb_map_apply_heat": (_I, [_P, _P, _I, _I, _I, _D, _P, _I, _P, _I, _DP, _P]),
+    "sfb_map_apply_dib": (_I, [_P, _P, _P, _I, _I, _D, _DP, _P, _I, _DP, _P]),
+    "sfb_map_destroy": (_I, [_P]),
+    "sfb_pre_create": (_I, [_I, _I, _I, _P, _P, _P, _P, C.POINTER(_P)]),
+    "sfb_pre_create_banded": (_I, [_I, _I, _I, _P, _I, _P, C.POINTER(_P)]),
+    "sfb_pre_apply": (_I, [_P, _P, _I, _P, _I, _P]),
+    "sfb_pre_transform": (_I, [_P, _P, _I, _P, _I, _P]),
+    "sfb_pre_destroy": (_I, [_P]),
+    "sfb_pcg_create": (_I, [_P, _P, C.POINTER(_P)]),
+    "sfb_pcg_solve": (_I, [_P, _P, _I, _P, _I, _P, _I, _I, _D, _I, _DP, _DP, _P, _I,
+                           C.POINTER(PcgResult), _P]),
+    "sfb_pcg_destroy": (_I, [_P]),
+    "sfb_diff_norm": (_I, [_P, _I, _P, _I, _I, _I, _DP, _P]),
+}
+
+_lib = None
+_lock = threading.Lock()
+_initialized = False
+
+
+def load_library():
+    """Load the shared library (no device needed).  Raises if it was not built."""
+    global _lib
+    if _lib is None:
+        with _lock:
+            if _lib is None:
+                if not os.path.exists(LIB_PATH):
+                    raise SylfemError(f"{LIB_PATH} is missing: build it with "
+                                      "`python -m paper_2109_01173_b200.build` (no CPU fallback)")
+                lib = C.CDLL(LIB_PATH)
+                for name, (res, args) in _SIGS.items():
+                    fn = getattr(lib, name)
+                    fn.restype = res
+                    fn.argtypes = args
+                _lib = lib
+    return _lib
+
+
+def lib():
+    """The library with a CUDA device initialised (raises loudly otherwise)."""
+    global _initialized
+    L = load_library()
+    if not _initialized:
+        with _lock:
+            if not _initialized:
+                import torch
+                if not torch.cuda.is_available():
+                    raise SylfemError("paper_2109_01173_b200 needs a CUDA device (B200); "
+                                      "there is no CPU fallback")
+                torch.cuda.init()
+                dev = torch.cuda.current_device()
+                n = C.c_int(0)
+                check(L.sfb_init(dev, C.byref(n)), "init")
+                _initialized = True
+    return L
+
+
+def last_error() -> str:
+    return load_library().sfb_last_error().decode(errors="replace")
+
+
+def check(rc: int, what: str = "") -> None:
+    if rc == OK:
+        return
+    msg = last_error()
+    where = f"{what}: " if what else ""
+    if rc == ERR_ARG:
+        raise OperatorError(where + msg)
+    raise SolverError(where + msg)
+
+
+# ---------------------------------------------------------------- torch glue
+def torch():
+    import torch as _t
+    return _t
+
+
+def stream() -> int:
+    t = torch()
+    return t.cuda.current_stream().cuda_stream
+
+
+def to_device(a):
+    """numpy / torch -> contiguous float64 CUDA tensor."""
+    t = torch()
+    if isinstance(a, t.Tensor):
+        return a.to(device="cuda", dtype=t.float64).contiguous()
+    return t.from_numpy(np.ascontiguousarray(np.asarray(a, dtype=np.float64))).to("cuda")
+
+
+def ptr(t) -> int:
+    return t.data_ptr()
+
+
+def host_ptr(a: np.ndarray):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def dptr(a: np.ndarray):
+    return a.ctypes.data_as(_DP)
+
+
+def is_device(a) -> bool:
+    t = torch()
+    return isinstance(a, t.Tensor) and a.is_cuda
+
+
+class Handle:
+    """Owns a native object; destroyed with its Python wrapper."""
+
+    def __init__(self, p, destroy):
+        self.p = p
+        self._destroy = destroy
+
+    def __del__(self):
+        try:
+            if self.p and _lib is not None:
+                self._destroy(self.p)
+        except Exception:  # interpreter shutdown
+            pass
+        self.p = None

@@ -1,0 +1,99 @@
+// Kernel-level interfaces shared between the translation units.
+#pragma once
+
+#include "sfb_common.cuh"
+
+namespace sfb {
+
+// ------------------------------------------------------------- GEMM -------
+enum GemmEpiMode {
+    EPI_STORE = 0,          // C[m][n] = acc
+    EPI_STORE_T = 1,        // C[n][m] = acc
+    EPI_HADAMARD_SUM = 2,   // C[m][n] = acc / (sr[m] + sc[n])      (solvers.py:245-253)
+    EPI_HADAMARD_PROD = 3,  // C[m][n] = acc * sr[m] * sc[n]        (sr, sc = 1/lambda)
+    EPI_STORE_DOT = 4,      // C[m][n] = acc; dot += acc * D[m][n]  (<Z,R>, solvers.py:448)
+    EPI_ACCUM = 5           // C[m][n] += acc
+};
+
+struct GemmEpi {
+    int mode = EPI_STORE;
+    double* C = nullptr;
+    int ldc = 0;
+    const double* sr = nullptr;
+    const double* sc = nullptr;
+    const double* D = nullptr;
+    int ldd = 0;
+    double* partials = nullptr;   // one per CTA (EPI_STORE_DOT)
+    unsigned* counter = nullptr;  // last-block counter (EPI_STORE_DOT)
+    PcgState* pcg = nullptr;      // status gate; receives rz_next
+    double* dot_out = nullptr;    // receives the dot total when non-null
+};
+
+int launch_dgemm_nt(const double* A, int lda, const double* Bt, int ldb, int M, int N, int K,
+                    const GemmEpi& ep, cudaStream_t stream);
+int gemm_grid_blocks(int M, int N);
+int gemm_smem_bytes();
+
+// ----------------------------------------------------------- banded -------
+enum BandLoad { LD_PLAIN = 0, LD_PCG = 1, LD_HEAT = 2, LD_DIB = 3 };
+enum BandEpi { EP_STORE = 0, EP_PCG = 1 };
+
+struct BandArgs {
+    int out_rows = 0, out_cols = 0, in_rows = 0, in_cols = 0;
+    int nterms = 0, width = 1, goff = 0, hoff = 0;
+    const double* gband = nullptr;  // [nterms][out_rows][width]
+    const double* hband = nullptr;  // [nterms][out_cols][width]
+    // loader
+    int ld_mode = LD_PLAIN;
+    const double* X = nullptr;  // plain input / Z (PCG) / U (heat, DIB)
+    int ldx = 0;
+    const double* X2 = nullptr;  // V (DIB) / F (heat)
+    int ldx2 = 0;
+    double* Q0 = nullptr;  // PCG direction double buffer
+    double* Q1 = nullptr;
+    int ldq = 0;
+    double c = 0.0;        // heat source scale / DIB tau*rho
+    int rs = 0, cs = 0;    // heat: full-grid offset of the interior state
+    int species = 0;
+    double kp[9] = {0};    // DIB parameters
+    unsigned long long* check = nullptr;  // [max|W| bits, non-finite flag]
+    // epilogue
+    int ep_mode = EP_STORE;
+    double* W = nullptr;
+    int ldw = 0;
+    double* partials = nullptr;  // [2][nblocks]
+    PcgState* pcg = nullptr;
+};
+
+int launch_band(const BandArgs& a, cudaStream_t stream);
+bool band_supported(int nterms, int width);
+int band_grid_blocks(int out_rows, int out_cols);
+
+// ----------------------------------------------------------- vector -------
+int launch_pcg_init_plain(const double* rhs, int ldr, double* R, double* U, int ld, int rows, int cols,
+                          double* partials, PcgState* st, double* hist, cudaStream_t s);
+int launch_pcg_init_warm(const double* rhs, int ldr, const double* W, double* R, int ld, int rows,
+                         int cols, double* partials, PcgState* st, double* hist, cudaStream_t s);
+int launch_pcg_direction(const double* Z, double* Q0, double* Q1, int ld, int rows, int cols,
+                         PcgState* st, cudaStream_t s);
+int launch_pcg_dots(const double* W, const double* Q0, const double* Q1, int ld, int rows, int cols,
+                    double* partials, PcgState* st, cudaStream_t s);
+int launch_pcg_update(double* U, double* R, const double* W, const double* Q0, const double* Q1, int ld,
+                      int rows, int cols, double* partials, PcgState* st, double* hist, double* incs,
+                      cudaStream_t s);
+int launch_pcg_record(const double* U, int ld, int rows, int cols, double* iterates, PcgState* st,
+                      cudaStream_t s);
+int launch_copy_dot(const double* R, double* Z, int ld, int rows, int cols, double* partials,
+                    PcgState* st, RedSlots* red, cudaStream_t s);
+int launch_loop_ctl(PcgState* st, unsigned long long handle, int use_handle, cudaStream_t s);
+int launch_norms(const double* A, int lda, const double* B, int ldb, int rows, int cols, double* partials,
+                 RedSlots* out, cudaStream_t s);
+int vector_grid_blocks();
+
+// ------------------------------------------------------ banded solves ----
+int launch_band_chol_cols(const double* lband, int bw, int n, double* X, int ld, int ncols,
+                          cudaStream_t s);
+int launch_band_chol_rows(const double* rband, int bw, int n, double* X, int ld, int nrows,
+                          cudaStream_t s);
+
+}  // namespace sfb

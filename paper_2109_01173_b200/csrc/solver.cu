@@ -1,0 +1,953 @@
+// Objects behind the C ABI (include/sylfem_b200.h): device-resident operators,
+// rhs maps, preconditioners and the MO-PCG driver.
+//
+// MO-PCG (solvers.py:365-453) runs entirely on the device: scalars (alpha,
+// beta, |R|, stop test) live in a PcgState and are produced by the last CTA
+// of the kernel that finishes each reduction, so no iteration needs a host
+// round trip.  One iteration is captured once into the body of a CUDA-graph
+// WHILE node whose condition is set by a one-thread control kernel; a whole
+// solve is then a single graph launch and one final synchronisation.
+#include <cuda.h>
+
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "sfb_common.cuh"
+#include "sfb_kernels.cuh"
+
+namespace sfb {
+
+static thread_local std::string g_last_error;
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+namespace {
+
+int dalloc(double** p, size_t n) {
+    if (n == 0) n = 1;
+    cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), n * sizeof(double));
+    if (e != cudaSuccess) {
+        set_error(std::string("cudaMalloc: ") + cudaGetErrorString(e));
+        return SFB_ERR_NOMEM;
+    }
+    return SFB_OK;
+}
+
+template <class T>
+int talloc(T** p, size_t bytes) {
+    cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), bytes);
+    if (e != cudaSuccess) {
+        set_error(std::string("cudaMalloc: ") + cudaGetErrorString(e));
+        return SFB_ERR_NOMEM;
+    }
+    return SFB_OK;
+}
+
+// Upload a host matrix (rows x cols, contiguous) into a device buffer with
+// leading dimension ld (zero padded).
+int upload_padded(double* dst, int ld, const double* src, int rows, int cols) {
+    SFB_CUDA_TRY(cudaMemset(dst, 0, (size_t)rows * ld * sizeof(double)));
+    SFB_CUDA_TRY(cudaMemcpy2D(dst, (size_t)ld * sizeof(double), src, (size_t)cols * sizeof(double),
+                              (size_t)cols * sizeof(double), rows, cudaMemcpyHostToDevice));
+    return SFB_OK;
+}
+
+struct ScopedFree {
+    std::vector<void*> ptrs;
+    cudaStream_t s;
+    explicit ScopedFree(cudaStream_t st) : s(st) {}
+    ~ScopedFree() {
+        for (void* p : ptrs) cudaFreeAsync(p, s);
+    }
+    template <class T>
+    int get(T** p, size_t bytes) {
+        cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(p), bytes ? bytes : 8, s);
+        if (e != cudaSuccess) {
+            set_error(std::string("cudaMallocAsync: ") + cudaGetErrorString(e));
+            return SFB_ERR_NOMEM;
+        }
+        ptrs.push_back(*p);
+        return SFB_OK;
+    }
+};
+
+inline int pad_ld(int cols) { return round_up(cols < 1 ? 1 : cols, 32); }
+
+}  // namespace
+}  // namespace sfb
+
+using namespace sfb;
+
+// =========================================================== operators ====
+struct sfb_op {
+    int qy = 0, qx = 0, nterms = 0;
+    bool dense = false;
+    int width = 1, goff = 0, hoff = 0;
+    double* gband = nullptr;
+    double* hband = nullptr;
+    // dense fallback: G_t (qy x qy) and H_t^T (qx x qx), padded rows
+    double* G = nullptr;
+    double* Ht = nullptr;
+    int ldG = 0, ldH = 0;
+};
+
+struct sfb_map {
+    int out_rows = 0, out_cols = 0, in_rows = 0, in_cols = 0;
+    int width = 1, goff = 0, hoff = 0;
+    double* gband = nullptr;
+    double* hband = nullptr;
+};
+
+struct sfb_pre {
+    int kind = SFB_PRE_IDENTITY;
+    int qy = 0, qx = 0;
+    // INVERSE: A1 = P_L^-1, B1 = (P_R^-1)^T.  SPECTRAL: A1 = V_L, A1t = V_L^T,
+    // B1 = V_R, B1t = V_R^T, sl/sr = lambda (sum) or 1/lambda (prod).
+    double *A1 = nullptr, *A1t = nullptr, *B1 = nullptr, *B1t = nullptr;
+    int ldA = 0, ldB = 0;
+    double *sl = nullptr, *sr = nullptr;
+    // BANDED: lower Cholesky factors in band storage
+    double *lband = nullptr, *rband = nullptr;
+    int bwL = 0, bwR = 0;
+};
+
+namespace sfb {
+namespace {
+
+// W = op(U) on device buffers (U must have an even ld and 16B alignment for
+// the dense path).  T1 is qx x qy scratch (ld ldt) for the dense path.
+int op_apply_impl(const sfb_op* op, const double* U, int ldu, double* W, int ldw, double* T1, int ldt,
+                  cudaStream_t s) {
+    if (!op->dense) {
+        BandArgs a;
+        a.out_rows = a.in_rows = op->qy;
+        a.out_cols = a.in_cols = op->qx;
+        a.nterms = op->nterms;
+        a.width = op->width;
+        a.goff = op->goff;
+        a.hoff = op->hoff;
+        a.gband = op->gband;
+        a.hband = op->hband;
+        a.ld_mode = LD_PLAIN;
+        a.X = U;
+        a.ldx = ldu;
+        a.ep_mode = EP_STORE;
+        a.W = W;
+        a.ldw = ldw;
+        return launch_band(a, s);
+    }
+    for (int t = 0; t < op->nterms; ++t) {
+        GemmEpi e1;
+        e1.mode = EPI_STORE_T;  // T1 = (U H_t)^T
+        e1.C = T1;
+        e1.ldc = ldt;
+        SFB_TRY(launch_dgemm_nt(U, ldu, op->Ht + (size_t)t * op->qx * op->ldH, op->ldH, op->qy, op->qx, op->qx,
+                                e1, s));
+        GemmEpi e2;
+        e2.mode = t == 0 ? EPI_STORE : EPI_ACCUM;  // W (+)= G_t (U H_t)
+        e2.C = W;
+        e2.ldc = ldw;
+        SFB_TRY(launch_dgemm_nt(op->G + (size_t)t * op->qy * op->ldG, op->ldG, T1, ldt, op->qy, op->qx, op->qy,
+                                e2, s));
+    }
+    return SFB_OK;
+}
+
+// Z = P^-1 R (or the reduced-solve sandwich).  R/Z device buffers with even
+// ld; T1 (qx x qy, ldt1) and T2 (qy x qx, ldt2) scratch.  When `pcg` is set,
+// kernels are gated on its status and <Z,R> lands in pcg->rz_next; otherwise
+// it lands in red->v[3] when red is set.
+int pre_apply_impl(const sfb_pre* p, const double* R, int ldr, double* Z, int ldz, double* T1, int ldt1,
+                   double* T2, int ldt2, double* partials, PcgState* pcg, RedSlots* red, cudaStream_t s) {
+    const int qy = p->qy, qx = p->qx;
+    unsigned* counter = pcg ? &pcg->counter[4] : (red ? &red->counter[2] : nullptr);
+    GemmEpi last;
+    last.mode = (pcg || red) ? EPI_STORE_DOT : EPI_STORE;
+    last.C = Z;
+    last.ldc = ldz;
+    last.D = R;
+    last.ldd = ldr;
+    last.partials = partials;
+    last.counter = counter;
+    last.pcg = pcg;
+    last.dot_out = red ? &red->v[3] : nullptr;
+    switch (p->kind) {
+        case SFB_PRE_IDENTITY:
+            if (ldr != ldz) return arg_error("identity preconditioner needs matching leading dimensions");
+            return launch_copy_dot(R, Z, ldz, qy, qx, partials, pcg, red, s);
+        case SFB_PRE_INVERSE: {
+            GemmEpi e1;  // T1 = (R P_R^-1)^T
+            e1.mode = EPI_STORE_T;
+            e1.C = T1;
+            e1.ldc = ldt1;
+            e1.pcg = pcg;
+            SFB_TRY(launch_dgemm_nt(R, ldr, p->B1, p->ldB, qy, qx, qx, e1, s));
+            // Z = P_L^-1 (R P_R^-1)
+            return launch_dgemm_nt(p->A1, p->ldA, T1, ldt1, qy, qx, qy, last, s);
+        }
+        case SFB_PRE_SPECTRAL_PROD:
+        case SFB_PRE_SPECTRAL_SUM: {
+            GemmEpi e1;  // T1 = (R V_R)^T
+            e1.mode = EPI_STORE_T;
+            e1.C = T1;
+            e1.ldc = ldt1;
+            e1.pcg = pcg;
+            SFB_TRY(launch_dgemm_nt(R, ldr, p->B1t, p->ldB, qy, qx, qx, e1, s));
+            GemmEpi e2;  // T2 = (V_L^T R V_R) o K
+            e2.mode = p->kind == SFB_PRE_SPECTRAL_SUM ? EPI_HADAMARD_SUM : EPI_HADAMARD_PROD;
+            e2.C = T2;
+            e2.ldc = ldt2;
+            e2.sr = p->sl;
+            e2.sc = p->sr;
+            e2.pcg = pcg;
+            SFB_TRY(launch_dgemm_nt(p->A1t, p->ldA, T1, ldt1, qy, qx, qy, e2, s));
+            GemmEpi e3;  // T1 = (T2 V_R^T)^T
+            e3.mode = EPI_STORE_T;
+            e3.C = T1;
+            e3.ldc = ldt1;
+            e3.pcg = pcg;
+            SFB_TRY(launch_dgemm_nt(T2, ldt2, p->B1, p->ldB, qy, qx, qx, e3, s));
+            // Z = V_L (T2 V_R^T)
+            return launch_dgemm_nt(p->A1, p->ldA, T1, ldt1, qy, qx, qy, last, s);
+        }
+        case SFB_PRE_BANDED: {
+            if (pcg == nullptr && red == nullptr && Z != R) {
+                SFB_CUDA_TRY(cudaMemcpy2DAsync(Z, (size_t)ldz * 8, R, (size_t)ldr * 8, (size_t)qx * 8, qy,
+                                               cudaMemcpyDeviceToDevice, s));
+            } else {
+                return arg_error("banded preconditioner inside MO-PCG not built yet");
+            }
+            SFB_TRY(launch_band_chol_cols(p->lband, p->bwL, qy, Z, ldz, qx, s));
+            return launch_band_chol_rows(p->rband, p->bwR, qx, Z, ldz, qy, s);
+        }
+    }
+    return arg_error("unknown preconditioner kind");
+}
+
+}  // namespace
+}  // namespace sfb
+
+// =============================================================== PCG =====
+struct sfb_pcg {
+    const sfb_op* op = nullptr;
+    const sfb_pre* pre = nullptr;
+    int qy = 0, qx = 0, ld = 0, ldt1 = 0, ldt2 = 0;
+    double *U = nullptr, *R = nullptr, *Z = nullptr, *Q0 = nullptr, *Q1 = nullptr, *W = nullptr, *B = nullptr;
+    double *T1 = nullptr, *T2 = nullptr;
+    double* partials = nullptr;
+    PcgState* st = nullptr;
+    double* hist = nullptr;
+    double* incs = nullptr;
+    int cap = 0;  // capacity of hist/incs (iterations)
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev_in = nullptr, ev_out = nullptr, ev_t0 = nullptr, ev_t1 = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    bool conditional = false;
+    int chunk = 0;
+    double* graph_iterates = nullptr;
+    std::mutex mu;
+};
+
+namespace sfb {
+namespace {
+
+int pcg_enqueue_iteration(sfb_pcg* s, double* iterates) {
+    cudaStream_t st = s->stream;
+    const sfb_op* op = s->op;
+    if (!op->dense) {
+        BandArgs a;
+        a.out_rows = a.in_rows = s->qy;
+        a.out_cols = a.in_cols = s->qx;
+        a.nterms = op->nterms;
+        a.width = op->width;
+        a.goff = op->goff;
+        a.hoff = op->hoff;
+        a.gband = op->gband;
+        a.hband = op->hband;
+        a.ld_mode = LD_PCG;
+        a.X = s->Z;
+        a.ldx = s->ld;
+        a.Q0 = s->Q0;
+        a.Q1 = s->Q1;
+        a.ldq = s->ld;
+        a.ep_mode = EP_PCG;
+        a.W = s->W;
+        a.ldw = s->ld;
+        a.partials = s->partials;
+        a.pcg = s->st;
+        SFB_TRY(launch_band(a, st));
+        SFB_TRY(launch_pcg_update(s->U, s->R, s->W, s->Q0, s->Q1, s->ld, s->qy, s->qx, s->partials, s->st,
+                                  s->hist, s->incs, st));
+    } else {
+        // dense operator: single direction buffer updated in place
+        SFB_TRY(launch_pcg_direction(s->Z, s->Q0, s->Q0, s->ld, s->qy, s->qx, s->st, st));
+        for (int t = 0; t < op->nterms; ++t) {
+            GemmEpi e1;
+            e1.mode = EPI_STORE_T;
+            e1.C = s->T1;
+            e1.ldc = s->ldt1;
+            e1.pcg = s->st;
+            SFB_TRY(launch_dgemm_nt(s->Q0, s->ld, op->Ht + (size_t)t * op->qx * op->ldH, op->ldH, s->qy, s->qx,
+                                    s->qx, e1, st));
+            GemmEpi e2;
+            e2.mode = t == 0 ? EPI_STORE : EPI_ACCUM;
+            e2.C = s->W;
+            e2.ldc = s->ld;
+            e2.pcg = s->st;
+            SFB_TRY(launch_dgemm_nt(op->G + (size_t)t * op->qy * op->ldG, op->ldG, s->T1, s->ldt1, s->qy, s->qx,
+                                    s->qy, e2, st));
+        }
+        SFB_TRY(launch_pcg_dots(s->W, s->Q0, s->Q0, s->ld, s->qy, s->qx, s->partials, s->st, st));
+        SFB_TRY(launch_pcg_update(s->U, s->R, s->W, s->Q0, s->Q0, s->ld, s->qy, s->qx, s->partials, s->st,
+                                  s->hist, s->incs, st));
+    }
+    if (iterates != nullptr) SFB_TRY(launch_pcg_record(s->U, s->ld, s->qy, s->qx, iterates, s->st, st));
+    return pre_apply_impl(s->pre, s->R, s->ld, s->Z, s->ld, s->T1, s->ldt1, s->T2, s->ldt2, s->partials, s->st,
+                          nullptr, st);
+}
+
+void drop_graph(sfb_pcg* s) {
+    if (s->exec) cudaGraphExecDestroy(s->exec);
+    s->exec = nullptr;
+}
+
+// Build the iteration graph: a WHILE conditional node whose body is one
+// MO-PCG iteration + the loop-control kernel.  Falls back to a plain graph of
+// `chunk` iterations (host-driven) if conditional nodes are unavailable.
+int build_graph(sfb_pcg* s, double* iterates) {
+    drop_graph(s);
+    cudaGraph_t g = nullptr;
+    SFB_CUDA_TRY(cudaGraphCreate(&g, 0));
+    cudaGraphConditionalHandle h;
+    bool ok = cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault) == cudaSuccess;
+    if (ok) {
+        alignas(cudaGraphNodeParams) unsigned char raw[sizeof(cudaGraphNodeParams)];
+        std::memset(raw, 0, sizeof(raw));
+        cudaGraphNodeParams& p = *reinterpret_cast<cudaGraphNodeParams*>(raw);
+        p.type = cudaGraphNodeTypeConditional;
+        p.conditional.handle = h;
+        p.conditional.type = cudaGraphCondTypeWhile;
+        p.conditional.size = 1;
+        cudaGraphNode_t node;
+        ok = cudaGraphAddNode(&node, g, nullptr, 0, &p) == cudaSuccess;
+        if (ok) {
+            cudaGraph_t body = p.conditional.phGraph_out[0];
+            ok = cudaStreamBeginCaptureToGraph(s->stream, body, nullptr, nullptr, 0,
+                                               cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+            if (ok) {
+                int rc = pcg_enqueue_iteration(s, iterates);
+                if (rc == SFB_OK) rc = launch_loop_ctl(s->st, (unsigned long long)h, 1, s->stream);
+                cudaGraph_t captured = nullptr;
+                cudaError_t e = cudaStreamEndCapture(s->stream, &captured);
+                if (rc != SFB_OK) {
+                    cudaGraphDestroy(g);
+                    return rc;
+                }
+                ok = e == cudaSuccess;
+            }
+        }
+        if (ok) ok = cudaGraphInstantiate(&s->exec, g, 0) == cudaSuccess;
+    }
+    cudaGraphDestroy(g);
+    cudaGetLastError();  // clear any error from an unsupported conditional path
+    if (ok) {
+        s->conditional = true;
+        s->graph_iterates = iterates;
+        return SFB_OK;
+    }
+    // fallback: plain graph of `chunk` iterations
+    s->conditional = false;
+    s->chunk = 16;
+    drop_graph(s);
+    SFB_CUDA_TRY(cudaStreamBeginCapture(s->stream, cudaStreamCaptureModeThreadLocal));
+    int rc = SFB_OK;
+    for (int i = 0; i < s->chunk && rc == SFB_OK; ++i) {
+        rc = pcg_enqueue_iteration(s, iterates);
+        if (rc == SFB_OK) rc = launch_loop_ctl(s->st, 0, 0, s->stream);
+    }
+    cudaGraph_t cg = nullptr;
+    cudaError_t e = cudaStreamEndCapture(s->stream, &cg);
+    if (rc != SFB_OK) {
+        if (cg) cudaGraphDestroy(cg);
+        return rc;
+    }
+    SFB_CUDA_TRY(e);
+    cudaError_t ei = cudaGraphInstantiate(&s->exec, cg, 0);
+    cudaGraphDestroy(cg);
+    SFB_CUDA_TRY(ei);
+    s->graph_iterates = iterates;
+    return SFB_OK;
+}
+
+}  // namespace
+}  // namespace sfb
+
+// ================================================================ ABI =====
+extern "C" {
+
+int sfb_version(void) { return 1; }
+
+const char* sfb_last_error(void) { return g_last_error.c_str(); }
+
+int sfb_init(int device, int* sm_count) {
+    SFB_CUDA_TRY(cudaSetDevice(device));
+    int n = 0;
+    SFB_CUDA_TRY(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device));
+    if (sm_count) *sm_count = n;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    return SFB_OK;
+}
+
+// ------------------------------------------------------------ operator ---
+int sfb_op_create(int qy, int qx, int nterms, int gw, int goff, const double* gband, int hw, int hoff,
+                  const double* hband, sfb_op** out) {
+    if (qy <= 0 || qx <= 0 || nterms <= 0) return arg_error("operator needs positive shape and terms");
+    if (gw != hw) return arg_error("left and right band widths must be padded to a common width");
+    if (!band_supported(nterms, gw)) {
+        set_error("banded operator: unsupported width/terms");
+        return SFB_ERR_UNSUPPORTED;
+    }
+    auto* op = new sfb_op;
+    op->qy = qy;
+    op->qx = qx;
+    op->nterms = nterms;
+    op->width = gw;
+    op->goff = goff;
+    op->hoff = hoff;
+    int rc = dalloc(&op->gband, (size_t)nterms * qy * gw);
+    if (rc == SFB_OK) rc = dalloc(&op->hband, (size_t)nterms * qx * hw);
+    if (rc == SFB_OK && cudaMemcpy(op->gband, gband, (size_t)nterms * qy * gw * 8, cudaMemcpyHostToDevice) != cudaSuccess)
+        rc = SFB_ERR_CUDA;
+    if (rc == SFB_OK && cudaMemcpy(op->hband, hband, (size_t)nterms * qx * hw * 8, cudaMemcpyHostToDevice) != cudaSuccess)
+        rc = SFB_ERR_CUDA;
+    if (rc != SFB_OK) {
+        if (rc == SFB_ERR_CUDA) set_error("uploading operator bands failed");
+        sfb_op_destroy(op);
+        return rc;
+    }
+    *out = op;
+    return SFB_OK;
+}
+
+int sfb_op_create_dense(int qy, int qx, int nterms, const double* G, const double* H, sfb_op** out) {
+    if (qy <= 0 || qx <= 0 || nterms <= 0) return arg_error("operator needs positive shape and terms");
+    auto* op = new sfb_op;
+    op->dense = true;
+    op->qy = qy;
+    op->qx = qx;
+    op->nterms = nterms;
+    op->ldG = pad_ld(qy);
+    op->ldH = pad_ld(qx);
+    int rc = dalloc(&op->G, (size_t)nterms * qy * op->ldG);
+    if (rc == SFB_OK) rc = dalloc(&op->Ht, (size_t)nterms * qx * op->ldH);
+    std::vector<double> tr((size_t)qx * qx);
+    for (int t = 0; t < nterms && rc == SFB_OK; ++t) {
+        rc = upload_padded(op->G + (size_t)t * qy * op->ldG, op->ldG, G + (size_t)t * qy * qy, qy, qy);
+        const double* Ht = H + (size_t)t * qx * qx;
+        for (int i = 0; i < qx; ++i)
+            for (int j = 0; j < qx; ++j) tr[(size_t)j * qx + i] = Ht[(size_t)i * qx + j];
+        if (rc == SFB_OK) rc = upload_padded(op->Ht + (size_t)t * qx * op->ldH, op->ldH, tr.data(), qx, qx);
+    }
+    if (rc != SFB_OK) {
+        sfb_op_destroy(op);
+        return rc;
+    }
+    *out = op;
+    return SFB_OK;
+}
+
+int sfb_op_apply(const sfb_op* op, const double* U, int ldu, double* W, int ldw, void* stream) {
+    if (!op) return arg_error("null operator");
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!op->dense) return op_apply_impl(op, U, ldu, W, ldw, nullptr, 0, s);
+    ScopedFree tmp(s);
+    const int ld = pad_ld(op->qx), ldt = pad_ld(op->qy);
+    double *Ub, *Wb, *T1;
+    SFB_TRY(tmp.get(&Ub, (size_t)op->qy * ld * 8));
+    SFB_TRY(tmp.get(&Wb, (size_t)op->qy * ld * 8));
+    SFB_TRY(tmp.get(&T1, (size_t)op->qx * ldt * 8));
+    SFB_CUDA_TRY(cudaMemcpy2DAsync(Ub, (size_t)ld * 8, U, (size_t)ldu * 8, (size_t)op->qx * 8, op->qy,
+                                   cudaMemcpyDeviceToDevice, s));
+    SFB_TRY(op_apply_impl(op, Ub, ld, Wb, ld, T1, ldt, s));
+    SFB_CUDA_TRY(cudaMemcpy2DAsync(W, (size_t)ldw * 8, Wb, (size_t)ld * 8, (size_t)op->qx * 8, op->qy,
+                                   cudaMemcpyDeviceToDevice, s));
+    return SFB_OK;
+}
+
+int sfb_op_residual(const sfb_op* op, const double* U, int ldu, const double* rhs, int ldr, double* out2,
+                    void* stream) {
+    if (!op) return arg_error("null operator");
+    cudaStream_t s = (cudaStream_t)stream;
+    ScopedFree tmp(s);
+    const int ld = pad_ld(op->qx);
+    double *Wb, *parts;
+    RedSlots* red;
+    SFB_TRY(tmp.get(&Wb, (size_t)op->qy * ld * 8));
+    SFB_TRY(tmp.get(&parts, (size_t)4 * vector_grid_blocks() * 8));
+    SFB_TRY(tmp.get(&red, 2 * sizeof(RedSlots)));
+    SFB_CUDA_TRY(cudaMemsetAsync(red, 0, 2 * sizeof(RedSlots), s));
+    SFB_TRY(sfb_op_apply(op, U, ldu, Wb, ld, stream));
+    SFB_TRY(launch_norms(Wb, ld, rhs, ldr, op->qy, op->qx, parts, red, s));
+    SFB_TRY(launch_norms(rhs, ldr, nullptr, 0, op->qy, op->qx, parts, red + 1, s));
+    RedSlots h[2];
+    SFB_CUDA_TRY(cudaMemcpyAsync(h, red, sizeof(h), cudaMemcpyDeviceToHost, s));
+    SFB_CUDA_TRY(cudaStreamSynchronize(s));
+    out2[0] = h[0].v[0];
+    out2[1] = h[1].v[0];
+    return SFB_OK;
+}
+
+int sfb_op_destroy(sfb_op* op) {
+    if (!op) return SFB_OK;
+    cudaFree(op->gband);
+    cudaFree(op->hband);
+    cudaFree(op->G);
+    cudaFree(op->Ht);
+    delete op;
+    return SFB_OK;
+}
+
+// ----------------------------------------------------------------- maps ---
+int sfb_map_create(int out_rows, int out_cols, int in_rows, int in_cols, int gw, int goff, const double* gband,
+                   int hw, int hoff, const double* hband, sfb_map** out) {
+    if (out_rows <= 0 || out_cols <= 0 || in_rows <= 0 || in_cols <= 0) return arg_error("empty map");
+    if (gw != hw) return arg_error("left and right band widths must be padded to a common width");
+    if (!band_supported(1, gw)) {
+        set_error("rhs map: unsupported band width");
+        return SFB_ERR_UNSUPPORTED;
+    }
+    auto* m = new sfb_map;
+    m->out_rows = out_rows;
+    m->out_cols = out_cols;
+    m->in_rows = in_rows;
+    m->in_cols = in_cols;
+    m->width = gw;
+    m->goff = goff;
+    m->hoff = hoff;
+    int rc = dalloc(&m->gband, (size_t)out_rows * gw);
+    if (rc == SFB_OK) rc = dalloc(&m->hband, (size_t)out_cols * hw);
+    if (rc == SFB_OK && (cudaMemcpy(m->gband, gband, (size_t)out_rows * gw * 8, cudaMemcpyHostToDevice) != cudaSuccess ||
+                         cudaMemcpy(m->hband, hband, (size_t)out_cols * hw * 8, cudaMemcpyHostToDevice) != cudaSuccess)) {
+        set_error("uploading map bands failed");
+        rc = SFB_ERR_CUDA;
+    }
+    if (rc != SFB_OK) {
+        sfb_map_destroy(m);
+        return rc;
+    }
+    *out = m;
+    return SFB_OK;
+}
+
+namespace {
+BandArgs map_args(const sfb_map* m, double* out, int ldo) {
+    BandArgs a;
+    a.out_rows = m->out_rows;
+    a.out_cols = m->out_cols;
+    a.in_rows = m->in_rows;
+    a.in_cols = m->in_cols;
+    a.nterms = 1;
+    a.width = m->width;
+    a.goff = m->goff;
+    a.hoff = m->hoff;
+    a.gband = m->gband;
+    a.hband = m->hband;
+    a.ep_mode = EP_STORE;
+    a.W = out;
+    a.ldw = ldo;
+    return a;
+}
+
+int run_checked(BandArgs& a, double* check2, cudaStream_t s) {
+    if (check2 == nullptr) return launch_band(a, s);
+    ScopedFree tmp(s);
+    unsigned long long* chk;
+    SFB_TRY(tmp.get(&chk, 2 * sizeof(unsigned long long)));
+    SFB_CUDA_TRY(cudaMemsetAsync(chk, 0, 2 * sizeof(unsigned long long), s));
+    a.check = chk;
+    SFB_TRY(launch_band(a, s));
+    unsigned long long h[2];
+    SFB_CUDA_TRY(cudaMemcpyAsync(h, chk, sizeof(h), cudaMemcpyDeviceToHost, s));
+    SFB_CUDA_TRY(cudaStreamSynchronize(s));
+    double mx;
+    std::memcpy(&mx, &h[0], 8);
+    check2[0] = mx;
+    check2[1] = (double)h[1];
+    return SFB_OK;
+}
+}  // namespace
+
+int sfb_map_apply(const sfb_map* m, const double* F, int ldf, double* out, int ldo, void* stream) {
+    if (!m) return arg_error("null map");
+    BandArgs a = map_args(m, out, ldo);
+    a.ld_mode = LD_PLAIN;
+    a.X = F;
+    a.ldx = ldf;
+    return launch_band(a, (cudaStream_t)stream);
+}
+
+int sfb_map_apply_heat(const sfb_map* m, const double* U, int ldu, int row_shift, int col_shift, double c,
+                       const double* F, int ldf, double* out, int ldo, double* check2, void* stream) {
+    if (!m) return arg_error("null map");
+    BandArgs a = map_args(m, out, ldo);
+    a.ld_mode = LD_HEAT;
+    a.X = U;
+    a.ldx = ldu;
+    a.X2 = F;
+    a.ldx2 = ldf;
+    a.c = c;
+    a.rs = row_shift;
+    a.cs = col_shift;
+    return run_checked(a, check2, (cudaStream_t)stream);
+}
+
+int sfb_map_apply_dib(const sfb_map* m, const double* U, const double* V, int ld, int species, double tau_rho,
+                      const double* params, double* out, int ldo, double* check2, void* stream) {
+    if (!m) return arg_error("null map");
+    if (m->in_rows != m->out_rows || m->in_cols != m->out_cols)
+        return arg_error("DIB rhs expects a zero-flux (square) map");
+    BandArgs a = map_args(m, out, ldo);
+    a.ld_mode = LD_DIB;
+    a.X = U;
+    a.X2 = V;
+    a.ldx = ld;
+    a.species = species;
+    a.c = tau_rho;
+    for (int i = 0; i < 9; ++i) a.kp[i] = params[i];
+    return run_checked(a, check2, (cudaStream_t)stream);
+}
+
+int sfb_map_destroy(sfb_map* m) {
+    if (!m) return SFB_OK;
+    cudaFree(m->gband);
+    cudaFree(m->hband);
+    delete m;
+    return SFB_OK;
+}
+
+// ------------------------------------------------------- preconditioner ---
+int sfb_pre_create(int qy, int qx, int kind, const double* L, const double* R, const double* lamL,
+                   const double* lamR, sfb_pre** out) {
+    if (qy <= 0 || qx <= 0) return arg_error("preconditioner needs a positive shape");
+    auto* p = new sfb_pre;
+    p->kind = kind;
+    p->qy = qy;
+    p->qx = qx;
+    p->ldA = pad_ld(qy);
+    p->ldB = pad_ld(qx);
+    int rc = SFB_OK;
+    auto fail = [&](int code) {
+        sfb_pre_destroy(p);
+        return code;
+    };
+    if (kind == SFB_PRE_IDENTITY) {
+        *out = p;
+        return SFB_OK;
+    }
+    if (kind == SFB_PRE_INVERSE) {
+        if (!L || !R) return fail(arg_error("inverse preconditioner needs both factors"));
+        rc = dalloc(&p->A1, (size_t)qy * p->ldA);
+        if (rc == SFB_OK) rc = dalloc(&p->B1, (size_t)qx * p->ldB);
+        if (rc == SFB_OK) rc = upload_padded(p->A1, p->ldA, L, qy, qy);
+        if (rc == SFB_OK) rc = upload_padded(p->B1, p->ldB, R, qx, qx);
+        if (rc != SFB_OK) return fail(rc);
+        *out = p;
+        return SFB_OK;
+    }
+    if (kind == SFB_PRE_SPECTRAL_PROD || kind == SFB_PRE_SPECTRAL_SUM) {
+        if (!L || !R || !lamL || !lamR) return fail(arg_error("spectral sandwich needs V_L, V_R and eigenvalues"));
+        std::vector<double> t((size_t)std::max(qy, qx) * std::max(qy, qx));
+        rc = dalloc(&p->A1, (size_t)qy * p->ldA);
+        if (rc == SFB_OK) rc = dalloc(&p->A1t, (size_t)qy * p->ldA);
+        if (rc == SFB_OK) rc = dalloc(&p->B1, (size_t)qx * p->ldB);
+        if (rc == SFB_OK) rc = dalloc(&p->B1t, (size_t)qx * p->ldB);
+        if (rc == SFB_OK) rc = dalloc(&p->sl, qy);
+        if (rc == SFB_OK) rc = dalloc(&p->sr, qx);
+        if (rc == SFB_OK) rc = upload_padded(p->A1, p->ldA, L, qy, qy);
+        for (int i = 0; i < qy; ++i)
+            for (int j = 0; j < qy; ++j) t[(size_t)j * qy + i] = L[(size_t)i * qy + j];
+        if (rc == SFB_OK) rc = upload_padded(p->A1t, p->ldA, t.data(), qy, qy);
+        if (rc == SFB_OK) rc = upload_padded(p->B1, p->ldB, R, qx, qx);
+        for (int i = 0; i < qx; ++i)
+            for (int j = 0; j < qx; ++j) t[(size_t)j * qx + i] = R[(size_t)i * qx + j];
+        if (rc == SFB_OK) rc = upload_padded(p->B1t, p->ldB, t.data(), qx, qx);
+        std::vector<double> vl(lamL, lamL + qy), vr(lamR, lamR + qx);
+        if (kind == SFB_PRE_SPECTRAL_PROD) {
+            for (auto& v : vl) v = 1.0 / v;
+            for (auto& v : vr) v = 1.0 / v;
+        }
+        if (rc == SFB_OK && (cudaMemcpy(p->sl, vl.data(), qy * 8, cudaMemcpyHostToDevice) != cudaSuccess ||
+                             cudaMemcpy(p->sr, vr.data(), qx * 8, cudaMemcpyHostToDevice) != cudaSuccess)) {
+            set_error("uploading eigenvalues failed");
+            rc = SFB_ERR_CUDA;
+        }
+        if (rc != SFB_OK) return fail(rc);
+        *out = p;
+        return SFB_OK;
+    }
+    return fail(arg_error("unknown preconditioner kind"));
+}
+
+int sfb_pre_create_banded(int qy, int qx, int bwL, const double* lband, int bwR, const double* rband,
+                          sfb_pre** out) {
+    if (qy <= 0 || qx <= 0 || bwL < 0 || bwR < 0) return arg_error("bad banded preconditioner shape");
+    auto* p = new sfb_pre;
+    p->kind = SFB_PRE_BANDED;
+    p->qy = qy;
+    p->qx = qx;
+    p->bwL = bwL;
+    p->bwR = bwR;
+    int rc = dalloc(&p->lband, (size_t)qy * (bwL + 1));
+    if (rc == SFB_OK) rc = dalloc(&p->rband, (size_t)qx * (bwR + 1));
+    if (rc == SFB_OK && (cudaMemcpy(p->lband, lband, (size_t)qy * (bwL + 1) * 8, cudaMemcpyHostToDevice) != cudaSuccess ||
+                         cudaMemcpy(p->rband, rband, (size_t)qx * (bwR + 1) * 8, cudaMemcpyHostToDevice) != cudaSuccess)) {
+        set_error("uploading Cholesky bands failed");
+        rc = SFB_ERR_CUDA;
+    }
+    if (rc != SFB_OK) {
+        sfb_pre_destroy(p);
+        return rc;
+    }
+    *out = p;
+    return SFB_OK;
+}
+
+int sfb_pre_apply(const sfb_pre* p, const double* R, int ldr, double* Z, int ldz, void* stream) {
+    if (!p) return arg_error("null preconditioner");
+    cudaStream_t s = (cudaStream_t)stream;
+    ScopedFree tmp(s);
+    const int ld = pad_ld(p->qx), ldt1 = pad_ld(p->qy);
+    double *Rb, *Zb, *T1 = nullptr, *T2 = nullptr;
+    SFB_TRY(tmp.get(&Rb, (size_t)p->qy * ld * 8));
+    SFB_TRY(tmp.get(&Zb, (size_t)p->qy * ld * 8));
+    if (p->kind != SFB_PRE_IDENTITY && p->kind != SFB_PRE_BANDED) {
+        SFB_TRY(tmp.get(&T1, (size_t)p->qx * ldt1 * 8));
+        SFB_TRY(tmp.get(&T2, (size_t)p->qy * ld * 8));
+    }
+    double* parts = nullptr;
+    RedSlots* red = nullptr;
+    SFB_TRY(tmp.get(&parts, (size_t)std::max(vector_grid_blocks(), gemm_grid_blocks(p->qy, p->qx)) * 8));
+    SFB_TRY(tmp.get(&red, sizeof(RedSlots)));
+    SFB_CUDA_TRY(cudaMemsetAsync(red, 0, sizeof(RedSlots), s));
+    SFB_CUDA_TRY(cudaMemcpy2DAsync(Rb, (size_t)ld * 8, R, (size_t)ldr * 8, (size_t)p->qx * 8, p->qy,
+                                   cudaMemcpyDeviceToDevice, s));
+    SFB_TRY(pre_apply_impl(p, Rb, ld, Zb, ld, T1, ldt1, T2, ld, parts,
+                           nullptr, p->kind == SFB_PRE_BANDED ? nullptr : red, s));
+    SFB_CUDA_TRY(cudaMemcpy2DAsync(Z, (size_t)ldz * 8, Zb, (size_t)ld * 8, (size_t)p->qx * 8, p->qy,
+                                   cudaMemcpyDeviceToDevice, s));
+    return SFB_OK;
+}
+
+int sfb_pre_transform(const sfb_pre* p, const double* X, int ldx, double* Y, int ldy, void* stream) {
+    if (!p) return arg_error("null preconditioner");
+    if (p->kind != SFB_PRE_SPECTRAL_PROD && p->kind != SFB_PRE_SPECTRAL_SUM)
+        return arg_error("spectral transform needs a spectral sandwich");
+    cudaStream_t s = (cudaStream_t)stream;
+    ScopedFree tmp(s);
+    const int ld = pad_ld(p->qx), ldt1 = pad_ld(p->qy);
+    double *Xb, *Yb, *T1;
+    SFB_TRY(tmp.get(&Xb, (size_t)p->qy * ld * 8));
+    SFB_TRY(tmp.get(&Yb, (size_t)p->qy * ld * 8));
+    SFB_TRY(tmp.get(&T1, (size_t)p->qx * ldt1 * 8));
+    SFB_CUDA_TRY(cudaMemcpy2DAsync(Xb, (size_t)ld * 8, X, (size_t)ldx * 8, (size_t)p->qx * 8, p->qy,
+                                   cudaMemcpyDeviceToDevice, s));
+    GemmEpi e1;  // T1 = (X V_R)^T
+    e1.mode = EPI_STORE_T;
+    e1.C = T1;
+    e1.ldc = ldt1;
+    SFB_TRY(launch_dgemm_nt(Xb, ld, p->B1t, p->ldB, p->qy, p->qx, p->qx, e1, s));
+    GemmEpi e2;  // Y = V_L^T X V_R
+    e2.mode = EPI_STORE;
+    e2.C = Yb;
+    e2.ldc = ld;
+    SFB_TRY(launch_dgemm_nt(p->A1t, p->ldA, T1, ldt1, p->qy, p->qx, p->qy, e2, s));
+    SFB_CUDA_TRY(cudaMemcpy2DAsync(Y, (size_t)ldy * 8, Yb, (size_t)ld * 8, (size_t)p->qx * 8, p->qy,
+                                   cudaMemcpyDeviceToDevice, s));
+    return SFB_OK;
+}
+
+int sfb_pre_destroy(sfb_pre* p) {
+    if (!p) return SFB_OK;
+    cudaFree(p->A1);
+    cudaFree(p->A1t);
+    cudaFree(p->B1);
+    cudaFree(p->B1t);
+    cudaFree(p->sl);
+    cudaFree(p->sr);
+    cudaFree(p->lband);
+    cudaFree(p->rband);
+    delete p;
+    return SFB_OK;
+}
+
+// ------------------------------------------------------------------ PCG ---
+int sfb_pcg_create(const sfb_op* op, const sfb_pre* pre, sfb_pcg** out) {
+    if (!op || !pre) return arg_error("mo_pcg needs an operator and a preconditioner");
+    if (op->qy != pre->qy || op->qx != pre->qx) return arg_error("preconditioner shape does not match operator");
+    if (pre->kind == SFB_PRE_SPECTRAL_SUM) return arg_error("the reduced-solve sandwich is not a preconditioner");
+    auto* s = new sfb_pcg;
+    s->op = op;
+    s->pre = pre;
+    s->qy = op->qy;
+    s->qx = op->qx;
+    s->ld = pad_ld(op->qx);
+    s->ldt1 = pad_ld(op->qy);
+    s->ldt2 = s->ld;
+    const size_t n = (size_t)s->qy * s->ld;
+    int rc = SFB_OK;
+    double** bufs[] = {&s->U, &s->R, &s->Z, &s->Q0, &s->Q1, &s->W, &s->B, &s->T2};
+    for (double** b : bufs)
+        if (rc == SFB_OK) rc = dalloc(b, n);
+    if (rc == SFB_OK) rc = dalloc(&s->T1, (size_t)s->qx * s->ldt1);
+    const int nparts = 2 * std::max(std::max(vector_grid_blocks(), band_grid_blocks(s->qy, s->qx)),
+                                    gemm_grid_blocks(s->qy, s->qx));
+    if (rc == SFB_OK) rc = dalloc(&s->partials, nparts);
+    if (rc == SFB_OK) rc = talloc(&s->st, sizeof(PcgState));
+    if (rc == SFB_OK) {
+        for (double** b : bufs) cudaMemset(*b, 0, n * 8);
+        cudaMemset(s->T1, 0, (size_t)s->qx * s->ldt1 * 8);
+        if (cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&s->ev_in, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&s->ev_out, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreate(&s->ev_t0) != cudaSuccess || cudaEventCreate(&s->ev_t1) != cudaSuccess) {
+            set_error("creating the MO-PCG stream/events failed");
+            rc = SFB_ERR_CUDA;
+        }
+    }
+    if (rc != SFB_OK) {
+        sfb_pcg_destroy(s);
+        return rc;
+    }
+    *out = s;
+    return SFB_OK;
+}
+
+int sfb_pcg_solve(sfb_pcg* s, const double* rhs, int ldr, const double* u0, int ldu0, double* U, int ldu, int rule,
+                  double value, int max_iter, double* history, double* increments, double* iterates,
+                  int n_iterates, sfb_pcg_result* res, void* stream) {
+    if (!s) return arg_error("null solver");
+    if (max_iter < 0) return arg_error("max_iter must be nonnegative");
+    std::lock_guard<std::mutex> lock(s->mu);
+    cudaStream_t cs = (cudaStream_t)stream, st = s->stream;
+    const int qy = s->qy, qx = s->qx, ld = s->ld;
+    // capacity for history / increments
+    if (max_iter + 1 > s->cap) {
+        drop_graph(s);
+        cudaFree(s->hist);
+        cudaFree(s->incs);
+        s->hist = s->incs = nullptr;
+        s->cap = std::max(max_iter + 1, 64);
+        SFB_TRY(dalloc(&s->hist, s->cap));
+        SFB_TRY(dalloc(&s->incs, s->cap));
+    }
+    if (n_iterates <= 0) iterates = nullptr;
+    if (s->exec == nullptr || s->graph_iterates != iterates) SFB_TRY(build_graph(s, iterates));
+
+    SFB_CUDA_TRY(cudaEventRecord(s->ev_in, cs));
+    SFB_CUDA_TRY(cudaStreamWaitEvent(st, s->ev_in, 0));
+    PcgState h;
+    std::memset(&h, 0, sizeof(h));
+    h.status = SFB_PCG_RUNNING;
+    h.max_iter = max_iter;
+    h.rule = rule;
+    h.value = value;
+    h.n_iterates = iterates ? n_iterates : 0;
+    h.recorded = -1;
+    if (max_iter == 0) h.status = SFB_PCG_MAX_ITER;
+    SFB_CUDA_TRY(cudaMemcpyAsync(s->st, &h, sizeof(h), cudaMemcpyHostToDevice, st));
+    SFB_CUDA_TRY(cudaMemcpy2DAsync(s->B, (size_t)ld * 8, rhs, (size_t)ldr * 8, (size_t)qx * 8, qy,
+                                   cudaMemcpyDeviceToDevice, st));
+    // initial residual (solvers.py:391-397)
+    if (u0 != nullptr) {
+        SFB_CUDA_TRY(cudaMemcpy2DAsync(s->U, (size_t)ld * 8, u0, (size_t)ldu0 * 8, (size_t)qx * 8, qy,
+                                       cudaMemcpyDeviceToDevice, st));
+        SFB_TRY(op_apply_impl(s->op, s->U, ld, s->W, ld, s->T1, s->ldt1, st));
+        SFB_TRY(launch_pcg_init_warm(s->B, ld, s->W, s->R, ld, qy, qx, s->partials, s->st, s->hist, st));
+    } else {
+        SFB_TRY(launch_pcg_init_plain(s->B, ld, s->R, s->U, ld, qy, qx, s->partials, s->st, s->hist, st));
+    }
+    if (iterates) SFB_TRY(launch_pcg_record(s->U, ld, qy, qx, iterates, s->st, st));
+    if (max_iter == 0) {
+        // nothing to iterate; max_iter status was preset (res0 still computed)
+    }
+    // Z = P^-1 R_0, rz (solvers.py:418-420)
+    SFB_TRY(pre_apply_impl(s->pre, s->R, ld, s->Z, ld, s->T1, s->ldt1, s->T2, s->ldt2, s->partials, s->st, nullptr,
+                           st));
+    SFB_CUDA_TRY(cudaEventRecord(s->ev_t0, st));
+    int chunks = 0;
+    if (s->conditional) {
+        SFB_CUDA_TRY(cudaGraphLaunch(s->exec, st));
+        chunks = 1;
+    } else {
+        for (;;) {
+            SFB_CUDA_TRY(cudaGraphLaunch(s->exec, st));
+            ++chunks;
+            PcgState cur;
+            SFB_CUDA_TRY(cudaMemcpyAsync(&cur, s->st, sizeof(cur), cudaMemcpyDeviceToHost, st));
+            SFB_CUDA_TRY(cudaStreamSynchronize(st));
+            if (cur.status != SFB_PCG_RUNNING || cur.iter >= max_iter) break;
+        }
+    }
+    SFB_CUDA_TRY(cudaEventRecord(s->ev_t1, st));
+    // outputs
+    SFB_CUDA_TRY(cudaMemcpy2DAsync(U, (size_t)ldu * 8, s->U, (size_t)ld * 8, (size_t)qx * 8, qy,
+                                   cudaMemcpyDeviceToDevice, st));
+    PcgState fin;
+    SFB_CUDA_TRY(cudaMemcpyAsync(&fin, s->st, sizeof(fin), cudaMemcpyDeviceToHost, st));
+    SFB_CUDA_TRY(cudaStreamSynchronize(st));
+    const int n = fin.iter;
+    if (history) SFB_CUDA_TRY(cudaMemcpy(history, s->hist, (size_t)(n + 1) * 8, cudaMemcpyDeviceToHost));
+    if (increments && n > 0) SFB_CUDA_TRY(cudaMemcpy(increments, s->incs, (size_t)n * 8, cudaMemcpyDeviceToHost));
+    SFB_CUDA_TRY(cudaEventRecord(s->ev_out, st));
+    SFB_CUDA_TRY(cudaStreamWaitEvent(cs, s->ev_out, 0));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, s->ev_t0, s->ev_t1);
+    if (res) {
+        res->iterations = n;
+        res->stop_reason = fin.status == SFB_PCG_RUNNING ? SFB_PCG_MAX_ITER : fin.status;
+        res->bad_iter = fin.bad_iter;
+        res->chunks = chunks;
+        res->res0 = fin.res0;
+        res->bad_value = fin.bad_value;
+        res->device_ms = ms;
+    }
+    return SFB_OK;
+}
+
+int sfb_pcg_destroy(sfb_pcg* s) {
+    if (!s) return SFB_OK;
+    drop_graph(s);
+    double* bufs[] = {s->U, s->R, s->Z, s->Q0, s->Q1, s->W, s->B, s->T1, s->T2, s->partials, s->hist, s->incs};
+    for (double* b : bufs) cudaFree(b);
+    cudaFree(s->st);
+    if (s->stream) cudaStreamDestroy(s->stream);
+    cudaEvent_t evs[] = {s->ev_in, s->ev_out, s->ev_t0, s->ev_t1};
+    for (auto e : evs)
+        if (e) cudaEventDestroy(e);
+    delete s;
+    return SFB_OK;
+}
+
+// ------------------------------------------------------------ reductions --
+int sfb_diff_norm(const double* A, int lda, const double* B, int ldb, int rows, int cols, double* out4,
+                  void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    ScopedFree tmp(s);
+    double* parts;
+    RedSlots* red;
+    SFB_TRY(tmp.get(&parts, (size_t)4 * vector_grid_blocks() * 8));
+    SFB_TRY(tmp.get(&red, sizeof(RedSlots)));
+    SFB_CUDA_TRY(cudaMemsetAsync(red, 0, sizeof(RedSlots), s));
+    SFB_TRY(launch_norms(A, lda, B, ldb, rows, cols, parts, red, s));
+    RedSlots h;
+    SFB_CUDA_TRY(cudaMemcpyAsync(&h, red, sizeof(h), cudaMemcpyDeviceToHost, s));
+    SFB_CUDA_TRY(cudaStreamSynchronize(s));
+    for (int i = 0; i < 4; ++i) out4[i] = h.v[i];
+    return SFB_OK;
+}
+
+}  // extern "C"

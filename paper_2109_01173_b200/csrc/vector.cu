@@ -1,0 +1,341 @@
+// Memory-bound MO-PCG passes, fused with their reductions.
+//
+//   pcg_update  : U += alpha Q; R -= alpha W; |R|^2; last block -> stop test
+//                 (solvers.py:432-446)
+//   pcg_init_*  : R = rhs (- op(u0)); |R_0| (solvers.py:391-397, 415-416)
+//   copy_dot    : identity preconditioner Z = R with <Z,R> (solvers.py:124-126)
+//   direction / dots : the dense-operator fallback of the fused banded path
+//   norms       : |A - B|, max|A|, #non-finite (timestepping.py:89-91, 155, 210)
+//
+// Grid: 2 CTAs per SM x 256 threads, rows distributed round-robin over CTAs,
+// columns over threads (coalesced).  Every reduction is deterministic: one
+// partial per CTA, summed in fixed order by the last CTA to finish.
+#include "sfb_common.cuh"
+#include "sfb_kernels.cuh"
+
+namespace sfb {
+
+namespace {
+
+constexpr int VT = 256;
+constexpr int VB = 2 * kNumSMs;
+
+#define ROW_LOOP(rows, cols)                                         \
+    for (int r = blockIdx.x; r < (rows); r += gridDim.x)            \
+        for (int cc = threadIdx.x; cc < (cols); cc += VT)
+
+__device__ __forceinline__ void pcg_finish_update(PcgState* st, double rr, double* hist, double* incs) {
+    // solvers.py:434-446 (runs in one thread of the last CTA)
+    const int s = st->iter;
+    const double res = sqrt(rr);
+    if (!isfinite(res)) {
+        st->status = SFB_PCG_NONFINITE;
+        st->bad_iter = s;
+        return;
+    }
+    hist[s + 1] = res;
+    const double inc = fabs(st->alpha) * sqrt(st->qq);
+    incs[s] = inc;
+    st->iter = s + 1;
+    if (st->rule == SFB_RULE_RESIDUAL && res <= st->value * st->res0) {
+        st->status = SFB_PCG_TOLERANCE;
+    } else if (st->rule == SFB_RULE_INCREMENT && inc <= st->value) {
+        st->status = SFB_PCG_INCREMENT;
+    } else if (s + 1 >= st->max_iter) {
+        st->status = SFB_PCG_MAX_ITER;
+    }
+}
+
+__global__ void __launch_bounds__(VT) pcg_update_kernel(double* U, double* R, const double* W, const double* Q0,
+                                                        const double* Q1, int ld, int rows, int cols,
+                                                        double* partials, PcgState* st, double* hist,
+                                                        double* incs) {
+    if (st->status != SFB_PCG_RUNNING) return;
+    const int s = st->iter;
+    const double alpha = st->alpha;
+    const double* Q = (s & 1) ? Q1 : Q0;
+    double rr = 0.0;
+    ROW_LOOP(rows, cols) {
+        const size_t o = (size_t)r * ld + cc;
+        U[o] = __dadd_rn(U[o], __dmul_rn(alpha, Q[o]));  // U += alpha Q
+        const double rv = __dsub_rn(R[o], __dmul_rn(alpha, W[o]));  // R -= alpha W
+        R[o] = rv;
+        rr = fma(rv, rv, rr);
+    }
+    __shared__ double sh[VT / 32];
+    const double p = block_sum<VT>(rr, sh);
+    if (threadIdx.x == 0) partials[blockIdx.x] = p;
+    if (arrive_last(&st->counter[1], gridDim.x)) {
+        const double tot = sum_partials<VT>(partials, gridDim.x, 1, sh);
+        if (threadIdx.x == 0) {
+            st->counter[1] = 0;
+            pcg_finish_update(st, tot, hist, incs);
+        }
+    }
+}
+
+__device__ __forceinline__ void pcg_finish_init(PcgState* st, double rr, double* hist) {
+    const double res0 = sqrt(rr);
+    st->res0 = res0;
+    hist[0] = res0;
+    if (res0 == 0.0) st->status = SFB_PCG_TOLERANCE;  // solvers.py:415-416
+}
+
+__global__ void __launch_bounds__(VT) pcg_init_plain_kernel(const double* rhs, int ldr, double* R, double* U,
+                                                            int ld, int rows, int cols, double* partials,
+                                                            PcgState* st, double* hist) {
+    double rr = 0.0;
+    ROW_LOOP(rows, cols) {
+        const double v = rhs[(size_t)r * ldr + cc];
+        R[(size_t)r * ld + cc] = v;
+        U[(size_t)r * ld + cc] = 0.0;
+        rr = fma(v, v, rr);
+    }
+    __shared__ double sh[VT / 32];
+    const double p = block_sum<VT>(rr, sh);
+    if (threadIdx.x == 0) partials[blockIdx.x] = p;
+    if (arrive_last(&st->counter[2], gridDim.x)) {
+        const double tot = sum_partials<VT>(partials, gridDim.x, 1, sh);
+        if (threadIdx.x == 0) {
+            st->counter[2] = 0;
+            pcg_finish_init(st, tot, hist);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(VT) pcg_init_warm_kernel(const double* rhs, int ldr, const double* W, double* R,
+                                                           int ld, int rows, int cols, double* partials,
+                                                           PcgState* st, double* hist) {
+    double rr = 0.0;
+    ROW_LOOP(rows, cols) {
+        const double v = __dsub_rn(rhs[(size_t)r * ldr + cc], W[(size_t)r * ld + cc]);  // R = rhs - op(U)
+        R[(size_t)r * ld + cc] = v;
+        rr = fma(v, v, rr);
+    }
+    __shared__ double sh[VT / 32];
+    const double p = block_sum<VT>(rr, sh);
+    if (threadIdx.x == 0) partials[blockIdx.x] = p;
+    if (arrive_last(&st->counter[2], gridDim.x)) {
+        const double tot = sum_partials<VT>(partials, gridDim.x, 1, sh);
+        if (threadIdx.x == 0) {
+            st->counter[2] = 0;
+            pcg_finish_init(st, tot, hist);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(VT) pcg_direction_kernel(const double* Z, double* Q0, double* Q1, int ld,
+                                                           int rows, int cols, PcgState* st) {
+    if (st->status != SFB_PCG_RUNNING) return;
+    const int s = st->iter;
+    const double beta = s > 0 ? st->rz_next / st->rz : 0.0;
+    double* Qc = (s & 1) ? Q1 : Q0;
+    const double* Qp = (s & 1) ? Q0 : Q1;
+    ROW_LOOP(rows, cols) {
+        const size_t o = (size_t)r * ld + cc;
+        Qc[o] = s > 0 ? __dadd_rn(__dmul_rn(beta, Qp[o]), Z[o]) : Z[o];
+    }
+}
+
+__global__ void __launch_bounds__(VT) pcg_dots_kernel(const double* W, const double* Q0, const double* Q1, int ld,
+                                                      int rows, int cols, double* partials, PcgState* st) {
+    if (st->status != SFB_PCG_RUNNING) return;
+    const int s = st->iter;
+    const double* Q = (s & 1) ? Q1 : Q0;
+    double wq = 0.0, qq = 0.0;
+    ROW_LOOP(rows, cols) {
+        const size_t o = (size_t)r * ld + cc;
+        const double q = Q[o];
+        wq = fma(W[o], q, wq);
+        qq = fma(q, q, qq);
+    }
+    __shared__ double sh[VT / 32];
+    const double p0 = block_sum<VT>(wq, sh);
+    const double p1 = block_sum<VT>(qq, sh);
+    if (threadIdx.x == 0) {
+        partials[blockIdx.x] = p0;
+        partials[gridDim.x + blockIdx.x] = p1;
+    }
+    if (arrive_last(&st->counter[0], gridDim.x)) {
+        const double qw = sum_partials<VT>(partials, gridDim.x, 1, sh);
+        const double q2 = sum_partials<VT>(partials + gridDim.x, gridDim.x, 1, sh);
+        if (threadIdx.x == 0) {
+            st->counter[0] = 0;
+            st->rz = st->rz_next;
+            st->qq = q2;
+            if (qw <= 0.0) {
+                st->status = SFB_PCG_INDEFINITE;
+                st->bad_value = qw;
+                st->bad_iter = s;
+            } else {
+                st->alpha = st->rz / qw;
+            }
+        }
+    }
+}
+
+__global__ void __launch_bounds__(VT) pcg_record_kernel(const double* U, int ld, int rows, int cols,
+                                                        double* iterates, PcgState* st) {
+    // record_iterates (solvers.py:441-442): copy U_s once per completed iteration
+    const int it = st->iter;
+    if (it >= st->n_iterates || st->recorded >= it) return;
+    if (st->status == SFB_PCG_INDEFINITE || st->status == SFB_PCG_NONFINITE) return;
+    double* dst = iterates + (size_t)it * rows * cols;
+    ROW_LOOP(rows, cols) dst[(size_t)r * cols + cc] = U[(size_t)r * ld + cc];
+    if (arrive_last(&st->counter[5], gridDim.x)) {
+        if (threadIdx.x == 0) {
+            st->counter[5] = 0;
+            st->recorded = it;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(VT) copy_dot_kernel(const double* R, double* Z, int ld, int rows, int cols,
+                                                      double* partials, PcgState* st, double* dot_out,
+                                                      unsigned* counter) {
+    if (st != nullptr && st->status != SFB_PCG_RUNNING) return;
+    double zr = 0.0;
+    ROW_LOOP(rows, cols) {
+        const size_t o = (size_t)r * ld + cc;
+        const double v = R[o];
+        Z[o] = v;
+        zr = fma(v, v, zr);
+    }
+    __shared__ double sh[VT / 32];
+    const double p = block_sum<VT>(zr, sh);
+    if (threadIdx.x == 0) partials[blockIdx.x] = p;
+    if (arrive_last(counter, gridDim.x)) {
+        const double tot = sum_partials<VT>(partials, gridDim.x, 1, sh);
+        if (threadIdx.x == 0) {
+            *counter = 0;
+            if (st != nullptr) st->rz_next = tot;
+            if (dot_out != nullptr) *dot_out = tot;
+        }
+    }
+}
+
+__global__ void loop_ctl_kernel(PcgState* st, cudaGraphConditionalHandle handle, int use_handle) {
+    // continue while running and below max_iter; the body counter is a hard
+    // backstop so a logic error can never spin the device forever.
+    const unsigned runs = ++st->counter[6];
+    const bool keep = st->status == SFB_PCG_RUNNING && st->iter < st->max_iter &&
+                      runs <= (unsigned)st->max_iter + 2u;
+    if (use_handle) cudaGraphSetConditional(handle, keep ? 1u : 0u);
+}
+
+__global__ void __launch_bounds__(VT) norms_kernel(const double* A, int lda, const double* B, int ldb, int rows,
+                                                   int cols, double* partials, RedSlots* out) {
+    // v = { |A - B|, max|A| (finite entries), #non-finite(A), |A| }
+    double d2 = 0.0, a2 = 0.0, mx = 0.0, bad = 0.0;
+    ROW_LOOP(rows, cols) {
+        const double a = A[(size_t)r * lda + cc];
+        const double d = B ? a - B[(size_t)r * ldb + cc] : a;
+        d2 = fma(d, d, d2);
+        a2 = fma(a, a, a2);
+        if (isfinite(a)) mx = fmax(mx, fabs(a));
+        else bad += 1.0;
+    }
+    __shared__ double sh[VT / 32];
+    __shared__ double smx[VT / 32];
+    const double p0 = block_sum<VT>(d2, sh);
+    const double p2 = block_sum<VT>(bad, sh);
+    const double p3 = block_sum<VT>(a2, sh);
+    #pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) smx[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    const unsigned nb = gridDim.x;
+    if (threadIdx.x == 0) {
+        double m = 0.0;
+        for (int i = 0; i < VT / 32; ++i) m = fmax(m, smx[i]);
+        partials[blockIdx.x] = p0;
+        partials[nb + blockIdx.x] = m;
+        partials[2 * nb + blockIdx.x] = p2;
+        partials[3 * nb + blockIdx.x] = p3;
+    }
+    if (arrive_last(&out->counter[0], nb)) {
+        const double t0 = sum_partials<VT>(partials, nb, 1, sh);
+        const double t2 = sum_partials<VT>(partials + 2 * nb, nb, 1, sh);
+        const double t3 = sum_partials<VT>(partials + 3 * nb, nb, 1, sh);
+        if (threadIdx.x == 0) {
+            double m = 0.0;
+            for (unsigned i = 0; i < nb; ++i) m = fmax(m, __ldcg(partials + nb + i));
+            out->counter[0] = 0;
+            out->v[0] = sqrt(t0);
+            out->v[1] = m;
+            out->v[2] = t2;
+            out->v[3] = sqrt(t3);
+        }
+    }
+}
+
+}  // namespace
+
+int vector_grid_blocks() { return VB; }
+
+int launch_pcg_init_plain(const double* rhs, int ldr, double* R, double* U, int ld, int rows, int cols,
+                          double* partials, PcgState* st, double* hist, cudaStream_t s) {
+    pcg_init_plain_kernel<<<VB, VT, 0, s>>>(rhs, ldr, R, U, ld, rows, cols, partials, st, hist);
+    SFB_CHECK_LAUNCH();
+    return SFB_OK;
+}
+
+int launch_pcg_init_warm(const double* rhs, int ldr, const double* W, double* R, int ld, int rows, int cols,
+                         double* partials, PcgState* st, double* hist, cudaStream_t s) {
+    pcg_init_warm_kernel<<<VB, VT, 0, s>>>(rhs, ldr, W, R, ld, rows, cols, partials, st, hist);
+    SFB_CHECK_LAUNCH();
+    return SFB_OK;
+}
+
+int launch_pcg_direction(const double* Z, double* Q0, double* Q1, int ld, int rows, int cols, PcgState* st,
+                         cudaStream_t s) {
+    pcg_direction_kernel<<<VB, VT, 0, s>>>(Z, Q0, Q1, ld, rows, cols, st);
+    SFB_CHECK_LAUNCH();
+    return SFB_OK;
+}
+
+int launch_pcg_dots(const double* W, const double* Q0, const double* Q1, int ld, int rows, int cols,
+                    double* partials, PcgState* st, cudaStream_t s) {
+    pcg_dots_kernel<<<VB, VT, 0, s>>>(W, Q0, Q1, ld, rows, cols, partials, st);
+    SFB_CHECK_LAUNCH();
+    return SFB_OK;
+}
+
+int launch_pcg_update(double* U, double* R, const double* W, const double* Q0, const double* Q1, int ld,
+                      int rows, int cols, double* partials, PcgState* st, double* hist, double* incs,
+                      cudaStream_t s) {
+    pcg_update_kernel<<<VB, VT, 0, s>>>(U, R, W, Q0, Q1, ld, rows, cols, partials, st, hist, incs);
+    SFB_CHECK_LAUNCH();
+    return SFB_OK;
+}
+
+int launch_pcg_record(const double* U, int ld, int rows, int cols, double* iterates, PcgState* st,
+                      cudaStream_t s) {
+    pcg_record_kernel<<<VB, VT, 0, s>>>(U, ld, rows, cols, iterates, st);
+    SFB_CHECK_LAUNCH();
+    return SFB_OK;
+}
+
+int launch_copy_dot(const double* R, double* Z, int ld, int rows, int cols, double* partials, PcgState* st,
+                    RedSlots* red, cudaStream_t s) {
+    unsigned* counter = st ? &st->counter[3] : &red->counter[1];
+    double* dot_out = red ? &red->v[3] : nullptr;
+    copy_dot_kernel<<<VB, VT, 0, s>>>(R, Z, ld, rows, cols, partials, st, dot_out, counter);
+    SFB_CHECK_LAUNCH();
+    return SFB_OK;
+}
+
+int launch_loop_ctl(PcgState* st, unsigned long long handle, int use_handle, cudaStream_t s) {
+    loop_ctl_kernel<<<1, 1, 0, s>>>(st, (cudaGraphConditionalHandle)handle, use_handle);
+    SFB_CHECK_LAUNCH();
+    return SFB_OK;
+}
+
+int launch_norms(const double* A, int lda, const double* B, int ldb, int rows, int cols, double* partials,
+                 RedSlots* out, cudaStream_t s) {
+    norms_kernel<<<VB, VT, 0, s>>>(A, lda, B, ldb, rows, cols, partials, out);
+    SFB_CHECK_LAUNCH();
+    return SFB_OK;
+}
+
+}  // namespace sfb

@@ -1,0 +1,571 @@
+"""Reduced (spectral) solve and MO-PCG on the B200 — drop-in for solvers.py.
+
+Same entry points, report types, stopping rules, guards and error messages as
+the reference (solvers.py:36-453).  What changes is where the work runs:
+
+* ``Preconditioner.apply_inverse`` (solvers.py:134-143) — the reference does
+  two dense LU solves.  Here the single-term preconditioner P_L U P_R is
+  applied with FP64 DMMA tensor-core GEMMs: ``mode="inverse"`` (default) as
+  Z = P_L^-1 R P_R^-1 with the dense inverses formed once on the device by
+  banded Cholesky sweeps (2 GEMMs, 4 q^3 flops); ``mode="spectral"`` as
+  V_L [(V_L^T R V_R) / (lam_i mu_j)] V_R^T (4 GEMMs); ``mode="banded"``
+   as banded Cholesky sweeps, O(q^2 k).
+* ``solve_reduced`` (solvers.py:284-300) — LAPACK generalized ``eigh`` on the
+  host (the reference's route, off the loop), then the 4-GEMM spectral
+  sandwich with the 1/(lam1_i + lam2_j) Hadamard fused into a GEMM epilogue.
+* ``mo_pcg`` (solvers.py:365-453) — the whole loop is device resident (one
+  CUDA-graph launch per solve; see csrc/solver.cu).
+"""
+
+from __future__ import annotations
+
+import os
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import scipy.linalg as sla
+import scipy.linalg.lapack as lapack
+
+from . import _native as nat
+from .banded import Band
+from .exceptions import OperatorError, SolverError
+from .fem1d import DirectionSet
+from .operators import SylvesterOperator, is_unit_degenerate
+
+RCOND_GUARD = 1e-14
+PENCIL_GUARD = 1e-12
+DEFAULT_TOL = 1e-10
+DEFAULT_MAX_ITER = 1000
+PRECOND_MODES = ("inverse", "spectral", "banded")
+
+
+def default_precond_mode() -> str:
+    mode = os.environ.get("SYLFEM_B200_PRECOND", "inverse")
+    if mode not in PRECOND_MODES:
+        raise SolverError(f"SYLFEM_B200_PRECOND must be one of {PRECOND_MODES}, got '{mode}'")
+    return mode
+
+
+@dataclass
+class SolveReport:
+    """Solution plus convergence record of one linear solve (solvers.py:36-46)."""
+
+    solution: object
+    method: str
+    iterations: int
+    residual_history: np.ndarray
+    stop_reason: str
+    wall_time: float
+    diagnostics: dict = field(default_factory=dict)
+
+
+# ------------------------------------------------------------- stopping ----
+@dataclass(frozen=True)
+class StoppingRule:
+    """Residual-relative or increment-absolute stop test (solvers.py:53-63)."""
+
+    kind: str
+    value: float
+
+    def describe(self) -> str:
+        if self.kind == "residual":
+            return f"|R_s| <= {self.value:g} * |R_0|"
+        return f"|U_s+1 - U_s| <= {self.value:g}"
+
+
+def relative_residual(tol: float = DEFAULT_TOL) -> StoppingRule:
+    return StoppingRule("residual", float(tol))
+
+
+def increment_threshold(threshold: float) -> StoppingRule:
+    return StoppingRule("increment", float(threshold))
+
+
+def reference_increment(reference_error_norm: float, fraction: float = 0.05) -> StoppingRule:
+    return increment_threshold(fraction * reference_error_norm)
+
+
+def timestep_residual(tau: float) -> StoppingRule:
+    return relative_residual(tau)
+
+
+# ------------------------------------------------------- preconditioner ----
+def _lapack_band(m: Band):
+    """LAPACK general-band storage (2kl+ku+1, n) of a square Band."""
+    lo, hi = m.offsets()
+    kl, ku = max(-lo, 0), max(hi, 0)
+    n = m.shape[0]
+    ab = np.zeros((2 * kl + ku + 1, n))
+    c = m.sparse.tocoo()
+    ab[kl + ku + c.row - c.col, c.col] = c.data
+    return ab, kl, ku
+
+
+def _rcond(mat) -> float:
+    """1-norm reciprocal condition number (estimate for banded factors)."""
+    if isinstance(mat, Band) and mat.half_bandwidth() <= 16:
+        ab, kl, ku = _lapack_band(mat)
+        anorm = float(np.max(np.asarray(abs(mat.sparse).sum(axis=0)).ravel()))
+        lu, ipiv, info = lapack.dgbtrf(ab, kl, ku)
+        if info > 0:
+            return 0.0
+        rc, info = lapack.dgbcon(kl, ku, lu, ipiv, anorm)
+        return float(rc) if np.isfinite(rc) else 0.0
+    try:
+        c = np.linalg.cond(np.asarray(mat, dtype=float), 1)
+    except np.linalg.LinAlgError:
+        c = np.inf
+    return 0.0 if not np.isfinite(c) else 1.0 / c
+
+
+def _rcond_guard(mat, name: str) -> None:
+    """solvers.py:90-100."""
+    rc = _rcond(mat)
+    if rc < RCOND_GUARD:
+        raise SolverError(f"preconditioner factor '{name}' is numerically singular (rcond ~ {rc:.2e})")
+
+
+def _as_factor(m):
+    if m is None:
+        return None
+    if isinstance(m, Band):
+        return m
+    import scipy.sparse as sp
+    if sp.issparse(m):
+        return Band(m)
+    return np.asarray(m, dtype=float)
+
+
+def _cholesky_band(m, q: int):
+    """Lower banded Cholesky in the device layout: band[i][d] = C[i][i-b+d],
+    band[i][b] = 1 / C[i][i].  Returns (b, band) or None if not SPD-banded."""
+    if m is None:
+        return 0, np.ones((q, 1))
+    b = m.half_bandwidth() if isinstance(m, Band) else None
+    if b is None or b > 4:
+        return None
+    M = m.sparse
+    if abs(M - M.T).max() > 1e-12 * max(m.max_abs(), 1e-300):
+        return None
+    ab = np.zeros((b + 1, q))  # LAPACK lower: ab[i-j, j] = A[i, j]
+    c = M.tocoo()
+    low = c.row >= c.col
+    ab[c.row[low] - c.col[low], c.col[low]] = c.data[low]
+    try:
+        L = sla.cholesky_banded(ab, lower=True)
+    except np.linalg.LinAlgError:
+        return None
+    band = np.zeros((q, b + 1))
+    for d in range(b + 1):  # C[i][i-b+d] = L[b-d, i-(b-d)]
+        off = b - d
+        band[off:, d] = L[off, : q - off]
+    band[:, b] = 1.0 / L[0, :]
+    return b, band
+
+
+class Preconditioner:
+    """Single-term preconditioner U -> P_L U P_R (solvers.py:103-150).
+
+    The factors are kept as given (Band or dense); the device form is built on
+    first use according to ``mode`` (see module docstring)."""
+
+    def __init__(self, left=None, right=None, left_name: str = "P_L", right_name: str = "P_R",
+                 mode: str | None = None):
+        self.left = _as_factor(left)
+        self.right = _as_factor(right)
+        self.left_name = left_name
+        self.right_name = right_name
+        self.mode = default_precond_mode() if mode is None else mode
+        if self.mode not in PRECOND_MODES:
+            raise SolverError(f"unknown preconditioner mode '{self.mode}'")
+        if self.left is not None:
+            _rcond_guard(self.left, left_name)
+        if self.right is not None:
+            _rcond_guard(self.right, right_name)
+        self._handle = None
+        self._fwd = None
+        self.shape = None if self.is_identity else (
+            (self.left.shape[0] if self.left is not None else self.right.shape[0]),
+            (self.right.shape[0] if self.right is not None else self.left.shape[0]))
+
+    @property
+    def is_identity(self) -> bool:
+        return self.left is None and self.right is None
+
+    # ---- device form -----------------------------------------------------
+    def native(self, shape=None):
+        """Device preconditioner for grids of ``shape`` (needed for identity)."""
+        shape = tuple(shape) if shape is not None else self.shape
+        if self._handle is not None and self._handle_shape == shape:
+            return self._handle.p
+        if shape is None:
+            raise SolverError("identity preconditioner needs a grid shape")
+        qy, qx = shape
+        L = nat.lib()
+        out = nat.C.c_void_p()
+        if self.is_identity:
+            nat.check(L.sfb_pre_create(qy, qx, nat.PRE_IDENTITY, None, None, None, None,
+                                       nat.C.byref(out)), "preconditioner")
+        elif self.mode == "banded":
+            cl, cr = _cholesky_band(self.left, qy), _cholesky_band(self.right, qx)
+            if cl is None or cr is None:
+                raise SolverError("banded preconditioner mode needs symmetric positive definite "
+                                  "factors with half-bandwidth <= 4")
+            nat.check(L.sfb_pre_create_banded(qy, qx, cl[0], nat.host_ptr(np.ascontiguousarray(cl[1])),
+                                              cr[0], nat.host_ptr(np.ascontiguousarray(cr[1])),
+                                              nat.C.byref(out)), "preconditioner")
+        elif self.mode == "spectral":
+            lamL, VL = self._eigh(self.left, qy)
+            lamR, VR = self._eigh(self.right, qx)
+            nat.check(L.sfb_pre_create(qy, qx, nat.PRE_SPECTRAL_PROD, nat.host_ptr(VL), nat.host_ptr(VR),
+                                       nat.host_ptr(lamL), nat.host_ptr(lamR), nat.C.byref(out)),
+                      "preconditioner")
+        else:
+            Linv = self._inverse(self.left, qy, left=True)
+            RinvT = np.ascontiguousarray(self._inverse(self.right, qx, left=False).T)
+            nat.check(L.sfb_pre_create(qy, qx, nat.PRE_INVERSE, nat.host_ptr(Linv), nat.host_ptr(RinvT),
+                                       None, None, nat.C.byref(out)), "preconditioner")
+        self._handle = nat.Handle(out.value, L.sfb_pre_destroy)
+        self._handle_shape = shape
+        return self._handle.p
+
+    @staticmethod
+    def _eigh(m, q):
+        if m is None:
+            return np.ones(q), np.eye(q)
+        A = np.asarray(m, dtype=float)
+        lam, V = sla.eigh(0.5 * (A + A.T), driver="evd")
+        return np.ascontiguousarray(lam), np.ascontiguousarray(V)
+
+    @staticmethod
+    def _inverse(m, q, left: bool):
+        """Dense inverse: device banded-Cholesky sweeps over the identity for
+        SPD banded factors, host LAPACK otherwise (setup, off the loop)."""
+        if m is None:
+            return np.eye(q)
+        ch = _cholesky_band(m, q)
+        if ch is None:
+            return np.ascontiguousarray(np.linalg.inv(np.asarray(m, dtype=float)))
+        L = nat.lib()
+        t = nat.torch()
+        one = np.ones((q, 1))
+        out = nat.C.c_void_p()
+        b = np.ascontiguousarray(ch[1])
+        if left:  # P^-1 I by column sweeps
+            rc = L.sfb_pre_create_banded(q, q, ch[0], nat.host_ptr(b), 0, nat.host_ptr(one), nat.C.byref(out))
+        else:     # I P^-1 by row sweeps
+            rc = L.sfb_pre_create_banded(q, q, 0, nat.host_ptr(one), ch[0], nat.host_ptr(b), nat.C.byref(out))
+        nat.check(rc, "preconditioner inverse")
+        h = nat.Handle(out.value, L.sfb_pre_destroy)
+        eye = t.eye(q, dtype=t.float64, device="cuda")
+        inv = t.empty_like(eye)
+        nat.check(L.sfb_pre_apply(h.p, nat.ptr(eye), q, nat.ptr(inv), q, nat.stream()), "inverse")
+        return np.ascontiguousarray(inv.cpu().numpy())
+
+    # ---- application -----------------------------------------------------
+    def apply(self, U):
+        """P_L U P_R (solvers.py:124-132)."""
+        if self.is_identity:
+            return U.clone() if nat.is_device(U) else np.array(U, copy=True)
+        if self._fwd is None:
+            qy, qx = self.shape
+            self._fwd = SylvesterOperator([(self.left if self.left is not None else Band.diag(np.ones(qy)),
+                                            self.right if self.right is not None else Band.diag(np.ones(qx)))])
+        return self._fwd.apply(U)
+
+    def apply_inverse(self, U):
+        """P_L^-1 U P_R^-1 (solvers.py:134-143)."""
+        on_dev = nat.is_device(U)
+        if self.is_identity:
+            return U.clone() if on_dev else np.array(U, copy=True)
+        t = nat.torch()
+        Ud = nat.to_device(U)
+        qy, qx = Ud.shape
+        if self.shape != (qy, qx):
+            raise OperatorError(f"grid shape {(qy, qx)} does not match preconditioner {self.shape}")
+        Z = t.empty_like(Ud)
+        nat.check(nat.lib().sfb_pre_apply(self.native(), nat.ptr(Ud), qx, nat.ptr(Z), qx, nat.stream()),
+                  "apply_inverse")
+        return Z if on_dev else Z.cpu().numpy()
+
+
+IDENTITY_PRECONDITIONER = "identity"
+
+
+def make_preconditioner(kind: str, x: DirectionSet, y: DirectionSet, *, d_u: float = 1.0,
+                        tau: float = 0.0, lumped: bool = False, mode: str | None = None) -> Preconditioner:
+    """Named single-term preconditioners (solvers.py:156-196)."""
+    if kind == "identity":
+        return Preconditioner()
+    if kind == "parabolic_lumped":
+        kind, lumped = "parabolic", True
+    mx, my = x.mats, y.mats
+    if lumped and (x.lumped is None or y.lumped is None):
+        raise SolverError("lumped preconditioner requested without lumped matrices")
+    flat = is_unit_degenerate(y)
+    if kind == "elliptic_square":
+        return Preconditioner(my.A, mx.A, "A(y)", "A(x)", mode=mode)
+    if kind == "elliptic_xnormal":
+        if lumped:
+            right = mx.A if flat else mx.A + x.lumped.A2
+            return Preconditioner(y.lumped.A1, right, "A1(y)", "A(x)" if flat else "A+A2(x)", mode=mode)
+        right = mx.A if flat else mx.A + mx.B2
+        return Preconditioner(my.B1, right, "B1(y)", "A(x)" if flat else "A+B2(x)", mode=mode)
+    if kind == "parabolic":
+        c = d_u * tau
+        if lumped:
+            left = y.lumped.M0 @ y.lumped.D1 + c * y.lumped.A1
+            right = x.lumped.M0 + c * (mx.A if flat else mx.A + x.lumped.A2)
+            return Preconditioner(left, right, "M0*D1+d*tau*A1(y)", "M0+d*tau*(A+A2)(x)", mode=mode)
+        left = my.M3 + c * my.B1
+        right = mx.M + c * (mx.A if flat else mx.A + mx.B2)
+        return Preconditioner(left, right, "M3+d*tau*B1(y)", "M+d*tau*(A+B2)(x)", mode=mode)
+    raise SolverError(f"unknown preconditioner kind '{kind}'")
+
+
+# ------------------------------------------------------ spectral solve -----
+def _fix_eigvectors(vecs: np.ndarray) -> np.ndarray:
+    """Largest-magnitude entry of each column positive (solvers.py:203-208)."""
+    idx = np.argmax(np.abs(vecs), axis=0)
+    signs = np.sign(vecs[idx, np.arange(vecs.shape[1])])
+    signs[signs == 0] = 1.0
+    return vecs * signs
+
+
+def _min_abs_pair_sum(a: np.ndarray, b: np.ndarray) -> float:
+    """min_ij |a_i + b_j| in O(n log n) (b sorted)."""
+    bs = np.sort(b)
+    pos = np.searchsorted(bs, -a)
+    best = np.full(a.shape, np.inf)
+    for p in (pos - 1, pos):
+        ok = (p >= 0) & (p < bs.size)
+        best[ok] = np.minimum(best[ok], np.abs(a[ok] + bs[p[ok]]))
+    return float(best.min())
+
+
+@dataclass
+class SpectralCache:
+    """Eigen-factorisations of the two pencils of a two-term equation
+    (solvers.py:211-253); the device sandwich is built on first use."""
+
+    lam1: np.ndarray
+    lam2: np.ndarray
+    P1: np.ndarray
+    P2: np.ndarray
+    G2: object
+    H1: object
+    swapped: bool
+
+    @property
+    def X1(self):
+        return self.P1
+
+    @property
+    def X1inv(self):
+        return self.P1.T @ np.asarray(self.G2)
+
+    @property
+    def X2(self):
+        return np.asarray(self.H1) @ self.P2
+
+    @property
+    def X2inv(self):
+        return self.P2.T
+
+    def kernel(self) -> np.ndarray:
+        self.check_pencils()
+        return 1.0 / (self.lam1[:, None] + self.lam2[None, :])
+
+    def check_pencils(self) -> None:
+        if _min_abs_pair_sum(self.lam1, self.lam2) < PENCIL_GUARD:
+            raise SolverError("spectral pencils are (numerically) singular: an eigenvalue "
+                              f"sum fell below {PENCIL_GUARD:g}")
+
+    def native(self):
+        h = getattr(self, "_handle", None)
+        if h is None:
+            L = nat.lib()
+            qy, qx = self.P1.shape[0], self.P2.shape[0]
+            out = nat.C.c_void_p()
+            nat.check(L.sfb_pre_create(qy, qx, nat.PRE_SPECTRAL_SUM,
+                                       nat.host_ptr(np.ascontiguousarray(self.P1)),
+                                       nat.host_ptr(np.ascontiguousarray(self.P2)),
+                                       nat.host_ptr(np.ascontiguousarray(self.lam1)),
+                                       nat.host_ptr(np.ascontiguousarray(self.lam2)), nat.C.byref(out)),
+                      "spectral cache")
+            h = nat.Handle(out.value, L.sfb_pre_destroy)
+            self._handle = h
+        return h.p
+
+
+def build_spectral_cache(op: SylvesterOperator) -> SpectralCache:
+    """Generalized SPD eigh of both pencils with term-order auto-detection
+    (solvers.py:256-281), on the host (LAPACK dsygvd, the reference's route)."""
+    if len(op.terms) != 2:
+        raise SolverError(f"spectral reduction needs a two-term operator, got {len(op.terms)} terms")
+    last = None
+    for i, j, swapped in ((0, 1, False), (1, 0, True)):
+        (G1, H1), (G2, H2) = op.terms[i], op.terms[j]
+        try:
+            lam1, P1 = sla.eigh(np.asarray(G1), np.asarray(G2))
+            lam2, P2 = sla.eigh(np.asarray(H2), np.asarray(H1))
+        except (np.linalg.LinAlgError, sla.LinAlgError) as exc:
+            last = exc
+            continue
+        return SpectralCache(lam1=lam1, lam2=lam2, P1=_fix_eigvectors(P1), P2=_fix_eigvectors(P2),
+                             G2=G2, H1=H1, swapped=swapped)
+    raise SolverError(f"operator is not reducible to Z1 U + U Z2 form: {last}")
+
+
+def solve_reduced(op: SylvesterOperator, rhs, cache: SpectralCache | None = None) -> SolveReport:
+    """U = P1 [(P1^T B P2) / (lam1_i + lam2_j)] P2^T on the device (solvers.py:284-300)."""
+    t0 = time.perf_counter()
+    if cache is None:
+        cache = build_spectral_cache(op)
+    cache.check_pencils()
+    on_dev = nat.is_device(rhs)
+    t = nat.torch()
+    B = nat.to_device(rhs)
+    qy, qx = B.shape
+    U = t.empty_like(B)
+    L = nat.lib()
+    nat.check(L.sfb_pre_apply(cache.native(), nat.ptr(B), qx, nat.ptr(U), qx, nat.stream()), "reduced solve")
+    out2 = np.zeros(2)
+    nat.check(L.sfb_op_residual(op.native(), nat.ptr(U), qx, nat.ptr(B), qx, nat.dptr(out2), nat.stream()),
+              "residual")
+    res = out2[0] / max(out2[1], 1e-300)
+    return SolveReport(solution=U if on_dev else U.cpu().numpy(), method="reduced", iterations=0,
+                       residual_history=np.array([res]), stop_reason="direct",
+                       wall_time=time.perf_counter() - t0,
+                       diagnostics={"pencil_swapped": cache.swapped})
+
+
+def dirichlet_p1_eigenvalues(N: int, gamma: float = 0.0) -> np.ndarray:
+    """Closed-form eigenvalues of M^-1 A + gamma/2, P1 Dirichlet (solvers.py:303-312)."""
+    i = np.arange(1, N)
+    lam_a = 2.0 * N * (1.0 - np.cos(i * np.pi / N))
+    return ((12.0 * N * N - gamma) * lam_a + 6.0 * N * gamma) / (12.0 * N - 2.0 * lam_a)
+
+
+def dirichlet_sine_basis(N: int) -> np.ndarray:
+    i = np.arange(1, N)
+    return np.sin(np.outer(i, i) * np.pi / N)
+
+
+def solve_reduced_closed_form(gamma: float, f_nodal, N: int) -> SolveReport:
+    """Sine-basis spectral solve, P1 Dirichlet square (solvers.py:321-354).
+
+    With V = sqrt(2/N) X (orthogonal, symmetric) the reference's
+    (2/N) X [(1/(lam_i+lam_j)) o ((2/N) X F X)] X is the device sandwich
+    V [(V F V) / (lam_i + lam_j)] V."""
+    t0 = time.perf_counter()
+    on_dev = nat.is_device(f_nodal)
+    F = nat.to_device(f_nodal)
+    q = N - 1
+    if tuple(F.shape) != (q, q):
+        raise SolverError(f"closed-form path needs a square {q} x {q} nodal source, got {tuple(F.shape)}")
+    if gamma < 0:
+        raise SolverError("reaction coefficient must be nonnegative")
+    lam = dirichlet_p1_eigenvalues(N, gamma)
+    if _min_abs_pair_sum(lam, lam) < PENCIL_GUARD:
+        raise SolverError("singular eigenvalue sum in closed-form reduction")
+    V = np.ascontiguousarray(np.sqrt(2.0 / N) * dirichlet_sine_basis(N))
+    cache = SpectralCache(lam1=lam, lam2=lam, P1=V, P2=V, G2=None, H1=None, swapped=False)
+    t = nat.torch()
+    L = nat.lib()
+    U = t.empty_like(F)
+    h = cache.native()
+    nat.check(L.sfb_pre_apply(h, nat.ptr(F), q, nat.ptr(U), q, nat.stream()), "closed form")
+    fh = t.empty_like(F)
+    uh = t.empty_like(F)
+    nat.check(L.sfb_pre_transform(h, nat.ptr(F), q, nat.ptr(fh), q, nat.stream()), "transform")
+    nat.check(L.sfb_pre_transform(h, nat.ptr(U), q, nat.ptr(uh), q, nat.stream()), "transform")
+    lt = t.from_numpy(lam).to("cuda")
+    denom = lt[:, None] + lt[None, :]
+    res = float(t.linalg.norm(denom * uh - fh) / max(float(t.linalg.norm(fh)), 1e-300))
+    return SolveReport(solution=U if on_dev else U.cpu().numpy(), method="reduced-closed", iterations=0,
+                       residual_history=np.array([res]), stop_reason="direct",
+                       wall_time=time.perf_counter() - t0,
+                       diagnostics={"residual_space": "spectral"})
+
+
+# --------------------------------------------------------------- MO-PCG ----
+_REASONS = {nat.PCG_TOLERANCE: "tolerance", nat.PCG_INCREMENT: "increment", nat.PCG_MAX_ITER: "max_iter"}
+
+
+class _PcgSolver:
+    """Device MO-PCG workspace bound to one (operator, preconditioner) pair."""
+
+    def __init__(self, op: SylvesterOperator, pre: Preconditioner):
+        L = nat.lib()
+        out = nat.C.c_void_p()
+        nat.check(L.sfb_pcg_create(op.native(), pre.native(op.shape), nat.C.byref(out)), "mo_pcg")
+        self.handle = nat.Handle(out.value, L.sfb_pcg_destroy)
+        self.op, self.pre = op, pre
+
+
+def _solver_for(op: SylvesterOperator, pre: Preconditioner) -> _PcgSolver:
+    key = id(pre)
+    s = op._pcg_cache.get(key)
+    if s is None or s.pre is not pre:
+        s = _PcgSolver(op, pre)
+        op._pcg_cache[key] = s
+    return s
+
+
+def mo_pcg(op: SylvesterOperator, rhs, precond: Preconditioner | None = None,
+           stop: StoppingRule | None = None, u0=None, max_iter: int = DEFAULT_MAX_ITER,
+           record_iterates: bool = False) -> SolveReport:
+    """Conjugate gradients with grid-matrix iterates (solvers.py:365-453).
+
+    Numpy in -> numpy out (drop-in); CUDA tensors in -> CUDA tensors out.
+    ``diagnostics["dense_grid_matrices"]`` keeps the reference's memory-model
+    constant (5); the device workspace is reported under ``"device"``."""
+    if not (op.symmetric and op.positive_definite):
+        raise OperatorError("mo_pcg needs an operator flagged self-adjoint positive definite")
+    if precond is None:
+        precond = Preconditioner()
+    if stop is None:
+        stop = relative_residual(DEFAULT_TOL)
+    t0 = time.perf_counter()
+    on_dev = nat.is_device(rhs)
+    t = nat.torch()
+    B = nat.to_device(rhs)
+    qy, qx = op.shape
+    if tuple(B.shape) != (qy, qx):
+        raise OperatorError(f"grid shape {tuple(B.shape)} does not match operator {op.shape}")
+    U0 = None if u0 is None else nat.to_device(u0)
+    if U0 is not None and tuple(U0.shape) != (qy, qx):
+        raise OperatorError(f"grid shape {tuple(U0.shape)} does not match operator {op.shape}")
+    solver = _solver_for(op, precond)
+    U = t.empty((qy, qx), dtype=t.float64, device="cuda")
+    hist = np.zeros(max_iter + 1)
+    incs = np.zeros(max(max_iter, 1))
+    its = t.empty((max_iter + 1, qy, qx), dtype=t.float64, device="cuda") if record_iterates else None
+    res = nat.PcgResult()
+    rule = nat.RULE_RESIDUAL if stop.kind == "residual" else nat.RULE_INCREMENT
+    nat.check(nat.lib().sfb_pcg_solve(
+        solver.handle.p, nat.ptr(B), qx, nat.ptr(U0) if U0 is not None else None, qx, nat.ptr(U), qx,
+        rule, float(stop.value), int(max_iter), nat.dptr(hist), nat.dptr(incs),
+        nat.ptr(its) if its is not None else None, max_iter + 1 if its is not None else 0,
+        nat.C.byref(res), nat.stream()), "mo_pcg")
+    n = res.iterations
+    if res.stop_reason == nat.PCG_INDEFINITE:
+        raise OperatorError("operator is not positive definite along a search direction "
+                            f"(<L(Q), Q> = {res.bad_value:.3e} at iteration {res.bad_iter})")
+    if res.stop_reason == nat.PCG_NONFINITE:
+        raise SolverError(f"mo_pcg residual became non-finite at iteration {res.bad_iter}")
+    diag = {"dense_grid_matrices": 5, "increments": incs[:n].copy(),
+            "preconditioner": (precond.left_name, precond.right_name)
+            if not precond.is_identity else ("identity", "identity"),
+            "stopping_rule": stop.describe(),
+            "device": {"loop_ms": res.device_ms, "graph_launches": res.chunks,
+                       "precond_mode": "identity" if precond.is_identity else precond.mode,
+                       "operator": "banded" if op.banded else "dense"}}
+    if record_iterates:
+        host = its[: n + 1].cpu().numpy()
+        diag["iterates"] = [host[i] for i in range(n + 1)]
+    return SolveReport(solution=U if on_dev else U.cpu().numpy(), method="mo-pcg", iterations=n,
+                       residual_history=hist[: n + 1].copy(), stop_reason=_REASONS[res.stop_reason],
+                       wall_time=time.perf_counter() - t0, diagnostics=diag)

@@ -1,0 +1,254 @@
+"""IMEX-Euler drivers on the B200 — drop-in for timestepping.py.
+
+Per step (timestepping.py:148-157, 200-218): the explicit part and the rhs
+weighting run as one fused banded pass on the device (``RhsBuilder.heat`` /
+``RhsBuilder.dib``; the blow-up test of timestepping.py:89-91 is a by-product
+of that pass), each species' implicit solve is a device-resident MO-PCG warm
+started from the previous state, and the increment / steady-state norms are
+one reduction kernel.  States never leave the device between steps.
+
+Sources given as ``SeparableSource`` (s(t) * F) and kinetics given as a
+``DIBKinetics`` pair are evaluated on the device; any other Python callable is
+evaluated on the host (the reference's contract: callables see numpy arrays)
+and its result uploaded once per step.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+from typing import Callable
+
+import numpy as np
+
+from . import _native as nat
+from .exceptions import ConfigError, SolverError
+from .fem1d import BCKind, DirectionSet
+from .geometry import DomainSpec
+from .models import DIBKinetics
+from .operators import expand_with_boundary, full_node_grid, parabolic_operator
+from .solvers import Preconditioner, make_preconditioner, mo_pcg, relative_residual, timestep_residual
+
+BLOWUP_LIMIT = 1e100
+
+
+@dataclass(frozen=True)
+class TimeGrid:
+    """Fixed-step axis, n_steps = ceil(t_final / tau) (timestepping.py:28-41)."""
+
+    tau: float
+    t_final: float
+
+    def __post_init__(self):
+        if self.tau <= 0 or self.t_final <= 0:
+            raise ConfigError("tau and t_final must be positive")
+
+    @property
+    def n_steps(self) -> int:
+        return max(1, math.ceil(self.t_final / self.tau - 1e-9))
+
+
+@dataclass(frozen=True)
+class InnerSolver:
+    """Per-step linear solver configuration (timestepping.py:44-59)."""
+
+    method: str = "mo-pcg"
+    precond: str = "auto"
+    rule: str = "tau"
+    tol: float = 1e-10
+    max_iter: int = 400
+    precond_mode: str | None = None  # device form of the preconditioner (solvers.PRECOND_MODES)
+
+    def stopping(self, tau: float):
+        if self.rule == "tau":
+            return timestep_residual(tau)
+        if self.rule == "residual":
+            return relative_residual(self.tol)
+        raise ConfigError(f"unknown stopping rule '{self.rule}'")
+
+
+class BlowUpError(SolverError):
+    """Non-finite state; carries the last finite state (timestepping.py:62-69)."""
+
+    def __init__(self, step: int, species: str, state):
+        super().__init__(f"solution blew up at step {step} (species {species})")
+        self.step = step
+        self.species = species
+        self.state = state
+
+
+@dataclass
+class Trajectory:
+    """Final state and per-step metrics (timestepping.py:72-82)."""
+
+    final: tuple
+    increments: np.ndarray
+    iterations: np.ndarray
+    times: np.ndarray
+    steady_step: int | None = None
+    snapshots: list = field(default_factory=list)
+    diagnostics: dict = field(default_factory=dict)
+
+
+class SeparableSource:
+    """source(u, X, Y, t) = time_factor(t) * F with F sampled on the full node
+    grid; evaluated on the device by the heat driver, and callable on the host
+    with the reference's signature."""
+
+    def __init__(self, F, time_factor: Callable[[float], float]):
+        self.F = np.asarray(F, dtype=float)
+        self.time_factor = time_factor
+
+    def __call__(self, u, X, Y, t):
+        return self.time_factor(t) * self.F
+
+
+def _step_setup(inner: InnerSolver):
+    if inner.method != "mo-pcg":
+        raise ConfigError(f"inner solver '{inner.method}' is the reference's sparse-LU oracle path; "
+                          "the B200 solve path uses mo-pcg")
+
+
+def _parabolic_precond(x, y, d_u, tau, lumped, inner: InnerSolver):
+    """timestepping.py:115-123."""
+    name = inner.precond
+    if name == "auto":
+        name = "parabolic_lumped" if lumped else "parabolic"
+    if name == "identity":
+        return Preconditioner()
+    return make_preconditioner(name, x, y, d_u=d_u, tau=tau, lumped=lumped, mode=inner.precond_mode)
+
+
+def _norms(A, B=None):
+    """{|A - B|, max|A|, #non-finite(A), |A|} on the device."""
+    out = np.zeros(4)
+    nat.check(nat.lib().sfb_diff_norm(nat.ptr(A), A.shape[1], nat.ptr(B) if B is not None else None,
+                                      A.shape[1], A.shape[0], A.shape[1], nat.dptr(out), nat.stream()),
+              "norm")
+    return out
+
+
+def _bad(chk) -> bool:
+    return chk[1] > 0 or chk[0] > BLOWUP_LIMIT
+
+
+def _host(t):
+    return t.cpu().numpy()
+
+
+def _solve(op, rhs, pre, stop, warm, inner: InnerSolver):
+    rep = mo_pcg(op, rhs, precond=pre, stop=stop, u0=warm, max_iter=inner.max_iter)
+    if rep.stop_reason == "max_iter":
+        raise SolverError(f"inner PCG did not converge in {inner.max_iter} iterations")
+    return rep.solution, rep.iterations
+
+
+def imex_euler_heat(domain: DomainSpec, x: DirectionSet, y: DirectionSet, d_u: float, source: Callable,
+                    u0, grid: TimeGrid, inner: InnerSolver | None = None, lumped: bool = False) -> Trajectory:
+    """u_t - d_u Lap u = source(u, x, y, t) (timestepping.py:126-159)."""
+    inner = inner or InnerSolver()
+    _step_setup(inner)
+    tau = grid.tau
+    op, rhs_of = parabolic_operator(x, y, d_u, tau, lumped=lumped)
+    pre = _parabolic_precond(x, y, d_u, tau, lumped, inner)
+    stop = inner.stopping(tau)
+    X = Y = None
+    F = None
+    if isinstance(source, SeparableSource):
+        F = nat.to_device(source.F)
+        if tuple(F.shape) != rhs_of.in_shape:
+            raise ConfigError(f"separable source must cover the full node grid {rhs_of.in_shape}")
+    else:
+        X, Y = full_node_grid(domain, x, y)
+    U = nat.to_device(u0).clone()
+    n = grid.n_steps
+    incs = np.empty(n)
+    iters = np.empty(n, dtype=int)
+    for k in range(n):
+        t_k = k * tau
+        if F is not None:
+            rhs, chk = rhs_of.heat(U, tau * float(source.time_factor(t_k)), F)
+        else:
+            Uf = expand_with_boundary(_host(U), x, y)
+            W = Uf + tau * np.asarray(source(Uf, X, Y, t_k), dtype=float)
+            fin = np.isfinite(W)
+            chk = (float(np.max(np.abs(W[fin]))) if fin.any() else 0.0, float((~fin).sum()))
+            rhs = rhs_of(nat.to_device(W))
+        if _bad(chk):
+            raise BlowUpError(k, "u", _host(U))
+        Un, it = _solve(op, rhs, pre, stop, U, inner)
+        nrm = _norms(Un, U)
+        if nrm[2] > 0 or nrm[1] > BLOWUP_LIMIT:
+            raise BlowUpError(k, "u", _host(U))
+        incs[k] = nrm[0]
+        iters[k] = it
+        U = Un
+    return Trajectory(final=(_host(U),), increments=incs, iterations=iters,
+                      times=(1 + np.arange(n)) * tau)
+
+
+def imex_euler_rds(domain: DomainSpec, x: DirectionSet, y: DirectionSet, d_u: float, d_v: float, kinetics,
+                   rho: float, state0, grid: TimeGrid, inner: InnerSolver | None = None, lumped: bool = False,
+                   snapshot_every: int = 0, steady_eps: float = 1e-8) -> Trajectory:
+    """Two-species reaction-diffusion, kinetics explicit (timestepping.py:162-220)."""
+    if d_u <= 0 or d_v <= 0 or rho <= 0:
+        raise ConfigError("d_u, d_v and rho must be positive")
+    if x.basis.bc is not BCKind.NEUMANN:
+        raise ConfigError("the reaction-diffusion stepper expects zero-flux BCs")
+    inner = inner or InnerSolver()
+    _step_setup(inner)
+    tau = grid.tau
+    f_fun, g_fun = kinetics
+    op_u, rhs_of = parabolic_operator(x, y, d_u, tau, lumped=lumped)
+    op_v, _ = parabolic_operator(x, y, d_v, tau, lumped=lumped)
+    stop = inner.stopping(tau)
+    pre_u = _parabolic_precond(x, y, d_u, tau, lumped, inner)
+    pre_v = _parabolic_precond(x, y, d_v, tau, lumped, inner)
+    device_kin = isinstance(kinetics, DIBKinetics)
+    kp = kinetics.params.device_params() if device_kin else None
+    U = nat.to_device(state0[0]).clone()
+    V = nat.to_device(state0[1]).clone()
+    n = grid.n_steps
+    incs = np.empty((n, 2))
+    iters = np.empty((n, 2), dtype=int)
+    snaps = []
+    steady = None
+    host_rates = None
+    for k in range(n):
+        if not device_kin:
+            Uh, Vh = _host(U), _host(V)
+            host_rates = (np.asarray(f_fun(Uh, Vh)), np.asarray(g_fun(Uh, Vh)))
+
+        def rhs_for(species):
+            if device_kin:
+                return rhs_of.dib(U, V, species, tau * rho, kp)
+            base = _host(U) if species == 0 else _host(V)
+            W = base + tau * rho * host_rates[species]
+            fin = np.isfinite(W)
+            chk = (float(np.max(np.abs(W[fin]))) if fin.any() else 0.0, float((~fin).sum()))
+            return rhs_of(nat.to_device(W)), chk
+
+        last = lambda: (_host(U), _host(V))  # noqa: E731
+        rhs_u, chk = rhs_for(0)
+        if _bad(chk):
+            raise BlowUpError(k, "u", last())
+        Un, it_u = _solve(op_u, rhs_u, pre_u, stop, U, inner)
+        nu = _norms(Un, U)
+        if nu[2] > 0 or nu[1] > BLOWUP_LIMIT:
+            raise BlowUpError(k, "u", last())
+        rhs_v, chk = rhs_for(1)
+        if _bad(chk):
+            raise BlowUpError(k, "v", last())
+        Vn, it_v = _solve(op_v, rhs_v, pre_v, stop, V, inner)
+        nv = _norms(Vn, V)
+        if nv[2] > 0 or nv[1] > BLOWUP_LIMIT:
+            raise BlowUpError(k, "v", last())
+        incs[k] = (nu[0], nv[0])
+        iters[k] = (it_u, it_v)
+        U, V = Un, Vn
+        if steady is None and np.all(incs[k] <= steady_eps * max(nu[3], 1e-300)):
+            steady = k
+        if snapshot_every and ((k + 1) % snapshot_every == 0 or k == n - 1):
+            snaps.append((k + 1, _host(U), _host(V)))
+    return Trajectory(final=(_host(U), _host(V)), increments=incs, iterations=iters,
+                      times=(1 + np.arange(n)) * tau, steady_step=steady, snapshots=snaps)

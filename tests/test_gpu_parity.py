@@ -1,0 +1,289 @@
+"""Parity of the CUDA path (through the C ABI) with the reference.
+
+Every comparison is against the golden vectors produced by the reference
+itself (tests/golden) or, where sizes vary, against the pinned oracle on the
+same seeded inputs.  Tolerances follow BASELINE.json's north star: 1e-10
+relative Frobenius for fp64 solutions (1e-12 for single operator / rhs /
+preconditioner applications), MO-PCG iteration counts within +-1.
+"""
+
+import numpy as np
+import pytest
+
+import oracle as orc
+import paper_2109_01173_b200 as pb
+from _cases import OBC, ODOMS, OP_CASES, cosine_source_rect, sine_source
+from conftest import relerr
+from test_host_logic import PBC, PDOM, RECT, WAVE
+
+pytestmark = pytest.mark.gpu
+
+D, NB = pb.BCKind.DIRICHLET, pb.BCKind.NEUMANN
+MODES = ["inverse", "spectral", "banded"]
+
+
+def build_op(i):
+    kind, k, n, dn, bc, p, lumped = OP_CASES[i]
+    x, y = pb.build_direction_sets(PDOM[dn], k, n, PBC[bc], lumped=lumped)
+    if kind == "ell":
+        return pb.elliptic_operator(x, y, p, lumped=lumped)
+    return pb.parabolic_operator(x, y, 1.0, p, lumped=lumped)
+
+
+# ------------------------------------------------------------ operators ----
+@pytest.mark.parametrize("i", range(len(OP_CASES)))
+def test_operator_apply_and_rhs_vs_reference(golden, i):
+    op, rhs_of = build_op(i)
+    tag = f"op/{i}"
+    assert relerr(op.apply(golden[f"{tag}/U"]), golden[f"{tag}/AU"]) <= 1e-12
+    assert relerr(rhs_of(golden[f"{tag}/F"]), golden[f"{tag}/rhs"]) <= 1e-12
+
+
+def test_dense_operator_fallback_matches_oracle():
+    rng = np.random.default_rng(5)
+    q = 37
+    S = rng.standard_normal((q, q))
+    M1 = S @ S.T + q * np.eye(q)
+    A1 = np.diag(np.arange(1.0, q + 1))
+    terms = [(A1, M1), (M1, A1)]
+    op = pb.SylvesterOperator(terms, symmetric=True, positive_definite=True)
+    assert not op.banded
+    U = rng.standard_normal((q, q))
+    assert relerr(op.apply(U), orc.apply_terms(terms, U)) <= 1e-13
+    rhs = rng.standard_normal((q, q))
+    rep = pb.solve_reduced(op, rhs)
+    assert np.linalg.norm(orc.apply_terms(terms, rep.solution) - rhs) <= 1e-10 * np.linalg.norm(rhs)
+
+
+def test_rectangular_grids():
+    x, y = pb.build_direction_sets(pb.CAP_DOMAIN, 2, (12, 8), D)
+    ox, oy = orc.direction_sets(orc.cap_domain(), 2, (12, 8), orc.DIRICHLET)
+    op, rhs_of = pb.elliptic_operator(x, y, 1.0)
+    ot, orhs = orc.elliptic_terms(ox, oy, 1.0)
+    U = np.random.default_rng(1).standard_normal(op.shape)
+    assert op.shape == (7, 11)
+    assert relerr(op.apply(U), orc.apply_terms(ot, U)) <= 1e-13
+    F = np.random.default_rng(2).standard_normal((9, 13))
+    assert relerr(rhs_of(F), orhs(F)) <= 1e-13
+
+
+# -------------------------------------------------------- reduced solve ----
+def test_reduced_cfg1_type(golden):
+    x, y = pb.build_direction_sets(pb.SQUARE, 1, 17, D)
+    op, rhs_of = pb.elliptic_operator(x, y, 1.0)
+    rhs = rhs_of(sine_source(17, 17, 1))
+    assert relerr(rhs, golden["red1/rhs"]) <= 1e-13
+    rep = pb.solve_reduced(op, rhs)
+    assert relerr(rep.solution, golden["red1/U"]) <= 1e-10
+    assert rep.residual_history[-1] <= 1e-11
+    assert rep.stop_reason == "direct" and rep.iterations == 0
+    assert rep.diagnostics["pencil_swapped"] is False
+
+
+def test_reduced_cfg2_type_swaps(golden):
+    x, y = pb.build_direction_sets(RECT, 3, 12, NB)
+    op, rhs_of = pb.elliptic_operator(x, y, 0.5)
+    assert len(op) == 2
+    rep = pb.solve_reduced(op, rhs_of(cosine_source_rect(12, 2)))
+    assert rep.diagnostics["pencil_swapped"] is True
+    assert relerr(rep.solution, golden["red2/U"]) <= 1e-10
+
+
+def test_hadamard_known_answer_and_singular_pencil():
+    Z = np.diag([2.0, 3.0])
+    op = pb.SylvesterOperator([(Z, np.eye(2)), (np.eye(2), Z)], symmetric=True, positive_definite=True)
+    rep = pb.solve_reduced(op, np.ones((2, 2)))
+    assert np.allclose(rep.solution, [[1 / 4, 1 / 5], [1 / 5, 1 / 6]], atol=1e-14)
+    bad = pb.SylvesterOperator([(np.diag([1.0, 2.0]), np.eye(2)), (np.eye(2), np.diag([-1.0, 3.0]))])
+    with pytest.raises(pb.SolverError, match="singular"):
+        pb.solve_reduced(bad, np.ones((2, 2)))
+
+
+@pytest.mark.parametrize("gamma", [0.0, 1.0])
+def test_closed_form_matches_reduced(gamma):
+    n = 24
+    x, y = pb.build_direction_sets(pb.SQUARE, 1, n, D)
+    op, rhs_of = pb.elliptic_operator(x, y, gamma)
+    X, Y = pb.full_node_grid(pb.SQUARE, x, y)
+    F = 8 * np.pi ** 2 * np.sin(2 * np.pi * X) * np.sin(2 * np.pi * Y)
+    a = pb.solve_reduced(op, rhs_of(F)).solution
+    rep = pb.solve_reduced_closed_form(gamma, pb.interior_values(F, x, y), n)
+    assert relerr(rep.solution, a) <= 1e-10
+    assert rep.residual_history[0] <= 1e-12
+
+
+# ------------------------------------------------------- preconditioner ----
+@pytest.mark.parametrize("mode", MODES)
+def test_preconditioner_inverse_vs_reference(golden, mode):
+    x, y = pb.build_direction_sets(WAVE, 2, 16, D)
+    pre = pb.make_preconditioner("elliptic_xnormal", x, y, mode=mode)
+    assert relerr(pre.apply_inverse(golden["pcg3/R"]), golden["pcg3/PinvR"]) <= 1e-12
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_preconditioner_round_trip(mode):
+    x, y = pb.build_direction_sets(pb.CAP_DOMAIN, 2, 8, D)
+    p = pb.make_preconditioner("elliptic_xnormal", x, y, mode=mode)
+    U = np.random.default_rng(3).standard_normal((y.q, x.q))
+    assert np.allclose(p.apply_inverse(p.apply(U)), U, atol=1e-12)
+    assert np.allclose(p.apply(p.apply_inverse(U)), U, atol=1e-12)
+
+
+# --------------------------------------------------------------- MO-PCG ----
+def cfg3_small():
+    x, y = pb.build_direction_sets(WAVE, 2, 16, D)
+    op, rhs_of = pb.elliptic_operator(x, y, 1.0)
+    return x, y, op, rhs_of(sine_source(16, 16, 3))
+
+
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("tol_tag,tol", [("t12", 1e-12), ("t8", 1e-8)])
+def test_mo_pcg_cfg3_type_vs_reference(golden, mode, tol_tag, tol):
+    x, y, op, rhs = cfg3_small()
+    pre = pb.make_preconditioner("elliptic_xnormal", x, y, mode=mode)
+    rep = pb.mo_pcg(op, rhs, precond=pre, stop=pb.relative_residual(tol), max_iter=5000,
+                    record_iterates=True)
+    tag = f"pcg3/{tol_tag}"
+    assert rep.stop_reason == "tolerance"
+    assert abs(rep.iterations - int(golden[f"{tag}/iters"])) <= 1
+    for a, b in zip(rep.diagnostics["iterates"][:8], golden[f"{tag}/first8"]):
+        assert relerr(a, b) <= 1e-10
+    assert relerr(rep.solution, golden[f"{tag}/U"]) <= (1e-10 if tol < 1e-10 else 1e-7)
+    hist = golden[f"{tag}/hist"]
+    m = min(len(hist), len(rep.residual_history), 8)
+    assert np.allclose(rep.residual_history[:m], hist[:m], rtol=1e-9)
+    assert rep.diagnostics["preconditioner"] == ("B1(y)", "A+B2(x)")
+    assert rep.diagnostics["dense_grid_matrices"] == 5
+    # the stopping criterion holds when re-evaluated with the reference's apply
+    ox, oy = orc.direction_sets(orc.wave_domain(), 2, 16, orc.DIRICHLET)
+    ot, _ = orc.elliptic_terms(ox, oy, 1.0)
+    r = np.linalg.norm(rhs - orc.apply_terms(ot, rep.solution))
+    assert r <= tol * np.linalg.norm(rhs) * 1.01 + 1e-14
+
+
+def test_mo_pcg_identity_operator_one_iteration():
+    q = 6
+    op = pb.SylvesterOperator([(np.eye(q), np.eye(q))], symmetric=True, positive_definite=True)
+    rhs = np.random.default_rng(1).standard_normal((q, q))
+    rep = pb.mo_pcg(op, rhs, stop=pb.relative_residual(1e-12))
+    assert rep.iterations == 1 and rep.stop_reason == "tolerance"
+    assert np.allclose(rep.solution, rhs, atol=1e-12)
+
+
+def test_mo_pcg_flags_indefinite_max_iter_zero_rhs():
+    with pytest.raises(pb.OperatorError):
+        pb.mo_pcg(pb.SylvesterOperator([(np.eye(3), np.eye(3))]), np.ones((3, 3)))
+    neg = pb.SylvesterOperator([(-np.eye(3), np.eye(3))], symmetric=True, positive_definite=True)
+    with pytest.raises(pb.OperatorError, match="positive definite"):
+        pb.mo_pcg(neg, np.random.default_rng(2).standard_normal((3, 3)))
+    x, y = pb.build_direction_sets(pb.CAP_DOMAIN, 1, 16, D, lumped=True)
+    op, _ = pb.elliptic_operator(x, y, 0.0)
+    rep = pb.mo_pcg(op, np.random.default_rng(3).standard_normal(op.shape),
+                    stop=pb.relative_residual(1e-14), max_iter=2)
+    assert rep.stop_reason == "max_iter" and rep.iterations == 2
+    assert len(rep.residual_history) == 3 and len(rep.diagnostics["increments"]) == 2
+    rep = pb.mo_pcg(op, np.zeros(op.shape))
+    assert rep.iterations == 0 and rep.stop_reason == "tolerance"
+    assert np.array_equal(rep.solution, np.zeros(op.shape))
+
+
+def test_mo_pcg_warm_start_and_monotone_residual():
+    x, y = pb.build_direction_sets(pb.JAR_DOMAIN, 1, 16, D, lumped=True)
+    op, _ = pb.elliptic_operator(x, y, 0.0)
+    pre = pb.make_preconditioner("elliptic_xnormal", x, y)
+    rhs = np.random.default_rng(4).standard_normal(op.shape)
+    rep = pb.mo_pcg(op, rhs, precond=pre, stop=pb.relative_residual(1e-10), max_iter=500)
+    h = rep.residual_history
+    assert np.max((h[1:] - h[:-1]) / h[0]) <= 1e-8
+    warm = pb.mo_pcg(op, rhs, precond=pre, u0=rep.solution, stop=pb.relative_residual(1e-10))
+    assert warm.residual_history[0] <= 1e-9 * h[0]
+
+
+def test_mo_pcg_increment_rule_and_dense_operator():
+    rng = np.random.default_rng(7)
+    q = 20
+    S = rng.standard_normal((q, q))
+    G = S @ S.T + q * np.eye(q)
+    terms = [(G, np.eye(q)), (np.eye(q), G)]
+    op = pb.SylvesterOperator(terms, symmetric=True, positive_definite=True)
+    rhs = rng.standard_normal((q, q))
+    rep = pb.mo_pcg(op, rhs, stop=pb.relative_residual(1e-12), max_iter=500, record_iterates=True)
+    ref = orc.mo_pcg(terms, rhs, rule=("residual", 1e-12), max_iter=500, record=True)
+    assert abs(rep.iterations - ref["iterations"]) <= 1
+    for a, b in list(zip(rep.diagnostics["iterates"], ref["iterates"]))[:8]:
+        assert relerr(a, b) <= 1e-10
+    assert relerr(rep.solution, ref["solution"]) <= 1e-10
+    inc = pb.mo_pcg(op, rhs, stop=pb.increment_threshold(1e-6), max_iter=500)
+    ri = orc.mo_pcg(terms, rhs, rule=("increment", 1e-6), max_iter=500)
+    assert inc.stop_reason == "increment" and abs(inc.iterations - ri["iterations"]) <= 1
+
+
+def test_mo_pcg_device_tensors_round_trip():
+    import torch
+    x, y, op, rhs = cfg3_small()
+    pre = pb.make_preconditioner("elliptic_xnormal", x, y)
+    rd = torch.from_numpy(rhs).cuda()
+    rep = pb.mo_pcg(op, rd, precond=pre, stop=pb.relative_residual(1e-12), max_iter=5000)
+    assert rep.solution.is_cuda
+    host = pb.mo_pcg(op, rhs, precond=pre, stop=pb.relative_residual(1e-12), max_iter=5000)
+    assert np.array_equal(rep.solution.cpu().numpy(), host.solution)  # deterministic reductions
+
+
+# ------------------------------------------------------------------ IMEX ----
+@pytest.mark.parametrize("tol_tag,tol", [("t12", 1e-12), ("t8", 1e-8)])
+@pytest.mark.parametrize("device_source", [True, False])
+def test_imex_heat_cfg4_type_vs_reference(golden, tol_tag, tol, device_source):
+    x, y = pb.build_direction_sets(WAVE, 4, 8, D)
+    F = sine_source(8, 8, 4)
+    src = pb.SeparableSource(F, lambda t: np.exp(-t)) if device_source else \
+        (lambda u, X, Y, t: np.exp(-t) * F)
+    tr = pb.imex_euler_heat(WAVE, x, y, 1.0, src, golden["heat/u0"], pb.TimeGrid(1e-3, 5e-3),
+                            inner=pb.InnerSolver(rule="residual", tol=tol, max_iter=5000))
+    assert np.all(np.abs(tr.iterations - golden[f"heat/{tol_tag}/iters"]) <= 1)
+    assert relerr(tr.final[0], golden[f"heat/{tol_tag}/U"]) <= (1e-10 if tol < 1e-10 else 1e-7)
+    assert np.allclose(tr.increments, golden[f"heat/{tol_tag}/incs"], rtol=1e-6)
+
+
+@pytest.mark.parametrize("tag", ["tau", "t12"])
+@pytest.mark.parametrize("device_kin", [True, False])
+def test_imex_dib_cfg5_type_vs_reference(golden, tag, device_kin):
+    p = pb.dib_presets("spots_worms").replace(rho=400.0)
+    x, y = pb.build_direction_sets(pb.SQUARE, 1, 15, NB, lumped=True)
+    state0 = (golden["dib/eta0"], golden["dib/theta0"])
+    kin = pb.dib_kinetics_pair(p) if device_kin else \
+        (lambda u, v: pb.dib_kinetics(u, v, p)[0], lambda u, v: pb.dib_kinetics(u, v, p)[1])
+    tau = 5e-3 / p.rho
+    inner = pb.InnerSolver(rule="residual", tol=1e-12, max_iter=2000) if tag == "t12" else pb.InnerSolver()
+    tr = pb.imex_euler_rds(pb.SQUARE, x, y, 1.0, p.d_theta, kin, p.rho, state0, pb.TimeGrid(tau, 6 * tau),
+                           inner=inner, lumped=True, snapshot_every=2)
+    assert np.array_equal(tr.iterations, golden[f"dib/{tag}/iters"])
+    assert [s[0] for s in tr.snapshots] == list(golden[f"dib/{tag}/snap_steps"])
+    tolr = 1e-10 if tag == "t12" else 1e-8
+    assert relerr(tr.final[0], golden[f"dib/{tag}/U"]) <= tolr
+    assert relerr(tr.final[1], golden[f"dib/{tag}/V"]) <= tolr
+
+
+def test_imex_guards():
+    x, y = pb.build_direction_sets(pb.CAP_DOMAIN, 1, 8, D)
+    z = np.zeros((y.q, x.q))
+    with pytest.raises(pb.ConfigError, match="zero-flux"):
+        pb.imex_euler_rds(pb.CAP_DOMAIN, x, y, 1.0, 1.0, (lambda u, v: u, lambda u, v: v), 1.0, (z, z),
+                          pb.TimeGrid(0.01, 0.05))
+    u0 = np.random.default_rng(1).standard_normal((y.q, x.q))
+    with pytest.raises(pb.SolverError, match="did not converge"):
+        pb.imex_euler_heat(pb.CAP_DOMAIN, x, y, 0.1, lambda u, X, Y, t: np.ones_like(u), u0,
+                           pb.TimeGrid(0.1, 0.3), inner=pb.InnerSolver(rule="residual", tol=1e-14, max_iter=1))
+    p = pb.dib_presets("spots_worms")
+    xn, yn = pb.build_direction_sets(pb.CAP_DOMAIN, 1, (12, 8), NB, lumped=True)
+    e0, t0 = pb.initial_fields((yn.q, xn.q), pb.InitialData(amplitude=1e-4, seed=11))
+    with pytest.raises(pb.BlowUpError) as info:
+        pb.imex_euler_rds(pb.CAP_DOMAIN, xn, yn, 1.0, p.d_theta,
+                          (lambda u, v: 1e12 * (1.0 + u ** 2), lambda u, v: np.zeros_like(v)), p.rho,
+                          (e0, t0), pb.TimeGrid(0.5, 5.0),
+                          inner=pb.InnerSolver(rule="residual", tol=1e-8, max_iter=2000))
+    assert info.value.species == "u" and info.value.state is not None
+    zero = (lambda u, v: np.zeros_like(u), lambda u, v: np.zeros_like(u))
+    tr = pb.imex_euler_rds(pb.CAP_DOMAIN, xn, yn, 1.0, p.d_theta, zero, p.rho,
+                           (np.full((yn.q, xn.q), 0.7), np.full((yn.q, xn.q), 0.3)), pb.TimeGrid(0.01, 0.1),
+                           inner=pb.InnerSolver(rule="residual", tol=1e-13))
+    assert np.max(tr.increments) <= 1e-12 and tr.steady_step == 0
