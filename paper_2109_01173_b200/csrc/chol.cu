@@ -22,7 +22,10 @@ namespace {
 
 template <int B>
 __global__ void __launch_bounds__(128) chol_cols_kernel(const double* __restrict__ band, int n,
-                                                        double* __restrict__ X, int ld, int ncols) {
+                                                        const double* __restrict__ Xin, int ldi,
+                                                        double* __restrict__ X, int ld, int ncols,
+                                                        const PcgState* st) {
+    if (st != nullptr && st->status != SFB_PCG_RUNNING) return;
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= ncols) return;
     double w[B > 0 ? B : 1];
@@ -32,7 +35,7 @@ __global__ void __launch_bounds__(128) chol_cols_kernel(const double* __restrict
     #pragma unroll 4
     for (int i = 0; i < n; ++i) {
         const double* c = band + (size_t)i * (B + 1);
-        double v = X[(size_t)i * ld + j];
+        double v = Xin[(size_t)i * ldi + j];
         #pragma unroll
         for (int d = 0; d < B; ++d) v = fma(-c[d], w[d], v);  // w[d] = y[i-B+d]
         v *= c[B];
@@ -63,8 +66,11 @@ constexpr int RT = 32;  // rows per warp / tile width
 
 template <int B>
 __global__ void __launch_bounds__(32) chol_rows_kernel(const double* __restrict__ band, int n,
-                                                       double* __restrict__ X, int ld, int nrows) {
+                                                       double* __restrict__ X, int ld, int nrows,
+                                                       ZrDot zr) {
+    if (zr.pcg != nullptr && zr.pcg->status != SFB_PCG_RUNNING) return;
     __shared__ double tile[RT][RT + 1];
+    double dot = 0.0;
     const int lane = threadIdx.x;
     const int i0 = blockIdx.x * RT;
     const int my_row = i0 + lane;
@@ -131,41 +137,65 @@ __global__ void __launch_bounds__(32) chol_rows_kernel(const double* __restrict_
         #pragma unroll 8
         for (int r = 0; r < RT; ++r) {
             const int gi = i0 + r;
-            if (gi < nrows && jc < n) X[(size_t)gi * ld + jc] = tile[r][lane];
+            if (gi < nrows && jc < n) {
+                const double z = tile[r][lane];
+                X[(size_t)gi * ld + jc] = z;
+                if (zr.R != nullptr) dot = fma(z, zr.R[(size_t)gi * zr.ldr + jc], dot);
+            }
         }
         __syncwarp();
     }
     (void)my_row;
+    if (zr.R != nullptr) {  // <Z,R> for beta (solvers.py:448), deterministic
+        #pragma unroll
+        for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+        if (lane == 0) zr.partials[blockIdx.x] = dot;
+        if (arrive_last(zr.counter, gridDim.x)) {
+            double v = 0.0;
+            for (unsigned i = lane; i < gridDim.x; i += 32) v += __ldcg(zr.partials + i);
+            #pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (lane == 0) {
+                *zr.counter = 0;
+                if (zr.pcg != nullptr) zr.pcg->rz_next = v;
+                if (zr.dot_out != nullptr) *zr.dot_out = v;
+            }
+        }
+    }
 }
 
 }  // namespace
 
-int launch_band_chol_cols(const double* lband, int bw, int n, double* X, int ld, int ncols, cudaStream_t s) {
+int launch_band_chol_cols(const double* lband, int bw, int n, const double* Xin, int ldi, double* X, int ld,
+                          int ncols, const PcgState* st, cudaStream_t s) {
     const dim3 grid((ncols + 127) / 128);
     switch (bw) {
-        case 0: chol_cols_kernel<0><<<grid, 128, 0, s>>>(lband, n, X, ld, ncols); break;
-        case 1: chol_cols_kernel<1><<<grid, 128, 0, s>>>(lband, n, X, ld, ncols); break;
-        case 2: chol_cols_kernel<2><<<grid, 128, 0, s>>>(lband, n, X, ld, ncols); break;
-        case 3: chol_cols_kernel<3><<<grid, 128, 0, s>>>(lband, n, X, ld, ncols); break;
-        case 4: chol_cols_kernel<4><<<grid, 128, 0, s>>>(lband, n, X, ld, ncols); break;
+        case 0: chol_cols_kernel<0><<<grid, 128, 0, s>>>(lband, n, Xin, ldi, X, ld, ncols, st); break;
+        case 1: chol_cols_kernel<1><<<grid, 128, 0, s>>>(lband, n, Xin, ldi, X, ld, ncols, st); break;
+        case 2: chol_cols_kernel<2><<<grid, 128, 0, s>>>(lband, n, Xin, ldi, X, ld, ncols, st); break;
+        case 3: chol_cols_kernel<3><<<grid, 128, 0, s>>>(lband, n, Xin, ldi, X, ld, ncols, st); break;
+        case 4: chol_cols_kernel<4><<<grid, 128, 0, s>>>(lband, n, Xin, ldi, X, ld, ncols, st); break;
         default: set_error("banded Cholesky: half-bandwidth > 4"); return SFB_ERR_UNSUPPORTED;
     }
     SFB_CHECK_LAUNCH();
     return SFB_OK;
 }
 
-int launch_band_chol_rows(const double* rband, int bw, int n, double* X, int ld, int nrows, cudaStream_t s) {
+int launch_band_chol_rows(const double* rband, int bw, int n, double* X, int ld, int nrows, const ZrDot& zr,
+                          cudaStream_t s) {
     const dim3 grid((nrows + RT - 1) / RT);
     switch (bw) {
-        case 0: chol_rows_kernel<0><<<grid, 32, 0, s>>>(rband, n, X, ld, nrows); break;
-        case 1: chol_rows_kernel<1><<<grid, 32, 0, s>>>(rband, n, X, ld, nrows); break;
-        case 2: chol_rows_kernel<2><<<grid, 32, 0, s>>>(rband, n, X, ld, nrows); break;
-        case 3: chol_rows_kernel<3><<<grid, 32, 0, s>>>(rband, n, X, ld, nrows); break;
-        case 4: chol_rows_kernel<4><<<grid, 32, 0, s>>>(rband, n, X, ld, nrows); break;
+        case 0: chol_rows_kernel<0><<<grid, 32, 0, s>>>(rband, n, X, ld, nrows, zr); break;
+        case 1: chol_rows_kernel<1><<<grid, 32, 0, s>>>(rband, n, X, ld, nrows, zr); break;
+        case 2: chol_rows_kernel<2><<<grid, 32, 0, s>>>(rband, n, X, ld, nrows, zr); break;
+        case 3: chol_rows_kernel<3><<<grid, 32, 0, s>>>(rband, n, X, ld, nrows, zr); break;
+        case 4: chol_rows_kernel<4><<<grid, 32, 0, s>>>(rband, n, X, ld, nrows, zr); break;
         default: set_error("banded Cholesky: half-bandwidth > 4"); return SFB_ERR_UNSUPPORTED;
     }
     SFB_CHECK_LAUNCH();
     return SFB_OK;
 }
+
+int band_chol_rows_blocks(int nrows) { return (nrows + RT - 1) / RT; }
 
 }  // namespace sfb

@@ -9,9 +9,10 @@
 // sm_100a has no FP64 tcgen05 kind, so the FP64 tensor path is the warp-level
 // DMMA.8x8x4 (mma.sync m8n8k4 f64).  Tiles are staged by TMA
 // (cp.async.bulk.tensor, SWIZZLE_128B) into a 4-stage shared-memory ring
-// guarded by mbarriers; one producer warp issues the copies, eight consumer
-// warps issue DMMA.  Both operands are K-contiguous ("NT"), which lets every
-// fragment load be a conflict-free LDS.128: thread t of a quad owns the
+// guarded by mbarriers; one thread issues the copies three k-tiles ahead and
+// all eight warps (two per SM sub-partition, 255-register budget) issue DMMA.
+// Both operands are K-contiguous ("NT"), which lets every fragment load be a
+// conflict-free LDS.128: thread t of a quad owns the
 // physical k = 4t+s for mma step s, so A[row][4t..4t+3] and Bt[col][4t..4t+3]
 // are two 16-byte chunks per 128-byte row.
 #include <cuda.h>
@@ -25,10 +26,10 @@ namespace sfb {
 namespace {
 
 constexpr int BM = 128, BN = 128, BK = 16, STAGES = 4;
-constexpr int NCONS = 8;                    // consumer warps (2 x 4)
-constexpr int NTHREADS = (NCONS + 1) * 32;  // + 1 producer warp
+constexpr int NWARPS = 8;                   // 2 x 4 warp grid, 64 x 32 per warp
+constexpr int NTHREADS = NWARPS * 32;       // 2 warps per SM sub-partition (<= 255 regs each)
 constexpr int TILE_BYTES = BM * BK * 8;     // 16 KB per operand per stage
-constexpr int SMEM_BYTES = 2 * STAGES * TILE_BYTES + 2 * STAGES * 8 + 1024;
+constexpr int SMEM_BYTES = 2 * STAGES * TILE_BYTES + STAGES * 8 + 1024;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -73,7 +74,7 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
                  : "d"(a), "d"(b));
 }
 
-__global__ void __maxnreg__(224)
+__global__ void __launch_bounds__(NTHREADS, 1)
     dgemm_nt_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     int M, int N, int K, GemmEpi ep) {
     if (ep.pcg != nullptr && ep.pcg->status != SFB_PCG_RUNNING) return;  // uniform gate
@@ -83,18 +84,22 @@ __global__ void __maxnreg__(224)
     uint8_t* sA = smem;
     uint8_t* sB = smem + STAGES * TILE_BYTES;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + 2 * STAGES * TILE_BYTES);
-    uint64_t* empty = full + STAGES;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
     const int KT = (K + BK - 1) / BK;
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < STAGES; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], NCONS);
-        }
+        for (int s = 0; s < STAGES; ++s) mbar_init(&full[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+        // prologue: fill STAGES-1 slots
+        for (int kt = 0; kt < STAGES - 1 && kt < KT; ++kt) {
+            mbar_expect_tx(&full[kt], 2 * TILE_BYTES);
+            tma_load_2d(sA + kt * TILE_BYTES, &tmA, &full[kt], kt * BK, m0);
+            tma_load_2d(sB + kt * TILE_BYTES, &tmB, &full[kt], kt * BK, n0);
+        }
     }
     __syncthreads();
 
@@ -107,54 +112,46 @@ __global__ void __maxnreg__(224)
     const int wm = warp >> 2, wn = warp & 3;  // consumer warp grid 2 x 4 (64 x 32 each)
     const int g = lane >> 2, t = lane & 3;
 
-    if (warp == NCONS) {
-        // ---------------- TMA producer (one elected lane) ----------------
-        if (lane == 0) {
-            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
-            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
-            for (int kt = 0; kt < KT; ++kt) {
-                const int s = kt % STAGES;
-                const uint32_t ph = (kt / STAGES) & 1;
-                mbar_wait(&empty[s], ph ^ 1);
-                mbar_expect_tx(&full[s], 2 * TILE_BYTES);
-                tma_load_2d(sA + s * TILE_BYTES, &tmA, &full[s], kt * BK, m0);
-                tma_load_2d(sB + s * TILE_BYTES, &tmB, &full[s], kt * BK, n0);
+    // One thread issues TMA for k-tile kt+STAGES-1 into the slot consumed at
+    // kt-1; the block barrier at the top of each step guarantees every warp
+    // has finished reading that slot (WAR), the mbarrier signals the bytes.
+    for (int kt = 0; kt < KT; ++kt) {
+        const int s = kt % STAGES;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const int kn = kt + STAGES - 1;
+            if (kn < KT) {
+                const int sn = kn % STAGES;
+                mbar_expect_tx(&full[sn], 2 * TILE_BYTES);
+                tma_load_2d(sA + sn * TILE_BYTES, &tmA, &full[sn], kn * BK, m0);
+                tma_load_2d(sB + sn * TILE_BYTES, &tmB, &full[sn], kn * BK, n0);
             }
         }
-    } else {
-        // ---------------- DMMA consumers ----------------
-        for (int kt = 0; kt < KT; ++kt) {
-            const int s = kt % STAGES;
-            mbar_wait(&full[s], (kt / STAGES) & 1);
-            const uint8_t* a_base = sA + s * TILE_BYTES + (wm * 64 + g) * 128;
-            const uint8_t* b_base = sB + s * TILE_BYTES + (wn * 32 + g) * 128;
+        mbar_wait(&full[s], (kt / STAGES) & 1);
+        const uint8_t* a_base = sA + s * TILE_BYTES + (wm * 64 + g) * 128;
+        const uint8_t* b_base = sB + s * TILE_BYTES + (wn * 32 + g) * 128;
+        #pragma unroll
+        for (int half = 0; half < 2; ++half) {
+            const int chunk = ((2 * t + half) ^ g) << 4;  // SWIZZLE_128B: chunk ^= row & 7 (= g)
+            double2 a[8], b[4];
             #pragma unroll
-            for (int half = 0; half < 2; ++half) {
-                const int chunk = ((2 * t + half) ^ g) << 4;  // SWIZZLE_128B: chunk ^= row & 7 (= g)
-                double2 a[8], b[4];
+            for (int i = 0; i < 8; ++i) a[i] = *reinterpret_cast<const double2*>(a_base + i * 8 * 128 + chunk);
+            #pragma unroll
+            for (int j = 0; j < 4; ++j) b[j] = *reinterpret_cast<const double2*>(b_base + j * 8 * 128 + chunk);
+            #pragma unroll
+            for (int i = 0; i < 8; ++i)
                 #pragma unroll
-                for (int i = 0; i < 8; ++i)
-                    a[i] = *reinterpret_cast<const double2*>(a_base + i * 8 * 128 + chunk);
+                for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i].x, b[j].x);
+            #pragma unroll
+            for (int i = 0; i < 8; ++i)
                 #pragma unroll
-                for (int j = 0; j < 4; ++j)
-                    b[j] = *reinterpret_cast<const double2*>(b_base + j * 8 * 128 + chunk);
-                #pragma unroll
-                for (int i = 0; i < 8; ++i)
-                    #pragma unroll
-                    for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i].x, b[j].x);
-                #pragma unroll
-                for (int i = 0; i < 8; ++i)
-                    #pragma unroll
-                    for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i].y, b[j].y);
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[s]);
+                for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i].y, b[j].y);
         }
     }
 
     // ---------------- epilogue (registers -> global) ----------------
     double dot = 0.0;
-    if (warp < NCONS) {
+    {
         #pragma unroll
         for (int i = 0; i < 8; ++i) {
             const int m = m0 + wm * 64 + i * 8 + g;

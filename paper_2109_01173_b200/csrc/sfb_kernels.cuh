@@ -91,9 +91,19 @@ int launch_norms(const double* A, int lda, const double* B, int ldb, int rows, i
 int vector_grid_blocks();
 
 // ------------------------------------------------------ banded solves ----
-int launch_band_chol_cols(const double* lband, int bw, int n, double* X, int ld, int ncols,
+// <Z,R> fused into the last row sweep (R == nullptr: no dot)
+struct ZrDot {
+    const double* R = nullptr;
+    int ldr = 0;
+    double* partials = nullptr;
+    unsigned* counter = nullptr;
+    PcgState* pcg = nullptr;   // status gate; receives rz_next
+    double* dot_out = nullptr;
+};
+int launch_band_chol_cols(const double* lband, int bw, int n, const double* Xin, int ldi, double* X, int ld,
+                          int ncols, const PcgState* st, cudaStream_t s);
+int launch_band_chol_rows(const double* rband, int bw, int n, double* X, int ld, int nrows, const ZrDot& zr,
                           cudaStream_t s);
-int launch_band_chol_rows(const double* rband, int bw, int n, double* X, int ld, int nrows,
-                          cudaStream_t s);
+int band_chol_rows_blocks(int nrows);
 
 }  // namespace sfb

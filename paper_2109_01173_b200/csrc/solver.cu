@@ -211,14 +211,19 @@ int pre_apply_impl(const sfb_pre* p, const double* R, int ldr, double* Z, int ld
             return launch_dgemm_nt(p->A1, p->ldA, T1, ldt1, qy, qx, qy, last, s);
         }
         case SFB_PRE_BANDED: {
-            if (pcg == nullptr && red == nullptr && Z != R) {
-                SFB_CUDA_TRY(cudaMemcpy2DAsync(Z, (size_t)ldz * 8, R, (size_t)ldr * 8, (size_t)qx * 8, qy,
-                                               cudaMemcpyDeviceToDevice, s));
-            } else {
-                return arg_error("banded preconditioner inside MO-PCG not built yet");
+            // Z = P_L^-1 R by column sweeps (R -> Z), then Z P_R^-1 by row
+            // sweeps in place with <Z,R> fused into the final pass.
+            SFB_TRY(launch_band_chol_cols(p->lband, p->bwL, qy, R, ldr, Z, ldz, qx, pcg, s));
+            ZrDot zr;
+            if (pcg || red) {
+                zr.R = R;
+                zr.ldr = ldr;
+                zr.partials = partials;
+                zr.counter = counter;
+                zr.pcg = pcg;
+                zr.dot_out = red ? &red->v[3] : nullptr;
             }
-            SFB_TRY(launch_band_chol_cols(p->lband, p->bwL, qy, Z, ldz, qx, s));
-            return launch_band_chol_rows(p->rband, p->bwR, qx, Z, ldz, qy, s);
+            return launch_band_chol_rows(p->rband, p->bwR, qx, Z, ldz, qy, zr, s);
         }
     }
     return arg_error("unknown preconditioner kind");
@@ -730,13 +735,13 @@ int sfb_pre_apply(const sfb_pre* p, const double* R, int ldr, double* Z, int ldz
     }
     double* parts = nullptr;
     RedSlots* red = nullptr;
-    SFB_TRY(tmp.get(&parts, (size_t)std::max(vector_grid_blocks(), gemm_grid_blocks(p->qy, p->qx)) * 8));
+    SFB_TRY(tmp.get(&parts, (size_t)std::max(std::max(vector_grid_blocks(), gemm_grid_blocks(p->qy, p->qx)),
+                                             band_chol_rows_blocks(p->qy)) * 8));
     SFB_TRY(tmp.get(&red, sizeof(RedSlots)));
     SFB_CUDA_TRY(cudaMemsetAsync(red, 0, sizeof(RedSlots), s));
     SFB_CUDA_TRY(cudaMemcpy2DAsync(Rb, (size_t)ld * 8, R, (size_t)ldr * 8, (size_t)p->qx * 8, p->qy,
                                    cudaMemcpyDeviceToDevice, s));
-    SFB_TRY(pre_apply_impl(p, Rb, ld, Zb, ld, T1, ldt1, T2, ld, parts,
-                           nullptr, p->kind == SFB_PRE_BANDED ? nullptr : red, s));
+    SFB_TRY(pre_apply_impl(p, Rb, ld, Zb, ld, T1, ldt1, T2, ld, parts, nullptr, red, s));
     SFB_CUDA_TRY(cudaMemcpy2DAsync(Z, (size_t)ldz * 8, Zb, (size_t)ld * 8, (size_t)p->qx * 8, p->qy,
                                    cudaMemcpyDeviceToDevice, s));
     return SFB_OK;
@@ -804,7 +809,7 @@ int sfb_pcg_create(const sfb_op* op, const sfb_pre* pre, sfb_pcg** out) {
         if (rc == SFB_OK) rc = dalloc(b, n);
     if (rc == SFB_OK) rc = dalloc(&s->T1, (size_t)s->qx * s->ldt1);
     const int nparts = 2 * std::max(std::max(vector_grid_blocks(), band_grid_blocks(s->qy, s->qx)),
-                                    gemm_grid_blocks(s->qy, s->qx));
+                                    std::max(gemm_grid_blocks(s->qy, s->qx), band_chol_rows_blocks(s->qy)));
     if (rc == SFB_OK) rc = dalloc(&s->partials, nparts);
     if (rc == SFB_OK) rc = talloc(&s->st, sizeof(PcgState));
     if (rc == SFB_OK) {
