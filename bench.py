@@ -1,0 +1,368 @@
+#!/usr/bin/env python
+"""MO-PCG DoF*iterations/s (fp64) on B200 — the BASELINE.json headline metric.
+
+Workload (default): BASELINE configs[2] ("cfg3"): -Lap u + u = f on the wave
+domain 0 <= x <= 1 + 0.3 sin(2 pi y), Dirichlet, MO-FEM P2 with N = 2048
+(q = 2047; q = 2048 is inadmissible for P2/Dirichlet), the
+5-term Sylvester operator and the single-term elliptic_xnormal preconditioner.
+One "step" is one MO-PCG solve with a fixed budget of --iters-per-step
+iterations (stop rule disabled so every step does the same work), run
+through the drop-in API on device-resident inputs.  DoF*it/s = q_y q_x *
+iterations / seconds.
+
+Printed (rank 0, one JSON line): value (device-resident), e2e (host numpy
+rhs in, host solution out, H2D/D2H inside the timed region), roofline of the
+dominant kernel (the FP64 DMMA GEMM of the preconditioner), cpu_baseline (the
+oracle port of the reference on the host cores, bounded sample), clocks.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import signal
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "MO-PCG DoF*iterations/s (fp64)"
+UNIT = "DoF*iterations/s"
+L2_BYTES = 126 * 1024 * 1024
+FP64_PEAK_FALLBACK = 35.48  # cuBLAS DGEMM 8192^3 measured on this pool (profiles/fp64_peaks_r01.log)
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["native", "reference"], default="native")
+    ap.add_argument("--N", type=int, default=2048, help="subintervals of the cfg3 workload")
+    ap.add_argument("--iters-per-step", type=int, default=50)
+    ap.add_argument("--precond-mode", default="inverse", choices=["inverse", "spectral", "banded"])
+    ap.add_argument("--cpu-iters", type=int, default=3, help="oracle iterations in the cpu_baseline sample")
+    ap.add_argument("--ref-iters-per-step", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ clocks --
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100", "-f", self.path], stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def stop(self):
+        out = {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        if self.proc is None:
+            return out
+        time.sleep(0.25)
+        self.proc.send_signal(signal.SIGTERM)
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        rows = []
+        try:
+            for line in open(self.path):
+                f = [c.strip() for c in line.split(",")]
+                if len(f) >= 8 and f[0].replace(".", "").isdigit():
+                    rows.append(f)
+        finally:
+            os.unlink(self.path)
+        if not rows:
+            return out
+        sm = [float(r[0]) for r in rows]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[4 + i].lower() == "active"})
+        out.update(sm_mhz=statistics.median(sm), sm_max_mhz=float(rows[0][1]), reasons=reasons,
+                   samples=len(rows), power_w_max=max(float(r[2]) for r in rows if r[2] not in ("", "[N/A]")))
+        return out
+
+
+# -------------------------------------------------------------- oracle leg --
+def oracle_cfg3(N: int):
+    """cfg3 in the oracle (the reference restated): dense factors, LU preconditioner."""
+    import oracle as orc
+    from paper_2109_01173_b200.workloads import sine_source
+    x, y = orc.direction_sets(orc.wave_domain(), 2, N, orc.DIRICHLET)
+    terms, rhs_of = orc.elliptic_terms(x, y, 1.0)
+    pre = orc.LUPrecond(*orc.precond_factors("elliptic_xnormal", x, y))
+    return orc, terms, rhs_of(sine_source(N, N, 3)), pre
+
+
+def cpu_sample(N: int, iters: int):
+    """Time `iters` oracle MO-PCG iterations on the step-0 system (setup excluded)."""
+    t0 = time.perf_counter()
+    orc, terms, rhs, pre = oracle_cfg3(N)
+    setup = time.perf_counter() - t0
+    r = orc.mo_pcg(terms, rhs, pre.inverse, ("residual", 1e-30), max_iter=iters)
+    q = rhs.shape[0] * rhs.shape[1]
+    return q * r["iterations"] / r["wall"], r["wall"], setup, r["iterations"]
+
+
+def cores() -> int:
+    for k in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS"):
+        if os.environ.get(k, "").isdigit():
+            return int(os.environ[k])
+    return os.cpu_count() or 1
+
+
+# ---------------------------------------------------------------- dist ------
+def dist_init(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def run_reference(args):
+    world, rank, _ = dist_init(args)
+    if rank != 0:
+        return
+    N, per = args.N, args.ref_iters_per_step
+    orc, terms, rhs, pre = oracle_cfg3(N)
+    q = rhs.shape[0] * rhs.shape[1]
+    for _ in range(args.warmup):
+        orc.mo_pcg(terms, rhs, pre.inverse, ("residual", 1e-30), max_iter=per)
+    t0 = time.perf_counter()
+    its = 0
+    for _ in range(args.steps):
+        its += orc.mo_pcg(terms, rhs, pre.inverse, ("residual", 1e-30), max_iter=per)["iterations"]
+    dt = time.perf_counter() - t0
+    value = q * its / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded 8-mode sine source, SURVEY App. A)",
+        "config": {"workload": "cfg3 (BASELINE configs[2]) wave domain P2 Dirichlet, N=%d q=%d" % (N, N - 1),
+                   "iterations_per_step": per, "parallelism": "host BLAS threads"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores(), "kind": "port",
+                         "sample": f"oracle restatement of sylfem mo_pcg (dense GEMM apply, LU preconditioner), "
+                                   f"{per} iterations per step on the cfg3 step-0 system, setup excluded"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_native(args):
+    import torch
+
+    world, rank, local = dist_init(args)
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+
+    import paper_2109_01173_b200 as pb
+    from paper_2109_01173_b200 import _native as nat
+    from paper_2109_01173_b200 import workloads as wl
+
+    t_setup = time.perf_counter()
+    w = wl.cfg3(N=args.N, mode=args.precond_mode)
+    op, pre = w.op, w.precond
+    qy, qx = op.shape
+    pre.native(op.shape)
+    setup_s = time.perf_counter() - t_setup
+    K_it = args.iters_per_step
+    stop = pb.relative_residual(1e-30)  # fixed iteration budget per step
+    rhs_d = torch.from_numpy(w.rhs).cuda()
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def step(rhs):
+        return pb.mo_pcg(op, rhs, precond=pre, stop=stop, max_iter=K_it)
+
+    for _ in range(max(args.warmup, 1)):
+        rep = step(rhs_d)
+    barrier()
+    clocks = Clocks(local)
+    clocks.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    its = 0
+    loop_ms = []
+    for _ in range(args.steps):
+        rep = step(rhs_d)
+        its += rep.iterations
+        loop_ms.append(rep.diagnostics["device"]["loop_ms"])
+    e1.record()
+    barrier()
+    clk = clocks.stop()
+    elapsed = e0.elapsed_time(e1) / 1e3
+    if dist is not None:
+        t = torch.tensor([elapsed], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed = float(t.item())
+    value = world * qy * qx * its / elapsed
+
+    # ---- e2e through the drop-in API with host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        barrier()
+        e0.record()
+        its_e = 0
+        for _ in range(args.steps):
+            rep_h = step(w.rhs)  # numpy in: H2D of rhs, D2H of solution + history
+            its_e += rep_h.iterations
+        e1.record()
+        barrier()
+        el = e0.elapsed_time(e1) / 1e3
+        if dist is not None:
+            t = torch.tensor([el], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            el = float(t.item())
+        e2e = {"value": world * qy * qx * its_e / el, "unit": UNIT,
+               "h2d_bytes_per_step": int(qy * qx * 8),
+               "d2h_bytes_per_step": int(qy * qx * 8 + (2 * K_it + 1) * 8)}
+
+    # ---- roofline of the dominant kernel: the DMMA GEMM (q x q x q) ----
+    L = nat.lib()
+    ldq = qy + (qy % 2)
+    A = torch.randn(qy, ldq, dtype=torch.float64, device="cuda")
+    B = torch.randn(qx, ldq, dtype=torch.float64, device="cuda")
+    C = torch.empty(qy, ldq, dtype=torch.float64, device="cuda")
+    s = torch.cuda.current_stream().cuda_stream
+
+    def gemm():
+        nat.check(L.sfb_dgemm_nt(A.data_ptr(), ldq, B.data_ptr(), ldq, qy, qx, qy, C.data_ptr(), ldq, s))
+
+    for _ in range(3):
+        gemm()
+    torch.cuda.synchronize()
+    reps = 20
+    g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    g0.record()
+    for _ in range(reps):
+        gemm()
+    g1.record()
+    torch.cuda.synchronize()
+    t_gemm = g0.elapsed_time(g1) / 1e3 / reps
+    gemm_tf = 2.0 * qy * qx * qy / t_gemm / 1e12
+    # cuBLAS DGEMM peak measured live on this box (the FP64 roofline denominator)
+    n8 = 8192
+    a8 = torch.randn(n8, n8, dtype=torch.float64, device="cuda")
+    b8 = torch.randn(n8, n8, dtype=torch.float64, device="cuda")
+    for _ in range(2):
+        a8 @ b8
+    torch.cuda.synchronize()
+    g0.record()
+    for _ in range(3):
+        a8 @ b8
+    g1.record()
+    torch.cuda.synchronize()
+    peak = 2.0 * n8 ** 3 / (g0.elapsed_time(g1) / 1e3 / 3) / 1e12
+    del a8, b8
+    cublas_same = None
+    try:
+        Ad = A[:, :qy].contiguous()
+        Bd = B[:, :qy].contiguous()
+        for _ in range(2):
+            Ad @ Bd.T
+        torch.cuda.synchronize()
+        g0.record()
+        for _ in range(5):
+            Ad @ Bd.T
+        g1.record()
+        torch.cuda.synchronize()
+        cublas_same = 2.0 * qy * qx * qy / (g0.elapsed_time(g1) / 1e3 / 5) / 1e12
+    except RuntimeError:
+        pass
+    n_gemm_per_iter = 2 if args.precond_mode == "inverse" else (4 if args.precond_mode == "spectral" else 0)
+    iter_ms = statistics.median(loop_ms) / K_it
+    share = (n_gemm_per_iter * t_gemm * 1e3) / iter_ms if n_gemm_per_iter else 0.0
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_dgemm_r01.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+        except (OSError, ValueError):
+            traffic = None
+
+    # ---- CPU baseline (rank 0, N = 1 only) ----
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, wall, setup, n_it = cpu_sample(args.N, args.cpu_iters)
+        cpu = {"value": v, "unit": UNIT, "cores": cores(), "kind": "port",
+               "sample": f"oracle restatement of sylfem mo_pcg (dense GEMM apply + LU preconditioner) on the "
+                         f"same cfg3 system, {n_it} iterations ({wall:.1f} s), setup {setup:.1f} s excluded"}
+
+    per_step_launches = 3 + (5 if not op.banded else 3 + n_gemm_per_iter) * K_it
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * elapsed / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded 8-mode sine source, SURVEY App. A)",
+            "config": {"workload": f"cfg3 (BASELINE configs[2]): wave domain, P2, Dirichlet, N={args.N}, "
+                                   f"q={qy}x{qx}, {len(op)}-term operator, MO-PCG with elliptic_xnormal "
+                                   f"preconditioner ({args.precond_mode})",
+                       "iterations_per_step": K_it, "preconditioner_mode": args.precond_mode,
+                       "l2": "inputs larger than L2 (8 grid buffers + 2 dense inverses = "
+                             f"{(8 * qy * qx + qy * qy + qx * qx) * 8 / 2**20:.0f} MiB > 126 MiB)",
+                       "parallelism": f"dp{world} replicas" if world > 1 else "single GPU",
+                       "setup_s": round(setup_s, 3)},
+            "roofline": {"bound": "tensor", "kernel": "dgemm_nt (DMMA.8x8x4 + TMA)",
+                         "achieved": gemm_tf, "peak": peak, "unit": "TFLOP/s", "frac": gemm_tf / peak,
+                         "traffic": traffic, "flops_per_launch": 2.0 * qy * qx * qy,
+                         "launch_ms": t_gemm * 1e3, "peak_source": "cuBLAS DGEMM 8192^3 measured in this run",
+                         "cublas_same_shape_tflops": cublas_same,
+                         "share_of_iteration": share, "iteration_ms": iter_ms},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": per_step_launches * args.steps,
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_native(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -155,6 +155,12 @@ int sfb_pcg_solve(sfb_pcg* s, const double* rhs_dev, int ldr,
                   sfb_pcg_result* res, void* stream);
 int sfb_pcg_destroy(sfb_pcg* s);
 
+/* ---- FP64 tensor-core GEMM (the kernel behind every spectral / inverse
+ *      application): C = A Bt^T, A (M x K) and Bt (N x K) row-major with even
+ *      leading dimensions and 16-byte aligned rows (TMA requirement). ------ */
+int sfb_dgemm_nt(const double* A_dev, int lda, const double* Bt_dev, int ldb,
+                 int M, int N, int K, double* C_dev, int ldc, void* stream);
+
 /* ---- reductions for the IMEX drivers (timestepping.py:89-91, 155, 210-215) */
 /* out4_host = { |A - B|_F (B may be NULL), max|A|, #non-finite(A), |A|_F }. */
 int sfb_diff_norm(const double* A_dev, int lda, const double* B_dev, int ldb,

@@ -30,7 +30,7 @@ EXPORTS = [
     "sfb_op_create", "sfb_op_create_dense", "sfb_op_apply", "sfb_op_residual", "sfb_op_destroy",
     "sfb_map_create", "sfb_map_apply", "sfb_map_apply_heat", "sfb_map_apply_dib", "sfb_map_destroy",
     "sfb_pre_create", "sfb_pre_create_banded", "sfb_pre_apply", "sfb_pre_transform", "sfb_pre_destroy",
-    "sfb_pcg_create", "sfb_pcg_solve", "sfb_pcg_destroy", "sfb_diff_norm",
+    "sfb_pcg_create", "sfb_pcg_solve", "sfb_pcg_destroy", "sfb_dgemm_nt", "sfb_diff_norm",
 ]
 
 
@@ -68,6 +68,7 @@ _SIGS = {
     "sfb_pcg_solve": (_I, [_P, _P, _I, _P, _I, _P, _I, _I, _D, _I, _DP, _DP, _P, _I,
                            C.POINTER(PcgResult), _P]),
     "sfb_pcg_destroy": (_I, [_P]),
+    "sfb_dgemm_nt": (_I, [_P, _I, _P, _I, _I, _I, _I, _P, _I, _P]),
     "sfb_diff_norm": (_I, [_P, _I, _P, _I, _I, _I, _DP, _P]),
 }
 

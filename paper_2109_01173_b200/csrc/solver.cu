@@ -937,6 +937,16 @@ int sfb_pcg_destroy(sfb_pcg* s) {
     return SFB_OK;
 }
 
+// ----------------------------------------------------------------- GEMM ---
+int sfb_dgemm_nt(const double* A, int lda, const double* Bt, int ldb, int M, int N, int K, double* C, int ldc,
+                 void* stream) {
+    GemmEpi e;
+    e.mode = EPI_STORE;
+    e.C = C;
+    e.ldc = ldc;
+    return launch_dgemm_nt(A, lda, Bt, ldb, M, N, K, e, (cudaStream_t)stream);
+}
+
 // ------------------------------------------------------------ reductions --
 int sfb_diff_norm(const double* A, int lda, const double* B, int ldb, int rows, int cols, double* out4,
                   void* stream) {
