@@ -35,170 +35,236 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-                 "r"(bytes)
-                 : "memory");
-}
-
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    asm volatile(
-        "{\n\t.reg .pred P1;\n"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-        "@!P1 bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
-                                            int c1) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
-        : "memory");
-}
-
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                  : "+d"(c0), "+d"(c1)
                  : "d"(a), "d"(b));
 }
 
-__global__ void __launch_bounds__(NTHREADS, 1)
-    dgemm_nt_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                    int M, int N, int K, GemmEpi ep) {
-    if (ep.pcg != nullptr && ep.pcg->status != SFB_PCG_RUNNING) return;  // uniform gate
+__device__ __forceinline__ double2 lds128(uint32_t addr) {
+    double2 v;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr));
+    return v;
+}
 
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t* sA = smem;
-    uint8_t* sB = smem + STAGES * TILE_BYTES;
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + 2 * STAGES * TILE_BYTES);
+__device__ __forceinline__ void mbar_init_u32(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
 
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
-    const int KT = (K + BK - 1) / BK;
+__device__ __forceinline__ void mbar_expect_tx_u32(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
 
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < STAGES; ++s) mbar_init(&full[s], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
-        // prologue: fill STAGES-1 slots
-        for (int kt = 0; kt < STAGES - 1 && kt < KT; ++kt) {
-            mbar_expect_tx(&full[kt], 2 * TILE_BYTES);
-            tma_load_2d(sA + kt * TILE_BYTES, &tmA, &full[kt], kt * BK, m0);
-            tma_load_2d(sB + kt * TILE_BYTES, &tmB, &full[kt], kt * BK, n0);
-        }
+__device__ __forceinline__ void mbar_wait_u32(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n}" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_load_u32(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1)
+        : "memory");
+}
+
+struct Sched {
+    int tiles_n;         // tiles along N
+    int KT;              // k-tiles per output tile
+    long long U;         // total (tile, k-tile) iterations
+    int G;               // CTAs
+    __device__ long long start(int c) const { return (long long)c * U / G; }
+    __device__ int owner(long long i) const {  // CTA whose range holds linear iteration i
+        int c = (int)((i * G) / U);
+        while (c + 1 < G && start(c + 1) <= i) ++c;
+        while (c > 0 && start(c) > i) --c;
+        return c;
     }
-    __syncthreads();
+};
 
-    double acc[8][4][2];
-    #pragma unroll
-    for (int i = 0; i < 8; ++i)
-        #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-
-    const int wm = warp >> 2, wn = warp & 3;  // consumer warp grid 2 x 4 (64 x 32 each)
-    const int g = lane >> 2, t = lane & 3;
-
-    // One thread issues TMA for k-tile kt+STAGES-1 into the slot consumed at
-    // kt-1; the block barrier at the top of each step guarantees every warp
-    // has finished reading that slot (WAR), the mbarrier signals the bytes.
-    for (int kt = 0; kt < KT; ++kt) {
-        const int s = kt % STAGES;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            const int kn = kt + STAGES - 1;
-            if (kn < KT) {
-                const int sn = kn % STAGES;
-                mbar_expect_tx(&full[sn], 2 * TILE_BYTES);
-                tma_load_2d(sA + sn * TILE_BYTES, &tmA, &full[sn], kn * BK, m0);
-                tma_load_2d(sB + sn * TILE_BYTES, &tmB, &full[sn], kn * BK, n0);
-            }
-        }
-        mbar_wait(&full[s], (kt / STAGES) & 1);
-        const uint8_t* a_base = sA + s * TILE_BYTES + (wm * 64 + g) * 128;
-        const uint8_t* b_base = sB + s * TILE_BYTES + (wn * 32 + g) * 128;
-        #pragma unroll
-        for (int half = 0; half < 2; ++half) {
-            const int chunk = ((2 * t + half) ^ g) << 4;  // SWIZZLE_128B: chunk ^= row & 7 (= g)
-            double2 a[8], b[4];
-            #pragma unroll
-            for (int i = 0; i < 8; ++i) a[i] = *reinterpret_cast<const double2*>(a_base + i * 8 * 128 + chunk);
-            #pragma unroll
-            for (int j = 0; j < 4; ++j) b[j] = *reinterpret_cast<const double2*>(b_base + j * 8 * 128 + chunk);
-            #pragma unroll
-            for (int i = 0; i < 8; ++i)
-                #pragma unroll
-                for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i].x, b[j].x);
-            #pragma unroll
-            for (int i = 0; i < 8; ++i)
-                #pragma unroll
-                for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i].y, b[j].y);
-        }
-    }
-
-    // ---------------- epilogue (registers -> global) ----------------
+// Epilogue of one finished 128x128 tile (registers -> global).
+__device__ __forceinline__ double tile_epilogue(double (&acc)[8][4][2], const GemmEpi& ep, int M, int N, int m0,
+                                                int n0, int wm, int wn, int g, int t) {
     double dot = 0.0;
-    {
+    #pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int m = m0 + wm * 64 + i * 8 + g;
+        if (m >= M) continue;
         #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const int m = m0 + wm * 64 + i * 8 + g;
-            if (m >= M) continue;
-            #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const int n = n0 + wn * 32 + j * 8 + 2 * t;
-                double v0 = acc[i][j][0], v1 = acc[i][j][1];
-                const bool ok0 = n < N, ok1 = n + 1 < N;
-                switch (ep.mode) {
-                    case EPI_STORE_T:
-                        if (ok0) ep.C[(size_t)n * ep.ldc + m] = v0;
-                        if (ok1) ep.C[(size_t)(n + 1) * ep.ldc + m] = v1;
-                        break;
-                    case EPI_ACCUM:
-                        if (ok0) ep.C[(size_t)m * ep.ldc + n] += v0;
-                        if (ok1) ep.C[(size_t)m * ep.ldc + n + 1] += v1;
-                        break;
-                    default: {
-                        if (ep.mode == EPI_HADAMARD_SUM) {
-                            if (ok0) v0 *= 1.0 / (ep.sr[m] + ep.sc[n]);
-                            if (ok1) v1 *= 1.0 / (ep.sr[m] + ep.sc[n + 1]);
-                        } else if (ep.mode == EPI_HADAMARD_PROD) {
-                            if (ok0) v0 *= ep.sr[m] * ep.sc[n];
-                            if (ok1) v1 *= ep.sr[m] * ep.sc[n + 1];
-                        }
-                        double* c = ep.C + (size_t)m * ep.ldc + n;
-                        if (ok1) {
-                            *reinterpret_cast<double2*>(c) = make_double2(v0, v1);
-                        } else if (ok0) {
-                            c[0] = v0;
-                        }
-                        if (ep.mode == EPI_STORE_DOT) {
-                            const double* d = ep.D + (size_t)m * ep.ldd + n;
-                            if (ok0) dot = fma(v0, d[0], dot);
-                            if (ok1) dot = fma(v1, d[1], dot);
-                        }
+        for (int j = 0; j < 4; ++j) {
+            const int n = n0 + wn * 32 + j * 8 + 2 * t;
+            double v0 = acc[i][j][0], v1 = acc[i][j][1];
+            const bool ok0 = n < N, ok1 = n + 1 < N;
+            switch (ep.mode) {
+                case EPI_STORE_T:
+                    if (ok0) ep.C[(size_t)n * ep.ldc + m] = v0;
+                    if (ok1) ep.C[(size_t)(n + 1) * ep.ldc + m] = v1;
+                    break;
+                case EPI_ACCUM:
+                    if (ok0) ep.C[(size_t)m * ep.ldc + n] += v0;
+                    if (ok1) ep.C[(size_t)m * ep.ldc + n + 1] += v1;
+                    break;
+                default: {
+                    if (ep.mode == EPI_HADAMARD_SUM) {
+                        if (ok0) v0 *= 1.0 / (ep.sr[m] + ep.sc[n]);
+                        if (ok1) v1 *= 1.0 / (ep.sr[m] + ep.sc[n + 1]);
+                    } else if (ep.mode == EPI_HADAMARD_PROD) {
+                        if (ok0) v0 *= ep.sr[m] * ep.sc[n];
+                        if (ok1) v1 *= ep.sr[m] * ep.sc[n + 1];
+                    }
+                    double* c = ep.C + (size_t)m * ep.ldc + n;
+                    if (ok1) {
+                        *reinterpret_cast<double2*>(c) = make_double2(v0, v1);
+                    } else if (ok0) {
+                        c[0] = v0;
+                    }
+                    if (ep.mode == EPI_STORE_DOT) {
+                        const double* d = ep.D + (size_t)m * ep.ldd + n;
+                        if (ok0) dot = fma(v0, d[0], dot);
+                        if (ok1) dot = fma(v1, d[1], dot);
                     }
                 }
             }
         }
     }
+    return dot;
+}
+
+// Persistent stream-K schedule: CTA c owns the linear (tile, k-tile)
+// iterations [c U / G, (c+1) U / G).  A tile split across CTAs is finished by
+// the CTA holding its k = 0 piece (the last thing that CTA computes); the
+// other pieces are the first things their CTAs compute, are parked in `ws`
+// and counted in `flags[tile]`, so the finishing CTA never waits long.  With
+// ws == nullptr every CTA owns whole tiles (grid = tile count).
+__global__ void __launch_bounds__(NTHREADS, 1)
+    dgemm_nt_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
+                    int K, GemmEpi ep, Sched sc) {
+    if (ep.pcg != nullptr && ep.pcg->status != SFB_PCG_RUNNING) return;  // uniform gate
+
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
+    const uint32_t sA = base, sB = base + STAGES * TILE_BYTES, full = base + 2 * STAGES * TILE_BYTES;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int wm = warp >> 2, wn = warp & 3;  // 2 x 4 warps, 64 x 32 each
+    const int g = lane >> 2, t = lane & 3;
+    const int KT = sc.KT;
+    const long long beg = sc.start(blockIdx.x), fin = sc.start(blockIdx.x + 1);
+    const int n_it = (int)(fin - beg);
+
+    auto issue = [&](int it) {  // TMA for local iteration `it` into its ring slot
+        const long long li = beg + it;
+        const int tile = (int)(li / KT), kt = (int)(li - (long long)tile * KT);
+        const int m0 = (tile / sc.tiles_n) * BM, n0 = (tile % sc.tiles_n) * BN;
+        const int sl = it % STAGES;
+        mbar_expect_tx_u32(full + 8 * sl, 2 * TILE_BYTES);
+        tma_load_u32(sA + sl * TILE_BYTES, &tmA, full + 8 * sl, kt * BK, m0);
+        tma_load_u32(sB + sl * TILE_BYTES, &tmB, full + 8 * sl, kt * BK, n0);
+    };
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) mbar_init_u32(full + 8 * s, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+        for (int it = 0; it < STAGES - 1 && it < n_it; ++it) issue(it);
+    }
+    __syncthreads();
+
+    double dot = 0.0;
+    double acc[8][4][2];
+    int it = 0;
+    while (it < n_it) {
+        const long long li0 = beg + it;
+        const int tile = (int)(li0 / KT), k0 = (int)(li0 - (long long)tile * KT);
+        const int seg_end = (int)min((long long)n_it, (long long)it + (KT - k0));
+        const int kl = k0 + (seg_end - it) - 1;  // last k-tile of this piece
+        #pragma unroll
+        for (int i = 0; i < 8; ++i)
+            #pragma unroll
+            for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+        for (; it < seg_end; ++it) {
+            const int s = it % STAGES;
+            __syncthreads();  // every warp is done with the slot refilled below (WAR)
+            if (threadIdx.x == 0 && it + STAGES - 1 < n_it) issue(it + STAGES - 1);
+            mbar_wait_u32(full + 8 * s, (it / STAGES) & 1);
+            const uint32_t a_base = sA + s * TILE_BYTES + (wm * 64 + g) * 128;
+            const uint32_t b_base = sB + s * TILE_BYTES + (wn * 32 + g) * 128;
+            #pragma unroll
+            for (int half = 0; half < 2; ++half) {
+                const uint32_t ch = ((2 * t + half) ^ g) << 4;  // SWIZZLE_128B: chunk ^= row & 7 (= g)
+                double2 a[8], b[4];
+                #pragma unroll
+                for (int i = 0; i < 8; ++i) a[i] = lds128(a_base + i * 1024 + ch);
+                #pragma unroll
+                for (int j = 0; j < 4; ++j) b[j] = lds128(b_base + j * 1024 + ch);
+                #pragma unroll
+                for (int i = 0; i < 8; ++i)
+                    #pragma unroll
+                    for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i].x, b[j].x);
+                #pragma unroll
+                for (int i = 0; i < 8; ++i)
+                    #pragma unroll
+                    for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i].y, b[j].y);
+            }
+        }
+
+        const int m0 = (tile / sc.tiles_n) * BM, n0 = (tile % sc.tiles_n) * BN;
+        if (k0 != 0) {
+            // continuation piece: park the partial tile and count it
+            double* w = ep.sk_ws + (size_t)blockIdx.x * (BM * BN);
+            #pragma unroll
+            for (int i = 0; i < 8; ++i)
+                #pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int e = (i * 4 + j) * 2;
+                    __stcg(reinterpret_cast<double2*>(w + (size_t)e * NTHREADS) + threadIdx.x,
+                           make_double2(acc[i][j][0], acc[i][j][1]));
+                }
+            __threadfence();
+            __syncthreads();
+            if (threadIdx.x == 0) atomicAdd(ep.sk_flags + tile, 1u);
+        } else {
+            if (kl != KT - 1) {
+                // first piece of a split tile: fold in the continuation pieces
+                const int last = sc.owner((long long)(tile + 1) * KT - 1);
+                const unsigned expect = (unsigned)(last - (int)blockIdx.x);
+                if (threadIdx.x == 0) {
+                    volatile unsigned* f = ep.sk_flags + tile;
+                    while (*f < expect) __nanosleep(64);
+                    *f = 0;
+                }
+                __syncthreads();
+                __threadfence();
+                for (int c = (int)blockIdx.x + 1; c <= last; ++c) {
+                    const double* w = ep.sk_ws + (size_t)c * (BM * BN);
+                    #pragma unroll
+                    for (int i = 0; i < 8; ++i)
+                        #pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            const int e = (i * 4 + j) * 2;
+                            const double2 v = __ldcg(reinterpret_cast<const double2*>(w + (size_t)e * NTHREADS) +
+                                                     threadIdx.x);
+                            acc[i][j][0] += v.x;
+                            acc[i][j][1] += v.y;
+                        }
+                }
+            }
+            dot += tile_epilogue(acc, ep, M, N, m0, n0, wm, wn, g, t);
+        }
+    }
+
     if (ep.mode == EPI_STORE_DOT) {
         __shared__ double sh[NTHREADS / 32];
         const double part = block_sum<NTHREADS>(dot, sh);
-        const unsigned nblk = gridDim.x * gridDim.y;
-        if (threadIdx.x == 0) ep.partials[blockIdx.y * gridDim.x + blockIdx.x] = part;
+        const unsigned nblk = gridDim.x;
+        if (threadIdx.x == 0) ep.partials[blockIdx.x] = part;
         if (arrive_last(ep.counter, nblk)) {
             const double tot = sum_partials<NTHREADS>(ep.partials, nblk, 1, sh);
             if (threadIdx.x == 0) {
@@ -248,6 +314,28 @@ int make_map(CUtensorMap* map, const double* ptr, int rows, int cols, int ld) {
 
 int gemm_smem_bytes() { return SMEM_BYTES; }
 
+int num_sms() {
+    static int n = 0;
+    if (n == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = kNumSMs;
+    }
+    return n;
+}
+
+// Grid of the stream-K schedule (at most one CTA per SM, at least ~8 k-tiles
+// of work per CTA); tile-aligned data-parallel grid when that already fills
+// the machine evenly or no workspace is available.
+int gemm_grid_for(int M, int N, int K, bool have_ws) {
+    const int tiles = ((N + BN - 1) / BN) * ((M + BM - 1) / BM);
+    const int KT = (K + BK - 1) / BK;
+    const int sms = num_sms();
+    if (!have_ws || tiles % sms == 0) return tiles;
+    const long long U = (long long)tiles * KT;
+    return (int)std::max(1LL, std::min<long long>(sms, U / 8));
+}
+
 // C[M x N] = A[M x K] * Bt[N x K]^T, both row-major K-contiguous.
 int launch_dgemm_nt(const double* A, int lda, const double* Bt, int ldb, int M, int N, int K,
                     const GemmEpi& ep, cudaStream_t stream) {
@@ -261,12 +349,43 @@ int launch_dgemm_nt(const double* A, int lda, const double* Bt, int ldb, int M, 
     CUtensorMap ma, mb;
     SFB_TRY(make_map(&ma, A, M, K, lda));
     SFB_TRY(make_map(&mb, Bt, N, K, ldb));
-    dim3 grid((N + BN - 1) / BN, (M + BM - 1) / BM);
-    dgemm_nt_kernel<<<grid, NTHREADS, SMEM_BYTES, stream>>>(ma, mb, M, N, K, ep);
-    SFB_CHECK_LAUNCH();
+    Sched sc;
+    sc.tiles_n = (N + BN - 1) / BN;
+    sc.KT = (K + BK - 1) / BK;
+    const int tiles = sc.tiles_n * ((M + BM - 1) / BM);
+    sc.U = (long long)tiles * sc.KT;
+    const bool have_ws = ep.sk_ws != nullptr && ep.sk_flags != nullptr;
+    sc.G = gemm_grid_for(M, N, K, have_ws);
+    if (sc.G != tiles) {
+        // split tiles: all CTAs must be co-resident (finishing CTAs wait on
+        // continuation pieces), which a cooperative launch guarantees
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(sc.G);
+        cfg.blockDim = dim3(NTHREADS);
+        cfg.dynamicSmemBytes = SMEM_BYTES;
+        cfg.stream = stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeCooperative;
+        attr[0].val.cooperative = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        if (cudaLaunchKernelEx(&cfg, dgemm_nt_kernel, ma, mb, M, N, K, ep, sc) != cudaSuccess) {
+            // e.g. inside a capture that rejects the attribute: a one-CTA-per-SM
+            // persistent grid is co-resident on an otherwise idle device
+            cudaGetLastError();
+            cfg.numAttrs = 0;
+            SFB_CUDA_TRY(cudaLaunchKernelEx(&cfg, dgemm_nt_kernel, ma, mb, M, N, K, ep, sc));
+        }
+    } else {
+        dgemm_nt_kernel<<<sc.G, NTHREADS, SMEM_BYTES, stream>>>(ma, mb, M, N, K, ep, sc);
+        SFB_CHECK_LAUNCH();
+    }
     return SFB_OK;
 }
 
 int gemm_grid_blocks(int M, int N) { return ((N + BN - 1) / BN) * ((M + BM - 1) / BM); }
+
+size_t gemm_workspace_doubles() { return (size_t)num_sms() * BM * BN; }
+int gemm_max_tiles() { return 65536; }
 
 }  // namespace sfb

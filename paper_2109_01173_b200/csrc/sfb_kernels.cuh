@@ -27,12 +27,16 @@ struct GemmEpi {
     unsigned* counter = nullptr;  // last-block counter (EPI_STORE_DOT)
     PcgState* pcg = nullptr;      // status gate; receives rz_next
     double* dot_out = nullptr;    // receives the dot total when non-null
+    double* sk_ws = nullptr;      // stream-K partial tiles (gemm_workspace_doubles())
+    unsigned* sk_flags = nullptr; // stream-K per-tile counters (gemm_max_tiles(), zeroed once)
 };
 
 int launch_dgemm_nt(const double* A, int lda, const double* Bt, int ldb, int M, int N, int K,
                     const GemmEpi& ep, cudaStream_t stream);
 int gemm_grid_blocks(int M, int N);
 int gemm_smem_bytes();
+size_t gemm_workspace_doubles();
+int gemm_max_tiles();
 
 // ----------------------------------------------------------- banded -------
 enum BandLoad { LD_PLAIN = 0, LD_PCG = 1, LD_HEAT = 2, LD_DIB = 3 };

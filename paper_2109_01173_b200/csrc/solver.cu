@@ -9,6 +9,7 @@
 // solve is then a single graph launch and one final synchronisation.
 #include <cuda.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -74,6 +75,30 @@ struct ScopedFree {
 inline int pad_ld(int cols) { return round_up(cols < 1 ? 1 : cols, 32); }
 
 }  // namespace
+
+// Stream-K workspace of the DMMA GEMM (partial tiles + per-tile counters).
+struct GemmWs {
+    double* ws = nullptr;
+    unsigned* flags = nullptr;
+};
+
+// Temporary stream-K workspace from the stream-ordered pool.
+template <class Pool>
+int temp_ws(Pool& tmp, GemmWs& w, cudaStream_t s) {
+    SFB_TRY(tmp.get(&w.ws, gemm_workspace_doubles() * sizeof(double)));
+    SFB_TRY(tmp.get(&w.flags, (size_t)gemm_max_tiles() * sizeof(unsigned)));
+    SFB_CUDA_TRY(cudaMemsetAsync(w.flags, 0, (size_t)gemm_max_tiles() * sizeof(unsigned), s));
+    return SFB_OK;
+}
+
+inline GemmEpi with_ws(GemmEpi e, const GemmWs* w) {
+    if (w != nullptr) {
+        e.sk_ws = w->ws;
+        e.sk_flags = w->flags;
+    }
+    return e;
+}
+
 }  // namespace sfb
 
 using namespace sfb;
@@ -117,7 +142,7 @@ namespace {
 // W = op(U) on device buffers (U must have an even ld and 16B alignment for
 // the dense path).  T1 is qx x qy scratch (ld ldt) for the dense path.
 int op_apply_impl(const sfb_op* op, const double* U, int ldu, double* W, int ldw, double* T1, int ldt,
-                  cudaStream_t s) {
+                  const GemmWs* gw, cudaStream_t s) {
     if (!op->dense) {
         BandArgs a;
         a.out_rows = a.in_rows = op->qy;
@@ -142,13 +167,13 @@ int op_apply_impl(const sfb_op* op, const double* U, int ldu, double* W, int ldw
         e1.C = T1;
         e1.ldc = ldt;
         SFB_TRY(launch_dgemm_nt(U, ldu, op->Ht + (size_t)t * op->qx * op->ldH, op->ldH, op->qy, op->qx, op->qx,
-                                e1, s));
+                                with_ws(e1, gw), s));
         GemmEpi e2;
         e2.mode = t == 0 ? EPI_STORE : EPI_ACCUM;  // W (+)= G_t (U H_t)
         e2.C = W;
         e2.ldc = ldw;
         SFB_TRY(launch_dgemm_nt(op->G + (size_t)t * op->qy * op->ldG, op->ldG, T1, ldt, op->qy, op->qx, op->qy,
-                                e2, s));
+                                with_ws(e2, gw), s));
     }
     return SFB_OK;
 }
@@ -158,7 +183,8 @@ int op_apply_impl(const sfb_op* op, const double* U, int ldu, double* W, int ldw
 // kernels are gated on its status and <Z,R> lands in pcg->rz_next; otherwise
 // it lands in red->v[3] when red is set.
 int pre_apply_impl(const sfb_pre* p, const double* R, int ldr, double* Z, int ldz, double* T1, int ldt1,
-                   double* T2, int ldt2, double* partials, PcgState* pcg, RedSlots* red, cudaStream_t s) {
+                   double* T2, int ldt2, double* partials, PcgState* pcg, RedSlots* red, const GemmWs* gw,
+                   cudaStream_t s) {
     const int qy = p->qy, qx = p->qx;
     unsigned* counter = pcg ? &pcg->counter[4] : (red ? &red->counter[2] : nullptr);
     GemmEpi last;
@@ -181,9 +207,9 @@ int pre_apply_impl(const sfb_pre* p, const double* R, int ldr, double* Z, int ld
             e1.C = T1;
             e1.ldc = ldt1;
             e1.pcg = pcg;
-            SFB_TRY(launch_dgemm_nt(R, ldr, p->B1, p->ldB, qy, qx, qx, e1, s));
+            SFB_TRY(launch_dgemm_nt(R, ldr, p->B1, p->ldB, qy, qx, qx, with_ws(e1, gw), s));
             // Z = P_L^-1 (R P_R^-1)
-            return launch_dgemm_nt(p->A1, p->ldA, T1, ldt1, qy, qx, qy, last, s);
+            return launch_dgemm_nt(p->A1, p->ldA, T1, ldt1, qy, qx, qy, with_ws(last, gw), s);
         }
         case SFB_PRE_SPECTRAL_PROD:
         case SFB_PRE_SPECTRAL_SUM: {
@@ -192,7 +218,7 @@ int pre_apply_impl(const sfb_pre* p, const double* R, int ldr, double* Z, int ld
             e1.C = T1;
             e1.ldc = ldt1;
             e1.pcg = pcg;
-            SFB_TRY(launch_dgemm_nt(R, ldr, p->B1t, p->ldB, qy, qx, qx, e1, s));
+            SFB_TRY(launch_dgemm_nt(R, ldr, p->B1t, p->ldB, qy, qx, qx, with_ws(e1, gw), s));
             GemmEpi e2;  // T2 = (V_L^T R V_R) o K
             e2.mode = p->kind == SFB_PRE_SPECTRAL_SUM ? EPI_HADAMARD_SUM : EPI_HADAMARD_PROD;
             e2.C = T2;
@@ -200,15 +226,15 @@ int pre_apply_impl(const sfb_pre* p, const double* R, int ldr, double* Z, int ld
             e2.sr = p->sl;
             e2.sc = p->sr;
             e2.pcg = pcg;
-            SFB_TRY(launch_dgemm_nt(p->A1t, p->ldA, T1, ldt1, qy, qx, qy, e2, s));
+            SFB_TRY(launch_dgemm_nt(p->A1t, p->ldA, T1, ldt1, qy, qx, qy, with_ws(e2, gw), s));
             GemmEpi e3;  // T1 = (T2 V_R^T)^T
             e3.mode = EPI_STORE_T;
             e3.C = T1;
             e3.ldc = ldt1;
             e3.pcg = pcg;
-            SFB_TRY(launch_dgemm_nt(T2, ldt2, p->B1, p->ldB, qy, qx, qx, e3, s));
+            SFB_TRY(launch_dgemm_nt(T2, ldt2, p->B1, p->ldB, qy, qx, qx, with_ws(e3, gw), s));
             // Z = V_L (T2 V_R^T)
-            return launch_dgemm_nt(p->A1, p->ldA, T1, ldt1, qy, qx, qy, last, s);
+            return launch_dgemm_nt(p->A1, p->ldA, T1, ldt1, qy, qx, qy, with_ws(last, gw), s);
         }
         case SFB_PRE_BANDED: {
             // Z = P_L^-1 R by column sweeps (R -> Z), then Z P_R^-1 by row
@@ -240,6 +266,7 @@ struct sfb_pcg {
     double *U = nullptr, *R = nullptr, *Z = nullptr, *Q0 = nullptr, *Q1 = nullptr, *W = nullptr, *B = nullptr;
     double *T1 = nullptr, *T2 = nullptr;
     double* partials = nullptr;
+    GemmWs gw;
     PcgState* st = nullptr;
     double* hist = nullptr;
     double* incs = nullptr;
@@ -293,14 +320,14 @@ int pcg_enqueue_iteration(sfb_pcg* s, double* iterates) {
             e1.ldc = s->ldt1;
             e1.pcg = s->st;
             SFB_TRY(launch_dgemm_nt(s->Q0, s->ld, op->Ht + (size_t)t * op->qx * op->ldH, op->ldH, s->qy, s->qx,
-                                    s->qx, e1, st));
+                                    s->qx, with_ws(e1, &s->gw), st));
             GemmEpi e2;
             e2.mode = t == 0 ? EPI_STORE : EPI_ACCUM;
             e2.C = s->W;
             e2.ldc = s->ld;
             e2.pcg = s->st;
             SFB_TRY(launch_dgemm_nt(op->G + (size_t)t * op->qy * op->ldG, op->ldG, s->T1, s->ldt1, s->qy, s->qx,
-                                    s->qy, e2, st));
+                                    s->qy, with_ws(e2, &s->gw), st));
         }
         SFB_TRY(launch_pcg_dots(s->W, s->Q0, s->Q0, s->ld, s->qy, s->qx, s->partials, s->st, st));
         SFB_TRY(launch_pcg_update(s->U, s->R, s->W, s->Q0, s->Q0, s->ld, s->qy, s->qx, s->partials, s->st,
@@ -308,7 +335,7 @@ int pcg_enqueue_iteration(sfb_pcg* s, double* iterates) {
     }
     if (iterates != nullptr) SFB_TRY(launch_pcg_record(s->U, s->ld, s->qy, s->qx, iterates, s->st, st));
     return pre_apply_impl(s->pre, s->R, s->ld, s->Z, s->ld, s->T1, s->ldt1, s->T2, s->ldt2, s->partials, s->st,
-                          nullptr, st);
+                          nullptr, &s->gw, st);
 }
 
 void drop_graph(sfb_pcg* s) {
@@ -324,7 +351,11 @@ int build_graph(sfb_pcg* s, double* iterates) {
     cudaGraph_t g = nullptr;
     SFB_CUDA_TRY(cudaGraphCreate(&g, 0));
     cudaGraphConditionalHandle h;
-    bool ok = cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault) == cudaSuccess;
+    // SYLFEM_B200_GRAPH=chunked forces the host-driven fallback (ncu cannot
+    // profile kernel nodes of graphs that contain conditional nodes).
+    const char* mode = std::getenv("SYLFEM_B200_GRAPH");
+    const bool want_cond = !(mode && std::strcmp(mode, "chunked") == 0);
+    bool ok = want_cond && cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault) == cudaSuccess;
     if (ok) {
         alignas(cudaGraphNodeParams) unsigned char raw[sizeof(cudaGraphNodeParams)];
         std::memset(raw, 0, sizeof(raw));
@@ -468,7 +499,7 @@ int sfb_op_create_dense(int qy, int qx, int nterms, const double* G, const doubl
 int sfb_op_apply(const sfb_op* op, const double* U, int ldu, double* W, int ldw, void* stream) {
     if (!op) return arg_error("null operator");
     cudaStream_t s = (cudaStream_t)stream;
-    if (!op->dense) return op_apply_impl(op, U, ldu, W, ldw, nullptr, 0, s);
+    if (!op->dense) return op_apply_impl(op, U, ldu, W, ldw, nullptr, 0, nullptr, s);
     ScopedFree tmp(s);
     const int ld = pad_ld(op->qx), ldt = pad_ld(op->qy);
     double *Ub, *Wb, *T1;
@@ -477,7 +508,9 @@ int sfb_op_apply(const sfb_op* op, const double* U, int ldu, double* W, int ldw,
     SFB_TRY(tmp.get(&T1, (size_t)op->qx * ldt * 8));
     SFB_CUDA_TRY(cudaMemcpy2DAsync(Ub, (size_t)ld * 8, U, (size_t)ldu * 8, (size_t)op->qx * 8, op->qy,
                                    cudaMemcpyDeviceToDevice, s));
-    SFB_TRY(op_apply_impl(op, Ub, ld, Wb, ld, T1, ldt, s));
+    GemmWs gw;
+    SFB_TRY(temp_ws(tmp, gw, s));
+    SFB_TRY(op_apply_impl(op, Ub, ld, Wb, ld, T1, ldt, &gw, s));
     SFB_CUDA_TRY(cudaMemcpy2DAsync(W, (size_t)ldw * 8, Wb, (size_t)ld * 8, (size_t)op->qx * 8, op->qy,
                                    cudaMemcpyDeviceToDevice, s));
     return SFB_OK;
@@ -741,7 +774,9 @@ int sfb_pre_apply(const sfb_pre* p, const double* R, int ldr, double* Z, int ldz
     SFB_CUDA_TRY(cudaMemsetAsync(red, 0, sizeof(RedSlots), s));
     SFB_CUDA_TRY(cudaMemcpy2DAsync(Rb, (size_t)ld * 8, R, (size_t)ldr * 8, (size_t)p->qx * 8, p->qy,
                                    cudaMemcpyDeviceToDevice, s));
-    SFB_TRY(pre_apply_impl(p, Rb, ld, Zb, ld, T1, ldt1, T2, ld, parts, nullptr, red, s));
+    GemmWs gw;
+    if (T1 != nullptr) SFB_TRY(temp_ws(tmp, gw, s));
+    SFB_TRY(pre_apply_impl(p, Rb, ld, Zb, ld, T1, ldt1, T2, ld, parts, nullptr, red, T1 ? &gw : nullptr, s));
     SFB_CUDA_TRY(cudaMemcpy2DAsync(Z, (size_t)ldz * 8, Zb, (size_t)ld * 8, (size_t)p->qx * 8, p->qy,
                                    cudaMemcpyDeviceToDevice, s));
     return SFB_OK;
@@ -764,12 +799,14 @@ int sfb_pre_transform(const sfb_pre* p, const double* X, int ldx, double* Y, int
     e1.mode = EPI_STORE_T;
     e1.C = T1;
     e1.ldc = ldt1;
-    SFB_TRY(launch_dgemm_nt(Xb, ld, p->B1t, p->ldB, p->qy, p->qx, p->qx, e1, s));
+    GemmWs gw;
+    SFB_TRY(temp_ws(tmp, gw, s));
+    SFB_TRY(launch_dgemm_nt(Xb, ld, p->B1t, p->ldB, p->qy, p->qx, p->qx, with_ws(e1, &gw), s));
     GemmEpi e2;  // Y = V_L^T X V_R
     e2.mode = EPI_STORE;
     e2.C = Yb;
     e2.ldc = ld;
-    SFB_TRY(launch_dgemm_nt(p->A1t, p->ldA, T1, ldt1, p->qy, p->qx, p->qy, e2, s));
+    SFB_TRY(launch_dgemm_nt(p->A1t, p->ldA, T1, ldt1, p->qy, p->qx, p->qy, with_ws(e2, &gw), s));
     SFB_CUDA_TRY(cudaMemcpy2DAsync(Y, (size_t)ldy * 8, Yb, (size_t)ld * 8, (size_t)p->qx * 8, p->qy,
                                    cudaMemcpyDeviceToDevice, s));
     return SFB_OK;
@@ -812,6 +849,10 @@ int sfb_pcg_create(const sfb_op* op, const sfb_pre* pre, sfb_pcg** out) {
                                     std::max(gemm_grid_blocks(s->qy, s->qx), band_chol_rows_blocks(s->qy)));
     if (rc == SFB_OK) rc = dalloc(&s->partials, nparts);
     if (rc == SFB_OK) rc = talloc(&s->st, sizeof(PcgState));
+    if (rc == SFB_OK) rc = dalloc(&s->gw.ws, gemm_workspace_doubles());
+    if (rc == SFB_OK) rc = talloc(&s->gw.flags, (size_t)gemm_max_tiles() * sizeof(unsigned));
+    if (rc == SFB_OK && cudaMemset(s->gw.flags, 0, (size_t)gemm_max_tiles() * sizeof(unsigned)) != cudaSuccess)
+        rc = SFB_ERR_CUDA;
     if (rc == SFB_OK) {
         for (double** b : bufs) cudaMemset(*b, 0, n * 8);
         cudaMemset(s->T1, 0, (size_t)s->qx * s->ldt1 * 8);
@@ -870,7 +911,7 @@ int sfb_pcg_solve(sfb_pcg* s, const double* rhs, int ldr, const double* u0, int 
     if (u0 != nullptr) {
         SFB_CUDA_TRY(cudaMemcpy2DAsync(s->U, (size_t)ld * 8, u0, (size_t)ldu0 * 8, (size_t)qx * 8, qy,
                                        cudaMemcpyDeviceToDevice, st));
-        SFB_TRY(op_apply_impl(s->op, s->U, ld, s->W, ld, s->T1, s->ldt1, st));
+        SFB_TRY(op_apply_impl(s->op, s->U, ld, s->W, ld, s->T1, s->ldt1, &s->gw, st));
         SFB_TRY(launch_pcg_init_warm(s->B, ld, s->W, s->R, ld, qy, qx, s->partials, s->st, s->hist, st));
     } else {
         SFB_TRY(launch_pcg_init_plain(s->B, ld, s->R, s->U, ld, qy, qx, s->partials, s->st, s->hist, st));
@@ -881,7 +922,7 @@ int sfb_pcg_solve(sfb_pcg* s, const double* rhs, int ldr, const double* u0, int 
     }
     // Z = P^-1 R_0, rz (solvers.py:418-420)
     SFB_TRY(pre_apply_impl(s->pre, s->R, ld, s->Z, ld, s->T1, s->ldt1, s->T2, s->ldt2, s->partials, s->st, nullptr,
-                           st));
+                           &s->gw, st));
     SFB_CUDA_TRY(cudaEventRecord(s->ev_t0, st));
     int chunks = 0;
     if (s->conditional) {
@@ -929,6 +970,8 @@ int sfb_pcg_destroy(sfb_pcg* s) {
     double* bufs[] = {s->U, s->R, s->Z, s->Q0, s->Q1, s->W, s->B, s->T1, s->T2, s->partials, s->hist, s->incs};
     for (double* b : bufs) cudaFree(b);
     cudaFree(s->st);
+    cudaFree(s->gw.ws);
+    cudaFree(s->gw.flags);
     if (s->stream) cudaStreamDestroy(s->stream);
     cudaEvent_t evs[] = {s->ev_in, s->ev_out, s->ev_t0, s->ev_t1};
     for (auto e : evs)
@@ -944,7 +987,11 @@ int sfb_dgemm_nt(const double* A, int lda, const double* Bt, int ldb, int M, int
     e.mode = EPI_STORE;
     e.C = C;
     e.ldc = ldc;
-    return launch_dgemm_nt(A, lda, Bt, ldb, M, N, K, e, (cudaStream_t)stream);
+    cudaStream_t s = (cudaStream_t)stream;
+    ScopedFree tmp(s);
+    GemmWs gw;
+    SFB_TRY(temp_ws(tmp, gw, s));
+    return launch_dgemm_nt(A, lda, Bt, ldb, M, N, K, with_ws(e, &gw), s);
 }
 
 // ------------------------------------------------------------ reductions --
