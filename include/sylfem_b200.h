@@ -85,6 +85,12 @@ int sfb_init(int device, int* sm_count);
 int sfb_op_create(int qy, int qx, int nterms,
                   int gw, int goff, const double* gband_host,
                   int hw, int hoff, const double* hband_host, sfb_op** out);
+/* Halo-extended column block of a banded operator (column-sharded MO-PCG,
+ * SURVEY §8 e): out_cols local output columns computed from in_cols input
+ * columns (the local block plus the neighbours' halo). */
+int sfb_op_create_block(int qy, int out_cols, int in_cols, int nterms, int w, int goff,
+                        const double* gband_host, int hoff, const double* hband_host,
+                        sfb_op** out);
 /* Dense term list (factors too wide for the banded kernels). */
 int sfb_op_create_dense(int qy, int qx, int nterms, const double* G_host,
                         const double* H_host, sfb_op** out);
@@ -160,6 +166,19 @@ int sfb_pcg_destroy(sfb_pcg* s);
  *      leading dimensions and 16-byte aligned rows (TMA requirement). ------ */
 int sfb_dgemm_nt(const double* A_dev, int lda, const double* Bt_dev, int ldb,
                  int M, int N, int K, double* C_dev, int ldc, void* stream);
+
+/* ---- host-synchronous blocks of the column-sharded MO-PCG (one rank's
+ *      columns; the collectives run between these calls) --------------- */
+/* U += alpha Q; R -= alpha W; *rr_host = local sum R^2 (solvers.py:432-434). */
+int sfb_vec_update(double* U_dev, double* R_dev, const double* Q_dev, const double* W_dev,
+                   int ld, int rows, int cols, double alpha, double* rr_host, void* stream);
+/* Q = Z + beta Q (first != 0: Q = Z) (solvers.py:419, 451-452). */
+int sfb_vec_xpby(double* Q_dev, int ldq, const double* Z_dev, int ldz, int rows, int cols,
+                 double beta, int first, void* stream);
+/* out2_host = { <A,B>, <C,D> } (C, D may be NULL) over the local block. */
+int sfb_vec_dots(const double* A_dev, const double* B_dev, const double* C_dev,
+                 const double* D_dev, int ld, int rows, int cols, double* out2_host,
+                 void* stream);
 
 /* ---- reductions for the IMEX drivers (timestepping.py:89-91, 155, 210-215) */
 /* out4_host = { |A - B|_F (B may be NULL), max|A|, #non-finite(A), |A|_F }. */

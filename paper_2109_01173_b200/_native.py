@@ -27,10 +27,11 @@ PRE_IDENTITY, PRE_INVERSE, PRE_SPECTRAL_PROD, PRE_SPECTRAL_SUM, PRE_BANDED = ran
 
 EXPORTS = [
     "sfb_version", "sfb_last_error", "sfb_init",
-    "sfb_op_create", "sfb_op_create_dense", "sfb_op_apply", "sfb_op_residual", "sfb_op_destroy",
+    "sfb_op_create", "sfb_op_create_block", "sfb_op_create_dense", "sfb_op_apply", "sfb_op_residual", "sfb_op_destroy",
     "sfb_map_create", "sfb_map_apply", "sfb_map_apply_heat", "sfb_map_apply_dib", "sfb_map_destroy",
     "sfb_pre_create", "sfb_pre_create_banded", "sfb_pre_apply", "sfb_pre_transform", "sfb_pre_destroy",
     "sfb_pcg_create", "sfb_pcg_solve", "sfb_pcg_destroy", "sfb_dgemm_nt", "sfb_diff_norm",
+    "sfb_vec_update", "sfb_vec_xpby", "sfb_vec_dots",
 ]
 
 
@@ -50,6 +51,7 @@ _SIGS = {
     "sfb_last_error": (C.c_char_p, []),
     "sfb_init": (_I, [_I, C.POINTER(_I)]),
     "sfb_op_create": (_I, [_I, _I, _I, _I, _I, _P, _I, _I, _P, C.POINTER(_P)]),
+    "sfb_op_create_block": (_I, [_I, _I, _I, _I, _I, _I, _P, _I, _P, C.POINTER(_P)]),
     "sfb_op_create_dense": (_I, [_I, _I, _I, _P, _P, C.POINTER(_P)]),
     "sfb_op_apply": (_I, [_P, _P, _I, _P, _I, _P]),
     "sfb_op_residual": (_I, [_P, _P, _I, _P, _I, _DP, _P]),
@@ -69,6 +71,9 @@ _SIGS = {
                            C.POINTER(PcgResult), _P]),
     "sfb_pcg_destroy": (_I, [_P]),
     "sfb_dgemm_nt": (_I, [_P, _I, _P, _I, _I, _I, _I, _P, _I, _P]),
+    "sfb_vec_update": (_I, [_P, _P, _P, _P, _I, _I, _I, _D, _DP, _P]),
+    "sfb_vec_xpby": (_I, [_P, _I, _P, _I, _I, _I, _D, _I, _P]),
+    "sfb_vec_dots": (_I, [_P, _P, _P, _P, _I, _I, _I, _DP, _P]),
     "sfb_diff_norm": (_I, [_P, _I, _P, _I, _I, _I, _DP, _P]),
 }
 

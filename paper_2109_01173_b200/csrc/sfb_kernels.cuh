@@ -93,6 +93,12 @@ int launch_loop_ctl(PcgState* st, unsigned long long handle, int use_handle, cud
 int launch_norms(const double* A, int lda, const double* B, int ldb, int rows, int cols, double* partials,
                  RedSlots* out, cudaStream_t s);
 int vector_grid_blocks();
+int launch_sh_update(double* U, double* R, const double* Q, const double* W, int ld, int rows, int cols,
+                     double alpha, double* partials, RedSlots* out, cudaStream_t s);
+int launch_sh_xpby(double* Q, int ldq, const double* Z, int ldz, int rows, int cols, double beta, int first,
+                   cudaStream_t s);
+int launch_sh_dots(const double* A, const double* B, const double* C, const double* D, int ld, int rows, int cols,
+                   double* partials, RedSlots* out, cudaStream_t s);
 
 // ------------------------------------------------------ banded solves ----
 // <Z,R> fused into the last row sweep (R == nullptr: no dot)

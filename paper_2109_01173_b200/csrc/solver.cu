@@ -106,6 +106,7 @@ using namespace sfb;
 // =========================================================== operators ====
 struct sfb_op {
     int qy = 0, qx = 0, nterms = 0;
+    int in_cols = 0;  // == qx except for halo-extended column blocks (sharded)
     bool dense = false;
     int width = 1, goff = 0, hoff = 0;
     double* gband = nullptr;
@@ -146,7 +147,8 @@ int op_apply_impl(const sfb_op* op, const double* U, int ldu, double* W, int ldw
     if (!op->dense) {
         BandArgs a;
         a.out_rows = a.in_rows = op->qy;
-        a.out_cols = a.in_cols = op->qx;
+        a.out_cols = op->qx;
+        a.in_cols = op->in_cols;
         a.nterms = op->nterms;
         a.width = op->width;
         a.goff = op->goff;
@@ -419,6 +421,26 @@ int build_graph(sfb_pcg* s, double* iterates) {
 }  // namespace sfb
 
 // ================================================================ ABI =====
+namespace sfb {
+namespace {
+template <class Fn>
+int reduce_call(double* out, int n, cudaStream_t s, Fn fn) {
+    ScopedFree tmp(s);
+    double* parts;
+    RedSlots* red;
+    SFB_TRY(tmp.get(&parts, (size_t)2 * vector_grid_blocks() * 8));
+    SFB_TRY(tmp.get(&red, sizeof(RedSlots)));
+    SFB_CUDA_TRY(cudaMemsetAsync(red, 0, sizeof(RedSlots), s));
+    SFB_TRY(fn(parts, red));
+    RedSlots h;
+    SFB_CUDA_TRY(cudaMemcpyAsync(&h, red, sizeof(h), cudaMemcpyDeviceToHost, s));
+    SFB_CUDA_TRY(cudaStreamSynchronize(s));
+    for (int i = 0; i < n; ++i) out[i] = h.v[i];
+    return SFB_OK;
+}
+}  // namespace
+}  // namespace sfb
+
 extern "C" {
 
 int sfb_version(void) { return 1; }
@@ -450,6 +472,7 @@ int sfb_op_create(int qy, int qx, int nterms, int gw, int goff, const double* gb
     auto* op = new sfb_op;
     op->qy = qy;
     op->qx = qx;
+    op->in_cols = qx;
     op->nterms = nterms;
     op->width = gw;
     op->goff = goff;
@@ -469,12 +492,21 @@ int sfb_op_create(int qy, int qx, int nterms, int gw, int goff, const double* gb
     return SFB_OK;
 }
 
+int sfb_op_create_block(int qy, int out_cols, int in_cols, int nterms, int w, int goff, const double* gband,
+                        int hoff, const double* hband, sfb_op** out) {
+    if (in_cols < out_cols) return arg_error("halo-extended block needs in_cols >= out_cols");
+    SFB_TRY(sfb_op_create(qy, out_cols, nterms, w, goff, gband, w, hoff, hband, out));
+    (*out)->in_cols = in_cols;
+    return SFB_OK;
+}
+
 int sfb_op_create_dense(int qy, int qx, int nterms, const double* G, const double* H, sfb_op** out) {
     if (qy <= 0 || qx <= 0 || nterms <= 0) return arg_error("operator needs positive shape and terms");
     auto* op = new sfb_op;
     op->dense = true;
     op->qy = qy;
     op->qx = qx;
+    op->in_cols = qx;
     op->nterms = nterms;
     op->ldG = pad_ld(qy);
     op->ldH = pad_ld(qx);
@@ -992,6 +1024,29 @@ int sfb_dgemm_nt(const double* A, int lda, const double* Bt, int ldb, int M, int
     GemmWs gw;
     SFB_TRY(temp_ws(tmp, gw, s));
     return launch_dgemm_nt(A, lda, Bt, ldb, M, N, K, with_ws(e, &gw), s);
+}
+
+// ------------------------------------------------ sharded MO-PCG blocks ---
+
+int sfb_vec_update(double* U, double* R, const double* Q, const double* W, int ld, int rows, int cols, double alpha,
+                   double* rr_host, void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    return reduce_call(rr_host, 1, s, [&](double* parts, RedSlots* red) {
+        return launch_sh_update(U, R, Q, W, ld, rows, cols, alpha, parts, red, s);
+    });
+}
+
+int sfb_vec_xpby(double* Q, int ldq, const double* Z, int ldz, int rows, int cols, double beta, int first,
+                 void* stream) {
+    return launch_sh_xpby(Q, ldq, Z, ldz, rows, cols, beta, first, (cudaStream_t)stream);
+}
+
+int sfb_vec_dots(const double* A, const double* B, const double* C, const double* D, int ld, int rows, int cols,
+                 double* out2_host, void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    return reduce_call(out2_host, 2, s, [&](double* parts, RedSlots* red) {
+        return launch_sh_dots(A, B, C, D, ld, rows, cols, parts, red, s);
+    });
 }
 
 // ------------------------------------------------------------ reductions --

@@ -269,6 +269,66 @@ __global__ void __launch_bounds__(VT) norms_kernel(const double* A, int lda, con
     }
 }
 
+// ---- host-synchronous building blocks of the sharded (multi-GPU) MO-PCG ----
+__global__ void __launch_bounds__(VT) sh_update_kernel(double* U, double* R, const double* Q, const double* W, int ld,
+                                                       int rows, int cols, double alpha, double* partials,
+                                                       RedSlots* out) {
+    double rr = 0.0;
+    ROW_LOOP(rows, cols) {
+        const size_t o = (size_t)r * ld + cc;
+        U[o] = __dadd_rn(U[o], __dmul_rn(alpha, Q[o]));
+        const double rv = __dsub_rn(R[o], __dmul_rn(alpha, W[o]));
+        R[o] = rv;
+        rr = fma(rv, rv, rr);
+    }
+    __shared__ double sh[VT / 32];
+    const double p = block_sum<VT>(rr, sh);
+    if (threadIdx.x == 0) partials[blockIdx.x] = p;
+    if (arrive_last(&out->counter[0], gridDim.x)) {
+        const double t = sum_partials<VT>(partials, gridDim.x, 1, sh);
+        if (threadIdx.x == 0) {
+            out->counter[0] = 0;
+            out->v[0] = t;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(VT) sh_xpby_kernel(double* Q, int ldq, const double* Z, int ldz, int rows, int cols,
+                                                     double beta, int first) {
+    ROW_LOOP(rows, cols) {
+        const double z = Z[(size_t)r * ldz + cc];
+        double* q = Q + (size_t)r * ldq + cc;
+        *q = first ? z : __dadd_rn(__dmul_rn(beta, *q), z);
+    }
+}
+
+__global__ void __launch_bounds__(VT) sh_dots_kernel(const double* A, const double* B, const double* C,
+                                                     const double* D, int ld, int rows, int cols, double* partials,
+                                                     RedSlots* out) {
+    double ab = 0.0, cd = 0.0;
+    ROW_LOOP(rows, cols) {
+        const size_t o = (size_t)r * ld + cc;
+        ab = fma(A[o], B[o], ab);
+        if (C) cd = fma(C[o], D[o], cd);
+    }
+    __shared__ double sh[VT / 32];
+    const double p0 = block_sum<VT>(ab, sh);
+    const double p1 = block_sum<VT>(cd, sh);
+    if (threadIdx.x == 0) {
+        partials[blockIdx.x] = p0;
+        partials[gridDim.x + blockIdx.x] = p1;
+    }
+    if (arrive_last(&out->counter[0], gridDim.x)) {
+        const double t0 = sum_partials<VT>(partials, gridDim.x, 1, sh);
+        const double t1 = sum_partials<VT>(partials + gridDim.x, gridDim.x, 1, sh);
+        if (threadIdx.x == 0) {
+            out->counter[0] = 0;
+            out->v[0] = t0;
+            out->v[1] = t1;
+        }
+    }
+}
+
 }  // namespace
 
 int vector_grid_blocks() { return VB; }
@@ -334,6 +394,27 @@ int launch_loop_ctl(PcgState* st, unsigned long long handle, int use_handle, cud
 int launch_norms(const double* A, int lda, const double* B, int ldb, int rows, int cols, double* partials,
                  RedSlots* out, cudaStream_t s) {
     norms_kernel<<<VB, VT, 0, s>>>(A, lda, B, ldb, rows, cols, partials, out);
+    SFB_CHECK_LAUNCH();
+    return SFB_OK;
+}
+
+int launch_sh_update(double* U, double* R, const double* Q, const double* W, int ld, int rows, int cols,
+                     double alpha, double* partials, RedSlots* out, cudaStream_t s) {
+    sh_update_kernel<<<VB, VT, 0, s>>>(U, R, Q, W, ld, rows, cols, alpha, partials, out);
+    SFB_CHECK_LAUNCH();
+    return SFB_OK;
+}
+
+int launch_sh_xpby(double* Q, int ldq, const double* Z, int ldz, int rows, int cols, double beta, int first,
+                   cudaStream_t s) {
+    sh_xpby_kernel<<<VB, VT, 0, s>>>(Q, ldq, Z, ldz, rows, cols, beta, first);
+    SFB_CHECK_LAUNCH();
+    return SFB_OK;
+}
+
+int launch_sh_dots(const double* A, const double* B, const double* C, const double* D, int ld, int rows, int cols,
+                   double* partials, RedSlots* out, cudaStream_t s) {
+    sh_dots_kernel<<<VB, VT, 0, s>>>(A, B, C, D, ld, rows, cols, partials, out);
     SFB_CHECK_LAUNCH();
     return SFB_OK;
 }

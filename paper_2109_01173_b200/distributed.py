@@ -1,0 +1,315 @@
+"""Column-sharded MO-PCG across the GPUs of one node (SURVEY §8 e).
+
+Each rank owns a contiguous block of grid columns (x direction) of U, R, Z,
+Q and W.  Per iteration (the reference recurrences, solvers.py:423-452):
+
+* W = L(Q): left factors act within columns (local); right factors couple
+  columns j-b..j+b, so each rank first receives a b-column halo from both
+  neighbours (point-to-point) and runs the banded kernel on its extended
+  block (``sfb_op_create_block``);
+* <W,Q>, |Q|^2 -> one allreduce of 2 doubles -> alpha;
+* U += alpha Q, R -= alpha W (local), |R|^2 local;
+* Z = P_L^-1 R P_R^-1 with the inverse-form preconditioner: R is transposed
+  to row shards by an all-to-all, each rank computes X^T = P_R^-T R_rows^T
+  (DMMA GEMM), a second all-to-all returns X^T in column shards and
+  Z = P_L^-1 X (DMMA GEMM) is local;
+* {|R|^2, <Z,R>} -> one allreduce (computing Z before the stop test is
+  result-identical: the residual is unchanged) -> stop test, beta;
+* Q = Z + beta Q (local).
+
+So two scalar allreduces, one halo exchange and two all-to-alls per
+iteration.  The collectives are ``torch.distributed`` (NCCL over NVLink on
+GPUs, gloo in the CPU tests); the local compute is a ``Backend`` — the CUDA
+one below (C ABI), or a numpy one in the tests.
+"""
+
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as nat
+from .exceptions import OperatorError, SolverError
+from .solvers import SolveReport, StoppingRule, relative_residual
+
+
+def partition(n: int, parts: int):
+    counts = [n // parts + (1 if r < n % parts else 0) for r in range(parts)]
+    offs = [0]
+    for c in counts[:-1]:
+        offs.append(offs[-1] + c)
+    return counts, offs
+
+
+@dataclass
+class Layout:
+    qy: int
+    qx: int
+    world: int
+    rank: int
+
+    def __post_init__(self):
+        self.col_counts, self.col_offs = partition(self.qx, self.world)
+        self.row_counts, self.row_offs = partition(self.qy, self.world)
+
+    @property
+    def n(self):
+        return self.col_counts[self.rank]
+
+    @property
+    def c0(self):
+        return self.col_offs[self.rank]
+
+    @property
+    def m(self):
+        return self.row_counts[self.rank]
+
+    @property
+    def r0(self):
+        return self.row_offs[self.rank]
+
+
+class Comm:
+    """Collectives of the sharded iteration over torch.distributed."""
+
+    def __init__(self, layout: Layout, device, group=None):
+        import torch
+        import torch.distributed as dist
+        self.t, self.dist = torch, dist
+        self.L = layout
+        self.device = device
+        self.group = group
+
+    def allreduce(self, vals):
+        t = self.t.tensor(vals, dtype=self.t.float64, device=self.device)
+        if self.L.world > 1:
+            self.dist.all_reduce(t, group=self.group)
+        return [float(v) for v in t.tolist()]
+
+    def halo(self, X, b: int):
+        """q_y x (n + 2b) block: left halo | X | right halo (zeros at the domain ends)."""
+        t, L = self.t, self.L
+        qy, n = X.shape
+        ext = t.zeros((qy, n + 2 * b), dtype=X.dtype, device=X.device)
+        ext[:, b:b + n] = X
+        if b == 0 or L.world == 1:
+            return ext
+        if n < b:
+            raise SolverError(f"column shard of {n} columns is narrower than the halo {b}")
+        ops = []
+        left, right = L.rank - 1, L.rank + 1
+        lrecv = t.empty((qy, b), dtype=X.dtype, device=X.device)
+        rrecv = t.empty((qy, b), dtype=X.dtype, device=X.device)
+        if left >= 0:
+            ops.append(self.dist.P2POp(self.dist.isend, X[:, :b].contiguous(), left, group=self.group))
+            ops.append(self.dist.P2POp(self.dist.irecv, lrecv, left, group=self.group))
+        if right < L.world:
+            ops.append(self.dist.P2POp(self.dist.isend, X[:, n - b:].contiguous(), right, group=self.group))
+            ops.append(self.dist.P2POp(self.dist.irecv, rrecv, right, group=self.group))
+        for req in self.dist.batch_isend_irecv(ops):
+            req.wait()
+        if left >= 0:
+            ext[:, :b] = lrecv
+        if right < L.world:
+            ext[:, b + n:] = rrecv
+        return ext
+
+    def _all_to_all(self, send_blocks, recv_shapes, dtype, device):
+        t = self.t
+        send = t.cat([blk.reshape(-1) for blk in send_blocks])
+        rsizes = [a * c for a, c in recv_shapes]
+        recv = t.empty(sum(rsizes), dtype=dtype, device=device)
+        if self.L.world == 1:
+            recv.copy_(send)
+        else:
+            self.dist.all_to_all_single(recv, send, rsizes, [blk.numel() for blk in send_blocks],
+                                        group=self.group)
+        return t.split(recv, rsizes)
+
+    def cols_to_rows(self, Xc):
+        """q_y x n (column shard) -> m x q_x (row shard)."""
+        L = self.L
+        send = [Xc[L.row_offs[s]:L.row_offs[s] + L.row_counts[s], :] for s in range(L.world)]
+        parts = self._all_to_all(send, [(L.m, L.col_counts[s]) for s in range(L.world)], Xc.dtype, Xc.device)
+        return self.t.cat([p.reshape(L.m, L.col_counts[s]) for s, p in enumerate(parts)], dim=1)
+
+    def rowsT_to_colsT(self, XrT):
+        """q_x x m (transposed row shard) -> n x q_y (transposed column shard)."""
+        L = self.L
+        send = [XrT[L.col_offs[s]:L.col_offs[s] + L.col_counts[s], :] for s in range(L.world)]
+        parts = self._all_to_all(send, [(L.n, L.row_counts[s]) for s in range(L.world)], XrT.dtype,
+                                 XrT.device)
+        return self.t.cat([p.reshape(L.n, L.row_counts[s]) for s, p in enumerate(parts)], dim=1)
+
+
+class CudaBackend:
+    """Local compute of one rank through the C ABI (banded block operator,
+    DMMA GEMMs, fused vector passes)."""
+
+    def __init__(self, op, precond, layout: Layout):
+        import torch
+        self.t = torch
+        self.L = layout
+        L = nat.lib()
+        if not op.banded:
+            raise SolverError("the sharded MO-PCG needs a banded operator")
+        w, off, g, h = op.band_layout()
+        self.b = (w - 1) // 2
+        hl = np.ascontiguousarray(h[:, layout.c0:layout.c0 + layout.n, :])
+        out = nat.C.c_void_p()
+        nat.check(L.sfb_op_create_block(layout.qy, layout.n, layout.n + 2 * self.b, len(op.terms), w, off,
+                                        nat.host_ptr(g), 0, nat.host_ptr(hl), nat.C.byref(out)), "block op")
+        self._op = nat.Handle(out.value, L.sfb_op_destroy)
+        if precond.is_identity:
+            self.Linv = self.RinvT = None
+        else:
+            qy, qx = layout.qy, layout.qx
+            Linv = precond._inverse(precond.left, qy, left=True)
+            RinvT = np.ascontiguousarray(precond._inverse(precond.right, qx, left=False).T)
+            self.Linv = self._padded_from(Linv)
+            self.RinvT = self._padded_from(RinvT)
+
+    # -- helpers ------------------------------------------------------------
+    def _padded(self, rows, cols):
+        t = self.t
+        buf = t.zeros((rows, cols + (cols % 2)), dtype=t.float64, device="cuda")
+        return buf[:, :cols]
+
+    def _padded_from(self, a):
+        v = self._padded(*a.shape)
+        v.copy_(self.t.from_numpy(np.ascontiguousarray(a)))
+        return v
+
+    def _gemm(self, A, Bt, M, N, K):
+        C = self._padded(M, N)
+        As, Bs = A, Bt
+        if As.stride(0) % 2 or As.data_ptr() % 16:
+            As = self._padded(*A.shape)
+            As.copy_(A)
+        if Bs.stride(0) % 2 or Bs.data_ptr() % 16:
+            Bs = self._padded(*Bt.shape)
+            Bs.copy_(Bt)
+        nat.check(nat.lib().sfb_dgemm_nt(As.data_ptr(), As.stride(0), Bs.data_ptr(), Bs.stride(0), M, N, K,
+                                         C.data_ptr(), C.stride(0), nat.stream()), "gemm")
+        return C
+
+    # -- backend interface ----------------------------------------------------
+    def zeros(self, rows, cols):
+        return self._padded(rows, cols)
+
+    def from_host(self, a):
+        if isinstance(a, self.t.Tensor):
+            v = self._padded(*a.shape)
+            v.copy_(a)
+            return v
+        return self._padded_from(np.asarray(a, dtype=float))
+
+    def apply_ext(self, ext):
+        L = self.L
+        W = self._padded(L.qy, L.n)
+        e = ext.contiguous()
+        nat.check(nat.lib().sfb_op_apply(self._op.p, e.data_ptr(), e.stride(0), W.data_ptr(), W.stride(0),
+                                         nat.stream()), "apply")
+        return W
+
+    def right_T(self, R_rows):  # (P_R^-1)^T R_rows^T  : q_x x m
+        return self._gemm(self.RinvT, R_rows, self.L.qx, R_rows.shape[0], self.L.qx)
+
+    def left(self, XcT):  # P_L^-1 X_cols : q_y x n
+        return self._gemm(self.Linv, XcT, self.L.qy, XcT.shape[0], self.L.qy)
+
+    def copy(self, X):
+        Y = self._padded(*X.shape)
+        Y.copy_(X)
+        return Y
+
+    def update(self, U, R, Q, W, alpha):
+        out = np.zeros(1)
+        nat.check(nat.lib().sfb_vec_update(U.data_ptr(), R.data_ptr(), Q.data_ptr(), W.data_ptr(), U.stride(0),
+                                           U.shape[0], U.shape[1], float(alpha), nat.dptr(out), nat.stream()),
+                  "update")
+        return float(out[0])
+
+    def xpby(self, Q, Z, beta, first=False):
+        nat.check(nat.lib().sfb_vec_xpby(Q.data_ptr(), Q.stride(0), Z.data_ptr(), Z.stride(0), Q.shape[0],
+                                         Q.shape[1], float(beta), int(first), nat.stream()), "xpby")
+
+    def dots(self, A, B, C=None, D=None):
+        out = np.zeros(2)
+        nat.check(nat.lib().sfb_vec_dots(A.data_ptr(), B.data_ptr(), C.data_ptr() if C is not None else None,
+                                         D.data_ptr() if D is not None else None, A.stride(0), A.shape[0],
+                                         A.shape[1], nat.dptr(out), nat.stream()), "dots")
+        return float(out[0]), float(out[1])
+
+    def to_host(self, X):
+        return X.cpu().numpy()
+
+
+def sharded_mo_pcg(backend, comm: Comm, rhs_local, stop: StoppingRule | None = None, u0_local=None,
+                   max_iter: int = 1000, identity: bool = False, keep_on_device: bool = False) -> SolveReport:
+    """MO-PCG over column shards; same recurrences, stop logic and report as
+    solvers.mo_pcg (solvers.py:365-453).  Returns this rank's columns."""
+    stop = stop or relative_residual()
+    t0 = time.perf_counter()
+    L = comm.L
+    b = getattr(backend, "b", 0)
+    B = backend.from_host(rhs_local)
+    R = backend.copy(B)
+    U = backend.zeros(L.qy, L.n)
+    if u0_local is not None:
+        U = backend.from_host(u0_local)
+        W0 = backend.apply_ext(comm.halo(U, b))
+        scratch = backend.zeros(L.qy, L.n)
+        backend.update(scratch, R, backend.zeros(L.qy, L.n), W0, 1.0)  # R = rhs - L(U0)
+    rr_loc, _ = backend.dots(R, R)
+    res0 = math.sqrt(comm.allreduce([rr_loc])[0])
+    hist, incs = [res0], []
+
+    def report(n, why):
+        return SolveReport(solution=U if keep_on_device else backend.to_host(U), method="mo-pcg-sharded",
+                           iterations=n,
+                           residual_history=np.asarray(hist), stop_reason=why,
+                           wall_time=time.perf_counter() - t0,
+                           diagnostics={"dense_grid_matrices": 5, "increments": np.asarray(incs),
+                                        "stopping_rule": stop.describe(), "world": L.world,
+                                        "columns": (L.c0, L.c0 + L.n)})
+
+    if res0 == 0.0:
+        return report(0, "tolerance")
+
+    def precond(Rk):
+        if identity:
+            return backend.copy(Rk)
+        XrT = backend.right_T(comm.cols_to_rows(Rk))
+        return backend.left(comm.rowsT_to_colsT(XrT))
+
+    Z = precond(R)
+    rz = comm.allreduce([backend.dots(Z, R)[0]])[0]
+    Q = backend.zeros(L.qy, L.n)
+    backend.xpby(Q, Z, 0.0, first=True)
+    for s in range(max_iter):
+        W = backend.apply_ext(comm.halo(Q, b))
+        wq, qq = comm.allreduce(list(backend.dots(W, Q, Q, Q)))
+        if wq <= 0.0:
+            raise OperatorError("operator is not positive definite along a search direction "
+                                f"(<L(Q), Q> = {wq:.3e} at iteration {s})")
+        alpha = rz / wq
+        rr_loc = backend.update(U, R, Q, W, alpha)
+        Z = precond(R)
+        rr, rz_new = comm.allreduce([rr_loc, backend.dots(Z, R)[0]])
+        res = math.sqrt(rr)
+        if not math.isfinite(res):
+            raise SolverError(f"mo_pcg residual became non-finite at iteration {s}")
+        hist.append(res)
+        incs.append(abs(alpha) * math.sqrt(qq))
+        if stop.kind == "residual" and res <= stop.value * res0:
+            return report(s + 1, "tolerance")
+        if stop.kind == "increment" and incs[-1] <= stop.value:
+            return report(s + 1, "increment")
+        beta = rz_new / rz
+        rz = rz_new
+        backend.xpby(Q, Z, beta)
+    return report(max_iter, "max_iter")

@@ -1,0 +1,116 @@
+"""Worker for the world_size > 1 gloo tests of the sharded MO-PCG (CPU).
+
+The collective/halo/transpose logic under test is the product's
+(paper_2109_01173_b200.distributed); the local compute is a numpy backend
+built from the oracle's dense factors (test infrastructure)."""
+
+import os
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+import oracle as orc
+from _cases import sine_source
+from paper_2109_01173_b200.distributed import Comm, Layout, sharded_mo_pcg
+
+
+class NumpyBackend:
+    def __init__(self, terms, Linv, RinvT, layout, b):
+        self.L, self.b = layout, b
+        self.terms = terms
+        self.Linv, self.RinvT = Linv, RinvT
+        qx, n, c0 = layout.qx, layout.n, layout.c0
+        self.Hsub = []
+        for _, H in terms:
+            hs = np.zeros((n + 2 * b, n))
+            for e in range(n + 2 * b):
+                gcol = c0 - b + e
+                if 0 <= gcol < qx:
+                    hs[e] = H[gcol, c0:c0 + n]
+            self.Hsub.append(hs)
+
+    def zeros(self, r, c):
+        return torch.zeros((r, c), dtype=torch.float64)
+
+    def from_host(self, a):
+        return torch.from_numpy(np.array(a, dtype=float, copy=True))
+
+    def copy(self, X):
+        return X.clone()
+
+    def apply_ext(self, ext):
+        e = ext.numpy()
+        return torch.from_numpy(sum(G @ e @ hs for (G, _), hs in zip(self.terms, self.Hsub)))
+
+    def right_T(self, R_rows):
+        return torch.from_numpy(self.RinvT @ R_rows.numpy().T)
+
+    def left(self, XcT):
+        return torch.from_numpy(self.Linv @ XcT.numpy().T)
+
+    def update(self, U, R, Q, W, alpha):
+        U += alpha * Q
+        R -= alpha * W
+        return float((R * R).sum())
+
+    def xpby(self, Q, Z, beta, first=False):
+        if first:
+            Q.copy_(Z)
+        else:
+            Q.mul_(beta).add_(Z)
+
+    def dots(self, A, B, C=None, D=None):
+        return float((A * B).sum()), (float((C * D).sum()) if C is not None else 0.0)
+
+    def to_host(self, X):
+        return X.numpy().copy()
+
+
+def problem(N, k=2):
+    x, y = orc.direction_sets(orc.wave_domain(), k, N, orc.DIRICHLET)
+    terms, rhs_of = orc.elliptic_terms(x, y, 1.0)
+    L, R, _, _ = orc.precond_factors("elliptic_xnormal", x, y)
+    return x, y, terms, rhs_of(sine_source(N, N, 3)), L, R
+
+
+def worker(rank, world, port, N, out_dir, warm):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        x, y, terms, rhs, PL, PR = problem(N)
+        qy, qx = rhs.shape
+        lay = Layout(qy, qx, world, rank)
+        b = 2
+        be = NumpyBackend(terms, np.linalg.inv(PL), np.linalg.inv(PR).T, lay, b)
+        comm = Comm(lay, "cpu")
+        # collective unit checks
+        rng = np.random.default_rng(7)
+        full = rng.standard_normal((qy, qx))
+        loc = torch.from_numpy(full[:, lay.c0:lay.c0 + lay.n].copy())
+        ext = comm.halo(loc, b).numpy()
+        want = np.zeros((qy, lay.n + 2 * b))
+        for e in range(lay.n + 2 * b):
+            g = lay.c0 - b + e
+            if 0 <= g < qx:
+                want[:, e] = full[:, g]
+        assert np.array_equal(ext, want)
+        rows = comm.cols_to_rows(loc).numpy()
+        assert np.array_equal(rows, full[lay.r0:lay.r0 + lay.m, :])
+        colsT = comm.rowsT_to_colsT(torch.from_numpy(full.T[:, lay.r0:lay.r0 + lay.m].copy())).numpy()
+        assert np.array_equal(colsT, full.T[lay.c0:lay.c0 + lay.n, :])
+        u0 = None
+        if warm:
+            u0 = 1e-2 * np.random.default_rng(4).standard_normal((qy, qx))[:, lay.c0:lay.c0 + lay.n]
+        rep = sharded_mo_pcg(be, comm, rhs[:, lay.c0:lay.c0 + lay.n],
+                             stop=orc_stop(), u0_local=u0, max_iter=5000)
+        np.savez(os.path.join(out_dir, f"rank{rank}.npz"), U=rep.solution, iters=rep.iterations,
+                 hist=rep.residual_history, c0=lay.c0, n=lay.n)
+    finally:
+        dist.destroy_process_group()
+
+
+def orc_stop():
+    from paper_2109_01173_b200.solvers import relative_residual
+    return relative_residual(1e-12)

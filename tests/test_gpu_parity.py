@@ -287,3 +287,30 @@ def test_imex_guards():
                            (np.full((yn.q, xn.q), 0.7), np.full((yn.q, xn.q), 0.3)), pb.TimeGrid(0.01, 0.1),
                            inner=pb.InnerSolver(rule="residual", tol=1e-13))
     assert np.max(tr.increments) <= 1e-12 and tr.steady_step == 0
+
+
+# ------------------------------------------------------- sharded (§8 e) ----
+def test_sharded_cuda_backend_single_rank_matches_mo_pcg():
+    import os
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2109_01173_b200.distributed import Comm, CudaBackend, Layout, sharded_mo_pcg
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        x, y, op, rhs = cfg3_small()
+        pre = pb.make_preconditioner("elliptic_xnormal", x, y)
+        lay = Layout(*op.shape, 1, 0)
+        rep = sharded_mo_pcg(CudaBackend(op, pre, lay), Comm(lay, torch.device("cuda")), rhs,
+                             stop=pb.relative_residual(1e-12), max_iter=5000)
+        ref = pb.mo_pcg(op, rhs, precond=pre, stop=pb.relative_residual(1e-12), max_iter=5000)
+        assert abs(rep.iterations - ref.iterations) <= 1
+        assert relerr(rep.solution, ref.solution) <= 1e-10
+    finally:
+        dist.destroy_process_group()

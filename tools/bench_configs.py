@@ -1,0 +1,156 @@
+"""Measure every BASELINE.json configuration (bench.py covers the cfg3 headline).
+
+    python tools/bench_configs.py cfg1 cfg2 cfg4 cfg5 [--steps K] [--iters I] [--mode inverse|banded|spectral]
+                                  [--cpu] [--N n]
+
+One JSON line per config on stdout.  Metrics:
+  cfg1/cfg2 (reduced solve)   DoF/s (one spectral solve = 1 "iteration", SURVEY §8 d)
+  cfg4 (heat IMEX)            DoF*it/s over IMEX steps with a fixed inner budget
+  cfg5 (DIB IMEX, 2 species)  DoF*it/s over IMEX steps with a fixed inner budget per species
+The device time covers the whole step (rhs kernel + device MO-PCG + norms).
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def timed(fn, steps, warm=2):
+    import torch
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    out = [fn() for _ in range(steps)]
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / 1e3, out
+
+
+def reduced(name, args):
+    import torch
+    import paper_2109_01173_b200 as pb
+    from paper_2109_01173_b200 import workloads as wl
+    t0 = time.perf_counter()
+    w = wl.CONFIGS[name](N=args.N)
+    cache = pb.build_spectral_cache(w.op)
+    cache.native()
+    setup = time.perf_counter() - t0
+    qy, qx = w.op.shape
+    rhs = torch.from_numpy(w.rhs).cuda()
+    dt, reps = timed(lambda: pb.solve_reduced(w.op, rhs, cache), args.steps)
+    res = reps[-1].residual_history[0]
+    flops = 4.0 * qy * qx * (qy + qx)
+    line = {"workload": name, "metric": "reduced-solve DoF/s (fp64)", "value": qy * qx * args.steps / dt,
+            "ms_per_solve": 1e3 * dt / args.steps, "q": [qy, qx], "terms": len(w.op),
+            "pencil_swapped": cache.swapped, "relative_residual": res, "setup_s": setup,
+            "sandwich_tflops": flops / (dt / args.steps) / 1e12}
+    if args.cpu:
+        import oracle as orc
+        from paper_2109_01173_b200.workloads import cosine_source_rect, sine_source
+        if name == "cfg1":
+            x, y = orc.direction_sets(orc.unit_square(), 1, w.N, orc.DIRICHLET)
+            terms, rhs_of = orc.elliptic_terms(x, y, 1.0)
+            b = rhs_of(sine_source(w.N, w.N, 1))
+        else:
+            x, y = orc.direction_sets(orc.rect_domain(), 3, w.N, orc.NEUMANN)
+            terms, rhs_of = orc.elliptic_terms(x, y, 0.5)
+            b = rhs_of(cosine_source_rect(w.N, 2))
+        t1 = time.perf_counter()
+        oc = orc.spectral_cache(terms)
+        eig = time.perf_counter() - t1
+        t1 = time.perf_counter()
+        n = 3
+        for _ in range(n):
+            U, rel, _ = orc.reduced_solve(terms, b, oc)
+        cpu_dt = (time.perf_counter() - t1) / n
+        line["cpu_baseline"] = {"value": qy * qx / cpu_dt, "unit": "DoF/s", "cores": os.cpu_count(),
+                                "kind": "port", "sample": f"oracle reduced solve incl. residual, median of {n}; "
+                                                          f"host eigh setup {eig:.2f} s excluded"}
+        line["rel_diff_vs_oracle"] = float(np.linalg.norm(reps[-1].solution.cpu().numpy() - U) / np.linalg.norm(U))
+    return line
+
+
+def imex(name, args):
+    import torch
+    import paper_2109_01173_b200 as pb
+    from paper_2109_01173_b200 import _native as nat
+    from paper_2109_01173_b200 import workloads as wl
+    t0 = time.perf_counter()
+    w = wl.CONFIGS[name](N=args.N, mode=args.mode)
+    ex = w.extra
+    tau = ex["tau"]
+    qy, qx = w.op.shape
+    stop = pb.relative_residual(1e-30)
+    it_budget = args.iters
+    if name == "cfg4":
+        pre = w.precond
+        pre.native(w.op.shape)
+        F = nat.to_device(ex["source"].F)
+        U0 = nat.to_device(ex["u0"])
+        state = {"U": U0.clone(), "k": 0}
+
+        def step():
+            U = state["U"]
+            rhs, _ = w.rhs_of.heat(U, tau * float(np.exp(-state["k"] * tau)), F, check=False)
+            rep = pb.mo_pcg(w.op, rhs, precond=pre, stop=stop, u0=U, max_iter=it_budget)
+            state["U"] = rep.solution
+            state["k"] += 1
+            return rep.iterations
+        per_step_dof_its = qy * qx
+    else:
+        p = ex["params"]
+        kp = p.device_params()
+        op_v, _ = pb.parabolic_operator(w.x, w.y, p.d_theta, tau, lumped=True)
+        pre_u = pb.make_preconditioner("parabolic", w.x, w.y, d_u=1.0, tau=tau, lumped=True, mode=args.mode)
+        pre_v = pb.make_preconditioner("parabolic", w.x, w.y, d_u=p.d_theta, tau=tau, lumped=True,
+                                       mode=args.mode)
+        pre_u.native(w.op.shape)
+        pre_v.native(w.op.shape)
+        state = {"U": nat.to_device(ex["state0"][0]).clone(), "V": nat.to_device(ex["state0"][1]).clone()}
+
+        def step():
+            U, V = state["U"], state["V"]
+            ru, _ = w.rhs_of.dib(U, V, 0, tau * p.rho, kp, check=False)
+            rv, _ = w.rhs_of.dib(U, V, 1, tau * p.rho, kp, check=False)
+            a = pb.mo_pcg(w.op, ru, precond=pre_u, stop=stop, u0=U, max_iter=it_budget)
+            b = pb.mo_pcg(op_v, rv, precond=pre_v, stop=stop, u0=V, max_iter=it_budget)
+            state["U"], state["V"] = a.solution, b.solution
+            return a.iterations + b.iterations
+        per_step_dof_its = qy * qx
+    setup = time.perf_counter() - t0
+    dt, its = timed(step, args.steps, warm=1)
+    line = {"workload": name, "metric": "MO-PCG DoF*iterations/s (fp64), IMEX steps", "value":
+            per_step_dof_its * sum(its) / dt, "ms_per_step": 1e3 * dt / args.steps, "q": [qy, qx],
+            "terms": len(w.op), "inner_iterations_per_step": its[-1], "precond_mode": args.mode,
+            "setup_s": setup, "note": "fixed inner budget per species per step (full runs need ~1e3-1e4 "
+                                      "iterations per step, SURVEY finding 5)"}
+    return line
+
+
+def main():
+    import argparse
+    ap = argparse.ArgumentParser()
+    ap.add_argument("configs", nargs="+")
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--mode", default="inverse")
+    ap.add_argument("--cpu", action="store_true")
+    ap.add_argument("--N", type=int, default=None)
+    args = ap.parse_args()
+    for name in args.configs:
+        line = reduced(name, args) if name in ("cfg1", "cfg2") else imex(name, args)
+        print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()
