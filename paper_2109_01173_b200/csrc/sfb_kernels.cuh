@@ -101,19 +101,30 @@ int launch_sh_dots(const double* A, const double* B, const double* C, const doub
                    double* partials, RedSlots* out, cudaStream_t s);
 
 // ------------------------------------------------------ banded solves ----
-// <Z,R> fused into the last row sweep (R == nullptr: no dot)
-struct ZrDot {
+// --------------------------------------------- segmented banded solves ----
+// One SPD banded factor P = C C^T prepared for segmented solves (seg_solve.cu).
+struct SegFactor {
+    int n = 0, b = 0;
+    double* band = nullptr;  // [n + b][b + 1], reciprocal diagonal at d = b, b zero rows appended
+    double* Hf = nullptr;    // [P][S][b] forward responses to unit incoming states
+    double* Hb = nullptr;    // [P][S][b] backward responses
+    double* Tf = nullptr;    // [P][b][b] forward state transfer
+    double* Tb = nullptr;    // [P][b][b] backward state transfer
+};
+struct SegDot {
     const double* R = nullptr;
     int ldr = 0;
-    double* partials = nullptr;
+    double* partials = nullptr;  // one per tile
     unsigned* counter = nullptr;
-    PcgState* pcg = nullptr;   // status gate; receives rz_next
+    PcgState* pcg = nullptr;
     double* dot_out = nullptr;
 };
-int launch_band_chol_cols(const double* lband, int bw, int n, const double* Xin, int ldi, double* X, int ld,
-                          int ncols, const PcgState* st, cudaStream_t s);
-int launch_band_chol_rows(const double* rband, int bw, int n, double* X, int ld, int nrows, const ZrDot& zr,
-                          cudaStream_t s);
-int band_chol_rows_blocks(int nrows);
+int seg_length();
+// Solve P y = x for every line: along_rows = 0 -> lines are columns (P acts
+// from the left), 1 -> lines are rows (P acts from the right).  X may alias
+// Xin.  sv_f / sv_b: scratch of [P][b][nlines] doubles each.
+int launch_seg_factor(const SegFactor& f, int along_rows, const double* Xin, int ldi, double* X, int ld,
+                      int nlines, const SegDot* dot, double* sv_f, double* sv_b, const PcgState* pcg_gate,
+                      cudaStream_t s);
 
 }  // namespace sfb

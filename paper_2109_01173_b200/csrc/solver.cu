@@ -80,6 +80,8 @@ inline int pad_ld(int cols) { return round_up(cols < 1 ? 1 : cols, 32); }
 struct GemmWs {
     double* ws = nullptr;
     unsigned* flags = nullptr;
+    double* seg_f = nullptr;  // segmented-solve boundary states (banded preconditioner)
+    double* seg_b = nullptr;
 };
 
 // Temporary stream-K workspace from the stream-ordered pool.
@@ -132,13 +134,88 @@ struct sfb_pre {
     double *A1 = nullptr, *A1t = nullptr, *B1 = nullptr, *B1t = nullptr;
     int ldA = 0, ldB = 0;
     double *sl = nullptr, *sr = nullptr;
-    // BANDED: lower Cholesky factors in band storage
-    double *lband = nullptr, *rband = nullptr;
-    int bwL = 0, bwR = 0;
+    // BANDED: Cholesky factors prepared for segmented solves
+    SegFactor fl, fr;
+    size_t seg_doubles = 0;  // scratch per boundary-state buffer
 };
 
 namespace sfb {
 namespace {
+
+inline int seg_tiles(int qy, int qx) {
+    const int S = seg_length();
+    return ((qx + S - 1) / S) * ((qy + S - 1) / S);
+}
+
+// Host precompute of a segmented banded factor (seg_solve.cu): band with the
+// reciprocal diagonal and b zero rows appended, the responses H of every
+// segment to unit incoming states, and the b x b state transfers T.
+int build_seg_factor(int n, int b, const double* band_host, SegFactor& f) {
+    const int S = seg_length();
+    const int P = (n + S - 1) / S;
+    const int bb = std::max(b, 1);
+    std::vector<double> band((size_t)(n + b) * (b + 1), 0.0);
+    std::copy(band_host, band_host + (size_t)n * (b + 1), band.begin());
+    auto C = [&](int i, int d) { return band[(size_t)i * (b + 1) + d]; };  // C[i][i-b+d], 1/C_ii at d=b
+    std::vector<double> Hf((size_t)P * S * bb, 0.0), Hb((size_t)P * S * bb, 0.0);
+    std::vector<double> Tf((size_t)P * bb * bb, 0.0), Tb((size_t)P * bb * bb, 0.0);
+    std::vector<double> w(bb);
+    for (int p = 0; p < P; ++p) {
+        const int start = p * S, len = std::min(S, n - start), end = start + len;
+        for (int d = 0; d < b; ++d) {
+            // forward: incoming state y_{start-b+d'} = delta(d', d)
+            std::fill(w.begin(), w.end(), 0.0);
+            w[d] = 1.0;
+            for (int k = 0; k < len; ++k) {
+                const int i = start + k;
+                double v = 0.0;
+                for (int e = 0; e < b; ++e) v -= C(i, e) * w[e];
+                v *= C(i, b);
+                for (int e = 0; e + 1 < b; ++e) w[e] = w[e + 1];
+                w[b - 1] = v;
+                Hf[((size_t)p * S + k) * bb + d] = v;
+            }
+            for (int o = 0; o < b; ++o) {
+                const int r = end - b + o;
+                Tf[((size_t)p * bb + o) * bb + d] = r >= start ? Hf[((size_t)p * S + (r - start)) * bb + d]
+                                                               : (r - (start - b) == d ? 1.0 : 0.0);
+            }
+            // backward: incoming state z_{end+e} = delta(e, d); w[e-1] = z[i+e]
+            std::fill(w.begin(), w.end(), 0.0);
+            w[d] = 1.0;
+            for (int k = len - 1; k >= 0; --k) {
+                const int i = start + k;
+                double v = 0.0;
+                for (int e = b; e >= 1; --e) v -= C(i + e, b - e) * w[e - 1];
+                v *= C(i, b);
+                for (int e = b - 1; e >= 1; --e) w[e] = w[e - 1];
+                w[0] = v;
+                Hb[((size_t)p * S + k) * bb + d] = v;
+            }
+            for (int o = 0; o < b; ++o) {
+                const int r = start + o;
+                Tb[((size_t)p * bb + o) * bb + d] = r < end ? Hb[((size_t)p * S + (r - start)) * bb + d]
+                                                           : (r - end == d ? 1.0 : 0.0);
+            }
+        }
+    }
+    f.n = n;
+    f.b = b;
+    auto up = [](double** dst, const std::vector<double>& v) {
+        if (dalloc(dst, v.size()) != SFB_OK) return SFB_ERR_NOMEM;
+        if (cudaMemcpy(*dst, v.data(), v.size() * 8, cudaMemcpyHostToDevice) != cudaSuccess) {
+            set_error("uploading segmented factor failed");
+            return SFB_ERR_CUDA;
+        }
+        return SFB_OK;
+    };
+    SFB_TRY(up(&f.band, band));
+    SFB_TRY(up(&f.Hf, Hf));
+    SFB_TRY(up(&f.Hb, Hb));
+    SFB_TRY(up(&f.Tf, Tf));
+    SFB_TRY(up(&f.Tb, Tb));
+    return SFB_OK;
+}
 
 // W = op(U) on device buffers (U must have an even ld and 16B alignment for
 // the dense path).  T1 is qx x qy scratch (ld ldt) for the dense path.
@@ -239,19 +316,19 @@ int pre_apply_impl(const sfb_pre* p, const double* R, int ldr, double* Z, int ld
             return launch_dgemm_nt(p->A1, p->ldA, T1, ldt1, qy, qx, qy, with_ws(last, gw), s);
         }
         case SFB_PRE_BANDED: {
-            // Z = P_L^-1 R by column sweeps (R -> Z), then Z P_R^-1 by row
-            // sweeps in place with <Z,R> fused into the final pass.
-            SFB_TRY(launch_band_chol_cols(p->lband, p->bwL, qy, R, ldr, Z, ldz, qx, pcg, s));
-            ZrDot zr;
-            if (pcg || red) {
-                zr.R = R;
-                zr.ldr = ldr;
-                zr.partials = partials;
-                zr.counter = counter;
-                zr.pcg = pcg;
-                zr.dot_out = red ? &red->v[3] : nullptr;
-            }
-            return launch_band_chol_rows(p->rband, p->bwR, qx, Z, ldz, qy, zr, s);
+            // Z = P_L^-1 R (lines = columns, R -> Z), then Z P_R^-1 in place
+            // (lines = rows) with <Z,R> fused into the last tile pass.
+            if (gw == nullptr || gw->seg_f == nullptr) return arg_error("banded preconditioner needs scratch");
+            SFB_TRY(launch_seg_factor(p->fl, 0, R, ldr, Z, ldz, qx, nullptr, gw->seg_f, gw->seg_b, pcg, s));
+            SegDot dot;
+            dot.R = R;
+            dot.ldr = ldr;
+            dot.partials = partials;
+            dot.counter = counter;
+            dot.pcg = pcg;
+            dot.dot_out = red ? &red->v[3] : nullptr;
+            return launch_seg_factor(p->fr, 1, Z, ldz, Z, ldz, qy, (pcg || red) ? &dot : nullptr, gw->seg_f,
+                                     gw->seg_b, pcg, s);
         }
     }
     return arg_error("unknown preconditioner kind");
@@ -764,24 +841,21 @@ int sfb_pre_create(int qy, int qx, int kind, const double* L, const double* R, c
 
 int sfb_pre_create_banded(int qy, int qx, int bwL, const double* lband, int bwR, const double* rband,
                           sfb_pre** out) {
-    if (qy <= 0 || qx <= 0 || bwL < 0 || bwR < 0) return arg_error("bad banded preconditioner shape");
+    if (qy <= 0 || qx <= 0 || bwL < 0 || bwR < 0 || bwL > 4 || bwR > 4)
+        return arg_error("bad banded preconditioner shape (half-bandwidth 0..4)");
     auto* p = new sfb_pre;
     p->kind = SFB_PRE_BANDED;
     p->qy = qy;
     p->qx = qx;
-    p->bwL = bwL;
-    p->bwR = bwR;
-    int rc = dalloc(&p->lband, (size_t)qy * (bwL + 1));
-    if (rc == SFB_OK) rc = dalloc(&p->rband, (size_t)qx * (bwR + 1));
-    if (rc == SFB_OK && (cudaMemcpy(p->lband, lband, (size_t)qy * (bwL + 1) * 8, cudaMemcpyHostToDevice) != cudaSuccess ||
-                         cudaMemcpy(p->rband, rband, (size_t)qx * (bwR + 1) * 8, cudaMemcpyHostToDevice) != cudaSuccess)) {
-        set_error("uploading Cholesky bands failed");
-        rc = SFB_ERR_CUDA;
-    }
+    int rc = build_seg_factor(qy, bwL, lband, p->fl);
+    if (rc == SFB_OK) rc = build_seg_factor(qx, bwR, rband, p->fr);
     if (rc != SFB_OK) {
         sfb_pre_destroy(p);
         return rc;
     }
+    const size_t S = (size_t)seg_length();
+    p->seg_doubles = std::max(((qy + S - 1) / S) * std::max(bwL, 1) * (size_t)qx,
+                              ((qx + S - 1) / S) * std::max(bwR, 1) * (size_t)qy);
     *out = p;
     return SFB_OK;
 }
@@ -801,14 +875,18 @@ int sfb_pre_apply(const sfb_pre* p, const double* R, int ldr, double* Z, int ldz
     double* parts = nullptr;
     RedSlots* red = nullptr;
     SFB_TRY(tmp.get(&parts, (size_t)std::max(std::max(vector_grid_blocks(), gemm_grid_blocks(p->qy, p->qx)),
-                                             band_chol_rows_blocks(p->qy)) * 8));
+                                             seg_tiles(p->qy, p->qx)) * 8));
     SFB_TRY(tmp.get(&red, sizeof(RedSlots)));
     SFB_CUDA_TRY(cudaMemsetAsync(red, 0, sizeof(RedSlots), s));
     SFB_CUDA_TRY(cudaMemcpy2DAsync(Rb, (size_t)ld * 8, R, (size_t)ldr * 8, (size_t)p->qx * 8, p->qy,
                                    cudaMemcpyDeviceToDevice, s));
     GemmWs gw;
     if (T1 != nullptr) SFB_TRY(temp_ws(tmp, gw, s));
-    SFB_TRY(pre_apply_impl(p, Rb, ld, Zb, ld, T1, ldt1, T2, ld, parts, nullptr, red, T1 ? &gw : nullptr, s));
+    if (p->kind == SFB_PRE_BANDED) {
+        SFB_TRY(tmp.get(&gw.seg_f, p->seg_doubles * 8));
+        SFB_TRY(tmp.get(&gw.seg_b, p->seg_doubles * 8));
+    }
+    SFB_TRY(pre_apply_impl(p, Rb, ld, Zb, ld, T1, ldt1, T2, ld, parts, nullptr, red, &gw, s));
     SFB_CUDA_TRY(cudaMemcpy2DAsync(Z, (size_t)ldz * 8, Zb, (size_t)ld * 8, (size_t)p->qx * 8, p->qy,
                                    cudaMemcpyDeviceToDevice, s));
     return SFB_OK;
@@ -852,8 +930,13 @@ int sfb_pre_destroy(sfb_pre* p) {
     cudaFree(p->B1t);
     cudaFree(p->sl);
     cudaFree(p->sr);
-    cudaFree(p->lband);
-    cudaFree(p->rband);
+    for (SegFactor* f : {&p->fl, &p->fr}) {
+        cudaFree(f->band);
+        cudaFree(f->Hf);
+        cudaFree(f->Hb);
+        cudaFree(f->Tf);
+        cudaFree(f->Tb);
+    }
     delete p;
     return SFB_OK;
 }
@@ -878,13 +961,17 @@ int sfb_pcg_create(const sfb_op* op, const sfb_pre* pre, sfb_pcg** out) {
         if (rc == SFB_OK) rc = dalloc(b, n);
     if (rc == SFB_OK) rc = dalloc(&s->T1, (size_t)s->qx * s->ldt1);
     const int nparts = 2 * std::max(std::max(vector_grid_blocks(), band_grid_blocks(s->qy, s->qx)),
-                                    std::max(gemm_grid_blocks(s->qy, s->qx), band_chol_rows_blocks(s->qy)));
+                                    std::max(gemm_grid_blocks(s->qy, s->qx), seg_tiles(s->qy, s->qx)));
     if (rc == SFB_OK) rc = dalloc(&s->partials, nparts);
     if (rc == SFB_OK) rc = talloc(&s->st, sizeof(PcgState));
     if (rc == SFB_OK) rc = dalloc(&s->gw.ws, gemm_workspace_doubles());
     if (rc == SFB_OK) rc = talloc(&s->gw.flags, (size_t)gemm_max_tiles() * sizeof(unsigned));
     if (rc == SFB_OK && cudaMemset(s->gw.flags, 0, (size_t)gemm_max_tiles() * sizeof(unsigned)) != cudaSuccess)
         rc = SFB_ERR_CUDA;
+    if (rc == SFB_OK && pre->kind == SFB_PRE_BANDED) {
+        rc = dalloc(&s->gw.seg_f, pre->seg_doubles);
+        if (rc == SFB_OK) rc = dalloc(&s->gw.seg_b, pre->seg_doubles);
+    }
     if (rc == SFB_OK) {
         for (double** b : bufs) cudaMemset(*b, 0, n * 8);
         cudaMemset(s->T1, 0, (size_t)s->qx * s->ldt1 * 8);
@@ -1004,6 +1091,8 @@ int sfb_pcg_destroy(sfb_pcg* s) {
     cudaFree(s->st);
     cudaFree(s->gw.ws);
     cudaFree(s->gw.flags);
+    cudaFree(s->gw.seg_f);
+    cudaFree(s->gw.seg_b);
     if (s->stream) cudaStreamDestroy(s->stream);
     cudaEvent_t evs[] = {s->ev_in, s->ev_out, s->ev_t0, s->ev_t1};
     for (auto e : evs)
