@@ -58,6 +58,7 @@ def parse():
     ap.add_argument("--ref-iters-per-step", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-alt", action="store_true", help="skip the banded-preconditioner (f1) measurement")
     return ap.parse_args()
 
 
@@ -272,6 +273,29 @@ def run_native(args):
                "h2d_bytes_per_step": int(qy * qx * 8),
                "d2h_bytes_per_step": int(qy * qx * 8 + (2 * K_it + 1) * 8)}
 
+    # ---- the same workload with the f1 preconditioner (banded Cholesky,
+    #      segmented solves): same operator, parity-neutral, HBM-bound ----
+    alt = {}
+    if world == 1 and not args.no_alt and args.precond_mode != "banded":
+        pre_b = pb.make_preconditioner("elliptic_xnormal", w.x, w.y, mode="banded")
+        pre_b.native(op.shape)
+        for _ in range(max(args.warmup, 1)):
+            pb.mo_pcg(op, rhs_d, precond=pre_b, stop=stop, max_iter=K_it)
+        barrier()
+        e0.record()
+        its_b, lms = 0, []
+        for _ in range(args.steps):
+            rb = pb.mo_pcg(op, rhs_d, precond=pre_b, stop=stop, max_iter=K_it)
+            its_b += rb.iterations
+            lms.append(rb.diagnostics["device"]["loop_ms"])
+        e1.record()
+        barrier()
+        el_b = e0.elapsed_time(e1) / 1e3
+        alt["banded"] = {"value": qy * qx * its_b / el_b, "unit": UNIT, "ms_per_step": 1e3 * el_b / args.steps,
+                         "iteration_ms": statistics.median(lms) / K_it,
+                         "note": "SURVEY §8 f1: same preconditioner P_L U P_R applied by segmented banded "
+                                 "Cholesky solves instead of dense-inverse GEMMs (parity-neutral)"}
+
     # ---- roofline of the dominant kernel: the DMMA GEMM (q x q x q) ----
     L = nat.lib()
     ldq = qy + (qy % 2)
@@ -369,6 +393,7 @@ def run_native(args):
             "e2e": e2e,
             "gpu_launches": per_step_launches * args.steps,
             "clocks": clk,
+            "alt_preconditioner": alt or None,
         }
         print(json.dumps(line), flush=True)
     if dist is not None:

@@ -16,6 +16,7 @@
 // (solvers.py:424-431).
 #include "sfb_common.cuh"
 #include "sfb_kernels.cuh"
+#include "sfb_launch.cuh"
 
 namespace sfb {
 
@@ -24,17 +25,23 @@ namespace {
 constexpr int TX = 128;
 constexpr int TY = 32;
 
+template <int W>
+__host__ __device__ constexpr int wpad() {
+    return W + 1;  // even: the coefficients of one halo row load as 16-byte pairs
+}
+
 template <int T, int W>
 constexpr int band_smem() {
-    return ((TY + W - 1) * (TX + W - 1) + T * (TY + 2 * (W - 1)) * W) * 8;
+    return ((TY + W - 1) * (TX + W - 1) + T * (TY + W - 1) * wpad<W>()) * 8;
 }
 
 template <int T, int W>
 __global__ void __launch_bounds__(TX) band_kernel(BandArgs a) {
-    constexpr int HR = TY + W - 1, HC = TX + W - 1, GR = TY + 2 * (W - 1);
+    SFB_PDL_PROLOGUE();
+    constexpr int HR = TY + W - 1, HC = TX + W - 1;
     extern __shared__ double sm[];
     double* Qs = sm;             // [HR][HC]
-    double* Gs = sm + HR * HC;   // [T][GR][W]
+    double* Gs = sm + HR * HC;   // [T][HR][W+1]
 
     PcgState* st = a.pcg;
     int s = 0;
@@ -53,8 +60,9 @@ __global__ void __launch_bounds__(TX) band_kernel(BandArgs a) {
     const int urows = a.in_rows - 2 * a.rs, ucols = a.in_cols - 2 * a.cs;
     bool flag = false;
     double vmax = 0.0;
+    #pragma unroll 4
     for (int idx = threadIdx.x; idx < HR * HC; idx += TX) {
-        const int r = idx / HC, cc = idx - r * HC;
+        const int r = idx / HC, cc = idx - r * HC;  // HC is a compile-time constant
         const int gr = y0 + a.goff + r, gx = x0 + a.hoff + cc;
         double v = 0.0;
         if (gr >= 0 && gr < a.in_rows && gx >= 0 && gx < a.in_cols) {
@@ -96,18 +104,20 @@ __global__ void __launch_bounds__(TX) band_kernel(BandArgs a) {
                 else vmax = fmax(vmax, fabs(v));
             }
         }
-        Qs[idx] = v;
+        Qs[r * HC + cc] = v;
     }
     if (a.check != nullptr) {
         if (flag) atomicOr(a.check + 1, 1ull);
         if (vmax > 0.0) atomicMax(a.check, (unsigned long long)__double_as_longlong(vmax));
     }
     // ---- left-factor coefficients of this row tile (zero outside [0,TY)) ----
-    for (int idx = threadIdx.x; idx < T * GR * W; idx += TX) {
-        const int t = idx / (GR * W), rem = idx - t * GR * W, rr = rem / W, d = rem - rr * W;
-        const int i = rr - (W - 1), gi = y0 + i;
+    // halo-row-major: Gs[t][r][d] multiplies Y_t(r) into output row i = r - d
+    constexpr int WP = wpad<W>();
+    for (int idx = threadIdx.x; idx < T * HR * WP; idx += TX) {
+        const int t = idx / (HR * WP), rem = idx - t * HR * WP, r = rem / WP, d = rem - r * WP;
+        const int i = r - d, gi = y0 + i;
         double v = 0.0;
-        if (t < a.nterms && i >= 0 && i < TY && gi < a.out_rows)
+        if (d < W && t < a.nterms && i >= 0 && i < TY && gi < a.out_rows)
             v = a.gband[((size_t)t * a.out_rows + gi) * W + d];
         Gs[idx] = v;
     }
@@ -139,11 +149,16 @@ __global__ void __launch_bounds__(TX) band_kernel(BandArgs a) {
                     double y = 0.0;
                     #pragma unroll
                     for (int e = 0; e < W; ++e) y = fma(qv[e], h[t][e], y);
-                    const double* gp = Gs + (t * GR + r + W - 1) * W;
+                    const double2* gp = reinterpret_cast<const double2*>(Gs + (t * HR + r) * WP);
                     #pragma unroll
-                    for (int d = 0; d < W; ++d) {
-                        const int slot = (u - d + W) % W;
-                        acc[slot] = fma(gp[-d * W + d], y, acc[slot]);
+                    for (int dd = 0; dd < WP / 2; ++dd) {
+                        const double2 g = gp[dd];
+                        const int s0 = (u - 2 * dd + 2 * W) % W;
+                        acc[s0] = fma(g.x, y, acc[s0]);
+                        if (2 * dd + 1 < W) {
+                            const int s1 = (u - 2 * dd - 1 + 2 * W) % W;
+                            acc[s1] = fma(g.y, y, acc[s1]);
+                        }
                     }
                 }
                 const int i = r - (W - 1);
@@ -203,7 +218,7 @@ int launch_tw(const BandArgs& a, cudaStream_t stream) {
         attr = true;
     }
     dim3 grid((a.out_cols + TX - 1) / TX, (a.out_rows + TY - 1) / TY);
-    band_kernel<T, W><<<grid, TX, smem, stream>>>(a);
+    SFB_TRY(launch_kernel(band_kernel<T, W>, dim3(grid), dim3(TX), smem, stream, a));
     SFB_CHECK_LAUNCH();
     return SFB_OK;
 }

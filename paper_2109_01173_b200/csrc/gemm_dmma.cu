@@ -20,6 +20,7 @@
 
 #include "sfb_common.cuh"
 #include "sfb_kernels.cuh"
+#include "sfb_launch.cuh"
 
 namespace sfb {
 
@@ -144,6 +145,7 @@ __device__ __forceinline__ double tile_epilogue(double (&acc)[8][4][2], const Ge
 __global__ void __launch_bounds__(NTHREADS, 1)
     dgemm_nt_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
                     int K, GemmEpi ep, Sched sc) {
+    SFB_PDL_PROLOGUE();
     if (ep.pcg != nullptr && ep.pcg->status != SFB_PCG_RUNNING) return;  // uniform gate
 
     extern __shared__ uint8_t smem_raw[];
@@ -356,31 +358,12 @@ int launch_dgemm_nt(const double* A, int lda, const double* Bt, int ldb, int M, 
     sc.U = (long long)tiles * sc.KT;
     const bool have_ws = ep.sk_ws != nullptr && ep.sk_flags != nullptr;
     sc.G = gemm_grid_for(M, N, K, have_ws);
-    if (sc.G != tiles) {
-        // split tiles: all CTAs must be co-resident (finishing CTAs wait on
-        // continuation pieces), which a cooperative launch guarantees
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(sc.G);
-        cfg.blockDim = dim3(NTHREADS);
-        cfg.dynamicSmemBytes = SMEM_BYTES;
-        cfg.stream = stream;
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeCooperative;
-        attr[0].val.cooperative = 1;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-        if (cudaLaunchKernelEx(&cfg, dgemm_nt_kernel, ma, mb, M, N, K, ep, sc) != cudaSuccess) {
-            // e.g. inside a capture that rejects the attribute: a one-CTA-per-SM
-            // persistent grid is co-resident on an otherwise idle device
-            cudaGetLastError();
-            cfg.numAttrs = 0;
-            SFB_CUDA_TRY(cudaLaunchKernelEx(&cfg, dgemm_nt_kernel, ma, mb, M, N, K, ep, sc));
-        }
-    } else {
-        dgemm_nt_kernel<<<sc.G, NTHREADS, SMEM_BYTES, stream>>>(ma, mb, M, N, K, ep, sc);
-        SFB_CHECK_LAUNCH();
-    }
-    return SFB_OK;
+    // Split tiles need all CTAs co-resident (a finishing CTA waits for the
+    // continuation pieces of later CTAs): the grid is at most one CTA per SM
+    // and each CTA fills an SM, so every CTA is resident once the previous
+    // kernel drains; continuation pieces are the first work of their CTA and
+    // never wait, so progress is guaranteed.
+    return launch_kernel(dgemm_nt_kernel, dim3(sc.G), dim3(NTHREADS), SMEM_BYTES, stream, ma, mb, M, N, K, ep, sc);
 }
 
 int gemm_grid_blocks(int M, int N) { return ((N + BN - 1) / BN) * ((M + BM - 1) / BM); }

@@ -20,6 +20,7 @@
 // produces <Z,R> for MO-PCG's beta.
 #include "sfb_common.cuh"
 #include "sfb_kernels.cuh"
+#include "sfb_launch.cuh"
 
 namespace sfb {
 
@@ -30,20 +31,22 @@ constexpr int S = 64;  // segment length == tile edge == threads per CTA
 enum { DIR_COL = 0, DIR_ROW = 1 };
 enum { PH_FWD = 0, PH_FIX_BWD = 1, PH_FIX = 2 };
 
-// tile[a][c]: a = position along the sweep, c = line within the tile
+constexpr int NT = 256;  // threads per tile CTA: all load/store, the first S sweep
+
+// tile[a][c]: a = position along the sweep, c = line within the tile.  All
+// NT threads move the tile (coalesced along the contiguous global index).
 template <int DIR>
 __device__ __forceinline__ void tile_load(double (*tile)[S + 1], const double* X, int ld, int sweep0, int line0,
                                           int nsweep, int nlines) {
-    const int t = threadIdx.x;
-    if (DIR == DIR_COL) {  // element (row = sweep0 + a, col = line0 + t)
-        for (int a = 0; a < S; ++a) {
-            const int i = sweep0 + a, j = line0 + t;
-            tile[a][t] = (i < nsweep && j < nlines) ? X[(size_t)i * ld + j] : 0.0;
-        }
-    } else {  // element (row = line0 + c, col = sweep0 + t)
-        for (int c = 0; c < S; ++c) {
-            const int i = line0 + c, j = sweep0 + t;
-            tile[t][c] = (i < nlines && j < nsweep) ? X[(size_t)i * ld + j] : 0.0;
+    const int t = threadIdx.x, lo = t % S, hi = t / S;
+    #pragma unroll 4
+    for (int k = hi; k < S; k += NT / S) {
+        if (DIR == DIR_COL) {  // element (row = sweep0 + k, col = line0 + lo)
+            const int i = sweep0 + k, j = line0 + lo;
+            tile[k][lo] = (i < nsweep && j < nlines) ? X[(size_t)i * ld + j] : 0.0;
+        } else {  // element (row = line0 + k, col = sweep0 + lo)
+            const int i = line0 + k, j = sweep0 + lo;
+            tile[lo][k] = (i < nlines && j < nsweep) ? X[(size_t)i * ld + j] : 0.0;
         }
     }
 }
@@ -51,16 +54,15 @@ __device__ __forceinline__ void tile_load(double (*tile)[S + 1], const double* X
 template <int DIR>
 __device__ __forceinline__ void tile_store(double (*tile)[S + 1], double* X, int ld, int sweep0, int line0,
                                            int nsweep, int nlines) {
-    const int t = threadIdx.x;
-    if (DIR == DIR_COL) {
-        for (int a = 0; a < S; ++a) {
-            const int i = sweep0 + a, j = line0 + t;
-            if (i < nsweep && j < nlines) X[(size_t)i * ld + j] = tile[a][t];
-        }
-    } else {
-        for (int c = 0; c < S; ++c) {
-            const int i = line0 + c, j = sweep0 + t;
-            if (i < nlines && j < nsweep) X[(size_t)i * ld + j] = tile[t][c];
+    const int t = threadIdx.x, lo = t % S, hi = t / S;
+    #pragma unroll 4
+    for (int k = hi; k < S; k += NT / S) {
+        if (DIR == DIR_COL) {
+            const int i = sweep0 + k, j = line0 + lo;
+            if (i < nsweep && j < nlines) X[(size_t)i * ld + j] = tile[k][lo];
+        } else {
+            const int i = line0 + k, j = sweep0 + lo;
+            if (i < nlines && j < nsweep) X[(size_t)i * ld + j] = tile[lo][k];
         }
     }
 }
@@ -87,7 +89,8 @@ struct SegArgs {
 };
 
 template <int B, int DIR, int PH>
-__global__ void __launch_bounds__(S) seg_tile_kernel(SegArgs a) {
+__global__ void __launch_bounds__(NT) seg_tile_kernel(SegArgs a) {
+    SFB_PDL_PROLOGUE();
     if (a.pcg != nullptr && a.pcg->status != SFB_PCG_RUNNING) return;
     __shared__ double tile[S][S + 1];
     const int p = blockIdx.x;             // segment along the sweep
@@ -98,7 +101,7 @@ __global__ void __launch_bounds__(S) seg_tile_kernel(SegArgs a) {
     const int gl = line0 + c;
     tile_load<DIR>(tile, PH == PH_FWD ? a.Xin : a.X, PH == PH_FWD ? a.ldi : a.ld, start, line0, a.n, a.nlines);
     __syncthreads();
-    const bool live = gl < a.nlines;
+    const bool live = c < S && gl < a.nlines;
     if (live) {
         if (PH == PH_FWD) {
             double w[B > 0 ? B : 1];
@@ -154,21 +157,22 @@ __global__ void __launch_bounds__(S) seg_tile_kernel(SegArgs a) {
     if (PH == PH_FIX && a.R != nullptr) {
         // <Z,R> over this tile (deterministic: fixed thread/tile order)
         double dot = 0.0;
-        if (DIR == DIR_COL) {
-            for (int k = 0; k < len; ++k)
-                if (live) dot = fma(tile[k][c], a.R[(size_t)(start + k) * a.ldr + gl], dot);
-        } else {
-            for (int cc = 0; cc < S; ++cc) {
-                const int i = line0 + cc, j = start + c;
-                if (i < a.nlines && c < len) dot = fma(tile[c][cc], a.R[(size_t)i * a.ldr + j], dot);
+        const int t = threadIdx.x, lo = t % S, hi = t / S;
+        for (int k = hi; k < S; k += NT / S) {
+            if (DIR == DIR_COL) {
+                const int i = start + k, j = line0 + lo;
+                if (k < len && j < a.nlines) dot = fma(tile[k][lo], a.R[(size_t)i * a.ldr + j], dot);
+            } else {
+                const int i = line0 + k, j = start + lo;
+                if (i < a.nlines && lo < len) dot = fma(tile[lo][k], a.R[(size_t)i * a.ldr + j], dot);
             }
         }
-        __shared__ double sh[S / 32];
-        const double part = block_sum<S>(dot, sh);
+        __shared__ double sh[NT / 32];
+        const double part = block_sum<NT>(dot, sh);
         const unsigned nblk = gridDim.x * gridDim.y;
         if (threadIdx.x == 0) a.partials[blockIdx.y * gridDim.x + blockIdx.x] = part;
         if (arrive_last(a.counter, nblk)) {
-            const double tot = sum_partials<S>(a.partials, nblk, 1, sh);
+            const double tot = sum_partials<NT>(a.partials, nblk, 1, sh);
             if (threadIdx.x == 0) {
                 *a.counter = 0;
                 if (a.pcg != nullptr) a.pcg->rz_next = tot;
@@ -180,34 +184,51 @@ __global__ void __launch_bounds__(S) seg_tile_kernel(SegArgs a) {
 
 // Boundary scans: one thread per line, P sequential steps of a b x b update.
 template <int B, int DIR, bool FWD>
-__global__ void __launch_bounds__(128) seg_scan_kernel(const double* X, int ld, int n, int nlines, int P,
+__global__ void __launch_bounds__(64) seg_scan_kernel(const double* X, int ld, int n, int nlines, int P,
                                                        const double* T, double* sv, const PcgState* pcg) {
+    SFB_PDL_PROLOGUE();
     if (pcg != nullptr && pcg->status != SFB_PCG_RUNNING) return;
     const int gl = blockIdx.x * blockDim.x + threadIdx.x;
     if (gl >= nlines) return;
     double s[B > 0 ? B : 1];
     #pragma unroll
     for (int d = 0; d < B; ++d) s[d] = 0.0;
-    for (int step = 0; step < P; ++step) {
-        const int p = FWD ? step : P - 1 - step;
-        const int start = p * S, end = min(n, start + S);
+    constexpr int CH = 8;  // boundary values prefetched per chunk (independent of the state chain)
+    constexpr int BB = B > 0 ? B : 1;
+    for (int s0 = 0; s0 < P; s0 += CH) {
+        double tail[CH][BB];
         #pragma unroll
-        for (int d = 0; d < B; ++d) sv[((size_t)p * B + d) * nlines + gl] = s[d];
-        // next state: forward -> last B values up to `end`; backward -> first B values from `start`
-        double nx[B > 0 ? B : 1];
-        const double* Tp = T + (size_t)p * B * B;
-        #pragma unroll
-        for (int d = 0; d < B; ++d) {
-            const int r = FWD ? end - B + d : start + d;
-            const bool inside = FWD ? r >= start : r < end;
-            double v = 0.0;
-            if (inside) v = DIR == DIR_COL ? X[(size_t)r * ld + gl] : X[(size_t)gl * ld + r];
+        for (int u = 0; u < CH; ++u) {
+            const int step = s0 + u;
+            const int p = FWD ? step : P - 1 - step;
+            const int start = p * S, end = min(n, start + S);
             #pragma unroll
-            for (int e = 0; e < B; ++e) v = fma(Tp[d * B + e], s[e], v);
-            nx[d] = v;
+            for (int d = 0; d < B; ++d) {
+                const int r = FWD ? end - B + d : start + d;
+                const bool inside = step < P && (FWD ? r >= start : r < end);
+                tail[u][d] = inside ? (DIR == DIR_COL ? X[(size_t)r * ld + gl] : X[(size_t)gl * ld + r]) : 0.0;
+            }
         }
         #pragma unroll
-        for (int d = 0; d < B; ++d) s[d] = nx[d];
+        for (int u = 0; u < CH; ++u) {
+            const int step = s0 + u;
+            if (step >= P) break;
+            const int p = FWD ? step : P - 1 - step;
+            #pragma unroll
+            for (int d = 0; d < B; ++d) sv[((size_t)p * B + d) * nlines + gl] = s[d];
+            // next state: forward -> last B values of segment p; backward -> first B values
+            double nx[BB];
+            const double* Tp = T + (size_t)p * B * B;
+            #pragma unroll
+            for (int d = 0; d < B; ++d) {
+                double v = tail[u][d];
+                #pragma unroll
+                for (int e = 0; e < B; ++e) v = fma(Tp[d * B + e], s[e], v);
+                nx[d] = v;
+            }
+            #pragma unroll
+            for (int d = 0; d < B; ++d) s[d] = nx[d];
+        }
     }
 }
 
@@ -229,17 +250,17 @@ int run_factor(const SegFactor& f, int DIR, const double* Xin, int ldi, double* 
     a.pcg = const_cast<PcgState*>(pcg_gate);
     const int P = (f.n + S - 1) / S;
     const dim3 grid(P, (nlines + S - 1) / S);
-    const int sb = (nlines + 127) / 128;
+    const int sb = (nlines + 63) / 64;
     if (DIR == DIR_COL) {
-        seg_tile_kernel<B, DIR_COL, PH_FWD><<<grid, S, 0, s>>>(a);
-        seg_scan_kernel<B, DIR_COL, true><<<sb, 128, 0, s>>>(X, ld, f.n, nlines, P, f.Tf, sv_f, pcg_gate);
-        seg_tile_kernel<B, DIR_COL, PH_FIX_BWD><<<grid, S, 0, s>>>(a);
-        seg_scan_kernel<B, DIR_COL, false><<<sb, 128, 0, s>>>(X, ld, f.n, nlines, P, f.Tb, sv_b, pcg_gate);
+        SFB_TRY(launch_kernel(seg_tile_kernel<B, DIR_COL, PH_FWD>, dim3(grid), dim3(NT), 0, s, a));
+        SFB_TRY(launch_kernel(seg_scan_kernel<B, DIR_COL, true>, dim3(sb), dim3(64), 0, s, X, ld, f.n, nlines, P, f.Tf, sv_f, pcg_gate));
+        SFB_TRY(launch_kernel(seg_tile_kernel<B, DIR_COL, PH_FIX_BWD>, dim3(grid), dim3(NT), 0, s, a));
+        SFB_TRY(launch_kernel(seg_scan_kernel<B, DIR_COL, false>, dim3(sb), dim3(64), 0, s, X, ld, f.n, nlines, P, f.Tb, sv_b, pcg_gate));
     } else {
-        seg_tile_kernel<B, DIR_ROW, PH_FWD><<<grid, S, 0, s>>>(a);
-        seg_scan_kernel<B, DIR_ROW, true><<<sb, 128, 0, s>>>(X, ld, f.n, nlines, P, f.Tf, sv_f, pcg_gate);
-        seg_tile_kernel<B, DIR_ROW, PH_FIX_BWD><<<grid, S, 0, s>>>(a);
-        seg_scan_kernel<B, DIR_ROW, false><<<sb, 128, 0, s>>>(X, ld, f.n, nlines, P, f.Tb, sv_b, pcg_gate);
+        SFB_TRY(launch_kernel(seg_tile_kernel<B, DIR_ROW, PH_FWD>, dim3(grid), dim3(NT), 0, s, a));
+        SFB_TRY(launch_kernel(seg_scan_kernel<B, DIR_ROW, true>, dim3(sb), dim3(64), 0, s, X, ld, f.n, nlines, P, f.Tf, sv_f, pcg_gate));
+        SFB_TRY(launch_kernel(seg_tile_kernel<B, DIR_ROW, PH_FIX_BWD>, dim3(grid), dim3(NT), 0, s, a));
+        SFB_TRY(launch_kernel(seg_scan_kernel<B, DIR_ROW, false>, dim3(sb), dim3(64), 0, s, X, ld, f.n, nlines, P, f.Tb, sv_b, pcg_gate));
     }
     if (dot != nullptr) {
         a.R = dot->R;
@@ -250,9 +271,9 @@ int run_factor(const SegFactor& f, int DIR, const double* Xin, int ldi, double* 
         a.dot_out = dot->dot_out;
     }
     if (DIR == DIR_COL)
-        seg_tile_kernel<B, DIR_COL, PH_FIX><<<grid, S, 0, s>>>(a);
+        SFB_TRY(launch_kernel(seg_tile_kernel<B, DIR_COL, PH_FIX>, dim3(grid), dim3(NT), 0, s, a));
     else
-        seg_tile_kernel<B, DIR_ROW, PH_FIX><<<grid, S, 0, s>>>(a);
+        SFB_TRY(launch_kernel(seg_tile_kernel<B, DIR_ROW, PH_FIX>, dim3(grid), dim3(NT), 0, s, a));
     SFB_CHECK_LAUNCH();
     return SFB_OK;
 }

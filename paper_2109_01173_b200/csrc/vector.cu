@@ -12,13 +12,14 @@
 // partial per CTA, summed in fixed order by the last CTA to finish.
 #include "sfb_common.cuh"
 #include "sfb_kernels.cuh"
+#include "sfb_launch.cuh"
 
 namespace sfb {
 
 namespace {
 
 constexpr int VT = 256;
-constexpr int VB = 2 * kNumSMs;
+constexpr int VB = 8 * kNumSMs;  // full occupancy: enough bytes in flight for HBM
 
 #define ROW_LOOP(rows, cols)                                         \
     for (int r = blockIdx.x; r < (rows); r += gridDim.x)            \
@@ -46,21 +47,38 @@ __device__ __forceinline__ void pcg_finish_update(PcgState* st, double rr, doubl
     }
 }
 
-__global__ void __launch_bounds__(VT) pcg_update_kernel(double* U, double* R, const double* W, const double* Q0,
+__global__ void __launch_bounds__(VT) pcg_update_kernel(double* __restrict__ U, double* __restrict__ R,
+                                                        const double* __restrict__ W, const double* Q0,
                                                         const double* Q1, int ld, int rows, int cols,
                                                         double* partials, PcgState* st, double* hist,
                                                         double* incs) {
+    SFB_PDL_PROLOGUE();
     if (st->status != SFB_PCG_RUNNING) return;
     const int s = st->iter;
     const double alpha = st->alpha;
     const double* Q = (s & 1) ? Q1 : Q0;
     double rr = 0.0;
-    ROW_LOOP(rows, cols) {
-        const size_t o = (size_t)r * ld + cc;
-        U[o] = __dadd_rn(U[o], __dmul_rn(alpha, Q[o]));  // U += alpha Q
-        const double rv = __dsub_rn(R[o], __dmul_rn(alpha, W[o]));  // R -= alpha W
-        R[o] = rv;
-        rr = fma(rv, rv, rr);
+    // The solver's buffers are rows x ld with zero padding columns that every
+    // kernel leaves at zero, so the update runs over the flat padded array in
+    // 16-byte vectors (the padding contributes exactly 0 to |R|^2).
+    const size_t n2 = (size_t)rows * ld / 2;
+    double2* U2 = reinterpret_cast<double2*>(U);
+    double2* R2 = reinterpret_cast<double2*>(R);
+    const double2* Q2 = reinterpret_cast<const double2*>(Q);
+    const double2* W2 = reinterpret_cast<const double2*>(W);
+    (void)cols;
+    #pragma unroll 2
+    for (size_t i = (size_t)blockIdx.x * VT + threadIdx.x; i < n2; i += (size_t)gridDim.x * VT) {
+        const double2 q = __ldg(Q2 + i), wv = __ldg(W2 + i);
+        double2 u = U2[i], rv = R2[i];
+        u.x = __dadd_rn(u.x, __dmul_rn(alpha, q.x));  // U += alpha Q
+        u.y = __dadd_rn(u.y, __dmul_rn(alpha, q.y));
+        rv.x = __dsub_rn(rv.x, __dmul_rn(alpha, wv.x));  // R -= alpha W
+        rv.y = __dsub_rn(rv.y, __dmul_rn(alpha, wv.y));
+        U2[i] = u;
+        R2[i] = rv;
+        rr = fma(rv.x, rv.x, rr);
+        rr = fma(rv.y, rv.y, rr);
     }
     __shared__ double sh[VT / 32];
     const double p = block_sum<VT>(rr, sh);
@@ -84,6 +102,7 @@ __device__ __forceinline__ void pcg_finish_init(PcgState* st, double rr, double*
 __global__ void __launch_bounds__(VT) pcg_init_plain_kernel(const double* rhs, int ldr, double* R, double* U,
                                                             int ld, int rows, int cols, double* partials,
                                                             PcgState* st, double* hist) {
+    SFB_PDL_PROLOGUE();
     double rr = 0.0;
     ROW_LOOP(rows, cols) {
         const double v = rhs[(size_t)r * ldr + cc];
@@ -106,6 +125,7 @@ __global__ void __launch_bounds__(VT) pcg_init_plain_kernel(const double* rhs, i
 __global__ void __launch_bounds__(VT) pcg_init_warm_kernel(const double* rhs, int ldr, const double* W, double* R,
                                                            int ld, int rows, int cols, double* partials,
                                                            PcgState* st, double* hist) {
+    SFB_PDL_PROLOGUE();
     double rr = 0.0;
     ROW_LOOP(rows, cols) {
         const double v = __dsub_rn(rhs[(size_t)r * ldr + cc], W[(size_t)r * ld + cc]);  // R = rhs - op(U)
@@ -126,6 +146,7 @@ __global__ void __launch_bounds__(VT) pcg_init_warm_kernel(const double* rhs, in
 
 __global__ void __launch_bounds__(VT) pcg_direction_kernel(const double* Z, double* Q0, double* Q1, int ld,
                                                            int rows, int cols, PcgState* st) {
+    SFB_PDL_PROLOGUE();
     if (st->status != SFB_PCG_RUNNING) return;
     const int s = st->iter;
     const double beta = s > 0 ? st->rz_next / st->rz : 0.0;
@@ -139,6 +160,7 @@ __global__ void __launch_bounds__(VT) pcg_direction_kernel(const double* Z, doub
 
 __global__ void __launch_bounds__(VT) pcg_dots_kernel(const double* W, const double* Q0, const double* Q1, int ld,
                                                       int rows, int cols, double* partials, PcgState* st) {
+    SFB_PDL_PROLOGUE();
     if (st->status != SFB_PCG_RUNNING) return;
     const int s = st->iter;
     const double* Q = (s & 1) ? Q1 : Q0;
@@ -176,6 +198,7 @@ __global__ void __launch_bounds__(VT) pcg_dots_kernel(const double* W, const dou
 
 __global__ void __launch_bounds__(VT) pcg_record_kernel(const double* U, int ld, int rows, int cols,
                                                         double* iterates, PcgState* st) {
+    SFB_PDL_PROLOGUE();
     // record_iterates (solvers.py:441-442): copy U_s once per completed iteration
     const int it = st->iter;
     if (it >= st->n_iterates || st->recorded >= it) return;
@@ -193,6 +216,7 @@ __global__ void __launch_bounds__(VT) pcg_record_kernel(const double* U, int ld,
 __global__ void __launch_bounds__(VT) copy_dot_kernel(const double* R, double* Z, int ld, int rows, int cols,
                                                       double* partials, PcgState* st, double* dot_out,
                                                       unsigned* counter) {
+    SFB_PDL_PROLOGUE();
     if (st != nullptr && st->status != SFB_PCG_RUNNING) return;
     double zr = 0.0;
     ROW_LOOP(rows, cols) {
@@ -215,6 +239,7 @@ __global__ void __launch_bounds__(VT) copy_dot_kernel(const double* R, double* Z
 }
 
 __global__ void loop_ctl_kernel(PcgState* st, cudaGraphConditionalHandle handle, int use_handle) {
+    SFB_PDL_PROLOGUE();
     // continue while running and below max_iter; the body counter is a hard
     // backstop so a logic error can never spin the device forever.
     const unsigned runs = ++st->counter[6];
@@ -225,6 +250,7 @@ __global__ void loop_ctl_kernel(PcgState* st, cudaGraphConditionalHandle handle,
 
 __global__ void __launch_bounds__(VT) norms_kernel(const double* A, int lda, const double* B, int ldb, int rows,
                                                    int cols, double* partials, RedSlots* out) {
+    SFB_PDL_PROLOGUE();
     // v = { |A - B|, max|A| (finite entries), #non-finite(A), |A| }
     double d2 = 0.0, a2 = 0.0, mx = 0.0, bad = 0.0;
     ROW_LOOP(rows, cols) {
@@ -273,6 +299,7 @@ __global__ void __launch_bounds__(VT) norms_kernel(const double* A, int lda, con
 __global__ void __launch_bounds__(VT) sh_update_kernel(double* U, double* R, const double* Q, const double* W, int ld,
                                                        int rows, int cols, double alpha, double* partials,
                                                        RedSlots* out) {
+    SFB_PDL_PROLOGUE();
     double rr = 0.0;
     ROW_LOOP(rows, cols) {
         const size_t o = (size_t)r * ld + cc;
@@ -295,6 +322,7 @@ __global__ void __launch_bounds__(VT) sh_update_kernel(double* U, double* R, con
 
 __global__ void __launch_bounds__(VT) sh_xpby_kernel(double* Q, int ldq, const double* Z, int ldz, int rows, int cols,
                                                      double beta, int first) {
+    SFB_PDL_PROLOGUE();
     ROW_LOOP(rows, cols) {
         const double z = Z[(size_t)r * ldz + cc];
         double* q = Q + (size_t)r * ldq + cc;
@@ -305,6 +333,7 @@ __global__ void __launch_bounds__(VT) sh_xpby_kernel(double* Q, int ldq, const d
 __global__ void __launch_bounds__(VT) sh_dots_kernel(const double* A, const double* B, const double* C,
                                                      const double* D, int ld, int rows, int cols, double* partials,
                                                      RedSlots* out) {
+    SFB_PDL_PROLOGUE();
     double ab = 0.0, cd = 0.0;
     ROW_LOOP(rows, cols) {
         const size_t o = (size_t)r * ld + cc;
@@ -335,28 +364,28 @@ int vector_grid_blocks() { return VB; }
 
 int launch_pcg_init_plain(const double* rhs, int ldr, double* R, double* U, int ld, int rows, int cols,
                           double* partials, PcgState* st, double* hist, cudaStream_t s) {
-    pcg_init_plain_kernel<<<VB, VT, 0, s>>>(rhs, ldr, R, U, ld, rows, cols, partials, st, hist);
+    SFB_TRY(launch_kernel(pcg_init_plain_kernel, dim3(VB), dim3(VT), 0, s, rhs, ldr, R, U, ld, rows, cols, partials, st, hist));
     SFB_CHECK_LAUNCH();
     return SFB_OK;
 }
 
 int launch_pcg_init_warm(const double* rhs, int ldr, const double* W, double* R, int ld, int rows, int cols,
                          double* partials, PcgState* st, double* hist, cudaStream_t s) {
-    pcg_init_warm_kernel<<<VB, VT, 0, s>>>(rhs, ldr, W, R, ld, rows, cols, partials, st, hist);
+    SFB_TRY(launch_kernel(pcg_init_warm_kernel, dim3(VB), dim3(VT), 0, s, rhs, ldr, W, R, ld, rows, cols, partials, st, hist));
     SFB_CHECK_LAUNCH();
     return SFB_OK;
 }
 
 int launch_pcg_direction(const double* Z, double* Q0, double* Q1, int ld, int rows, int cols, PcgState* st,
                          cudaStream_t s) {
-    pcg_direction_kernel<<<VB, VT, 0, s>>>(Z, Q0, Q1, ld, rows, cols, st);
+    SFB_TRY(launch_kernel(pcg_direction_kernel, dim3(VB), dim3(VT), 0, s, Z, Q0, Q1, ld, rows, cols, st));
     SFB_CHECK_LAUNCH();
     return SFB_OK;
 }
 
 int launch_pcg_dots(const double* W, const double* Q0, const double* Q1, int ld, int rows, int cols,
                     double* partials, PcgState* st, cudaStream_t s) {
-    pcg_dots_kernel<<<VB, VT, 0, s>>>(W, Q0, Q1, ld, rows, cols, partials, st);
+    SFB_TRY(launch_kernel(pcg_dots_kernel, dim3(VB), dim3(VT), 0, s, W, Q0, Q1, ld, rows, cols, partials, st));
     SFB_CHECK_LAUNCH();
     return SFB_OK;
 }
@@ -364,14 +393,14 @@ int launch_pcg_dots(const double* W, const double* Q0, const double* Q1, int ld,
 int launch_pcg_update(double* U, double* R, const double* W, const double* Q0, const double* Q1, int ld,
                       int rows, int cols, double* partials, PcgState* st, double* hist, double* incs,
                       cudaStream_t s) {
-    pcg_update_kernel<<<VB, VT, 0, s>>>(U, R, W, Q0, Q1, ld, rows, cols, partials, st, hist, incs);
+    SFB_TRY(launch_kernel(pcg_update_kernel, dim3(VB), dim3(VT), 0, s, U, R, W, Q0, Q1, ld, rows, cols, partials, st, hist, incs));
     SFB_CHECK_LAUNCH();
     return SFB_OK;
 }
 
 int launch_pcg_record(const double* U, int ld, int rows, int cols, double* iterates, PcgState* st,
                       cudaStream_t s) {
-    pcg_record_kernel<<<VB, VT, 0, s>>>(U, ld, rows, cols, iterates, st);
+    SFB_TRY(launch_kernel(pcg_record_kernel, dim3(VB), dim3(VT), 0, s, U, ld, rows, cols, iterates, st));
     SFB_CHECK_LAUNCH();
     return SFB_OK;
 }
@@ -380,41 +409,41 @@ int launch_copy_dot(const double* R, double* Z, int ld, int rows, int cols, doub
                     RedSlots* red, cudaStream_t s) {
     unsigned* counter = st ? &st->counter[3] : &red->counter[1];
     double* dot_out = red ? &red->v[3] : nullptr;
-    copy_dot_kernel<<<VB, VT, 0, s>>>(R, Z, ld, rows, cols, partials, st, dot_out, counter);
+    SFB_TRY(launch_kernel(copy_dot_kernel, dim3(VB), dim3(VT), 0, s, R, Z, ld, rows, cols, partials, st, dot_out, counter));
     SFB_CHECK_LAUNCH();
     return SFB_OK;
 }
 
 int launch_loop_ctl(PcgState* st, unsigned long long handle, int use_handle, cudaStream_t s) {
-    loop_ctl_kernel<<<1, 1, 0, s>>>(st, (cudaGraphConditionalHandle)handle, use_handle);
+    SFB_TRY(launch_kernel(loop_ctl_kernel, dim3(1), dim3(1), 0, s, st, (cudaGraphConditionalHandle)handle, use_handle));
     SFB_CHECK_LAUNCH();
     return SFB_OK;
 }
 
 int launch_norms(const double* A, int lda, const double* B, int ldb, int rows, int cols, double* partials,
                  RedSlots* out, cudaStream_t s) {
-    norms_kernel<<<VB, VT, 0, s>>>(A, lda, B, ldb, rows, cols, partials, out);
+    SFB_TRY(launch_kernel(norms_kernel, dim3(VB), dim3(VT), 0, s, A, lda, B, ldb, rows, cols, partials, out));
     SFB_CHECK_LAUNCH();
     return SFB_OK;
 }
 
 int launch_sh_update(double* U, double* R, const double* Q, const double* W, int ld, int rows, int cols,
                      double alpha, double* partials, RedSlots* out, cudaStream_t s) {
-    sh_update_kernel<<<VB, VT, 0, s>>>(U, R, Q, W, ld, rows, cols, alpha, partials, out);
+    SFB_TRY(launch_kernel(sh_update_kernel, dim3(VB), dim3(VT), 0, s, U, R, Q, W, ld, rows, cols, alpha, partials, out));
     SFB_CHECK_LAUNCH();
     return SFB_OK;
 }
 
 int launch_sh_xpby(double* Q, int ldq, const double* Z, int ldz, int rows, int cols, double beta, int first,
                    cudaStream_t s) {
-    sh_xpby_kernel<<<VB, VT, 0, s>>>(Q, ldq, Z, ldz, rows, cols, beta, first);
+    SFB_TRY(launch_kernel(sh_xpby_kernel, dim3(VB), dim3(VT), 0, s, Q, ldq, Z, ldz, rows, cols, beta, first));
     SFB_CHECK_LAUNCH();
     return SFB_OK;
 }
 
 int launch_sh_dots(const double* A, const double* B, const double* C, const double* D, int ld, int rows, int cols,
                    double* partials, RedSlots* out, cudaStream_t s) {
-    sh_dots_kernel<<<VB, VT, 0, s>>>(A, B, C, D, ld, rows, cols, partials, out);
+    SFB_TRY(launch_kernel(sh_dots_kernel, dim3(VB), dim3(VT), 0, s, A, B, C, D, ld, rows, cols, partials, out));
     SFB_CHECK_LAUNCH();
     return SFB_OK;
 }
