@@ -59,6 +59,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-alt", action="store_true", help="skip the banded-preconditioner (f1) measurement")
+    ap.add_argument("--no-full", action="store_true", help="skip the full solve to 1e-8 (time to solution)")
     return ap.parse_args()
 
 
@@ -296,6 +297,22 @@ def run_native(args):
                          "note": "SURVEY §8 f1: same preconditioner P_L U P_R applied by segmented banded "
                                  "Cholesky solves instead of dense-inverse GEMMs (parity-neutral)"}
 
+    # ---- time to solution: the full cfg3 solve to the BASELINE tolerance 1e-8 ----
+    tts = None
+    if world == 1 and not args.no_full:
+        tts = {}
+        modes = [args.precond_mode] + ([] if args.no_alt or args.precond_mode == "banded" else ["banded"])
+        for mode in modes:
+            p_full = pre if mode == args.precond_mode else pre_b
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
+            rf = pb.mo_pcg(op, rhs_d, precond=p_full, stop=pb.relative_residual(1e-8), max_iter=100000)
+            torch.cuda.synchronize()
+            dt_full = time.perf_counter() - t1
+            tts[mode] = {"seconds": dt_full, "iterations": rf.iterations, "stop_reason": rf.stop_reason,
+                         "final_relative_residual": float(rf.residual_history[-1] / rf.residual_history[0]),
+                         "dof_it_per_s": qy * qx * rf.iterations / dt_full}
+
     # ---- roofline of the dominant kernel: the DMMA GEMM (q x q x q) ----
     L = nat.lib()
     ldq = qy + (qy % 2)
@@ -394,6 +411,7 @@ def run_native(args):
             "gpu_launches": per_step_launches * args.steps,
             "clocks": clk,
             "alt_preconditioner": alt or None,
+            "time_to_solution": tts,
         }
         print(json.dumps(line), flush=True)
     if dist is not None:
