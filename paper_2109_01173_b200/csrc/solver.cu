@@ -945,7 +945,8 @@ int sfb_pre_destroy(sfb_pre* p) {
 int sfb_pcg_create(const sfb_op* op, const sfb_pre* pre, sfb_pcg** out) {
     if (!op || !pre) return arg_error("mo_pcg needs an operator and a preconditioner");
     if (op->qy != pre->qy || op->qx != pre->qx) return arg_error("preconditioner shape does not match operator");
-    if (pre->kind == SFB_PRE_SPECTRAL_SUM) return arg_error("the reduced-solve sandwich is not a preconditioner");
+    // SFB_PRE_SPECTRAL_SUM is accepted: the exact inverse of a two-term SPD
+    // operator is a valid (opt-in) MO-PCG preconditioner.
     auto* s = new sfb_pcg;
     s->op = op;
     s->pre = pre;

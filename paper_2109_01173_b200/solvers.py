@@ -293,6 +293,60 @@ class Preconditioner:
 IDENTITY_PRECONDITIONER = "identity"
 
 
+class TwoTermPreconditioner:
+    """Opt-in preconditioner P(U) = G1 U H1 + G2 U H2 applied exactly in the
+    spectral space of its two pencils (the north star's
+    "(lambda_i + mu_j)" form): Z = P1 [(P1^T R P2) / (lam1_i + lam2_j)] P2^T,
+    the same 4-GEMM DMMA sandwich as ``solve_reduced``.
+
+    This is NOT the reference's preconditioner (which is a single Kronecker
+    term, solvers.py:103-196): it changes MO-PCG iteration counts, so it is
+    judged on converged-solution parity only.  For a two-term operator it is
+    the exact inverse (one iteration)."""
+
+    mode = "two-term-spectral"
+    is_identity = False
+    left = right = None
+
+    def __init__(self, terms, left_name: str = "two-term", right_name: str = "(lam_i+mu_j)"):
+        self._op = SylvesterOperator(terms, symmetric=True, positive_definite=True)
+        if len(self._op) != 2:
+            raise SolverError(f"two-term preconditioner needs two nonzero terms, got {len(self._op)}")
+        self.cache = build_spectral_cache(self._op)
+        self.cache.check_pencils()
+        self.shape = self._op.shape
+        self.left_name, self.right_name = left_name, right_name
+
+    def native(self, shape=None):
+        if shape is not None and tuple(shape) != self.shape:
+            raise OperatorError(f"grid shape {tuple(shape)} does not match preconditioner {self.shape}")
+        return self.cache.native()
+
+    def apply(self, U):
+        return self._op.apply(U)
+
+    def apply_inverse(self, U):
+        on_dev = nat.is_device(U)
+        t = nat.torch()
+        Ud = nat.to_device(U)
+        qy, qx = Ud.shape
+        if (qy, qx) != self.shape:
+            raise OperatorError(f"grid shape {(qy, qx)} does not match preconditioner {self.shape}")
+        Z = t.empty_like(Ud)
+        nat.check(nat.lib().sfb_pre_apply(self.native(), nat.ptr(Ud), qx, nat.ptr(Z), qx, nat.stream()),
+                  "apply_inverse")
+        return Z if on_dev else Z.cpu().numpy()
+
+
+def two_term_preconditioner(op: SylvesterOperator, which=(0, 1)) -> TwoTermPreconditioner:
+    """The two-term spectral preconditioner built from terms ``which`` of an
+    operator (reference term order, operators.py:198-204 / 272-278): for the
+    general elliptic operator (M1, A) + (B1 + gamma M3, M), for the parabolic
+    one (M3 + c B1, M) + (c M1, A); exact for two-term operators."""
+    terms = [op.terms[i] for i in which]
+    return TwoTermPreconditioner(terms)
+
+
 def make_preconditioner(kind: str, x: DirectionSet, y: DirectionSet, *, d_u: float = 1.0,
                         tau: float = 0.0, lumped: bool = False, mode: str | None = None) -> Preconditioner:
     """Named single-term preconditioners (solvers.py:156-196)."""

@@ -27,7 +27,8 @@ from .fem1d import BCKind, DirectionSet
 from .geometry import DomainSpec
 from .models import DIBKinetics
 from .operators import expand_with_boundary, full_node_grid, parabolic_operator
-from .solvers import Preconditioner, make_preconditioner, mo_pcg, relative_residual, timestep_residual
+from .solvers import (Preconditioner, make_preconditioner, mo_pcg, relative_residual, timestep_residual,
+                      two_term_preconditioner)
 
 BLOWUP_LIMIT = 1e100
 
@@ -109,13 +110,16 @@ def _step_setup(inner: InnerSolver):
                           "the B200 solve path uses mo-pcg")
 
 
-def _parabolic_precond(x, y, d_u, tau, lumped, inner: InnerSolver):
-    """timestepping.py:115-123."""
+def _parabolic_precond(x, y, d_u, tau, lumped, inner: InnerSolver, op=None):
+    """timestepping.py:115-123; ``precond="two_term"`` selects the opt-in
+    spectral preconditioner of SURVEY §8 f3 built from the step operator."""
     name = inner.precond
     if name == "auto":
         name = "parabolic_lumped" if lumped else "parabolic"
     if name == "identity":
         return Preconditioner()
+    if name == "two_term":
+        return two_term_preconditioner(op)
     return make_preconditioner(name, x, y, d_u=d_u, tau=tau, lumped=lumped, mode=inner.precond_mode)
 
 
@@ -150,7 +154,7 @@ def imex_euler_heat(domain: DomainSpec, x: DirectionSet, y: DirectionSet, d_u: f
     _step_setup(inner)
     tau = grid.tau
     op, rhs_of = parabolic_operator(x, y, d_u, tau, lumped=lumped)
-    pre = _parabolic_precond(x, y, d_u, tau, lumped, inner)
+    pre = _parabolic_precond(x, y, d_u, tau, lumped, inner, op)
     stop = inner.stopping(tau)
     X = Y = None
     F = None
@@ -202,8 +206,8 @@ def imex_euler_rds(domain: DomainSpec, x: DirectionSet, y: DirectionSet, d_u: fl
     op_u, rhs_of = parabolic_operator(x, y, d_u, tau, lumped=lumped)
     op_v, _ = parabolic_operator(x, y, d_v, tau, lumped=lumped)
     stop = inner.stopping(tau)
-    pre_u = _parabolic_precond(x, y, d_u, tau, lumped, inner)
-    pre_v = _parabolic_precond(x, y, d_v, tau, lumped, inner)
+    pre_u = _parabolic_precond(x, y, d_u, tau, lumped, inner, op_u)
+    pre_v = _parabolic_precond(x, y, d_v, tau, lumped, inner, op_v)
     device_kin = isinstance(kinetics, DIBKinetics)
     kp = kinetics.params.device_params() if device_kin else None
     U = nat.to_device(state0[0]).clone()

@@ -1,0 +1,69 @@
+"""GPU tests of the SURVEY §8 f rows (beyond the reference's own algorithm).
+
+f1 (banded preconditioner) is parity-neutral and already runs through every
+MO-PCG parity test in tests/test_gpu_parity.py; here: f3, the two-term
+spectral preconditioner, which changes iteration counts and is therefore
+judged on converged-solution parity against the oracle."""
+
+import numpy as np
+import pytest
+
+import oracle as orc
+import paper_2109_01173_b200 as pb
+from _cases import sine_source
+from conftest import relerr
+from test_host_logic import WAVE
+
+pytestmark = pytest.mark.gpu
+
+D, NB = pb.BCKind.DIRICHLET, pb.BCKind.NEUMANN
+
+
+@pytest.mark.parametrize("N", [16, 48])
+def test_two_term_preconditioner_converges_to_reference_solution(N):
+    x, y = pb.build_direction_sets(WAVE, 2, N, D)
+    op, rhs_of = pb.elliptic_operator(x, y, 1.0)
+    rhs = rhs_of(sine_source(N, N, 3))
+    pre2 = pb.two_term_preconditioner(op)
+    rep2 = pb.mo_pcg(op, rhs, precond=pre2, stop=pb.relative_residual(1e-12), max_iter=5000)
+    pre1 = pb.make_preconditioner("elliptic_xnormal", x, y)
+    rep1 = pb.mo_pcg(op, rhs, precond=pre1, stop=pb.relative_residual(1e-12), max_iter=5000)
+    # oracle: the reference's own (single-term LU) MO-PCG at the same tolerance
+    ox, oy = orc.direction_sets(orc.wave_domain(), 2, N, orc.DIRICHLET)
+    terms, _ = orc.elliptic_terms(ox, oy, 1.0)
+    opre = orc.LUPrecond(*orc.precond_factors("elliptic_xnormal", ox, oy))
+    ref = orc.mo_pcg(terms, rhs, opre.inverse, ("residual", 1e-12), max_iter=5000)
+    assert rep2.stop_reason == "tolerance"
+    assert relerr(rep2.solution, ref["solution"]) <= 1e-10
+    # the point of f3: far fewer iterations, independent of N
+    assert rep2.iterations < rep1.iterations / 4
+    assert rep2.diagnostics["device"]["precond_mode"] == "two-term-spectral"
+
+
+def test_two_term_preconditioner_is_exact_for_two_term_operators():
+    # cfg5-type lumped parabolic operator on the square has exactly two terms
+    x, y = pb.build_direction_sets(pb.SQUARE, 1, 31, NB, lumped=True)
+    op, _ = pb.parabolic_operator(x, y, 20.0, 5e-3 / 400, lumped=True)
+    assert len(op) == 2
+    rhs = np.random.default_rng(3).standard_normal(op.shape)
+    rep = pb.mo_pcg(op, rhs, precond=pb.two_term_preconditioner(op), stop=pb.relative_residual(1e-12),
+                    max_iter=50)
+    assert rep.iterations <= 2
+    assert relerr(rep.solution, pb.solve_reduced(op, rhs).solution) <= 1e-10
+
+
+def test_two_term_preconditioner_in_imex_dib():
+    p = pb.dib_presets("spots_worms").replace(rho=400.0)
+    x, y = pb.build_direction_sets(pb.SQUARE, 1, 15, NB, lumped=True)
+    e0, t0 = pb.initial_fields((y.q, x.q), pb.InitialData(amplitude=2e-3, seed=5))
+    state0 = (e0 - 1e-3, t0 - 1e-3)
+    tau = 5e-3 / p.rho
+    grid = pb.TimeGrid(tau, 6 * tau)
+    kin = pb.dib_kinetics_pair(p)
+    ref = pb.imex_euler_rds(pb.SQUARE, x, y, 1.0, p.d_theta, kin, p.rho, state0, grid, lumped=True,
+                            inner=pb.InnerSolver(rule="residual", tol=1e-12, max_iter=2000))
+    two = pb.imex_euler_rds(pb.SQUARE, x, y, 1.0, p.d_theta, kin, p.rho, state0, grid, lumped=True,
+                            inner=pb.InnerSolver(rule="residual", tol=1e-12, max_iter=2000, precond="two_term"))
+    assert np.all(two.iterations <= 2)
+    assert relerr(two.final[0], ref.final[0]) <= 1e-10
+    assert relerr(two.final[1], ref.final[1]) <= 1e-10
