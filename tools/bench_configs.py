@@ -137,6 +137,37 @@ def imex(name, args):
     return line
 
 
+def full_imex(name, args):
+    """The real drivers (imex_euler_heat / imex_euler_rds) with the reference's
+    stopping rules (cfg4: |R| <= 1e-8 |R0|; cfg5: the tau rule) for
+    --imex-steps steps at full size."""
+    import torch
+    import paper_2109_01173_b200 as pb
+    from paper_2109_01173_b200 import workloads as wl
+    w = wl.CONFIGS[name](N=args.N, mode=args.mode, steps=args.imex_steps)
+    ex = w.extra
+    qy, qx = w.op.shape
+    prec = args.precond
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    if name == "cfg4":
+        inner = pb.InnerSolver(rule="residual", tol=1e-8, max_iter=100000, precond=prec, precond_mode=args.mode)
+        tr = pb.imex_euler_heat(wl.WAVE, w.x, w.y, 1.0, ex["source"], ex["u0"], ex["grid"], inner=inner)
+    else:
+        p = ex["params"]
+        inner = pb.InnerSolver(max_iter=100000, precond=prec, precond_mode=args.mode)
+        tr = pb.imex_euler_rds(pb.SQUARE, w.x, w.y, 1.0, p.d_theta, ex["kinetics"], p.rho, ex["state0"],
+                               ex["grid"], inner=inner, lumped=True)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    its = np.asarray(tr.iterations)
+    return {"workload": name, "metric": "IMEX steps, full inner solves (reference stopping rule)",
+            "steps": int(its.shape[0]), "seconds": dt, "s_per_step": dt / its.shape[0],
+            "inner_iterations": its.tolist(), "precond": prec, "precond_mode": args.mode, "q": [qy, qx],
+            "dof_it_per_s": qy * qx * float(its.sum()) / dt,
+            "increments_last": np.asarray(tr.increments)[-1].tolist()}
+
+
 def main():
     import argparse
     ap = argparse.ArgumentParser()
@@ -146,9 +177,14 @@ def main():
     ap.add_argument("--mode", default="inverse")
     ap.add_argument("--cpu", action="store_true")
     ap.add_argument("--N", type=int, default=None)
+    ap.add_argument("--imex-steps", type=int, default=0, help="run the full IMEX drivers for this many steps")
+    ap.add_argument("--precond", default="auto", help="IMEX preconditioner: auto (reference) or two_term (f3)")
     args = ap.parse_args()
     for name in args.configs:
-        line = reduced(name, args) if name in ("cfg1", "cfg2") else imex(name, args)
+        if args.imex_steps and name in ("cfg4", "cfg5"):
+            line = full_imex(name, args)
+        else:
+            line = reduced(name, args) if name in ("cfg1", "cfg2") else imex(name, args)
         print(json.dumps(line), flush=True)
 
 
