@@ -67,3 +67,17 @@ def test_two_term_preconditioner_in_imex_dib():
     assert np.all(two.iterations <= 2)
     assert relerr(two.final[0], ref.final[0]) <= 1e-10
     assert relerr(two.final[1], ref.final[1]) <= 1e-10
+
+
+def test_device_eigensolver_route_for_reduced_solves(golden):
+    from _cases import cosine_source_rect
+    from test_host_logic import RECT
+    x, y = pb.build_direction_sets(pb.SQUARE, 1, 17, D)
+    op, rhs_of = pb.elliptic_operator(x, y, 1.0)
+    c = pb.build_spectral_cache(op, eig="device")
+    assert relerr(pb.solve_reduced(op, rhs_of(sine_source(17, 17, 1)), c).solution, golden["red1/U"]) <= 1e-10
+    x, y = pb.build_direction_sets(RECT, 3, 12, NB)
+    op, rhs_of = pb.elliptic_operator(x, y, 0.5)
+    c = pb.build_spectral_cache(op, eig="device")
+    assert c.swapped
+    assert relerr(pb.solve_reduced(op, rhs_of(cosine_source_rect(12, 2)), c).solution, golden["red2/U"]) <= 1e-10
