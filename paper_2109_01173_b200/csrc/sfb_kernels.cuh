@@ -110,6 +110,11 @@ struct SegFactor {
     double* Hb = nullptr;    // [P][S][b] backward responses
     double* Tf = nullptr;    // [P][b][b] forward state transfer
     double* Tb = nullptr;    // [P][b][b] backward state transfer
+    // the same at the 16-long sub-segment level (one thread sweeps one sub-segment)
+    double* Hf16 = nullptr;
+    double* Hb16 = nullptr;
+    double* Tf16 = nullptr;
+    double* Tb16 = nullptr;
 };
 struct SegDot {
     const double* R = nullptr;
@@ -120,6 +125,7 @@ struct SegDot {
     double* dot_out = nullptr;
 };
 int seg_length();
+int seg_sub_length();
 // Solve P y = x for every line: along_rows = 0 -> lines are columns (P acts
 // from the left), 1 -> lines are rows (P acts from the right).  X may alias
 // Xin.  sv_f / sv_b: scratch of [P][b][nlines] doubles each.

@@ -151,54 +151,63 @@ inline int seg_tiles(int qy, int qx) {
 // reciprocal diagonal and b zero rows appended, the responses H of every
 // segment to unit incoming states, and the b x b state transfers T.
 int build_seg_factor(int n, int b, const double* band_host, SegFactor& f) {
-    const int S = seg_length();
-    const int P = (n + S - 1) / S;
     const int bb = std::max(b, 1);
     std::vector<double> band((size_t)(n + b) * (b + 1), 0.0);
     std::copy(band_host, band_host + (size_t)n * (b + 1), band.begin());
     auto C = [&](int i, int d) { return band[(size_t)i * (b + 1) + d]; };  // C[i][i-b+d], 1/C_ii at d=b
-    std::vector<double> Hf((size_t)P * S * bb, 0.0), Hb((size_t)P * S * bb, 0.0);
-    std::vector<double> Tf((size_t)P * bb * bb, 0.0), Tb((size_t)P * bb * bb, 0.0);
-    std::vector<double> w(bb);
-    for (int p = 0; p < P; ++p) {
-        const int start = p * S, len = std::min(S, n - start), end = start + len;
-        for (int d = 0; d < b; ++d) {
-            // forward: incoming state y_{start-b+d'} = delta(d', d)
-            std::fill(w.begin(), w.end(), 0.0);
-            w[d] = 1.0;
-            for (int k = 0; k < len; ++k) {
-                const int i = start + k;
-                double v = 0.0;
-                for (int e = 0; e < b; ++e) v -= C(i, e) * w[e];
-                v *= C(i, b);
-                for (int e = 0; e + 1 < b; ++e) w[e] = w[e + 1];
-                w[b - 1] = v;
-                Hf[((size_t)p * S + k) * bb + d] = v;
-            }
-            for (int o = 0; o < b; ++o) {
-                const int r = end - b + o;
-                Tf[((size_t)p * bb + o) * bb + d] = r >= start ? Hf[((size_t)p * S + (r - start)) * bb + d]
-                                                               : (r - (start - b) == d ? 1.0 : 0.0);
-            }
-            // backward: incoming state z_{end+e} = delta(e, d); w[e-1] = z[i+e]
-            std::fill(w.begin(), w.end(), 0.0);
-            w[d] = 1.0;
-            for (int k = len - 1; k >= 0; --k) {
-                const int i = start + k;
-                double v = 0.0;
-                for (int e = b; e >= 1; --e) v -= C(i + e, b - e) * w[e - 1];
-                v *= C(i, b);
-                for (int e = b - 1; e >= 1; --e) w[e] = w[e - 1];
-                w[0] = v;
-                Hb[((size_t)p * S + k) * bb + d] = v;
-            }
-            for (int o = 0; o < b; ++o) {
-                const int r = start + o;
-                Tb[((size_t)p * bb + o) * bb + d] = r < end ? Hb[((size_t)p * S + (r - start)) * bb + d]
-                                                           : (r - end == d ? 1.0 : 0.0);
+    // responses / transfers of segments of length S (two levels: S = 64 tiles,
+    // S = 16 sub-segments swept by one thread each)
+    auto responses = [&](int S, std::vector<double>& Hf, std::vector<double>& Hb, std::vector<double>& Tf,
+                         std::vector<double>& Tb) {
+        const int P = (n + S - 1) / S;
+        Hf.assign((size_t)P * S * bb, 0.0);
+        Hb.assign((size_t)P * S * bb, 0.0);
+        Tf.assign((size_t)P * bb * bb, 0.0);
+        Tb.assign((size_t)P * bb * bb, 0.0);
+        std::vector<double> w(bb);
+        for (int p = 0; p < P; ++p) {
+            const int start = p * S, len = std::min(S, n - start), end = start + len;
+            for (int d = 0; d < b; ++d) {
+                // forward: incoming state y_{start-b+d'} = delta(d', d)
+                std::fill(w.begin(), w.end(), 0.0);
+                w[d] = 1.0;
+                for (int k = 0; k < len; ++k) {
+                    const int i = start + k;
+                    double v = 0.0;
+                    for (int e = 0; e < b; ++e) v -= C(i, e) * w[e];
+                    v *= C(i, b);
+                    for (int e = 0; e + 1 < b; ++e) w[e] = w[e + 1];
+                    w[b - 1] = v;
+                    Hf[((size_t)p * S + k) * bb + d] = v;
+                }
+                for (int o = 0; o < b; ++o) {
+                    const int r = end - b + o;
+                    Tf[((size_t)p * bb + o) * bb + d] = r >= start ? Hf[((size_t)p * S + (r - start)) * bb + d]
+                                                                   : (r - (start - b) == d ? 1.0 : 0.0);
+                }
+                // backward: incoming state z_{end+e} = delta(e, d); w[e-1] = z[i+e]
+                std::fill(w.begin(), w.end(), 0.0);
+                w[d] = 1.0;
+                for (int k = len - 1; k >= 0; --k) {
+                    const int i = start + k;
+                    double v = 0.0;
+                    for (int e = b; e >= 1; --e) v -= C(i + e, b - e) * w[e - 1];
+                    v *= C(i, b);
+                    for (int e = b - 1; e >= 1; --e) w[e] = w[e - 1];
+                    w[0] = v;
+                    Hb[((size_t)p * S + k) * bb + d] = v;
+                }
+                for (int o = 0; o < b; ++o) {
+                    const int r = start + o;
+                    Tb[((size_t)p * bb + o) * bb + d] = r < end ? Hb[((size_t)p * S + (r - start)) * bb + d]
+                                                               : (r - end == d ? 1.0 : 0.0);
+                }
             }
         }
-    }
+    };
+    std::vector<double> Hf, Hb, Tf, Tb, Hf16, Hb16, Tf16, Tb16;
+    responses(seg_length(), Hf, Hb, Tf, Tb);
+    responses(seg_sub_length(), Hf16, Hb16, Tf16, Tb16);
     f.n = n;
     f.b = b;
     auto up = [](double** dst, const std::vector<double>& v) {
@@ -214,6 +223,10 @@ int build_seg_factor(int n, int b, const double* band_host, SegFactor& f) {
     SFB_TRY(up(&f.Hb, Hb));
     SFB_TRY(up(&f.Tf, Tf));
     SFB_TRY(up(&f.Tb, Tb));
+    SFB_TRY(up(&f.Hf16, Hf16));
+    SFB_TRY(up(&f.Hb16, Hb16));
+    SFB_TRY(up(&f.Tf16, Tf16));
+    SFB_TRY(up(&f.Tb16, Tb16));
     return SFB_OK;
 }
 
@@ -931,11 +944,7 @@ int sfb_pre_destroy(sfb_pre* p) {
     cudaFree(p->sl);
     cudaFree(p->sr);
     for (SegFactor* f : {&p->fl, &p->fr}) {
-        cudaFree(f->band);
-        cudaFree(f->Hf);
-        cudaFree(f->Hb);
-        cudaFree(f->Tf);
-        cudaFree(f->Tb);
+        for (double* a : {f->band, f->Hf, f->Hb, f->Tf, f->Tb, f->Hf16, f->Hb16, f->Tf16, f->Tb16}) cudaFree(a);
     }
     delete p;
     return SFB_OK;
