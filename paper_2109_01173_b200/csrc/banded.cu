@@ -5,151 +5,302 @@
 // 281-282).  All FEM factors are banded with half-bandwidth <= k (SURVEY
 // App. B), so each output element needs a (W x W) window of X.
 //
-// One CTA owns a TY x TX output tile.  It stages the (TY+W-1) x (TX+W-1)
-// halo of X in shared memory (applying an input transform on the way in:
-// the MO-PCG direction update Q = Z + beta Q, the IMEX heat source, or the
-// DIB kinetics), keeps the right-factor band of its column in registers and
-// sweeps down the halo rows: Y_t(r) = sum_e X[r][c+e] h_t[e] is formed once
+// One CTA owns a TX-column strip of RY output rows (RY sized so the grid is
+// one wave of ~3 CTAs per SM).  It streams the (RY+W-1) x (TX+W-1) input
+// halo down the strip in chunks of CH rows through a 3-stage TMA ring (one
+// thread issues the boxes; out-of-bounds rows/columns arrive zero-filled),
+// together with the left-factor coefficients of those rows, read as a box
+// of the row-skewed copy gskew[t][j][d] = G_t[j-d][d] made at creation.  Each landed
+// chunk gets its input transform applied in shared memory (the MO-PCG
+// direction update Q = Z + beta Q, the IMEX heat source, or the DIB
+// kinetics), then every thread (one per output column, right-factor band in
+// registers) sweeps its rows: Y_t(r) = sum_e X[r][c+e] h_t[e] is formed once
 // per row and scattered into a ring of W partial outputs with the left-factor
-// coefficients (shared-memory broadcasts).  Epilogues: plain store, or the
-// MO-PCG store + <W,Q>, |Q|^2 partials with a last-block alpha step
-// (solvers.py:424-431).
+// coefficients (shared-memory broadcasts).  Loads of the next chunks overlap
+// the sweep of the current one.  Epilogues: plain store, or the MO-PCG store
+// + <W,Q>, |Q|^2 partials with a last-block alpha step (solvers.py:424-431).
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
 #include "sfb_common.cuh"
 #include "sfb_kernels.cuh"
 #include "sfb_launch.cuh"
+#include "sfb_tma.cuh"
 
 namespace sfb {
 
 namespace {
 
-constexpr int TX = 128;
-constexpr int TY = 32;
+constexpr int TX = 128;                   // output columns per CTA (one per thread)
+constexpr int NS = 3;                     // TMA ring stages
+constexpr int CTA_TARGET = 3 * kNumSMs;   // one wave of 3 CTAs per SM
+constexpr int RY_MIN = 32;
 
 template <int W>
-__host__ __device__ constexpr int wpad() {
-    return W + 1;  // even: the coefficients of one halo row load as 16-byte pairs
+__host__ __device__ constexpr int chunk_rows() {
+    return W * (W >= 8 ? 1 : (8 + W - 1) / W);  // a multiple of W (static ring slots), >= 8
+}
+
+__host__ __device__ constexpr int pad128(int doubles) { return (doubles + 15) / 16 * 16; }
+
+template <int T, int W>
+struct BandCfg {
+    static constexpr int CH = chunk_rows<W>();
+    static constexpr int HC = TX + W - 1;    // halo columns
+    static constexpr int HCB = HC + 2;       // box columns: boxes start at an even column (16-byte rows)
+    static constexpr int WP = W + 1;         // even: coefficient pairs load as 16 bytes
+    static constexpr int XS = CH * HCB;      // doubles of one input box
+    static constexpr int GS = T * CH * WP;   // doubles of the chunk's left coefficients
+    static constexpr int XSP = pad128(XS);   // 128-byte aligned regions
+    static constexpr int GSP = pad128(GS);
+    static constexpr int STAGE = 2 * XSP + GSP;
+    static constexpr int SMEM = NS * STAGE * 8 + 128;
+};
+
+struct BandMaps {
+    CUtensorMap a;       // input A (X / Z / U / eta), box {HCB, CH}
+    CUtensorMap b[2];    // input B (Q0, Q1 / F / theta)
+    CUtensorMap g;       // gskew, box {WP, CH, T}
+};
+
+// rows per CTA and row blocks for an output of `rows` x `cols`
+__host__ inline void band_geometry(int rows, int cols, int* ry, int* nrb) {
+    const int nstrips = (cols + TX - 1) / TX;
+    const int want = std::max(1, CTA_TARGET / nstrips);
+    const int r = std::max(RY_MIN, (rows + want - 1) / want);
+    *ry = r;
+    *nrb = (rows + r - 1) / r;
 }
 
 template <int T, int W>
-constexpr int band_smem() {
-    return ((TY + W - 1) * (TX + W - 1) + T * (TY + W - 1) * wpad<W>()) * 8;
-}
-
-template <int T, int W>
-__global__ void __launch_bounds__(TX) band_kernel(BandArgs a) {
+__global__ void __launch_bounds__(TX, 3) band_kernel(BandArgs a, const __grid_constant__ BandMaps maps, int ry) {
     SFB_PDL_PROLOGUE();
-    constexpr int HR = TY + W - 1, HC = TX + W - 1;
-    extern __shared__ double sm[];
-    double* Qs = sm;             // [HR][HC]
-    double* Gs = sm + HR * HC;   // [T][HR][W+1]
+    using C = BandCfg<T, W>;
+    constexpr int CH = C::CH, HCB = C::HCB, WP = C::WP;
+    constexpr int NPAIR = HCB / 2;           // HCB is even (W odd)
+    constexpr int NPP = (NPAIR + 63) / 64;   // column pairs per thread in the transform
+    constexpr int NRR = (CH + 1) / 2;        // rows per thread and chunk in the transform
+    extern __shared__ double sm_raw[];       // NS x {A[CH][HCB], B[CH][HCB], G[T][CH][WP]}
+    double* sm = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(sm_raw) + 127) & ~uintptr_t(127));
+    __shared__ __align__(8) uint64_t full[NS];
 
+    const int mode = a.ld_mode;
     PcgState* st = a.pcg;
     int s = 0;
     double beta = 0.0;
-    if (a.ld_mode == LD_PCG) {
+    if (mode == LD_PCG) {
         if (st->status != SFB_PCG_RUNNING) return;  // uniform gate
         s = st->iter;
         if (s > 0) beta = st->rz_next / st->rz;      // solvers.py:448-452
     }
-    const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
-    const int c = threadIdx.x, gc = x0 + c;
-    double* Qcur = (s & 1) ? a.Q1 : a.Q0;
-    const double* Qprev = (s & 1) ? a.Q0 : a.Q1;
+    const int x0 = blockIdx.x * TX, y0 = blockIdx.y * ry;
+    const int rows_here = min(ry, a.out_rows - y0);
+    const int hry = rows_here + W - 1;             // halo rows streamed by this CTA
+    const int nch = (hry + CH - 1) / CH;
+    const int t = threadIdx.x, c = t, gc = x0 + c;
+    const int goff = a.goff, hoff = a.hoff;
 
-    // ---- stage the input halo (with its transform) ----
-    const int urows = a.in_rows - 2 * a.rs, ucols = a.in_cols - 2 * a.cs;
-    bool flag = false;
-    double vmax = 0.0;
-    #pragma unroll 4
-    for (int idx = threadIdx.x; idx < HR * HC; idx += TX) {
-        const int r = idx / HC, cc = idx - r * HC;  // HC is a compile-time constant
-        const int gr = y0 + a.goff + r, gx = x0 + a.hoff + cc;
-        double v = 0.0;
-        if (gr >= 0 && gr < a.in_rows && gx >= 0 && gx < a.in_cols) {
-            switch (a.ld_mode) {
-                case LD_PCG: {
-                    v = a.X[(size_t)gr * a.ldx + gx];
-                    if (s > 0) v = __dadd_rn(__dmul_rn(beta, Qprev[(size_t)gr * a.ldq + gx]), v);  // Q*=beta; Q+=Z
-                    if (gr >= y0 && gr < y0 + TY && gx >= x0 && gx < x0 + TX)
-                        Qcur[(size_t)gr * a.ldq + gx] = v;
-                    break;
-                }
-                case LD_HEAT: {
-                    const int ur = gr - a.rs, uc = gx - a.cs;
-                    const double u =
-                        (ur >= 0 && ur < urows && uc >= 0 && uc < ucols) ? a.X[(size_t)ur * a.ldx + uc] : 0.0;
-                    v = a.X2 ? u + a.c * a.X2[(size_t)gr * a.ldx2 + gx] : u;
-                    break;
-                }
-                case LD_DIB: {
-                    // models.py:74-82 and timestepping.py:201-207
-                    const double* p = a.kp;  // alpha, gamma_k, A1, A2, B, C, D, k2, k3
-                    const double eta = a.X[(size_t)gr * a.ldx + gx];
-                    const double th = a.X2[(size_t)gr * a.ldx + gx];
-                    if (a.species == 0) {
-                        const double f = p[2] * (1.0 - th) * eta - p[3] * (eta * eta * eta) - p[4] * (th - p[0]);
-                        v = eta + a.c * f;
-                    } else {
-                        const double g = p[5] * (1.0 + p[7] * eta) * (1.0 - th) * (1.0 - p[1] * (1.0 - th)) -
-                                         p[6] * th * (1.0 + p[1] * th) * (1.0 + p[8] * eta);
-                        v = th + a.c * g;
+    // ---- sources ----
+    int acs = 0, ars = 0;
+    bool hasB = false;
+    const CUtensorMap* mb = &maps.b[0];
+    double* Qcur = nullptr;
+    if (mode == LD_PCG) {
+        Qcur = (s & 1) ? a.Q1 : a.Q0;
+        hasB = s > 0;
+        mb = &maps.b[(s & 1) ? 0 : 1];  // previous direction
+    } else if (mode == LD_HEAT) {      // interior state U at offset (rs, cs): zero outside
+        ars = a.rs;
+        acs = a.cs;
+        hasB = a.X2 != nullptr;
+    } else if (mode == LD_DIB) {
+        hasB = true;
+    }
+    // A's box starts at full-grid column x0 + hoff - shA (U column minus acs), B's at x0 + hoff - shB;
+    // both even, so every box row is 16-byte aligned in global memory
+    const int shA = (hoff - acs) & 1, shB = hoff & 1;
+    const int dbg = a.dbg;
+    const bool doA = !(dbg & 1), doG = !(dbg & 2);
+    if (dbg & 4) hasB = false;
+    const uint32_t tx_bytes = (uint32_t)(((hasB ? 1 : 0) + (doA ? 1 : 0)) * C::XS + (doG ? C::GS : 0)) * 8;
+
+    auto issue = [&](int k) {  // one thread
+        if (k < nch) {
+            const int sl = k % NS;
+            double* A = sm + sl * C::STAGE;
+            const uint32_t bar = smem_u32(&full[sl]);
+            const int r0 = k * CH;
+            if (dbg & 8) { asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory"); return; }
+            mbar_expect_tx_u32(bar, tx_bytes);
+            if (doA) tma_load_u32(smem_u32(A), &maps.a, bar, x0 + hoff - acs - shA, y0 + goff + r0 - ars);
+            if (hasB) tma_load_u32(smem_u32(A + C::XSP), mb, bar, x0 + hoff - shB, y0 + goff + r0);
+            if (doG) tma_load3_u32(smem_u32(A + 2 * C::XSP), &maps.g, bar, 0, y0 + r0, 0);
+        }
+    };
+
+    if (t == 0) {
+        for (int i = 0; i < NS; ++i) mbar_init_u32(smem_u32(&full[i]), 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        #pragma unroll
+        for (int k = 0; k < NS - 1; ++k) issue(k);
+    }
+
+    // ---- per-thread transform geometry: smem column pairs pc, pc + 64 of rows rh, rh + 2, ...
+    // (A's column space: smem column m holds full-grid column x0 + hoff - shA + m) ----
+    const int pc = t & 63, rh = t >> 6;
+    unsigned mdom[NPP], mq[NPP];
+    int gxs[NPP];
+    #pragma unroll
+    for (int j = 0; j < NPP; ++j) {
+        const int pp = pc + 64 * j;
+        const int gx = x0 + hoff - shA + 2 * pp;
+        const bool has = pp < NPAIR;
+        auto pm = [](int col, int n) {
+            return ((unsigned)col < (unsigned)n ? 1u : 0u) | ((unsigned)(col + 1) < (unsigned)n ? 2u : 0u);
+        };
+        gxs[j] = gx;
+        // in the grid and in this CTA's halo (the box's extra columns stay out of the checks)
+        mdom[j] = has ? (pm(gx, a.in_cols) & pm(2 * pp - shA, C::HC)) : 0u;
+        mq[j] = has ? (pm(gx, a.in_cols) & pm(gx - x0, TX)) : 0u;
+    }
+    // visit this thread's pairs of a landed chunk: f(gr, j, double2* a_pair, const double* b_elems),
+    // b_elems = B at the same full-grid columns (16-byte aligned unless shA != shB: heat only)
+    auto for_pairs = [&](double* A, int r0, auto&& f) {
+        const double* B = A + C::XSP + (shB - shA);
+        #pragma unroll
+        for (int i = 0; i < NRR; ++i) {
+            const int rr = rh + 2 * i;
+            if (rr < CH) {
+                const int gr = y0 + goff + r0 + rr;
+                #pragma unroll
+                for (int j = 0; j < NPP; ++j) {
+                    if (j == 0 || pc + 64 * j < NPAIR) {
+                        const int o = rr * HCB + 2 * (pc + 64 * j);
+                        f(gr, j, reinterpret_cast<double2*>(A + o), B + o);
                     }
-                    break;
                 }
-                default:
-                    v = a.X[(size_t)gr * a.ldx + gx];
-            }
-            if (a.check != nullptr) {
-                if (!isfinite(v)) flag = true;
-                else vmax = fmax(vmax, fabs(v));
             }
         }
-        Qs[r * HC + cc] = v;
-    }
-    if (a.check != nullptr) {
-        if (flag) atomicOr(a.check + 1, 1ull);
-        if (vmax > 0.0) atomicMax(a.check, (unsigned long long)__double_as_longlong(vmax));
-    }
-    // ---- left-factor coefficients of this row tile (zero outside [0,TY)) ----
-    // halo-row-major: Gs[t][r][d] multiplies Y_t(r) into output row i = r - d
-    constexpr int WP = wpad<W>();
-    for (int idx = threadIdx.x; idx < T * HR * WP; idx += TX) {
-        const int t = idx / (HR * WP), rem = idx - t * HR * WP, r = rem / WP, d = rem - r * WP;
-        const int i = r - d, gi = y0 + i;
-        double v = 0.0;
-        if (d < W && t < a.nterms && i >= 0 && i < TY && gi < a.out_rows)
-            v = a.gband[((size_t)t * a.out_rows + gi) * W + d];
-        Gs[idx] = v;
-    }
+    };
+
     // ---- right-factor band of this thread's column, in registers ----
     double h[T][W];
     #pragma unroll
-    for (int t = 0; t < T; ++t)
+    for (int tt = 0; tt < T; ++tt)
         #pragma unroll
         for (int e = 0; e < W; ++e)
-            h[t][e] = (t < a.nterms && gc < a.out_cols) ? a.hband[((size_t)t * a.out_cols + gc) * W + e] : 0.0;
-    __syncthreads();
+            h[tt][e] = (tt < a.nterms && gc < a.out_cols) ? a.hband[((size_t)tt * a.out_cols + gc) * W + e] : 0.0;
 
-    // ---- sweep: ring of W partial output rows ----
-    double acc[W];
+    double acc[W], cen[W];
     #pragma unroll
-    for (int d = 0; d < W; ++d) acc[d] = 0.0;
+    for (int d = 0; d < W; ++d) acc[d] = cen[d] = 0.0;
     double pdot = 0.0, pqq = 0.0;
     const bool col_ok = gc < a.out_cols;
-    for (int r0 = 0; r0 < HR; r0 += W) {
-        #pragma unroll
-        for (int u = 0; u < W; ++u) {
-            const int r = r0 + u;
-            if (r < HR) {
+    const bool pcg_ep = a.ep_mode == EP_PCG;
+    double* const Wout = a.W;
+    const int ldw = a.ldw;
+    bool flag = false;
+    double vmax = 0.0;
+    auto check = [&](double v) {
+        if (!isfinite(v)) flag = true;
+        else vmax = fmax(vmax, fabs(v));
+    };
+    __syncthreads();  // barrier init visible
+
+    for (int k = 0; k < nch; ++k) {
+        double* A = sm + (k % NS) * C::STAGE;
+        const double* G = A + 2 * C::XSP;
+        const int r0 = k * CH;
+        mbar_wait_u32(smem_u32(&full[k % NS]), (k / NS) & 1);
+        // ---- input transform, in place (generic-proxy writes, fenced before the stage is refilled) ----
+        if (mode == LD_PCG) {
+            const double b = beta;
+            const bool upd = s > 0;
+            const bool q16 = (hoff & 1) == 0;
+            for_pairs(A, r0, [&](int gr, int j, double2* ap, const double* bp) {
+                double2 v = *ap;
+                if (upd) {
+                    const double2 q = *reinterpret_cast<const double2*>(bp);
+                    v.x = __dadd_rn(__dmul_rn(b, q.x), v.x);  // Q*=beta; Q+=Z
+                    v.y = __dadd_rn(__dmul_rn(b, q.y), v.y);
+                    *ap = v;
+                }
+                if (gr >= y0 && gr < y0 + rows_here) {
+                    double* qp = Qcur + (size_t)gr * a.ldq + gxs[j];
+                    const unsigned m = mq[j];
+                    if (q16 && m == 3u) *reinterpret_cast<double2*>(qp) = v;
+                    else {
+                        if (m & 1u) qp[0] = v.x;
+                        if (m & 2u) qp[1] = v.y;
+                    }
+                }
+            });
+        } else if (mode == LD_HEAT) {
+            const double cc = a.c;
+            const bool chk = a.check != nullptr;
+            const int in_rows = a.in_rows;
+            for_pairs(A, r0, [&](int gr, int j, double2* ap, const double* bp) {
+                double2 v = *ap;
+                if (hasB) {
+                    v.x = v.x + cc * bp[0];
+                    v.y = v.y + cc * bp[1];
+                    *ap = v;
+                }
+                if (chk && (unsigned)gr < (unsigned)in_rows) {
+                    if (mdom[j] & 1u) check(v.x);
+                    if (mdom[j] & 2u) check(v.y);
+                }
+            });
+        } else if (mode == LD_DIB) {  // models.py:74-82 and timestepping.py:201-207
+            const double* p = a.kp;  // alpha, gamma_k, A1, A2, B, C, D, k2, k3
+            const double cc = a.c;
+            const bool sp0 = a.species == 0, chk = a.check != nullptr;
+            const int in_rows = a.in_rows;
+            for_pairs(A, r0, [&](int gr, int j, double2* ap, const double* bp) {
+                const double2 e2 = *ap, t2 = *reinterpret_cast<const double2*>(bp);
+                const unsigned m = (unsigned)gr < (unsigned)in_rows ? mdom[j] : 0u;
+                double v[2];
+                const double ev[2] = {e2.x, e2.y}, tv[2] = {t2.x, t2.y};
+                #pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    const double eta = ev[q], th = tv[q];
+                    double r;
+                    if (sp0) {
+                        const double f = p[2] * (1.0 - th) * eta - p[3] * (eta * eta * eta) - p[4] * (th - p[0]);
+                        r = eta + cc * f;
+                    } else {
+                        const double g = p[5] * (1.0 + p[7] * eta) * (1.0 - th) * (1.0 - p[1] * (1.0 - th)) -
+                                         p[6] * th * (1.0 + p[1] * th) * (1.0 + p[8] * eta);
+                        r = th + cc * g;
+                    }
+                    v[q] = (m >> q) & 1u ? r : 0.0;  // outside the grid the halo is zero
+                    if (chk && ((m >> q) & 1u)) check(v[q]);
+                }
+                *ap = make_double2(v[0], v[1]);
+            });
+        }
+        fence_proxy_async_smem();
+        __syncthreads();  // transform visible; every thread is done with chunk k-1
+        if (t == 0) issue(k + NS - 1);  // refill the stage chunk k-1 used
+
+        // ---- sweep the chunk's halo rows (rows past the halo feed only unstored outputs) ----
+        #pragma unroll 1
+        for (int m = 0; m < CH / W; ++m) {
+            #pragma unroll
+            for (int u = 0; u < W; ++u) {
+                const int rr = m * W + u;  // r0 + rr == u (mod W)
                 double qv[W];
                 #pragma unroll
-                for (int e = 0; e < W; ++e) qv[e] = Qs[r * HC + c + e];
+                for (int e = 0; e < W; ++e) qv[e] = A[rr * HCB + shA + c + e];
+                cen[u] = qv[(W - 1) / 2];
                 #pragma unroll
-                for (int t = 0; t < T; ++t) {
+                for (int tt = 0; tt < T; ++tt) {
                     double y = 0.0;
                     #pragma unroll
-                    for (int e = 0; e < W; ++e) y = fma(qv[e], h[t][e], y);
-                    const double2* gp = reinterpret_cast<const double2*>(Gs + (t * HR + r) * WP);
+                    for (int e = 0; e < W; ++e) y = fma(qv[e], h[tt][e], y);
+                    const double2* gp = reinterpret_cast<const double2*>(G + (tt * CH + rr) * WP);
                     #pragma unroll
                     for (int dd = 0; dd < WP / 2; ++dd) {
                         const double2 g = gp[dd];
@@ -161,23 +312,25 @@ __global__ void __launch_bounds__(TX) band_kernel(BandArgs a) {
                         }
                     }
                 }
-                const int i = r - (W - 1);
+                const int i = r0 + rr - (W - 1);
                 const int slot = (u + 1) % W;
-                if (i >= 0) {
-                    const int gi = y0 + i;
-                    if (col_ok && gi < a.out_rows) {
-                        const double w = acc[slot];
-                        a.W[(size_t)gi * a.ldw + gc] = w;
-                        if (a.ep_mode == EP_PCG) {
-                            const double q = Qs[(i - a.goff) * HC + c - a.hoff];
-                            pdot = fma(w, q, pdot);
-                            pqq = fma(q, q, pqq);
-                        }
+                if ((unsigned)i < (unsigned)rows_here && col_ok) {
+                    const double w = acc[slot];
+                    Wout[(size_t)(y0 + i) * ldw + gc] = w;
+                    if (pcg_ep) {
+                        // Q at (y0 + i, gc): centre of halo row i - goff = r - (W-1)/2
+                        const double q = cen[(u - (W - 1) / 2 + W) % W];
+                        pdot = fma(w, q, pdot);
+                        pqq = fma(q, q, pqq);
                     }
-                    acc[slot] = 0.0;
                 }
+                acc[slot] = 0.0;
             }
         }
+    }
+    if (a.check != nullptr) {
+        if (flag) atomicOr(a.check + 1, 1ull);
+        if (vmax > 0.0) atomicMax(a.check, (unsigned long long)__double_as_longlong(vmax));
     }
 
     if (a.ep_mode == EP_PCG) {
@@ -211,14 +364,42 @@ __global__ void __launch_bounds__(TX) band_kernel(BandArgs a) {
 
 template <int T, int W>
 int launch_tw(const BandArgs& a, cudaStream_t stream) {
-    constexpr int smem = band_smem<T, W>();
+    using C = BandCfg<T, W>;
+    constexpr int smem = C::SMEM;
     static bool attr = false;
     if (!attr) {
         SFB_CUDA_TRY(cudaFuncSetAttribute(band_kernel<T, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         attr = true;
     }
-    dim3 grid((a.out_cols + TX - 1) / TX, (a.out_rows + TY - 1) / TY);
-    SFB_TRY(launch_kernel(band_kernel<T, W>, dim3(grid), dim3(TX), smem, stream, a));
+    // tensor maps of the inputs (zero fill outside each source's extents)
+    BandMaps maps;
+    std::memset(&maps, 0, sizeof(maps));
+    const cuuint32_t xbox[2] = {(cuuint32_t)C::HCB, (cuuint32_t)C::CH};
+    auto xmap = [&](CUtensorMap* m, const double* p, int ld, int rows, int cols) {
+        const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+        return tma_make_map(m, p, 2, dims, ld, xbox, CU_TENSOR_MAP_SWIZZLE_NONE);
+    };
+    if (a.ld_mode == LD_HEAT) {
+        SFB_TRY(xmap(&maps.a, a.X, a.ldx, a.in_rows - 2 * a.rs, a.in_cols - 2 * a.cs));
+        if (a.X2 != nullptr) SFB_TRY(xmap(&maps.b[0], a.X2, a.ldx2, a.in_rows, a.in_cols));
+    } else {
+        SFB_TRY(xmap(&maps.a, a.X, a.ldx, a.in_rows, a.in_cols));
+        if (a.ld_mode == LD_PCG) {
+            SFB_TRY(xmap(&maps.b[0], a.Q0, a.ldq, a.in_rows, a.in_cols));
+            SFB_TRY(xmap(&maps.b[1], a.Q1, a.ldq, a.in_rows, a.in_cols));
+        } else if (a.ld_mode == LD_DIB) {
+            SFB_TRY(xmap(&maps.b[0], a.X2, a.ldx2, a.in_rows, a.in_cols));
+        }
+    }
+    {
+        const cuuint64_t dims[3] = {(cuuint64_t)C::WP, (cuuint64_t)a.gskew_rows, (cuuint64_t)a.nterms};
+        const cuuint32_t gbox[3] = {(cuuint32_t)C::WP, (cuuint32_t)C::CH, (cuuint32_t)T};
+        SFB_TRY(tma_make_map(&maps.g, a.gskew, 3, dims, C::WP, gbox, CU_TENSOR_MAP_SWIZZLE_NONE));
+    }
+    int ry, nrb;
+    band_geometry(a.out_rows, a.out_cols, &ry, &nrb);
+    dim3 grid((a.out_cols + TX - 1) / TX, nrb);
+    SFB_TRY(launch_kernel(band_kernel<T, W>, grid, dim3(TX), smem, stream, a, maps, ry));
     SFB_CHECK_LAUNCH();
     return SFB_OK;
 }
@@ -243,7 +424,9 @@ bool band_supported(int nterms, int width) {
 }
 
 int band_grid_blocks(int out_rows, int out_cols) {
-    return ((out_cols + TX - 1) / TX) * ((out_rows + TY - 1) / TY);
+    int ry, nrb;
+    band_geometry(out_rows, out_cols, &ry, &nrb);
+    return ((out_cols + TX - 1) / TX) * nrb;
 }
 
 int launch_band(const BandArgs& a, cudaStream_t stream) {
@@ -252,9 +435,31 @@ int launch_band(const BandArgs& a, cudaStream_t stream) {
         return SFB_ERR_UNSUPPORTED;
     }
     if (a.out_rows <= 0 || a.out_cols <= 0) return SFB_OK;
-    if (a.nterms == 1) return launch_t<1>(a, stream);
-    if (a.nterms == 2) return launch_t<2>(a, stream);
-    return launch_t<5>(a, stream);
+    if (a.ep_mode == EP_PCG && (a.goff != -(a.width - 1) / 2 || a.hoff != -(a.width - 1) / 2)) {
+        set_error("banded kernel: the MO-PCG epilogue needs a centred square operator");
+        return SFB_ERR_UNSUPPORTED;
+    }
+    if (a.gskew == nullptr || a.gskew_rows != a.out_rows + a.width - 1)
+        return arg_error("banded kernel: missing skewed left-factor coefficients");
+    BandArgs b = a;
+    if (const char* e = std::getenv("SYLFEM_B200_BAND_DBG")) b.dbg = std::atoi(e);
+    if (a.nterms == 1) return launch_t<1>(b, stream);
+    if (a.nterms == 2) return launch_t<2>(b, stream);
+    return launch_t<5>(b, stream);
+}
+
+// gskew[t][j][d] = gband[t][j - d][d] for 0 <= j - d < rows (zero elsewhere),
+// j in [0, rows + w - 1), d < w; rows padded to w + 1 doubles.
+std::vector<double> band_skew(const double* gband, int nterms, int rows, int w) {
+    const int R = rows + w - 1, WP = w + 1;
+    std::vector<double> out((size_t)nterms * R * WP, 0.0);
+    for (int t = 0; t < nterms; ++t)
+        for (int j = 0; j < R; ++j)
+            for (int d = 0; d < w; ++d) {
+                const int i = j - d;
+                if (i >= 0 && i < rows) out[((size_t)t * R + j) * WP + d] = gband[((size_t)t * rows + i) * w + d];
+            }
+    return out;
 }
 
 }  // namespace sfb

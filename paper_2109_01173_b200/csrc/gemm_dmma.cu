@@ -21,6 +21,7 @@
 #include "sfb_common.cuh"
 #include "sfb_kernels.cuh"
 #include "sfb_launch.cuh"
+#include "sfb_tma.cuh"
 
 namespace sfb {
 
@@ -32,10 +33,6 @@ constexpr int NTHREADS = NWARPS * 32;       // 2 warps per SM sub-partition (<= 
 constexpr int TILE_BYTES = BM * BK * 8;     // 16 KB per operand per stage
 constexpr int SMEM_BYTES = 2 * STAGES * TILE_BYTES + STAGES * 8 + 1024;
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                  : "+d"(c0), "+d"(c1)
@@ -46,32 +43,6 @@ __device__ __forceinline__ double2 lds128(uint32_t addr) {
     double2 v;
     asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr));
     return v;
-}
-
-__device__ __forceinline__ void mbar_init_u32(uint32_t bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
-}
-
-__device__ __forceinline__ void mbar_expect_tx_u32(uint32_t bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait_u32(uint32_t bar, uint32_t parity) {
-    asm volatile(
-        "{\n\t.reg .pred P1;\n"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-        "@!P1 bra WAIT_%=;\n}" ::"r"(bar),
-        "r"(parity)
-        : "memory");
-}
-
-__device__ __forceinline__ void tma_load_u32(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1)
-        : "memory");
 }
 
 struct Sched {
@@ -278,38 +249,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
 }
 
-PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-    if (fn == nullptr) {
-        cudaDriverEntryPointQueryResult q;
-        void* p = nullptr;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-            q == cudaDriverEntryPointSuccess)
-            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-    }
-    return fn;
-}
-
 int make_map(CUtensorMap* map, const double* ptr, int rows, int cols, int ld) {
-    auto fn = encode_fn();
-    if (fn == nullptr) {
-        set_error("cuTensorMapEncodeTiled entry point unavailable");
-        return SFB_ERR_CUDA;
-    }
-    if ((ld % 2) != 0 || (reinterpret_cast<uintptr_t>(ptr) % 16) != 0)
-        return arg_error("DMMA GEMM operands need 16-byte aligned rows (even leading dimension)");
-    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-    cuuint64_t strides[1] = {(cuuint64_t)ld * sizeof(double)};
-    cuuint32_t box[2] = {BK, BM};
-    cuuint32_t estr[2] = {1, 1};
-    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(ptr), dims, strides, box,
-                    estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) {
-        set_error("cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
-        return SFB_ERR_CUDA;
-    }
-    return SFB_OK;
+    if (!tma_aligned(ptr, ld)) return arg_error("DMMA GEMM operands need 16-byte aligned rows (even leading dimension)");
+    const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    const cuuint32_t box[2] = {BK, BM};
+    return tma_make_map(map, ptr, 2, dims, ld, box, CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
 }  // namespace

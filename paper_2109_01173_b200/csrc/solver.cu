@@ -16,6 +16,7 @@
 
 #include "sfb_common.cuh"
 #include "sfb_kernels.cuh"
+#include "sfb_tma.cuh"
 
 namespace sfb {
 
@@ -74,6 +75,35 @@ struct ScopedFree {
 
 inline int pad_ld(int cols) { return round_up(cols < 1 ? 1 : cols, 32); }
 
+// The banded kernel reads its inputs by TMA (16-byte aligned rows).  Inputs
+// that are not (odd leading dimension, offset views) are first copied into
+// padded stream-ordered scratch.
+int stage_aligned(ScopedFree& tmp, const double*& p, int& ld, int rows, int cols, cudaStream_t s) {
+    if (p == nullptr || rows <= 0 || cols <= 0 || tma_aligned(p, ld)) return SFB_OK;
+    const int pl = pad_ld(cols);
+    double* q;
+    SFB_TRY(tmp.get(&q, (size_t)rows * pl * 8));
+    SFB_CUDA_TRY(cudaMemcpy2DAsync(q, (size_t)pl * 8, p, (size_t)ld * 8, (size_t)cols * 8, rows,
+                                   cudaMemcpyDeviceToDevice, s));
+    p = q;
+    ld = pl;
+    return SFB_OK;
+}
+
+int launch_band_staged(BandArgs a, cudaStream_t s) {
+    ScopedFree tmp(s);
+    if (a.ld_mode == LD_HEAT) {
+        SFB_TRY(stage_aligned(tmp, a.X, a.ldx, a.in_rows - 2 * a.rs, a.in_cols - 2 * a.cs, s));
+        SFB_TRY(stage_aligned(tmp, a.X2, a.ldx2, a.in_rows, a.in_cols, s));
+    } else if (a.ld_mode == LD_DIB) {
+        SFB_TRY(stage_aligned(tmp, a.X, a.ldx, a.in_rows, a.in_cols, s));
+        SFB_TRY(stage_aligned(tmp, a.X2, a.ldx2, a.in_rows, a.in_cols, s));
+    } else if (a.ld_mode == LD_PLAIN) {
+        SFB_TRY(stage_aligned(tmp, a.X, a.ldx, a.in_rows, a.in_cols, s));
+    }
+    return launch_band(a, s);
+}
+
 }  // namespace
 
 // Stream-K workspace of the DMMA GEMM (partial tiles + per-tile counters).
@@ -112,6 +142,7 @@ struct sfb_op {
     bool dense = false;
     int width = 1, goff = 0, hoff = 0;
     double* gband = nullptr;
+    double* gskew = nullptr;  // band_skew(gband): TMA-boxable left coefficients
     double* hband = nullptr;
     // dense fallback: G_t (qy x qy) and H_t^T (qx x qx), padded rows
     double* G = nullptr;
@@ -123,6 +154,7 @@ struct sfb_map {
     int out_rows = 0, out_cols = 0, in_rows = 0, in_cols = 0;
     int width = 1, goff = 0, hoff = 0;
     double* gband = nullptr;
+    double* gskew = nullptr;
     double* hband = nullptr;
 };
 
@@ -244,6 +276,8 @@ int op_apply_impl(const sfb_op* op, const double* U, int ldu, double* W, int ldw
         a.goff = op->goff;
         a.hoff = op->hoff;
         a.gband = op->gband;
+        a.gskew = op->gskew;
+        a.gskew_rows = op->qy + op->width - 1;
         a.hband = op->hband;
         a.ld_mode = LD_PLAIN;
         a.X = U;
@@ -251,7 +285,7 @@ int op_apply_impl(const sfb_op* op, const double* U, int ldu, double* W, int ldw
         a.ep_mode = EP_STORE;
         a.W = W;
         a.ldw = ldw;
-        return launch_band(a, s);
+        return launch_band_staged(a, s);
     }
     for (int t = 0; t < op->nterms; ++t) {
         GemmEpi e1;
@@ -387,6 +421,8 @@ int pcg_enqueue_iteration(sfb_pcg* s, double* iterates) {
         a.goff = op->goff;
         a.hoff = op->hoff;
         a.gband = op->gband;
+        a.gskew = op->gskew;
+        a.gskew_rows = op->qy + op->width - 1;
         a.hband = op->hband;
         a.ld_mode = LD_PCG;
         a.X = s->Z;
@@ -567,7 +603,11 @@ int sfb_op_create(int qy, int qx, int nterms, int gw, int goff, const double* gb
     op->width = gw;
     op->goff = goff;
     op->hoff = hoff;
+    const std::vector<double> skew = band_skew(gband, nterms, qy, gw);
     int rc = dalloc(&op->gband, (size_t)nterms * qy * gw);
+    if (rc == SFB_OK) rc = dalloc(&op->gskew, skew.size());
+    if (rc == SFB_OK && cudaMemcpy(op->gskew, skew.data(), skew.size() * 8, cudaMemcpyHostToDevice) != cudaSuccess)
+        rc = SFB_ERR_CUDA;
     if (rc == SFB_OK) rc = dalloc(&op->hband, (size_t)nterms * qx * hw);
     if (rc == SFB_OK && cudaMemcpy(op->gband, gband, (size_t)nterms * qy * gw * 8, cudaMemcpyHostToDevice) != cudaSuccess)
         rc = SFB_ERR_CUDA;
@@ -664,6 +704,7 @@ int sfb_op_residual(const sfb_op* op, const double* U, int ldu, const double* rh
 int sfb_op_destroy(sfb_op* op) {
     if (!op) return SFB_OK;
     cudaFree(op->gband);
+    cudaFree(op->gskew);
     cudaFree(op->hband);
     cudaFree(op->G);
     cudaFree(op->Ht);
@@ -688,9 +729,12 @@ int sfb_map_create(int out_rows, int out_cols, int in_rows, int in_cols, int gw,
     m->width = gw;
     m->goff = goff;
     m->hoff = hoff;
+    const std::vector<double> skew = band_skew(gband, 1, out_rows, gw);
     int rc = dalloc(&m->gband, (size_t)out_rows * gw);
+    if (rc == SFB_OK) rc = dalloc(&m->gskew, skew.size());
     if (rc == SFB_OK) rc = dalloc(&m->hband, (size_t)out_cols * hw);
     if (rc == SFB_OK && (cudaMemcpy(m->gband, gband, (size_t)out_rows * gw * 8, cudaMemcpyHostToDevice) != cudaSuccess ||
+                         cudaMemcpy(m->gskew, skew.data(), skew.size() * 8, cudaMemcpyHostToDevice) != cudaSuccess ||
                          cudaMemcpy(m->hband, hband, (size_t)out_cols * hw * 8, cudaMemcpyHostToDevice) != cudaSuccess)) {
         set_error("uploading map bands failed");
         rc = SFB_ERR_CUDA;
@@ -715,6 +759,8 @@ BandArgs map_args(const sfb_map* m, double* out, int ldo) {
     a.goff = m->goff;
     a.hoff = m->hoff;
     a.gband = m->gband;
+    a.gskew = m->gskew;
+    a.gskew_rows = m->out_rows + m->width - 1;
     a.hband = m->hband;
     a.ep_mode = EP_STORE;
     a.W = out;
@@ -723,13 +769,13 @@ BandArgs map_args(const sfb_map* m, double* out, int ldo) {
 }
 
 int run_checked(BandArgs& a, double* check2, cudaStream_t s) {
-    if (check2 == nullptr) return launch_band(a, s);
+    if (check2 == nullptr) return launch_band_staged(a, s);
     ScopedFree tmp(s);
     unsigned long long* chk;
     SFB_TRY(tmp.get(&chk, 2 * sizeof(unsigned long long)));
     SFB_CUDA_TRY(cudaMemsetAsync(chk, 0, 2 * sizeof(unsigned long long), s));
     a.check = chk;
-    SFB_TRY(launch_band(a, s));
+    SFB_TRY(launch_band_staged(a, s));
     unsigned long long h[2];
     SFB_CUDA_TRY(cudaMemcpyAsync(h, chk, sizeof(h), cudaMemcpyDeviceToHost, s));
     SFB_CUDA_TRY(cudaStreamSynchronize(s));
@@ -747,7 +793,7 @@ int sfb_map_apply(const sfb_map* m, const double* F, int ldf, double* out, int l
     a.ld_mode = LD_PLAIN;
     a.X = F;
     a.ldx = ldf;
-    return launch_band(a, (cudaStream_t)stream);
+    return launch_band_staged(a, (cudaStream_t)stream);
 }
 
 int sfb_map_apply_heat(const sfb_map* m, const double* U, int ldu, int row_shift, int col_shift, double c,
@@ -775,6 +821,7 @@ int sfb_map_apply_dib(const sfb_map* m, const double* U, const double* V, int ld
     a.X = U;
     a.X2 = V;
     a.ldx = ld;
+    a.ldx2 = ld;
     a.species = species;
     a.c = tau_rho;
     for (int i = 0; i < 9; ++i) a.kp[i] = params[i];
@@ -784,6 +831,7 @@ int sfb_map_apply_dib(const sfb_map* m, const double* U, const double* V, int ld
 int sfb_map_destroy(sfb_map* m) {
     if (!m) return SFB_OK;
     cudaFree(m->gband);
+    cudaFree(m->gskew);
     cudaFree(m->hband);
     delete m;
     return SFB_OK;
