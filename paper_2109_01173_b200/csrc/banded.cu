@@ -74,7 +74,8 @@ __host__ inline void band_geometry(int rows, int cols, int* ry, int* nrb) {
     *nrb = (rows + r - 1) / r;
 }
 
-template <int T, int W>
+// MODE = the loader (LD_*); the MO-PCG loader always comes with the MO-PCG epilogue.
+template <int T, int W, int MODE>
 __global__ void __launch_bounds__(TX, 3) band_kernel(BandArgs a, const __grid_constant__ BandMaps maps, int ry) {
     SFB_PDL_PROLOGUE();
     using C = BandCfg<T, W>;
@@ -83,14 +84,15 @@ __global__ void __launch_bounds__(TX, 3) band_kernel(BandArgs a, const __grid_co
     constexpr int NPP = (NPAIR + 63) / 64;   // column pairs per thread in the transform
     constexpr int NRR = (CH + 1) / 2;        // rows per thread and chunk in the transform
     extern __shared__ double sm_raw[];       // NS x {A[CH][HCB], B[CH][HCB], G[T][CH][WP]}
-    double* sm = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(sm_raw) + 127) & ~uintptr_t(127));
+    // 128-byte aligned ring (pointer arithmetic on the shared array keeps LDS/STS addressing)
+    double* sm = sm_raw + (((128u - (smem_u32(sm_raw) & 127u)) & 127u) >> 3);
     __shared__ __align__(8) uint64_t full[NS];
 
-    const int mode = a.ld_mode;
+    constexpr int mode = MODE;
     PcgState* st = a.pcg;
     int s = 0;
     double beta = 0.0;
-    if (mode == LD_PCG) {
+    if constexpr (mode == LD_PCG) {
         if (st->status != SFB_PCG_RUNNING) return;  // uniform gate
         s = st->iter;
         if (s > 0) beta = st->rz_next / st->rz;      // solvers.py:448-452
@@ -107,15 +109,15 @@ __global__ void __launch_bounds__(TX, 3) band_kernel(BandArgs a, const __grid_co
     bool hasB = false;
     const CUtensorMap* mb = &maps.b[0];
     double* Qcur = nullptr;
-    if (mode == LD_PCG) {
+    if constexpr (mode == LD_PCG) {
         Qcur = (s & 1) ? a.Q1 : a.Q0;
         hasB = s > 0;
         mb = &maps.b[(s & 1) ? 0 : 1];  // previous direction
-    } else if (mode == LD_HEAT) {      // interior state U at offset (rs, cs): zero outside
+    } else if constexpr (mode == LD_HEAT) {  // interior state U at offset (rs, cs): zero outside
         ars = a.rs;
         acs = a.cs;
         hasB = a.X2 != nullptr;
-    } else if (mode == LD_DIB) {
+    } else if constexpr (mode == LD_DIB) {
         hasB = true;
     }
     // A's box starts at full-grid column x0 + hoff - shA (U column minus acs), B's at x0 + hoff - shB;
@@ -198,7 +200,7 @@ __global__ void __launch_bounds__(TX, 3) band_kernel(BandArgs a, const __grid_co
     for (int d = 0; d < W; ++d) acc[d] = cen[d] = 0.0;
     double pdot = 0.0, pqq = 0.0;
     const bool col_ok = gc < a.out_cols;
-    const bool pcg_ep = a.ep_mode == EP_PCG;
+    constexpr bool pcg_ep = mode == LD_PCG;
     double* const Wout = a.W;
     const int ldw = a.ldw;
     bool flag = false;
@@ -215,7 +217,7 @@ __global__ void __launch_bounds__(TX, 3) band_kernel(BandArgs a, const __grid_co
         const int r0 = k * CH;
         mbar_wait_u32(smem_u32(&full[k % NS]), (k / NS) & 1);
         // ---- input transform, in place (generic-proxy writes, fenced before the stage is refilled) ----
-        if (mode == LD_PCG) {
+        if constexpr (mode == LD_PCG) {
             const double b = beta;
             const bool upd = s > 0;
             const bool q16 = (hoff & 1) == 0;
@@ -237,7 +239,7 @@ __global__ void __launch_bounds__(TX, 3) band_kernel(BandArgs a, const __grid_co
                     }
                 }
             });
-        } else if (mode == LD_HEAT) {
+        } else if constexpr (mode == LD_HEAT) {
             const double cc = a.c;
             const bool chk = a.check != nullptr;
             const int in_rows = a.in_rows;
@@ -253,7 +255,7 @@ __global__ void __launch_bounds__(TX, 3) band_kernel(BandArgs a, const __grid_co
                     if (mdom[j] & 2u) check(v.y);
                 }
             });
-        } else if (mode == LD_DIB) {  // models.py:74-82 and timestepping.py:201-207
+        } else if constexpr (mode == LD_DIB) {  // models.py:74-82 and timestepping.py:201-207
             const double* p = a.kp;  // alpha, gamma_k, A1, A2, B, C, D, k2, k3
             const double cc = a.c;
             const bool sp0 = a.species == 0, chk = a.check != nullptr;
@@ -317,7 +319,7 @@ __global__ void __launch_bounds__(TX, 3) band_kernel(BandArgs a, const __grid_co
                 if ((unsigned)i < (unsigned)rows_here && col_ok) {
                     const double w = acc[slot];
                     Wout[(size_t)(y0 + i) * ldw + gc] = w;
-                    if (pcg_ep) {
+                    if constexpr (pcg_ep) {
                         // Q at (y0 + i, gc): centre of halo row i - goff = r - (W-1)/2
                         const double q = cen[(u - (W - 1) / 2 + W) % W];
                         pdot = fma(w, q, pdot);
@@ -333,7 +335,7 @@ __global__ void __launch_bounds__(TX, 3) band_kernel(BandArgs a, const __grid_co
         if (vmax > 0.0) atomicMax(a.check, (unsigned long long)__double_as_longlong(vmax));
     }
 
-    if (a.ep_mode == EP_PCG) {
+    if constexpr (pcg_ep) {
         __shared__ double sh[TX / 32];
         const unsigned nblk = gridDim.x * gridDim.y;
         const unsigned bid = blockIdx.y * gridDim.x + blockIdx.x;
@@ -362,13 +364,13 @@ __global__ void __launch_bounds__(TX, 3) band_kernel(BandArgs a, const __grid_co
     }
 }
 
-template <int T, int W>
-int launch_tw(const BandArgs& a, cudaStream_t stream) {
+template <int T, int W, int MODE>
+int launch_twm(const BandArgs& a, cudaStream_t stream) {
     using C = BandCfg<T, W>;
     constexpr int smem = C::SMEM;
     static bool attr = false;
     if (!attr) {
-        SFB_CUDA_TRY(cudaFuncSetAttribute(band_kernel<T, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        SFB_CUDA_TRY(cudaFuncSetAttribute(band_kernel<T, W, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         attr = true;
     }
     // tensor maps of the inputs (zero fill outside each source's extents)
@@ -399,9 +401,23 @@ int launch_tw(const BandArgs& a, cudaStream_t stream) {
     int ry, nrb;
     band_geometry(a.out_rows, a.out_cols, &ry, &nrb);
     dim3 grid((a.out_cols + TX - 1) / TX, nrb);
-    SFB_TRY(launch_kernel(band_kernel<T, W>, grid, dim3(TX), smem, stream, a, maps, ry));
+    SFB_TRY(launch_kernel(band_kernel<T, W, MODE>, grid, dim3(TX), smem, stream, a, maps, ry));
     SFB_CHECK_LAUNCH();
     return SFB_OK;
+}
+
+template <int T, int W>
+int launch_tw(const BandArgs& a, cudaStream_t stream) {
+    switch (a.ld_mode) {
+        case LD_PLAIN: return launch_twm<T, W, LD_PLAIN>(a, stream);
+        case LD_PCG: return launch_twm<T, W, LD_PCG>(a, stream);
+    }
+    if constexpr (T == 1) {  // the rhs maps are single-term
+        if (a.ld_mode == LD_HEAT) return launch_twm<T, W, LD_HEAT>(a, stream);
+        if (a.ld_mode == LD_DIB) return launch_twm<T, W, LD_DIB>(a, stream);
+    }
+    set_error("banded kernel: unsupported loader for this term count");
+    return SFB_ERR_UNSUPPORTED;
 }
 
 template <int T>
@@ -435,6 +451,7 @@ int launch_band(const BandArgs& a, cudaStream_t stream) {
         return SFB_ERR_UNSUPPORTED;
     }
     if (a.out_rows <= 0 || a.out_cols <= 0) return SFB_OK;
+    if ((a.ep_mode == EP_PCG) != (a.ld_mode == LD_PCG)) return arg_error("banded kernel: MO-PCG loader without its epilogue");
     if (a.ep_mode == EP_PCG && (a.goff != -(a.width - 1) / 2 || a.hoff != -(a.width - 1) / 2)) {
         set_error("banded kernel: the MO-PCG epilogue needs a centred square operator");
         return SFB_ERR_UNSUPPORTED;
