@@ -17,7 +17,8 @@ import numpy as np
 from .exceptions import OperatorError, SolverError, SylfemError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsylfem_b200.so")
+# SYLFEM_B200_LIB: an alternative in-tree build of the same library (kernel experiments)
+LIB_PATH = os.environ.get("SYLFEM_B200_LIB") or os.path.join(_HERE, "libsylfem_b200.so")
 
 # status codes / kinds (mirror include/sylfem_b200.h)
 OK, ERR_ARG, ERR_CUDA, ERR_NOMEM, ERR_UNSUPPORTED = 0, -1, -2, -3, -4

@@ -6,19 +6,24 @@
 // App. B), so each output element needs a (W x W) window of X.
 //
 // One CTA owns a TX-column strip of RY output rows (RY sized so the grid is
-// one wave of ~3 CTAs per SM).  It streams the (RY+W-1) x (TX+W-1) input
-// halo down the strip in chunks of CH rows through a 3-stage TMA ring (one
-// thread issues the boxes; out-of-bounds rows/columns arrive zero-filled),
-// together with the left-factor coefficients of those rows, read as a box
-// of the row-skewed copy gskew[t][j][d] = G_t[j-d][d] made at creation.  Each landed
-// chunk gets its input transform applied in shared memory (the MO-PCG
-// direction update Q = Z + beta Q, the IMEX heat source, or the DIB
-// kinetics), then every thread (one per output column, right-factor band in
-// registers) sweeps its rows: Y_t(r) = sum_e X[r][c+e] h_t[e] is formed once
-// per row and scattered into a ring of W partial outputs with the left-factor
-// coefficients (shared-memory broadcasts).  Loads of the next chunks overlap
-// the sweep of the current one.  Epilogues: plain store, or the MO-PCG store
-// + <W,Q>, |Q|^2 partials with a last-block alpha step (solvers.py:424-431).
+// one wave of 2-3 CTAs per SM).  A producer warp streams the (RY+W-1) x
+// (TX+W-1) input halo down the strip in chunks of CH rows through a 3-stage
+// TMA ring (full/empty mbarriers; out-of-bounds rows/columns arrive
+// zero-filled), together with the left-factor coefficients of those rows,
+// read as a box of the row-skewed copy gskew[t][j][d] = G_t[j-d][d] made at
+// creation.  Four consumer warps (one thread per output column, right-factor
+// band in registers) sweep the rows of each landed chunk: Y_t(r) =
+// sum_e X[r][c+e] h_t[e] is formed once per row and scattered into a ring of
+// W partial outputs with the left-factor coefficients (shared-memory
+// broadcasts).  The MO-PCG direction update Q = Z + beta Q is applied inline
+// as the halo values are read (the new Q column is stored by its owner); the
+// IMEX heat source and the DIB kinetics are applied to the landed chunk in
+// shared memory first (named barrier among the consumers).  Epilogues: plain
+// store, or the MO-PCG store + <W,Q>, |Q|^2 partials with a last-block alpha
+// step (solvers.py:424-431).
+//
+// Cost per output element: 2*T*W FMAs (the FP64 pipe bounds the plain
+// 5-term apply; the MO-PCG pass also moves four grids through HBM).
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
@@ -33,9 +38,18 @@ namespace sfb {
 
 namespace {
 
-constexpr int TX = 128;                   // output columns per CTA (one per thread)
-constexpr int NS = 3;                     // TMA ring stages
-constexpr int CTA_TARGET = 3 * kNumSMs;   // one wave of 3 CTAs per SM
+constexpr int TX = 128;                   // output columns per CTA (one consumer thread each)
+constexpr int NTH = TX + 32;              // + one producer warp
+#ifndef BAND_NS
+#define BAND_NS 3
+#endif
+#ifndef BAND_MINB
+#define BAND_MINB 3
+#endif
+constexpr int NS = BAND_NS;                       // TMA ring stages
+// CTAs per SM: the register budget of the widest bands (W >= 7) allows two
+template <int W>
+constexpr int band_minb() { return W >= 7 ? 2 : BAND_MINB; }
 constexpr int RY_MIN = 32;
 
 template <int W>
@@ -66,9 +80,10 @@ struct BandMaps {
 };
 
 // rows per CTA and row blocks for an output of `rows` x `cols`
-__host__ inline void band_geometry(int rows, int cols, int* ry, int* nrb) {
+// (one wave of `minb` CTAs per SM)
+__host__ inline void band_geometry(int rows, int cols, int minb, int* ry, int* nrb) {
     const int nstrips = (cols + TX - 1) / TX;
-    const int want = std::max(1, CTA_TARGET / nstrips);
+    const int want = std::max(1, minb * kNumSMs / nstrips);
     const int r = std::max(RY_MIN, (rows + want - 1) / want);
     *ry = r;
     *nrb = (rows + r - 1) / r;
@@ -76,7 +91,7 @@ __host__ inline void band_geometry(int rows, int cols, int* ry, int* nrb) {
 
 // MODE = the loader (LD_*); the MO-PCG loader always comes with the MO-PCG epilogue.
 template <int T, int W, int MODE>
-__global__ void __launch_bounds__(TX, 3) band_kernel(BandArgs a, const __grid_constant__ BandMaps maps, int ry) {
+__global__ void __launch_bounds__(TX + 32, band_minb<W>()) band_kernel(BandArgs a, const __grid_constant__ BandMaps maps, int ry) {
     SFB_PDL_PROLOGUE();
     using C = BandCfg<T, W>;
     constexpr int CH = C::CH, HCB = C::HCB, WP = C::WP;
@@ -86,9 +101,10 @@ __global__ void __launch_bounds__(TX, 3) band_kernel(BandArgs a, const __grid_co
     extern __shared__ double sm_raw[];       // NS x {A[CH][HCB], B[CH][HCB], G[T][CH][WP]}
     // 128-byte aligned ring (pointer arithmetic on the shared array keeps LDS/STS addressing)
     double* sm = sm_raw + (((128u - (smem_u32(sm_raw) & 127u)) & 127u) >> 3);
-    __shared__ __align__(8) uint64_t full[NS];
+    __shared__ __align__(8) uint64_t full[NS], empty[NS];
 
     constexpr int mode = MODE;
+    constexpr bool pcg_ep = mode == LD_PCG;
     PcgState* st = a.pcg;
     int s = 0;
     double beta = 0.0;
@@ -123,211 +139,204 @@ __global__ void __launch_bounds__(TX, 3) band_kernel(BandArgs a, const __grid_co
     // A's box starts at full-grid column x0 + hoff - shA (U column minus acs), B's at x0 + hoff - shB;
     // both even, so every box row is 16-byte aligned in global memory
     const int shA = (hoff - acs) & 1, shB = hoff & 1;
-    const int dbg = a.dbg;
-    const bool doA = !(dbg & 1), doG = !(dbg & 2);
-    if (dbg & 4) hasB = false;
-    const uint32_t tx_bytes = (uint32_t)(((hasB ? 1 : 0) + (doA ? 1 : 0)) * C::XS + (doG ? C::GS : 0)) * 8;
-
-    auto issue = [&](int k) {  // one thread
-        if (k < nch) {
-            const int sl = k % NS;
-            double* A = sm + sl * C::STAGE;
-            const uint32_t bar = smem_u32(&full[sl]);
-            const int r0 = k * CH;
-            if (dbg & 8) { asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory"); return; }
-            mbar_expect_tx_u32(bar, tx_bytes);
-            if (doA) tma_load_u32(smem_u32(A), &maps.a, bar, x0 + hoff - acs - shA, y0 + goff + r0 - ars);
-            if (hasB) tma_load_u32(smem_u32(A + C::XSP), mb, bar, x0 + hoff - shB, y0 + goff + r0);
-            if (doG) tma_load3_u32(smem_u32(A + 2 * C::XSP), &maps.g, bar, 0, y0 + r0, 0);
-        }
-    };
+    const uint32_t tx_bytes = (uint32_t)((hasB ? 2 : 1) * C::XS + C::GS) * 8;
+    const bool producer = t >= TX;  // warp 4 feeds the ring; warps 0-3 consume it
 
     if (t == 0) {
-        for (int i = 0; i < NS; ++i) mbar_init_u32(smem_u32(&full[i]), 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        #pragma unroll
-        for (int k = 0; k < NS - 1; ++k) issue(k);
-    }
-
-    // ---- per-thread transform geometry: smem column pairs pc, pc + 64 of rows rh, rh + 2, ...
-    // (A's column space: smem column m holds full-grid column x0 + hoff - shA + m) ----
-    const int pc = t & 63, rh = t >> 6;
-    unsigned mdom[NPP], mq[NPP];
-    int gxs[NPP];
-    #pragma unroll
-    for (int j = 0; j < NPP; ++j) {
-        const int pp = pc + 64 * j;
-        const int gx = x0 + hoff - shA + 2 * pp;
-        const bool has = pp < NPAIR;
-        auto pm = [](int col, int n) {
-            return ((unsigned)col < (unsigned)n ? 1u : 0u) | ((unsigned)(col + 1) < (unsigned)n ? 2u : 0u);
-        };
-        gxs[j] = gx;
-        // in the grid and in this CTA's halo (the box's extra columns stay out of the checks)
-        mdom[j] = has ? (pm(gx, a.in_cols) & pm(2 * pp - shA, C::HC)) : 0u;
-        mq[j] = has ? (pm(gx, a.in_cols) & pm(gx - x0, TX)) : 0u;
-    }
-    // visit this thread's pairs of a landed chunk: f(gr, j, double2* a_pair, const double* b_elems),
-    // b_elems = B at the same full-grid columns (16-byte aligned unless shA != shB: heat only)
-    auto for_pairs = [&](double* A, int r0, auto&& f) {
-        const double* B = A + C::XSP + (shB - shA);
-        #pragma unroll
-        for (int i = 0; i < NRR; ++i) {
-            const int rr = rh + 2 * i;
-            if (rr < CH) {
-                const int gr = y0 + goff + r0 + rr;
-                #pragma unroll
-                for (int j = 0; j < NPP; ++j) {
-                    if (j == 0 || pc + 64 * j < NPAIR) {
-                        const int o = rr * HCB + 2 * (pc + 64 * j);
-                        f(gr, j, reinterpret_cast<double2*>(A + o), B + o);
-                    }
-                }
-            }
+        for (int i = 0; i < NS; ++i) {
+            mbar_init_u32(smem_u32(&full[i]), 1);
+            mbar_init_u32(smem_u32(&empty[i]), TX / 32);  // one arrive per consumer warp
         }
-    };
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
 
-    // ---- right-factor band of this thread's column, in registers ----
-    double h[T][W];
-    #pragma unroll
-    for (int tt = 0; tt < T; ++tt)
-        #pragma unroll
-        for (int e = 0; e < W; ++e)
-            h[tt][e] = (tt < a.nterms && gc < a.out_cols) ? a.hband[((size_t)tt * a.out_cols + gc) * W + e] : 0.0;
-
-    double acc[W], cen[W];
-    #pragma unroll
-    for (int d = 0; d < W; ++d) acc[d] = cen[d] = 0.0;
     double pdot = 0.0, pqq = 0.0;
-    const bool col_ok = gc < a.out_cols;
-    constexpr bool pcg_ep = mode == LD_PCG;
-    double* const Wout = a.W;
-    const int ldw = a.ldw;
     bool flag = false;
     double vmax = 0.0;
-    auto check = [&](double v) {
-        if (!isfinite(v)) flag = true;
-        else vmax = fmax(vmax, fabs(v));
-    };
-    __syncthreads();  // barrier init visible
-
-    for (int k = 0; k < nch; ++k) {
-        double* A = sm + (k % NS) * C::STAGE;
-        const double* G = A + 2 * C::XSP;
-        const int r0 = k * CH;
-        mbar_wait_u32(smem_u32(&full[k % NS]), (k / NS) & 1);
-        // ---- input transform, in place (generic-proxy writes, fenced before the stage is refilled) ----
-        if constexpr (mode == LD_PCG) {
-            const double b = beta;
-            const bool upd = s > 0;
-            const bool q16 = (hoff & 1) == 0;
-            for_pairs(A, r0, [&](int gr, int j, double2* ap, const double* bp) {
-                double2 v = *ap;
-                if (upd) {
-                    const double2 q = *reinterpret_cast<const double2*>(bp);
-                    v.x = __dadd_rn(__dmul_rn(b, q.x), v.x);  // Q*=beta; Q+=Z
-                    v.y = __dadd_rn(__dmul_rn(b, q.y), v.y);
-                    *ap = v;
-                }
-                if (gr >= y0 && gr < y0 + rows_here) {
-                    double* qp = Qcur + (size_t)gr * a.ldq + gxs[j];
-                    const unsigned m = mq[j];
-                    if (q16 && m == 3u) *reinterpret_cast<double2*>(qp) = v;
-                    else {
-                        if (m & 1u) qp[0] = v.x;
-                        if (m & 2u) qp[1] = v.y;
-                    }
-                }
-            });
-        } else if constexpr (mode == LD_HEAT) {
-            const double cc = a.c;
-            const bool chk = a.check != nullptr;
-            const int in_rows = a.in_rows;
-            for_pairs(A, r0, [&](int gr, int j, double2* ap, const double* bp) {
-                double2 v = *ap;
-                if (hasB) {
-                    v.x = v.x + cc * bp[0];
-                    v.y = v.y + cc * bp[1];
-                    *ap = v;
-                }
-                if (chk && (unsigned)gr < (unsigned)in_rows) {
-                    if (mdom[j] & 1u) check(v.x);
-                    if (mdom[j] & 2u) check(v.y);
-                }
-            });
-        } else if constexpr (mode == LD_DIB) {  // models.py:74-82 and timestepping.py:201-207
-            const double* p = a.kp;  // alpha, gamma_k, A1, A2, B, C, D, k2, k3
-            const double cc = a.c;
-            const bool sp0 = a.species == 0, chk = a.check != nullptr;
-            const int in_rows = a.in_rows;
-            for_pairs(A, r0, [&](int gr, int j, double2* ap, const double* bp) {
-                const double2 e2 = *ap, t2 = *reinterpret_cast<const double2*>(bp);
-                const unsigned m = (unsigned)gr < (unsigned)in_rows ? mdom[j] : 0u;
-                double v[2];
-                const double ev[2] = {e2.x, e2.y}, tv[2] = {t2.x, t2.y};
-                #pragma unroll
-                for (int q = 0; q < 2; ++q) {
-                    const double eta = ev[q], th = tv[q];
-                    double r;
-                    if (sp0) {
-                        const double f = p[2] * (1.0 - th) * eta - p[3] * (eta * eta * eta) - p[4] * (th - p[0]);
-                        r = eta + cc * f;
-                    } else {
-                        const double g = p[5] * (1.0 + p[7] * eta) * (1.0 - th) * (1.0 - p[1] * (1.0 - th)) -
-                                         p[6] * th * (1.0 + p[1] * th) * (1.0 + p[8] * eta);
-                        r = th + cc * g;
-                    }
-                    v[q] = (m >> q) & 1u ? r : 0.0;  // outside the grid the halo is zero
-                    if (chk && ((m >> q) & 1u)) check(v[q]);
-                }
-                *ap = make_double2(v[0], v[1]);
-            });
+    if (producer) {
+        if (t == TX) {
+            for (int k = 0; k < nch; ++k) {
+                const int sl = k % NS;
+                if (k >= NS) mbar_wait_u32(smem_u32(&empty[sl]), ((k / NS) - 1) & 1);
+                double* A = sm + sl * C::STAGE;
+                const uint32_t bar = smem_u32(&full[sl]);
+                const int r0 = k * CH;
+                mbar_expect_tx_u32(bar, tx_bytes);
+                tma_load_u32(smem_u32(A), &maps.a, bar, x0 + hoff - acs - shA, y0 + goff + r0 - ars);
+                if (hasB) tma_load_u32(smem_u32(A + C::XSP), mb, bar, x0 + hoff - shB, y0 + goff + r0);
+                tma_load3_u32(smem_u32(A + 2 * C::XSP), &maps.g, bar, 0, y0 + r0, 0);
+            }
         }
-        fence_proxy_async_smem();
-        __syncthreads();  // transform visible; every thread is done with chunk k-1
-        if (t == 0) issue(k + NS - 1);  // refill the stage chunk k-1 used
-
-        // ---- sweep the chunk's halo rows (rows past the halo feed only unstored outputs) ----
-        #pragma unroll 1
-        for (int m = 0; m < CH / W; ++m) {
+    } else {
+        // ---- HEAT / DIB: per-thread transform geometry, smem column pairs pc, pc + 64 of rows rh, rh + 2, ...
+        // (A's column space: smem column m holds full-grid column x0 + hoff - shA + m) ----
+        const int pc = t & 63, rh = t >> 6;
+        unsigned mdom[NPP];
+        #pragma unroll
+        for (int j = 0; j < NPP; ++j) {
+            const int pp = pc + 64 * j;
+            const int gx = x0 + hoff - shA + 2 * pp;
+            auto pm = [](int col, int n) {
+                return ((unsigned)col < (unsigned)n ? 1u : 0u) | ((unsigned)(col + 1) < (unsigned)n ? 2u : 0u);
+            };
+            // in the grid and in this CTA's halo (the box's extra columns stay out of the checks)
+            mdom[j] = pp < NPAIR ? (pm(gx, a.in_cols) & pm(2 * pp - shA, C::HC)) : 0u;
+        }
+        // visit this thread's pairs of a landed chunk: f(gr, j, double2* a_pair, const double* b_elems),
+        // b_elems = B at the same full-grid columns (16-byte aligned unless shA != shB: heat only)
+        auto for_pairs = [&](double* A, int r0, auto&& f) {
+            const double* B = A + C::XSP + (shB - shA);
             #pragma unroll
-            for (int u = 0; u < W; ++u) {
-                const int rr = m * W + u;  // r0 + rr == u (mod W)
-                double qv[W];
-                #pragma unroll
-                for (int e = 0; e < W; ++e) qv[e] = A[rr * HCB + shA + c + e];
-                cen[u] = qv[(W - 1) / 2];
-                #pragma unroll
-                for (int tt = 0; tt < T; ++tt) {
-                    double y = 0.0;
+            for (int i = 0; i < NRR; ++i) {
+                const int rr = rh + 2 * i;
+                if (rr < CH) {
+                    const int gr = y0 + goff + r0 + rr;
                     #pragma unroll
-                    for (int e = 0; e < W; ++e) y = fma(qv[e], h[tt][e], y);
-                    const double2* gp = reinterpret_cast<const double2*>(G + (tt * CH + rr) * WP);
-                    #pragma unroll
-                    for (int dd = 0; dd < WP / 2; ++dd) {
-                        const double2 g = gp[dd];
-                        const int s0 = (u - 2 * dd + 2 * W) % W;
-                        acc[s0] = fma(g.x, y, acc[s0]);
-                        if (2 * dd + 1 < W) {
-                            const int s1 = (u - 2 * dd - 1 + 2 * W) % W;
-                            acc[s1] = fma(g.y, y, acc[s1]);
+                    for (int j = 0; j < NPP; ++j) {
+                        if (j == 0 || pc + 64 * j < NPAIR) {
+                            const int o = rr * HCB + 2 * (pc + 64 * j);
+                            f(gr, j, reinterpret_cast<double2*>(A + o), B + o);
                         }
                     }
                 }
-                const int i = r0 + rr - (W - 1);
-                const int slot = (u + 1) % W;
-                if ((unsigned)i < (unsigned)rows_here && col_ok) {
-                    const double w = acc[slot];
-                    Wout[(size_t)(y0 + i) * ldw + gc] = w;
-                    if constexpr (pcg_ep) {
-                        // Q at (y0 + i, gc): centre of halo row i - goff = r - (W-1)/2
-                        const double q = cen[(u - (W - 1) / 2 + W) % W];
-                        pdot = fma(w, q, pdot);
-                        pqq = fma(q, q, pqq);
-                    }
-                }
-                acc[slot] = 0.0;
             }
+        };
+        auto check = [&](double v) {
+            if (!isfinite(v)) flag = true;
+            else vmax = fmax(vmax, fabs(v));
+        };
+
+        // ---- right-factor band of this thread's column, in registers ----
+        double h[T][W];
+        #pragma unroll
+        for (int tt = 0; tt < T; ++tt)
+            #pragma unroll
+            for (int e = 0; e < W; ++e)
+                h[tt][e] = (tt < a.nterms && gc < a.out_cols) ? a.hband[((size_t)tt * a.out_cols + gc) * W + e] : 0.0;
+
+        double acc[W], cen[W];
+        #pragma unroll
+        for (int d = 0; d < W; ++d) acc[d] = cen[d] = 0.0;
+        const bool col_ok = gc < a.out_cols;
+        double* const Wout = a.W;
+        const int ldw = a.ldw;
+        const bool upd = hasB;  // PCG: Q = Z + beta Qprev from the second iteration on
+
+        for (int k = 0; k < nch; ++k) {
+            const int sl = k % NS;
+            double* A = sm + sl * C::STAGE;
+            const double* Bs = A + C::XSP;
+            const double* G = A + 2 * C::XSP;
+            const int r0 = k * CH;
+            mbar_wait_u32(smem_u32(&full[sl]), (k / NS) & 1);
+            // ---- HEAT / DIB input transform, in place; consumers sync on named barrier 1 ----
+            if constexpr (mode == LD_HEAT) {
+                const double cc = a.c;
+                const bool chk = a.check != nullptr;
+                const int in_rows = a.in_rows;
+                for_pairs(A, r0, [&](int gr, int j, double2* ap, const double* bp) {
+                    double2 v = *ap;
+                    if (hasB) {
+                        v.x = v.x + cc * bp[0];
+                        v.y = v.y + cc * bp[1];
+                        *ap = v;
+                    }
+                    if (chk && (unsigned)gr < (unsigned)in_rows) {
+                        if (mdom[j] & 1u) check(v.x);
+                        if (mdom[j] & 2u) check(v.y);
+                    }
+                });
+            } else if constexpr (mode == LD_DIB) {  // models.py:74-82 and timestepping.py:201-207
+                const double* p = a.kp;  // alpha, gamma_k, A1, A2, B, C, D, k2, k3
+                const double cc = a.c;
+                const bool sp0 = a.species == 0, chk = a.check != nullptr;
+                const int in_rows = a.in_rows;
+                for_pairs(A, r0, [&](int gr, int j, double2* ap, const double* bp) {
+                    const double2 e2 = *ap, t2 = *reinterpret_cast<const double2*>(bp);
+                    const unsigned m = (unsigned)gr < (unsigned)in_rows ? mdom[j] : 0u;
+                    double v[2];
+                    const double ev[2] = {e2.x, e2.y}, tv[2] = {t2.x, t2.y};
+                    #pragma unroll
+                    for (int q = 0; q < 2; ++q) {
+                        const double eta = ev[q], th = tv[q];
+                        double r;
+                        if (sp0) {
+                            const double f = p[2] * (1.0 - th) * eta - p[3] * (eta * eta * eta) - p[4] * (th - p[0]);
+                            r = eta + cc * f;
+                        } else {
+                            const double g = p[5] * (1.0 + p[7] * eta) * (1.0 - th) * (1.0 - p[1] * (1.0 - th)) -
+                                             p[6] * th * (1.0 + p[1] * th) * (1.0 + p[8] * eta);
+                            r = th + cc * g;
+                        }
+                        v[q] = (m >> q) & 1u ? r : 0.0;  // outside the grid the halo is zero
+                        if (chk && ((m >> q) & 1u)) check(v[q]);
+                    }
+                    *ap = make_double2(v[0], v[1]);
+                });
+            }
+            if constexpr (mode == LD_HEAT || mode == LD_DIB)
+                asm volatile("bar.sync 1, %0;" ::"n"(TX) : "memory");  // transformed chunk visible
+
+            // ---- sweep the chunk's halo rows (rows past the halo feed only unstored outputs) ----
+            #pragma unroll 1
+            for (int m = 0; m < CH / W; ++m) {
+                #pragma unroll
+                for (int u = 0; u < W; ++u) {
+                    const int rr = m * W + u;  // r0 + rr == u (mod W)
+                    // Y_t(row) = sum_e X[row][c+e] h_t[e]: one input value live at a
+                    // time, T independent chains
+                    double y[T];
+                    #pragma unroll
+                    for (int tt = 0; tt < T; ++tt) y[tt] = 0.0;
+                    #pragma unroll
+                    for (int e = 0; e < W; ++e) {
+                        const double z = A[rr * HCB + shA + c + e];
+                        double q = z;
+                        if constexpr (mode == LD_PCG)  // Q*=beta; Q+=Z (solvers.py:448-452), inline
+                            q = upd ? __dadd_rn(__dmul_rn(beta, Bs[rr * HCB + shA + c + e]), z) : z;
+                        if (e == (W - 1) / 2) cen[u] = q;
+                        #pragma unroll
+                        for (int tt = 0; tt < T; ++tt) y[tt] = fma(q, h[tt][e], y[tt]);
+                    }
+                    if constexpr (mode == LD_PCG) {
+                        // this thread's column of the new direction, interior rows only
+                        const int gr = y0 + goff + r0 + rr;
+                        if (gr >= y0 && gr < y0 + rows_here && col_ok) Qcur[(size_t)gr * a.ldq + gc] = cen[u];
+                    }
+                    #pragma unroll
+                    for (int tt = 0; tt < T; ++tt) {
+                        const double2* gp = reinterpret_cast<const double2*>(G + (tt * CH + rr) * WP);
+                        #pragma unroll
+                        for (int dd = 0; dd < WP / 2; ++dd) {
+                            const double2 g = gp[dd];
+                            const int s0 = (u - 2 * dd + 2 * W) % W;
+                            acc[s0] = fma(g.x, y[tt], acc[s0]);
+                            if (2 * dd + 1 < W) {
+                                const int s1 = (u - 2 * dd - 1 + 2 * W) % W;
+                                acc[s1] = fma(g.y, y[tt], acc[s1]);
+                            }
+                        }
+                    }
+                    const int i = r0 + rr - (W - 1);
+                    const int slot = (u + 1) % W;
+                    if ((unsigned)i < (unsigned)rows_here && col_ok) {
+                        const double w = acc[slot];
+                        Wout[(size_t)(y0 + i) * ldw + gc] = w;
+                        if constexpr (pcg_ep) {
+                            // Q at (y0 + i, gc): centre of halo row i - goff = r - (W-1)/2
+                            const double q = cen[(u - (W - 1) / 2 + W) % W];
+                            pdot = fma(w, q, pdot);
+                            pqq = fma(q, q, pqq);
+                        }
+                    }
+                    acc[slot] = 0.0;
+                }
+            }
+            // release the stage to the producer (generic writes ordered before the TMA refill)
+            if constexpr (mode == LD_HEAT || mode == LD_DIB) fence_proxy_async_smem();
+            __syncwarp();
+            if ((t & 31) == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[sl])) : "memory");
         }
     }
     if (a.check != nullptr) {
@@ -336,18 +345,18 @@ __global__ void __launch_bounds__(TX, 3) band_kernel(BandArgs a, const __grid_co
     }
 
     if constexpr (pcg_ep) {
-        __shared__ double sh[TX / 32];
+        __shared__ double sh[NTH / 32];
         const unsigned nblk = gridDim.x * gridDim.y;
         const unsigned bid = blockIdx.y * gridDim.x + blockIdx.x;
-        const double p0 = block_sum<TX>(pdot, sh);
-        const double p1 = block_sum<TX>(pqq, sh);
+        const double p0 = block_sum<NTH>(pdot, sh);
+        const double p1 = block_sum<NTH>(pqq, sh);
         if (threadIdx.x == 0) {
             a.partials[bid] = p0;
             a.partials[nblk + bid] = p1;
         }
         if (arrive_last(&st->counter[0], nblk)) {
-            const double qw = sum_partials<TX>(a.partials, nblk, 1, sh);
-            const double qq = sum_partials<TX>(a.partials + nblk, nblk, 1, sh);
+            const double qw = sum_partials<NTH>(a.partials, nblk, 1, sh);
+            const double qq = sum_partials<NTH>(a.partials + nblk, nblk, 1, sh);
             if (threadIdx.x == 0) {
                 st->counter[0] = 0;
                 st->rz = st->rz_next;
@@ -399,9 +408,9 @@ int launch_twm(const BandArgs& a, cudaStream_t stream) {
         SFB_TRY(tma_make_map(&maps.g, a.gskew, 3, dims, C::WP, gbox, CU_TENSOR_MAP_SWIZZLE_NONE));
     }
     int ry, nrb;
-    band_geometry(a.out_rows, a.out_cols, &ry, &nrb);
+    band_geometry(a.out_rows, a.out_cols, band_minb<W>(), &ry, &nrb);
     dim3 grid((a.out_cols + TX - 1) / TX, nrb);
-    SFB_TRY(launch_kernel(band_kernel<T, W, MODE>, grid, dim3(TX), smem, stream, a, maps, ry));
+    SFB_TRY(launch_kernel(band_kernel<T, W, MODE>, grid, dim3(NTH), smem, stream, a, maps, ry));
     SFB_CHECK_LAUNCH();
     return SFB_OK;
 }
@@ -439,9 +448,9 @@ bool band_supported(int nterms, int width) {
     return nterms >= 1 && nterms <= 5 && width >= 1 && width <= 9 && (width % 2) == 1;
 }
 
-int band_grid_blocks(int out_rows, int out_cols) {
+int band_grid_blocks(int out_rows, int out_cols) {  // upper bound over band widths
     int ry, nrb;
-    band_geometry(out_rows, out_cols, &ry, &nrb);
+    band_geometry(out_rows, out_cols, std::max(BAND_MINB, 2), &ry, &nrb);
     return ((out_cols + TX - 1) / TX) * nrb;
 }
 
@@ -459,7 +468,6 @@ int launch_band(const BandArgs& a, cudaStream_t stream) {
     if (a.gskew == nullptr || a.gskew_rows != a.out_rows + a.width - 1)
         return arg_error("banded kernel: missing skewed left-factor coefficients");
     BandArgs b = a;
-    if (const char* e = std::getenv("SYLFEM_B200_BAND_DBG")) b.dbg = std::atoi(e);
     if (a.nterms == 1) return launch_t<1>(b, stream);
     if (a.nterms == 2) return launch_t<2>(b, stream);
     return launch_t<5>(b, stream);

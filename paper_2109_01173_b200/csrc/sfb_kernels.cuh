@@ -50,7 +50,6 @@ struct BandArgs {
     const double* gband = nullptr;  // [nterms][out_rows][width]
     const double* gskew = nullptr;  // [nterms][gskew_rows][width + 1] (band_skew)
     int gskew_rows = 0;             // out_rows + width - 1
-    int dbg = 0;
     const double* hband = nullptr;  // [nterms][out_cols][width]
     // loader
     int ld_mode = LD_PLAIN;

@@ -213,17 +213,39 @@ __global__ void __launch_bounds__(VT) pcg_record_kernel(const double* U, int ld,
     }
 }
 
-__global__ void __launch_bounds__(VT) copy_dot_kernel(const double* R, double* Z, int ld, int rows, int cols,
-                                                      double* partials, PcgState* st, double* dot_out,
-                                                      unsigned* counter) {
+__global__ void __launch_bounds__(VT) copy_dot_kernel(const double* __restrict__ R, double* __restrict__ Z, int ld,
+                                                      int rows, int cols, double* partials, PcgState* st,
+                                                      double* dot_out, unsigned* counter) {
     SFB_PDL_PROLOGUE();
     if (st != nullptr && st->status != SFB_PCG_RUNNING) return;
     double zr = 0.0;
-    ROW_LOOP(rows, cols) {
-        const size_t o = (size_t)r * ld + cc;
-        const double v = R[o];
-        Z[o] = v;
-        zr = fma(v, v, zr);
+    const bool vec = (ld & 1) == 0 && ((reinterpret_cast<uintptr_t>(R) | reinterpret_cast<uintptr_t>(Z)) & 15) == 0;
+    if (vec) {
+        // 16-byte pairs per row; several loads in flight per thread
+        const int np = cols / 2;
+        for (int r = blockIdx.x; r < rows; r += gridDim.x) {
+            const double2* R2 = reinterpret_cast<const double2*>(R + (size_t)r * ld);
+            double2* Z2 = reinterpret_cast<double2*>(Z + (size_t)r * ld);
+            #pragma unroll 4
+            for (int q = threadIdx.x; q < np; q += VT) {
+                const double2 v = R2[q];
+                Z2[q] = v;
+                zr = fma(v.x, v.x, zr);
+                zr = fma(v.y, v.y, zr);
+            }
+            if ((cols & 1) && threadIdx.x == 0) {
+                const double v = R[(size_t)r * ld + cols - 1];
+                Z[(size_t)r * ld + cols - 1] = v;
+                zr = fma(v, v, zr);
+            }
+        }
+    } else {
+        ROW_LOOP(rows, cols) {
+            const size_t o = (size_t)r * ld + cc;
+            const double v = R[o];
+            Z[o] = v;
+            zr = fma(v, v, zr);
+        }
     }
     __shared__ double sh[VT / 32];
     const double p = block_sum<VT>(zr, sh);
