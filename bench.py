@@ -392,6 +392,34 @@ def run_native(args):
         except (OSError, ValueError):
             traffic = None
 
+    # ---- HBM roofline of the memory-bound passes of the headline iteration
+    #      (banded pass 32q^2 B incl. the direction update,
+    #      vector update 48q^2 B), timed per launch on the solver's buffers ----
+    hbm = None
+    if world == 1 and op.banded:
+        pt = pb.solvers.pcg_pass_times(op, pre, reps=20)
+        hbm_peak, hbm_src = 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+        try:
+            mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+            if mp.get("hbm_gbs"):
+                hbm_peak, hbm_src = float(mp["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (copy, burst)"
+        except (OSError, ValueError):
+            pass
+        n2 = qy * qx * 8
+        band_gbs = 4 * n2 / (pt["operator_ms"] * 1e-3) / 1e9
+        upd_gbs = 6 * n2 / (pt["update_ms"] * 1e-3) / 1e9
+        hbm = {"bound": "hbm", "unit": "GB/s", "peak": hbm_peak, "peak_source": hbm_src,
+               "banded_operator_pass": {
+                   "kernel": f"band_kernel<{len(op)} terms, W={2 * op.half_bandwidth + 1}> (LD_PCG)",
+                   "achieved": band_gbs, "frac": band_gbs / hbm_peak, "launch_ms": pt["operator_ms"],
+                   "algorithmic_bytes": 4 * n2,
+                   "note": "read Z, Q_prev; write Q, W (+ <W,Q>, |Q|^2); 2*T*W FMAs per element on the FP64 pipe"},
+               "vector_update_pass": {
+                   "kernel": "pcg_update_kernel", "achieved": upd_gbs, "frac": upd_gbs / hbm_peak,
+                   "launch_ms": pt["update_ms"], "algorithmic_bytes": 6 * n2,
+                   "note": "read U, R, Q, W; write U, R (+ |R|^2, stop test)"},
+               "preconditioner_ms": pt["preconditioner_ms"]}
+
     # ---- CPU baseline (rank 0, N = 1 only) ----
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -422,6 +450,7 @@ def run_native(args):
                          "launch_ms": t_gemm * 1e3, "peak_source": "cuBLAS DGEMM 8192^3 measured in this run",
                          "cublas_same_shape_tflops": cublas_same,
                          "share_of_iteration": share, "iteration_ms": iter_ms},
+            "roofline_hbm": hbm,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": per_step_launches * args.steps,

@@ -159,6 +159,12 @@ int sfb_pcg_solve(sfb_pcg* s, const double* rhs_dev, int ldr,
                   double* history_host, double* increments_host,
                   double* iterates_dev, int n_iterates,
                   sfb_pcg_result* res, void* stream);
+/* Device time (ms per launch, averaged over `reps` back-to-back launches)
+ * of the passes of one MO-PCG iteration on the solver's buffers, for the
+ * roofline report: ms[0] banded operator pass, ms[1] vector update pass,
+ * ms[2] preconditioner.  Call after a solve; clobbers the solver buffers.
+ * Measurement only: no reference counterpart. */
+int sfb_pcg_pass_times(sfb_pcg* s, int reps, double* ms);
 int sfb_pcg_destroy(sfb_pcg* s);
 
 /* ---- FP64 tensor-core GEMM (the kernel behind every spectral / inverse

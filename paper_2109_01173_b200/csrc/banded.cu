@@ -44,10 +44,12 @@ constexpr int NTH = TX + 32;              // + one producer warp
 #define BAND_NS 3
 #endif
 #ifndef BAND_MINB
-#define BAND_MINB 3
+#define BAND_MINB 2
 #endif
+
 constexpr int NS = BAND_NS;                       // TMA ring stages
-// CTAs per SM: the register budget of the widest bands (W >= 7) allows two
+// CTAs per SM (2 x 5 warps: 168 registers per thread keep the 5-term band
+// in registers; measured faster than 3 CTAs at 128 registers)
 template <int W>
 constexpr int band_minb() { return W >= 7 ? 2 : BAND_MINB; }
 constexpr int RY_MIN = 32;
@@ -183,6 +185,7 @@ __global__ void __launch_bounds__(TX + 32, band_minb<W>()) band_kernel(BandArgs 
             // in the grid and in this CTA's halo (the box's extra columns stay out of the checks)
             mdom[j] = pp < NPAIR ? (pm(gx, a.in_cols) & pm(2 * pp - shA, C::HC)) : 0u;
         }
+        constexpr bool smem_pass = mode == LD_HEAT || mode == LD_DIB;
         // visit this thread's pairs of a landed chunk: f(gr, j, double2* a_pair, const double* b_elems),
         // b_elems = B at the same full-grid columns (16-byte aligned unless shA != shB: heat only)
         auto for_pairs = [&](double* A, int r0, auto&& f) {
@@ -230,7 +233,7 @@ __global__ void __launch_bounds__(TX + 32, band_minb<W>()) band_kernel(BandArgs 
             const double* G = A + 2 * C::XSP;
             const int r0 = k * CH;
             mbar_wait_u32(smem_u32(&full[sl]), (k / NS) & 1);
-            // ---- HEAT / DIB input transform, in place; consumers sync on named barrier 1 ----
+            // ---- input transform, in place; consumers sync on named barrier 1 ----
             if constexpr (mode == LD_HEAT) {
                 const double cc = a.c;
                 const bool chk = a.check != nullptr;
@@ -275,7 +278,7 @@ __global__ void __launch_bounds__(TX + 32, band_minb<W>()) band_kernel(BandArgs 
                     *ap = make_double2(v[0], v[1]);
                 });
             }
-            if constexpr (mode == LD_HEAT || mode == LD_DIB)
+            if constexpr (smem_pass)
                 asm volatile("bar.sync 1, %0;" ::"n"(TX) : "memory");  // transformed chunk visible
 
             // ---- sweep the chunk's halo rows (rows past the halo feed only unstored outputs) ----
@@ -334,7 +337,7 @@ __global__ void __launch_bounds__(TX + 32, band_minb<W>()) band_kernel(BandArgs 
                 }
             }
             // release the stage to the producer (generic writes ordered before the TMA refill)
-            if constexpr (mode == LD_HEAT || mode == LD_DIB) fence_proxy_async_smem();
+            if constexpr (smem_pass) fence_proxy_async_smem();
             __syncwarp();
             if ((t & 31) == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[sl])) : "memory");
         }

@@ -10,6 +10,7 @@
 #include <cuda.h>
 
 #include <cstdlib>
+#include <functional>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -1137,6 +1138,92 @@ int sfb_pcg_solve(sfb_pcg* s, const double* rhs, int ldr, const double* u0, int 
         res->res0 = fin.res0;
         res->bad_value = fin.bad_value;
         res->device_ms = ms;
+    }
+    return SFB_OK;
+}
+
+// Device time of each pass of one MO-PCG iteration, launched `reps` times
+// back to back on the solver's stream over its own buffers (after a solve):
+// ms[0] banded operator pass (direction update + W = L(Q) + <W,Q>, |Q|^2),
+// ms[1] vector update pass (U, R, |R|), ms[2] preconditioner.  A scratch
+// state keeps the gates open; the solver's buffers are clobbered (the next
+// solve re-initialises them).
+int sfb_pcg_pass_times(sfb_pcg* s, int reps, double* ms) {
+    if (!s || !ms || reps <= 0) return arg_error("pass timing needs a solver, reps > 0 and 3 outputs");
+    if (s->op->dense) {
+        set_error("pass timing covers the banded operator");
+        return SFB_ERR_UNSUPPORTED;
+    }
+    std::lock_guard<std::mutex> lock(s->mu);
+    cudaStream_t st = s->stream;
+    ScopedFree tmp(st);
+    PcgState* ps;
+    double *hist, *incs;
+    const int cap = 2 * reps + 8;
+    SFB_TRY(tmp.get(&ps, sizeof(PcgState)));
+    SFB_TRY(tmp.get(&hist, (size_t)cap * 8));
+    SFB_TRY(tmp.get(&incs, (size_t)cap * 8));
+    PcgState h;
+    std::memset(&h, 0, sizeof(h));
+    h.status = SFB_PCG_RUNNING;
+    h.iter = 1;
+    h.max_iter = 1 << 30;
+    h.rule = SFB_RULE_RESIDUAL;
+    h.value = 0.0;
+    h.res0 = 1.0;
+    h.rz = h.rz_next = 1.0;
+    h.recorded = -1;
+    SFB_CUDA_TRY(cudaMemcpyAsync(ps, &h, sizeof(h), cudaMemcpyHostToDevice, st));
+    const sfb_op* op = s->op;
+    BandArgs a;
+    a.out_rows = a.in_rows = s->qy;
+    a.out_cols = a.in_cols = s->qx;
+    a.nterms = op->nterms;
+    a.width = op->width;
+    a.goff = op->goff;
+    a.hoff = op->hoff;
+    a.gband = op->gband;
+    a.gskew = op->gskew;
+    a.gskew_rows = op->qy + op->width - 1;
+    a.hband = op->hband;
+    a.ld_mode = LD_PCG;
+    a.X = s->Z;
+    a.ldx = s->ld;
+    a.Q0 = s->Q0;
+    a.Q1 = s->Q1;
+    a.ldq = s->ld;
+    a.ep_mode = EP_PCG;
+    a.W = s->W;
+    a.ldw = s->ld;
+    a.partials = s->partials;
+    a.pcg = ps;
+    auto band = [&]() { return launch_band(a, st); };
+    auto update = [&]() {
+        return launch_pcg_update(s->U, s->R, s->W, s->Q0, s->Q1, s->ld, s->qy, s->qx, s->partials, ps, hist, incs, st);
+    };
+    auto pre = [&]() {
+        return pre_apply_impl(s->pre, s->R, s->ld, s->Z, s->ld, s->T1, s->ldt1, s->T2, s->ldt2, s->partials, ps,
+                              nullptr, &s->gw, st);
+    };
+    std::function<int()> passes[3] = {band, update, pre};
+    for (int k = 0; k < 3; ++k) {
+        // reset the iteration counter so the update's history slots stay in range
+        SFB_CUDA_TRY(cudaMemcpyAsync(ps, &h, sizeof(h), cudaMemcpyHostToDevice, st));
+        SFB_TRY(passes[k]());  // warm
+        SFB_CUDA_TRY(cudaEventRecord(s->ev_t0, st));
+        for (int r = 0; r < reps; ++r) SFB_TRY(passes[k]());
+        SFB_CUDA_TRY(cudaEventRecord(s->ev_t1, st));
+        SFB_CUDA_TRY(cudaEventSynchronize(s->ev_t1));
+        float el = 0.f;
+        SFB_CUDA_TRY(cudaEventElapsedTime(&el, s->ev_t0, s->ev_t1));
+        ms[k] = (double)el / reps;
+    }
+    PcgState after;
+    SFB_CUDA_TRY(cudaMemcpyAsync(&after, ps, sizeof(after), cudaMemcpyDeviceToHost, st));
+    SFB_CUDA_TRY(cudaStreamSynchronize(st));
+    if (after.status != SFB_PCG_RUNNING) {
+        set_error("pass timing: a gate closed during the run (status " + std::to_string(after.status) + ")");
+        return SFB_ERR_CUDA;
     }
     return SFB_OK;
 }

@@ -593,6 +593,20 @@ def _solver_for(op: SylvesterOperator, pre: Preconditioner) -> _PcgSolver:
     return s
 
 
+def pcg_pass_times(op: SylvesterOperator, precond: Preconditioner | None = None, reps: int = 20) -> dict:
+    """Device ms per launch of the passes of one MO-PCG iteration (banded
+    operator, vector update, preconditioner) on the solver that `mo_pcg`
+    built for (op, precond); call after a solve.  Measurement helper for the
+    roofline report (no reference counterpart)."""
+    precond = precond if precond is not None else Preconditioner()
+    s = op._pcg_cache.get(id(precond))
+    if s is None or s.pre is not precond:
+        raise SolverError("pcg_pass_times needs a prior mo_pcg solve with this operator and preconditioner")
+    ms = np.zeros(3)
+    nat.check(nat.lib().sfb_pcg_pass_times(s.handle.p, int(reps), nat.dptr(ms)), "pass timing")
+    return {"operator_ms": float(ms[0]), "update_ms": float(ms[1]), "preconditioner_ms": float(ms[2])}
+
+
 def mo_pcg(op: SylvesterOperator, rhs, precond: Preconditioner | None = None,
            stop: StoppingRule | None = None, u0=None, max_iter: int = DEFAULT_MAX_ITER,
            record_iterates: bool = False) -> SolveReport:
