@@ -47,15 +47,20 @@ enum { PH_FWD = 0, PH_FIX_BWD = 1, PH_FIX = 2 };
 template <int DIR>
 __device__ __forceinline__ void tile_load(double (*tile)[S + 1], const double* X, int ld, int sweep0, int line0,
                                           int nsweep, int nlines) {
+    // global rows rb + hi + 4u, columns cb + lo (lo = lane-contiguous)
     const int t = threadIdx.x, lo = t % S, hi = t / S;
+    const int rb = DIR == DIR_COL ? sweep0 : line0, cb = DIR == DIR_COL ? line0 : sweep0;
+    const int nr = DIR == DIR_COL ? nsweep : nlines, nc = DIR == DIR_COL ? nlines : nsweep;
+    const double* p = X + (size_t)(rb + hi) * ld + cb + lo;
+    const size_t step = (size_t)NSUB * ld;
     double v[S / NSUB];
-    #pragma unroll
-    for (int u = 0; u < S / NSUB; ++u) {
-        const int kk = hi + u * NSUB;
-        const int i = DIR == DIR_COL ? sweep0 + kk : line0 + kk;
-        const int j = DIR == DIR_COL ? line0 + lo : sweep0 + lo;
-        const bool ok = DIR == DIR_COL ? (i < nsweep && j < nlines) : (i < nlines && j < nsweep);
-        v[u] = ok ? X[(size_t)i * ld + j] : 0.0;
+    if (rb + S <= nr && cb + S <= nc) {  // interior tile (uniform)
+        #pragma unroll
+        for (int u = 0; u < S / NSUB; ++u) v[u] = p[u * step];
+    } else {
+        const bool cok = cb + lo < nc;
+        #pragma unroll
+        for (int u = 0; u < S / NSUB; ++u) v[u] = (cok && rb + hi + u * NSUB < nr) ? p[u * step] : 0.0;
     }
     #pragma unroll
     for (int u = 0; u < S / NSUB; ++u) {
@@ -69,16 +74,17 @@ template <int DIR>
 __device__ __forceinline__ void tile_store(double (*tile)[S + 1], double* X, int ld, int sweep0, int line0,
                                            int nsweep, int nlines) {
     const int t = threadIdx.x, lo = t % S, hi = t / S;
+    const int rb = DIR == DIR_COL ? sweep0 : line0, cb = DIR == DIR_COL ? line0 : sweep0;
+    const int nr = DIR == DIR_COL ? nsweep : nlines, nc = DIR == DIR_COL ? nlines : nsweep;
+    double* p = X + (size_t)(rb + hi) * ld + cb + lo;
+    const size_t step = (size_t)NSUB * ld;
+    const bool full = rb + S <= nr && cb + S <= nc;
+    const bool cok = cb + lo < nc;
     #pragma unroll
     for (int u = 0; u < S / NSUB; ++u) {
         const int kk = hi + u * NSUB;
-        if (DIR == DIR_COL) {
-            const int i = sweep0 + kk, j = line0 + lo;
-            if (i < nsweep && j < nlines) X[(size_t)i * ld + j] = tile[kk][lo];
-        } else {
-            const int i = line0 + kk, j = sweep0 + lo;
-            if (i < nlines && j < nsweep) X[(size_t)i * ld + j] = tile[lo][kk];
-        }
+        const double v = DIR == DIR_COL ? tile[kk][lo] : tile[lo][kk];
+        if (full || (cok && rb + kk < nr)) p[u * step] = v;
     }
 }
 
@@ -307,6 +313,10 @@ __global__ void __launch_bounds__(64) seg_scan_kernel(int nlines, int P, const d
                                                       const PcgState* pcg) {
     SFB_PDL_PROLOGUE();
     if (pcg != nullptr && pcg->status != SFB_PCG_RUNNING) return;
+    // the P transfer matrices, staged once: every step of the chain reads one
+    extern __shared__ double Ts[];
+    for (int i = threadIdx.x; i < P * B * B; i += blockDim.x) Ts[i] = T[i];
+    __syncthreads();
     const int gl = blockIdx.x * blockDim.x + threadIdx.x;
     if (gl >= nlines) return;
     constexpr int BB = B > 0 ? B : 1;
@@ -331,7 +341,7 @@ __global__ void __launch_bounds__(64) seg_scan_kernel(int nlines, int P, const d
             #pragma unroll
             for (int d = 0; d < B; ++d) sv[((size_t)p * B + d) * nlines + gl] = s[d];
             double nx[BB];
-            const double* Tp = T + (size_t)p * B * B;
+            const double* Tp = Ts + p * B * B;
             #pragma unroll
             for (int d = 0; d < B; ++d) {
                 double v = tail[u][d];
@@ -369,9 +379,14 @@ int run_factor(const SegFactor& f, const double* Xin, int ldi, double* X, int ld
     const dim3 grid(P, (nlines + S - 1) / S);
     const dim3 sgrid((nlines + 63) / 64);
     SFB_TRY(launch_kernel(seg_tile_kernel<B, DIR, PH_FWD>, grid, dim3(NT), 0, s, a));
-    if (B > 0) SFB_TRY(launch_kernel(seg_scan_kernel<B, true>, sgrid, dim3(64), 0, s, nlines, P, f.Tf, sv_f, pcg_gate));
+    const size_t tsm = (size_t)P * B * B * 8;
+    if (tsm > 48 * 1024) {
+        set_error("banded preconditioner: order too large for the segment scan");
+        return SFB_ERR_UNSUPPORTED;
+    }
+    if (B > 0) SFB_TRY(launch_kernel(seg_scan_kernel<B, true>, sgrid, dim3(64), tsm, s, nlines, P, f.Tf, sv_f, pcg_gate));
     SFB_TRY(launch_kernel(seg_tile_kernel<B, DIR, PH_FIX_BWD>, grid, dim3(NT), 0, s, a));
-    if (B > 0) SFB_TRY(launch_kernel(seg_scan_kernel<B, false>, sgrid, dim3(64), 0, s, nlines, P, f.Tb, sv_b, pcg_gate));
+    if (B > 0) SFB_TRY(launch_kernel(seg_scan_kernel<B, false>, sgrid, dim3(64), tsm, s, nlines, P, f.Tb, sv_b, pcg_gate));
     if (dot != nullptr) {
         a.R = dot->R;
         a.ldr = dot->ldr;
