@@ -27,11 +27,21 @@ namespace sfb {
 
 namespace {
 
-constexpr int BM = 128, BN = 128, BK = 16, STAGES = 4;
+#ifndef GEMM_STAGES
+#define GEMM_STAGES 5
+#endif
+#ifndef GEMM_EMPTY
+#define GEMM_EMPTY 1  // per-stage empty barriers (1) or a CTA barrier per k-tile (0)
+#endif
+constexpr int BM = 128, BN = 128, BK = 16, STAGES = GEMM_STAGES;
+// k-tiles in flight ahead of the one being consumed: with per-stage empty
+// barriers one slot of slack lets warps drift by a k-tile without stalling
+// the issuing thread
+constexpr int LOOKAHEAD = GEMM_EMPTY ? STAGES - 2 : STAGES - 1;
 constexpr int NWARPS = 8;                   // 2 x 4 warp grid, 64 x 32 per warp
 constexpr int NTHREADS = NWARPS * 32;       // 2 warps per SM sub-partition (<= 255 regs each)
 constexpr int TILE_BYTES = BM * BK * 8;     // 16 KB per operand per stage
-constexpr int SMEM_BYTES = 2 * STAGES * TILE_BYTES + STAGES * 8 + 1024;
+constexpr int SMEM_BYTES = 2 * STAGES * TILE_BYTES + 2 * STAGES * 8 + 1024;
 
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -122,6 +132,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     extern __shared__ uint8_t smem_raw[];
     const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
     const uint32_t sA = base, sB = base + STAGES * TILE_BYTES, full = base + 2 * STAGES * TILE_BYTES;
+    const uint32_t empty = full + 8 * STAGES;  // one arrive per warp when it is done reading a slot
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int wm = warp >> 2, wn = warp & 3;  // 2 x 4 warps, 64 x 32 each
@@ -141,11 +152,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     };
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < STAGES; ++s) mbar_init_u32(full + 8 * s, 1);
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init_u32(full + 8 * s, 1);
+            mbar_init_u32(empty + 8 * s, NWARPS);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
-        for (int it = 0; it < STAGES - 1 && it < n_it; ++it) issue(it);
+        for (int it = 0; it < LOOKAHEAD && it < n_it; ++it) issue(it);
     }
     __syncthreads();
 
@@ -164,8 +178,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 
         for (; it < seg_end; ++it) {
             const int s = it % STAGES;
+#if GEMM_EMPTY
+            if (threadIdx.x == 0 && it + LOOKAHEAD < n_it) {
+                const int nx = it + LOOKAHEAD;  // its slot was last read in local iteration nx - STAGES
+                if (nx >= STAGES) mbar_wait_u32(empty + 8 * (nx % STAGES), ((nx / STAGES) - 1) & 1);
+                issue(nx);
+            }
+#else
             __syncthreads();  // every warp is done with the slot refilled below (WAR)
-            if (threadIdx.x == 0 && it + STAGES - 1 < n_it) issue(it + STAGES - 1);
+            if (threadIdx.x == 0 && it + LOOKAHEAD < n_it) issue(it + LOOKAHEAD);
+#endif
             mbar_wait_u32(full + 8 * s, (it / STAGES) & 1);
             const uint32_t a_base = sA + s * TILE_BYTES + (wm * 64 + g) * 128;
             const uint32_t b_base = sB + s * TILE_BYTES + (wn * 32 + g) * 128;
@@ -186,6 +208,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     #pragma unroll
                     for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i].y, b[j].y);
             }
+#if GEMM_EMPTY
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(empty + 8 * s) : "memory");
+#endif
         }
 
         const int m0 = (tile / sc.tiles_n) * BM, n0 = (tile % sc.tiles_n) * BN;
