@@ -44,6 +44,17 @@ inline int arg_error(const std::string& msg) {
 
 constexpr int kNumSMs = 148;
 
+// device allocation of n doubles (at least one), SFB_ERR_NOMEM on failure
+inline int dalloc(double** p, size_t n) {
+    if (n == 0) n = 1;
+    cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), n * sizeof(double));
+    if (e != cudaSuccess) {
+        set_error(std::string("cudaMalloc: ") + cudaGetErrorString(e));
+        return SFB_ERR_NOMEM;
+    }
+    return SFB_OK;
+}
+
 inline int round_up(int v, int m) { return (v + m - 1) / m * m; }
 
 // ------------------------------------------------- device scalar state ----

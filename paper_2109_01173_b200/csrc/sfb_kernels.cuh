@@ -106,21 +106,18 @@ int launch_sh_xpby(double* Q, int ldq, const double* Z, int ldz, int rows, int c
 int launch_sh_dots(const double* A, const double* B, const double* C, const double* D, int ld, int rows, int cols,
                    double* partials, RedSlots* out, cudaStream_t s);
 
-// ------------------------------------------------------ banded solves ----
-// --------------------------------------------- segmented banded solves ----
-// One SPD banded factor P = C C^T prepared for segmented solves (seg_solve.cu).
-struct SegFactor {
+// ------------------------------------------ banded preconditioner solves ----
+// One SPD banded preconditioner factor prepared for the SPIKE solves (spike.cu).
+struct SpikeFactor {
     int n = 0, b = 0;
-    double* band = nullptr;  // [n + b][b + 1], reciprocal diagonal at d = b, b zero rows appended
-    double* Hf = nullptr;    // [P][S][b] forward responses to unit incoming states
-    double* Hb = nullptr;    // [P][S][b] backward responses
-    double* Tf = nullptr;    // [P][b][b] forward state transfer
-    double* Tb = nullptr;    // [P][b][b] backward state transfer
-    // the same at the 16-long sub-segment level (one thread sweeps one sub-segment)
-    double* Hf16 = nullptr;
+    double* band = nullptr;  // [n + b][b + 1] segment-local Cholesky rows (1/L_ii at d = b)
+    double* Hf16 = nullptr;  // [P16][16][b] sub-segment responses, forward / backward
     double* Hb16 = nullptr;
-    double* Tf16 = nullptr;
+    double* Tf16 = nullptr;  // [P16][b][b] sub-segment transfers
     double* Tb16 = nullptr;
+    double* V = nullptr;     // [P][64][b] spikes
+    double* W = nullptr;
+    double* coef = nullptr;  // [P][(2b)^2 + 2 (2b) b] interface block-LU
 };
 struct SegDot {
     const double* R = nullptr;
@@ -130,13 +127,14 @@ struct SegDot {
     PcgState* pcg = nullptr;
     double* dot_out = nullptr;
 };
-int seg_length();
-int seg_sub_length();
-// Solve P y = x for every line: along_rows = 0 -> lines are columns (P acts
-// from the left), 1 -> lines are rows (P acts from the right).  X may alias
-// Xin.  sv_f / sv_b: scratch of [P][b][nlines] doubles each.
-int launch_seg_factor(const SegFactor& f, int along_rows, const double* Xin, int ldi, double* X, int ld,
-                      int nlines, const SegDot* dot, double* sv_f, double* sv_b, const PcgState* pcg_gate,
-                      cudaStream_t s);
+int spike_length();
+size_t spike_interface_doubles(int n, int b, int nlines);
+int build_spike_factor(int n, int b, const double* cholesky_band_host, SpikeFactor& f);
+void free_spike_factor(SpikeFactor& f);
+// Z = P_L^-1 R P_R^-1 (Z may alias nothing but itself; R is read once).
+// svL / svR: interface scratch of spike_interface_doubles(qy, bL, qx) and
+// spike_interface_doubles(qx, bR, qy) doubles.  `dot` (nullable) receives <Z,R>.
+int launch_spike_pre(const SpikeFactor& L, const SpikeFactor& R, const double* Rin, int ldr, double* Z, int ldz,
+                     const SegDot* dot, double* svL, double* svR, const PcgState* gate, cudaStream_t s);
 
 }  // namespace sfb

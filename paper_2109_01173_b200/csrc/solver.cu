@@ -26,16 +26,6 @@ void set_error(const std::string& msg) { g_last_error = msg; }
 
 namespace {
 
-int dalloc(double** p, size_t n) {
-    if (n == 0) n = 1;
-    cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), n * sizeof(double));
-    if (e != cudaSuccess) {
-        set_error(std::string("cudaMalloc: ") + cudaGetErrorString(e));
-        return SFB_ERR_NOMEM;
-    }
-    return SFB_OK;
-}
-
 template <class T>
 int talloc(T** p, size_t bytes) {
     cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), bytes);
@@ -167,100 +157,17 @@ struct sfb_pre {
     double *A1 = nullptr, *A1t = nullptr, *B1 = nullptr, *B1t = nullptr;
     int ldA = 0, ldB = 0;
     double *sl = nullptr, *sr = nullptr;
-    // BANDED: Cholesky factors prepared for segmented solves
-    SegFactor fl, fr;
-    size_t seg_doubles = 0;  // scratch per boundary-state buffer
+    // BANDED: factors prepared for the SPIKE solves (spike.cu)
+    SpikeFactor fl, fr;
+    size_t seg_doubles = 0;  // scratch per interface buffer
 };
 
 namespace sfb {
 namespace {
 
 inline int seg_tiles(int qy, int qx) {
-    const int S = seg_length();
+    const int S = spike_length();
     return ((qx + S - 1) / S) * ((qy + S - 1) / S);
-}
-
-// Host precompute of a segmented banded factor (seg_solve.cu): band with the
-// reciprocal diagonal and b zero rows appended, the responses H of every
-// segment to unit incoming states, and the b x b state transfers T.
-int build_seg_factor(int n, int b, const double* band_host, SegFactor& f) {
-    const int bb = std::max(b, 1);
-    std::vector<double> band((size_t)(n + b) * (b + 1), 0.0);
-    std::copy(band_host, band_host + (size_t)n * (b + 1), band.begin());
-    auto C = [&](int i, int d) { return band[(size_t)i * (b + 1) + d]; };  // C[i][i-b+d], 1/C_ii at d=b
-    // responses / transfers of segments of length S (two levels: S = 64 tiles,
-    // S = 16 sub-segments swept by one thread each)
-    auto responses = [&](int S, std::vector<double>& Hf, std::vector<double>& Hb, std::vector<double>& Tf,
-                         std::vector<double>& Tb) {
-        const int P = (n + S - 1) / S;
-        Hf.assign((size_t)P * S * bb, 0.0);
-        Hb.assign((size_t)P * S * bb, 0.0);
-        Tf.assign((size_t)P * bb * bb, 0.0);
-        Tb.assign((size_t)P * bb * bb, 0.0);
-        std::vector<double> w(bb);
-        for (int p = 0; p < P; ++p) {
-            const int start = p * S, len = std::min(S, n - start), end = start + len;
-            for (int d = 0; d < b; ++d) {
-                // forward: incoming state y_{start-b+d'} = delta(d', d)
-                std::fill(w.begin(), w.end(), 0.0);
-                w[d] = 1.0;
-                for (int k = 0; k < len; ++k) {
-                    const int i = start + k;
-                    double v = 0.0;
-                    for (int e = 0; e < b; ++e) v -= C(i, e) * w[e];
-                    v *= C(i, b);
-                    for (int e = 0; e + 1 < b; ++e) w[e] = w[e + 1];
-                    w[b - 1] = v;
-                    Hf[((size_t)p * S + k) * bb + d] = v;
-                }
-                for (int o = 0; o < b; ++o) {
-                    const int r = end - b + o;
-                    Tf[((size_t)p * bb + o) * bb + d] = r >= start ? Hf[((size_t)p * S + (r - start)) * bb + d]
-                                                                   : (r - (start - b) == d ? 1.0 : 0.0);
-                }
-                // backward: incoming state z_{end+e} = delta(e, d); w[e-1] = z[i+e]
-                std::fill(w.begin(), w.end(), 0.0);
-                w[d] = 1.0;
-                for (int k = len - 1; k >= 0; --k) {
-                    const int i = start + k;
-                    double v = 0.0;
-                    for (int e = b; e >= 1; --e) v -= C(i + e, b - e) * w[e - 1];
-                    v *= C(i, b);
-                    for (int e = b - 1; e >= 1; --e) w[e] = w[e - 1];
-                    w[0] = v;
-                    Hb[((size_t)p * S + k) * bb + d] = v;
-                }
-                for (int o = 0; o < b; ++o) {
-                    const int r = start + o;
-                    Tb[((size_t)p * bb + o) * bb + d] = r < end ? Hb[((size_t)p * S + (r - start)) * bb + d]
-                                                               : (r - end == d ? 1.0 : 0.0);
-                }
-            }
-        }
-    };
-    std::vector<double> Hf, Hb, Tf, Tb, Hf16, Hb16, Tf16, Tb16;
-    responses(seg_length(), Hf, Hb, Tf, Tb);
-    responses(seg_sub_length(), Hf16, Hb16, Tf16, Tb16);
-    f.n = n;
-    f.b = b;
-    auto up = [](double** dst, const std::vector<double>& v) {
-        if (dalloc(dst, v.size()) != SFB_OK) return SFB_ERR_NOMEM;
-        if (cudaMemcpy(*dst, v.data(), v.size() * 8, cudaMemcpyHostToDevice) != cudaSuccess) {
-            set_error("uploading segmented factor failed");
-            return SFB_ERR_CUDA;
-        }
-        return SFB_OK;
-    };
-    SFB_TRY(up(&f.band, band));
-    SFB_TRY(up(&f.Hf, Hf));
-    SFB_TRY(up(&f.Hb, Hb));
-    SFB_TRY(up(&f.Tf, Tf));
-    SFB_TRY(up(&f.Tb, Tb));
-    SFB_TRY(up(&f.Hf16, Hf16));
-    SFB_TRY(up(&f.Hb16, Hb16));
-    SFB_TRY(up(&f.Tf16, Tf16));
-    SFB_TRY(up(&f.Tb16, Tb16));
-    return SFB_OK;
 }
 
 // W = op(U) on device buffers (U must have an even ld and 16B alignment for
@@ -364,10 +271,9 @@ int pre_apply_impl(const sfb_pre* p, const double* R, int ldr, double* Z, int ld
             return launch_dgemm_nt(p->A1, p->ldA, T1, ldt1, qy, qx, qy, with_ws(last, gw), s);
         }
         case SFB_PRE_BANDED: {
-            // Z = P_L^-1 R (lines = columns, R -> Z), then Z P_R^-1 in place
-            // (lines = rows) with <Z,R> fused into the last tile pass.
+            // Z = P_L^-1 R P_R^-1 by SPIKE solves (left along columns, right
+            // along rows) with <Z,R> fused into the last tile pass.
             if (gw == nullptr || gw->seg_f == nullptr) return arg_error("banded preconditioner needs scratch");
-            SFB_TRY(launch_seg_factor(p->fl, 0, R, ldr, Z, ldz, qx, nullptr, gw->seg_f, gw->seg_b, pcg, s));
             SegDot dot;
             dot.R = R;
             dot.ldr = ldr;
@@ -375,8 +281,8 @@ int pre_apply_impl(const sfb_pre* p, const double* R, int ldr, double* Z, int ld
             dot.counter = counter;
             dot.pcg = pcg;
             dot.dot_out = red ? &red->v[3] : nullptr;
-            return launch_seg_factor(p->fr, 1, Z, ldz, Z, ldz, qy, (pcg || red) ? &dot : nullptr, gw->seg_f,
-                                     gw->seg_b, pcg, s);
+            return launch_spike_pre(p->fl, p->fr, R, ldr, Z, ldz, (pcg || red) ? &dot : nullptr, gw->seg_f,
+                                    gw->seg_b, pcg, s);
         }
     }
     return arg_error("unknown preconditioner kind");
@@ -909,15 +815,13 @@ int sfb_pre_create_banded(int qy, int qx, int bwL, const double* lband, int bwR,
     p->kind = SFB_PRE_BANDED;
     p->qy = qy;
     p->qx = qx;
-    int rc = build_seg_factor(qy, bwL, lband, p->fl);
-    if (rc == SFB_OK) rc = build_seg_factor(qx, bwR, rband, p->fr);
+    int rc = build_spike_factor(qy, bwL, lband, p->fl);
+    if (rc == SFB_OK) rc = build_spike_factor(qx, bwR, rband, p->fr);
     if (rc != SFB_OK) {
         sfb_pre_destroy(p);
         return rc;
     }
-    const size_t S = (size_t)seg_length();
-    p->seg_doubles = std::max(((qy + S - 1) / S) * std::max(bwL, 1) * (size_t)qx,
-                              ((qx + S - 1) / S) * std::max(bwR, 1) * (size_t)qy);
+    p->seg_doubles = std::max(spike_interface_doubles(qy, bwL, qx), spike_interface_doubles(qx, bwR, qy));
     *out = p;
     return SFB_OK;
 }
@@ -992,9 +896,8 @@ int sfb_pre_destroy(sfb_pre* p) {
     cudaFree(p->B1t);
     cudaFree(p->sl);
     cudaFree(p->sr);
-    for (SegFactor* f : {&p->fl, &p->fr}) {
-        for (double* a : {f->band, f->Hf, f->Hb, f->Tf, f->Tb, f->Hf16, f->Hb16, f->Tf16, f->Tb16}) cudaFree(a);
-    }
+    free_spike_factor(p->fl);
+    free_spike_factor(p->fr);
     delete p;
     return SFB_OK;
 }
