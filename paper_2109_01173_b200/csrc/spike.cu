@@ -77,22 +77,49 @@ __device__ __forceinline__ void tile_load(double (*tile)[S + 1], const double* X
     }
 }
 
+// Store the tile; with R != nullptr also return this thread's part of
+// <tile, R> over the same (valid) elements.
 template <int DIR>
-__device__ __forceinline__ void tile_store(double (*tile)[S + 1], double* X, int ld, int sweep0, int line0,
-                                           int nsweep, int nlines) {
+__device__ __forceinline__ double tile_store(double (*tile)[S + 1], double* X, int ld, int sweep0, int line0,
+                                             int nsweep, int nlines, const double* R = nullptr, int ldr = 0) {
     const int t = threadIdx.x, lo = t % S, hi = t / S;
     const int rb = DIR == DIR_COL ? sweep0 : line0, cb = DIR == DIR_COL ? line0 : sweep0;
     const int nr = DIR == DIR_COL ? nsweep : nlines, nc = DIR == DIR_COL ? nlines : nsweep;
     double* p = X + (size_t)(rb + hi) * ld + cb + lo;
-    const size_t step = (size_t)NSUB * ld;
-    const bool full = rb + S <= nr && cb + S <= nc;
-    const bool cok = cb + lo < nc;
-    #pragma unroll
-    for (int u = 0; u < S / NSUB; ++u) {
-        const int kk = hi + u * NSUB;
-        const double v = DIR == DIR_COL ? tile[kk][lo] : tile[lo][kk];
-        if (full || (cok && rb + kk < nr)) p[u * step] = v;
+    const double* q = R != nullptr ? R + (size_t)(rb + hi) * ldr + cb + lo : nullptr;
+    const size_t step = (size_t)NSUB * ld, stepr = (size_t)NSUB * ldr;
+    double dot = 0.0;
+    if (rb + S <= nr && cb + S <= nc) {  // interior tile (uniform)
+        if (q != nullptr) {
+            double r[S / NSUB];
+            #pragma unroll
+            for (int u = 0; u < S / NSUB; ++u) r[u] = q[u * stepr];
+            #pragma unroll
+            for (int u = 0; u < S / NSUB; ++u) {
+                const int kk = hi + u * NSUB;
+                const double v = DIR == DIR_COL ? tile[kk][lo] : tile[lo][kk];
+                p[u * step] = v;
+                dot = fma(v, r[u], dot);
+            }
+        } else {
+            #pragma unroll
+            for (int u = 0; u < S / NSUB; ++u) {
+                const int kk = hi + u * NSUB;
+                p[u * step] = DIR == DIR_COL ? tile[kk][lo] : tile[lo][kk];
+            }
+        }
+    } else if (cb + lo < nc) {
+        #pragma unroll
+        for (int u = 0; u < S / NSUB; ++u) {
+            const int kk = hi + u * NSUB;
+            if (rb + kk < nr) {
+                const double v = DIR == DIR_COL ? tile[kk][lo] : tile[lo][kk];
+                p[u * step] = v;
+                if (q != nullptr) dot = fma(v, q[u * stepr], dot);
+            }
+        }
     }
+    return dot;
 }
 
 struct SpikeArgs {
@@ -328,21 +355,10 @@ __global__ void __launch_bounds__(NT) spike_tile_kernel(SpikeArgs a) {
         }
     }
     if (PH == PH_FIX) __syncthreads();
-    tile_store<DIR>(tile, a.X, a.ld, start, line0, a.n, a.nlines);
-    if (PH == PH_FIX && a.R != nullptr) {
+    const bool want_dot = PH == PH_FIX && a.R != nullptr;
+    const double dot = tile_store<DIR>(tile, a.X, a.ld, start, line0, a.n, a.nlines, want_dot ? a.R : nullptr, a.ldr);
+    if (want_dot) {
         // <Z,R> over this tile (deterministic: fixed thread/tile order)
-        double dot = 0.0;
-        const int lo = t % S, hi = t / S;
-        #pragma unroll 4
-        for (int kk = hi; kk < S; kk += NSUB) {
-            if (DIR == DIR_COL) {
-                const int i = start + kk, j = line0 + lo;
-                if (kk < len && j < a.nlines) dot = fma(tile[kk][lo], a.R[(size_t)i * a.ldr + j], dot);
-            } else {
-                const int i = line0 + kk, j = start + lo;
-                if (i < a.nlines && lo < len) dot = fma(tile[lo][kk], a.R[(size_t)i * a.ldr + j], dot);
-            }
-        }
         __shared__ double sh[NT / 32];
         const double part = block_sum<NT>(dot, sh);
         const unsigned nblk = gridDim.x * gridDim.y;
@@ -360,80 +376,79 @@ __global__ void __launch_bounds__(NT) spike_tile_kernel(SpikeArgs a) {
 
 // Interface system of one factor, one thread per line: block-LU forward
 // chain d_p = K_p gamma_p - KA_p u(d_{p-1}), backward z_p = d_p - Ch_p t(z_{p+1})
-// (K, KA, Ch precomputed, staged in shared memory); sv holds gamma on entry
-// and the interface values z_p = (t_p, u_p) on exit.
+// (K, KA, Ch precomputed; read through L1, the same for every line).  The CTA
+// first stages its lines' gamma values in shared memory with all loads in
+// flight, runs both chains there in place (every operand off the chain is a
+// shared-memory or L1 load that can be issued early) and writes the
+// interface solution z_p = (t_p, u_p) back in one coalesced pass.
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
+                 "l"(src)
+                 : "memory");
+}
+
 template <int B>
-__global__ void __launch_bounds__(64) spike_chain_kernel(int nlines, int P, const double* coef, double* sv,
-                                                         const PcgState* gate) {
+__global__ void __launch_bounds__(32) spike_chain_kernel(int nlines, int P, const double* __restrict__ coef,
+                                                         double* sv, int coef_in_smem, const PcgState* gate) {
     SFB_PDL_PROLOGUE();
     if (gate != nullptr && gate->status != SFB_PCG_RUNNING) return;
     constexpr int B2 = 2 * B;
     constexpr int PER = B2 * B2 + 2 * B2 * B;  // K (2B x 2B), KA (2B x B), Ch (2B x B)
-    extern __shared__ double cs[];
-    for (int i = threadIdx.x; i < P * PER; i += blockDim.x) cs[i] = coef[i];
+    extern __shared__ double gs[];             // [P][2B][L], then the coefficients when they fit
+    const int L = blockDim.x, l = threadIdx.x, line0 = blockIdx.x * L;
+    const bool live = line0 + l < nlines;
+    // stage with every load in flight (cp.async, one wait)
+    double* cs = gs + (size_t)P * B2 * L;
+    if (live)
+        for (int row = 0; row < P * B2; ++row) cp_async8(gs + row * L + l, sv + (size_t)row * nlines + line0 + l);
+    if (coef_in_smem)
+        for (int i = l; i < P * PER; i += L) cp_async8(cs + i, coef + i);
+    asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
-    const int gl = blockIdx.x * blockDim.x + threadIdx.x;
-    if (gl >= nlines) return;
-    double prev[B];  // u part of d_{p-1}
-    #pragma unroll
-    for (int d = 0; d < B; ++d) prev[d] = 0.0;
-    constexpr int CH = 4;
-    for (int p0 = 0; p0 < P; p0 += CH) {
-        double g[CH][B2];
+    const double* cf = coef_in_smem ? cs : coef;
+    if (live) {
+        double prev[B];  // u part of d_{p-1}
         #pragma unroll
-        for (int u = 0; u < CH; ++u)
-            #pragma unroll
-            for (int d = 0; d < B2; ++d)
-                g[u][d] = p0 + u < P ? sv[((size_t)(p0 + u) * B2 + d) * nlines + gl] : 0.0;
-        #pragma unroll
-        for (int u = 0; u < CH; ++u) {
-            const int p = p0 + u;
-            if (p >= P) break;
-            const double* K = cs + (size_t)p * PER;
+        for (int d = 0; d < B; ++d) prev[d] = 0.0;
+        #pragma unroll 2
+        for (int p = 0; p < P; ++p) {
+            const double* K = cf + (size_t)p * PER;
             const double* KA = K + B2 * B2;
-            double dv[B2];
+            double g[B2], dv[B2];
+            #pragma unroll
+            for (int j = 0; j < B2; ++j) g[j] = gs[(p * B2 + j) * L + l];
             #pragma unroll
             for (int i = 0; i < B2; ++i) {
                 double v = 0.0;
                 #pragma unroll
-                for (int j = 0; j < B2; ++j) v = fma(K[i * B2 + j], g[u][j], v);
+                for (int j = 0; j < B2; ++j) v = fma(K[i * B2 + j], g[j], v);
                 #pragma unroll
                 for (int j = 0; j < B; ++j) v = fma(-KA[i * B + j], prev[j], v);
                 dv[i] = v;
             }
             #pragma unroll
-            for (int i = 0; i < B2; ++i) sv[((size_t)p * B2 + i) * nlines + gl] = dv[i];
+            for (int i = 0; i < B2; ++i) gs[(p * B2 + i) * L + l] = dv[i];
             #pragma unroll
             for (int d = 0; d < B; ++d) prev[d] = dv[B + d];
         }
-    }
-    double nxt[B];  // t part of z_{p+1}
-    #pragma unroll
-    for (int d = 0; d < B; ++d) nxt[d] = 0.0;
-    for (int p0 = P - 1; p0 >= 0; p0 -= CH) {
-        double dd[CH][B2];
+        double nx[B];  // t part of z_{p+1}
         #pragma unroll
-        for (int u = 0; u < CH; ++u)
-            #pragma unroll
-            for (int d = 0; d < B2; ++d)
-                dd[u][d] = p0 - u >= 0 ? sv[((size_t)(p0 - u) * B2 + d) * nlines + gl] : 0.0;
-        #pragma unroll
-        for (int u = 0; u < CH; ++u) {
-            const int p = p0 - u;
-            if (p < 0) break;
-            const double* Ch = cs + (size_t)p * PER + B2 * B2 + B2 * B;
+        for (int d = 0; d < B; ++d) nx[d] = 0.0;
+        #pragma unroll 2
+        for (int p = P - 1; p >= 0; --p) {
+            const double* Ch = cf + (size_t)p * PER + B2 * B2 + B2 * B;
             double z[B2];
             #pragma unroll
             for (int i = 0; i < B2; ++i) {
-                double v = dd[u][i];
+                double v = gs[(p * B2 + i) * L + l];
                 #pragma unroll
-                for (int j = 0; j < B; ++j) v = fma(-Ch[i * B + j], nxt[j], v);
+                for (int j = 0; j < B; ++j) v = fma(-Ch[i * B + j], nx[j], v);
                 z[i] = v;
             }
             #pragma unroll
-            for (int i = 0; i < B2; ++i) sv[((size_t)p * B2 + i) * nlines + gl] = z[i];
+            for (int i = 0; i < B2; ++i) sv[((size_t)p * B2 + i) * nlines + line0 + l] = z[i];
             #pragma unroll
-            for (int d = 0; d < B; ++d) nxt[d] = z[d];
+            for (int d = 0; d < B; ++d) nx[d] = z[d];
         }
     }
 }
@@ -444,17 +459,25 @@ int chain(const SpikeFactor& f, int nlines, double* sv, const PcgState* gate, cu
         return SFB_OK;  // diagonal factor: no interfaces
     } else {
         const int P = (f.n + S - 1) / S;
-        const size_t sm = (size_t)P * (4 * B * B + 4 * B * B) * 8;
-        if (sm > 48 * 1024) {
-            if (sm > 200 * 1024) {
-                set_error("banded preconditioner: order too large for the interface chain");
-                return SFB_ERR_UNSUPPORTED;
-            }
+        constexpr size_t cap = 200 * 1024;
+        int L = 32;
+        size_t sm = (size_t)P * 2 * B * L * 8;
+        if (sm > cap) {
+            L = 16;
+            sm /= 2;
+        }
+        if (sm > cap) {
+            set_error("banded preconditioner: order too large for the interface chain");
+            return SFB_ERR_UNSUPPORTED;
+        }
+        const size_t csm = (size_t)P * (8 * B * B) * 8;
+        const int cin = sm + csm <= cap ? 1 : 0;
+        if (cin) sm += csm;
+        if (sm > 48 * 1024)
             SFB_CUDA_TRY(cudaFuncSetAttribute(spike_chain_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                               (int)sm));
-        }
-        return launch_kernel(spike_chain_kernel<B>, dim3((nlines + 63) / 64), dim3(64), sm, s, nlines, P, f.coef,
-                             sv, gate);
+        return launch_kernel(spike_chain_kernel<B>, dim3((nlines + L - 1) / L), dim3(L), sm, s, nlines, P, f.coef,
+                             sv, cin, gate);
     }
 }
 

@@ -81,3 +81,30 @@ def test_device_eigensolver_route_for_reduced_solves(golden):
     c = pb.build_spectral_cache(op, eig="device")
     assert c.swapped
     assert relerr(pb.solve_reduced(op, rhs_of(cosine_source_rect(12, 2)), c).solution, golden["red2/U"]) <= 1e-10
+
+
+# f1: the SPIKE banded solves across several 64-row segments, including a
+# last segment shorter than the half-bandwidth (q = 64 m + 1, 64 m + 3).
+@pytest.mark.parametrize("deg,N,lumped", [(1, 130, False), (2, 130, False), (2, 66, False), (3, 201, False),
+                                          (4, 260, False), (1, 200, True)])
+def test_banded_preconditioner_multi_segment(deg, N, lumped):
+    x, y = pb.build_direction_sets(WAVE, deg, N, D, lumped=lumped)
+    kw = dict(lumped=True) if lumped else {}
+    pre_b = pb.make_preconditioner("elliptic_xnormal", x, y, mode="banded", **kw)
+    pre_i = pb.make_preconditioner("elliptic_xnormal", x, y, mode="inverse", **kw)
+    U = np.random.default_rng(deg * 1000 + N).standard_normal((y.q, x.q))
+    assert y.q > 64 and x.q > 64
+    assert relerr(pre_b.apply_inverse(U), pre_i.apply_inverse(U)) <= 1e-11
+    # round trip limited by the factors' conditioning (P4 ~ 1e7), like the LU path
+    assert relerr(pre_b.apply(pre_b.apply_inverse(U)), U) <= 1e-8
+
+
+def test_banded_mode_mo_pcg_multi_segment_matches_inverse_mode():
+    N = 200
+    x, y = pb.build_direction_sets(WAVE, 2, N, D)
+    op, rhs_of = pb.elliptic_operator(x, y, 1.0)
+    rhs = rhs_of(sine_source(N, N, 3))
+    reps = [pb.mo_pcg(op, rhs, precond=pb.make_preconditioner("elliptic_xnormal", x, y, mode=m),
+                      stop=pb.relative_residual(1e-10), max_iter=20000) for m in ("inverse", "banded")]
+    assert abs(reps[0].iterations - reps[1].iterations) <= max(2, reps[0].iterations // 200)
+    assert relerr(reps[1].solution, reps[0].solution) <= 1e-8
