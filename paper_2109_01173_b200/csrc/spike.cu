@@ -52,9 +52,10 @@ enum { PH_LOCAL = 0, PH_FUSED = 1, PH_FIX = 2 };
 // from the right); the tile is stored transposed for DIR_ROW so both sweep
 // along the first index.  All NT threads move the tile, coalesced along the
 // contiguous global index.
-template <int DIR>
+template <int DIR, int NTH = NT>
 __device__ __forceinline__ void tile_load(double (*tile)[S + 1], const double* X, int ld, int sweep0, int line0,
                                           int nsweep, int nlines) {
+    constexpr int NSUB = NTH / S;  // row groups
     const int t = threadIdx.x, lo = t % S, hi = t / S;
     const int rb = DIR == DIR_COL ? sweep0 : line0, cb = DIR == DIR_COL ? line0 : sweep0;
     const int nr = DIR == DIR_COL ? nsweep : nlines, nc = DIR == DIR_COL ? nlines : nsweep;
@@ -79,9 +80,10 @@ __device__ __forceinline__ void tile_load(double (*tile)[S + 1], const double* X
 
 // Store the tile; with R != nullptr also return this thread's part of
 // <tile, R> over the same (valid) elements.
-template <int DIR>
+template <int DIR, int NTH = NT>
 __device__ __forceinline__ double tile_store(double (*tile)[S + 1], double* X, int ld, int sweep0, int line0,
                                              int nsweep, int nlines, const double* R = nullptr, int ldr = 0) {
+    constexpr int NSUB = NTH / S;  // row groups
     const int t = threadIdx.x, lo = t % S, hi = t / S;
     const int rb = DIR == DIR_COL ? sweep0 : line0, cb = DIR == DIR_COL ? line0 : sweep0;
     const int nr = DIR == DIR_COL ? nsweep : nlines, nc = DIR == DIR_COL ? nlines : nsweep;
