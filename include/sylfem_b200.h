@@ -130,9 +130,11 @@ int sfb_map_destroy(sfb_map* m);
 /* kind SFB_PRE_INVERSE: L = P_L^-1 (q_y x q_y), R = (P_R^-1)^T (q_x x q_x).
  * kind SFB_PRE_SPECTRAL_*: L = V_L, R = V_R, lamL/lamR eigenvalues.
  * kind SFB_PRE_BANDED: L/R = banded Cholesky factors, see sfb_pre_create_banded.
- * Host arrays are row-major and uploaded once. */
-int sfb_pre_create(int qy, int qx, int kind, const double* L_host,
-                   const double* R_host, const double* lamL_host,
+ * L/R are row-major and copied once; they may live in host or device memory
+ * (a device-resident eigendecomposition is not staged through the host).
+ * lamL/lamR are host arrays. */
+int sfb_pre_create(int qy, int qx, int kind, const double* L,
+                   const double* R, const double* lamL_host,
                    const double* lamR_host, sfb_pre** out);
 /* Banded SPD factors: lower Cholesky factors in band storage
  * lband[i][d] = C_L[i][i - bw + d] (d = 0..bw), same for the right factor. */

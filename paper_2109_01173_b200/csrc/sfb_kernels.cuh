@@ -99,6 +99,7 @@ int launch_loop_ctl(PcgState* st, unsigned long long handle, int use_handle, cud
 int launch_norms(const double* A, int lda, const double* B, int ldb, int rows, int cols, double* partials,
                  RedSlots* out, cudaStream_t s);
 int vector_grid_blocks();
+int launch_transpose(const double* src, int lds, double* dst, int ldd, int rows, int cols, cudaStream_t s);
 int launch_sh_update(double* U, double* R, const double* Q, const double* W, int ld, int rows, int cols,
                      double alpha, double* partials, RedSlots* out, cudaStream_t s);
 int launch_sh_xpby(double* Q, int ldq, const double* Z, int ldz, int rows, int cols, double beta, int first,

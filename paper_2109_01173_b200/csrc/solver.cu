@@ -38,10 +38,11 @@ int talloc(T** p, size_t bytes) {
 
 // Upload a host matrix (rows x cols, contiguous) into a device buffer with
 // leading dimension ld (zero padded).
+// src may be host or device memory (unified addressing decides the copy)
 int upload_padded(double* dst, int ld, const double* src, int rows, int cols) {
     SFB_CUDA_TRY(cudaMemset(dst, 0, (size_t)rows * ld * sizeof(double)));
     SFB_CUDA_TRY(cudaMemcpy2D(dst, (size_t)ld * sizeof(double), src, (size_t)cols * sizeof(double),
-                              (size_t)cols * sizeof(double), rows, cudaMemcpyHostToDevice));
+                              (size_t)cols * sizeof(double), rows, cudaMemcpyDefault));
     return SFB_OK;
 }
 
@@ -775,21 +776,20 @@ int sfb_pre_create(int qy, int qx, int kind, const double* L, const double* R, c
     }
     if (kind == SFB_PRE_SPECTRAL_PROD || kind == SFB_PRE_SPECTRAL_SUM) {
         if (!L || !R || !lamL || !lamR) return fail(arg_error("spectral sandwich needs V_L, V_R and eigenvalues"));
-        std::vector<double> t((size_t)std::max(qy, qx) * std::max(qy, qx));
         rc = dalloc(&p->A1, (size_t)qy * p->ldA);
         if (rc == SFB_OK) rc = dalloc(&p->A1t, (size_t)qy * p->ldA);
         if (rc == SFB_OK) rc = dalloc(&p->B1, (size_t)qx * p->ldB);
         if (rc == SFB_OK) rc = dalloc(&p->B1t, (size_t)qx * p->ldB);
         if (rc == SFB_OK) rc = dalloc(&p->sl, qy);
         if (rc == SFB_OK) rc = dalloc(&p->sr, qx);
+        // V (host or device memory) is copied once; the transposes are made on the device
         if (rc == SFB_OK) rc = upload_padded(p->A1, p->ldA, L, qy, qy);
-        for (int i = 0; i < qy; ++i)
-            for (int j = 0; j < qy; ++j) t[(size_t)j * qy + i] = L[(size_t)i * qy + j];
-        if (rc == SFB_OK) rc = upload_padded(p->A1t, p->ldA, t.data(), qy, qy);
+        if (rc == SFB_OK) rc = cudaMemset(p->A1t, 0, (size_t)qy * p->ldA * 8) == cudaSuccess ? SFB_OK : SFB_ERR_CUDA;
+        if (rc == SFB_OK) rc = launch_transpose(p->A1, p->ldA, p->A1t, p->ldA, qy, qy, nullptr);
         if (rc == SFB_OK) rc = upload_padded(p->B1, p->ldB, R, qx, qx);
-        for (int i = 0; i < qx; ++i)
-            for (int j = 0; j < qx; ++j) t[(size_t)j * qx + i] = R[(size_t)i * qx + j];
-        if (rc == SFB_OK) rc = upload_padded(p->B1t, p->ldB, t.data(), qx, qx);
+        if (rc == SFB_OK) rc = cudaMemset(p->B1t, 0, (size_t)qx * p->ldB * 8) == cudaSuccess ? SFB_OK : SFB_ERR_CUDA;
+        if (rc == SFB_OK) rc = launch_transpose(p->B1, p->ldB, p->B1t, p->ldB, qx, qx, nullptr);
+        if (rc == SFB_OK && cudaDeviceSynchronize() != cudaSuccess) rc = SFB_ERR_CUDA;
         std::vector<double> vl(lamL, lamL + qy), vr(lamR, lamR + qx);
         if (kind == SFB_PRE_SPECTRAL_PROD) {
             for (auto& v : vl) v = 1.0 / v;

@@ -382,6 +382,22 @@ __global__ void __launch_bounds__(VT) sh_dots_kernel(const double* A, const doub
 
 }  // namespace
 
+// dst = src^T (rows x cols -> cols x rows) through 32 x 33 shared tiles.
+__global__ void transpose_kernel(const double* __restrict__ src, int lds, double* __restrict__ dst, int ldd,
+                                 int rows, int cols) {
+    __shared__ double tl[32][33];
+    const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
+    for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+        const int r = r0 + k, c = c0 + threadIdx.x;
+        if (r < rows && c < cols) tl[k][threadIdx.x] = src[(size_t)r * lds + c];
+    }
+    __syncthreads();
+    for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+        const int c = c0 + k, r = r0 + threadIdx.x;
+        if (c < cols && r < rows) dst[(size_t)c * ldd + r] = tl[threadIdx.x][k];
+    }
+}
+
 int vector_grid_blocks() { return VB; }
 
 int launch_pcg_init_plain(const double* rhs, int ldr, double* R, double* U, int ld, int rows, int cols,
@@ -466,6 +482,13 @@ int launch_sh_xpby(double* Q, int ldq, const double* Z, int ldz, int rows, int c
 int launch_sh_dots(const double* A, const double* B, const double* C, const double* D, int ld, int rows, int cols,
                    double* partials, RedSlots* out, cudaStream_t s) {
     SFB_TRY(launch_kernel(sh_dots_kernel, dim3(VB), dim3(VT), 0, s, A, B, C, D, ld, rows, cols, partials, out));
+    SFB_CHECK_LAUNCH();
+    return SFB_OK;
+}
+
+int launch_transpose(const double* src, int lds, double* dst, int ldd, int rows, int cols, cudaStream_t s) {
+    const dim3 grid((cols + 31) / 32, (rows + 31) / 32), block(32, 8);
+    transpose_kernel<<<grid, block, 0, s>>>(src, lds, dst, ldd, rows, cols);
     SFB_CHECK_LAUNCH();
     return SFB_OK;
 }

@@ -381,8 +381,15 @@ def make_preconditioner(kind: str, x: DirectionSet, y: DirectionSet, *, d_u: flo
 
 
 # ------------------------------------------------------ spectral solve -----
-def _fix_eigvectors(vecs: np.ndarray) -> np.ndarray:
-    """Largest-magnitude entry of each column positive (solvers.py:203-208)."""
+def _fix_eigvectors(vecs):
+    """Largest-magnitude entry of each column positive (solvers.py:203-208).
+    Device tensors stay on the device."""
+    if nat.is_device(vecs):
+        t = nat.torch()
+        idx = t.argmax(vecs.abs(), dim=0)
+        signs = t.sign(vecs[idx, t.arange(vecs.shape[1], device=vecs.device)])
+        signs[signs == 0] = 1.0
+        return (vecs * signs).contiguous()
     idx = np.argmax(np.abs(vecs), axis=0)
     signs = np.sign(vecs[idx, np.arange(vecs.shape[1])])
     signs[signs == 0] = 1.0
@@ -400,10 +407,16 @@ def _min_abs_pair_sum(a: np.ndarray, b: np.ndarray) -> float:
     return float(best.min())
 
 
+def _host_mat(m) -> np.ndarray:
+    return m.cpu().numpy() if nat.is_device(m) else m
+
+
 @dataclass
 class SpectralCache:
     """Eigen-factorisations of the two pencils of a two-term equation
-    (solvers.py:211-253); the device sandwich is built on first use."""
+    (solvers.py:211-253); the device sandwich is built on first use.  P1/P2
+    are numpy arrays (host eigensolver) or CUDA tensors (device eigensolver:
+    they never leave the GPU on the solve path)."""
 
     lam1: np.ndarray
     lam2: np.ndarray
@@ -415,19 +428,19 @@ class SpectralCache:
 
     @property
     def X1(self):
-        return self.P1
+        return _host_mat(self.P1)
 
     @property
     def X1inv(self):
-        return self.P1.T @ np.asarray(self.G2)
+        return _host_mat(self.P1).T @ np.asarray(self.G2)
 
     @property
     def X2(self):
-        return np.asarray(self.H1) @ self.P2
+        return np.asarray(self.H1) @ _host_mat(self.P2)
 
     @property
     def X2inv(self):
-        return self.P2.T
+        return _host_mat(self.P2).T
 
     def kernel(self) -> np.ndarray:
         self.check_pencils()
@@ -444,9 +457,11 @@ class SpectralCache:
             L = nat.lib()
             qy, qx = self.P1.shape[0], self.P2.shape[0]
             out = nat.C.c_void_p()
-            nat.check(L.sfb_pre_create(qy, qx, nat.PRE_SPECTRAL_SUM,
-                                       nat.host_ptr(np.ascontiguousarray(self.P1)),
-                                       nat.host_ptr(np.ascontiguousarray(self.P2)),
+
+            # device tensors are read in place (sfb_pre_create copies device to device)
+            keep = [m.contiguous() if nat.is_device(m) else np.ascontiguousarray(m) for m in (self.P1, self.P2)]
+            ptrs = [nat.ptr(m) if nat.is_device(m) else nat.host_ptr(m) for m in keep]
+            nat.check(L.sfb_pre_create(qy, qx, nat.PRE_SPECTRAL_SUM, ptrs[0], ptrs[1],
                                        nat.host_ptr(np.ascontiguousarray(self.lam1)),
                                        nat.host_ptr(np.ascontiguousarray(self.lam2)), nat.C.byref(out)),
                       "spectral cache")
@@ -455,13 +470,26 @@ class SpectralCache:
         return h.p
 
 
+def _dense_device(m):
+    """Dense fp64 CUDA copy of a factor; band-stored factors are scattered on
+    the device from their (row, col, value) triplets (no dense host array)."""
+    t = nat.torch()
+    if isinstance(m, Band):
+        c = m.sparse.tocoo()
+        out = t.zeros(m.shape, dtype=t.float64, device="cuda")
+        rows = t.from_numpy(c.row.astype(np.int64)).cuda()
+        cols = t.from_numpy(c.col.astype(np.int64)).cuda()
+        out.index_put_((rows, cols), t.from_numpy(np.asarray(c.data, dtype=float)).cuda(), accumulate=True)
+        return out
+    return t.from_numpy(np.ascontiguousarray(np.asarray(m, dtype=float))).cuda()
+
+
 def _geigh_device(A, B):
     """Generalized SPD eigenproblem A v = lam B v on the GPU (setup only):
     B = L L^T (cuSOLVER potrf), the standard problem L^-1 A L^-T (cuSOLVER
     syevd), v = L^-T y.  Eigenvectors are B-orthonormal like LAPACK dsygvd's."""
     t = nat.torch()
-    Ad = t.from_numpy(np.ascontiguousarray(np.asarray(A, dtype=float))).cuda()
-    Bd = t.from_numpy(np.ascontiguousarray(np.asarray(B, dtype=float))).cuda()
+    Ad, Bd = _dense_device(A), _dense_device(B)
     L, info = t.linalg.cholesky_ex(0.5 * (Bd + Bd.T))
     if int(info.item()) != 0:
         raise np.linalg.LinAlgError("matrix B is not positive definite")
@@ -469,7 +497,7 @@ def _geigh_device(A, B):
     M = t.linalg.solve_triangular(L, M.T, upper=False)
     lam, Y = t.linalg.eigh(0.5 * (M + M.T))
     V = t.linalg.solve_triangular(L.T, Y, upper=True)
-    return lam.cpu().numpy(), V.cpu().numpy()
+    return lam.cpu().numpy(), V.contiguous()
 
 
 def build_spectral_cache(op: SylvesterOperator, eig: str = "host") -> SpectralCache:
