@@ -108,3 +108,16 @@ def test_banded_mode_mo_pcg_multi_segment_matches_inverse_mode():
                       stop=pb.relative_residual(1e-10), max_iter=20000) for m in ("inverse", "banded")]
     assert abs(reps[0].iterations - reps[1].iterations) <= max(2, reps[0].iterations // 200)
     assert relerr(reps[1].solution, reps[0].solution) <= 1e-8
+
+
+def test_two_term_preconditioner_in_imex_heat_matches_reference_trajectory(golden):
+    # cfg4-type (P4, wave domain): the f3 preconditioner changes iteration
+    # counts only; at tol 1e-12 the trajectory is the reference's
+    x, y = pb.build_direction_sets(WAVE, 4, 8, D)
+    F = sine_source(8, 8, 4)
+    tr = pb.imex_euler_heat(WAVE, x, y, 1.0, pb.SeparableSource(F, lambda t: np.exp(-t)), golden["heat/u0"],
+                            pb.TimeGrid(1e-3, 5e-3),
+                            inner=pb.InnerSolver(rule="residual", tol=1e-12, max_iter=5000, precond="two_term"))
+    assert np.all(tr.iterations < golden["heat/t12/iters"])
+    assert relerr(tr.final[0], golden["heat/t12/U"]) <= 1e-10
+    assert np.allclose(tr.increments, golden["heat/t12/incs"], rtol=1e-8)
