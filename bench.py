@@ -294,8 +294,8 @@ def run_native(args):
         el_b = e0.elapsed_time(e1) / 1e3
         alt["banded"] = {"value": qy * qx * its_b / el_b, "unit": UNIT, "ms_per_step": 1e3 * el_b / args.steps,
                          "iteration_ms": statistics.median(lms) / K_it,
-                         "note": "SURVEY §8 f1: same preconditioner P_L U P_R applied by segmented banded "
-                                 "Cholesky solves instead of dense-inverse GEMMs (parity-neutral)"}
+                         "note": "SURVEY §8 f1: same preconditioner P_L U P_R applied by SPIKE-partitioned banded "
+                                 "solves instead of dense-inverse GEMMs (parity-neutral)"}
 
     # ---- time to solution: the full cfg3 solve to the BASELINE tolerance 1e-8 ----
     tts = None
