@@ -154,6 +154,18 @@ def to_device(a):
     return t.from_numpy(np.ascontiguousarray(np.asarray(a, dtype=np.float64))).to("cuda")
 
 
+def to_host(t) -> np.ndarray:
+    """CUDA tensor -> numpy array returned to the caller.  The copy lands in
+    page-locked memory from torch's caching host allocator (the numpy array
+    keeps that block alive; it returns to the cache when the array dies):
+    a DMA at full PCIe/NVLink-C2C rate instead of a pageable copy that
+    first-touches a freshly mapped host buffer."""
+    th = torch()
+    out = th.empty(tuple(t.shape), dtype=t.dtype, pin_memory=True)
+    out.copy_(t)
+    return out.numpy()
+
+
 def ptr(t) -> int:
     return t.data_ptr()
 

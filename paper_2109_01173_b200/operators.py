@@ -196,7 +196,7 @@ class SylvesterOperator:
         W = t.empty_like(Ud)
         qx = self.shape[1]
         nat.check(nat.lib().sfb_op_apply(h, nat.ptr(Ud), qx, nat.ptr(W), qx, nat.stream()), "apply")
-        return W if on_dev else W.cpu().numpy()
+        return W if on_dev else nat.to_host(W)
 
     __call__ = apply
 
@@ -250,7 +250,7 @@ class RhsBuilder:
         out = t.empty(self.out_shape, dtype=t.float64, device="cuda")
         nat.check(nat.lib().sfb_map_apply(self.native(), nat.ptr(Fd), self.in_shape[1], nat.ptr(out),
                                           self.out_shape[1], nat.stream()), "rhs")
-        return out if on_dev else out.cpu().numpy()
+        return out if on_dev else nat.to_host(out)
 
     def heat(self, U, c: float, F=None, out=None, check: bool = True):
         """rhs of W = expand(U) + c F (device tensors); returns (rhs, [max|W|, #nonfinite])."""

@@ -287,7 +287,7 @@ class Preconditioner:
         Z = t.empty_like(Ud)
         nat.check(nat.lib().sfb_pre_apply(self.native(), nat.ptr(Ud), qx, nat.ptr(Z), qx, nat.stream()),
                   "apply_inverse")
-        return Z if on_dev else Z.cpu().numpy()
+        return Z if on_dev else nat.to_host(Z)
 
 
 IDENTITY_PRECONDITIONER = "identity"
@@ -336,7 +336,7 @@ class TwoTermPreconditioner:
         Z = t.empty_like(Ud)
         nat.check(nat.lib().sfb_pre_apply(self.native(), nat.ptr(Ud), qx, nat.ptr(Z), qx, nat.stream()),
                   "apply_inverse")
-        return Z if on_dev else Z.cpu().numpy()
+        return Z if on_dev else nat.to_host(Z)
 
 
 def two_term_preconditioner(op: SylvesterOperator, which=(0, 1), eig: str = "device") -> TwoTermPreconditioner:
@@ -542,7 +542,7 @@ def solve_reduced(op: SylvesterOperator, rhs, cache: SpectralCache | None = None
     nat.check(L.sfb_op_residual(op.native(), nat.ptr(U), qx, nat.ptr(B), qx, nat.dptr(out2), nat.stream()),
               "residual")
     res = out2[0] / max(out2[1], 1e-300)
-    return SolveReport(solution=U if on_dev else U.cpu().numpy(), method="reduced", iterations=0,
+    return SolveReport(solution=U if on_dev else nat.to_host(U), method="reduced", iterations=0,
                        residual_history=np.array([res]), stop_reason="direct",
                        wall_time=time.perf_counter() - t0,
                        diagnostics={"pencil_swapped": cache.swapped})
@@ -591,7 +591,7 @@ def solve_reduced_closed_form(gamma: float, f_nodal, N: int) -> SolveReport:
     lt = t.from_numpy(lam).to("cuda")
     denom = lt[:, None] + lt[None, :]
     res = float(t.linalg.norm(denom * uh - fh) / max(float(t.linalg.norm(fh)), 1e-300))
-    return SolveReport(solution=U if on_dev else U.cpu().numpy(), method="reduced-closed", iterations=0,
+    return SolveReport(solution=U if on_dev else nat.to_host(U), method="reduced-closed", iterations=0,
                        residual_history=np.array([res]), stop_reason="direct",
                        wall_time=time.perf_counter() - t0,
                        diagnostics={"residual_space": "spectral"})
@@ -685,8 +685,8 @@ def mo_pcg(op: SylvesterOperator, rhs, precond: Preconditioner | None = None,
                        "precond_mode": "identity" if precond.is_identity else precond.mode,
                        "operator": "banded" if op.banded else "dense"}}
     if record_iterates:
-        host = its[: n + 1].cpu().numpy()
+        host = nat.to_host(its[: n + 1])
         diag["iterates"] = [host[i] for i in range(n + 1)]
-    return SolveReport(solution=U if on_dev else U.cpu().numpy(), method="mo-pcg", iterations=n,
+    return SolveReport(solution=U if on_dev else nat.to_host(U), method="mo-pcg", iterations=n,
                        residual_history=hist[: n + 1].copy(), stop_reason=_REASONS[res.stop_reason],
                        wall_time=time.perf_counter() - t0, diagnostics=diag)

@@ -137,7 +137,7 @@ def _bad(chk) -> bool:
 
 
 def _host(t):
-    return t.cpu().numpy()
+    return nat.to_host(t)
 
 
 def _solve(op, rhs, pre, stop, warm, inner: InnerSolver):
