@@ -257,6 +257,7 @@ def run_native(args):
     # ---- e2e through the drop-in API with host buffers ----
     e2e = None
     if not args.no_e2e:
+        step(w.rhs)  # warm-up of the host path (page-locked result buffers enter the cache)
         barrier()
         e0.record()
         its_e = 0
