@@ -8,9 +8,11 @@
 //
 // sm_100a has no FP64 tcgen05 kind, so the FP64 tensor path is the warp-level
 // DMMA.8x8x4 (mma.sync m8n8k4 f64).  Tiles are staged by TMA
-// (cp.async.bulk.tensor, SWIZZLE_128B) into a 4-stage shared-memory ring
-// guarded by mbarriers; one thread issues the copies three k-tiles ahead and
-// all eight warps (two per SM sub-partition, 255-register budget) issue DMMA.
+// (cp.async.bulk.tensor, SWIZZLE_128B) into a 5-stage shared-memory ring
+// guarded by full/empty mbarriers; one thread issues the copies three k-tiles
+// ahead (after the slot's empty barrier completes: every warp released it)
+// and sixteen warps (four per SM sub-partition, 32 x 32 warp tiles, 128
+// registers) issue DMMA.
 // Both operands are K-contiguous ("NT"), which lets every fragment load be a
 // conflict-free LDS.128: thread t of a quad owns the
 // physical k = 4t+s for mma step s, so A[row][4t..4t+3] and Bt[col][4t..4t+3]
@@ -38,8 +40,12 @@ constexpr int BM = 128, BN = 128, BK = 16, STAGES = GEMM_STAGES;
 // barriers one slot of slack lets warps drift by a k-tile without stalling
 // the issuing thread
 constexpr int LOOKAHEAD = GEMM_EMPTY ? STAGES - 2 : STAGES - 1;
-constexpr int NWARPS = 8;                   // 2 x 4 warp grid, 64 x 32 per warp
-constexpr int NTHREADS = NWARPS * 32;       // 2 warps per SM sub-partition (<= 255 regs each)
+#ifndef GEMM_WM
+#define GEMM_WM 32  // rows per warp: 32 (16 warps, 128 regs; measured +4 % at q = 2047) or 64 (8 warps, 255 regs)
+#endif
+constexpr int WM = GEMM_WM, MI = WM / 8;   // warp tile WM x 32: MI x 4 DMMA 8x8 blocks
+constexpr int NWARPS = (BM / WM) * 4;      // (BM/WM) x 4 warp grid
+constexpr int NTHREADS = NWARPS * 32;
 constexpr int TILE_BYTES = BM * BK * 8;     // 16 KB per operand per stage
 constexpr int SMEM_BYTES = 2 * STAGES * TILE_BYTES + 2 * STAGES * 8 + 1024;
 
@@ -70,12 +76,12 @@ struct Sched {
 };
 
 // Epilogue of one finished 128x128 tile (registers -> global).
-__device__ __forceinline__ double tile_epilogue(double (&acc)[8][4][2], const GemmEpi& ep, int M, int N, int m0,
+__device__ __forceinline__ double tile_epilogue(double (&acc)[MI][4][2], const GemmEpi& ep, int M, int N, int m0,
                                                 int n0, int wm, int wn, int g, int t) {
     double dot = 0.0;
     #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        const int m = m0 + wm * 64 + i * 8 + g;
+    for (int i = 0; i < MI; ++i) {
+        const int m = m0 + wm * WM + i * 8 + g;
         if (m >= M) continue;
         #pragma unroll
         for (int j = 0; j < 4; ++j) {
@@ -135,7 +141,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const uint32_t empty = full + 8 * STAGES;  // one arrive per warp when it is done reading a slot
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int wm = warp >> 2, wn = warp & 3;  // 2 x 4 warps, 64 x 32 each
+    const int wm = warp >> 2, wn = warp & 3;  // (BM/WM) x 4 warps, WM x 32 each
     const int g = lane >> 2, t = lane & 3;
     const int KT = sc.KT;
     const long long beg = sc.start(blockIdx.x), fin = sc.start(blockIdx.x + 1);
@@ -164,7 +170,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     __syncthreads();
 
     double dot = 0.0;
-    double acc[8][4][2];
+    double acc[MI][4][2];
     int it = 0;
     while (it < n_it) {
         const long long li0 = beg + it;
@@ -172,7 +178,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const int seg_end = (int)min((long long)n_it, (long long)it + (KT - k0));
         const int kl = k0 + (seg_end - it) - 1;  // last k-tile of this piece
         #pragma unroll
-        for (int i = 0; i < 8; ++i)
+        for (int i = 0; i < MI; ++i)
             #pragma unroll
             for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
@@ -189,22 +195,22 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             if (threadIdx.x == 0 && it + LOOKAHEAD < n_it) issue(it + LOOKAHEAD);
 #endif
             mbar_wait_u32(full + 8 * s, (it / STAGES) & 1);
-            const uint32_t a_base = sA + s * TILE_BYTES + (wm * 64 + g) * 128;
+            const uint32_t a_base = sA + s * TILE_BYTES + (wm * WM + g) * 128;
             const uint32_t b_base = sB + s * TILE_BYTES + (wn * 32 + g) * 128;
             #pragma unroll
             for (int half = 0; half < 2; ++half) {
                 const uint32_t ch = ((2 * t + half) ^ g) << 4;  // SWIZZLE_128B: chunk ^= row & 7 (= g)
-                double2 a[8], b[4];
+                double2 a[MI], b[4];
                 #pragma unroll
-                for (int i = 0; i < 8; ++i) a[i] = lds128(a_base + i * 1024 + ch);
+                for (int i = 0; i < MI; ++i) a[i] = lds128(a_base + i * 1024 + ch);
                 #pragma unroll
                 for (int j = 0; j < 4; ++j) b[j] = lds128(b_base + j * 1024 + ch);
                 #pragma unroll
-                for (int i = 0; i < 8; ++i)
+                for (int i = 0; i < MI; ++i)
                     #pragma unroll
                     for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i].x, b[j].x);
                 #pragma unroll
-                for (int i = 0; i < 8; ++i)
+                for (int i = 0; i < MI; ++i)
                     #pragma unroll
                     for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i].y, b[j].y);
             }
@@ -219,7 +225,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             // continuation piece: park the partial tile and count it
             double* w = ep.sk_ws + (size_t)blockIdx.x * (BM * BN);
             #pragma unroll
-            for (int i = 0; i < 8; ++i)
+            for (int i = 0; i < MI; ++i)
                 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
                     const int e = (i * 4 + j) * 2;
@@ -244,7 +250,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 for (int c = (int)blockIdx.x + 1; c <= last; ++c) {
                     const double* w = ep.sk_ws + (size_t)c * (BM * BN);
                     #pragma unroll
-                    for (int i = 0; i < 8; ++i)
+                    for (int i = 0; i < MI; ++i)
                         #pragma unroll
                         for (int j = 0; j < 4; ++j) {
                             const int e = (i * 4 + j) * 2;
