@@ -45,7 +45,7 @@ constexpr int NSUB = S / SS;   // sub-segments per segment
 constexpr int NT = S * NSUB;   // threads per tile CTA
 
 enum { DIR_COL = 0, DIR_ROW = 1 };
-enum { PH_LOCAL = 0, PH_FUSED = 1, PH_FIX = 2 };
+enum { PH_LOCAL = 0, PH_FUSED = 1 };  // plain local solve, or the previous factor's correction first
 
 // tile[k][c] (padded): k = position along the sweep, c = line.  DIR_COL:
 // lines are columns (P acts from the left), DIR_ROW: lines are rows (P acts
@@ -144,7 +144,7 @@ struct SpikeArgs {
     int ldi;
     double* X;
     int ld;
-    // <Z,R> (PH_FIX of the right factor)
+    // <Z,R> (spike_fix_kernel of the right factor)
     const double* R;
     int ldr;
     double* partials;
@@ -246,29 +246,20 @@ __global__ void __launch_bounds__(NT) spike_tile_kernel(SpikeArgs a) {
     __shared__ double bandS[(S + 4) * 5];   // rows start .. start+S+B-1 of the segment factor
     __shared__ double H16s[NSUB * SS * BB];
     __shared__ double T16s[NSUB * BB * BB];
-    // spikes of this segment (PH_FIX) or of the previous factor (PH_FUSED, used
-    // before the local solve needs sst): aliased onto sst (2 S B <= NSUB B S)
+    // PH_FUSED: the previous factor's spikes, used before the local solve
+    // needs sst, aliased onto it (2 S B <= NSUB B S)
     double (*VWs)[S * BB] = reinterpret_cast<double (*)[S * BB]>(&sst[0][0][0]);
     const int p = blockIdx.x;             // segment along the sweep
     const int line0 = blockIdx.y * S;     // first line of this tile
     const int start = p * S;
     const int len = min(S, a.n - start);
-    const int P = (a.n + S - 1) / S;
     const int t = threadIdx.x, c = t % S, k = t / S;  // line, sub-segment
     const int gl = line0 + c;
     const bool live = gl < a.nlines;
 
-    if (PH != PH_FIX) {
-        for (int i = t; i < (S + B) * (B + 1); i += NT) {
-            const int row = start + i / (B + 1);
-            bandS[i] = row < a.n + B ? a.band[(size_t)start * (B + 1) + i] : 0.0;
-        }
-    }
-    if (PH == PH_FIX && B > 0) {
-        for (int i = t; i < S * B; i += NT) {
-            VWs[0][i] = a.V[(size_t)p * S * B + i];
-            VWs[1][i] = a.W[(size_t)p * S * B + i];
-        }
+    for (int i = t; i < (S + B) * (B + 1); i += NT) {
+        const int row = start + i / (B + 1);
+        bandS[i] = row < a.n + B ? a.band[(size_t)start * (B + 1) + i] : 0.0;
     }
     if (PH == PH_FUSED && B > 0) {
         // the previous factor acts along this tile's lines: its segment is blockIdx.y
@@ -308,59 +299,101 @@ __global__ void __launch_bounds__(NT) spike_tile_kernel(SpikeArgs a) {
         __syncthreads();
     }
 
-    if (PH != PH_FIX) {
-        // local solve P_p g = x: forward with L_p, backward with L_p^T
-        {
-            const int n16 = (a.n + SS - 1) / SS;
-            for (int i = t; i < NSUB * SS * BB; i += NT)
-                H16s[i] = p * NSUB + i / (SS * BB) < n16 ? a.Hf16[(size_t)p * NSUB * SS * BB + i] : 0.0;
-            for (int i = t; i < NSUB * BB * BB; i += NT)
-                T16s[i] = p * NSUB + i / (BB * BB) < n16 ? a.Tf16[(size_t)p * NSUB * BB * BB + i] : 0.0;
-        }
-        __syncthreads();
-        tile_solve<B, true>(tile, sst, bandS, H16s, T16s, len, c, k, live);
-        {
-            const int n16 = (a.n + SS - 1) / SS;
-            for (int i = t; i < NSUB * SS * BB; i += NT)
-                H16s[i] = p * NSUB + i / (SS * BB) < n16 ? a.Hb16[(size_t)p * NSUB * SS * BB + i] : 0.0;
-            for (int i = t; i < NSUB * BB * BB; i += NT)
-                T16s[i] = p * NSUB + i / (BB * BB) < n16 ? a.Tb16[(size_t)p * NSUB * BB * BB + i] : 0.0;
-        }
-        __syncthreads();
-        tile_solve<B, false>(tile, sst, bandS, H16s, T16s, len, c, k, live);
-        if (B > 0 && live && k == 0) {
-            // interface values of g: first B and last B rows of the segment
-            #pragma unroll
-            for (int d = 0; d < B; ++d) {
-                a.sv[((size_t)p * 2 * B + d) * a.nlines + gl] = d < len ? tile[d][c] : 0.0;
-                const int r = len - B + d;
-                a.sv[((size_t)p * 2 * B + B + d) * a.nlines + gl] = r >= 0 ? tile[r][c] : 0.0;
-            }
-        }
-    } else if (B > 0 && live) {
-        // spike correction y = g - V_p t_{p+1} - W_p u_{p-1}
-        double tn[BB], up[BB];
+    // local solve P_p g = x: forward with L_p, backward with L_p^T
+    const int n16 = (a.n + SS - 1) / SS;
+    for (int i = t; i < NSUB * SS * BB; i += NT)
+        H16s[i] = p * NSUB + i / (SS * BB) < n16 ? a.Hf16[(size_t)p * NSUB * SS * BB + i] : 0.0;
+    for (int i = t; i < NSUB * BB * BB; i += NT)
+        T16s[i] = p * NSUB + i / (BB * BB) < n16 ? a.Tf16[(size_t)p * NSUB * BB * BB + i] : 0.0;
+    __syncthreads();
+    tile_solve<B, true>(tile, sst, bandS, H16s, T16s, len, c, k, live);
+    for (int i = t; i < NSUB * SS * BB; i += NT)
+        H16s[i] = p * NSUB + i / (SS * BB) < n16 ? a.Hb16[(size_t)p * NSUB * SS * BB + i] : 0.0;
+    for (int i = t; i < NSUB * BB * BB; i += NT)
+        T16s[i] = p * NSUB + i / (BB * BB) < n16 ? a.Tb16[(size_t)p * NSUB * BB * BB + i] : 0.0;
+    __syncthreads();
+    tile_solve<B, false>(tile, sst, bandS, H16s, T16s, len, c, k, live);
+    if (B > 0 && live && k == 0) {
+        // interface values of g: first B and last B rows of the segment
         #pragma unroll
         for (int d = 0; d < B; ++d) {
-            tn[d] = p + 1 < P ? a.sv[((size_t)(p + 1) * 2 * B + d) * a.nlines + gl] : 0.0;
-            up[d] = p > 0 ? a.sv[((size_t)(p - 1) * 2 * B + B + d) * a.nlines + gl] : 0.0;
-        }
-        #pragma unroll 4
-        for (int kk = k; kk < len; kk += NSUB) {
-            double v = tile[kk][c];
-            #pragma unroll
-            for (int d = 0; d < B; ++d) {
-                v = fma(-VWs[0][kk * B + d], tn[d], v);
-                v = fma(-VWs[1][kk * B + d], up[d], v);
-            }
-            tile[kk][c] = v;
+            a.sv[((size_t)p * 2 * B + d) * a.nlines + gl] = d < len ? tile[d][c] : 0.0;
+            const int r = len - B + d;
+            a.sv[((size_t)p * 2 * B + B + d) * a.nlines + gl] = r >= 0 ? tile[r][c] : 0.0;
         }
     }
-    if (PH == PH_FIX) __syncthreads();
-    const bool want_dot = PH == PH_FIX && a.R != nullptr;
-    const double dot = tile_store<DIR>(tile, a.X, a.ld, start, line0, a.n, a.nlines, want_dot ? a.R : nullptr, a.ldr);
-    if (want_dot) {
-        // <Z,R> over this tile (deterministic: fixed thread/tile order)
+    tile_store<DIR>(tile, a.X, a.ld, start, line0, a.n, a.nlines);
+}
+
+// Interface system of one factor, one thread per line: block-LU forward
+// chain d_p = K_p gamma_p - KA_p u(d_{p-1}), backward z_p = d_p - Ch_p t(z_{p+1})
+// (K, KA, Ch precomputed; read through L1, the same for every line).  The CTA
+// first stages its lines' gamma values in shared memory with all loads in
+// flight, runs both chains there in place (every operand off the chain is a
+// shared-memory or L1 load that can be issued early) and writes the
+// interface solution z_p = (t_p, u_p) back in one coalesced pass.
+// Spike correction y = g - V_p t_{p+1} - W_p u_{p-1} of one 64 x 64 tile,
+// register to register: each thread keeps the tile elements of one global
+// column (the load/store mapping of tile_load/tile_store, coalesced) and
+// the interface values of the tile's 64 lines come from shared memory.
+// <Z,R> optional (one partial per CTA, last CTA sums them in order).
+template <int B, int DIR>
+__global__ void __launch_bounds__(NT) spike_fix_kernel(SpikeArgs a) {
+    SFB_PDL_PROLOGUE();
+    if (a.gate != nullptr && a.gate->status != SFB_PCG_RUNNING) return;
+    constexpr int BB = B > 0 ? B : 1;
+    __shared__ double tu[2][BB][S];     // t_{p+1}, u_{p-1} of the tile's lines
+    __shared__ double VW[2][S][BB];     // this segment's spikes
+    const int p = blockIdx.x, line0 = blockIdx.y * S, start = p * S;
+    const int P = (a.n + S - 1) / S;
+    const int t = threadIdx.x, lo = t % S, hi = t / S;
+    for (int i = t; i < 2 * B * S; i += NT) {
+        const int which = i / (B * S), d = (i / S) % B, l = i % S, gl = line0 + l;
+        double v = 0.0;
+        if (gl < a.nlines) {
+            if (which == 0 && p + 1 < P) v = a.sv[((size_t)(p + 1) * 2 * B + d) * a.nlines + gl];
+            if (which == 1 && p > 0) v = a.sv[((size_t)(p - 1) * 2 * B + B + d) * a.nlines + gl];
+        }
+        tu[which][d][l] = v;
+    }
+    for (int i = t; i < S * B; i += NT) {
+        VW[0][i / B][i % B] = a.V[(size_t)p * S * B + i];
+        VW[1][i / B][i % B] = a.W[(size_t)p * S * B + i];
+    }
+    __syncthreads();
+    // global rows rb + hi + NSUB u, column cb + lo (as tile_load/tile_store)
+    const int rb = DIR == DIR_COL ? start : line0, cb = DIR == DIR_COL ? line0 : start;
+    const int nr = DIR == DIR_COL ? a.n : a.nlines, nc = DIR == DIR_COL ? a.nlines : a.n;
+    const bool cok = cb + lo < nc;
+    const double* gp = a.Xin + (size_t)(rb + hi) * a.ldi + cb + lo;
+    double* yp = a.X + (size_t)(rb + hi) * a.ld + cb + lo;
+    const double* rp = a.R != nullptr ? a.R + (size_t)(rb + hi) * a.ldr + cb + lo : nullptr;
+    const size_t si = (size_t)NSUB * a.ldi, so = (size_t)NSUB * a.ld, sr = (size_t)NSUB * a.ldr;
+    double g[S / NSUB], r[S / NSUB];
+    #pragma unroll
+    for (int u = 0; u < S / NSUB; ++u) {
+        const bool ok = cok && rb + hi + u * NSUB < nr;
+        g[u] = ok ? gp[u * si] : 0.0;
+        r[u] = (ok && rp != nullptr) ? rp[u * sr] : 0.0;
+    }
+    double dot = 0.0;
+    #pragma unroll
+    for (int u = 0; u < S / NSUB; ++u) {
+        const int kk = hi + u * NSUB;             // tile row
+        const int pos = DIR == DIR_COL ? kk : lo;  // position along the sweep
+        const int ln = DIR == DIR_COL ? lo : kk;   // line within the tile
+        double v = g[u];
+        #pragma unroll
+        for (int d = 0; d < B; ++d) {
+            v = fma(-VW[0][pos][d], tu[0][d][ln], v);
+            v = fma(-VW[1][pos][d], tu[1][d][ln], v);
+        }
+        if (cok && rb + kk < nr) {
+            yp[u * so] = v;
+            dot = fma(v, r[u], dot);
+        }
+    }
+    if (a.R != nullptr) {
         __shared__ double sh[NT / 32];
         const double part = block_sum<NT>(dot, sh);
         const unsigned nblk = gridDim.x * gridDim.y;
@@ -376,13 +409,6 @@ __global__ void __launch_bounds__(NT) spike_tile_kernel(SpikeArgs a) {
     }
 }
 
-// Interface system of one factor, one thread per line: block-LU forward
-// chain d_p = K_p gamma_p - KA_p u(d_{p-1}), backward z_p = d_p - Ch_p t(z_{p+1})
-// (K, KA, Ch precomputed; read through L1, the same for every line).  The CTA
-// first stages its lines' gamma values in shared memory with all loads in
-// flight, runs both chains there in place (every operand off the chain is a
-// shared-memory or L1 load that can be issued early) and writes the
-// interface solution z_p = (t_p, u_p) back in one coalesced pass.
 __device__ __forceinline__ void cp_async8(double* dst, const double* src) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
                  "l"(src)
@@ -528,7 +554,7 @@ int run_pair(const SpikeFactor& L, const SpikeFactor& Rf, const double* Rin, int
         SpikeArgs c = a;
         c.Xin = Z;
         c.ldi = ldz;
-        SFB_TRY(launch_kernel(spike_tile_kernel<BL, DIR_COL, PH_FIX>, gL, dim3(NT), 0, s, c));
+        SFB_TRY(launch_kernel(spike_fix_kernel<BL, DIR_COL>, gL, dim3(NT), 0, s, c));
         SFB_TRY(launch_kernel(spike_tile_kernel<BR, DIR_ROW, PH_LOCAL>, gR, dim3(NT), 0, s, b));
     }
     SFB_TRY(chain<BR>(Rf, qy, svR, gate, s));
@@ -540,7 +566,7 @@ int run_pair(const SpikeFactor& L, const SpikeFactor& Rf, const double* Rin, int
         b.pcg = dot->pcg;
         b.dot_out = dot->dot_out;
     }
-    return launch_kernel(spike_tile_kernel<BR, DIR_ROW, PH_FIX>, gR, dim3(NT), 0, s, b);
+    return launch_kernel(spike_fix_kernel<BR, DIR_ROW>, gR, dim3(NT), 0, s, b);
 }
 
 template <int BL>
