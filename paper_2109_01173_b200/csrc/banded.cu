@@ -10,7 +10,7 @@
 // (TX+W-1) input halo down the strip in chunks of CH rows through a 3-stage
 // TMA ring (full/empty mbarriers; out-of-bounds rows/columns arrive
 // zero-filled), together with the left-factor coefficients of those rows,
-// read as a box of the row-skewed copy gskew[t][j][d] = G_t[j-d][d] made at
+// read as a box of the row-skewed copy gskew[j][t*W+d] = G_t[j-d][d] made at
 // creation.  Four consumer warps (one thread per output column, right-factor
 // band in registers) sweep the rows of each landed chunk: Y_t(r) =
 // sum_e X[r][c+e] h_t[e] is formed once per row and scattered into a ring of
@@ -66,9 +66,9 @@ struct BandCfg {
     static constexpr int CH = chunk_rows<W>();
     static constexpr int HC = TX + W - 1;    // halo columns
     static constexpr int HCB = HC + 2;       // box columns: boxes start at an even column (16-byte rows)
-    static constexpr int WP = W + 1;         // even: coefficient pairs load as 16 bytes
+    static constexpr int TWP = (T * W + 1) / 2 * 2;  // a row's T*W left coefficients, padded to pairs
     static constexpr int XS = CH * HCB;      // doubles of one input box
-    static constexpr int GS = T * CH * WP;   // doubles of the chunk's left coefficients
+    static constexpr int GS = CH * TWP;      // doubles of the chunk's left coefficients
     static constexpr int XSP = pad128(XS);   // 128-byte aligned regions
     static constexpr int GSP = pad128(GS);
     static constexpr int STAGE = 2 * XSP + GSP;
@@ -78,7 +78,7 @@ struct BandCfg {
 struct BandMaps {
     CUtensorMap a;       // input A (X / Z / U / eta), box {HCB, CH}
     CUtensorMap b[2];    // input B (Q0, Q1 / F / theta)
-    CUtensorMap g;       // gskew, box {WP, CH, T}
+    CUtensorMap g;       // gskew, box {TWP, CH}
 };
 
 // rows per CTA and row blocks for an output of `rows` x `cols`
@@ -96,11 +96,11 @@ template <int T, int W, int MODE>
 __global__ void __launch_bounds__(TX + 32, band_minb<W>()) band_kernel(BandArgs a, const __grid_constant__ BandMaps maps, int ry) {
     SFB_PDL_PROLOGUE();
     using C = BandCfg<T, W>;
-    constexpr int CH = C::CH, HCB = C::HCB, WP = C::WP;
+    constexpr int CH = C::CH, HCB = C::HCB, TWP = C::TWP;
     constexpr int NPAIR = HCB / 2;           // HCB is even (W odd)
     constexpr int NPP = (NPAIR + 63) / 64;   // column pairs per thread in the transform
     constexpr int NRR = (CH + 1) / 2;        // rows per thread and chunk in the transform
-    extern __shared__ double sm_raw[];       // NS x {A[CH][HCB], B[CH][HCB], G[T][CH][WP]}
+    extern __shared__ double sm_raw[];       // NS x {A[CH][HCB], B[CH][HCB], G[CH][TWP]}
     // 128-byte aligned ring (pointer arithmetic on the shared array keeps LDS/STS addressing)
     double* sm = sm_raw + (((128u - (smem_u32(sm_raw) & 127u)) & 127u) >> 3);
     __shared__ __align__(8) uint64_t full[NS], empty[NS];
@@ -167,7 +167,7 @@ __global__ void __launch_bounds__(TX + 32, band_minb<W>()) band_kernel(BandArgs 
                 mbar_expect_tx_u32(bar, tx_bytes);
                 tma_load_u32(smem_u32(A), &maps.a, bar, x0 + hoff - acs - shA, y0 + goff + r0 - ars);
                 if (hasB) tma_load_u32(smem_u32(A + C::XSP), mb, bar, x0 + hoff - shB, y0 + goff + r0);
-                tma_load3_u32(smem_u32(A + 2 * C::XSP), &maps.g, bar, 0, y0 + r0, 0);
+                tma_load_u32(smem_u32(A + 2 * C::XSP), &maps.g, bar, 0, y0 + r0);
             }
         }
     } else {
@@ -307,17 +307,19 @@ __global__ void __launch_bounds__(TX + 32, band_minb<W>()) band_kernel(BandArgs 
                         const int gr = y0 + goff + r0 + rr;
                         if (gr >= y0 && gr < y0 + rows_here && col_ok) Qcur[(size_t)gr * a.ldq + gc] = cen[u];
                     }
+                    // scatter: the row's T*W left coefficients are contiguous (pairs may
+                    // straddle two terms), G[rr][tt*W + d] multiplies Y_tt into output row r - d
+                    const double2* gp = reinterpret_cast<const double2*>(G + rr * TWP);
                     #pragma unroll
-                    for (int tt = 0; tt < T; ++tt) {
-                        const double2* gp = reinterpret_cast<const double2*>(G + (tt * CH + rr) * WP);
+                    for (int f2 = 0; f2 < TWP / 2; ++f2) {
+                        const double2 g = gp[f2];
                         #pragma unroll
-                        for (int dd = 0; dd < WP / 2; ++dd) {
-                            const double2 g = gp[dd];
-                            const int s0 = (u - 2 * dd + 2 * W) % W;
-                            acc[s0] = fma(g.x, y[tt], acc[s0]);
-                            if (2 * dd + 1 < W) {
-                                const int s1 = (u - 2 * dd - 1 + 2 * W) % W;
-                                acc[s1] = fma(g.y, y[tt], acc[s1]);
+                        for (int q = 0; q < 2; ++q) {
+                            const int f = 2 * f2 + q;
+                            if (f < T * W) {
+                                const int tt = f / W, d = f - tt * W;
+                                const int sl = (u - d + 2 * W) % W;
+                                acc[sl] = fma(q == 0 ? g.x : g.y, y[tt], acc[sl]);
                             }
                         }
                     }
@@ -406,9 +408,10 @@ int launch_twm(const BandArgs& a, cudaStream_t stream) {
         }
     }
     {
-        const cuuint64_t dims[3] = {(cuuint64_t)C::WP, (cuuint64_t)a.gskew_rows, (cuuint64_t)a.nterms};
-        const cuuint32_t gbox[3] = {(cuuint32_t)C::WP, (cuuint32_t)C::CH, (cuuint32_t)T};
-        SFB_TRY(tma_make_map(&maps.g, a.gskew, 3, dims, C::WP, gbox, CU_TENSOR_MAP_SWIZZLE_NONE));
+        if (a.gskew_terms != T) return arg_error("banded kernel: skewed coefficients built for another term count");
+        const cuuint64_t dims[2] = {(cuuint64_t)C::TWP, (cuuint64_t)a.gskew_rows};
+        const cuuint32_t gbox[2] = {(cuuint32_t)C::TWP, (cuuint32_t)C::CH};
+        SFB_TRY(tma_make_map(&maps.g, a.gskew, 2, dims, C::TWP, gbox, CU_TENSOR_MAP_SWIZZLE_NONE));
     }
     int ry, nrb;
     band_geometry(a.out_rows, a.out_cols, band_minb<W>(), &ry, &nrb);
@@ -476,16 +479,19 @@ int launch_band(const BandArgs& a, cudaStream_t stream) {
     return launch_t<5>(b, stream);
 }
 
-// gskew[t][j][d] = gband[t][j - d][d] for 0 <= j - d < rows (zero elsewhere),
-// j in [0, rows + w - 1), d < w; rows padded to w + 1 doubles.
+// gskew[j][t * w + d] = gband[t][j - d][d] for 0 <= j - d < rows (zero
+// elsewhere), j in [0, rows + w - 1), t < band_skew_terms(nterms) (the
+// kernel's term slots), rows padded to an even number of doubles.
+int band_skew_terms(int nterms) { return nterms <= 1 ? 1 : (nterms == 2 ? 2 : 5); }
+
 std::vector<double> band_skew(const double* gband, int nterms, int rows, int w) {
-    const int R = rows + w - 1, WP = w + 1;
-    std::vector<double> out((size_t)nterms * R * WP, 0.0);
+    const int R = rows + w - 1, T = band_skew_terms(nterms), TWP = (T * w + 1) / 2 * 2;
+    std::vector<double> out((size_t)R * TWP, 0.0);
     for (int t = 0; t < nterms; ++t)
         for (int j = 0; j < R; ++j)
             for (int d = 0; d < w; ++d) {
                 const int i = j - d;
-                if (i >= 0 && i < rows) out[((size_t)t * R + j) * WP + d] = gband[((size_t)t * rows + i) * w + d];
+                if (i >= 0 && i < rows) out[(size_t)j * TWP + t * w + d] = gband[((size_t)t * rows + i) * w + d];
             }
     return out;
 }

@@ -48,8 +48,9 @@ struct BandArgs {
     int out_rows = 0, out_cols = 0, in_rows = 0, in_cols = 0;
     int nterms = 0, width = 1, goff = 0, hoff = 0;
     const double* gband = nullptr;  // [nterms][out_rows][width]
-    const double* gskew = nullptr;  // [nterms][gskew_rows][width + 1] (band_skew)
+    const double* gskew = nullptr;  // [gskew_rows][terms * width, padded even] (band_skew)
     int gskew_rows = 0;             // out_rows + width - 1
+    int gskew_terms = 0;            // band_skew_terms(nterms)
     const double* hband = nullptr;  // [nterms][out_cols][width]
     // loader
     int ld_mode = LD_PLAIN;
@@ -76,6 +77,7 @@ struct BandArgs {
 // Every input of `a` needs 16-byte aligned rows (even leading dimension).
 int launch_band(const BandArgs& a, cudaStream_t stream);
 std::vector<double> band_skew(const double* gband, int nterms, int rows, int w);
+int band_skew_terms(int nterms);
 bool band_supported(int nterms, int width);
 int band_grid_blocks(int out_rows, int out_cols);
 

@@ -171,23 +171,30 @@ inline int seg_tiles(int qy, int qx) {
     return ((qx + S - 1) / S) * ((qy + S - 1) / S);
 }
 
+// Banded-kernel arguments describing an operator's factors (every use).
+BandArgs op_band_args(const sfb_op* op) {
+    BandArgs a;
+    a.out_rows = a.in_rows = op->qy;
+    a.out_cols = op->qx;
+    a.in_cols = op->in_cols;
+    a.nterms = op->nterms;
+    a.width = op->width;
+    a.goff = op->goff;
+    a.hoff = op->hoff;
+    a.gband = op->gband;
+    a.gskew = op->gskew;
+    a.gskew_rows = op->qy + op->width - 1;
+    a.gskew_terms = band_skew_terms(op->nterms);
+    a.hband = op->hband;
+    return a;
+}
+
 // W = op(U) on device buffers (U must have an even ld and 16B alignment for
 // the dense path).  T1 is qx x qy scratch (ld ldt) for the dense path.
 int op_apply_impl(const sfb_op* op, const double* U, int ldu, double* W, int ldw, double* T1, int ldt,
                   const GemmWs* gw, cudaStream_t s) {
     if (!op->dense) {
-        BandArgs a;
-        a.out_rows = a.in_rows = op->qy;
-        a.out_cols = op->qx;
-        a.in_cols = op->in_cols;
-        a.nterms = op->nterms;
-        a.width = op->width;
-        a.goff = op->goff;
-        a.hoff = op->hoff;
-        a.gband = op->gband;
-        a.gskew = op->gskew;
-        a.gskew_rows = op->qy + op->width - 1;
-        a.hband = op->hband;
+        BandArgs a = op_band_args(op);
         a.ld_mode = LD_PLAIN;
         a.X = U;
         a.ldx = ldu;
@@ -321,17 +328,7 @@ int pcg_enqueue_iteration(sfb_pcg* s, double* iterates) {
     cudaStream_t st = s->stream;
     const sfb_op* op = s->op;
     if (!op->dense) {
-        BandArgs a;
-        a.out_rows = a.in_rows = s->qy;
-        a.out_cols = a.in_cols = s->qx;
-        a.nterms = op->nterms;
-        a.width = op->width;
-        a.goff = op->goff;
-        a.hoff = op->hoff;
-        a.gband = op->gband;
-        a.gskew = op->gskew;
-        a.gskew_rows = op->qy + op->width - 1;
-        a.hband = op->hband;
+        BandArgs a = op_band_args(op);
         a.ld_mode = LD_PCG;
         a.X = s->Z;
         a.ldx = s->ld;
@@ -669,6 +666,7 @@ BandArgs map_args(const sfb_map* m, double* out, int ldo) {
     a.gband = m->gband;
     a.gskew = m->gskew;
     a.gskew_rows = m->out_rows + m->width - 1;
+    a.gskew_terms = band_skew_terms(1);
     a.hband = m->hband;
     a.ep_mode = EP_STORE;
     a.W = out;
@@ -1078,17 +1076,7 @@ int sfb_pcg_pass_times(sfb_pcg* s, int reps, double* ms) {
     h.recorded = -1;
     SFB_CUDA_TRY(cudaMemcpyAsync(ps, &h, sizeof(h), cudaMemcpyHostToDevice, st));
     const sfb_op* op = s->op;
-    BandArgs a;
-    a.out_rows = a.in_rows = s->qy;
-    a.out_cols = a.in_cols = s->qx;
-    a.nterms = op->nterms;
-    a.width = op->width;
-    a.goff = op->goff;
-    a.hoff = op->hoff;
-    a.gband = op->gband;
-    a.gskew = op->gskew;
-    a.gskew_rows = op->qy + op->width - 1;
-    a.hband = op->hband;
+    BandArgs a = op_band_args(op);
     a.ld_mode = LD_PCG;
     a.X = s->Z;
     a.ldx = s->ld;
