@@ -43,11 +43,15 @@ constexpr int NTH = TX + 32;              // + one producer warp
 #ifndef BAND_NS
 #define BAND_NS 3
 #endif
+#ifndef BAND_MUNROLL
+#define BAND_MUNROLL 2
+#endif
 #ifndef BAND_MINB
 #define BAND_MINB 2
 #endif
 
-constexpr int NS = BAND_NS;                       // TMA ring stages
+constexpr int NS = BAND_NS;
+constexpr int kMUnroll = BAND_MUNROLL;  // unroll of the chunk's W-row groups                       // TMA ring stages
 // CTAs per SM (2 x 5 warps: 168 registers per thread keep the 5-term band
 // in registers; measured faster than 3 CTAs at 128 registers)
 template <int W>
@@ -282,7 +286,7 @@ __global__ void __launch_bounds__(TX + 32, band_minb<W>()) band_kernel(BandArgs 
                 asm volatile("bar.sync 1, %0;" ::"n"(TX) : "memory");  // transformed chunk visible
 
             // ---- sweep the chunk's halo rows (rows past the halo feed only unstored outputs) ----
-            #pragma unroll 1
+            #pragma unroll kMUnroll
             for (int m = 0; m < CH / W; ++m) {
                 #pragma unroll
                 for (int u = 0; u < W; ++u) {
@@ -325,15 +329,15 @@ __global__ void __launch_bounds__(TX + 32, band_minb<W>()) band_kernel(BandArgs 
                     }
                     const int i = r0 + rr - (W - 1);
                     const int slot = (u + 1) % W;
-                    if ((unsigned)i < (unsigned)rows_here && col_ok) {
-                        const double w = acc[slot];
-                        Wout[(size_t)(y0 + i) * ldw + gc] = w;
-                        if constexpr (pcg_ep) {
-                            // Q at (y0 + i, gc): centre of halo row i - goff = r - (W-1)/2
-                            const double q = cen[(u - (W - 1) / 2 + W) % W];
-                            pdot = fma(w, q, pdot);
-                            pqq = fma(q, q, pqq);
-                        }
+                    // branch-free epilogue: predicated store, masked dot terms
+                    const bool store = (unsigned)i < (unsigned)rows_here && col_ok;
+                    const double w = acc[slot];
+                    if (store) Wout[(size_t)(y0 + i) * ldw + gc] = w;
+                    if constexpr (pcg_ep) {
+                        // Q at (y0 + i, gc): centre of halo row i - goff = r - (W-1)/2
+                        const double q = store ? cen[(u - (W - 1) / 2 + W) % W] : 0.0;
+                        pdot = fma(w, q, pdot);
+                        pqq = fma(q, q, pqq);
                     }
                     acc[slot] = 0.0;
                 }
