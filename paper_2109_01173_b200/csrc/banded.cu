@@ -43,6 +43,9 @@ constexpr int NTH = TX + 32;              // + one producer warp
 #ifndef BAND_NS
 #define BAND_NS 3
 #endif
+#ifndef BAND_ACC2
+#define BAND_ACC2 0  // 1: split accumulators (measured: plain apply -2 %, MO-PCG pass +2 %)
+#endif
 #ifndef BAND_MUNROLL
 #define BAND_MUNROLL 2
 #endif
@@ -222,9 +225,11 @@ __global__ void __launch_bounds__(TX + 32, band_minb<W>()) band_kernel(BandArgs 
             for (int e = 0; e < W; ++e)
                 h[tt][e] = (tt < a.nterms && gc < a.out_cols) ? a.hband[((size_t)tt * a.out_cols + gc) * W + e] : 0.0;
 
-        double acc[W], cen[W];
+        // two partial accumulators per ring slot (even / odd terms): twice the
+        // independent FMA chains in the scatter
+        double acc[W], acc2[W], cen[W];
         #pragma unroll
-        for (int d = 0; d < W; ++d) acc[d] = cen[d] = 0.0;
+        for (int d = 0; d < W; ++d) acc[d] = acc2[d] = cen[d] = 0.0;
         const bool col_ok = gc < a.out_cols;
         double* const Wout = a.W;
         const int ldw = a.ldw;
@@ -323,7 +328,11 @@ __global__ void __launch_bounds__(TX + 32, band_minb<W>()) band_kernel(BandArgs 
                             if (f < T * W) {
                                 const int tt = f / W, d = f - tt * W;
                                 const int sl = (u - d + 2 * W) % W;
-                                acc[sl] = fma(q == 0 ? g.x : g.y, y[tt], acc[sl]);
+#if BAND_ACC2
+                                if (tt & 1) acc2[sl] = fma(q == 0 ? g.x : g.y, y[tt], acc2[sl]);
+                                else
+#endif
+                                    acc[sl] = fma(q == 0 ? g.x : g.y, y[tt], acc[sl]);
                             }
                         }
                     }
@@ -331,7 +340,12 @@ __global__ void __launch_bounds__(TX + 32, band_minb<W>()) band_kernel(BandArgs 
                     const int slot = (u + 1) % W;
                     // branch-free epilogue: predicated store, masked dot terms
                     const bool store = (unsigned)i < (unsigned)rows_here && col_ok;
+#if BAND_ACC2
+                    const double w = acc[slot] + acc2[slot];
+                    acc2[slot] = 0.0;
+#else
                     const double w = acc[slot];
+#endif
                     if (store) Wout[(size_t)(y0 + i) * ldw + gc] = w;
                     if constexpr (pcg_ep) {
                         // Q at (y0 + i, gc): centre of halo row i - goff = r - (W-1)/2
