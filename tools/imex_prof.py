@@ -1,3 +1,4 @@
+"""cProfile of a full IMEX run with the two-term preconditioner: python tools/imex_prof.py cfg4|cfg5 N steps"""
 import cProfile, pstats, sys, os, time
 sys.path.insert(0, os.getcwd())
 import torch
