@@ -1,4 +1,4 @@
-"""Back-to-back applications of the banded (SPIKE) preconditioner through sfb_pre_apply, for ncu and timing.
+"""Back-to-back applications of the banded (SPIKE) preconditioner through sfb_pre_apply, for ncu and timing."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
