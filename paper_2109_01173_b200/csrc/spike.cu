@@ -156,6 +156,12 @@ struct SpikeArgs {
 
 // Two-level triangular solve of the tile's lines in place (zero state at the
 // segment boundary).  FWD: L y = x with L's rows in bandS; otherwise L^T.
+// Every thread sweeps its 16-row sub-segment with a zero incoming state and
+// parks the sub-segment's outgoing boundary values (last / first B of the
+// local solution) in sst; after one barrier each thread chains the boundary
+// values of the sub-segments before it (at most 3 steps of B x B work)
+// itself and corrects its own rows: two barriers per direction, no idle
+// phase.
 template <int B, bool FWD>
 __device__ __forceinline__ void tile_solve(double (*tile)[S + 1], double (*sst)[B > 0 ? B : 1][S],
                                            const double* bandS, const double* H16s, const double* T16s, int len,
@@ -190,42 +196,40 @@ __device__ __forceinline__ void tile_solve(double (*tile)[S + 1], double (*sst)[
                 tile[kk][c] = v;
             }
         }
+        // outgoing boundary values of this sub-segment's local solution, in
+        // the order the transfer matrices expect (zero-padded when shorter than B)
+        #pragma unroll
+        for (int d = 0; d < B; ++d) {
+            const int r = FWD ? a1 - B + d : a0 + d;
+            const bool inside = FWD ? r >= a0 : r < a1;
+            sst[k][d][c] = inside ? tile[r][c] : 0.0;
+        }
     }
     __syncthreads();
     if (B == 0) return;
-    if (k == 0 && live) {
-        // chain over the 4 sub-segments of this line
+    const int kfirst = FWD ? 0 : (len - 1) / SS;  // first sub-segment in sweep order
+    if (live && a0 < a1 && k != kfirst) {
         double s[BB];
         #pragma unroll
         for (int d = 0; d < BB; ++d) s[d] = 0.0;
         #pragma unroll
-        for (int step = 0; step < NSUB; ++step) {
-            const int kk = FWD ? step : NSUB - 1 - step;
-            const int s0 = kk * SS, s1 = min(s0 + SS, len);
-            if (s0 >= len) continue;  // empty sub-segment at the end of the line
-            #pragma unroll
-            for (int d = 0; d < B; ++d) sst[kk][d][c] = s[d];
-            const double* T = T16s + kk * BB * BB;
-            double nx[BB];
-            #pragma unroll
-            for (int d = 0; d < B; ++d) {
-                const int r = FWD ? s1 - B + d : s0 + d;
-                const bool inside = FWD ? r >= s0 : r < s1;
-                double v = inside ? tile[r][c] : 0.0;
+        for (int step = 0; step < NSUB - 1; ++step) {
+            const int kk = FWD ? step : kfirst - step;  // sub-segments before mine, in sweep order
+            if (FWD ? kk < k : kk > k) {
+                const double* T = T16s + kk * BB * BB;
+                double nx[BB];
                 #pragma unroll
-                for (int e = 0; e < B; ++e) v = fma(T[d * B + e], s[e], v);
-                nx[d] = v;
+                for (int d = 0; d < B; ++d) {
+                    double v = sst[kk][d][c];
+                    #pragma unroll
+                    for (int e = 0; e < B; ++e) v = fma(T[d * B + e], s[e], v);
+                    nx[d] = v;
+                }
+                #pragma unroll
+                for (int d = 0; d < B; ++d) s[d] = nx[d];
             }
-            #pragma unroll
-            for (int d = 0; d < B; ++d) s[d] = nx[d];
         }
-    }
-    __syncthreads();
-    if (live && a0 < a1 && k != (FWD ? 0 : (len - 1) / SS)) {
         const double* H = H16s + k * SS * BB;
-        double s[BB];
-        #pragma unroll
-        for (int d = 0; d < B; ++d) s[d] = sst[k][d][c];
         for (int kk = a0; kk < a1; ++kk) {
             double v = tile[kk][c];
             #pragma unroll
