@@ -1,0 +1,65 @@
+"""Worker for the multi-rank test of the CUDA backend of the sharded MO-PCG.
+
+Every rank computes with the product's CudaBackend (C ABI kernels) on the one
+visible GPU; the collectives go through gloo on host copies (HostStagedComm),
+so the ranks only meet on the host and no kernel waits on another rank's.
+This checks the backend's multi-rank logic (halo-extended block operator,
+transposed GEMM shards, device dots) — not NVLink performance."""
+
+import os
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+import paper_2109_01173_b200 as pb
+from _cases import sine_source
+from paper_2109_01173_b200.distributed import Comm, CudaBackend, Layout, sharded_mo_pcg
+from test_host_logic import WAVE
+
+
+class HostStagedComm:
+    """Comm interface of distributed.sharded_mo_pcg over gloo: CUDA tensors
+    are staged through host memory for each collective."""
+
+    def __init__(self, layout):
+        self.L = layout
+        self.inner = Comm(layout, "cpu")
+
+    def allreduce(self, vals):
+        return self.inner.allreduce(vals)
+
+    def halo(self, X, b):
+        return self.inner.halo(X.cpu(), b).to(X.device)
+
+    def cols_to_rows(self, Xc):
+        return self.inner.cols_to_rows(Xc.cpu()).to(Xc.device)
+
+    def rowsT_to_colsT(self, XrT):
+        return self.inner.rowsT_to_colsT(XrT.cpu()).to(XrT.device)
+
+
+def problem(N):
+    x, y = pb.build_direction_sets(WAVE, 2, N, pb.BCKind.DIRICHLET)
+    op, rhs_of = pb.elliptic_operator(x, y, 1.0)
+    pre = pb.make_preconditioner("elliptic_xnormal", x, y, mode="inverse")
+    return op, pre, rhs_of(sine_source(N, N, 3))
+
+
+def worker(rank, world, port, N, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        op, pre, rhs = problem(N)
+        qy, qx = rhs.shape
+        lay = Layout(qy, qx, world, rank)
+        be = CudaBackend(op, pre, lay)
+        comm = HostStagedComm(lay)
+        rep = sharded_mo_pcg(be, comm, rhs[:, lay.c0:lay.c0 + lay.n], stop=pb.relative_residual(1e-12),
+                             max_iter=5000)
+        np.savez(os.path.join(out_dir, f"rank{rank}.npz"), U=rep.solution, iters=rep.iterations,
+                 hist=rep.residual_history)
+    finally:
+        dist.destroy_process_group()
