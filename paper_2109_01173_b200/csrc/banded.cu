@@ -400,11 +400,7 @@ template <int T, int W, int MODE>
 int launch_twm(const BandArgs& a, cudaStream_t stream) {
     using C = BandCfg<T, W>;
     constexpr int smem = C::SMEM;
-    static bool attr = false;
-    if (!attr) {
-        SFB_CUDA_TRY(cudaFuncSetAttribute(band_kernel<T, W, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        attr = true;
-    }
+    SFB_TRY(ensure_dynamic_smem(band_kernel<T, W, MODE>, smem));
     // tensor maps of the inputs (zero fill outside each source's extents)
     BandMaps maps;
     std::memset(&maps, 0, sizeof(maps));

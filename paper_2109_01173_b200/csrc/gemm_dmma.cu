@@ -317,12 +317,7 @@ int gemm_grid_for(int M, int N, int K, bool have_ws) {
 // C[M x N] = A[M x K] * Bt[N x K]^T, both row-major K-contiguous.
 int launch_dgemm_nt(const double* A, int lda, const double* Bt, int ldb, int M, int N, int K,
                     const GemmEpi& ep, cudaStream_t stream) {
-    static bool attr_set = false;
-    if (!attr_set) {
-        SFB_CUDA_TRY(cudaFuncSetAttribute(dgemm_nt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          SMEM_BYTES));
-        attr_set = true;
-    }
+    SFB_TRY(ensure_dynamic_smem(dgemm_nt_kernel, SMEM_BYTES));
     if (M <= 0 || N <= 0 || K <= 0) return arg_error("empty GEMM");
     CUtensorMap ma, mb;
     SFB_TRY(make_map(&ma, A, M, K, lda));

@@ -17,6 +17,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <string>
 #include <unordered_set>
 #include <utility>
 
@@ -59,6 +60,29 @@ inline bool first_launch(const void* fn) {
     static std::unordered_set<const void*> seen;
     std::lock_guard<std::mutex> lock(mu);
     return seen.insert(fn).second;
+}
+
+// Dynamic shared memory above 48 KB must be opted into per kernel and per
+// device; the (kernel, device, bytes) triples already set are remembered
+// (thread-safe, so several devices or threads in one process are fine).
+template <typename... KArgs>
+inline int ensure_dynamic_smem(void (*kernel)(KArgs...), size_t bytes) {
+    if (bytes <= 48 * 1024) return SFB_OK;
+    static std::mutex mu;
+    static std::unordered_set<std::string> done;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const std::string key = std::to_string(reinterpret_cast<uintptr_t>(kernel)) + "/" + std::to_string(dev) + "/" +
+                            std::to_string(bytes);
+    std::lock_guard<std::mutex> lock(mu);
+    if (done.count(key)) return SFB_OK;
+    const cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e != cudaSuccess) {
+        set_error(std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+        return SFB_ERR_CUDA;
+    }
+    done.insert(key);
+    return SFB_OK;
 }
 
 template <typename... KArgs>

@@ -505,9 +505,7 @@ int chain(const SpikeFactor& f, int nlines, double* sv, const PcgState* gate, cu
         const size_t csm = (size_t)P * (8 * B * B) * 8;
         const int cin = sm + csm <= cap ? 1 : 0;
         if (cin) sm += csm;
-        if (sm > 48 * 1024)
-            SFB_CUDA_TRY(cudaFuncSetAttribute(spike_chain_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              (int)sm));
+        SFB_TRY(ensure_dynamic_smem(spike_chain_kernel<B>, sm));
         return launch_kernel(spike_chain_kernel<B>, dim3((nlines + L - 1) / L), dim3(L), sm, s, nlines, P, f.coef,
                              sv, cin, gate);
     }
