@@ -47,7 +47,7 @@ def reduced(name, args):
     setup = time.perf_counter() - t0
     qy, qx = w.op.shape
     rhs = torch.from_numpy(w.rhs).cuda()
-    dt, reps = timed(lambda: pb.solve_reduced(w.op, rhs, cache), args.steps)
+    dt, reps = timed(lambda: pb.solve_reduced(w.op, rhs, cache), args.steps, warm=20)  # clocks ramp on short runs
     res = reps[-1].residual_history[0]
     flops = 4.0 * qy * qx * (qy + qx)
     line = {"workload": name, "metric": "reduced-solve DoF/s (fp64)", "value": qy * qx * args.steps / dt,
