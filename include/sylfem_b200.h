@@ -63,6 +63,7 @@ typedef struct sfb_op sfb_op;
 typedef struct sfb_map sfb_map;
 typedef struct sfb_pre sfb_pre;
 typedef struct sfb_pcg sfb_pcg;
+typedef struct sfb_csr sfb_csr;
 
 typedef struct {
     int iterations;       /* completed iterations                        */
@@ -192,6 +193,16 @@ int sfb_vec_dots(const double* A_dev, const double* B_dev, const double* C_dev,
 /* out4_host = { |A - B|_F (B may be NULL), max|A|, #non-finite(A), |A|_F }. */
 int sfb_diff_norm(const double* A_dev, int lda, const double* B_dev, int ldb,
                   int rows, int cols, double* out4_host, void* stream);
+
+/* ---- sparse vec-form matrices for the Kronecker cross-check path
+ *      (operators.py:141-155 to_kronecker; vector_pcg, solvers.py:456-517) */
+/* K (n x n) in CSR from host arrays: indptr n+1 (int64), indices nnz (int32,
+ * column indices), data nnz (fp64); copied once. */
+int sfb_csr_create(int n, long long nnz, const long long* indptr_host, const int* indices_host,
+                   const double* data_host, sfb_csr** out);
+/* y = K x (`w = K @ q`, solvers.py:486); deterministic sum order. */
+int sfb_csr_spmv(const sfb_csr* K, const double* x_dev, double* y_dev, void* stream);
+int sfb_csr_destroy(sfb_csr* K);
 
 #ifdef __cplusplus
 }

@@ -33,6 +33,7 @@ EXPORTS = [
     "sfb_pre_create", "sfb_pre_create_banded", "sfb_pre_apply", "sfb_pre_transform", "sfb_pre_destroy",
     "sfb_pcg_create", "sfb_pcg_solve", "sfb_pcg_pass_times", "sfb_pcg_destroy", "sfb_dgemm_nt", "sfb_diff_norm",
     "sfb_vec_update", "sfb_vec_xpby", "sfb_vec_dots",
+    "sfb_csr_create", "sfb_csr_spmv", "sfb_csr_destroy",
 ]
 
 
@@ -48,6 +49,9 @@ _I = C.c_int
 _DP = C.POINTER(C.c_double)
 
 _SIGS = {
+    "sfb_csr_create": (C.c_int, [C.c_int, C.c_longlong, C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_void_p)]),
+    "sfb_csr_spmv": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "sfb_csr_destroy": (C.c_int, [C.c_void_p]),
     "sfb_version": (_I, []),
     "sfb_last_error": (C.c_char_p, []),
     "sfb_init": (_I, [_I, C.POINTER(_I)]),

@@ -140,4 +140,8 @@ void free_spike_factor(SpikeFactor& f);
 int launch_spike_pre(const SpikeFactor& L, const SpikeFactor& R, const double* Rin, int ldr, double* Z, int ldz,
                      const SegDot* dot, double* svL, double* svR, const PcgState* gate, cudaStream_t s);
 
+// ------------------------------------------------------------ sparse -----
+int launch_csr_spmv(int n, const long long* indptr, const int* indices, const double* data, const double* x,
+                    double* y, cudaStream_t s);
+
 }  // namespace sfb

@@ -1193,3 +1193,53 @@ int sfb_diff_norm(const double* A, int lda, const double* B, int ldb, int rows, 
 }
 
 }  // extern "C"
+
+// --------------------------------------------------------------- sparse ---
+struct sfb_csr {
+    int n = 0;
+    long long nnz = 0;
+    long long* indptr = nullptr;
+    int* indices = nullptr;
+    double* data = nullptr;
+};
+
+int sfb_csr_create(int n, long long nnz, const long long* indptr, const int* indices, const double* data,
+                   sfb_csr** out) {
+    if (n <= 0 || nnz < 0 || !indptr || (nnz > 0 && (!indices || !data)) || !out)
+        return arg_error("CSR matrix needs n > 0 and its three arrays");
+    auto* K = new sfb_csr;
+    K->n = n;
+    K->nnz = nnz;
+    int rc = SFB_OK;
+    auto up = [&](void** dst, const void* src, size_t bytes) {
+        if (rc != SFB_OK) return;
+        if (cudaMalloc(dst, bytes ? bytes : 8) != cudaSuccess ||
+            (bytes && cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice) != cudaSuccess)) {
+            set_error("uploading the CSR matrix failed");
+            rc = SFB_ERR_NOMEM;
+        }
+    };
+    up(reinterpret_cast<void**>(&K->indptr), indptr, (size_t)(n + 1) * sizeof(long long));
+    up(reinterpret_cast<void**>(&K->indices), indices, (size_t)nnz * sizeof(int));
+    up(reinterpret_cast<void**>(&K->data), data, (size_t)nnz * sizeof(double));
+    if (rc != SFB_OK) {
+        sfb_csr_destroy(K);
+        return rc;
+    }
+    *out = K;
+    return SFB_OK;
+}
+
+int sfb_csr_spmv(const sfb_csr* K, const double* x, double* y, void* stream) {
+    if (!K || !x || !y) return arg_error("null CSR operand");
+    return launch_csr_spmv(K->n, K->indptr, K->indices, K->data, x, y, (cudaStream_t)stream);
+}
+
+int sfb_csr_destroy(sfb_csr* K) {
+    if (!K) return SFB_OK;
+    cudaFree(K->indptr);
+    cudaFree(K->indices);
+    cudaFree(K->data);
+    delete K;
+    return SFB_OK;
+}

@@ -206,6 +206,28 @@ def apply(op: SylvesterOperator, U):
     return op.apply(U)
 
 
+def _sparse(m):
+    if isinstance(m, Band):
+        return m.sparse.tocsr()
+    return sp.csr_matrix(np.asarray(m, dtype=float))
+
+
+def to_kronecker(op: SylvesterOperator) -> sp.csr_matrix:
+    """The vec-form sparse matrix with to_kronecker(op) @ vec(U) = vec(op(U))
+    (operators.py:141-155): sum_t H_t^T (x) G_t, assembly noise pruned.
+    Desk-size cross-check format; the guard is the reference's."""
+    qy, qx = op.shape
+    if qx * qy > KRONECKER_GUARD:
+        raise OperatorError(f"Kronecker assembly guarded at {KRONECKER_GUARD} unknowns, got {qx * qy}")
+    out = None
+    for G, H in op.terms:
+        blk = sp.kron(_sparse(H).T.tocsr(), _sparse(G), format="csr")
+        out = blk if out is None else out + blk
+    out.data[np.abs(out.data) < PRUNE_TOL] = 0.0
+    out.eliminate_zeros()
+    return out
+
+
 # --------------------------------------------------------- rhs builders ---
 class RhsBuilder:
     """out = G F H^T over the full node grid F: the weak right-hand side of

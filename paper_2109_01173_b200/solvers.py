@@ -19,19 +19,21 @@ the reference (solvers.py:36-453).  What changes is where the work runs:
 
 from __future__ import annotations
 
+import math
 import os
 import time
 from dataclasses import dataclass, field
 
 import numpy as np
 import scipy.linalg as sla
+import scipy.sparse as sp
 import scipy.linalg.lapack as lapack
 
 from . import _native as nat
 from .banded import Band
 from .exceptions import OperatorError, SolverError
 from .fem1d import DirectionSet
-from .operators import SylvesterOperator, is_unit_degenerate
+from .operators import SylvesterOperator, is_unit_degenerate, to_kronecker, unvec, vec
 
 RCOND_GUARD = 1e-14
 PENCIL_GUARD = 1e-12
@@ -164,6 +166,18 @@ def _cholesky_band(m, q: int):
     return b, band
 
 
+def _sparse_of(m):
+    return m.sparse.tocsr() if isinstance(m, Band) else sp.csr_matrix(np.asarray(m, dtype=float))
+
+
+class KroneckerCSR(sp.csr_matrix):
+    """csr_matrix of a Kronecker-structured preconditioner (as_kronecker)
+    that carries the Preconditioner it was built from."""
+
+    sfb_pre = None
+    sfb_shape = None
+
+
 class Preconditioner:
     """Single-term preconditioner U -> P_L U P_R (solvers.py:103-150).
 
@@ -192,6 +206,18 @@ class Preconditioner:
     @property
     def is_identity(self) -> bool:
         return self.left is None and self.right is None
+
+    def as_kronecker(self, shape) -> sp.csr_matrix:
+        """Sparse vec-form matrix P_R^T (x) P_L (solvers.py:145-150), for the
+        vector cross-check path.  The returned matrix remembers this
+        preconditioner, so vector_pcg applies its inverse with the device
+        kernels instead of a sparse factorisation."""
+        qy, qx = shape
+        left = sp.identity(qy, format="csr") if self.left is None else _sparse_of(self.left)
+        right = sp.identity(qx, format="csr") if self.right is None else _sparse_of(self.right)
+        K = KroneckerCSR(sp.kron(right.T.tocsr(), left, format="csr"))
+        K.sfb_pre, K.sfb_shape = self, (qy, qx)
+        return K
 
     # ---- device form -----------------------------------------------------
     def native(self, shape=None):
@@ -690,3 +716,173 @@ def mo_pcg(op: SylvesterOperator, rhs, precond: Preconditioner | None = None,
     return SolveReport(solution=U if on_dev else nat.to_host(U), method="mo-pcg", iterations=n,
                        residual_history=hist[: n + 1].copy(), stop_reason=_REASONS[res.stop_reason],
                        wall_time=time.perf_counter() - t0, diagnostics=diag)
+
+
+# ------------------------------------------- Kronecker cross-check path ----
+class _DeviceCSR:
+    """A sparse vec-form matrix uploaded once for the device SpMV."""
+
+    def __init__(self, K):
+        K = sp.csr_matrix(K)
+        K.sort_indices()
+        n = K.shape[0]
+        if K.shape != (n, n):
+            raise OperatorError(f"vector_pcg needs a square matrix, got {K.shape}")
+        self.n, self.nnz = n, int(K.nnz)
+        indptr = np.ascontiguousarray(K.indptr, dtype=np.int64)
+        indices = np.ascontiguousarray(K.indices, dtype=np.int32)
+        data = np.ascontiguousarray(K.data, dtype=float)
+        L = nat.lib()
+        out = nat.C.c_void_p()
+        nat.check(L.sfb_csr_create(n, self.nnz, nat.host_ptr(indptr), nat.host_ptr(indices), nat.host_ptr(data),
+                                   nat.C.byref(out)), "csr")
+        self.handle = nat.Handle(out.value, L.sfb_csr_destroy)
+
+    def matvec(self, x, y):
+        nat.check(nat.lib().sfb_csr_spmv(self.handle.p, nat.ptr(x), nat.ptr(y), nat.stream()), "spmv")
+
+
+def _vec_ops(n):
+    """Host-synchronous vector passes (the sharded MO-PCG blocks) on 1 x n rows."""
+    L = nat.lib()
+
+    def update(x, r, q, w, alpha):  # x += alpha q; r -= alpha w; -> |r|^2
+        out = np.zeros(1)
+        nat.check(L.sfb_vec_update(nat.ptr(x), nat.ptr(r), nat.ptr(q), nat.ptr(w), n, 1, n, float(alpha),
+                                   nat.dptr(out), nat.stream()), "update")
+        return float(out[0])
+
+    def dots(a, b, c=None, d=None):
+        out = np.zeros(2)
+        nat.check(L.sfb_vec_dots(nat.ptr(a), nat.ptr(b), nat.ptr(c) if c is not None else None,
+                                 nat.ptr(d) if d is not None else None, n, 1, n, nat.dptr(out), nat.stream()),
+                  "dots")
+        return float(out[0]), float(out[1])
+
+    def xpby(q, z, beta, first=False):  # q = z + beta q
+        nat.check(L.sfb_vec_xpby(nat.ptr(q), n, nat.ptr(z), n, 1, n, float(beta), int(first), nat.stream()), "xpby")
+
+    return update, dots, xpby
+
+
+def vector_pcg(K, b, P=None, stop: StoppingRule | None = None, x0=None, max_iter: int = DEFAULT_MAX_ITER,
+               record_iterates: bool = False) -> SolveReport:
+    """Classical vector PCG on the assembled sparse system (solvers.py:456-517),
+    the independent cross-check of mo_pcg, on the device: CSR SpMV kernel,
+    fused update / dot / direction passes.  ``P`` is None (identity) or a
+    Kronecker-structured preconditioner from ``Preconditioner.as_kronecker``,
+    whose inverse runs through the preconditioner's own device kernels
+    (the reference factors P with SuperLU)."""
+    if stop is None:
+        stop = relative_residual(DEFAULT_TOL)
+    t0 = time.perf_counter()
+    t = nat.torch()
+    Kd = _DeviceCSR(K)
+    n = Kd.n
+    bh = np.asarray(b, dtype=float).reshape(-1)
+    if bh.size != n:
+        raise OperatorError(f"right-hand side of length {bh.size} does not match the {n} x {n} matrix")
+    if P is None:
+        pre = None
+    else:
+        pre = getattr(P, "sfb_pre", None)
+        if pre is None:
+            raise SolverError("vector_pcg applies its preconditioner with the device kernels: pass "
+                              "P = Preconditioner.as_kronecker(shape) (or None)")
+        qy, qx = P.sfb_shape
+        if qy * qx != n:
+            raise OperatorError(f"preconditioner of grid {P.sfb_shape} does not match the {n} unknowns")
+
+    def solve_p(r, z):
+        if pre is None:
+            z.copy_(r)
+            return
+        U = r.view(qx, qy).t().contiguous()  # unvec (column stacking)
+        Zm = pre.apply_inverse(U)
+        z.copy_(Zm.t().contiguous().view(1, n))
+
+    update, dots, xpby = _vec_ops(n)
+    dev = lambda a: t.from_numpy(np.ascontiguousarray(a, dtype=float).reshape(1, n)).cuda()  # noqa: E731
+    B = dev(bh)
+    x = dev(np.zeros(n) if x0 is None else x0)
+    r = B.clone()
+    w = t.empty_like(B)
+    if x0 is not None:
+        Kd.matvec(x, w)
+        r.sub_(w)  # r = b - K x0 (solvers.py:476)
+    res0 = math.sqrt(dots(r, r)[0])
+    history = [res0]
+    iterates = [nat.to_host(x).reshape(-1)] if record_iterates else None
+
+    def report(iters, reason):
+        diag = {"iterates": iterates} if record_iterates else {}
+        return SolveReport(solution=nat.to_host(x).reshape(-1), method="vector-pcg", iterations=iters,
+                           residual_history=np.asarray(history), stop_reason=reason,
+                           wall_time=time.perf_counter() - t0, diagnostics=diag)
+
+    if res0 == 0.0:
+        return report(0, "tolerance")
+    z = t.empty_like(B)
+    q = t.empty_like(B)
+    solve_p(r, z)
+    xpby(q, z, 0.0, first=True)
+    rz = dots(r, z)[0]
+    for s in range(max_iter):
+        Kd.matvec(q, w)
+        qw, qq = dots(q, w, q, q)
+        if qw <= 0.0:
+            raise OperatorError("matrix is not positive definite along a direction")
+        alpha = rz / qw
+        res = math.sqrt(update(x, r, q, w, alpha))
+        history.append(res)
+        if record_iterates:
+            iterates.append(nat.to_host(x).reshape(-1))
+        if stop.kind == "residual" and res <= stop.value * res0:
+            return report(s + 1, "tolerance")
+        if stop.kind == "increment" and abs(alpha) * math.sqrt(qq) <= stop.value:
+            return report(s + 1, "increment")
+        solve_p(r, z)
+        rz_new = dots(r, z)[0]
+        beta = rz_new / rz
+        rz = rz_new
+        xpby(q, z, beta)
+    return report(max_iter, "max_iter")
+
+
+def solve_direct(op: SylvesterOperator, rhs) -> SolveReport:
+    """Solution of the Kronecker system to round-off (solvers.py:521-555).
+
+    The reference factors to_kronecker(op) with sparse LU.  Here the system is
+    solved on the device: the spectral reduced solve for two-term operators,
+    otherwise MO-PCG to a 1e-14 relative residual with the two-term spectral
+    preconditioner of the operator's first two terms; the reference's
+    Kronecker guard, relative-residual check (> 1e-9 -> SolverError) and report
+    fields are kept.  Symmetric positive definite operators only."""
+    t0 = time.perf_counter()
+    rhs = np.asarray(rhs, dtype=float)
+    K = to_kronecker(op)  # the reference's guard and the residual check below
+    if not (op.symmetric and op.positive_definite):
+        raise SolverError("the device direct solve needs an operator flagged symmetric positive definite")
+    if tuple(rhs.shape) != tuple(op.shape):
+        raise OperatorError(f"grid shape {rhs.shape} does not match operator {op.shape}")
+    try:
+        if len(op.terms) == 2:
+            U = solve_reduced(op, rhs).solution
+        else:
+            pre = two_term_preconditioner(op)
+            U = mo_pcg(op, rhs, precond=pre, stop=relative_residual(1e-14), max_iter=100000).solution
+    except (SolverError, np.linalg.LinAlgError):
+        U = mo_pcg(op, rhs, stop=relative_residual(1e-14), max_iter=100000).solution
+    b = vec(rhs)
+    Kd = _DeviceCSR(K)
+    t = nat.torch()
+    xd = t.from_numpy(np.ascontiguousarray(vec(U))).cuda()
+    yd = t.empty_like(xd)
+    Kd.matvec(xd, yd)
+    Kx = nat.to_host(yd)
+    res = float(np.linalg.norm(Kx - b) / max(np.linalg.norm(b), 1e-300))
+    if not np.all(np.isfinite(U)) or res > 1e-9:
+        raise SolverError(f"sparse direct solve failed (relative residual {res:.2e}; singular operator?)")
+    return SolveReport(solution=np.asarray(U), method="direct", iterations=0, residual_history=np.array([res]),
+                       stop_reason="direct", wall_time=time.perf_counter() - t0,
+                       diagnostics={"nnz": int(K.nnz), "n": int(K.shape[0])})

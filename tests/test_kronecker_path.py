@@ -1,0 +1,108 @@
+"""the Kronecker (vector) cross-check path.
+
+CPU: to_kronecker / as_kronecker assembly against the oracle's dense terms
+and factors (solvers.py:145-150, operators.py:141-155), the guard.
+GPU: vector_pcg (device CSR SpMV + fused vector passes) iterate by iterate
+against mo_pcg and the oracle, solve_direct against a dense direct solve."""
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+import oracle as orc
+import paper_2109_01173_b200 as pb
+from _cases import sine_source
+from conftest import relerr
+from test_host_logic import WAVE
+
+D = pb.BCKind.DIRICHLET
+
+
+def _dense_kron(terms):
+    return sum(np.kron(H.T, G) for G, H in terms)
+
+
+@pytest.mark.parametrize("k,N,lumped", [(1, 12, False), (2, 12, False), (4, 8, False), (1, 12, True)])
+def test_to_kronecker_matches_oracle_terms(k, N, lumped):
+    x, y = pb.build_direction_sets(WAVE, k, N, D, lumped=lumped)
+    op, _ = pb.elliptic_operator(x, y, 1.0, lumped=lumped)
+    ox, oy = orc.direction_sets(orc.wave_domain(), k, N, orc.DIRICHLET, lumped=lumped)
+    terms, _ = orc.elliptic_terms(ox, oy, 1.0, lumped=lumped)
+    K = pb.to_kronecker(op)
+    assert sp.issparse(K)
+    assert np.abs(K.toarray() - _dense_kron(terms)).max() <= 1e-12 * np.abs(_dense_kron(terms)).max()
+    U = np.random.default_rng(k).standard_normal(op.shape)
+    assert np.allclose(K @ pb.vec(U), pb.vec(orc.apply_terms(terms, U)), atol=1e-12)
+
+
+def test_as_kronecker_and_guard():
+    x, y = pb.build_direction_sets(WAVE, 2, 12, D)
+    pre = pb.make_preconditioner("elliptic_xnormal", x, y)
+    P = pre.as_kronecker((y.q, x.q))
+    ox, oy = orc.direction_sets(orc.wave_domain(), 2, 12, orc.DIRICHLET)
+    L, R, _, _ = orc.precond_factors("elliptic_xnormal", ox, oy)
+    assert np.allclose(P.toarray(), np.kron(R.T, L), atol=1e-13)
+    assert P.sfb_pre is pre and P.sfb_shape == (y.q, x.q)
+    xb, yb = pb.build_direction_sets(pb.SQUARE, 1, 460, D)
+    op, _ = pb.elliptic_operator(xb, yb, 1.0)
+    with pytest.raises(pb.OperatorError, match="guarded"):
+        pb.to_kronecker(op)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["inverse", "banded"])
+def test_vector_pcg_matches_mo_pcg_iterate_by_iterate(mode):
+    N = 16
+    x, y = pb.build_direction_sets(WAVE, 2, N, D)
+    op, rhs_of = pb.elliptic_operator(x, y, 1.0)
+    rhs = rhs_of(sine_source(N, N, 3))
+    pre = pb.make_preconditioner("elliptic_xnormal", x, y, mode=mode)
+    stop = pb.relative_residual(1e-10)
+    rm = pb.mo_pcg(op, rhs, precond=pre, stop=stop, record_iterates=True)
+    rv = pb.vector_pcg(pb.to_kronecker(op), pb.vec(rhs), P=pre.as_kronecker(op.shape), stop=stop,
+                       record_iterates=True)
+    assert rv.method == "vector-pcg" and abs(rv.iterations - rm.iterations) <= 1
+    for s in range(min(8, rm.iterations)):
+        assert relerr(pb.unvec(rv.diagnostics["iterates"][s + 1], op.shape),
+                      rm.diagnostics["iterates"][s + 1]) <= 1e-10
+    assert relerr(pb.unvec(rv.solution, op.shape), rm.solution) <= 1e-8
+    # the oracle's vector-free recurrences agree as well
+    ox, oy = orc.direction_sets(orc.wave_domain(), 2, N, orc.DIRICHLET)
+    terms, _ = orc.elliptic_terms(ox, oy, 1.0)
+    oref = orc.mo_pcg(terms, rhs, orc.LUPrecond(*orc.precond_factors("elliptic_xnormal", ox, oy)).inverse,
+                      ("residual", 1e-10))
+    assert abs(rv.iterations - oref["iterations"]) <= 1
+
+
+@pytest.mark.gpu
+def test_vector_pcg_identity_warm_start_increment_rule_and_errors():
+    x, y = pb.build_direction_sets(WAVE, 1, 12, D)
+    op, rhs_of = pb.elliptic_operator(x, y, 1.0)
+    K = pb.to_kronecker(op)
+    b = pb.vec(rhs_of(sine_source(12, 12, 3)))
+    x0 = 1e-3 * np.random.default_rng(2).standard_normal(b.size)
+    r = pb.vector_pcg(K, b, stop=pb.relative_residual(1e-12), x0=x0, max_iter=5000)
+    exact = np.linalg.solve(K.toarray(), b)
+    assert r.stop_reason == "tolerance" and relerr(r.solution, exact) <= 1e-9
+    r2 = pb.vector_pcg(K, b, stop=pb.increment_threshold(1e-10), max_iter=5000)
+    assert r2.stop_reason == "increment"
+    assert pb.vector_pcg(K, np.zeros_like(b)).iterations == 0
+    with pytest.raises(pb.SolverError, match="as_kronecker"):
+        pb.vector_pcg(K, b, P=sp.identity(b.size, format="csr"))
+    with pytest.raises(pb.OperatorError, match="not positive definite"):
+        pb.vector_pcg(-K, b, max_iter=10)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("k,N", [(1, 14), (2, 12)])
+def test_solve_direct_matches_dense_solve(k, N):
+    x, y = pb.build_direction_sets(WAVE, k, N, D)
+    op, rhs_of = pb.elliptic_operator(x, y, 1.0)
+    rhs = rhs_of(sine_source(N, N, 3))
+    rep = pb.solve_direct(op, rhs)
+    K = pb.to_kronecker(op).toarray()
+    exact = pb.unvec(np.linalg.solve(K, pb.vec(rhs)), op.shape)
+    assert rep.method == "direct" and rep.stop_reason == "direct" and rep.iterations == 0
+    assert rep.residual_history[0] <= 1e-12
+    assert relerr(rep.solution, exact) <= 1e-10
+    assert rep.diagnostics["n"] == op.shape[0] * op.shape[1]
