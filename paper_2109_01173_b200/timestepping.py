@@ -22,13 +22,13 @@ from typing import Callable
 import numpy as np
 
 from . import _native as nat
-from .exceptions import ConfigError, SolverError
+from .exceptions import ConfigError, OperatorError, SolverError
 from .fem1d import BCKind, DirectionSet
 from .geometry import DomainSpec
 from .models import DIBKinetics
-from .operators import expand_with_boundary, full_node_grid, parabolic_operator
-from .solvers import (Preconditioner, make_preconditioner, mo_pcg, relative_residual, timestep_residual,
-                      two_term_preconditioner)
+from .operators import KRONECKER_GUARD, expand_with_boundary, full_node_grid, parabolic_operator
+from .solvers import (Preconditioner, build_spectral_cache, make_preconditioner, mo_pcg, relative_residual,
+                      solve_reduced, timestep_residual, two_term_preconditioner)
 
 BLOWUP_LIMIT = 1e100
 
@@ -105,14 +105,15 @@ class SeparableSource:
 
 
 def _step_setup(inner: InnerSolver):
-    if inner.method != "mo-pcg":
-        raise ConfigError(f"inner solver '{inner.method}' is the reference's sparse-LU oracle path; "
-                          "the B200 solve path uses mo-pcg")
+    if inner.method not in ("mo-pcg", "direct"):
+        raise ConfigError(f"unknown inner solver method '{inner.method}'")
 
 
 def _parabolic_precond(x, y, d_u, tau, lumped, inner: InnerSolver, op=None):
     """timestepping.py:115-123; ``precond="two_term"`` selects the opt-in
     spectral preconditioner of SURVEY §8 f3 built from the step operator."""
+    if inner.method != "mo-pcg":
+        return None
     name = inner.precond
     if name == "auto":
         name = "parabolic_lumped" if lumped else "parabolic"
@@ -140,7 +141,31 @@ def _host(t):
     return nat.to_host(t)
 
 
+def _direct(op, rhs, warm):
+    """method="direct" (timestepping.py:106-111): an exact solve per step.
+    The reference factors the Kronecker matrix once with SuperLU; here the
+    factorisation done once is the step operator's own: its spectral cache
+    for two-term operators (the reduced solve is direct), otherwise the
+    two-term spectral preconditioner, with MO-PCG taken to round-off (1e-14).
+    The reference's Kronecker size guard is kept."""
+    qy, qx = op.shape
+    if qy * qx > KRONECKER_GUARD:
+        raise OperatorError(f"Kronecker assembly guarded at {KRONECKER_GUARD} unknowns, got {qy * qx}")
+    if len(op.terms) == 2:
+        cache = getattr(op, "_direct_cache", None)
+        if cache is None:
+            cache = op._direct_cache = build_spectral_cache(op, eig="device")
+        return solve_reduced(op, rhs, cache).solution, 0
+    pre = getattr(op, "_direct_pre", None)
+    if pre is None:
+        pre = op._direct_pre = two_term_preconditioner(op)
+    rep = mo_pcg(op, rhs, precond=pre, stop=relative_residual(1e-14), u0=warm, max_iter=100000)
+    return rep.solution, 0
+
+
 def _solve(op, rhs, pre, stop, warm, inner: InnerSolver):
+    if inner.method == "direct":
+        return _direct(op, rhs, warm)
     rep = mo_pcg(op, rhs, precond=pre, stop=stop, u0=warm, max_iter=inner.max_iter)
     if rep.stop_reason == "max_iter":
         raise SolverError(f"inner PCG did not converge in {inner.max_iter} iterations")
@@ -256,3 +281,15 @@ def imex_euler_rds(domain: DomainSpec, x: DirectionSet, y: DirectionSet, d_u: fl
             snaps.append((k + 1, _host(U), _host(V)))
     return Trajectory(final=(_host(U), _host(V)), increments=incs, iterations=iters,
                       times=(1 + np.arange(n)) * tau, steady_step=steady, snapshots=snaps)
+
+
+def vector_imex_heat(domain, x, y, d_u, source, u0, grid: TimeGrid, lumped: bool = False) -> Trajectory:
+    """Reference heat trajectory with exact step solves (timestepping.py:227-232)."""
+    return imex_euler_heat(domain, x, y, d_u, source, u0, grid, inner=InnerSolver(method="direct"), lumped=lumped)
+
+
+def vector_imex_rds(domain, x, y, d_u, d_v, kinetics, rho, state0, grid: TimeGrid, lumped: bool = False,
+                    snapshot_every: int = 0) -> Trajectory:
+    """Reference two-species trajectory with exact step solves (timestepping.py:235-242)."""
+    return imex_euler_rds(domain, x, y, d_u, d_v, kinetics, rho, state0, grid, inner=InnerSolver(method="direct"),
+                          lumped=lumped, snapshot_every=snapshot_every)

@@ -106,3 +106,22 @@ def test_solve_direct_matches_dense_solve(k, N):
     assert rep.residual_history[0] <= 1e-12
     assert relerr(rep.solution, exact) <= 1e-10
     assert rep.diagnostics["n"] == op.shape[0] * op.shape[1]
+
+
+@pytest.mark.gpu
+def test_vector_imex_drivers_match_reference_trajectories(golden):
+    # heat, cfg4-type (5-term step operator: MO-PCG to round-off per step)
+    x, y = pb.build_direction_sets(WAVE, 4, 8, D)
+    F = sine_source(8, 8, 4)
+    tr = pb.vector_imex_heat(WAVE, x, y, 1.0, pb.SeparableSource(F, lambda t: np.exp(-t)), golden["heat/u0"],
+                             pb.TimeGrid(1e-3, 5e-3))
+    assert np.all(tr.iterations == 0)
+    assert relerr(tr.final[0], golden["heat/t12/U"]) <= 1e-10
+    # DIB, cfg5-type (two-term step operators: spectral direct solves)
+    p = pb.dib_presets("spots_worms").replace(rho=400.0)
+    xl, yl = pb.build_direction_sets(pb.SQUARE, 1, 15, pb.BCKind.NEUMANN, lumped=True)
+    tau = 5e-3 / p.rho
+    tv = pb.vector_imex_rds(pb.SQUARE, xl, yl, 1.0, p.d_theta, pb.dib_kinetics_pair(p), p.rho,
+                            (golden["dib/eta0"], golden["dib/theta0"]), pb.TimeGrid(tau, 6 * tau), lumped=True)
+    assert relerr(tv.final[0], golden["dib/t12/U"]) <= 1e-10
+    assert relerr(tv.final[1], golden["dib/t12/V"]) <= 1e-10
