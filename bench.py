@@ -409,15 +409,22 @@ def run_native(args):
         n2 = qy * qx * 8
         band_gbs = 4 * n2 / (pt["operator_ms"] * 1e-3) / 1e9
         upd_gbs = 6 * n2 / (pt["update_ms"] * 1e-3) / 1e9
+        ptraffic = {}
+        try:
+            ptraffic = json.load(open(os.path.join(ROOT, "profiles", "ncu_passes_r01.json")))
+        except (OSError, ValueError):
+            pass
         hbm = {"bound": "hbm", "unit": "GB/s", "peak": hbm_peak, "peak_source": hbm_src,
                "banded_operator_pass": {
                    "kernel": f"band_kernel<{len(op)} terms, W={2 * op.half_bandwidth + 1}> (LD_PCG)",
                    "achieved": band_gbs, "frac": band_gbs / hbm_peak, "launch_ms": pt["operator_ms"],
                    "algorithmic_bytes": 4 * n2,
+                   "traffic": ptraffic.get("band_kernel<5,5,PCG>", {}).get("dram_bytes_per_launch"),
                    "note": "read Z, Q_prev; write Q, W (+ <W,Q>, |Q|^2); 2*T*W FMAs per element on the FP64 pipe"},
                "vector_update_pass": {
                    "kernel": "pcg_update_kernel", "achieved": upd_gbs, "frac": upd_gbs / hbm_peak,
                    "launch_ms": pt["update_ms"], "algorithmic_bytes": 6 * n2,
+                   "traffic": ptraffic.get("pcg_update_kernel", {}).get("dram_bytes_per_launch"),
                    "note": "read U, R, Q, W; write U, R (+ |R|^2, stop test)"},
                "preconditioner_ms": pt["preconditioner_ms"]}
 
