@@ -32,7 +32,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _native as nat
-from .exceptions import OperatorError, SolverError
+from .exceptions import ConfigError, OperatorError, SolverError
 from .solvers import SolveReport, StoppingRule, relative_residual
 
 
@@ -313,3 +313,167 @@ def sharded_mo_pcg(backend, comm: Comm, rhs_local, stop: StoppingRule | None = N
         rz = rz_new
         backend.xpby(Q, Z, beta)
     return report(max_iter, "max_iter")
+
+
+# =========================================================================
+# Species-parallel IMEX for the two-species reaction-diffusion system
+# =========================================================================
+#
+# Within one IMEX step the two species' implicit solves are independent: both
+# right-hand sides are built from the state at the start of the step
+# (timestepping.py:200-211), so species u and species v can be solved on
+# different GPUs at the same time.  Rank r owns species r.  Per step:
+#
+#   1. rhs_r = weak rhs of S_r + tau rho kin_r(U, V)     (local, both states held)
+#   2. S_r' = MO-PCG solve, warm started from S_r        (local)
+#   3. one all-gather of 6 status doubles per rank: the blow-up / convergence
+#      flags are then resolved in the reference's order (u rhs, u solve,
+#      v rhs, v solve; timestepping.py:202-209) on every rank, so all ranks
+#      raise the same exception at the same step;
+#   4. one all-gather of the new states (q^2 doubles per rank) so every rank
+#      holds (U', V') for the next step's kinetics.
+#
+# The result is bit-identical to the single-GPU driver (same kernels on the
+# same inputs in the same order; only the placement differs).
+
+
+class SpeciesComm:
+    """Collectives of the species-parallel step over torch.distributed
+    (NCCL with CUDA tensors, or gloo with CPU tensors)."""
+
+    def __init__(self, device, group=None):
+        import torch
+        import torch.distributed as dist
+        self.t, self.dist = torch, dist
+        self.device = device
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+
+    def gather_status(self, vals):
+        t = self.t.tensor(vals, dtype=self.t.float64, device=self.device)
+        out = [self.t.empty_like(t) for _ in range(self.world)]
+        self.dist.all_gather(out, t, group=self.group)
+        return [o.tolist() for o in out]
+
+    def exchange(self, own):
+        """all-gather of one state per rank -> the list of states by rank."""
+        own = own.contiguous()
+        out = [self.t.empty_like(own) for _ in range(self.world)]
+        self.dist.all_gather(out, own, group=self.group)
+        out[self.rank] = own
+        return out
+
+
+class CudaSpeciesStepper:
+    """One species' IMEX step on this rank's GPU through the C ABI: the fused
+    rhs+kinetics banded map, the device MO-PCG, the device norms — the same
+    calls the single-GPU driver (timestepping.imex_euler_rds) makes."""
+
+    def __init__(self, x, y, d, tau, rho, kinetics, inner, lumped, species):
+        from .models import DIBKinetics
+        from .operators import parabolic_operator
+        from .timestepping import _parabolic_precond
+        self.species = species
+        self.tau, self.rho = tau, rho
+        self.inner = inner
+        self.op, self.rhs_of = parabolic_operator(x, y, d, tau, lumped=lumped)
+        self.pre = _parabolic_precond(x, y, d, tau, lumped, inner, self.op)
+        self.stop = inner.stopping(tau)
+        self.kinetics = kinetics
+        self.device_kin = isinstance(kinetics, DIBKinetics)
+        self.kp = kinetics.params.device_params() if self.device_kin else None
+
+    def to_local(self, a):
+        return nat.to_device(a).clone()
+
+    def rhs(self, U, V):
+        if self.device_kin:
+            return self.rhs_of.dib(U, V, self.species, self.tau * self.rho, self.kp)
+        Uh, Vh = nat.to_host(U), nat.to_host(V)
+        rate = np.asarray(self.kinetics[self.species](Uh, Vh))
+        W = (Uh if self.species == 0 else Vh) + self.tau * self.rho * rate
+        fin = np.isfinite(W)
+        chk = (float(np.max(np.abs(W[fin]))) if fin.any() else 0.0, float((~fin).sum()))
+        return self.rhs_of(nat.to_device(W)), chk
+
+    def solve(self, rhs, warm):
+        """-> (new state, iterations, converged)."""
+        from .solvers import mo_pcg
+        from .timestepping import _direct
+        if self.inner.method == "direct":
+            sol, it = _direct(self.op, rhs, warm)
+            return sol, it, True
+        rep = mo_pcg(self.op, rhs, precond=self.pre, stop=self.stop, u0=warm, max_iter=self.inner.max_iter)
+        return rep.solution, rep.iterations, rep.stop_reason != "max_iter"
+
+    def norms(self, A, B):
+        from .timestepping import _norms
+        return [float(v) for v in _norms(A, B)]
+
+    def host(self, X):
+        return nat.to_host(X)
+
+
+def species_parallel_imex_rds(domain, x, y, d_u: float, d_v: float, kinetics, rho: float, state0, grid,
+                              inner=None, lumped: bool = False, snapshot_every: int = 0,
+                              steady_eps: float = 1e-8, comm: SpeciesComm | None = None,
+                              stepper_factory=None):
+    """imex_euler_rds (timestepping.py:162-220) with species r solved on rank r
+    of a 2-rank group.  Every rank returns the same Trajectory.
+
+    ``stepper_factory(x, y, d, tau, rho, kinetics, inner, lumped, species)``
+    builds the local compute (default: ``CudaSpeciesStepper``)."""
+    from .timestepping import BLOWUP_LIMIT, BlowUpError, InnerSolver, Trajectory, _step_setup
+    if d_u <= 0 or d_v <= 0 or rho <= 0:
+        raise ConfigError("d_u, d_v and rho must be positive")
+    from .fem1d import BCKind
+    if x.basis.bc is not BCKind.NEUMANN:
+        raise ConfigError("the reaction-diffusion stepper expects zero-flux BCs")
+    inner = inner or InnerSolver()
+    _step_setup(inner)
+    if comm is None:
+        import torch
+        comm = SpeciesComm("cuda" if torch.cuda.is_available() else "cpu")
+    if comm.world != 2:
+        raise ConfigError(f"species-parallel stepping needs a group of 2 ranks (one per species), got {comm.world}")
+    s = comm.rank
+    factory = stepper_factory or CudaSpeciesStepper
+    tau = grid.tau
+    st = factory(x, y, (d_u, d_v)[s], tau, rho, kinetics, inner, lumped, s)
+    S = [st.to_local(state0[0]), st.to_local(state0[1])]
+    n = grid.n_steps
+    incs = np.empty((n, 2))
+    iters = np.empty((n, 2), dtype=int)
+    snaps = []
+    steady = None
+    names = ("u", "v")
+    for k in range(n):
+        rhs, chk = st.rhs(S[0], S[1])
+        rhs_bad = float(chk[1] > 0 or chk[0] > BLOWUP_LIMIT)
+        conv, sol_bad, it, nrm = 1.0, 0.0, 0, [0.0, 0.0, 0.0, 0.0]
+        new = None
+        if not rhs_bad:
+            new, it, ok = st.solve(rhs, S[s])
+            conv = float(ok)
+            if ok:
+                nrm = st.norms(new, S[s])
+                sol_bad = float(nrm[2] > 0 or nrm[1] > BLOWUP_LIMIT)
+        stat = comm.gather_status([rhs_bad, conv, sol_bad, float(it), nrm[0], nrm[3]])
+        for r in range(2):  # the reference's order of checks
+            if stat[r][0]:
+                raise BlowUpError(k, names[r], (st.host(S[0]), st.host(S[1])))
+            if not stat[r][1]:
+                raise SolverError(f"inner PCG did not converge in {inner.max_iter} iterations")
+            if stat[r][2]:
+                raise BlowUpError(k, names[r], (st.host(S[0]), st.host(S[1])))
+        incs[k] = (stat[0][4], stat[1][4])
+        iters[k] = (int(stat[0][3]), int(stat[1][3]))
+        S = comm.exchange(new)
+        if steady is None and np.all(incs[k] <= steady_eps * max(stat[0][5], 1e-300)):
+            steady = k
+        if snapshot_every and ((k + 1) % snapshot_every == 0 or k == n - 1):
+            snaps.append((k + 1, st.host(S[0]), st.host(S[1])))
+    return Trajectory(final=(st.host(S[0]), st.host(S[1])), increments=incs, iterations=iters,
+                      times=(1 + np.arange(n)) * tau, steady_step=steady, snapshots=snaps,
+                      diagnostics={"species_rank": s, "world": comm.world})
