@@ -121,7 +121,9 @@ int sfb_map_apply_heat(const sfb_map* m, const double* U_dev, int ldu,
                        double* check2_host, void* stream);
 /* IMEX DIB rhs (timestepping.py:201-207, models.py:74-82): species 0 uses
  * W = U + tau_rho f(U,V), species 1 W = V + tau_rho g(U,V); then
- * out = G W H^T.  params = {alpha, gamma_k, A1, A2, B, C, D, k2, k3}. */
+ * out = G W H^T.  params = {alpha, gamma_k, A1, A2, B, C, D, k2, k3}.
+ * The map may read a halo-extended column block (in_cols > out_cols, same
+ * rows): the column-sharded IMEX driver's local rhs. */
 int sfb_map_apply_dib(const sfb_map* m, const double* U_dev, const double* V_dev,
                       int ld, int species, double tau_rho, const double* params_host,
                       double* out_dev, int ldo, double* check2_host, void* stream);

@@ -720,7 +720,9 @@ int sfb_map_apply_heat(const sfb_map* m, const double* U, int ldu, int row_shift
 int sfb_map_apply_dib(const sfb_map* m, const double* U, const double* V, int ld, int species, double tau_rho,
                       const double* params, double* out, int ldo, double* check2, void* stream) {
     if (!m) return arg_error("null map");
-    if (m->in_rows != m->out_rows || m->in_cols != m->out_cols)
+    // zero-flux: the input grid is the output grid, or a column block of it
+    // extended by a halo (in_cols > out_cols, the sharded IMEX driver)
+    if (m->in_rows != m->out_rows || m->in_cols < m->out_cols)
         return arg_error("DIB rhs expects a zero-flux (square) map");
     BandArgs a = map_args(m, out, ldo);
     a.ld_mode = LD_DIB;

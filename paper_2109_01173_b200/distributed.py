@@ -477,3 +477,153 @@ def species_parallel_imex_rds(domain, x, y, d_u: float, d_v: float, kinetics, rh
     return Trajectory(final=(st.host(S[0]), st.host(S[1])), increments=incs, iterations=iters,
                       times=(1 + np.arange(n)) * tau, steady_step=steady, snapshots=snaps,
                       diagnostics={"species_rank": s, "world": comm.world})
+
+
+# =========================================================================
+# Column-sharded IMEX for the two-species reaction-diffusion system (cfg5)
+# =========================================================================
+#
+# Both species' states are column-sharded like the MO-PCG iterates.  Per step
+# (timestepping.py:200-218):
+#
+#   1. b_rhs-column halos of U and V (zero for the lumped P1 rhs, whose right
+#      factor M0 is diagonal);
+#   2. per species: rhs = G_full (S + tau rho kin(U, V)) H_full^T on the local
+#      block (the fused DIB map kernel reading the halo-extended block), the
+#      blow-up check reduced over ranks (max, count), then the column-sharded
+#      MO-PCG warm started from the local state, then the increment / blow-up
+#      norms reduced over ranks;
+#   3. steady-state test and snapshots on the reduced norms.
+#
+# Every rank takes the same decisions from the same reduced scalars, so all
+# ranks raise the same exception at the same step.
+
+
+def _allreduce_max(comm, vals):
+    """max over ranks through the sum-allreduce of Comm: gather by slot."""
+    L = comm.L
+    slots = [0.0] * (len(vals) * L.world)
+    slots[L.rank * len(vals):(L.rank + 1) * len(vals)] = list(vals)
+    tot = comm.allreduce(slots)
+    return [max(tot[r * len(vals) + i] for r in range(L.world)) for i in range(len(vals))]
+
+
+class CudaShardedDibStepper:
+    """Local compute of the column-sharded DIB step: per-species CudaBackend
+    (block operator, inverse-form DMMA preconditioner, vector passes) and the
+    block DIB rhs map, all through the C ABI."""
+
+    def __init__(self, x, y, d_u, d_v, tau, rho, kinetics, inner, lumped, layout: Layout):
+        from .models import DIBKinetics
+        from .operators import parabolic_operator
+        from .timestepping import _parabolic_precond
+        if not isinstance(kinetics, DIBKinetics):
+            raise ConfigError("the column-sharded DIB driver evaluates the kinetics on the device: "
+                              "pass a DIBKinetics pair")
+        if inner.method != "mo-pcg" or inner.precond == "two_term":
+            raise ConfigError("the column-sharded DIB driver runs MO-PCG with the reference preconditioner")
+        self.L = layout
+        self.tau_rho = tau * rho
+        self.kp = np.ascontiguousarray(kinetics.params.device_params(), dtype=float)
+        self.backends = []
+        for d in (d_u, d_v):
+            op, rhs_of = parabolic_operator(x, y, d, tau, lumped=lumped)
+            pre = _parabolic_precond(x, y, d, tau, lumped, inner, op)
+            self.backends.append(CudaBackend(op, pre, layout))
+        w, goff, g, hoff, h = rhs_of.layout()
+        self.b = max(0, -hoff, hoff + w - 1)
+        n = layout.n
+        hl = np.ascontiguousarray(h[layout.c0:layout.c0 + n])
+        out = nat.C.c_void_p()
+        nat.check(nat.lib().sfb_map_create(layout.qy, n, layout.qy, n + 2 * self.b, w, goff,
+                                           nat.host_ptr(np.ascontiguousarray(g)), w, hoff + self.b,
+                                           nat.host_ptr(hl), nat.C.byref(out)), "block rhs map")
+        self._map = nat.Handle(out.value, nat.lib().sfb_map_destroy)
+
+    def to_local(self, a):
+        L = self.L
+        if nat.is_device(a):
+            return self.backends[0].from_host(a[:, L.c0:L.c0 + L.n])
+        return self.backends[0].from_host(np.asarray(a, dtype=float)[:, L.c0:L.c0 + L.n])
+
+    def rhs(self, species, extU, extV):
+        be = self.backends[0]
+        U, V = extU.contiguous(), extV.contiguous()
+        out = be.zeros(self.L.qy, self.L.n)
+        chk = np.zeros(2)
+        nat.check(nat.lib().sfb_map_apply_dib(self._map.p, U.data_ptr(), V.data_ptr(), U.stride(0), int(species),
+                                              self.tau_rho, nat.dptr(self.kp), out.data_ptr(), out.stride(0),
+                                              nat.dptr(chk), nat.stream()), "dib rhs")
+        return out, chk
+
+    def norms(self, A, B):
+        """local {sum (A-B)^2, max|A|, #non-finite(A), sum A^2}."""
+        out = np.zeros(4)
+        nat.check(nat.lib().sfb_diff_norm(A.data_ptr(), A.stride(0), B.data_ptr(), B.stride(0), A.shape[0],
+                                          A.shape[1], nat.dptr(out), nat.stream()), "norm")
+        return [out[0] ** 2, out[1], out[2], out[3] ** 2]
+
+    def host(self, X):
+        return nat.to_host(X)
+
+
+def sharded_imex_rds(domain, x, y, d_u: float, d_v: float, kinetics, rho: float, state0, grid, inner=None,
+                     lumped: bool = False, snapshot_every: int = 0, steady_eps: float = 1e-8,
+                     comm: Comm | None = None, stepper=None):
+    """imex_euler_rds (timestepping.py:162-220) with both species' states
+    column-sharded over the ranks of ``comm`` (SURVEY §8 e).  ``state0`` is
+    the full pair (each rank keeps its columns).  Returns this rank's columns
+    in ``final`` / ``snapshots`` / ``BlowUpError.state``; increments,
+    iteration counts and the steady step are global and equal on all ranks."""
+    from .fem1d import BCKind
+    from .timestepping import BLOWUP_LIMIT, BlowUpError, InnerSolver, Trajectory, _step_setup
+    if d_u <= 0 or d_v <= 0 or rho <= 0:
+        raise ConfigError("d_u, d_v and rho must be positive")
+    if x.basis.bc is not BCKind.NEUMANN:
+        raise ConfigError("the reaction-diffusion stepper expects zero-flux BCs")
+    inner = inner or InnerSolver()
+    _step_setup(inner)
+    tau = grid.tau
+    if comm is None:
+        import torch.distributed as dist
+        comm = Comm(Layout(y.q, x.q, dist.get_world_size(), dist.get_rank()), "cuda")
+    L = comm.L
+    st = stepper or CudaShardedDibStepper(x, y, d_u, d_v, tau, rho, kinetics, inner, lumped, L)
+    stop = inner.stopping(tau)
+    S = [st.to_local(state0[0]), st.to_local(state0[1])]
+    n = grid.n_steps
+    incs = np.empty((n, 2))
+    iters = np.empty((n, 2), dtype=int)
+    snaps = []
+    steady = None
+    names = ("u", "v")
+    for k in range(n):
+        ext = (comm.halo(S[0], st.b), comm.halo(S[1], st.b))
+        last = lambda: (st.host(S[0]), st.host(S[1]))  # noqa: E731
+        new, sq = [None, None], [None, None]
+        for sp in (0, 1):
+            rhs, chk = st.rhs(sp, *ext)
+            mx, = _allreduce_max(comm, [chk[0]])
+            cnt, = comm.allreduce([chk[1]])
+            if cnt > 0 or mx > BLOWUP_LIMIT:
+                raise BlowUpError(k, names[sp], last())
+            rep = sharded_mo_pcg(st.backends[sp], comm, rhs, stop=stop, u0_local=S[sp], max_iter=inner.max_iter,
+                                 keep_on_device=True)
+            if rep.stop_reason == "max_iter":
+                raise SolverError(f"inner PCG did not converge in {inner.max_iter} iterations")
+            loc = st.norms(rep.solution, S[sp])
+            dd, bad, nn = comm.allreduce([loc[0], loc[2], loc[3]])
+            mx, = _allreduce_max(comm, [loc[1]])
+            if bad > 0 or mx > BLOWUP_LIMIT:
+                raise BlowUpError(k, names[sp], last())
+            new[sp], sq[sp] = rep.solution, nn
+            incs[k, sp] = math.sqrt(dd)
+            iters[k, sp] = rep.iterations
+        S = new
+        if steady is None and np.all(incs[k] <= steady_eps * max(math.sqrt(sq[0]), 1e-300)):
+            steady = k
+        if snapshot_every and ((k + 1) % snapshot_every == 0 or k == n - 1):
+            snaps.append((k + 1, st.host(S[0]), st.host(S[1])))
+    return Trajectory(final=(st.host(S[0]), st.host(S[1])), increments=incs, iterations=iters,
+                      times=(1 + np.arange(n)) * tau, steady_step=steady, snapshots=snaps,
+                      diagnostics={"world": L.world, "columns": (L.c0, L.c0 + L.n)})

@@ -35,3 +35,25 @@ def test_species_parallel_cuda_matches_single_gpu_driver():
         assert np.array_equal(r["incs"], ref.increments)
         assert list(r["snaps"]) == [s[0] for s in ref.snapshots]
     assert relerr(parts[0]["V"], ref.final[1]) == 0.0
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_rds_cuda_matches_single_gpu_driver(world):
+    from _sharded_rds_worker import worker as sharded_worker
+    N, steps = 15, 4
+    d = tempfile.mkdtemp()
+    mp.spawn(sharded_worker, args=(world, free_port(), "cuda", d, N, steps), nprocs=world, join=True)
+    parts = [dict(np.load(os.path.join(d, f"rank{r}.npz"))) for r in range(world)]
+    U = np.concatenate([p["U"] for p in parts], axis=1)
+    V = np.concatenate([p["V"] for p in parts], axis=1)
+    p, x, y, state0, tau = case(N)
+    ref = pb.imex_euler_rds(pb.SQUARE, x, y, 1.0, p.d_theta, pb.dib_kinetics_pair(p), p.rho, state0,
+                            pb.TimeGrid(tau, steps * tau),
+                            inner=pb.InnerSolver(rule="residual", tol=1e-12, max_iter=2000), lumped=True,
+                            snapshot_every=2)
+    for r in parts:
+        assert np.all(np.abs(r["iters"] - ref.iterations) <= 1)
+        assert np.allclose(r["incs"], ref.increments, rtol=1e-8)
+        assert list(r["snaps"]) == [s[0] for s in ref.snapshots]
+    assert relerr(U, ref.final[0]) <= 1e-10
+    assert relerr(V, ref.final[1]) <= 1e-10
