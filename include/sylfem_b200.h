@@ -59,6 +59,15 @@ enum {
     SFB_PRE_BANDED = 4         /* Z = PL^-1 R PR^-1 by banded Cholesky sweeps */
 };
 
+/* IMEX run outcomes (timestepping.py:62-69, 86-112) */
+enum {
+    SFB_IMEX_OK = 0,
+    SFB_IMEX_BLOWUP = 1,        /* non-finite or > 1e100 state   -> BlowUpError(step, species, state) */
+    SFB_IMEX_NOT_CONVERGED = 2, /* inner MO-PCG hit max_iter     -> SolverError "did not converge"   */
+    SFB_IMEX_INDEFINITE = 3,    /* inner MO-PCG: <L(Q),Q> <= 0   -> OperatorError                    */
+    SFB_IMEX_NONFINITE = 4      /* inner MO-PCG residual non-finite -> SolverError                   */
+};
+
 typedef struct sfb_op sfb_op;
 typedef struct sfb_map sfb_map;
 typedef struct sfb_pre sfb_pre;
@@ -74,6 +83,16 @@ typedef struct {
     double bad_value;     /* <L(Q),Q> at INDEFINITE                      */
     double device_ms;     /* device time of the iteration loop           */
 } sfb_pcg_result;
+
+typedef struct {
+    int steps_done;       /* completed time steps                        */
+    int fail_step;        /* step of the failure (-1: none)              */
+    int fail_kind;        /* SFB_IMEX_*                                  */
+    int fail_species;     /* 0 = u (eta), 1 = v (theta); -1: none        */
+    int steady_step;      /* first steady step of the run (-1: none)     */
+    int pcg_bad_iter;     /* inner MO-PCG iteration of an INDEFINITE / NONFINITE failure */
+    double pcg_bad_value; /* <L(Q),Q> of an INDEFINITE failure           */
+} sfb_imex_result;
 
 /* ---- library ---------------------------------------------------------- */
 int sfb_version(void);
@@ -171,6 +190,37 @@ int sfb_pcg_solve(sfb_pcg* s, const double* rhs_dev, int ldr,
  * Measurement only: no reference counterpart. */
 int sfb_pcg_pass_times(sfb_pcg* s, int reps, double* ms);
 int sfb_pcg_destroy(sfb_pcg* s);
+/* grid shape (q_y, q_x) the solver was created for */
+int sfb_pcg_shape(const sfb_pcg* s, int* qy, int* qx);
+
+/* ---- IMEX-Euler step loops (timestepping.py:126-159, 162-220) --------- */
+/* Heat: per step k, W = expand(U) + c_host[k] F (F may be NULL: no source;
+ * row/col shifts place the interior state in the full node grid as in
+ * sfb_map_apply_heat), rhs = G W H^T, blow-up check of W, MO-PCG on
+ * `solver` warm started from U (rule/value/max_iter per step), increment
+ * |U_new - U| and finiteness of U_new; then U = U_new.  c_host[k] = tau *
+ * s(k tau) for a separable source s(t) F.  U_dev (ldu) holds u0 on entry and
+ * the final state on exit — or, when res->fail_kind != SFB_IMEX_OK, the
+ * state at the start of the failing step.  iterations_host / increments_host
+ * receive n_steps entries (the completed ones are valid). */
+int sfb_imex_heat_run(sfb_pcg* solver, const sfb_map* rhs_map, int row_shift, int col_shift,
+                      const double* F_dev, int ldf, const double* c_host, int n_steps,
+                      int rule, double value, int max_iter, double* U_dev, int ldu,
+                      int* iterations_host, double* increments_host, sfb_imex_result* res,
+                      void* stream);
+/* Two-species reaction-diffusion (DIB kinetics, params as in
+ * sfb_map_apply_dib): per step both rhs from the state at the start of the
+ * step, species u solved on solver_u then species v on solver_v (checks in
+ * the reference's order), increments and the steady test |dU|,|dV| <=
+ * steady_eps |U_new|.  U_dev, V_dev (ld) in: state0, out: final state (or
+ * the state at the start of the failing step).  iterations_host and
+ * increments_host are n_steps x 2 (row-major: u, v). */
+int sfb_imex_rds_run(sfb_pcg* solver_u, sfb_pcg* solver_v, const sfb_map* rhs_map,
+                     const double* params_host, double tau_rho, int n_steps,
+                     int rule, double value, int max_iter, double steady_eps,
+                     double* U_dev, double* V_dev, int ld,
+                     int* iterations_host, double* increments_host, sfb_imex_result* res,
+                     void* stream);
 
 /* ---- FP64 tensor-core GEMM (the kernel behind every spectral / inverse
  *      application): C = A Bt^T, A (M x K) and Bt (N x K) row-major with even

@@ -34,13 +34,21 @@ EXPORTS = [
     "sfb_pcg_create", "sfb_pcg_solve", "sfb_pcg_pass_times", "sfb_pcg_destroy", "sfb_dgemm_nt", "sfb_diff_norm",
     "sfb_vec_update", "sfb_vec_xpby", "sfb_vec_dots",
     "sfb_csr_create", "sfb_csr_spmv", "sfb_csr_destroy",
+    "sfb_pcg_shape", "sfb_imex_heat_run", "sfb_imex_rds_run",
 ]
+IMEX_OK, IMEX_BLOWUP, IMEX_NOT_CONVERGED, IMEX_INDEFINITE, IMEX_NONFINITE = range(5)
 
 
 class PcgResult(C.Structure):
     _fields_ = [("iterations", C.c_int), ("stop_reason", C.c_int), ("bad_iter", C.c_int),
                 ("chunks", C.c_int), ("res0", C.c_double), ("bad_value", C.c_double),
                 ("device_ms", C.c_double)]
+
+
+class ImexResult(C.Structure):
+    _fields_ = [("steps_done", C.c_int), ("fail_step", C.c_int), ("fail_kind", C.c_int),
+                ("fail_species", C.c_int), ("steady_step", C.c_int), ("pcg_bad_iter", C.c_int),
+                ("pcg_bad_value", C.c_double)]
 
 
 _P = C.c_void_p
@@ -81,6 +89,11 @@ _SIGS = {
     "sfb_vec_xpby": (_I, [_P, _I, _P, _I, _I, _I, _D, _I, _P]),
     "sfb_vec_dots": (_I, [_P, _P, _P, _P, _I, _I, _I, _DP, _P]),
     "sfb_diff_norm": (_I, [_P, _I, _P, _I, _I, _I, _DP, _P]),
+    "sfb_pcg_shape": (_I, [_P, C.POINTER(_I), C.POINTER(_I)]),
+    "sfb_imex_heat_run": (_I, [_P, _P, _I, _I, _P, _I, _DP, _I, _I, _D, _I, _P, _I, C.POINTER(_I), _DP,
+                               C.POINTER(ImexResult), _P]),
+    "sfb_imex_rds_run": (_I, [_P, _P, _P, _DP, _D, _I, _I, _D, _I, _D, _P, _P, _I, C.POINTER(_I), _DP,
+                              C.POINTER(ImexResult), _P]),
 }
 
 _lib = None

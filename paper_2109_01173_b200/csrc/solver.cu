@@ -1051,6 +1051,13 @@ int sfb_pcg_solve(sfb_pcg* s, const double* rhs, int ldr, const double* u0, int 
 // ms[1] vector update pass (U, R, |R|), ms[2] preconditioner.  A scratch
 // state keeps the gates open; the solver's buffers are clobbered (the next
 // solve re-initialises them).
+int sfb_pcg_shape(const sfb_pcg* s, int* qy, int* qx) {
+    if (!s || !qy || !qx) return arg_error("null solver or output");
+    *qy = s->qy;
+    *qx = s->qx;
+    return SFB_OK;
+}
+
 int sfb_pcg_pass_times(sfb_pcg* s, int reps, double* ms) {
     if (!s || !ms || reps <= 0) return arg_error("pass timing needs a solver, reps > 0 and 3 outputs");
     if (s->op->dense) {

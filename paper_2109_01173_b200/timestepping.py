@@ -27,8 +27,8 @@ from .fem1d import BCKind, DirectionSet
 from .geometry import DomainSpec
 from .models import DIBKinetics
 from .operators import KRONECKER_GUARD, expand_with_boundary, full_node_grid, parabolic_operator
-from .solvers import (Preconditioner, build_spectral_cache, make_preconditioner, mo_pcg, relative_residual,
-                      solve_reduced, timestep_residual, two_term_preconditioner)
+from .solvers import (Preconditioner, _solver_for, build_spectral_cache, make_preconditioner, mo_pcg,
+                      relative_residual, solve_reduced, timestep_residual, two_term_preconditioner)
 
 BLOWUP_LIMIT = 1e100
 
@@ -172,6 +172,45 @@ def _solve(op, rhs, pre, stop, warm, inner: InnerSolver):
     return rep.solution, rep.iterations
 
 
+# ------------------------------------------------- native step loops ----
+def _rule(stop):
+    return nat.RULE_RESIDUAL if stop.kind == "residual" else nat.RULE_INCREMENT
+
+
+def _raise_imex(res, inner: InnerSolver, state):
+    """Map a native run's failure onto the reference's exceptions."""
+    kind = res.fail_kind
+    if kind == nat.IMEX_OK:
+        return
+    species = "uv"[max(res.fail_species, 0)]
+    if kind == nat.IMEX_BLOWUP:
+        raise BlowUpError(res.fail_step, species, state())
+    if kind == nat.IMEX_NOT_CONVERGED:
+        raise SolverError(f"inner PCG did not converge in {inner.max_iter} iterations")
+    if kind == nat.IMEX_INDEFINITE:
+        raise OperatorError("operator is not positive definite along a search direction "
+                            f"(<L(Q), Q> = {res.pcg_bad_value:.3e} at iteration {res.pcg_bad_iter})")
+    raise SolverError(f"mo_pcg residual became non-finite at iteration {res.pcg_bad_iter}")
+
+
+def _heat_native(op, rhs_of, pre, stop, inner: InnerSolver, F, time_factor, U, n: int, tau: float):
+    """The whole heat loop in one native call (sfb_imex_heat_run)."""
+    solver = _solver_for(op, pre if pre is not None else Preconditioner())
+    c = np.ascontiguousarray([tau * float(time_factor(k * tau)) for k in range(n)], dtype=float)
+    iters = np.zeros(n, dtype=np.int32)
+    incs = np.zeros(n)
+    res = nat.ImexResult()
+    rs = 1 if rhs_of.y.basis.bc is BCKind.DIRICHLET else 0
+    cs = 1 if rhs_of.x.basis.bc is BCKind.DIRICHLET else 0
+    nat.check(nat.lib().sfb_imex_heat_run(
+        solver.handle.p, rhs_of.native(), rs, cs, nat.ptr(F), F.shape[1], nat.dptr(c), n, _rule(stop),
+        float(stop.value), int(inner.max_iter), nat.ptr(U), U.shape[1],
+        iters.ctypes.data_as(nat.C.POINTER(nat.C.c_int)), nat.dptr(incs), nat.C.byref(res), nat.stream()),
+        "imex heat")
+    _raise_imex(res, inner, lambda: _host(U))
+    return iters.astype(int), incs
+
+
 def imex_euler_heat(domain: DomainSpec, x: DirectionSet, y: DirectionSet, d_u: float, source: Callable,
                     u0, grid: TimeGrid, inner: InnerSolver | None = None, lumped: bool = False) -> Trajectory:
     """u_t - d_u Lap u = source(u, x, y, t) (timestepping.py:126-159)."""
@@ -191,6 +230,10 @@ def imex_euler_heat(domain: DomainSpec, x: DirectionSet, y: DirectionSet, d_u: f
         X, Y = full_node_grid(domain, x, y)
     U = nat.to_device(u0).clone()
     n = grid.n_steps
+    if F is not None and inner.method == "mo-pcg":
+        iters, incs = _heat_native(op, rhs_of, pre, stop, inner, F, source.time_factor, U, n, tau)
+        return Trajectory(final=(_host(U),), increments=incs, iterations=iters,
+                          times=(1 + np.arange(n)) * tau, diagnostics={"loop": "native"})
     incs = np.empty(n)
     iters = np.empty(n, dtype=int)
     for k in range(n):
@@ -243,6 +286,35 @@ def imex_euler_rds(domain: DomainSpec, x: DirectionSet, y: DirectionSet, d_u: fl
     snaps = []
     steady = None
     host_rates = None
+    if device_kin and inner.method == "mo-pcg":
+        # the whole loop natively (sfb_imex_rds_run), in segments ending at the snapshot steps
+        su = _solver_for(op_u, pre_u)
+        sv = _solver_for(op_v, pre_v)
+        kpar = np.ascontiguousarray(kp, dtype=float)
+        k0 = 0
+        while k0 < n:
+            m = min(snapshot_every, n - k0) if snapshot_every else n - k0
+            it = np.zeros((m, 2), dtype=np.int32)
+            inc = np.zeros((m, 2))
+            res = nat.ImexResult()
+            nat.check(nat.lib().sfb_imex_rds_run(
+                su.handle.p, sv.handle.p, rhs_of.native(), nat.dptr(kpar), float(tau * rho), m, _rule(stop),
+                float(stop.value), int(inner.max_iter), float(steady_eps), nat.ptr(U), nat.ptr(V), U.shape[1],
+                it.ctypes.data_as(nat.C.POINTER(nat.C.c_int)), nat.dptr(inc), nat.C.byref(res), nat.stream()),
+                "imex rds")
+            if res.fail_kind != nat.IMEX_OK:
+                res.fail_step += k0
+            _raise_imex(res, inner, lambda: (_host(U), _host(V)))
+            iters[k0:k0 + m] = it
+            incs[k0:k0 + m] = inc
+            if steady is None and res.steady_step >= 0:
+                steady = k0 + res.steady_step
+            k0 += m
+            if snapshot_every:
+                snaps.append((k0, _host(U), _host(V)))
+        return Trajectory(final=(_host(U), _host(V)), increments=incs, iterations=iters,
+                          times=(1 + np.arange(n)) * tau, steady_step=steady, snapshots=snaps,
+                          diagnostics={"loop": "native"})
     for k in range(n):
         if not device_kin:
             Uh, Vh = _host(U), _host(V)
