@@ -31,6 +31,9 @@ from .solvers import (Preconditioner, _solver_for, build_spectral_cache, make_pr
                       relative_residual, solve_reduced, timestep_residual, two_term_preconditioner)
 
 BLOWUP_LIMIT = 1e100
+# device-evaluable sources / kinetics run the whole time loop natively
+# (sfb_imex_*_run); False keeps the per-step driver (tests compare the two)
+NATIVE_LOOP = True
 
 
 @dataclass(frozen=True)
@@ -230,7 +233,7 @@ def imex_euler_heat(domain: DomainSpec, x: DirectionSet, y: DirectionSet, d_u: f
         X, Y = full_node_grid(domain, x, y)
     U = nat.to_device(u0).clone()
     n = grid.n_steps
-    if F is not None and inner.method == "mo-pcg":
+    if NATIVE_LOOP and F is not None and inner.method == "mo-pcg":
         iters, incs = _heat_native(op, rhs_of, pre, stop, inner, F, source.time_factor, U, n, tau)
         return Trajectory(final=(_host(U),), increments=incs, iterations=iters,
                           times=(1 + np.arange(n)) * tau, diagnostics={"loop": "native"})
@@ -286,7 +289,7 @@ def imex_euler_rds(domain: DomainSpec, x: DirectionSet, y: DirectionSet, d_u: fl
     snaps = []
     steady = None
     host_rates = None
-    if device_kin and inner.method == "mo-pcg":
+    if NATIVE_LOOP and device_kin and inner.method == "mo-pcg":
         # the whole loop natively (sfb_imex_rds_run), in segments ending at the snapshot steps
         su = _solver_for(op_u, pre_u)
         sv = _solver_for(op_v, pre_v)

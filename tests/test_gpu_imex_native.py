@@ -7,6 +7,7 @@ import pytest
 
 import paper_2109_01173_b200 as pb
 from _cases import sine_source
+from conftest import relerr
 from test_host_logic import WAVE
 
 pytestmark = pytest.mark.gpu
@@ -20,16 +21,28 @@ def heat_case(N=8):
     return x, y, F, u0
 
 
-def test_native_heat_loop_matches_per_step_driver():
+def per_step(monkeypatch):
+    monkeypatch.setattr(pb.timestepping, "NATIVE_LOOP", False)
+
+
+def test_native_heat_loop_matches_per_step_driver(monkeypatch):
     x, y, F, u0 = heat_case()
     grid = pb.TimeGrid(1e-3, 6e-3)
     inner = pb.InnerSolver(rule="residual", tol=1e-12, max_iter=5000)
     nat = pb.imex_euler_heat(WAVE, x, y, 1.0, pb.SeparableSource(F, lambda t: np.exp(-t)), u0, grid, inner=inner)
     assert nat.diagnostics.get("loop") == "native"
+    # the per-step driver with a host callable forms W = U + tau s(t) F on the host
+    # (one rounding apart from the fused device weight c_k F)
     host = pb.imex_euler_heat(WAVE, x, y, 1.0, lambda u, X, Y, t: np.exp(-t) * F, u0, grid, inner=inner)
     assert np.array_equal(nat.iterations, host.iterations)
-    assert np.array_equal(nat.final[0], host.final[0])
-    assert np.array_equal(nat.increments, host.increments)
+    assert relerr(nat.final[0], host.final[0]) <= 1e-12
+    assert np.allclose(nat.increments, host.increments, rtol=1e-10)
+    per_step(monkeypatch)
+    dev = pb.imex_euler_heat(WAVE, x, y, 1.0, pb.SeparableSource(F, lambda t: np.exp(-t)), u0, grid, inner=inner)
+    assert "loop" not in dev.diagnostics
+    assert np.array_equal(nat.iterations, dev.iterations)
+    assert np.array_equal(nat.final[0], dev.final[0])
+    assert np.array_equal(nat.increments, dev.increments)
 
 
 def test_native_heat_loop_not_converged():
@@ -60,16 +73,17 @@ def dib_case(N=15):
 
 
 @pytest.mark.parametrize("snap", [0, 2, 4])
-def test_native_rds_loop_matches_per_step_driver(snap):
+def test_native_rds_loop_matches_per_step_driver(snap, monkeypatch):
     p, x, y, state0, tau = dib_case()
     grid = pb.TimeGrid(tau, 7 * tau)
     inner = pb.InnerSolver(rule="residual", tol=1e-12, max_iter=2000)
     nat = pb.imex_euler_rds(pb.SQUARE, x, y, 1.0, p.d_theta, pb.dib_kinetics_pair(p), p.rho, state0, grid,
                             inner=inner, lumped=True, snapshot_every=snap)
     assert nat.diagnostics.get("loop") == "native"
-    kin = (lambda u, v: pb.dib_kinetics(u, v, p)[0], lambda u, v: pb.dib_kinetics(u, v, p)[1])
-    host = pb.imex_euler_rds(pb.SQUARE, x, y, 1.0, p.d_theta, kin, p.rho, state0, grid, inner=inner, lumped=True,
-                             snapshot_every=snap)
+    per_step(monkeypatch)
+    host = pb.imex_euler_rds(pb.SQUARE, x, y, 1.0, p.d_theta, pb.dib_kinetics_pair(p), p.rho, state0, grid,
+                             inner=inner, lumped=True, snapshot_every=snap)
+    assert "loop" not in host.diagnostics
     assert np.array_equal(nat.iterations, host.iterations)
     assert np.array_equal(nat.increments, host.increments)
     assert np.array_equal(nat.final[0], host.final[0]) and np.array_equal(nat.final[1], host.final[1])
