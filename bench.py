@@ -60,6 +60,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-alt", action="store_true", help="skip the banded-preconditioner (f1) measurement")
     ap.add_argument("--no-full", action="store_true", help="skip the full solve to 1e-8 (time to solution)")
+    ap.add_argument("--transposes", default="peer", choices=["peer", "nccl"],
+                    help="N > 1: preconditioner transposes over peer memory (P2P copies + the scatter GEMM) "
+                         "or NCCL all-to-alls")
     return ap.parse_args()
 
 
@@ -211,10 +214,11 @@ def run_native(args):
 
     if world > 1:
         # column-sharded MO-PCG over NCCL (SURVEY §8 e): total work fixed -> strong scaling
-        from paper_2109_01173_b200.distributed import Comm, CudaBackend, Layout, sharded_mo_pcg
+        from paper_2109_01173_b200.distributed import Comm, CudaBackend, Layout, PeerTransposes, sharded_mo_pcg
         lay = Layout(qy, qx, world, rank)
         backend = CudaBackend(op, pre, lay)
         comm = Comm(lay, torch.device("cuda", local))
+        peer = PeerTransposes(lay, backend, sync="stream") if args.transposes == "peer" else None
         rhs_d = rhs_d[:, lay.c0:lay.c0 + lay.n].contiguous()
         w.rhs = np.ascontiguousarray(w.rhs[:, lay.c0:lay.c0 + lay.n])
 
@@ -225,7 +229,7 @@ def run_native(args):
         def step(rhs):
             t1 = time.perf_counter()
             r = sharded_mo_pcg(backend, comm, rhs, stop=stop, max_iter=K_it,
-                               keep_on_device=not isinstance(rhs, np.ndarray))
+                               keep_on_device=not isinstance(rhs, np.ndarray), peer=peer)
             return _Rep(r, 1e3 * (time.perf_counter() - t1))
     else:
         def step(rhs):
@@ -449,7 +453,8 @@ def run_native(args):
                        "iterations_per_step": K_it, "preconditioner_mode": args.precond_mode,
                        "l2": "inputs larger than L2 (8 grid buffers + 2 dense inverses = "
                              f"{(8 * qy * qx + qy * qy + qx * qx) * 8 / 2**20:.0f} MiB > 126 MiB)",
-                       "parallelism": f"column-sharded x{world} (NCCL halo + all-to-all + allreduce)"
+                       "parallelism": f"column-sharded x{world} (NCCL halo + allreduce; transposes: "
+                                      f"{'P2P copies + GEMM-fused NVLink scatter' if args.transposes == 'peer' else 'NCCL all-to-all'})"
                        if world > 1 else "single GPU",
                        "setup_s": round(setup_s, 3)},
             "roofline": {"bound": "tensor", "kernel": "dgemm_nt (DMMA.8x8x4 + TMA)",

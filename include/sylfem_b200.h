@@ -231,6 +231,28 @@ int sfb_dgemm_nt(const double* A_dev, int lda, const double* Bt_dev, int ldb,
 /* ---- host-synchronous blocks of the column-sharded MO-PCG (one rank's
  *      columns; the collectives run between these calls) --------------- */
 /* U += alpha Q; R -= alpha W; *rr_host = local sum R^2 (solvers.py:432-434). */
+/* C = A Bt^T with row m of C sent to destination d, seg[d] <= m < seg[d+1]
+ * (seg_host: nseg + 1 increasing row offsets from 0 to M, nseg <= 8):
+ * dst[d][(m - seg[d]) * ldd[d] + col_off + n] = C[m][n].  The destinations
+ * may be peer GPUs' buffers (CUDA IPC, NVLink stores): the column-sharded
+ * preconditioner's second transpose all-to-all fused into its GEMM. */
+int sfb_dgemm_nt_scatter(const double* A_dev, int lda, const double* Bt_dev, int ldb,
+                         int M, int N, int K, int nseg, const int* seg_host,
+                         double* const* dst_dev_host, const int* ldd_host, int col_off,
+                         void* stream);
+/* dst (ldd) <- src (lds), rows x cols doubles; either side may be a peer GPU's
+ * buffer (the first transpose of the sharded preconditioner as P2P copies). */
+int sfb_copy2d(double* dst_dev, int ldd, const double* src_dev, int lds, int rows, int cols,
+               void* stream);
+/* CUDA IPC of a device buffer: a 64-byte handle of its allocation plus the
+ * buffer's offset inside it; open returns the mapped allocation base (for
+ * close) and the buffer pointer. */
+int sfb_ipc_get_handle(const void* ptr_dev, unsigned char* handle64_host,
+                       unsigned long long* offset_host);
+int sfb_ipc_open(const unsigned char* handle64_host, unsigned long long offset,
+                 void** base_dev, void** ptr_dev);
+int sfb_ipc_close(void* base_dev);
+
 int sfb_vec_update(double* U_dev, double* R_dev, const double* Q_dev, const double* W_dev,
                    int ld, int rows, int cols, double alpha, double* rr_host, void* stream);
 /* Q = Z + beta Q (first != 0: Q = Z) (solvers.py:419, 451-452). */

@@ -89,6 +89,18 @@ __device__ __forceinline__ double tile_epilogue(double (&acc)[MI][4][2], const G
             double v0 = acc[i][j][0], v1 = acc[i][j][1];
             const bool ok0 = n < N, ok1 = n + 1 < N;
             switch (ep.mode) {
+                case EPI_SCATTER: {
+                    int d = 0;
+                    while (d + 1 < ep.nseg && m >= ep.seg[d + 1]) ++d;
+                    double* c = ep.dst[d] + (size_t)(m - ep.seg[d]) * ep.ldd_seg[d] + ep.col_off + n;
+                    if (ok1 && (reinterpret_cast<uintptr_t>(c) & 15) == 0) {
+                        *reinterpret_cast<double2*>(c) = make_double2(v0, v1);
+                    } else {
+                        if (ok0) c[0] = v0;
+                        if (ok1) c[1] = v1;
+                    }
+                    break;
+                }
                 case EPI_STORE_T:
                     if (ok0) ep.C[(size_t)n * ep.ldc + m] = v0;
                     if (ok1) ep.C[(size_t)(n + 1) * ep.ldc + m] = v1;

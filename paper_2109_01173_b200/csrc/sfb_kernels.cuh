@@ -14,8 +14,13 @@ enum GemmEpiMode {
     EPI_HADAMARD_SUM = 2,   // C[m][n] = acc / (sr[m] + sc[n])      (solvers.py:245-253)
     EPI_HADAMARD_PROD = 3,  // C[m][n] = acc * sr[m] * sc[n]        (sr, sc = 1/lambda)
     EPI_STORE_DOT = 4,      // C[m][n] = acc; dot += acc * D[m][n]  (<Z,R>, solvers.py:448)
-    EPI_ACCUM = 5           // C[m][n] += acc
+    EPI_ACCUM = 5,          // C[m][n] += acc
+    EPI_SCATTER = 6         // row m of C goes to destination d (seg[d] <= m < seg[d+1]):
+                            // dst[d][(m - seg[d]) * ldd[d] + col_off + n] = acc  (the
+                            // transpose all-to-all of the sharded preconditioner fused
+                            // into the GEMM: dst[d] are peer GPUs' buffers over NVLink)
 };
+constexpr int kMaxScatter = 8;
 
 struct GemmEpi {
     int mode = EPI_STORE;
@@ -31,6 +36,12 @@ struct GemmEpi {
     double* dot_out = nullptr;    // receives the dot total when non-null
     double* sk_ws = nullptr;      // stream-K partial tiles (gemm_workspace_doubles())
     unsigned* sk_flags = nullptr; // stream-K per-tile counters (gemm_max_tiles(), zeroed once)
+    // EPI_SCATTER destinations
+    int nseg = 0;
+    int seg[kMaxScatter + 1] = {};
+    double* dst[kMaxScatter] = {};
+    int ldd_seg[kMaxScatter] = {};
+    int col_off = 0;
 };
 
 int launch_dgemm_nt(const double* A, int lda, const double* Bt, int ldb, int M, int N, int K,

@@ -1160,6 +1160,80 @@ int sfb_dgemm_nt(const double* A, int lda, const double* Bt, int ldb, int M, int
     return launch_dgemm_nt(A, lda, Bt, ldb, M, N, K, with_ws(e, &gw), s);
 }
 
+int sfb_dgemm_nt_scatter(const double* A, int lda, const double* Bt, int ldb, int M, int N, int K, int nseg,
+                         const int* seg_host, double* const* dst_host, const int* ldd_host, int col_off,
+                         void* stream) {
+    if (nseg <= 0 || nseg > kMaxScatter) return arg_error("scatter GEMM: 1..8 destinations");
+    if (!seg_host || !dst_host || !ldd_host) return arg_error("scatter GEMM: null destination table");
+    GemmEpi e;
+    e.mode = EPI_SCATTER;
+    e.nseg = nseg;
+    for (int d = 0; d <= nseg; ++d) e.seg[d] = seg_host[d];
+    if (e.seg[0] != 0 || e.seg[nseg] != M) return arg_error("scatter GEMM: segments must cover the M rows");
+    for (int d = 0; d < nseg; ++d) {
+        if (e.seg[d + 1] < e.seg[d]) return arg_error("scatter GEMM: segments must be increasing");
+        if (!dst_host[d] && e.seg[d + 1] > e.seg[d]) return arg_error("scatter GEMM: null destination");
+        e.dst[d] = dst_host[d];
+        e.ldd_seg[d] = ldd_host[d];
+    }
+    e.col_off = col_off;
+    cudaStream_t s = (cudaStream_t)stream;
+    ScopedFree tmp(s);
+    GemmWs gw;
+    SFB_TRY(temp_ws(tmp, gw, s));
+    return launch_dgemm_nt(A, lda, Bt, ldb, M, N, K, with_ws(e, &gw), s);
+}
+
+int sfb_copy2d(double* dst, int ldd, const double* src, int lds, int rows, int cols, void* stream) {
+    if (rows <= 0 || cols <= 0) return SFB_OK;
+    SFB_CUDA_TRY(cudaMemcpy2DAsync(dst, (size_t)ldd * 8, src, (size_t)lds * 8, (size_t)cols * 8, rows,
+                                   cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+    return SFB_OK;
+}
+
+// CUDA IPC of device buffers (the sharded preconditioner's receive buffers):
+// the handle names the whole allocation, so the pointer's offset inside it
+// travels with the handle.
+int sfb_ipc_get_handle(const void* ptr, unsigned char* handle64, unsigned long long* offset) {
+    if (!ptr || !handle64 || !offset) return arg_error("ipc handle: null argument");
+    static CUresult (*range)(CUdeviceptr*, size_t*, CUdeviceptr) = nullptr;
+    if (range == nullptr) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) != cudaSuccess || !p) {
+            set_error("cuMemGetAddressRange entry point unavailable");
+            return SFB_ERR_CUDA;
+        }
+        range = reinterpret_cast<CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr)>(p);
+    }
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (range(&base, &size, (CUdeviceptr)ptr) != CUDA_SUCCESS) {
+        set_error("cuMemGetAddressRange failed");
+        return SFB_ERR_CUDA;
+    }
+    cudaIpcMemHandle_t h;
+    SFB_CUDA_TRY(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));
+    std::memcpy(handle64, &h, sizeof(h));
+    *offset = (unsigned long long)((CUdeviceptr)ptr - base);
+    return SFB_OK;
+}
+
+int sfb_ipc_open(const unsigned char* handle64, unsigned long long offset, void** base, void** ptr) {
+    if (!handle64 || !base || !ptr) return arg_error("ipc open: null argument");
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle64, sizeof(h));
+    SFB_CUDA_TRY(cudaIpcOpenMemHandle(base, h, cudaIpcMemLazyEnablePeerAccess));
+    *ptr = static_cast<char*>(*base) + offset;
+    return SFB_OK;
+}
+
+int sfb_ipc_close(void* base) {
+    if (!base) return SFB_OK;
+    SFB_CUDA_TRY(cudaIpcCloseMemHandle(base));
+    return SFB_OK;
+}
+
 // ------------------------------------------------ sharded MO-PCG blocks ---
 
 int sfb_vec_update(double* U, double* R, const double* Q, const double* W, int ld, int rows, int cols, double alpha,

@@ -145,6 +145,114 @@ class Comm:
         return self.t.cat([p.reshape(L.n, L.row_counts[s]) for s, p in enumerate(parts)], dim=1)
 
 
+class PeerTransposes:
+    """The two transposes of the sharded preconditioner over peer memory
+    (CUDA IPC mappings of the other ranks' receive buffers; NVLink stores
+    between the GPUs of one node) instead of NCCL all-to-alls:
+
+    * cols -> rows: each rank copies the row block of rank s out of its
+      column shard of R straight into rank s's row buffer (P2P copies);
+    * rows^T -> cols^T: fused into the GEMM that produces the data —
+      X^T = P_R^-T R_rows^T is computed by ``sfb_dgemm_nt_scatter``, whose
+      epilogue stores output row j (a grid column) into the column-shard
+      buffer of the rank that owns column j.
+
+    ``sync()`` after each exchange makes the peers' stores visible:
+    ``"host"`` (stream synchronize + process-group barrier: the ranks only
+    meet on the host, so ranks sharing one GPU never wait on each other's
+    kernels) or ``"stream"`` (a one-element NCCL all-reduce on the stream,
+    for one GPU per rank).  Reuse of the receive buffers across iterations is
+    ordered by the scalar all-reduces of the iteration, which every rank
+    joins only after its preconditioner GEMMs have read them."""
+
+    def __init__(self, layout: Layout, backend, group=None, sync: str = "host"):
+        import torch
+        import torch.distributed as dist
+        self.t, self.dist, self.L, self.group = torch, dist, layout, group
+        if sync not in ("host", "stream"):
+            raise ConfigError(f"unknown peer sync mode '{sync}'")
+        self.sync_mode = sync
+        L = layout
+        # receive buffers: row shard of R (m x q_x) and transposed column shard (n x q_y)
+        self.rows = backend.zeros(L.m, L.qx)
+        self.colsT = backend.zeros(L.n, L.qy)
+        mine = [self._handle(self.rows), self._handle(self.colsT)]
+        allh = [None] * L.world
+        dist.all_gather_object(allh, mine, group=group)
+        self._bases = []
+        self.peer_rows, self.peer_colsT = [], []
+        for r in range(L.world):
+            if r == L.rank:
+                self.peer_rows.append((self.rows.data_ptr(), self.rows.stride(0)))
+                self.peer_colsT.append((self.colsT.data_ptr(), self.colsT.stride(0)))
+                continue
+            (hr, orr, ldr), (hc, oc, ldc) = allh[r]
+            self.peer_rows.append((self._open(hr, orr), ldr))
+            self.peer_colsT.append((self._open(hc, oc), ldc))
+        self._flag = torch.zeros(1, dtype=torch.float64, device="cuda") if sync == "stream" else None
+
+    def _handle(self, X):
+        h = (nat.C.c_ubyte * 64)()
+        off = nat.C.c_ulonglong(0)
+        nat.check(nat.lib().sfb_ipc_get_handle(X.data_ptr(), h, nat.C.byref(off)), "ipc handle")
+        return bytes(h), int(off.value), X.stride(0)
+
+    def _open(self, handle, offset):
+        base, ptr = nat.C.c_void_p(), nat.C.c_void_p()
+        nat.check(nat.lib().sfb_ipc_open((nat.C.c_ubyte * 64).from_buffer_copy(handle), offset,
+                                         nat.C.byref(base), nat.C.byref(ptr)), "ipc open")
+        self._bases.append(base.value)
+        return ptr.value
+
+    def close(self):
+        for b in self._bases:
+            nat.lib().sfb_ipc_close(b)
+        self._bases = []
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def sync(self):
+        if self.L.world == 1:
+            return
+        if self.sync_mode == "stream":
+            self.dist.all_reduce(self._flag, group=self.group)
+        else:
+            self.t.cuda.current_stream().synchronize()
+            self.dist.barrier(group=self.group)
+
+    def cols_to_rows(self, Xc):
+        """Push the row block of every rank out of this column shard (P2P copies)."""
+        L = self.L
+        Xc = Xc if Xc.stride(1) == 1 else Xc.contiguous()
+        for s in range(L.world):
+            dst, ldd = self.peer_rows[s]
+            src = Xc[L.row_offs[s]:L.row_offs[s] + L.row_counts[s], :]
+            nat.check(nat.lib().sfb_copy2d(dst + 8 * L.c0, ldd, src.data_ptr(), Xc.stride(0), L.row_counts[s], L.n,
+                                           nat.stream()), "peer copy")
+        self.sync()
+        return self.rows
+
+    def right_T_scatter(self, RinvT, R_rows):
+        """X^T = P_R^-T R_rows^T with each output row stored straight into
+        its owner's transposed column shard; returns this rank's shard."""
+        L = self.L
+        A, B = RinvT, R_rows
+        if B.stride(0) % 2 or B.data_ptr() % 16:
+            B = B.contiguous()
+        n = L.world
+        seg = (nat.C.c_int * (n + 1))(*(list(L.col_offs) + [L.qx]))
+        dst = (nat.C.c_void_p * n)(*[p for p, _ in self.peer_colsT])
+        ldd = (nat.C.c_int * n)(*[ld for _, ld in self.peer_colsT])
+        nat.check(nat.lib().sfb_dgemm_nt_scatter(A.data_ptr(), A.stride(0), B.data_ptr(), B.stride(0), L.qx, L.m,
+                                                  L.qx, n, seg, dst, ldd, L.r0, nat.stream()), "scatter gemm")
+        self.sync()
+        return self.colsT
+
+
 class CudaBackend:
     """Local compute of one rank through the C ABI (banded block operator,
     DMMA GEMMs, fused vector passes)."""
@@ -249,9 +357,12 @@ class CudaBackend:
 
 
 def sharded_mo_pcg(backend, comm: Comm, rhs_local, stop: StoppingRule | None = None, u0_local=None,
-                   max_iter: int = 1000, identity: bool = False, keep_on_device: bool = False) -> SolveReport:
+                   max_iter: int = 1000, identity: bool = False, keep_on_device: bool = False,
+                   peer: PeerTransposes | None = None) -> SolveReport:
     """MO-PCG over column shards; same recurrences, stop logic and report as
-    solvers.mo_pcg (solvers.py:365-453).  Returns this rank's columns."""
+    solvers.mo_pcg (solvers.py:365-453).  Returns this rank's columns.
+    With ``peer`` the preconditioner's transposes go over peer memory
+    (PeerTransposes) instead of the all-to-alls of ``comm``."""
     stop = stop or relative_residual()
     t0 = time.perf_counter()
     L = comm.L
@@ -283,6 +394,8 @@ def sharded_mo_pcg(backend, comm: Comm, rhs_local, stop: StoppingRule | None = N
     def precond(Rk):
         if identity:
             return backend.copy(Rk)
+        if peer is not None:  # transposes over peer memory, the second fused into the GEMM
+            return backend.left(peer.right_T_scatter(backend.RinvT, peer.cols_to_rows(Rk)))
         XrT = backend.right_T(comm.cols_to_rows(Rk))
         return backend.left(comm.rowsT_to_colsT(XrT))
 

@@ -14,7 +14,7 @@ import torch.distributed as dist
 
 import paper_2109_01173_b200 as pb
 from _cases import sine_source
-from paper_2109_01173_b200.distributed import Comm, CudaBackend, Layout, sharded_mo_pcg
+from paper_2109_01173_b200.distributed import Comm, CudaBackend, Layout, PeerTransposes, sharded_mo_pcg
 from test_host_logic import WAVE
 
 
@@ -46,7 +46,7 @@ def problem(N):
     return op, pre, rhs_of(sine_source(N, N, 3))
 
 
-def worker(rank, world, port, N, out_dir):
+def worker(rank, world, port, N, out_dir, peer=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -57,8 +57,15 @@ def worker(rank, world, port, N, out_dir):
         lay = Layout(qy, qx, world, rank)
         be = CudaBackend(op, pre, lay)
         comm = HostStagedComm(lay)
+        # peer: the transposes over CUDA IPC mappings (P2P copies + the scatter GEMM),
+        # synchronised on the host so ranks sharing the GPU never wait on each other's kernels
+        pt = PeerTransposes(lay, be, sync="host") if peer else None
         rep = sharded_mo_pcg(be, comm, rhs[:, lay.c0:lay.c0 + lay.n], stop=pb.relative_residual(1e-12),
-                             max_iter=5000)
+                             max_iter=5000, peer=pt)
+        if pt is not None:
+            torch.cuda.synchronize()
+            dist.barrier()
+            pt.close()
         np.savez(os.path.join(out_dir, f"rank{rank}.npz"), U=rep.solution, iters=rep.iterations,
                  hist=rep.residual_history)
     finally:

@@ -16,11 +16,11 @@ from test_sharded_cpu import free_port
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_sharded_cuda_backend_multirank_matches_mo_pcg(world):
+@pytest.mark.parametrize("world,peer", [(2, False), (3, False), (2, True), (3, True)])
+def test_sharded_cuda_backend_multirank_matches_mo_pcg(world, peer):
     N = 40
     with tempfile.TemporaryDirectory() as d:
-        mp.spawn(worker, args=(world, free_port(), N, d), nprocs=world, join=True)
+        mp.spawn(worker, args=(world, free_port(), N, d, peer), nprocs=world, join=True)
         parts = [np.load(os.path.join(d, f"rank{r}.npz")) for r in range(world)]
     U = np.concatenate([p["U"] for p in parts], axis=1)
     iters = {int(p["iters"]) for p in parts}
@@ -31,3 +31,31 @@ def test_sharded_cuda_backend_multirank_matches_mo_pcg(world):
     # couple of iterations (SURVEY finding 6); the solution is the parity check
     assert abs(iters.pop() - ref.iterations) <= max(2, ref.iterations // 200)
     assert relerr(U, ref.solution) <= 1e-10
+
+
+def test_scatter_gemm_places_rows_like_the_transpose():
+    """sfb_dgemm_nt_scatter with three local destinations (stand-ins for the
+    ranks' column-shard buffers) against the plain GEMM and the layout."""
+    import torch
+
+    from paper_2109_01173_b200 import _native as nat
+    from paper_2109_01173_b200.distributed import Layout
+
+    rng = np.random.default_rng(3)
+    qx, m, world, off = 302, 77, 3, 5  # even leading dimensions (TMA rows)
+    A = torch.from_numpy(rng.standard_normal((qx, qx))).cuda()
+    B = torch.from_numpy(rng.standard_normal((m, qx))).cuda()
+    ref = (A @ B.T).cpu().numpy()
+    lay = Layout(qy=150, qx=qx, world=world, rank=0)
+    bufs = [torch.full((lay.col_counts[s], 130 + 2 * s), np.nan, dtype=torch.float64, device="cuda")
+            for s in range(world)]
+    seg = (nat.C.c_int * (world + 1))(*(list(lay.col_offs) + [qx]))
+    dst = (nat.C.c_void_p * world)(*[b.data_ptr() for b in bufs])
+    ldd = (nat.C.c_int * world)(*[b.stride(0) for b in bufs])
+    nat.check(nat.lib().sfb_dgemm_nt_scatter(A.data_ptr(), qx, B.data_ptr(), qx, qx, m, qx, world, seg, dst, ldd,
+                                              off, nat.stream()), "scatter")
+    for s in range(world):
+        got = bufs[s].cpu().numpy()
+        c0, n = lay.col_offs[s], lay.col_counts[s]
+        assert np.allclose(got[:, off:off + m], ref[c0:c0 + n, :], rtol=1e-13, atol=1e-12)
+        assert np.all(np.isnan(got[:, :off])) and np.all(np.isnan(got[:, off + m:]))  # nothing outside the block
