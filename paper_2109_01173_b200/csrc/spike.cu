@@ -43,6 +43,9 @@ constexpr int S = 64;          // segment length == tile edge
 constexpr int SS = 16;         // sub-segment length (one thread's sweep)
 constexpr int NSUB = S / SS;   // sub-segments per segment
 constexpr int NT = S * NSUB;   // threads per tile CTA
+#ifndef CHAIN_L
+#define CHAIN_L 8              // lines per interface-chain CTA (2B threads each; 8: 87 vs 93 us per apply at 16)
+#endif
 
 enum { DIR_COL = 0, DIR_ROW = 1 };
 enum { PH_LOCAL = 0, PH_FUSED = 1 };  // plain local solve, or the previous factor's correction first
@@ -419,69 +422,66 @@ __device__ __forceinline__ void cp_async8(double* dst, const double* src) {
                  : "memory");
 }
 
+// One line's interface chain is spread over 2B threads (one per interface
+// value, consecutive lanes): each thread forms one row of the 2B x 2B block
+// step and the b values the next step needs travel by shuffle, so the
+// sequential critical path per step is two FMAs and a shuffle instead of a
+// whole block product, and the 2047-line chain occupies 4x the warps.
+__host__ __device__ constexpr int chain_group(int b) { return b == 1 ? 2 : (b == 2 ? 4 : 8); }  // 2B -> power of 2
+
 template <int B>
-__global__ void __launch_bounds__(32) spike_chain_kernel(int nlines, int P, const double* __restrict__ coef,
-                                                         double* sv, int coef_in_smem, const PcgState* gate) {
+__global__ void __launch_bounds__(CHAIN_L * chain_group(B)) spike_chain_kernel(int nlines, int P, const double* __restrict__ coef,
+                                                                      double* sv, int coef_in_smem,
+                                                                      const PcgState* gate) {
     SFB_PDL_PROLOGUE();
     if (gate != nullptr && gate->status != SFB_PCG_RUNNING) return;
     constexpr int B2 = 2 * B;
+    constexpr int L = CHAIN_L;                 // lines per CTA
     constexpr int PER = B2 * B2 + 2 * B2 * B;  // K (2B x 2B), KA (2B x B), Ch (2B x B)
     extern __shared__ double gs[];             // [P][2B][L], then the coefficients when they fit
-    const int L = blockDim.x, l = threadIdx.x, line0 = blockIdx.x * L;
-    const bool live = line0 + l < nlines;
+    constexpr int GP = chain_group(B);         // lanes per line (2B rounded up to a power of two)
+    const int t = threadIdx.x, l = t / GP, i0 = t % GP, line0 = blockIdx.x * L;
+    const bool live = line0 + l < nlines && i0 < B2;
+    const int i = i0 < B2 ? i0 : 0;            // padding lanes mirror row 0 and store nothing
+    const unsigned gmask = 0xffffffffu;        // whole warps (GP divides 32): every lane shuffles
+    const int gbase = (t & 31) - i0;           // lane of this line's row 0
     // stage with every load in flight (cp.async, one wait)
     double* cs = gs + (size_t)P * B2 * L;
     if (live)
-        for (int row = 0; row < P * B2; ++row) cp_async8(gs + row * L + l, sv + (size_t)row * nlines + line0 + l);
+        for (int p = 0; p < P; ++p) cp_async8(gs + (p * B2 + i) * L + l, sv + (size_t)(p * B2 + i) * nlines + line0 + l);
     if (coef_in_smem)
-        for (int i = l; i < P * PER; i += L) cp_async8(cs + i, coef + i);
+        for (int k = t; k < P * PER; k += L * GP) cp_async8(cs + k, coef + k);
     asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
     const double* cf = coef_in_smem ? cs : coef;
-    if (live) {
-        double prev[B];  // u part of d_{p-1}
+    double prev[B];  // u part of d_{p-1}
+    #pragma unroll
+    for (int d = 0; d < B; ++d) prev[d] = 0.0;
+    for (int p = 0; p < P; ++p) {
+        const double* K = cf + (size_t)p * PER + i * B2;
+        const double* KA = cf + (size_t)p * PER + B2 * B2 + i * B;
+        double v = 0.0;
         #pragma unroll
-        for (int d = 0; d < B; ++d) prev[d] = 0.0;
-        #pragma unroll 2
-        for (int p = 0; p < P; ++p) {
-            const double* K = cf + (size_t)p * PER;
-            const double* KA = K + B2 * B2;
-            double g[B2], dv[B2];
-            #pragma unroll
-            for (int j = 0; j < B2; ++j) g[j] = gs[(p * B2 + j) * L + l];
-            #pragma unroll
-            for (int i = 0; i < B2; ++i) {
-                double v = 0.0;
-                #pragma unroll
-                for (int j = 0; j < B2; ++j) v = fma(K[i * B2 + j], g[j], v);
-                #pragma unroll
-                for (int j = 0; j < B; ++j) v = fma(-KA[i * B + j], prev[j], v);
-                dv[i] = v;
-            }
-            #pragma unroll
-            for (int i = 0; i < B2; ++i) gs[(p * B2 + i) * L + l] = dv[i];
-            #pragma unroll
-            for (int d = 0; d < B; ++d) prev[d] = dv[B + d];
-        }
-        double nx[B];  // t part of z_{p+1}
+        for (int j = 0; j < B2; ++j) v = fma(K[j], line0 + l < nlines ? gs[(p * B2 + j) * L + l] : 0.0, v);
         #pragma unroll
-        for (int d = 0; d < B; ++d) nx[d] = 0.0;
-        #pragma unroll 2
-        for (int p = P - 1; p >= 0; --p) {
-            const double* Ch = cf + (size_t)p * PER + B2 * B2 + B2 * B;
-            double z[B2];
-            #pragma unroll
-            for (int i = 0; i < B2; ++i) {
-                double v = gs[(p * B2 + i) * L + l];
-                #pragma unroll
-                for (int j = 0; j < B; ++j) v = fma(-Ch[i * B + j], nx[j], v);
-                z[i] = v;
-            }
-            #pragma unroll
-            for (int i = 0; i < B2; ++i) sv[((size_t)p * B2 + i) * nlines + line0 + l] = z[i];
-            #pragma unroll
-            for (int d = 0; d < B; ++d) nx[d] = z[d];
-        }
+        for (int j = 0; j < B; ++j) v = fma(-KA[j], prev[j], v);
+        __syncwarp();  // the line's other rows have read step p's values
+        if (live) gs[(p * B2 + i) * L + l] = v;
+        #pragma unroll
+        for (int d = 0; d < B; ++d) prev[d] = __shfl_sync(gmask, v, gbase + B + d);
+    }
+    __syncwarp();
+    double nx[B];  // t part of z_{p+1}
+    #pragma unroll
+    for (int d = 0; d < B; ++d) nx[d] = 0.0;
+    for (int p = P - 1; p >= 0; --p) {
+        const double* Ch = cf + (size_t)p * PER + B2 * B2 + B2 * B + i * B;
+        double v = live ? gs[(p * B2 + i) * L + l] : 0.0;
+        #pragma unroll
+        for (int j = 0; j < B; ++j) v = fma(-Ch[j], nx[j], v);
+        if (live) sv[((size_t)p * B2 + i) * nlines + line0 + l] = v;
+        #pragma unroll
+        for (int d = 0; d < B; ++d) nx[d] = __shfl_sync(gmask, v, gbase + d);
     }
 }
 
@@ -492,12 +492,8 @@ int chain(const SpikeFactor& f, int nlines, double* sv, const PcgState* gate, cu
     } else {
         const int P = (f.n + S - 1) / S;
         constexpr size_t cap = 200 * 1024;
-        int L = 32;
+        constexpr int L = CHAIN_L;
         size_t sm = (size_t)P * 2 * B * L * 8;
-        if (sm > cap) {
-            L = 16;
-            sm /= 2;
-        }
         if (sm > cap) {
             set_error("banded preconditioner: order too large for the interface chain");
             return SFB_ERR_UNSUPPORTED;
@@ -506,8 +502,8 @@ int chain(const SpikeFactor& f, int nlines, double* sv, const PcgState* gate, cu
         const int cin = sm + csm <= cap ? 1 : 0;
         if (cin) sm += csm;
         SFB_TRY(ensure_dynamic_smem(spike_chain_kernel<B>, sm));
-        return launch_kernel(spike_chain_kernel<B>, dim3((nlines + L - 1) / L), dim3(L), sm, s, nlines, P, f.coef,
-                             sv, cin, gate);
+        return launch_kernel(spike_chain_kernel<B>, dim3((nlines + L - 1) / L), dim3(L * chain_group(B)), sm, s, nlines, P,
+                             f.coef, sv, cin, gate);
     }
 }
 
