@@ -411,8 +411,10 @@ def run_native(args):
         except (OSError, ValueError):
             pass
         n2 = qy * qx * 8
-        band_gbs = 4 * n2 / (pt["operator_ms"] * 1e-3) / 1e9
-        upd_gbs = 6 * n2 / (pt["update_ms"] * 1e-3) / 1e9
+        # the banded iteration defers U += alpha Q into the next operator pass
+        # (Q_prev is in shared memory there): operator pass 48 B, update pass 24 B
+        band_gbs = 6 * n2 / (pt["operator_ms"] * 1e-3) / 1e9
+        upd_gbs = 3 * n2 / (pt["update_ms"] * 1e-3) / 1e9
         ptraffic = {}
         try:
             ptraffic = json.load(open(os.path.join(ROOT, "profiles", "ncu_passes_r01.json")))
@@ -422,14 +424,15 @@ def run_native(args):
                "banded_operator_pass": {
                    "kernel": f"band_kernel<{len(op)} terms, W={2 * op.half_bandwidth + 1}> (LD_PCG)",
                    "achieved": band_gbs, "frac": band_gbs / hbm_peak, "launch_ms": pt["operator_ms"],
-                   "algorithmic_bytes": 4 * n2,
+                   "algorithmic_bytes": 6 * n2,
                    "traffic": ptraffic.get("band_kernel<5,5,PCG>", {}).get("dram_bytes_per_launch"),
-                   "note": "read Z, Q_prev; write Q, W (+ <W,Q>, |Q|^2); 2*T*W FMAs per element on the FP64 pipe"},
+                   "note": "read Z, Q_prev, U; write Q, W, U (the previous iteration's U += alpha Q rides along; "
+                           "+ <W,Q>, |Q|^2); 2*T*W FMAs per element on the FP64 pipe"},
                "vector_update_pass": {
-                   "kernel": "pcg_update_kernel", "achieved": upd_gbs, "frac": upd_gbs / hbm_peak,
-                   "launch_ms": pt["update_ms"], "algorithmic_bytes": 6 * n2,
-                   "traffic": ptraffic.get("pcg_update_kernel", {}).get("dram_bytes_per_launch"),
-                   "note": "read U, R, Q, W; write U, R (+ |R|^2, stop test)"},
+                   "kernel": "pcg_rupdate_kernel", "achieved": upd_gbs, "frac": upd_gbs / hbm_peak,
+                   "launch_ms": pt["update_ms"], "algorithmic_bytes": 3 * n2,
+                   "traffic": ptraffic.get("pcg_rupdate_kernel", {}).get("dram_bytes_per_launch"),
+                   "note": "read R, W; write R (+ |R|^2, stop test)"},
                "preconditioner_ms": pt["preconditioner_ms"]}
 
     # ---- CPU baseline (rank 0, N = 1 only) ----

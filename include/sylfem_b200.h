@@ -185,7 +185,9 @@ int sfb_pcg_solve(sfb_pcg* s, const double* rhs_dev, int ldr,
                   sfb_pcg_result* res, void* stream);
 /* Device time (ms per launch, averaged over `reps` back-to-back launches)
  * of the passes of one MO-PCG iteration on the solver's buffers, for the
- * roofline report: ms[0] banded operator pass, ms[1] vector update pass,
+ * roofline report: ms[0] banded operator pass (direction update, W = L(Q),
+ * <W,Q>, |Q|^2 and the previous iteration's deferred U += alpha Q),
+ * ms[1] vector update pass (R -= alpha W, |R|, stop test),
  * ms[2] preconditioner.  Call after a solve; clobbers the solver buffers.
  * Measurement only: no reference counterpart. */
 int sfb_pcg_pass_times(sfb_pcg* s, int reps, double* ms);

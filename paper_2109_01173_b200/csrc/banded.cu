@@ -16,7 +16,10 @@
 // sum_e X[r][c+e] h_t[e] is formed once per row and scattered into a ring of
 // W partial outputs with the left-factor coefficients (shared-memory
 // broadcasts).  The MO-PCG direction update Q = Z + beta Q is applied inline
-// as the halo values are read (the new Q column is stored by its owner); the
+// as the halo values are read (the new Q column is stored by its owner), and
+// the previous iteration's U += alpha Q rides along (U's rows come through
+// the same TMA ring; Q_prev is already there), so the update pass that
+// follows only handles R; the
 // IMEX heat source and the DIB kinetics are applied to the landed chunk in
 // shared memory first (named barrier among the consumers).  Epilogues: plain
 // store, or the MO-PCG store + <W,Q>, |Q|^2 partials with a last-block alpha
@@ -79,13 +82,20 @@ struct BandCfg {
     static constexpr int XSP = pad128(XS);   // 128-byte aligned regions
     static constexpr int GSP = pad128(GS);
     static constexpr int STAGE = 2 * XSP + GSP;
+    static constexpr int USP = pad128(CH * TX);  // MO-PCG: the strip's rows of U (deferred U += alpha Q)
     static constexpr int SMEM = NS * STAGE * 8 + 128;
+    static constexpr int SMEM_PCG = NS * (STAGE + USP) * 8 + 128;
 };
+template <int T, int W, int MODE>
+__host__ __device__ constexpr int band_stage() { return BandCfg<T, W>::STAGE + (MODE == LD_PCG ? BandCfg<T, W>::USP : 0); }
+template <int T, int W, int MODE>
+__host__ __device__ constexpr int band_smem() { return MODE == LD_PCG ? BandCfg<T, W>::SMEM_PCG : BandCfg<T, W>::SMEM; }
 
 struct BandMaps {
     CUtensorMap a;       // input A (X / Z / U / eta), box {HCB, CH}
     CUtensorMap b[2];    // input B (Q0, Q1 / F / theta)
     CUtensorMap g;       // gskew, box {TWP, CH}
+    CUtensorMap u;       // MO-PCG: U, box {TX, CH}
 };
 
 // rows per CTA and row blocks for an output of `rows` x `cols`
@@ -116,11 +126,14 @@ __global__ void __launch_bounds__(TX + 32, band_minb<W>()) band_kernel(BandArgs 
     constexpr bool pcg_ep = mode == LD_PCG;
     PcgState* st = a.pcg;
     int s = 0;
-    double beta = 0.0;
+    double beta = 0.0, alpha_prev = 0.0;
     if constexpr (mode == LD_PCG) {
         if (st->status != SFB_PCG_RUNNING) return;  // uniform gate
         s = st->iter;
-        if (s > 0) beta = st->rz_next / st->rz;      // solvers.py:448-452
+        if (s > 0) {
+            beta = st->rz_next / st->rz;             // solvers.py:448-452
+            alpha_prev = st->alpha;                  // the previous iteration's U += alpha Q, deferred here
+        }
     }
     const int x0 = blockIdx.x * TX, y0 = blockIdx.y * ry;
     const int rows_here = min(ry, a.out_rows - y0);
@@ -148,7 +161,10 @@ __global__ void __launch_bounds__(TX + 32, band_minb<W>()) band_kernel(BandArgs 
     // A's box starts at full-grid column x0 + hoff - shA (U column minus acs), B's at x0 + hoff - shB;
     // both even, so every box row is 16-byte aligned in global memory
     const int shA = (hoff - acs) & 1, shB = hoff & 1;
-    const uint32_t tx_bytes = (uint32_t)((hasB ? 2 : 1) * C::XS + C::GS) * 8;
+    constexpr int STG = band_stage<T, W, MODE>();  // doubles per ring stage
+    // MO-PCG from the second iteration on: U's rows ride in the ring too
+    const bool withU = mode == LD_PCG && hasB;
+    const uint32_t tx_bytes = (uint32_t)((hasB ? 2 : 1) * C::XS + C::GS + (withU ? CH * TX : 0)) * 8;
     const bool producer = t >= TX;  // warp 4 feeds the ring; warps 0-3 consume it
 
     if (t == 0) {
@@ -168,13 +184,14 @@ __global__ void __launch_bounds__(TX + 32, band_minb<W>()) band_kernel(BandArgs 
             for (int k = 0; k < nch; ++k) {
                 const int sl = k % NS;
                 if (k >= NS) mbar_wait_u32(smem_u32(&empty[sl]), ((k / NS) - 1) & 1);
-                double* A = sm + sl * C::STAGE;
+                double* A = sm + sl * STG;
                 const uint32_t bar = smem_u32(&full[sl]);
                 const int r0 = k * CH;
                 mbar_expect_tx_u32(bar, tx_bytes);
                 tma_load_u32(smem_u32(A), &maps.a, bar, x0 + hoff - acs - shA, y0 + goff + r0 - ars);
                 if (hasB) tma_load_u32(smem_u32(A + C::XSP), mb, bar, x0 + hoff - shB, y0 + goff + r0);
                 tma_load_u32(smem_u32(A + 2 * C::XSP), &maps.g, bar, 0, y0 + r0);
+                if (withU) tma_load_u32(smem_u32(A + 2 * C::XSP + C::GSP), &maps.u, bar, x0, y0 + goff + r0);
             }
         }
     } else {
@@ -237,7 +254,8 @@ __global__ void __launch_bounds__(TX + 32, band_minb<W>()) band_kernel(BandArgs 
 
         for (int k = 0; k < nch; ++k) {
             const int sl = k % NS;
-            double* A = sm + sl * C::STAGE;
+            double* A = sm + sl * STG;
+            const double* Us = A + 2 * C::XSP + C::GSP;  // MO-PCG: U at halo row rr, column c
             const double* Bs = A + C::XSP;
             const double* G = A + 2 * C::XSP;
             const int r0 = k * CH;
@@ -312,9 +330,16 @@ __global__ void __launch_bounds__(TX + 32, band_minb<W>()) band_kernel(BandArgs 
                         for (int tt = 0; tt < T; ++tt) y[tt] = fma(q, h[tt][e], y[tt]);
                     }
                     if constexpr (mode == LD_PCG) {
-                        // this thread's column of the new direction, interior rows only
+                        // this thread's column of the new direction, interior rows only; the
+                        // previous iteration's U += alpha Q (solvers.py:432) rides along: Q_prev
+                        // is already in shared memory, so it costs only U's read and write
                         const int gr = y0 + goff + r0 + rr;
-                        if (gr >= y0 && gr < y0 + rows_here && col_ok) Qcur[(size_t)gr * a.ldq + gc] = cen[u];
+                        if (gr >= y0 && gr < y0 + rows_here && col_ok) {
+                            Qcur[(size_t)gr * a.ldq + gc] = cen[u];
+                            if (upd)  // U's rows arrive with the halo (TMA), U += alpha_prev Q_prev
+                                a.U[(size_t)gr * a.ldq + gc] =
+                                    __dadd_rn(Us[rr * TX + c], __dmul_rn(alpha_prev, Bs[rr * HCB + shA + c + (W - 1) / 2]));
+                        }
                     }
                     // scatter: the row's T*W left coefficients are contiguous (pairs may
                     // straddle two terms), G[rr][tt*W + d] multiplies Y_tt into output row r - d
@@ -399,7 +424,7 @@ __global__ void __launch_bounds__(TX + 32, band_minb<W>()) band_kernel(BandArgs 
 template <int T, int W, int MODE>
 int launch_twm(const BandArgs& a, cudaStream_t stream) {
     using C = BandCfg<T, W>;
-    constexpr int smem = C::SMEM;
+    constexpr int smem = band_smem<T, W, MODE>();
     SFB_TRY(ensure_dynamic_smem(band_kernel<T, W, MODE>, smem));
     // tensor maps of the inputs (zero fill outside each source's extents)
     BandMaps maps;
@@ -426,6 +451,12 @@ int launch_twm(const BandArgs& a, cudaStream_t stream) {
         const cuuint64_t dims[2] = {(cuuint64_t)C::TWP, (cuuint64_t)a.gskew_rows};
         const cuuint32_t gbox[2] = {(cuuint32_t)C::TWP, (cuuint32_t)C::CH};
         SFB_TRY(tma_make_map(&maps.g, a.gskew, 2, dims, C::TWP, gbox, CU_TENSOR_MAP_SWIZZLE_NONE));
+    }
+    if (a.ld_mode == LD_PCG) {
+        if (a.U == nullptr) return arg_error("banded kernel: the MO-PCG pass needs U");
+        const cuuint64_t dims[2] = {(cuuint64_t)a.out_cols, (cuuint64_t)a.out_rows};
+        const cuuint32_t ubox[2] = {(cuuint32_t)TX, (cuuint32_t)C::CH};
+        SFB_TRY(tma_make_map(&maps.u, a.U, 2, dims, a.ldq, ubox, CU_TENSOR_MAP_SWIZZLE_NONE));
     }
     int ry, nrb;
     band_geometry(a.out_rows, a.out_cols, band_minb<W>(), &ry, &nrb);

@@ -72,6 +72,7 @@ struct BandArgs {
     double* Q0 = nullptr;  // PCG direction double buffer
     double* Q1 = nullptr;
     int ldq = 0;
+    double* U = nullptr;   // PCG: the iterate, receives the deferred U += alpha_{s-1} Q_{s-1} (ld = ldq)
     double c = 0.0;        // heat source scale / DIB tau*rho
     int rs = 0, cs = 0;    // heat: full-grid offset of the interior state
     int species = 0;
@@ -101,11 +102,16 @@ int launch_pcg_direction(const double* Z, double* Q0, double* Q1, int ld, int ro
                          PcgState* st, cudaStream_t s);
 int launch_pcg_dots(const double* W, const double* Q0, const double* Q1, int ld, int rows, int cols,
                     double* partials, PcgState* st, cudaStream_t s);
+int launch_pcg_rupdate(double* R, const double* W, int ld, int rows, double* partials, PcgState* st, double* hist,
+                       double* incs, cudaStream_t s);
+int launch_pcg_ufinal(double* U, const double* Q0, const double* Q1, int ld, int rows, PcgState* st,
+                      cudaStream_t s);
 int launch_pcg_update(double* U, double* R, const double* W, const double* Q0, const double* Q1, int ld,
                       int rows, int cols, double* partials, PcgState* st, double* hist, double* incs,
                       cudaStream_t s);
+// Q0/Q1 non-null: add the deferred alpha Q of the banded iteration to the record
 int launch_pcg_record(const double* U, int ld, int rows, int cols, double* iterates, PcgState* st,
-                      cudaStream_t s);
+                      cudaStream_t s, const double* Q0 = nullptr, const double* Q1 = nullptr);
 int launch_copy_dot(const double* R, double* Z, int ld, int rows, int cols, double* partials,
                     PcgState* st, RedSlots* red, cudaStream_t s);
 int launch_loop_ctl(PcgState* st, unsigned long long handle, int use_handle, cudaStream_t s);

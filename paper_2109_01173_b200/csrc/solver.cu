@@ -340,9 +340,11 @@ int pcg_enqueue_iteration(sfb_pcg* s, double* iterates) {
         a.ldw = s->ld;
         a.partials = s->partials;
         a.pcg = s->st;
+        a.U = s->U;  // receives the previous iteration's deferred U += alpha Q
         SFB_TRY(launch_band(a, st));
-        SFB_TRY(launch_pcg_update(s->U, s->R, s->W, s->Q0, s->Q1, s->ld, s->qy, s->qx, s->partials, s->st,
-                                  s->hist, s->incs, st));
+        SFB_TRY(launch_pcg_rupdate(s->R, s->W, s->ld, s->qy, s->partials, s->st, s->hist, s->incs, st));
+        if (iterates != nullptr)
+            SFB_TRY(launch_pcg_record(s->U, s->ld, s->qy, s->qx, iterates, s->st, st, s->Q0, s->Q1));
     } else {
         // dense operator: single direction buffer updated in place
         SFB_TRY(launch_pcg_direction(s->Z, s->Q0, s->Q0, s->ld, s->qy, s->qx, s->st, st));
@@ -365,8 +367,8 @@ int pcg_enqueue_iteration(sfb_pcg* s, double* iterates) {
         SFB_TRY(launch_pcg_dots(s->W, s->Q0, s->Q0, s->ld, s->qy, s->qx, s->partials, s->st, st));
         SFB_TRY(launch_pcg_update(s->U, s->R, s->W, s->Q0, s->Q0, s->ld, s->qy, s->qx, s->partials, s->st,
                                   s->hist, s->incs, st));
+        if (iterates != nullptr) SFB_TRY(launch_pcg_record(s->U, s->ld, s->qy, s->qx, iterates, s->st, st));
     }
-    if (iterates != nullptr) SFB_TRY(launch_pcg_record(s->U, s->ld, s->qy, s->qx, iterates, s->st, st));
     return pre_apply_impl(s->pre, s->R, s->ld, s->Z, s->ld, s->T1, s->ldt1, s->T2, s->ldt2, s->partials, s->st,
                           nullptr, &s->gw, st);
 }
@@ -1019,6 +1021,9 @@ int sfb_pcg_solve(sfb_pcg* s, const double* rhs, int ldr, const double* u0, int 
             if (cur.status != SFB_PCG_RUNNING || cur.iter >= max_iter) break;
         }
     }
+    // the banded iteration defers U += alpha Q into the next operator pass:
+    // apply the last completed iteration's
+    if (!s->op->dense) SFB_TRY(launch_pcg_ufinal(s->U, s->Q0, s->Q1, ld, qy, s->st, st));
     SFB_CUDA_TRY(cudaEventRecord(s->ev_t1, st));
     // outputs
     SFB_CUDA_TRY(cudaMemcpy2DAsync(U, (size_t)ldu * 8, s->U, (size_t)ld * 8, (size_t)qx * 8, qy,
@@ -1047,8 +1052,9 @@ int sfb_pcg_solve(sfb_pcg* s, const double* rhs, int ldr, const double* u0, int 
 
 // Device time of each pass of one MO-PCG iteration, launched `reps` times
 // back to back on the solver's stream over its own buffers (after a solve):
-// ms[0] banded operator pass (direction update + W = L(Q) + <W,Q>, |Q|^2),
-// ms[1] vector update pass (U, R, |R|), ms[2] preconditioner.  A scratch
+// ms[0] banded operator pass (direction update + W = L(Q) + <W,Q>, |Q|^2 +
+// the deferred U += alpha Q), ms[1] vector update pass (R, |R|), ms[2]
+// preconditioner.  A scratch
 // state keeps the gates open; the solver's buffers are clobbered (the next
 // solve re-initialises them).
 int sfb_pcg_shape(const sfb_pcg* s, int* qy, int* qx) {
@@ -1097,9 +1103,10 @@ int sfb_pcg_pass_times(sfb_pcg* s, int reps, double* ms) {
     a.ldw = s->ld;
     a.partials = s->partials;
     a.pcg = ps;
+    a.U = s->U;
     auto band = [&]() { return launch_band(a, st); };
-    auto update = [&]() {
-        return launch_pcg_update(s->U, s->R, s->W, s->Q0, s->Q1, s->ld, s->qy, s->qx, s->partials, ps, hist, incs, st);
+    auto update = [&]() {  // the banded iteration's update pass: R only (U rides in the operator pass)
+        return launch_pcg_rupdate(s->R, s->W, s->ld, s->qy, s->partials, ps, hist, incs, st);
     };
     auto pre = [&]() {
         return pre_apply_impl(s->pre, s->R, s->ld, s->Z, s->ld, s->T1, s->ldt1, s->T2, s->ldt2, s->partials, ps,

@@ -92,6 +92,64 @@ __global__ void __launch_bounds__(VT) pcg_update_kernel(double* __restrict__ U, 
     }
 }
 
+// R -= alpha W, |R|^2 and the stop test: the update pass of the banded
+// iteration, whose U += alpha Q is deferred into the next banded operator
+// pass (it re-reads Q there anyway) and, after the last iteration, into
+// pcg_ufinal_kernel.  Same arithmetic as pcg_update_kernel.
+__global__ void __launch_bounds__(VT) pcg_rupdate_kernel(double* __restrict__ R, const double* __restrict__ W,
+                                                         int ld, int rows, double* partials, PcgState* st,
+                                                         double* hist, double* incs) {
+    SFB_PDL_PROLOGUE();
+    if (st->status != SFB_PCG_RUNNING) return;
+    const double alpha = st->alpha;
+    double rr = 0.0;
+    const size_t n2 = (size_t)rows * ld / 2;
+    double2* R2 = reinterpret_cast<double2*>(R);
+    const double2* W2 = reinterpret_cast<const double2*>(W);
+    #pragma unroll 4
+    for (size_t i = (size_t)blockIdx.x * VT + threadIdx.x; i < n2; i += (size_t)gridDim.x * VT) {
+        const double2 wv = __ldg(W2 + i);
+        double2 rv = R2[i];
+        rv.x = __dsub_rn(rv.x, __dmul_rn(alpha, wv.x));  // R -= alpha W
+        rv.y = __dsub_rn(rv.y, __dmul_rn(alpha, wv.y));
+        R2[i] = rv;
+        rr = fma(rv.x, rv.x, rr);
+        rr = fma(rv.y, rv.y, rr);
+    }
+    __shared__ double sh[VT / 32];
+    const double p = block_sum<VT>(rr, sh);
+    if (threadIdx.x == 0) partials[blockIdx.x] = p;
+    if (arrive_last(&st->counter[1], gridDim.x)) {
+        const double tot = sum_partials<VT>(partials, gridDim.x, 1, sh);
+        if (threadIdx.x == 0) {
+            st->counter[1] = 0;
+            pcg_finish_update(st, tot, hist, incs);
+        }
+    }
+}
+
+// The last completed iteration's deferred U += alpha Q (after the loop).  No
+// pending update after INDEFINITE (that operator pass already applied it) or
+// NONFINITE (the solve raises).
+__global__ void __launch_bounds__(VT) pcg_ufinal_kernel(double* __restrict__ U, const double* Q0, const double* Q1,
+                                                        int ld, int rows, const PcgState* st) {
+    SFB_PDL_PROLOGUE();
+    const int n = st->iter;
+    if (n < 1 || st->status == SFB_PCG_INDEFINITE || st->status == SFB_PCG_NONFINITE) return;
+    const double alpha = st->alpha;
+    const double* Q = ((n - 1) & 1) ? Q1 : Q0;
+    const size_t n2 = (size_t)rows * ld / 2;
+    double2* U2 = reinterpret_cast<double2*>(U);
+    const double2* Q2 = reinterpret_cast<const double2*>(Q);
+    for (size_t i = (size_t)blockIdx.x * VT + threadIdx.x; i < n2; i += (size_t)gridDim.x * VT) {
+        const double2 q = __ldg(Q2 + i);
+        double2 u = U2[i];
+        u.x = __dadd_rn(u.x, __dmul_rn(alpha, q.x));  // U += alpha Q
+        u.y = __dadd_rn(u.y, __dmul_rn(alpha, q.y));
+        U2[i] = u;
+    }
+}
+
 __device__ __forceinline__ void pcg_finish_init(PcgState* st, double rr, double* hist) {
     const double res0 = sqrt(rr);
     st->res0 = res0;
@@ -197,14 +255,24 @@ __global__ void __launch_bounds__(VT) pcg_dots_kernel(const double* W, const dou
 }
 
 __global__ void __launch_bounds__(VT) pcg_record_kernel(const double* U, int ld, int rows, int cols,
-                                                        double* iterates, PcgState* st) {
+                                                        double* iterates, PcgState* st, const double* Q0,
+                                                        const double* Q1) {
     SFB_PDL_PROLOGUE();
-    // record_iterates (solvers.py:441-442): copy U_s once per completed iteration
+    // record_iterates (solvers.py:441-442): copy U_s once per completed iteration;
+    // with Q0 != nullptr (banded iteration) U still lacks the deferred
+    // alpha_{s-1} Q_{s-1}, which is added here with the same arithmetic
     const int it = st->iter;
     if (it >= st->n_iterates || st->recorded >= it) return;
     if (st->status == SFB_PCG_INDEFINITE || st->status == SFB_PCG_NONFINITE) return;
     double* dst = iterates + (size_t)it * rows * cols;
-    ROW_LOOP(rows, cols) dst[(size_t)r * cols + cc] = U[(size_t)r * ld + cc];
+    if (Q0 != nullptr && it >= 1) {
+        const double alpha = st->alpha;
+        const double* Q = ((it - 1) & 1) ? Q1 : Q0;
+        ROW_LOOP(rows, cols) dst[(size_t)r * cols + cc] =
+            __dadd_rn(U[(size_t)r * ld + cc], __dmul_rn(alpha, Q[(size_t)r * ld + cc]));
+    } else {
+        ROW_LOOP(rows, cols) dst[(size_t)r * cols + cc] = U[(size_t)r * ld + cc];
+    }
     if (arrive_last(&st->counter[5], gridDim.x)) {
         if (threadIdx.x == 0) {
             st->counter[5] = 0;
@@ -436,9 +504,22 @@ int launch_pcg_update(double* U, double* R, const double* W, const double* Q0, c
     return SFB_OK;
 }
 
+int launch_pcg_rupdate(double* R, const double* W, int ld, int rows, double* partials, PcgState* st, double* hist,
+                       double* incs, cudaStream_t s) {
+    SFB_TRY(launch_kernel(pcg_rupdate_kernel, dim3(VB), dim3(VT), 0, s, R, W, ld, rows, partials, st, hist, incs));
+    SFB_CHECK_LAUNCH();
+    return SFB_OK;
+}
+
+int launch_pcg_ufinal(double* U, const double* Q0, const double* Q1, int ld, int rows, PcgState* st, cudaStream_t s) {
+    SFB_TRY(launch_kernel(pcg_ufinal_kernel, dim3(VB), dim3(VT), 0, s, U, Q0, Q1, ld, rows, (const PcgState*)st));
+    SFB_CHECK_LAUNCH();
+    return SFB_OK;
+}
+
 int launch_pcg_record(const double* U, int ld, int rows, int cols, double* iterates, PcgState* st,
-                      cudaStream_t s) {
-    SFB_TRY(launch_kernel(pcg_record_kernel, dim3(VB), dim3(VT), 0, s, U, ld, rows, cols, iterates, st));
+                      cudaStream_t s, const double* Q0, const double* Q1) {
+    SFB_TRY(launch_kernel(pcg_record_kernel, dim3(VB), dim3(VT), 0, s, U, ld, rows, cols, iterates, st, Q0, Q1));
     SFB_CHECK_LAUNCH();
     return SFB_OK;
 }
