@@ -1,0 +1,12 @@
+#!/bin/bash
+# Round profiling recipe (run under gpurun from the repo root): the default
+# bench line, the ncu launch list of a short bench, and full captures of the
+# MO-PCG passes (DRAM traffic for bench's roofline_hbm.traffic).
+set -x
+python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
+SYLFEM_B200_GRAPH=chunked ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+  --log-file gpurun_out/launches.csv python bench.py --steps 1 --warmup 1 --iters-per-step 10 --no-full \
+  --no-cpu-baseline --no-e2e > gpurun_out/ncu_launch.log 2>&1
+ncu --set full --import-source on --clock-control none -k regex:"band_kernel|pcg_rupdate" -s 6 -c 2 \
+  -o gpurun_out/passes_full python tools/pass_probe.py 2048 identity cfg3 > gpurun_out/ncu_passes.log 2>&1
+tail -2 gpurun_out/bench.err
