@@ -138,6 +138,21 @@ def cpu_sample(N: int, iters: int):
     return q * r["iterations"] / r["wall"], r["wall"], setup, r["iterations"]
 
 
+def host_stack() -> str:
+    """numpy / scipy / BLAS of the host baseline (SURVEY §8 d protocol)."""
+    import scipy
+    blas = "BLAS unknown"
+    try:
+        from threadpoolctl import threadpool_info
+        for lib in threadpool_info():
+            if lib.get("user_api") == "blas":
+                blas = f"{lib.get('internal_api')} {lib.get('version')} ({lib.get('num_threads')} threads)"
+                break
+    except Exception:
+        pass
+    return f"numpy {np.__version__}, scipy {scipy.__version__}, {blas}"
+
+
 def cores() -> int:
     for k in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS"):
         if os.environ.get(k, "").isdigit():
@@ -177,7 +192,8 @@ def run_reference(args):
                    "iterations_per_step": per, "parallelism": "host BLAS threads"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores(), "kind": "port",
                          "sample": f"oracle restatement of sylfem mo_pcg (dense GEMM apply, LU preconditioner), "
-                                   f"{per} iterations per step on the cfg3 step-0 system, setup excluded"},
+                                   f"{per} iterations per step on the cfg3 step-0 system, setup excluded",
+                         "host_stack": host_stack()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -441,9 +457,13 @@ def run_native(args):
         v, wall, setup, n_it = cpu_sample(args.N, args.cpu_iters)
         cpu = {"value": v, "unit": UNIT, "cores": cores(), "kind": "port",
                "sample": f"oracle restatement of sylfem mo_pcg (dense GEMM apply + LU preconditioner) on the "
-                         f"same cfg3 system, {n_it} iterations ({wall:.1f} s), setup {setup:.1f} s excluded"}
+                         f"same cfg3 system, {n_it} iterations ({wall:.1f} s), setup {setup:.1f} s excluded",
+               "host_stack": host_stack()}
 
-    per_step_launches = 3 + (5 if not op.banded else 3 + n_gemm_per_iter) * K_it
+    # per solve: init + first preconditioner (+ the deferred-U fixup of the banded
+    # iteration); per iteration: operator pass(es), update, preconditioner, loop control
+    n_pre = n_gemm_per_iter if n_gemm_per_iter else 5  # banded: 3 SPIKE tile passes + 2 interface chains
+    per_step_launches = 1 + n_pre + (1 if op.banded else 0) + (3 + n_pre) * K_it
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
