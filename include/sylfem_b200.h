@@ -270,6 +270,13 @@ int sfb_vec_dots(const double* A_dev, const double* B_dev, const double* C_dev,
 int sfb_diff_norm(const double* A_dev, int lda, const double* B_dev, int ldb,
                   int rows, int cols, double* out4_host, void* stream);
 
+/* ---- trajectory frames (harness.py:475-491 write_pgm) --- */
+/* out_dev (rows x cols, contiguous) <- the 16-bit big-endian PGM pixels of
+ * A: min-max normalised per frame, rint((a - lo) / span * 65535), zeros for
+ * a frame constant up to roundoff; lohi_host (may be NULL) <- {min, max}. */
+int sfb_frame_pgm16(const double* A_dev, int lda, int rows, int cols,
+                    unsigned short* out_dev, double* lohi_host, void* stream);
+
 /* ---- sparse vec-form matrices for the Kronecker cross-check path
  *      (operators.py:141-155 to_kronecker; vector_pcg, solvers.py:456-517) */
 /* K (n x n) in CSR from host arrays: indptr n+1 (int64), indices nnz (int32,

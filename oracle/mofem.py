@@ -27,7 +27,7 @@ __all__ = [
     "apply_terms", "precond_factors", "LUPrecond", "spectral_cache",
     "reduced_solve", "mo_pcg", "imex_heat", "imex_rds", "dib_params",
     "dib_rates", "initial_fields", "full_node_grid", "expand_full",
-    "interior", "seeded_modes", "OracleError",
+    "interior", "seeded_modes", "OracleError", "pgm_bytes", "csv_text",
 ]
 
 DIRICHLET, NEUMANN = "dirichlet", "neumann"
@@ -645,3 +645,38 @@ def seeded_modes(seed, n_modes=8):
     b = rng.integers(1, 17, n_modes)
     c = rng.standard_normal(n_modes)
     return a, b, c
+
+
+# ---------------------------------------------------------------------------
+# trajectory outputs (harness.py:424-491)
+# ---------------------------------------------------------------------------
+
+def pgm_bytes(array):
+    """File bytes of harness.write_pgm (harness.py:475-491)."""
+    a = np.asarray(array, dtype=float)
+    lo, hi = float(np.min(a)), float(np.max(a))
+    span = hi - lo
+    if span > max(1e-12 * max(abs(hi), abs(lo)), 1e-14):
+        scaled = np.round((a - lo) / span * 65535.0)
+    else:
+        scaled = np.zeros_like(a)
+    return f"P5\n{a.shape[1]} {a.shape[0]}\n65535\n".encode() + scaled.astype(">u2").tobytes()
+
+
+def csv_text(header, rows):
+    """File text of harness.write_csv (harness.py:424-440): CRLF rows, repr floats."""
+    import csv as _csv
+    import io as _io
+
+    def fmt(v):
+        if isinstance(v, (float, np.floating)):
+            return repr(float(v))
+        if isinstance(v, (int, np.integer)):
+            return str(int(v))
+        return str(v)
+    buf = _io.StringIO(newline="")
+    w = _csv.writer(buf)
+    w.writerow(header)
+    for row in rows:
+        w.writerow([fmt(v) for v in row])
+    return buf.getvalue()

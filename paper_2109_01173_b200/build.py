@@ -18,7 +18,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(HERE, "csrc", "_obj")
 LIB = os.path.join(HERE, "libsylfem_b200.so")
-SOURCES = ["gemm_dmma.cu", "banded.cu", "vector.cu", "spike.cu", "sparse.cu", "solver.cu", "imex.cu"]
+SOURCES = ["gemm_dmma.cu", "banded.cu", "vector.cu", "spike.cu", "sparse.cu", "solver.cu", "imex.cu", "frames.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
 
