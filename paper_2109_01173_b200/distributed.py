@@ -75,19 +75,38 @@ class Layout:
 class Comm:
     """Collectives of the sharded iteration over torch.distributed."""
 
-    def __init__(self, layout: Layout, device, group=None):
+    def __init__(self, layout: Layout, device, group=None, ranks=None):
+        """``ranks``: the global ranks of ``group`` in group order (point-to-point
+        peers are addressed by global rank); default: the default group."""
         import torch
         import torch.distributed as dist
         self.t, self.dist = torch, dist
         self.L = layout
         self.device = device
         self.group = group
+        self.ranks = list(ranks) if ranks is not None else list(range(layout.world))
 
     def allreduce(self, vals):
         t = self.t.tensor(vals, dtype=self.t.float64, device=self.device)
         if self.L.world > 1:
             self.dist.all_reduce(t, group=self.group)
         return [float(v) for v in t.tolist()]
+
+    def sendrecv(self, X, peer: int):
+        """Swap X with the rank ``peer`` (global rank, default group)."""
+        recv = self.t.empty_like(X)
+        ops = [self.dist.P2POp(self.dist.isend, X.contiguous(), peer),
+               self.dist.P2POp(self.dist.irecv, recv, peer)]
+        for req in self.dist.batch_isend_irecv(ops):
+            req.wait()
+        return recv
+
+    def gather_world(self, vals):
+        """All-gather of a few scalars per rank over the default group."""
+        t = self.t.tensor(vals, dtype=self.t.float64, device=self.device)
+        out = [self.t.empty_like(t) for _ in range(self.dist.get_world_size())]
+        self.dist.all_gather(out, t)
+        return [o.tolist() for o in out]
 
     def halo(self, X, b: int):
         """q_y x (n + 2b) block: left halo | X | right halo (zeros at the domain ends)."""
@@ -104,11 +123,13 @@ class Comm:
         lrecv = t.empty((qy, b), dtype=X.dtype, device=X.device)
         rrecv = t.empty((qy, b), dtype=X.dtype, device=X.device)
         if left >= 0:
-            ops.append(self.dist.P2POp(self.dist.isend, X[:, :b].contiguous(), left, group=self.group))
-            ops.append(self.dist.P2POp(self.dist.irecv, lrecv, left, group=self.group))
+            peer = self.ranks[left]
+            ops.append(self.dist.P2POp(self.dist.isend, X[:, :b].contiguous(), peer, group=self.group))
+            ops.append(self.dist.P2POp(self.dist.irecv, lrecv, peer, group=self.group))
         if right < L.world:
-            ops.append(self.dist.P2POp(self.dist.isend, X[:, n - b:].contiguous(), right, group=self.group))
-            ops.append(self.dist.P2POp(self.dist.irecv, rrecv, right, group=self.group))
+            peer = self.ranks[right]
+            ops.append(self.dist.P2POp(self.dist.isend, X[:, n - b:].contiguous(), peer, group=self.group))
+            ops.append(self.dist.P2POp(self.dist.irecv, rrecv, peer, group=self.group))
         for req in self.dist.batch_isend_irecv(ops):
             req.wait()
         if left >= 0:
@@ -626,7 +647,7 @@ class CudaShardedDibStepper:
     (block operator, inverse-form DMMA preconditioner, vector passes) and the
     block DIB rhs map, all through the C ABI."""
 
-    def __init__(self, x, y, d_u, d_v, tau, rho, kinetics, inner, lumped, layout: Layout):
+    def __init__(self, x, y, d_u, d_v, tau, rho, kinetics, inner, lumped, layout: Layout, species=(0, 1)):
         from .models import DIBKinetics
         from .operators import parabolic_operator
         from .timestepping import _parabolic_precond
@@ -638,11 +659,12 @@ class CudaShardedDibStepper:
         self.L = layout
         self.tau_rho = tau * rho
         self.kp = np.ascontiguousarray(kinetics.params.device_params(), dtype=float)
-        self.backends = []
-        for d in (d_u, d_v):
+        self.backends = [None, None]
+        for sp, d in enumerate((d_u, d_v)):
             op, rhs_of = parabolic_operator(x, y, d, tau, lumped=lumped)
-            pre = _parabolic_precond(x, y, d, tau, lumped, inner, op)
-            self.backends.append(CudaBackend(op, pre, layout))
+            if sp in species:
+                pre = _parabolic_precond(x, y, d, tau, lumped, inner, op)
+                self.backends[sp] = CudaBackend(op, pre, layout)
         w, goff, g, hoff, h = rhs_of.layout()
         self.b = max(0, -hoff, hoff + w - 1)
         n = layout.n
@@ -653,14 +675,17 @@ class CudaShardedDibStepper:
                                            nat.host_ptr(hl), nat.C.byref(out)), "block rhs map")
         self._map = nat.Handle(out.value, nat.lib().sfb_map_destroy)
 
+    def _be(self):
+        return self.backends[0] if self.backends[0] is not None else self.backends[1]
+
     def to_local(self, a):
         L = self.L
         if nat.is_device(a):
-            return self.backends[0].from_host(a[:, L.c0:L.c0 + L.n])
-        return self.backends[0].from_host(np.asarray(a, dtype=float)[:, L.c0:L.c0 + L.n])
+            return self._be().from_host(a[:, L.c0:L.c0 + L.n])
+        return self._be().from_host(np.asarray(a, dtype=float)[:, L.c0:L.c0 + L.n])
 
     def rhs(self, species, extU, extV):
-        be = self.backends[0]
+        be = self._be()
         U, V = extU.contiguous(), extV.contiguous()
         out = be.zeros(self.L.qy, self.L.n)
         chk = np.zeros(2)
@@ -740,3 +765,136 @@ def sharded_imex_rds(domain, x, y, d_u: float, d_v: float, kinetics, rho: float,
     return Trajectory(final=(st.host(S[0]), st.host(S[1])), increments=incs, iterations=iters,
                       times=(1 + np.arange(n)) * tau, steady_step=steady, snapshots=snaps,
                       diagnostics={"world": L.world, "columns": (L.c0, L.c0 + L.n)})
+
+
+# =========================================================================
+# Species groups x column shards (cfg5 at 4 / 8 GPUs, SURVEY §8 e)
+# =========================================================================
+#
+# World 2G: ranks [0, G) solve species u, ranks [G, 2G) species v, each group
+# column-sharded over its G ranks with identical layouts, so rank r's
+# partner r +- G owns the same columns of the other species.  Per step:
+#
+#   1. halo of the own species inside the group; the halo-extended block is
+#      swapped with the partner (one send/recv of q x (n + 2b) doubles): the
+#      pointwise DIB kinetics of the rhs need both species at the same nodes;
+#   2. the rhs blow-up checks of both species, all-gathered over the world
+#      (one tiny collective), resolved in the reference's order;
+#   3. the own species' column-sharded MO-PCG inside the group;
+#   4. the solve outcomes and increment norms, all-gathered over the world,
+#      resolved in the reference's order (u rhs, u solve, v rhs, v solve).
+
+
+def _group_status(vals_by_rank, G, g):
+    """Rows of group g from an all-gathered status table."""
+    return vals_by_rank[g * G:(g + 1) * G]
+
+
+def grouped_imex_rds(domain, x, y, d_u: float, d_v: float, kinetics, rho: float, state0, grid, inner=None,
+                     lumped: bool = False, snapshot_every: int = 0, steady_eps: float = 1e-8, device=None,
+                     stepper_factory=None, comm_factory=None):
+    """imex_euler_rds (timestepping.py:162-220) with species g on the rank
+    group g (2 groups of G = world / 2 ranks), each column-sharded.  Returns
+    this rank's columns of both species (``final``, ``snapshots``,
+    ``BlowUpError.state``); increments, iteration counts and the steady step
+    are global and equal on all ranks.
+
+    ``stepper_factory(layout, species)`` / ``comm_factory(layout, group,
+    ranks)`` replace the CUDA stepper / torch.distributed collectives (tests)."""
+    import torch
+    import torch.distributed as dist
+
+    from .fem1d import BCKind
+    from .timestepping import BLOWUP_LIMIT, BlowUpError, InnerSolver, Trajectory, _step_setup
+    if d_u <= 0 or d_v <= 0 or rho <= 0:
+        raise ConfigError("d_u, d_v and rho must be positive")
+    if x.basis.bc is not BCKind.NEUMANN:
+        raise ConfigError("the reaction-diffusion stepper expects zero-flux BCs")
+    inner = inner or InnerSolver()
+    _step_setup(inner)
+    world, rank = dist.get_world_size(), dist.get_rank()
+    if world % 2:
+        raise ConfigError(f"species groups need an even number of ranks, got {world}")
+    G = world // 2
+    g, r = divmod(rank, G)
+    partner = (1 - g) * G + r
+    groups = [dist.new_group(list(range(k * G, (k + 1) * G))) for k in (0, 1)]
+    L = Layout(y.q, x.q, G, r)
+    device = device or ("cuda" if torch.cuda.is_available() else "cpu")
+    ranks = list(range(g * G, (g + 1) * G))
+    comm = comm_factory(L, groups[g], ranks) if comm_factory else Comm(L, device, group=groups[g], ranks=ranks)
+    tau = grid.tau
+    st = stepper_factory(L, g) if stepper_factory else \
+        CudaShardedDibStepper(x, y, d_u, d_v, tau, rho, kinetics, inner, lumped, L, species=(g,))
+    stop = inner.stopping(tau)
+    own = st.to_local(state0[g])
+    other = st.to_local(state0[1 - g])  # refreshed by the swap every step
+    n = grid.n_steps
+    incs = np.empty((n, 2))
+    iters = np.empty((n, 2), dtype=int)
+    snaps = []
+    steady = None
+    names = ("u", "v")
+
+    gather = comm.gather_world
+
+    def swap(ext):
+        return comm.sendrecv(ext, partner)
+
+    def centre(ext):
+        return ext[:, st.b:st.b + L.n]
+
+    def pair():
+        return (st.host(own), st.host(other)) if g == 0 else (st.host(other), st.host(own))
+
+    for k in range(n):
+        ext_own = comm.halo(own, st.b)
+        ext_other = swap(ext_own)
+        other = centre(ext_other).contiguous()
+        ext = (ext_own, ext_other) if g == 0 else (ext_other, ext_own)
+        rhs, chk = st.rhs(g, *ext)
+        tab = gather([chk[0], chk[1]])
+        rhs_bad = []
+        for sp in (0, 1):
+            rows = _group_status(tab, G, sp)
+            rhs_bad.append(max(v[0] for v in rows) > BLOWUP_LIMIT or sum(v[1] for v in rows) > 0)
+        # the reference checks u's rhs before anything else, v's rhs only after u's solve
+        if rhs_bad[0]:
+            raise BlowUpError(k, "u", pair())
+        ok, its, loc, new = 1.0, 0, [0.0, 0.0, 0.0, 0.0], None
+        if not rhs_bad[g]:
+            rep = sharded_mo_pcg(st.backends[g], comm, rhs, stop=stop, u0_local=own, max_iter=inner.max_iter,
+                                 keep_on_device=True)
+            ok, its, new = float(rep.stop_reason != "max_iter"), rep.iterations, rep.solution
+            if ok:
+                loc = st.norms(new, own)
+        tab = gather([ok, float(its), loc[0], loc[1], loc[2], loc[3]])
+        res = []
+        for sp in (0, 1):
+            rows = _group_status(tab, G, sp)
+            res.append({"ok": all(v[0] for v in rows), "its": int(rows[0][1]),
+                        "bad": sum(v[4] for v in rows) > 0 or max(v[3] for v in rows) > BLOWUP_LIMIT,
+                        "inc": math.sqrt(sum(v[2] for v in rows)), "nrm": math.sqrt(sum(v[5] for v in rows))})
+        for sp in (0, 1):  # u solve, v rhs, v solve
+            if sp == 1 and rhs_bad[1]:
+                raise BlowUpError(k, "v", pair())
+            if not res[sp]["ok"]:
+                raise SolverError(f"inner PCG did not converge in {inner.max_iter} iterations")
+            if res[sp]["bad"]:
+                raise BlowUpError(k, names[sp], pair())
+        incs[k] = (res[0]["inc"], res[1]["inc"])
+        iters[k] = (res[0]["its"], res[1]["its"])
+        own = new
+        if steady is None and np.all(incs[k] <= steady_eps * max(res[0]["nrm"], 1e-300)):
+            steady = k
+        last = k == n - 1
+        if (snapshot_every and ((k + 1) % snapshot_every == 0 or last)) or last:
+            other = centre(swap(comm.halo(own, st.b))).contiguous()
+            if snapshot_every and ((k + 1) % snapshot_every == 0 or last):
+                snaps.append((k + 1, *pair()))
+    fin = pair()
+    for pg in groups:
+        dist.destroy_process_group(pg)
+    return Trajectory(final=fin, increments=incs, iterations=iters, times=(1 + np.arange(n)) * tau,
+                      steady_step=steady, snapshots=snaps,
+                      diagnostics={"world": world, "species_group": g, "columns": (L.c0, L.c0 + L.n)})

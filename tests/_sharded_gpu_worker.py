@@ -22,9 +22,9 @@ class HostStagedComm:
     """Comm interface of distributed.sharded_mo_pcg over gloo: CUDA tensors
     are staged through host memory for each collective."""
 
-    def __init__(self, layout):
+    def __init__(self, layout, group=None, ranks=None):
         self.L = layout
-        self.inner = Comm(layout, "cpu")
+        self.inner = Comm(layout, "cpu", group=group, ranks=ranks)
 
     def allreduce(self, vals):
         return self.inner.allreduce(vals)
@@ -37,6 +37,12 @@ class HostStagedComm:
 
     def rowsT_to_colsT(self, XrT):
         return self.inner.rowsT_to_colsT(XrT.cpu()).to(XrT.device)
+
+    def sendrecv(self, X, peer):
+        return self.inner.sendrecv(X.cpu(), peer).to(X.device)
+
+    def gather_world(self, vals):
+        return self.inner.gather_world(vals)
 
 
 def problem(N):

@@ -16,7 +16,7 @@ import oracle as orc
 import paper_2109_01173_b200 as pb
 from _sharded_worker import NumpyBackend
 from _species_worker import case, oracle_kinetics
-from paper_2109_01173_b200.distributed import Comm, Layout, sharded_imex_rds
+from paper_2109_01173_b200.distributed import Comm, Layout, grouped_imex_rds, sharded_imex_rds
 
 
 class OracleShardedDib:
@@ -77,5 +77,31 @@ def worker(rank, world, port, mode, out_dir, N, steps):
                               inner=inner, lumped=True, snapshot_every=2, comm=comm, stepper=st)
         np.savez(os.path.join(out_dir, f"rank{rank}.npz"), U=tr.final[0], V=tr.final[1], iters=tr.iterations,
                  incs=tr.increments, snaps=[s[0] for s in tr.snapshots], c0=lay.c0)
+    finally:
+        dist.destroy_process_group()
+
+
+def grouped_worker(rank, world, port, mode, out_dir, N, steps):
+    """Species groups x column shards (world = 2G)."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        p, x, y, state0, tau = case(N)
+        inner = pb.InnerSolver(rule="residual", tol=1e-12, max_iter=2000)
+        if mode == "cpu":
+            kw = dict(device="cpu", stepper_factory=lambda L, g: OracleShardedDib(N, p, tau, L))
+            kin = None
+        else:
+            from _sharded_gpu_worker import HostStagedComm
+            torch.cuda.set_device(0)
+            kw = dict(device="cpu", comm_factory=lambda L, grp, ranks: HostStagedComm(L, grp, ranks))
+            kin = pb.dib_kinetics_pair(p)
+        tr = grouped_imex_rds(pb.SQUARE, x, y, 1.0, p.d_theta, kin, p.rho, state0, pb.TimeGrid(tau, steps * tau),
+                              inner=inner, lumped=True, snapshot_every=2, **kw)
+        c0, c1 = tr.diagnostics["columns"]
+        np.savez(os.path.join(out_dir, f"rank{rank}.npz"), U=tr.final[0], V=tr.final[1], iters=tr.iterations,
+                 incs=tr.increments, snaps=[s[0] for s in tr.snapshots], c0=c0, group=tr.diagnostics["species_group"],
+                 snapU=tr.snapshots[0][1], snapV=tr.snapshots[0][2])
     finally:
         dist.destroy_process_group()

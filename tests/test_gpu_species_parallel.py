@@ -57,3 +57,25 @@ def test_sharded_rds_cuda_matches_single_gpu_driver(world):
         assert list(r["snaps"]) == [s[0] for s in ref.snapshots]
     assert relerr(U, ref.final[0]) <= 1e-10
     assert relerr(V, ref.final[1]) <= 1e-10
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_grouped_species_sharded_cuda_matches_single_gpu_driver(world):
+    from _sharded_rds_worker import grouped_worker
+    N, steps = 15, 4
+    d = tempfile.mkdtemp()
+    mp.spawn(grouped_worker, args=(world, free_port(), "cuda", d, N, steps), nprocs=world, join=True)
+    parts = [dict(np.load(os.path.join(d, f"rank{r}.npz"))) for r in range(world)]
+    p, x, y, state0, tau = case(N)
+    ref = pb.imex_euler_rds(pb.SQUARE, x, y, 1.0, p.d_theta, pb.dib_kinetics_pair(p), p.rho, state0,
+                            pb.TimeGrid(tau, steps * tau),
+                            inner=pb.InnerSolver(rule="residual", tol=1e-12, max_iter=2000), lumped=True,
+                            snapshot_every=2)
+    for r in parts:
+        assert np.all(np.abs(r["iters"] - ref.iterations) <= 1)
+        assert np.allclose(r["incs"], ref.increments, rtol=1e-8)
+    for grp in (0, 1):
+        mine = sorted((r for r in parts if int(r["group"]) == grp), key=lambda r: int(r["c0"]))
+        U = np.concatenate([r["U"] for r in mine], axis=1)
+        V = np.concatenate([r["V"] for r in mine], axis=1)
+        assert relerr(U, ref.final[0]) <= 1e-10 and relerr(V, ref.final[1]) <= 1e-10
