@@ -234,7 +234,13 @@ def run_native(args):
         lay = Layout(qy, qx, world, rank)
         backend = CudaBackend(op, pre, lay)
         comm = Comm(lay, torch.device("cuda", local))
-        peer = PeerTransposes(lay, backend, sync="stream") if args.transposes == "peer" else None
+        peer = None
+        if args.transposes == "peer":
+            try:  # CUDA IPC between the ranks' GPUs; NCCL all-to-alls when peer mappings are unavailable
+                peer = PeerTransposes(lay, backend, sync="stream")
+            except Exception as exc:  # noqa: BLE001
+                log(f"peer transposes unavailable ({exc}); using NCCL all-to-alls")
+                args.transposes = "nccl"
         rhs_d = rhs_d[:, lay.c0:lay.c0 + lay.n].contiguous()
         w.rhs = np.ascontiguousarray(w.rhs[:, lay.c0:lay.c0 + lay.n])
 
