@@ -64,16 +64,23 @@ template <int W>
 constexpr int band_minb() { return W >= 7 ? 2 : BAND_MINB; }
 constexpr int RY_MIN = 32;
 
-template <int W>
+// Ring shape: NS stages of chunk_rows<W>() rows, or with FINE (MO-PCG pass of
+// narrow operators on short strips) 4 stages of W rows: the first rows land
+// sooner and the last chunk is shorter, which measured 44.0 -> 41.6 us at
+// q = 2047 (114 rows per CTA) and 144 -> 149 us at q = 4095 (455 rows).
+constexpr int FINE_NS = 4;
+constexpr int FINE_MAX_ROWS = 160;  // rows per CTA up to which the fine ring is used
+template <int W, bool FINE>
 __host__ __device__ constexpr int chunk_rows() {
-    return W * (W >= 8 ? 1 : (8 + W - 1) / W);  // a multiple of W (static ring slots), >= 8
+    return FINE ? W : W * (W >= 8 ? 1 : (8 + W - 1) / W);  // a multiple of W (static ring slots)
 }
 
 __host__ __device__ constexpr int pad128(int doubles) { return (doubles + 15) / 16 * 16; }
 
-template <int T, int W>
+template <int T, int W, bool FINE = false>
 struct BandCfg {
-    static constexpr int CH = chunk_rows<W>();
+    static constexpr int NS = FINE ? FINE_NS : ::sfb::NS;
+    static constexpr int CH = chunk_rows<W, FINE>();
     static constexpr int HC = TX + W - 1;    // halo columns
     static constexpr int HCB = HC + 2;       // box columns: boxes start at an even column (16-byte rows)
     static constexpr int TWP = (T * W + 1) / 2 * 2;  // a row's T*W left coefficients, padded to pairs
@@ -86,10 +93,14 @@ struct BandCfg {
     static constexpr int SMEM = NS * STAGE * 8 + 128;
     static constexpr int SMEM_PCG = NS * (STAGE + USP) * 8 + 128;
 };
-template <int T, int W, int MODE>
-__host__ __device__ constexpr int band_stage() { return BandCfg<T, W>::STAGE + (MODE == LD_PCG ? BandCfg<T, W>::USP : 0); }
-template <int T, int W, int MODE>
-__host__ __device__ constexpr int band_smem() { return MODE == LD_PCG ? BandCfg<T, W>::SMEM_PCG : BandCfg<T, W>::SMEM; }
+template <int T, int W, int MODE, bool FINE>
+__host__ __device__ constexpr int band_stage() {
+    return BandCfg<T, W, FINE>::STAGE + (MODE == LD_PCG ? BandCfg<T, W, FINE>::USP : 0);
+}
+template <int T, int W, int MODE, bool FINE>
+__host__ __device__ constexpr int band_smem() {
+    return MODE == LD_PCG ? BandCfg<T, W, FINE>::SMEM_PCG : BandCfg<T, W, FINE>::SMEM;
+}
 
 struct BandMaps {
     CUtensorMap a;       // input A (X / Z / U / eta), box {HCB, CH}
@@ -109,11 +120,11 @@ __host__ inline void band_geometry(int rows, int cols, int minb, int* ry, int* n
 }
 
 // MODE = the loader (LD_*); the MO-PCG loader always comes with the MO-PCG epilogue.
-template <int T, int W, int MODE>
+template <int T, int W, int MODE, bool FINE>
 __global__ void __launch_bounds__(TX + 32, band_minb<W>()) band_kernel(BandArgs a, const __grid_constant__ BandMaps maps, int ry) {
     SFB_PDL_PROLOGUE();
-    using C = BandCfg<T, W>;
-    constexpr int CH = C::CH, HCB = C::HCB, TWP = C::TWP;
+    using C = BandCfg<T, W, FINE>;
+    constexpr int CH = C::CH, HCB = C::HCB, TWP = C::TWP, NS = C::NS;
     constexpr int NPAIR = HCB / 2;           // HCB is even (W odd)
     constexpr int NPP = (NPAIR + 63) / 64;   // column pairs per thread in the transform
     constexpr int NRR = (CH + 1) / 2;        // rows per thread and chunk in the transform
@@ -161,7 +172,7 @@ __global__ void __launch_bounds__(TX + 32, band_minb<W>()) band_kernel(BandArgs 
     // A's box starts at full-grid column x0 + hoff - shA (U column minus acs), B's at x0 + hoff - shB;
     // both even, so every box row is 16-byte aligned in global memory
     const int shA = (hoff - acs) & 1, shB = hoff & 1;
-    constexpr int STG = band_stage<T, W, MODE>();  // doubles per ring stage
+    constexpr int STG = band_stage<T, W, MODE, FINE>();  // doubles per ring stage
     // MO-PCG from the second iteration on: U's rows ride in the ring too
     const bool withU = mode == LD_PCG && hasB;
     const uint32_t tx_bytes = (uint32_t)((hasB ? 2 : 1) * C::XS + C::GS + (withU ? CH * TX : 0)) * 8;
@@ -421,11 +432,11 @@ __global__ void __launch_bounds__(TX + 32, band_minb<W>()) band_kernel(BandArgs 
     }
 }
 
-template <int T, int W, int MODE>
-int launch_twm(const BandArgs& a, cudaStream_t stream) {
-    using C = BandCfg<T, W>;
-    constexpr int smem = band_smem<T, W, MODE>();
-    SFB_TRY(ensure_dynamic_smem(band_kernel<T, W, MODE>, smem));
+template <int T, int W, int MODE, bool FINE>
+int launch_twmf(const BandArgs& a, int ry, int nrb, cudaStream_t stream) {
+    using C = BandCfg<T, W, FINE>;
+    constexpr int smem = band_smem<T, W, MODE, FINE>();
+    SFB_TRY(ensure_dynamic_smem(band_kernel<T, W, MODE, FINE>, smem));
     // tensor maps of the inputs (zero fill outside each source's extents)
     BandMaps maps;
     std::memset(&maps, 0, sizeof(maps));
@@ -458,12 +469,22 @@ int launch_twm(const BandArgs& a, cudaStream_t stream) {
         const cuuint32_t ubox[2] = {(cuuint32_t)TX, (cuuint32_t)C::CH};
         SFB_TRY(tma_make_map(&maps.u, a.U, 2, dims, a.ldq, ubox, CU_TENSOR_MAP_SWIZZLE_NONE));
     }
-    int ry, nrb;
-    band_geometry(a.out_rows, a.out_cols, band_minb<W>(), &ry, &nrb);
     dim3 grid((a.out_cols + TX - 1) / TX, nrb);
-    SFB_TRY(launch_kernel(band_kernel<T, W, MODE>, grid, dim3(NTH), smem, stream, a, maps, ry));
+    SFB_TRY(launch_kernel(band_kernel<T, W, MODE, FINE>, grid, dim3(NTH), smem, stream, a, maps, ry));
     SFB_CHECK_LAUNCH();
     return SFB_OK;
+}
+
+template <int T, int W, int MODE>
+int launch_twm(const BandArgs& a, cudaStream_t stream) {
+    int ry, nrb;
+    band_geometry(a.out_rows, a.out_cols, band_minb<W>(), &ry, &nrb);
+    if constexpr (MODE == LD_PCG && W <= 5) {
+        // 2 CTAs/SM must still fit: 4 stages of W rows (+ U) is < 110 KB for W <= 5
+        static_assert(band_smem<T, W, MODE, true>() <= 110 * 1024, "fine ring too large for 2 CTAs/SM");
+        if (ry <= FINE_MAX_ROWS) return launch_twmf<T, W, MODE, true>(a, ry, nrb, stream);
+    }
+    return launch_twmf<T, W, MODE, false>(a, ry, nrb, stream);
 }
 
 template <int T, int W>
