@@ -270,6 +270,17 @@ int sfb_vec_dots(const double* A_dev, const double* B_dev, const double* C_dev,
 int sfb_diff_norm(const double* A_dev, int lda, const double* B_dev, int ldb,
                   int rows, int cols, double* out4_host, void* stream);
 
+/* ---- spectral setup (solvers.py:256-281 build_spectral_cache) --------- */
+/* Generalized SPD eigendecomposition A v = lam B v (scipy.linalg.eigh(A, B)
+ * of the reference, LAPACK dsygvd) on the device: cuSOLVER potrf + syevd,
+ * cuBLAS trsm; eigenvalues ascending into lam_host (q), B-orthonormal
+ * eigenvectors as the columns of V_dev (q x q row-major, ldv), each
+ * column's largest-magnitude entry positive (solvers.py:203-208).  A and B
+ * (symmetric) may be host or device memory.  SFB_ERR_ARG when B is not
+ * positive definite (the caller then tries the other term order). */
+int sfb_geigh(int q, const double* A, int lda, const double* B, int ldb,
+              double* lam_host, double* V_dev, int ldv, void* stream);
+
 /* ---- trajectory frames (harness.py:475-491 write_pgm) --- */
 /* out_dev (rows x cols, contiguous) <- the 16-bit big-endian PGM pixels of
  * A: min-max normalised per frame, rint((a - lo) / span * 65535), zeros for

@@ -18,7 +18,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(HERE, "csrc", "_obj")
 LIB = os.path.join(HERE, "libsylfem_b200.so")
-SOURCES = ["gemm_dmma.cu", "banded.cu", "vector.cu", "spike.cu", "sparse.cu", "solver.cu", "imex.cu", "frames.cu"]
+SOURCES = ["gemm_dmma.cu", "banded.cu", "vector.cu", "spike.cu", "sparse.cu", "solver.cu", "imex.cu", "frames.cu", "eigen.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
 
@@ -60,7 +60,7 @@ def build(force: bool = False, verbose: bool = False, lib: str = LIB, obj: str =
     with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as pool:
         objs = list(pool.map(compile_one, SOURCES))
     if force or _stale(lib, objs):
-        cmd = [nvcc, *ARCH, "-shared", "-o", lib, *objs, "-cudart", "static"]
+        cmd = [nvcc, *ARCH, "-shared", "-o", lib, *objs, "-cudart", "static", "-ldl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

@@ -511,19 +511,21 @@ def _dense_device(m):
 
 
 def _geigh_device(A, B):
-    """Generalized SPD eigenproblem A v = lam B v on the GPU (setup only):
-    B = L L^T (cuSOLVER potrf), the standard problem L^-1 A L^-T (cuSOLVER
-    syevd), v = L^-T y.  Eigenvectors are B-orthonormal like LAPACK dsygvd's."""
+    """Generalized SPD eigenproblem A v = lam B v on the GPU (setup only),
+    through the C ABI (``sfb_geigh``: cuSOLVER potrf + syevd, cuBLAS trsm,
+    the reference's sign rule applied on the device).  Eigenvectors are
+    B-orthonormal like LAPACK dsygvd's."""
     t = nat.torch()
     Ad, Bd = _dense_device(A), _dense_device(B)
-    L, info = t.linalg.cholesky_ex(0.5 * (Bd + Bd.T))
-    if int(info.item()) != 0:
-        raise np.linalg.LinAlgError("matrix B is not positive definite")
-    M = t.linalg.solve_triangular(L, Ad, upper=False)
-    M = t.linalg.solve_triangular(L, M.T, upper=False)
-    lam, Y = t.linalg.eigh(0.5 * (M + M.T))
-    V = t.linalg.solve_triangular(L.T, Y, upper=True)
-    return lam.cpu().numpy(), V.contiguous()
+    q = Ad.shape[0]
+    lam = np.zeros(q)
+    V = t.empty((q, q), dtype=t.float64, device="cuda")
+    rc = nat.lib().sfb_geigh(q, nat.ptr(Ad), Ad.stride(0), nat.ptr(Bd), Bd.stride(0), nat.dptr(lam), nat.ptr(V), q,
+                             nat.stream())
+    if rc == nat.ERR_ARG:
+        raise np.linalg.LinAlgError(nat.last_error())
+    nat.check(rc, "generalized eigensolver")
+    return lam, V
 
 
 def build_spectral_cache(op: SylvesterOperator, eig: str = "host") -> SpectralCache:

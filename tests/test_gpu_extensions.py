@@ -121,3 +121,29 @@ def test_two_term_preconditioner_in_imex_heat_matches_reference_trajectory(golde
     assert np.all(tr.iterations < golden["heat/t12/iters"])
     assert relerr(tr.final[0], golden["heat/t12/U"]) <= 1e-10
     assert np.allclose(tr.increments, golden["heat/t12/incs"], rtol=1e-8)
+
+
+@pytest.mark.gpu
+def test_native_generalized_eigensolver_matches_lapack():
+    """sfb_geigh (spectral setup on the device) against scipy.linalg.eigh(A, B)
+    (the reference's dsygvd route) with the reference's sign rule."""
+    import scipy.linalg as sla
+
+    from paper_2109_01173_b200.solvers import _geigh_device
+    rng = np.random.default_rng(9)
+    for q in (5, 64, 301):
+        X = rng.standard_normal((q, q))
+        A = X @ X.T + q * np.eye(q)
+        Y = rng.standard_normal((q, q))
+        B = Y @ Y.T + q * np.eye(q)
+        lam, V = _geigh_device(A, B)
+        V = V.cpu().numpy()
+        lr, Vr = sla.eigh(A, B)
+        idx = np.argmax(np.abs(Vr), axis=0)
+        Vr = Vr * np.sign(Vr[idx, np.arange(q)])
+        assert np.allclose(lam, lr, rtol=1e-12, atol=0)
+        assert np.abs(V - Vr).max() <= 1e-10 * np.abs(Vr).max()
+        assert np.allclose(V.T @ B @ V, np.eye(q), atol=1e-10)
+        assert np.all(V[np.argmax(np.abs(V), axis=0), np.arange(q)] > 0)
+    with pytest.raises(np.linalg.LinAlgError, match="not positive definite"):
+        _geigh_device(np.eye(4), -np.eye(4))
