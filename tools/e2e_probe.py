@@ -27,9 +27,11 @@ def t(fn, reps=5):
     return (time.perf_counter() - t0) / reps * 1e3
 
 
-rhs = w.rhs
+pinned_rhs = torch.empty(w.rhs.shape, dtype=torch.float64, pin_memory=True)
+pinned_rhs.copy_(torch.from_numpy(w.rhs))
+rhs = pinned_rhs.numpy() if os.environ.get("E2E_PINNED", "1") == "1" else w.rhs  # bench.py's e2e input is pinned
 d = nat.to_device(rhs)
-print(f"to_device (pageable H2D) {t(lambda: nat.to_device(rhs)):7.2f} ms")
+print(f"to_device (numpy H2D)    {t(lambda: nat.to_device(rhs)):7.2f} ms")
 print(f"cpu().numpy() (D2H)      {t(lambda: d.cpu().numpy()):7.2f} ms")
 pin = torch.empty(d.shape, dtype=torch.float64, pin_memory=True)
 pin2 = torch.empty_like(pin).pin_memory(); d2 = torch.empty_like(d)
