@@ -73,6 +73,7 @@ typedef struct sfb_map sfb_map;
 typedef struct sfb_pre sfb_pre;
 typedef struct sfb_pcg sfb_pcg;
 typedef struct sfb_csr sfb_csr;
+typedef struct sfb_reduced sfb_reduced;
 
 typedef struct {
     int iterations;       /* completed iterations                        */
@@ -168,6 +169,15 @@ int sfb_pre_apply(const sfb_pre* p, const double* R_dev, int ldr,
                   double* Z_dev, int ldz, void* stream);
 /* Y = V_L^T X V_R for the spectral kinds (the forward spectral transform;
  * used by the closed-form residual, solvers.py:345-348). */
+/* The reduced solve of a two-term operator (solvers.py:284-300) as one
+ * object: the spectral-sum sandwich of `pre` (SFB_PRE_SPECTRAL_SUM) and the
+ * residual |L(U) - B| through `op`, captured once into a CUDA graph with
+ * persistent buffers.  solve: U = sandwich(B); res2_host (may be NULL) <-
+ * { |L(U) - B|_F, |B|_F } (solvers.py:293-294).  Thread-safe per object. */
+int sfb_reduced_create(const sfb_pre* pre, const sfb_op* op, sfb_reduced** out);
+int sfb_reduced_solve(sfb_reduced* r, const double* B_dev, int ldb, double* U_dev, int ldu,
+                      double* res2_host, void* stream);
+int sfb_reduced_destroy(sfb_reduced* r);
 int sfb_pre_transform(const sfb_pre* p, const double* X_dev, int ldx, double* Y_dev, int ldy, void* stream);
 int sfb_pre_destroy(sfb_pre* p);
 

@@ -36,7 +36,7 @@ EXPORTS = [
     "sfb_csr_create", "sfb_csr_spmv", "sfb_csr_destroy",
     "sfb_pcg_shape", "sfb_imex_heat_run", "sfb_imex_rds_run",
     "sfb_dgemm_nt_scatter", "sfb_copy2d", "sfb_ipc_get_handle", "sfb_ipc_open", "sfb_ipc_close",
-    "sfb_frame_pgm16", "sfb_geigh",
+    "sfb_frame_pgm16", "sfb_geigh", "sfb_reduced_create", "sfb_reduced_solve", "sfb_reduced_destroy",
 ]
 IMEX_OK, IMEX_BLOWUP, IMEX_NOT_CONVERGED, IMEX_INDEFINITE, IMEX_NONFINITE = range(5)
 
@@ -99,6 +99,9 @@ _SIGS = {
     "sfb_ipc_close": (_I, [_P]),
     "sfb_frame_pgm16": (_I, [_P, _I, _I, _I, _P, _DP, _P]),
     "sfb_geigh": (_I, [_I, _P, _I, _P, _I, _DP, _P, _I, _P]),
+    "sfb_reduced_create": (_I, [_P, _P, C.POINTER(_P)]),
+    "sfb_reduced_solve": (_I, [_P, _P, _I, _P, _I, _DP, _P]),
+    "sfb_reduced_destroy": (_I, [_P]),
     "sfb_imex_heat_run": (_I, [_P, _P, _I, _I, _P, _I, _DP, _I, _I, _D, _I, _P, _I, C.POINTER(_I), _DP,
                                C.POINTER(ImexResult), _P]),
     "sfb_imex_rds_run": (_I, [_P, _P, _P, _DP, _D, _I, _I, _D, _I, _D, _P, _P, _I, C.POINTER(_I), _DP,

@@ -860,6 +860,130 @@ int sfb_pre_apply(const sfb_pre* p, const double* R, int ldr, double* Z, int ldz
     return SFB_OK;
 }
 
+// ------------------------------------------------------- reduced solve ---
+// solve_reduced (solvers.py:284-300) as one object: persistent padded
+// buffers and GEMM workspace, and the whole solve — the spectral sandwich
+// U = P1 [(P1^T B P2) / (lam1_i + lam2_j)] P2^T, the operator apply for the
+// residual and its two norms — captured once into a CUDA graph.  A call is
+// two copies, one graph launch and one sync (the per-call allocations and
+// launches dominated small solves: cfg1, q = 256).
+struct sfb_reduced {
+    const sfb_pre* pre = nullptr;
+    const sfb_op* op = nullptr;
+    int qy = 0, qx = 0, ld = 0, ldt1 = 0;
+    double *B = nullptr, *U = nullptr, *W = nullptr, *T1 = nullptr, *T2 = nullptr, *parts = nullptr;
+    RedSlots* red = nullptr;
+    double* host = nullptr;  // page-locked result scalars
+    GemmWs gw;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    std::mutex mu;
+};
+
+int sfb_reduced_destroy(sfb_reduced* r) {
+    if (!r) return SFB_OK;
+    if (r->exec) cudaGraphExecDestroy(r->exec);
+    for (void* p : {(void*)r->B, (void*)r->U, (void*)r->W, (void*)r->T1, (void*)r->T2, (void*)r->parts,
+                    (void*)r->red, (void*)r->gw.ws, (void*)r->gw.flags})
+        cudaFree(p);
+    if (r->host) cudaFreeHost(r->host);
+    if (r->stream) cudaStreamDestroy(r->stream);
+    if (r->ev_in) cudaEventDestroy(r->ev_in);
+    if (r->ev_out) cudaEventDestroy(r->ev_out);
+    delete r;
+    return SFB_OK;
+}
+
+int sfb_reduced_create(const sfb_pre* pre, const sfb_op* op, sfb_reduced** out) {
+    if (!pre || !op || !out) return arg_error("reduced solve: null argument");
+    if (pre->kind != SFB_PRE_SPECTRAL_SUM) return arg_error("reduced solve needs a spectral-sum sandwich");
+    if (pre->qy != op->qy || pre->qx != op->qx) return arg_error("reduced solve: operator and cache shapes differ");
+    auto* r = new sfb_reduced;
+    r->pre = pre;
+    r->op = op;
+    r->qy = op->qy;
+    r->qx = op->qx;
+    r->ld = pad_ld(r->qx);
+    r->ldt1 = pad_ld(r->qy);
+    const size_t g = (size_t)r->qy * r->ld;
+    const size_t nparts = (size_t)std::max(std::max(vector_grid_blocks(), gemm_grid_blocks(r->qy, r->qx)),
+                                           band_grid_blocks(r->qy, r->qx));
+    int rc = dalloc(&r->B, g);
+    if (rc == SFB_OK) rc = dalloc(&r->U, g);
+    if (rc == SFB_OK) rc = dalloc(&r->W, g);
+    if (rc == SFB_OK) rc = dalloc(&r->T1, (size_t)r->qx * r->ldt1);
+    if (rc == SFB_OK) rc = dalloc(&r->T2, g);
+    if (rc == SFB_OK) rc = dalloc(&r->parts, 4 * nparts);  // launch_norms: 4 partials per block
+    if (rc == SFB_OK) rc = dalloc(&r->gw.ws, gemm_workspace_doubles());
+    if (rc == SFB_OK && (cudaMalloc(reinterpret_cast<void**>(&r->red), 3 * sizeof(RedSlots)) != cudaSuccess ||
+                         cudaMalloc(reinterpret_cast<void**>(&r->gw.flags), gemm_max_tiles() * sizeof(unsigned)) !=
+                             cudaSuccess ||
+                         cudaMallocHost(reinterpret_cast<void**>(&r->host), 4 * sizeof(double)) != cudaSuccess))
+        rc = SFB_ERR_NOMEM;
+    // padding columns stay zero; the stream-K tile counters start (and return to) zero
+    if (rc == SFB_OK) {
+        for (double* p : {r->B, r->U, r->W, r->T2}) cudaMemset(p, 0, g * 8);
+        cudaMemset(r->T1, 0, (size_t)r->qx * r->ldt1 * 8);
+        cudaMemset(r->gw.flags, 0, gemm_max_tiles() * sizeof(unsigned));
+        if (cudaDeviceSynchronize() != cudaSuccess) rc = SFB_ERR_CUDA;
+    }
+    if (rc == SFB_OK && (cudaStreamCreateWithFlags(&r->stream, cudaStreamNonBlocking) != cudaSuccess ||
+                         cudaEventCreateWithFlags(&r->ev_in, cudaEventDisableTiming) != cudaSuccess ||
+                         cudaEventCreateWithFlags(&r->ev_out, cudaEventDisableTiming) != cudaSuccess))
+        rc = SFB_ERR_CUDA;
+    if (rc == SFB_OK) {
+        cudaStream_t st = r->stream;
+        cudaGraph_t graph = nullptr;
+        if (cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+            rc = SFB_ERR_CUDA;
+        } else {
+            int c = cudaMemsetAsync(r->red, 0, 3 * sizeof(RedSlots), st) == cudaSuccess ? SFB_OK : SFB_ERR_CUDA;
+            if (c == SFB_OK)
+                c = pre_apply_impl(pre, r->B, r->ld, r->U, r->ld, r->T1, r->ldt1, r->T2, r->ld, r->parts, nullptr,
+                                   r->red + 2, &r->gw, st);
+            if (c == SFB_OK) c = op_apply_impl(op, r->U, r->ld, r->W, r->ld, r->T1, r->ldt1, &r->gw, st);
+            if (c == SFB_OK) c = launch_norms(r->W, r->ld, r->B, r->ld, r->qy, r->qx, r->parts, r->red, st);
+            if (c == SFB_OK) c = launch_norms(r->B, r->ld, nullptr, 0, r->qy, r->qx, r->parts, r->red + 1, st);
+            const cudaError_t e = cudaStreamEndCapture(st, &graph);
+            rc = c != SFB_OK ? c : (e == cudaSuccess ? SFB_OK : SFB_ERR_CUDA);
+            if (rc == SFB_OK && cudaGraphInstantiate(&r->exec, graph, 0) != cudaSuccess) rc = SFB_ERR_CUDA;
+            if (graph) cudaGraphDestroy(graph);
+        }
+    }
+    if (rc != SFB_OK) {
+        if (rc == SFB_ERR_CUDA) set_error("reduced solve: building the solve graph failed");
+        sfb_reduced_destroy(r);
+        return rc;
+    }
+    *out = r;
+    return SFB_OK;
+}
+
+int sfb_reduced_solve(sfb_reduced* r, const double* B, int ldb, double* U, int ldu, double* res2_host,
+                                 void* stream) {
+    if (!r || !B || !U) return arg_error("reduced solve: null argument");
+    std::lock_guard<std::mutex> lock(r->mu);
+    cudaStream_t cs = (cudaStream_t)stream, st = r->stream;
+    SFB_CUDA_TRY(cudaEventRecord(r->ev_in, cs));
+    SFB_CUDA_TRY(cudaStreamWaitEvent(st, r->ev_in, 0));
+    SFB_CUDA_TRY(cudaMemcpy2DAsync(r->B, (size_t)r->ld * 8, B, (size_t)ldb * 8, (size_t)r->qx * 8, r->qy,
+                                   cudaMemcpyDeviceToDevice, st));
+    SFB_CUDA_TRY(cudaGraphLaunch(r->exec, st));
+    SFB_CUDA_TRY(cudaMemcpy2DAsync(U, (size_t)ldu * 8, r->U, (size_t)r->ld * 8, (size_t)r->qx * 8, r->qy,
+                                   cudaMemcpyDeviceToDevice, st));
+    if (res2_host) {
+        SFB_CUDA_TRY(cudaMemcpyAsync(r->host, &r->red[0].v[0], 8, cudaMemcpyDeviceToHost, st));
+        SFB_CUDA_TRY(cudaMemcpyAsync(r->host + 1, &r->red[1].v[0], 8, cudaMemcpyDeviceToHost, st));
+        SFB_CUDA_TRY(cudaStreamSynchronize(st));
+        res2_host[0] = r->host[0];
+        res2_host[1] = r->host[1];
+    }
+    SFB_CUDA_TRY(cudaEventRecord(r->ev_out, st));
+    SFB_CUDA_TRY(cudaStreamWaitEvent(cs, r->ev_out, 0));
+    return SFB_OK;
+}
+
 int sfb_pre_transform(const sfb_pre* p, const double* X, int ldx, double* Y, int ldy, void* stream) {
     if (!p) return arg_error("null preconditioner");
     if (p->kind != SFB_PRE_SPECTRAL_PROD && p->kind != SFB_PRE_SPECTRAL_SUM)

@@ -473,9 +473,24 @@ class SpectralCache:
         return 1.0 / (self.lam1[:, None] + self.lam2[None, :])
 
     def check_pencils(self) -> None:
-        if _min_abs_pair_sum(self.lam1, self.lam2) < PENCIL_GUARD:
-            raise SolverError("spectral pencils are (numerically) singular: an eigenvalue "
-                              f"sum fell below {PENCIL_GUARD:g}")
+        if not self.__dict__.get("_pencils_ok"):
+            if _min_abs_pair_sum(self.lam1, self.lam2) < PENCIL_GUARD:
+                raise SolverError("spectral pencils are (numerically) singular: an eigenvalue "
+                                  f"sum fell below {PENCIL_GUARD:g}")
+            self._pencils_ok = True
+
+    def reduced(self, op) -> int:
+        """Native reduced-solve object of (this cache, op): the sandwich and
+        the residual captured into one CUDA graph (sfb_reduced_*)."""
+        d = self.__dict__.setdefault("_reduced", {})
+        e = d.get(id(op))
+        if e is None or e[0] is not op:
+            L = nat.lib()
+            out = nat.C.c_void_p()
+            nat.check(L.sfb_reduced_create(self.native(), op.native(), nat.C.byref(out)), "reduced solve")
+            e = (op, nat.Handle(out.value, L.sfb_reduced_destroy))
+            d[id(op)] = e
+        return e[1].p
 
     def native(self):
         h = getattr(self, "_handle", None)
@@ -563,12 +578,12 @@ def solve_reduced(op: SylvesterOperator, rhs, cache: SpectralCache | None = None
     t = nat.torch()
     B = nat.to_device(rhs)
     qy, qx = B.shape
+    if (qy, qx) != tuple(op.shape):
+        raise OperatorError(f"grid shape {(qy, qx)} does not match operator {op.shape}")
     U = t.empty_like(B)
-    L = nat.lib()
-    nat.check(L.sfb_pre_apply(cache.native(), nat.ptr(B), qx, nat.ptr(U), qx, nat.stream()), "reduced solve")
     out2 = np.zeros(2)
-    nat.check(L.sfb_op_residual(op.native(), nat.ptr(U), qx, nat.ptr(B), qx, nat.dptr(out2), nat.stream()),
-              "residual")
+    nat.check(nat.lib().sfb_reduced_solve(cache.reduced(op), nat.ptr(B), qx, nat.ptr(U), qx, nat.dptr(out2),
+                                          nat.stream()), "reduced solve")
     res = out2[0] / max(out2[1], 1e-300)
     return SolveReport(solution=U if on_dev else nat.to_host(U), method="reduced", iterations=0,
                        residual_history=np.array([res]), stop_reason="direct",
