@@ -237,10 +237,10 @@ class PeerTransposes:
             pass
 
     def sync(self):
-        if self.L.world == 1:
-            return
-        if self.sync_mode == "stream":
+        if self.sync_mode == "stream":  # also at world 1: one code path (a no-op NCCL kernel)
             self.dist.all_reduce(self._flag, group=self.group)
+        elif self.L.world == 1:
+            return
         else:
             self.t.cuda.current_stream().synchronize()
             self.dist.barrier(group=self.group)

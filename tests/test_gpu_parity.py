@@ -307,10 +307,19 @@ def test_sharded_cuda_backend_single_rank_matches_mo_pcg():
         x, y, op, rhs = cfg3_small()
         pre = pb.make_preconditioner("elliptic_xnormal", x, y)
         lay = Layout(*op.shape, 1, 0)
-        rep = sharded_mo_pcg(CudaBackend(op, pre, lay), Comm(lay, torch.device("cuda")), rhs,
+        be = CudaBackend(op, pre, lay)
+        rep = sharded_mo_pcg(be, Comm(lay, torch.device("cuda")), rhs,
                              stop=pb.relative_residual(1e-12), max_iter=5000)
         ref = pb.mo_pcg(op, rhs, precond=pre, stop=pb.relative_residual(1e-12), max_iter=5000)
         assert abs(rep.iterations - ref.iterations) <= 1
         assert relerr(rep.solution, ref.solution) <= 1e-10
+        # the bench's N > 1 configuration: transposes over peer memory with
+        # stream-ordered NCCL synchronisation (here a one-rank communicator)
+        from paper_2109_01173_b200.distributed import PeerTransposes
+        pt = PeerTransposes(lay, be, sync="stream")
+        rep2 = sharded_mo_pcg(be, Comm(lay, torch.device("cuda")), rhs, stop=pb.relative_residual(1e-12),
+                              max_iter=5000, peer=pt)
+        assert rep2.iterations == rep.iterations
+        assert relerr(rep2.solution, rep.solution) <= 1e-13
     finally:
         dist.destroy_process_group()
