@@ -477,9 +477,10 @@ def run_native(args):
                "host_stack": host_stack()}
 
     # per solve: init + first preconditioner (+ the deferred-U fixup of the banded
-    # iteration); per iteration: operator pass(es), update, preconditioner, loop control
+    # iteration); per iteration: operator pass, update, preconditioner
     n_pre = n_gemm_per_iter if n_gemm_per_iter else 5  # banded: 3 SPIKE tile passes + 2 interface chains
-    per_step_launches = 1 + n_pre + (1 if op.banded else 0) + (3 + n_pre) * K_it
+    # (the banded iteration's R update also sets the loop condition: no loop-control kernel)
+    per_step_launches = 1 + n_pre + (1 if op.banded else 0) + ((2 if op.banded else 3) + n_pre) * K_it
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

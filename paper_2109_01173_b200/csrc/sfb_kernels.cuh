@@ -102,8 +102,9 @@ int launch_pcg_direction(const double* Z, double* Q0, double* Q1, int ld, int ro
                          PcgState* st, cudaStream_t s);
 int launch_pcg_dots(const double* W, const double* Q0, const double* Q1, int ld, int rows, int cols,
                     double* partials, PcgState* st, cudaStream_t s);
+// use_handle: also the loop control of the conditional iteration graph
 int launch_pcg_rupdate(double* R, const double* W, int ld, int rows, double* partials, PcgState* st, double* hist,
-                       double* incs, cudaStream_t s);
+                       double* incs, cudaStream_t s, unsigned long long handle = 0, int use_handle = 0);
 int launch_pcg_ufinal(double* U, const double* Q0, const double* Q1, int ld, int rows, PcgState* st,
                       cudaStream_t s);
 int launch_pcg_update(double* U, double* R, const double* W, const double* Q0, const double* Q1, int ld,

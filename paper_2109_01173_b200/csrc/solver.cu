@@ -324,7 +324,11 @@ struct sfb_pcg {
 namespace sfb {
 namespace {
 
-int pcg_enqueue_iteration(sfb_pcg* s, double* iterates) {
+// Enqueue one MO-PCG iteration; *ctl_done tells whether the iteration already
+// set the WHILE condition (banded iteration: the R update's last CTA does it)
+int pcg_enqueue_iteration(sfb_pcg* s, double* iterates, unsigned long long handle = 0, int use_handle = 0,
+                          bool* ctl_done = nullptr) {
+    if (ctl_done) *ctl_done = false;
     cudaStream_t st = s->stream;
     const sfb_op* op = s->op;
     if (!op->dense) {
@@ -342,7 +346,9 @@ int pcg_enqueue_iteration(sfb_pcg* s, double* iterates) {
         a.pcg = s->st;
         a.U = s->U;  // receives the previous iteration's deferred U += alpha Q
         SFB_TRY(launch_band(a, st));
-        SFB_TRY(launch_pcg_rupdate(s->R, s->W, s->ld, s->qy, s->partials, s->st, s->hist, s->incs, st));
+        SFB_TRY(launch_pcg_rupdate(s->R, s->W, s->ld, s->qy, s->partials, s->st, s->hist, s->incs, st, handle,
+                                   use_handle));
+        if (ctl_done) *ctl_done = true;
         if (iterates != nullptr)
             SFB_TRY(launch_pcg_record(s->U, s->ld, s->qy, s->qx, iterates, s->st, st, s->Q0, s->Q1));
     } else {
@@ -406,8 +412,9 @@ int build_graph(sfb_pcg* s, double* iterates) {
             ok = cudaStreamBeginCaptureToGraph(s->stream, body, nullptr, nullptr, 0,
                                                cudaStreamCaptureModeThreadLocal) == cudaSuccess;
             if (ok) {
-                int rc = pcg_enqueue_iteration(s, iterates);
-                if (rc == SFB_OK) rc = launch_loop_ctl(s->st, (unsigned long long)h, 1, s->stream);
+                bool ctl = false;
+                int rc = pcg_enqueue_iteration(s, iterates, (unsigned long long)h, 1, &ctl);
+                if (rc == SFB_OK && !ctl) rc = launch_loop_ctl(s->st, (unsigned long long)h, 1, s->stream);
                 cudaGraph_t captured = nullptr;
                 cudaError_t e = cudaStreamEndCapture(s->stream, &captured);
                 if (rc != SFB_OK) {
@@ -433,8 +440,9 @@ int build_graph(sfb_pcg* s, double* iterates) {
     SFB_CUDA_TRY(cudaStreamBeginCapture(s->stream, cudaStreamCaptureModeThreadLocal));
     int rc = SFB_OK;
     for (int i = 0; i < s->chunk && rc == SFB_OK; ++i) {
-        rc = pcg_enqueue_iteration(s, iterates);
-        if (rc == SFB_OK) rc = launch_loop_ctl(s->st, 0, 0, s->stream);
+        bool ctl = false;
+        rc = pcg_enqueue_iteration(s, iterates, 0, 0, &ctl);
+        if (rc == SFB_OK && !ctl) rc = launch_loop_ctl(s->st, 0, 0, s->stream);
     }
     cudaGraph_t cg = nullptr;
     cudaError_t e = cudaStreamEndCapture(s->stream, &cg);

@@ -98,9 +98,13 @@ __global__ void __launch_bounds__(VT) pcg_update_kernel(double* __restrict__ U, 
 // pcg_ufinal_kernel.  Same arithmetic as pcg_update_kernel.
 __global__ void __launch_bounds__(VT) pcg_rupdate_kernel(double* __restrict__ R, const double* __restrict__ W,
                                                          int ld, int rows, double* partials, PcgState* st,
-                                                         double* hist, double* incs) {
+                                                         double* hist, double* incs,
+                                                         cudaGraphConditionalHandle handle, int use_handle) {
     SFB_PDL_PROLOGUE();
-    if (st->status != SFB_PCG_RUNNING) return;
+    if (st->status != SFB_PCG_RUNNING) {  // e.g. INDEFINITE from this iteration's operator pass
+        if (use_handle && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(handle, 0u);
+        return;
+    }
     const double alpha = st->alpha;
     double rr = 0.0;
     const size_t n2 = (size_t)rows * ld / 2;
@@ -124,6 +128,13 @@ __global__ void __launch_bounds__(VT) pcg_rupdate_kernel(double* __restrict__ R,
         if (threadIdx.x == 0) {
             st->counter[1] = 0;
             pcg_finish_update(st, tot, hist, incs);
+            // the loop control of the iteration graph (loop_ctl_kernel's rule),
+            // here so the banded iteration needs no extra kernel: the rest of
+            // the body (the preconditioner) does not change the status
+            const unsigned runs = ++st->counter[6];
+            const bool keep = st->status == SFB_PCG_RUNNING && st->iter < st->max_iter &&
+                              runs <= (unsigned)st->max_iter + 2u;
+            if (use_handle) cudaGraphSetConditional(handle, keep ? 1u : 0u);
         }
     }
 }
@@ -505,8 +516,9 @@ int launch_pcg_update(double* U, double* R, const double* W, const double* Q0, c
 }
 
 int launch_pcg_rupdate(double* R, const double* W, int ld, int rows, double* partials, PcgState* st, double* hist,
-                       double* incs, cudaStream_t s) {
-    SFB_TRY(launch_kernel(pcg_rupdate_kernel, dim3(VB), dim3(VT), 0, s, R, W, ld, rows, partials, st, hist, incs));
+                       double* incs, cudaStream_t s, unsigned long long handle, int use_handle) {
+    SFB_TRY(launch_kernel(pcg_rupdate_kernel, dim3(VB), dim3(VT), 0, s, R, W, ld, rows, partials, st, hist, incs,
+                          (cudaGraphConditionalHandle)handle, use_handle));
     SFB_CHECK_LAUNCH();
     return SFB_OK;
 }
