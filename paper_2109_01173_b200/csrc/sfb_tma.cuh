@@ -49,6 +49,15 @@ __device__ __forceinline__ void tma_load3_u32(uint32_t dst, const CUtensorMap* m
         : "memory");
 }
 
+// 1-D bulk copy global -> shared (16-byte aligned, size a multiple of 16)
+// completing on an mbarrier's transaction count
+__device__ __forceinline__ void bulk_load_u32(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(bar)
+        : "memory");
+}
+
 // order this thread's generic-proxy shared-memory accesses before later
 // async-proxy (TMA) writes to the same buffers
 __device__ __forceinline__ void fence_proxy_async_smem() {

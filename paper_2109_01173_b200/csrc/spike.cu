@@ -34,6 +34,7 @@
 #include "sfb_common.cuh"
 #include "sfb_kernels.cuh"
 #include "sfb_launch.cuh"
+#include "sfb_tma.cuh"
 
 namespace sfb {
 
@@ -427,42 +428,39 @@ __device__ __forceinline__ void cp_async8(double* dst, const double* src) {
 // step and the b values the next step needs travel by shuffle, so the
 // sequential critical path per step is two FMAs and a shuffle instead of a
 // whole block product, and the 2047-line chain occupies 4x the warps.
-__host__ __device__ constexpr int chain_group(int b) { return b == 1 ? 2 : (b == 2 ? 4 : 8); }  // 2B -> power of 2
-
+// The two sweeps of one line's interface chain (the kernel below); inlined
+// once with the staged shared-memory coefficients and once with the global
+// ones, so every shared access compiles to LDS (a pointer that may point to
+// either space compiles to generic loads).  The step-to-step dependence is
+// only through the b interface values (prev / nx): K_p gamma_p is formed one
+// step ahead.
 template <int B>
-__global__ void __launch_bounds__(CHAIN_L * chain_group(B)) spike_chain_kernel(int nlines, int P, const double* __restrict__ coef,
-                                                                      double* sv, int coef_in_smem,
-                                                                      const PcgState* gate) {
-    SFB_PDL_PROLOGUE();
-    if (gate != nullptr && gate->status != SFB_PCG_RUNNING) return;
+__device__ __forceinline__ void chain_lines(const double* __restrict__ cf, double* gs, double* sv, int nlines, int P,
+                                            int line0, int l, int i, bool live, int gbase) {
     constexpr int B2 = 2 * B;
-    constexpr int L = CHAIN_L;                 // lines per CTA
-    constexpr int PER = B2 * B2 + 2 * B2 * B;  // K (2B x 2B), KA (2B x B), Ch (2B x B)
-    extern __shared__ double gs[];             // [P][2B][L], then the coefficients when they fit
-    constexpr int GP = chain_group(B);         // lanes per line (2B rounded up to a power of two)
-    const int t = threadIdx.x, l = t / GP, i0 = t % GP, line0 = blockIdx.x * L;
-    const bool live = line0 + l < nlines && i0 < B2;
-    const int i = i0 < B2 ? i0 : 0;            // padding lanes mirror row 0 and store nothing
-    const unsigned gmask = 0xffffffffu;        // whole warps (GP divides 32): every lane shuffles
-    const int gbase = (t & 31) - i0;           // lane of this line's row 0
-    // stage with every load in flight (cp.async, one wait)
-    double* cs = gs + (size_t)P * B2 * L;
-    if (live)
-        for (int p = 0; p < P; ++p) cp_async8(gs + (p * B2 + i) * L + l, sv + (size_t)(p * B2 + i) * nlines + line0 + l);
-    if (coef_in_smem)
-        for (int k = t; k < P * PER; k += L * GP) cp_async8(cs + k, coef + k);
-    asm volatile("cp.async.wait_all;" ::: "memory");
-    __syncthreads();
-    const double* cf = coef_in_smem ? cs : coef;
+    constexpr int L = CHAIN_L;
+    constexpr int PER = B2 * B2 + 2 * B2 * B;
+    const unsigned gmask = 0xffffffffu;
+    const bool line_ok = line0 + l < nlines;
+    auto kdot = [&](int p) {
+        const double* K = cf + (size_t)p * PER + i * B2;
+        double a0 = 0.0, a1 = 0.0;
+        #pragma unroll
+        for (int j = 0; j < B2; j += 2) {
+            a0 = fma(K[j], line_ok ? gs[(p * B2 + j) * L + l] : 0.0, a0);
+            a1 = fma(K[j + 1], line_ok ? gs[(p * B2 + j + 1) * L + l] : 0.0, a1);
+        }
+        return a0 + a1;
+    };
     double prev[B];  // u part of d_{p-1}
     #pragma unroll
     for (int d = 0; d < B; ++d) prev[d] = 0.0;
+    double kg = kdot(0);
     for (int p = 0; p < P; ++p) {
-        const double* K = cf + (size_t)p * PER + i * B2;
+        const double kg_p = kg;
+        if (p + 1 < P) kg = kdot(p + 1);
         const double* KA = cf + (size_t)p * PER + B2 * B2 + i * B;
-        double v = 0.0;
-        #pragma unroll
-        for (int j = 0; j < B2; ++j) v = fma(K[j], line0 + l < nlines ? gs[(p * B2 + j) * L + l] : 0.0, v);
+        double v = kg_p;
         #pragma unroll
         for (int j = 0; j < B; ++j) v = fma(-KA[j], prev[j], v);
         __syncwarp();  // the line's other rows have read step p's values
@@ -482,6 +480,52 @@ __global__ void __launch_bounds__(CHAIN_L * chain_group(B)) spike_chain_kernel(i
         if (live) sv[((size_t)p * B2 + i) * nlines + line0 + l] = v;
         #pragma unroll
         for (int d = 0; d < B; ++d) nx[d] = __shfl_sync(gmask, v, gbase + d);
+    }
+}
+
+__host__ __device__ constexpr int chain_group(int b) { return b == 1 ? 2 : (b == 2 ? 4 : 8); }  // 2B -> power of 2
+
+template <int B>
+__global__ void __launch_bounds__(CHAIN_L * chain_group(B)) spike_chain_kernel(int nlines, int P, const double* __restrict__ coef,
+                                                                      double* sv, int coef_in_smem,
+                                                                      const PcgState* gate) {
+    SFB_PDL_PROLOGUE();
+    if (gate != nullptr && gate->status != SFB_PCG_RUNNING) return;
+    constexpr int B2 = 2 * B;
+    constexpr int L = CHAIN_L;                 // lines per CTA
+    constexpr int PER = B2 * B2 + 2 * B2 * B;  // K (2B x 2B), KA (2B x B), Ch (2B x B)
+    extern __shared__ double gs[];             // [P][2B][L], then the coefficients when they fit
+    constexpr int GP = chain_group(B);         // lanes per line (2B rounded up to a power of two)
+    const int t = threadIdx.x, l = t / GP, i0 = t % GP, line0 = blockIdx.x * L;
+    const bool live = line0 + l < nlines && i0 < B2;
+    const int i = i0 < B2 ? i0 : 0;            // padding lanes mirror row 0 and store nothing
+    const unsigned gmask = 0xffffffffu;        // whole warps (GP divides 32): every lane shuffles
+    const int gbase = (t & 31) - i0;           // lane of this line's row 0
+    // stage with every load in flight: the coefficients (the same block for
+    // every CTA, P * PER doubles) as one bulk copy, the lines' values by cp.async
+    double* cs = gs + (size_t)P * B2 * L;
+    __shared__ __align__(8) uint64_t cbar;
+    if (coef_in_smem && t == 0) {
+        mbar_init_u32(smem_u32(&cbar), 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        const uint32_t bytes = (uint32_t)P * PER * 8;
+        mbar_expect_tx_u32(smem_u32(&cbar), bytes);
+        bulk_load_u32(smem_u32(cs), coef, bytes, smem_u32(&cbar));
+    }
+    {  // consecutive threads take consecutive lines of one row (coalesced segments)
+        const int nl = min(L, nlines - line0);
+        for (int k = t; k < P * B2 * L; k += L * GP) {
+            const int row = k / L, ll = k - row * L;
+            if (ll < nl) cp_async8(gs + row * L + ll, sv + (size_t)row * nlines + line0 + ll);
+        }
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();  // (also publishes the barrier init)
+    if (coef_in_smem) {
+        mbar_wait_u32(smem_u32(&cbar), 0);
+        chain_lines<B>(cs, gs, sv, nlines, P, line0, l, i, live, gbase);  // shared-space coefficient reads
+    } else {
+        chain_lines<B>(coef, gs, sv, nlines, P, line0, l, i, live, gbase);
     }
 }
 
