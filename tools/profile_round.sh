@@ -4,7 +4,9 @@
 # MO-PCG passes (DRAM traffic for bench's roofline_hbm.traffic).
 set -x
 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
+# (only this library's kernels: bench.py also times cuBLAS for the roofline peak)
 SYLFEM_B200_GRAPH=chunked ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+  --kernel-name-base demangled -k regex:"sfb::" \
   --log-file gpurun_out/launches.csv python bench.py --steps 1 --warmup 1 --iters-per-step 10 --no-full \
   --no-cpu-baseline --no-e2e > gpurun_out/ncu_launch.log 2>&1
 ncu --set full --import-source on --clock-control none -k regex:"band_kernel" -s 6 -c 1 \
