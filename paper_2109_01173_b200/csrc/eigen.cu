@@ -132,6 +132,7 @@ struct DevScratch {
 
 extern "C" int sfb_geigh(int q, const double* A, int lda, const double* B, int ldb, double* lam_host, double* V,
                          int ldv, void* stream) {
+    SFB_NVTX("sfb_geigh");
     using namespace sfb;
     if (q <= 0 || !A || !B || !lam_host || !V || lda < q || ldb < q || ldv < q) return arg_error("geigh: bad arguments");
     const DnApi& L = api();

@@ -74,6 +74,7 @@ extern "C" {
 int sfb_imex_heat_run(sfb_pcg* solver, const sfb_map* rhs_map, int row_shift, int col_shift, const double* F,
                       int ldf, const double* c_host, int n_steps, int rule, double value, int max_iter, double* U,
                       int ldu, int* iterations_host, double* increments_host, sfb_imex_result* res, void* stream) {
+    SFB_NVTX("sfb_imex_heat_run");
     if (!solver || !rhs_map || !U || !res) return sfb::arg_error("imex heat run: null argument");
     if (n_steps < 0 || max_iter < 0) return sfb::arg_error("imex heat run: negative step or iteration count");
     init_result(res);
@@ -124,6 +125,7 @@ int sfb_imex_rds_run(sfb_pcg* solver_u, sfb_pcg* solver_v, const sfb_map* rhs_ma
                      double tau_rho, int n_steps, int rule, double value, int max_iter, double steady_eps,
                      double* U, double* V, int ld, int* iterations_host, double* increments_host,
                      sfb_imex_result* res, void* stream) {
+    SFB_NVTX("sfb_imex_rds_run");
     if (!solver_u || !solver_v || !rhs_map || !params_host || !U || !V || !res)
         return sfb::arg_error("imex rds run: null argument");
     if (n_steps < 0 || max_iter < 0) return sfb::arg_error("imex rds run: negative step or iteration count");

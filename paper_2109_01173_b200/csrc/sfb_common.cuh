@@ -8,7 +8,17 @@
 
 #include "../../include/sylfem_b200.h"
 
+#include <nvtx3/nvToolsExt.h>
+
 namespace sfb {
+
+// NVTX range over an entry point (SURVEY §5 tracing): named ranges in nsys /
+// ncu timelines; header-only NVTX costs nothing without an attached tool.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+#define SFB_NVTX(name) ::sfb::NvtxRange sfb_nvtx_range_(name)
 
 // ---------------------------------------------------------------- errors --
 void set_error(const std::string& msg);

@@ -574,6 +574,7 @@ int sfb_op_create_dense(int qy, int qx, int nterms, const double* G, const doubl
 }
 
 int sfb_op_apply(const sfb_op* op, const double* U, int ldu, double* W, int ldw, void* stream) {
+    SFB_NVTX("sfb_op_apply");
     if (!op) return arg_error("null operator");
     cudaStream_t s = (cudaStream_t)stream;
     if (!op->dense) return op_apply_impl(op, U, ldu, W, ldw, nullptr, 0, nullptr, s);
@@ -714,6 +715,7 @@ int sfb_map_apply(const sfb_map* m, const double* F, int ldf, double* out, int l
 
 int sfb_map_apply_heat(const sfb_map* m, const double* U, int ldu, int row_shift, int col_shift, double c,
                        const double* F, int ldf, double* out, int ldo, double* check2, void* stream) {
+    SFB_NVTX("sfb_map_apply_heat");
     if (!m) return arg_error("null map");
     BandArgs a = map_args(m, out, ldo);
     a.ld_mode = LD_HEAT;
@@ -729,6 +731,7 @@ int sfb_map_apply_heat(const sfb_map* m, const double* U, int ldu, int row_shift
 
 int sfb_map_apply_dib(const sfb_map* m, const double* U, const double* V, int ld, int species, double tau_rho,
                       const double* params, double* out, int ldo, double* check2, void* stream) {
+    SFB_NVTX("sfb_map_apply_dib");
     if (!m) return arg_error("null map");
     // zero-flux: the input grid is the output grid, or a column block of it
     // extended by a halo (in_cols > out_cols, the sharded IMEX driver)
@@ -837,6 +840,7 @@ int sfb_pre_create_banded(int qy, int qx, int bwL, const double* lband, int bwR,
 }
 
 int sfb_pre_apply(const sfb_pre* p, const double* R, int ldr, double* Z, int ldz, void* stream) {
+    SFB_NVTX("sfb_pre_apply");
     if (!p) return arg_error("null preconditioner");
     cudaStream_t s = (cudaStream_t)stream;
     ScopedFree tmp(s);
@@ -970,6 +974,7 @@ int sfb_reduced_create(const sfb_pre* pre, const sfb_op* op, sfb_reduced** out) 
 
 int sfb_reduced_solve(sfb_reduced* r, const double* B, int ldb, double* U, int ldu, double* res2_host,
                                  void* stream) {
+    SFB_NVTX("sfb_reduced_solve");
     if (!r || !B || !U) return arg_error("reduced solve: null argument");
     std::lock_guard<std::mutex> lock(r->mu);
     cudaStream_t cs = (cudaStream_t)stream, st = r->stream;
@@ -1090,6 +1095,7 @@ int sfb_pcg_create(const sfb_op* op, const sfb_pre* pre, sfb_pcg** out) {
 int sfb_pcg_solve(sfb_pcg* s, const double* rhs, int ldr, const double* u0, int ldu0, double* U, int ldu, int rule,
                   double value, int max_iter, double* history, double* increments, double* iterates,
                   int n_iterates, sfb_pcg_result* res, void* stream) {
+    SFB_NVTX("sfb_pcg_solve");
     if (!s) return arg_error("null solver");
     if (max_iter < 0) return arg_error("max_iter must be nonnegative");
     std::lock_guard<std::mutex> lock(s->mu);
@@ -1288,6 +1294,7 @@ int sfb_pcg_destroy(sfb_pcg* s) {
 // ----------------------------------------------------------------- GEMM ---
 int sfb_dgemm_nt(const double* A, int lda, const double* Bt, int ldb, int M, int N, int K, double* C, int ldc,
                  void* stream) {
+    SFB_NVTX("sfb_dgemm_nt");
     GemmEpi e;
     e.mode = EPI_STORE;
     e.C = C;
