@@ -11,9 +11,13 @@ through the drop-in API on device-resident inputs.  DoF*it/s = q_y q_x *
 iterations / seconds.
 
 Printed (rank 0, one JSON line): value (device-resident), e2e (host numpy
-rhs in, host solution out, H2D/D2H inside the timed region), roofline of the
-dominant kernel (the FP64 DMMA GEMM of the preconditioner), cpu_baseline (the
-oracle port of the reference on the host cores, bounded sample), clocks.
+rhs in from page-locked memory, host solution out, H2D/D2H inside the timed
+region), roofline of the dominant kernel (the FP64 DMMA GEMM of the
+preconditioner) and roofline_hbm of the banded and update passes (live CUDA
+events; DRAM traffic from the committed ncu captures), cpu_baseline (the
+oracle port of the reference on the host cores, bounded sample), clocks,
+the banded-preconditioner alternative and the full solve to 1e-8.
+Under torchrun (N > 1) the same solve is column-sharded over the ranks.
 
     python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 """
