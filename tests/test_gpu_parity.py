@@ -350,3 +350,48 @@ def test_mo_pcg_rectangular_multi_block_vs_oracle(k, N, dom, gamma):
         # change of rounding (SURVEY finding 6); the solution is the parity check
         assert abs(rep.iterations - ref["iterations"]) <= max(1, ref["iterations"] // 100), mode
         assert relerr(rep.solution, ref["solution"]) <= 1e-10, mode
+
+
+@pytest.mark.parametrize("k,N,dom,bc,lumped", [(2, (12, 8), "cap", "n", False), (3, (12, 9), "jar", "d", False),
+                                               (1, (12, 9), "cap", "n", True)])
+def test_imex_heat_other_bcs_and_degrees_vs_oracle(k, N, dom, bc, lumped):
+    """The fused heat rhs (LD_HEAT) with Neumann (no interior shift) and
+    Dirichlet grids, consistent and lumped mass, through the native loop."""
+    from _cases import ODOMS, OBC
+    doms = {"cap": pb.CAP_DOMAIN, "jar": pb.JAR_DOMAIN}
+    bcs = {"d": D, "n": pb.BCKind.NEUMANN}
+    x, y = pb.build_direction_sets(doms[dom], k, N, bcs[bc], lumped=lumped)
+    ox, oy = orc.direction_sets(ODOMS[dom](), k, N, OBC[bc], lumped=lumped)
+    rng = np.random.default_rng(23)
+    F = rng.standard_normal((y.basis.n_sub + 1, x.basis.n_sub + 1))
+    u0 = 1e-2 * rng.standard_normal((y.q, x.q))
+    tr = pb.imex_euler_heat(doms[dom], x, y, 0.5, pb.SeparableSource(F, lambda t: np.cos(3 * t)), u0,
+                            pb.TimeGrid(2e-3, 1e-2), inner=pb.InnerSolver(rule="residual", tol=1e-13, max_iter=5000),
+                            lumped=lumped)
+    assert tr.diagnostics.get("loop") == "native"
+    ref = orc.imex_heat(ODOMS[dom](), ox, oy, 0.5, lambda u, X, Y, t: np.cos(3 * t) * F, u0, 2e-3, 1e-2,
+                        rule="residual", tol=1e-13, max_iter=5000, lumped=lumped)
+    assert np.all(np.abs(tr.iterations - ref["iterations"]) <= 1)
+    assert relerr(tr.final[0], ref["final"]) <= 1e-10
+    assert np.allclose(tr.increments, ref["increments"], rtol=1e-8)
+
+
+def test_imex_dib_consistent_mass_vs_oracle():
+    """DIB with the consistent (non-lumped) P1 mass: the fused kinetics rhs
+    (LD_DIB) through a banded mass map with a halo."""
+    p = pb.dib_presets("spots_worms").replace(rho=400.0)
+    x, y = pb.build_direction_sets(pb.SQUARE, 1, 13, pb.BCKind.NEUMANN)
+    ox, oy = orc.direction_sets(orc.unit_square(), 1, 13, orc.NEUMANN)
+    e0, t0 = pb.initial_fields((y.q, x.q), pb.InitialData(amplitude=2e-3, seed=7))
+    tau = 5e-3 / p.rho
+    inner = pb.InnerSolver(rule="residual", tol=1e-13, max_iter=5000)
+    tr = pb.imex_euler_rds(pb.SQUARE, x, y, 1.0, p.d_theta, pb.dib_kinetics_pair(p), p.rho, (e0, t0),
+                           pb.TimeGrid(tau, 4 * tau), inner=inner, lumped=False)
+    assert tr.diagnostics.get("loop") == "native"
+    op_p = orc.dib_params(alpha=p.alpha, gamma_k=p.gamma_k, A1=p.A1, A2=p.A2, B=p.B, C=p.C, D=p.D, k2=p.k2,
+                          k3=p.k3, d_theta=p.d_theta, rho=p.rho)
+    kin = (lambda u, v: orc.dib_rates(u, v, op_p)[0], lambda u, v: orc.dib_rates(u, v, op_p)[1])
+    ref = orc.imex_rds(ox, oy, 1.0, p.d_theta, kin, p.rho, (e0, t0), tau, 4 * tau, rule="residual", tol=1e-13,
+                       max_iter=5000, lumped=False)
+    assert np.all(np.abs(tr.iterations - ref["iterations"]) <= 1)
+    assert relerr(tr.final[0], ref["final"][0]) <= 1e-10 and relerr(tr.final[1], ref["final"][1]) <= 1e-10
