@@ -59,12 +59,12 @@ class OracleShardedDib:
         return X.numpy().copy()
 
 
-def worker(rank, world, port, mode, out_dir, N, steps):
+def worker(rank, world, port, mode, out_dir, N, steps, lumped=True):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        p, x, y, state0, tau = case(N)
+        p, x, y, state0, tau = case(N, lumped)
         lay = Layout(y.q, x.q, world, rank)
         inner = pb.InnerSolver(rule="residual", tol=1e-12, max_iter=2000)
         if mode == "cpu":
@@ -74,7 +74,7 @@ def worker(rank, world, port, mode, out_dir, N, steps):
             torch.cuda.set_device(0)
             comm, st, kin = HostStagedComm(lay), None, pb.dib_kinetics_pair(p)
         tr = sharded_imex_rds(pb.SQUARE, x, y, 1.0, p.d_theta, kin, p.rho, state0, pb.TimeGrid(tau, steps * tau),
-                              inner=inner, lumped=True, snapshot_every=2, comm=comm, stepper=st)
+                              inner=inner, lumped=lumped, snapshot_every=2, comm=comm, stepper=st)
         np.savez(os.path.join(out_dir, f"rank{rank}.npz"), U=tr.final[0], V=tr.final[1], iters=tr.iterations,
                  incs=tr.increments, snaps=[s[0] for s in tr.snapshots], c0=lay.c0)
     finally:

@@ -18,9 +18,9 @@ import paper_2109_01173_b200 as pb
 from paper_2109_01173_b200.distributed import SpeciesComm, species_parallel_imex_rds
 
 
-def case(N=15):
+def case(N=15, lumped=True):
     p = pb.dib_presets("spots_worms").replace(rho=400.0)
-    x, y = pb.build_direction_sets(pb.SQUARE, 1, N, pb.BCKind.NEUMANN, lumped=True)
+    x, y = pb.build_direction_sets(pb.SQUARE, 1, N, pb.BCKind.NEUMANN, lumped=lumped)
     e0, t0 = pb.initial_fields((y.q, x.q), pb.InitialData(amplitude=2e-3, seed=5))
     return p, x, y, (e0 - 1e-3, t0 - 1e-3), 5e-3 / p.rho
 

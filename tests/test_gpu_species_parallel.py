@@ -37,19 +37,20 @@ def test_species_parallel_cuda_matches_single_gpu_driver():
     assert relerr(parts[0]["V"], ref.final[1]) == 0.0
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_sharded_rds_cuda_matches_single_gpu_driver(world):
+@pytest.mark.parametrize("world,lumped", [(2, True), (3, True), (3, False)])
+def test_sharded_rds_cuda_matches_single_gpu_driver(world, lumped):
+    """lumped=False: the consistent mass makes the block rhs map read a 1-column halo."""
     from _sharded_rds_worker import worker as sharded_worker
     N, steps = 15, 4
     d = tempfile.mkdtemp()
-    mp.spawn(sharded_worker, args=(world, free_port(), "cuda", d, N, steps), nprocs=world, join=True)
+    mp.spawn(sharded_worker, args=(world, free_port(), "cuda", d, N, steps, lumped), nprocs=world, join=True)
     parts = [dict(np.load(os.path.join(d, f"rank{r}.npz"))) for r in range(world)]
     U = np.concatenate([p["U"] for p in parts], axis=1)
     V = np.concatenate([p["V"] for p in parts], axis=1)
-    p, x, y, state0, tau = case(N)
+    p, x, y, state0, tau = case(N, lumped)
     ref = pb.imex_euler_rds(pb.SQUARE, x, y, 1.0, p.d_theta, pb.dib_kinetics_pair(p), p.rho, state0,
                             pb.TimeGrid(tau, steps * tau),
-                            inner=pb.InnerSolver(rule="residual", tol=1e-12, max_iter=2000), lumped=True,
+                            inner=pb.InnerSolver(rule="residual", tol=1e-12, max_iter=2000), lumped=lumped,
                             snapshot_every=2)
     for r in parts:
         assert np.all(np.abs(r["iters"] - ref.iterations) <= 1)
