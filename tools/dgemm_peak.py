@@ -1,3 +1,4 @@
+"""cuBLAS DGEMM throughput at n = 2048 / 4096 / 8192 (the FP64 roofline denominator; profiles/fp64_peaks_r01.log)."""
 import torch, time
 for n in (2048, 4096, 8192):
     a = torch.randn(n, n, dtype=torch.float64, device='cuda'); b = torch.randn(n, n, dtype=torch.float64, device='cuda')

@@ -1,7 +1,7 @@
 """Small end-to-end exercise of every kernel family (a quick health check
 after kernel changes; compute-sanitizer is not available on this pool):
 
-    python tools/sanitize_probe.py
+    python tools/health_probe.py
 
 cfg3-type MO-PCG in the three preconditioner modes (banded operator pass,
 deferred U, DMMA GEMMs, SPIKE tiles and chains), a reduced solve, a native
