@@ -305,12 +305,12 @@ int make_map(CUtensorMap* map, const double* ptr, int rows, int cols, int ld) {
 int gemm_smem_bytes() { return SMEM_BYTES; }
 
 int num_sms() {
-    static int n = 0;
-    if (n == 0) {
-        int dev = 0;
+    static const int n = [] {  // thread-safe one-time query (every device of the box is a B200)
+        int dev = 0, m = 0;
         cudaGetDevice(&dev);
-        if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = kNumSMs;
-    }
+        if (cudaDeviceGetAttribute(&m, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || m <= 0) m = kNumSMs;
+        return m;
+    }();
     return n;
 }
 

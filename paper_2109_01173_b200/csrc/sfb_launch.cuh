@@ -32,14 +32,13 @@
 namespace sfb {
 
 inline bool pdl_enabled() {
-    static int on = -1;
-    if (on < 0) {
-        // on by default (measured: banded MO-PCG iteration -0.8 %, GEMM iteration
-        // -0.3 %); SYLFEM_B200_PDL=0 turns it off
+    // on by default (measured: banded MO-PCG iteration -0.8 %, GEMM iteration
+    // -0.3 %); SYLFEM_B200_PDL=0 turns it off (thread-safe one-time init)
+    static const bool on = [] {
         const char* e = std::getenv("SYLFEM_B200_PDL");
-        on = (e && std::strcmp(e, "0") == 0) ? 0 : 1;
-    }
-    return on == 1;
+        return !(e && std::strcmp(e, "0") == 0);
+    }();
+    return on;
 }
 
 // One shared-memory carveout for every kernel of the library: consecutive
@@ -48,12 +47,11 @@ inline bool pdl_enabled() {
 // everywhere keeps dependent kernels back to back.  SYLFEM_B200_CARVEOUT=0
 // leaves the driver default.
 inline bool carveout_pinned() {
-    static int on = -1;
-    if (on < 0) {
+    static const bool on = [] {
         const char* e = std::getenv("SYLFEM_B200_CARVEOUT");  // opt-in: measured neutral
-        on = (e && std::strcmp(e, "1") == 0) ? 1 : 0;
-    }
-    return on == 1;
+        return e && std::strcmp(e, "1") == 0;
+    }();
+    return on;
 }
 
 inline bool first_launch(const void* fn) {
