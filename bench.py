@@ -517,6 +517,13 @@ def run_native(args):
             "alt_preconditioner": alt or None,
             "time_to_solution": tts,
         }
+        if args.precond_mode == "banded" and hbm:
+            # no GEMM in this iteration: the dominant kernel is the banded MO-PCG pass
+            bp = hbm["banded_operator_pass"]
+            line["roofline"] = {"bound": "hbm", "kernel": bp["kernel"], "achieved": bp["achieved"],
+                                "peak": hbm["peak"], "unit": "GB/s", "frac": bp["frac"], "traffic": bp["traffic"],
+                                "algorithmic_bytes": bp["algorithmic_bytes"], "launch_ms": bp["launch_ms"],
+                                "peak_source": hbm["peak_source"], "iteration_ms": iter_ms}
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.barrier()
