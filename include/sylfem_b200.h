@@ -47,8 +47,12 @@ enum {
     SFB_PCG_MAX_ITER = 5       /* "max_iter" (report, not an error)           */
 };
 
-/* stopping rule kinds (solvers.py:53-83) */
-enum { SFB_RULE_RESIDUAL = 0, SFB_RULE_INCREMENT = 1 };
+/* stopping rule kinds (solvers.py:53-83).  SFB_RULE_BUDGET has no reference
+ * counterpart: no tolerance test, every solve runs exactly max_iter
+ * iterations and ends with SFB_PCG_MAX_ITER, which the IMEX loops then treat
+ * as a completed step rather than "did not converge" (fixed-work
+ * benchmarking, SURVEY §8 d). */
+enum { SFB_RULE_RESIDUAL = 0, SFB_RULE_INCREMENT = 1, SFB_RULE_BUDGET = 2 };
 
 /* preconditioner / spectral sandwich kinds (solvers.py:103-150, 211-300) */
 enum {

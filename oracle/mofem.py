@@ -24,7 +24,7 @@ __all__ = [
     "rect_domain", "DIRICHLET", "NEUMANN", "shape_tables", "dof_count",
     "dof_map", "assemble_dir", "assemble_lumped_dir", "direction_sets",
     "unit_degenerate", "prune_terms", "elliptic_terms", "parabolic_terms",
-    "apply_terms", "precond_factors", "LUPrecond", "spectral_cache",
+    "apply_terms", "precond_factors", "LUPrecond", "spectral_cache", "pcg_iterations",
     "reduced_solve", "mo_pcg", "imex_heat", "imex_rds", "dib_params",
     "dib_rates", "initial_fields", "full_node_grid", "expand_full",
     "interior", "seeded_modes", "OracleError", "pgm_bytes", "csv_text",
@@ -508,6 +508,40 @@ def mo_pcg(terms, rhs, pinv=None, rule=("residual", 1e-10), u0=None,
         Q *= beta
         Q += Z
     return out(max_iter, "max_iter")
+
+
+def pcg_iterations(terms, rhs, pinv, u0=None):
+    """The MO-PCG loop of solvers.py:415-452 one iteration at a time, without
+    a stop test: a generator whose first ``next()`` runs the setup part
+    (solvers.py:389-420: R_0, Z_0, <Z_0,R_0>) and yields |R_0|, and every
+    further ``next()`` runs one iteration and yields |R_s|.  The CPU-baseline
+    timer of bench.py times the iterations individually.  Same arithmetic
+    as ``mo_pcg``."""
+    A = lambda V: apply_terms(terms, V)
+    rhs = np.asarray(rhs, float)
+    if u0 is None:
+        U = np.zeros_like(rhs)
+        R = rhs.copy()
+    else:
+        U = np.array(u0, dtype=float, copy=True)
+        R = rhs - A(U)
+    Z = pinv(R)
+    Q = Z.copy()
+    rz = float(np.vdot(Z, R))
+    yield np.linalg.norm(R)
+    while True:
+        W = A(Q)
+        alpha = rz / float(np.vdot(W, Q))
+        U += alpha * Q
+        R -= alpha * W
+        res = np.linalg.norm(R)
+        Z = pinv(R)
+        rz_new = float(np.vdot(Z, R))
+        beta = rz_new / rz
+        rz = rz_new
+        Q *= beta
+        Q += Z
+        yield res
 
 
 # ---------------------------------------------------------------------------

@@ -23,7 +23,7 @@ LIB_PATH = os.environ.get("SYLFEM_B200_LIB") or os.path.join(_HERE, "libsylfem_b
 # status codes / kinds (mirror include/sylfem_b200.h)
 OK, ERR_ARG, ERR_CUDA, ERR_NOMEM, ERR_UNSUPPORTED = 0, -1, -2, -3, -4
 PCG_RUNNING, PCG_TOLERANCE, PCG_INCREMENT, PCG_INDEFINITE, PCG_NONFINITE, PCG_MAX_ITER = range(6)
-RULE_RESIDUAL, RULE_INCREMENT = 0, 1
+RULE_RESIDUAL, RULE_INCREMENT, RULE_BUDGET = 0, 1, 2
 PRE_IDENTITY, PRE_INVERSE, PRE_SPECTRAL_PROD, PRE_SPECTRAL_SUM, PRE_BANDED = range(5)
 
 EXPORTS = [

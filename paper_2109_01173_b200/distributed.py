@@ -296,10 +296,9 @@ class CudaBackend:
             self.Linv = self.RinvT = None
         else:
             qy, qx = layout.qy, layout.qx
-            Linv = precond._inverse(precond.left, qy, left=True)
-            RinvT = np.ascontiguousarray(precond._inverse(precond.right, qx, left=False).T)
-            self.Linv = self._padded_from(Linv)
-            self.RinvT = self._padded_from(RinvT)
+            # formed on the device and kept there (no host round trip)
+            self.Linv = self.from_host(precond._inverse(precond.left, qy, left=True))
+            self.RinvT = self.from_host(precond._inverse(precond.right, qx, left=False).T)
 
     # -- helpers ------------------------------------------------------------
     def _padded(self, rows, cols):
@@ -539,7 +538,7 @@ class CudaSpeciesStepper:
             sol, it = _direct(self.op, rhs, warm)
             return sol, it, True
         rep = mo_pcg(self.op, rhs, precond=self.pre, stop=self.stop, u0=warm, max_iter=self.inner.max_iter)
-        return rep.solution, rep.iterations, rep.stop_reason != "max_iter"
+        return rep.solution, rep.iterations, rep.stop_reason != "max_iter" or self.stop.kind == "budget"
 
     def norms(self, A, B):
         from .timestepping import _norms
@@ -747,7 +746,7 @@ def sharded_imex_rds(domain, x, y, d_u: float, d_v: float, kinetics, rho: float,
                 raise BlowUpError(k, names[sp], last())
             rep = sharded_mo_pcg(st.backends[sp], comm, rhs, stop=stop, u0_local=S[sp], max_iter=inner.max_iter,
                                  keep_on_device=True)
-            if rep.stop_reason == "max_iter":
+            if rep.stop_reason == "max_iter" and stop.kind != "budget":
                 raise SolverError(f"inner PCG did not converge in {inner.max_iter} iterations")
             loc = st.norms(rep.solution, S[sp])
             dd, bad, nn = comm.allreduce([loc[0], loc[2], loc[3]])
@@ -865,7 +864,7 @@ def grouped_imex_rds(domain, x, y, d_u: float, d_v: float, kinetics, rho: float,
         if not rhs_bad[g]:
             rep = sharded_mo_pcg(st.backends[g], comm, rhs, stop=stop, u0_local=own, max_iter=inner.max_iter,
                                  keep_on_device=True)
-            ok, its, new = float(rep.stop_reason != "max_iter"), rep.iterations, rep.solution
+            ok, its, new = float(rep.stop_reason != "max_iter" or stop.kind == "budget"), rep.iterations, rep.solution
             if ok:
                 loc = st.norms(new, own)
         tab = gather([ok, float(its), loc[0], loc[1], loc[2], loc[3]])

@@ -22,6 +22,7 @@ from __future__ import annotations
 import math
 import os
 import time
+import weakref
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -73,7 +74,14 @@ class StoppingRule:
     def describe(self) -> str:
         if self.kind == "residual":
             return f"|R_s| <= {self.value:g} * |R_0|"
+        if self.kind == "budget":
+            return "fixed iteration budget (max_iter)"
         return f"|U_s+1 - U_s| <= {self.value:g}"
+
+    @property
+    def native_kind(self) -> int:
+        return {"residual": nat.RULE_RESIDUAL, "increment": nat.RULE_INCREMENT,
+                "budget": nat.RULE_BUDGET}[self.kind]
 
 
 def relative_residual(tol: float = DEFAULT_TOL) -> StoppingRule:
@@ -90,6 +98,14 @@ def reference_increment(reference_error_norm: float, fraction: float = 0.05) -> 
 
 def timestep_residual(tau: float) -> StoppingRule:
     return relative_residual(tau)
+
+
+def fixed_budget() -> StoppingRule:
+    """No tolerance test: every solve runs exactly ``max_iter`` iterations and
+    reports "max_iter" (fixed-work benchmarking, SURVEY §8 d; no reference
+    counterpart).  Inside the IMEX drivers (``InnerSolver(rule="budget")``)
+    reaching the budget completes the step instead of raising."""
+    return StoppingRule("budget", 0.0)
 
 
 # ------------------------------------------------------- preconditioner ----
@@ -248,10 +264,12 @@ class Preconditioner:
                                        nat.host_ptr(lamL), nat.host_ptr(lamR), nat.C.byref(out)),
                       "preconditioner")
         else:
+            # the inverses stay on the device (sfb_pre_create copies device to device)
             Linv = self._inverse(self.left, qy, left=True)
-            RinvT = np.ascontiguousarray(self._inverse(self.right, qx, left=False).T)
-            nat.check(L.sfb_pre_create(qy, qx, nat.PRE_INVERSE, nat.host_ptr(Linv), nat.host_ptr(RinvT),
+            RinvT = self._inverse(self.right, qx, left=False).T.contiguous()
+            nat.check(L.sfb_pre_create(qy, qx, nat.PRE_INVERSE, nat.ptr(Linv), nat.ptr(RinvT),
                                        None, None, nat.C.byref(out)), "preconditioner")
+            del Linv, RinvT
         self._handle = nat.Handle(out.value, L.sfb_pre_destroy)
         self._handle_shape = shape
         return self._handle.p
@@ -266,15 +284,17 @@ class Preconditioner:
 
     @staticmethod
     def _inverse(m, q, left: bool):
-        """Dense inverse: device banded-Cholesky sweeps over the identity for
-        SPD banded factors, host LAPACK otherwise (setup, off the loop)."""
+        """Dense inverse as a CUDA tensor (setup, off the loop): device
+        banded-Cholesky sweeps over the identity for SPD banded factors, host
+        LAPACK otherwise.  It is never staged through the host on the banded
+        route (2 x q^2 doubles per factor at q = 8192 would be 1 GB of copies)."""
+        t = nat.torch()
         if m is None:
-            return np.eye(q)
+            return t.eye(q, dtype=t.float64, device="cuda")
         ch = _cholesky_band(m, q)
         if ch is None:
-            return np.ascontiguousarray(np.linalg.inv(np.asarray(m, dtype=float)))
+            return nat.to_device(np.linalg.inv(np.asarray(m, dtype=float)))
         L = nat.lib()
-        t = nat.torch()
         one = np.ones((q, 1))
         out = nat.C.c_void_p()
         b = np.ascontiguousarray(ch[1])
@@ -287,7 +307,7 @@ class Preconditioner:
         eye = t.eye(q, dtype=t.float64, device="cuda")
         inv = t.empty_like(eye)
         nat.check(L.sfb_pre_apply(h.p, nat.ptr(eye), q, nat.ptr(inv), q, nat.stream()), "inverse")
-        return np.ascontiguousarray(inv.cpu().numpy())
+        return inv
 
     # ---- application -----------------------------------------------------
     def apply(self, U):
@@ -483,13 +503,24 @@ class SpectralCache:
         """Native reduced-solve object of (this cache, op): the sandwich and
         the residual captured into one CUDA graph (sfb_reduced_*)."""
         d = self.__dict__.setdefault("_reduced", {})
-        e = d.get(id(op))
-        if e is None or e[0] is not op:
+        key = id(op)
+        e = d.get(key)
+        if e is None or e[0]() is not op:
             L = nat.lib()
             out = nat.C.c_void_p()
             nat.check(L.sfb_reduced_create(self.native(), op.native(), nat.C.byref(out)), "reduced solve")
-            e = (op, nat.Handle(out.value, L.sfb_reduced_destroy))
-            d[id(op)] = e
+            selfref = weakref.ref(self)
+
+            def _evict(ref, key=key, selfref=selfref):
+                c = selfref()
+                ent = c.__dict__.get("_reduced", {}).get(key) if c is not None else None
+                if ent is not None and ent[0] is ref:
+                    del c.__dict__["_reduced"][key]
+
+            # weak in the operator (op._direct_cache -> this cache -> op would be a cycle);
+            # the native object keeps the operator's native handle alive itself
+            e = (weakref.ref(op, _evict), nat.Handle(out.value, L.sfb_reduced_destroy), op._handle, self._handle)
+            d[key] = e
         return e[1].p
 
     def native(self):
@@ -645,23 +676,58 @@ _REASONS = {nat.PCG_TOLERANCE: "tolerance", nat.PCG_INCREMENT: "increment", nat.
 
 
 class _PcgSolver:
-    """Device MO-PCG workspace bound to one (operator, preconditioner) pair."""
+    """Device MO-PCG workspace bound to one (operator, preconditioner) pair.
 
-    def __init__(self, op: SylvesterOperator, pre: Preconditioner):
+    It keeps the two native objects it points into (the operator's and the
+    preconditioner's handles) alive, but not the Python operator or
+    preconditioner: the cache entry lives on the operator, so a reference
+    back to it would be a cycle that only the cyclic GC frees."""
+
+    def __init__(self, op: SylvesterOperator, pre):
         L = nat.lib()
         out = nat.C.c_void_p()
         nat.check(L.sfb_pcg_create(op.native(), pre.native(op.shape), nat.C.byref(out)), "mo_pcg")
         self.handle = nat.Handle(out.value, L.sfb_pcg_destroy)
-        self.op, self.pre = op, pre
+        owner = getattr(pre, "cache", pre)  # TwoTermPreconditioner: the spectral cache owns the sandwich
+        self._keep = (op._handle, getattr(owner, "_handle", None))
 
 
-def _solver_for(op: SylvesterOperator, pre: Preconditioner) -> _PcgSolver:
+def _identity_for(op: SylvesterOperator) -> Preconditioner:
+    """One identity preconditioner per operator (mo_pcg's precond=None), so
+    repeated solves reuse one cached device solver."""
+    pre = op.__dict__.get("_identity_pre")
+    if pre is None:
+        pre = op._identity_pre = Preconditioner()
+    return pre
+
+
+def _solver_for(op: SylvesterOperator, pre) -> _PcgSolver:
+    """The cached device solver of (op, pre).  Entries are keyed by the
+    preconditioner's identity and dropped when that preconditioner dies (a
+    weak reference with an eviction callback), so a loop that builds a fresh
+    preconditioner per call does not accumulate device workspaces."""
     key = id(pre)
-    s = op._pcg_cache.get(key)
-    if s is None or s.pre is not pre:
-        s = _PcgSolver(op, pre)
-        op._pcg_cache[key] = s
-    return s
+    cache = op._pcg_cache
+    e = cache.get(key)
+    if e is not None and e[0]() is pre:
+        return e[1]
+    solver = _PcgSolver(op, pre)
+    opref = weakref.ref(op)
+
+    def _evict(ref, key=key, opref=opref):
+        o = opref()
+        if o is not None:
+            ent = o._pcg_cache.get(key)
+            if ent is not None and ent[0] is ref:
+                del o._pcg_cache[key]
+
+    cache[key] = (weakref.ref(pre, _evict), solver)
+    return solver
+
+
+def _cached_solver(op: SylvesterOperator, pre):
+    e = op._pcg_cache.get(id(pre))
+    return e[1] if e is not None and e[0]() is pre else None
 
 
 def pcg_pass_times(op: SylvesterOperator, precond: Preconditioner | None = None, reps: int = 20) -> dict:
@@ -669,9 +735,9 @@ def pcg_pass_times(op: SylvesterOperator, precond: Preconditioner | None = None,
     operator, vector update, preconditioner) on the solver that `mo_pcg`
     built for (op, precond); call after a solve.  Measurement helper for the
     roofline report (no reference counterpart)."""
-    precond = precond if precond is not None else Preconditioner()
-    s = op._pcg_cache.get(id(precond))
-    if s is None or s.pre is not precond:
+    precond = precond if precond is not None else _identity_for(op)
+    s = _cached_solver(op, precond)
+    if s is None:
         raise SolverError("pcg_pass_times needs a prior mo_pcg solve with this operator and preconditioner")
     ms = np.zeros(3)
     nat.check(nat.lib().sfb_pcg_pass_times(s.handle.p, int(reps), nat.dptr(ms)), "pass timing")
@@ -689,7 +755,7 @@ def mo_pcg(op: SylvesterOperator, rhs, precond: Preconditioner | None = None,
     if not (op.symmetric and op.positive_definite):
         raise OperatorError("mo_pcg needs an operator flagged self-adjoint positive definite")
     if precond is None:
-        precond = Preconditioner()
+        precond = _identity_for(op)
     if stop is None:
         stop = relative_residual(DEFAULT_TOL)
     t0 = time.perf_counter()
@@ -708,7 +774,7 @@ def mo_pcg(op: SylvesterOperator, rhs, precond: Preconditioner | None = None,
     incs = np.zeros(max(max_iter, 1))
     its = t.empty((max_iter + 1, qy, qx), dtype=t.float64, device="cuda") if record_iterates else None
     res = nat.PcgResult()
-    rule = nat.RULE_RESIDUAL if stop.kind == "residual" else nat.RULE_INCREMENT
+    rule = stop.native_kind
     nat.check(nat.lib().sfb_pcg_solve(
         solver.handle.p, nat.ptr(B), qx, nat.ptr(U0) if U0 is not None else None, qx, nat.ptr(U), qx,
         rule, float(stop.value), int(max_iter), nat.dptr(hist), nat.dptr(incs),

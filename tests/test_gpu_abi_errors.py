@@ -66,7 +66,7 @@ def test_pcg_shape_reports_solver_grid():
     op, rhs_of = pb.elliptic_operator(x, y, 1.0)
     pre = pb.make_preconditioner("elliptic_xnormal", x, y)
     pb.mo_pcg(op, np.ones(op.shape), precond=pre, stop=pb.relative_residual(1e-6), max_iter=50)
-    s = op._pcg_cache[id(pre)]
+    s = pb.solvers._cached_solver(op, pre)
     qy, qx = C.c_int(0), C.c_int(0)
     assert lib().sfb_pcg_shape(s.handle.p, C.byref(qy), C.byref(qx)) == nat.OK
     assert (qy.value, qx.value) == op.shape
