@@ -66,6 +66,7 @@ struct Sched {
     int KT;              // k-tiles per output tile
     long long U;         // total (tile, k-tile) iterations
     int G;               // CTAs
+    int tiles_total;     // output tiles (one <C,D> partial each)
     __device__ long long start(int c) const { return (long long)c * U / G; }
     __device__ int owner(long long i) const {  // CTA whose range holds linear iteration i
         int c = (int)((i * G) / U);
@@ -74,6 +75,13 @@ struct Sched {
         return c;
     }
 };
+
+// Parking slot of a split tile's piece: a CTA holds at most one continuation
+// piece (k0 != 0, the first work of its range) and at most one split first
+// piece (k0 == 0, the last work of its range).
+__device__ __forceinline__ size_t ws_slot(int cta, int k0) {
+    return ((size_t)2 * cta + (k0 == 0 ? 1 : 0)) * (BM * BN);
+}
 
 // Epilogue of one finished 128x128 tile (registers -> global).
 __device__ __forceinline__ double tile_epilogue(double (&acc)[MI][4][2], const GemmEpi& ep, int M, int N, int m0,
@@ -137,10 +145,13 @@ __device__ __forceinline__ double tile_epilogue(double (&acc)[MI][4][2], const G
 
 // Persistent stream-K schedule: CTA c owns the linear (tile, k-tile)
 // iterations [c U / G, (c+1) U / G).  A tile split across CTAs is finished by
-// the CTA holding its k = 0 piece (the last thing that CTA computes); the
-// other pieces are the first things their CTAs compute, are parked in `ws`
-// and counted in `flags[tile]`, so the finishing CTA never waits long.  With
-// ws == nullptr every CTA owns whole tiles (grid = tile count).
+// whichever of its pieces arrives last: the others park their partial tile in
+// `ws` and take a ticket in `flags[tile]`; the last arriver (usually the k = 0
+// piece, the last work of its CTA, which then parks nothing) sums the pieces
+// in k order and runs the epilogue.  No CTA waits on another, so the kernel is
+// deadlock-free however many kernels share the GPU.  <C,D> partials are per
+// tile, so every sum is independent of who finished.  With ws == nullptr
+// every CTA owns whole tiles (grid = tile count).
 __global__ void __launch_bounds__(NTHREADS, 1)
     dgemm_nt_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
                     int K, GemmEpi ep, Sched sc) {
@@ -181,7 +192,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
     __syncthreads();
 
-    double dot = 0.0;
+    __shared__ int s_fin;
+    __shared__ double sh_dot[NTHREADS / 32];
     double acc[MI][4][2];
     int it = 0;
     while (it < n_it) {
@@ -233,57 +245,83 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
 
         const int m0 = (tile / sc.tiles_n) * BM, n0 = (tile % sc.tiles_n) * BN;
-        if (k0 != 0) {
-            // continuation piece: park the partial tile and count it
-            double* w = ep.sk_ws + (size_t)blockIdx.x * (BM * BN);
-            #pragma unroll
-            for (int i = 0; i < MI; ++i)
+        bool finish = true;
+        if (k0 != 0 || kl != KT - 1) {
+            // split tile: the last piece to arrive finishes it (no CTA ever
+            // waits on another, so any residency order makes progress)
+            const int c_first = sc.owner((long long)tile * KT), c_last = sc.owner((long long)(tile + 1) * KT - 1);
+            const int me = (int)blockIdx.x;
+            const unsigned others = (unsigned)(c_last - c_first);
+            auto park = [&]() {
+                double* w = ep.sk_ws + ws_slot(me, k0);
                 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const int e = (i * 4 + j) * 2;
-                    __stcg(reinterpret_cast<double2*>(w + (size_t)e * NTHREADS) + threadIdx.x,
-                           make_double2(acc[i][j][0], acc[i][j][1]));
-                }
-            __threadfence();
-            __syncthreads();
-            if (threadIdx.x == 0) atomicAdd(ep.sk_flags + tile, 1u);
-        } else {
-            if (kl != KT - 1) {
-                // first piece of a split tile: fold in the continuation pieces
-                const int last = sc.owner((long long)(tile + 1) * KT - 1);
-                const unsigned expect = (unsigned)(last - (int)blockIdx.x);
+                for (int i = 0; i < MI; ++i)
+                    #pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        __stcg(reinterpret_cast<double2*>(w + (size_t)((i * 4 + j) * 2) * NTHREADS) + threadIdx.x,
+                               make_double2(acc[i][j][0], acc[i][j][1]));
+            };
+            auto fold = [&](int c, int piece_k0, bool assign) {  // acc (=|+=) parked piece of CTA c
+                const double* w = ep.sk_ws + ws_slot(c, piece_k0);
+                #pragma unroll
+                for (int i = 0; i < MI; ++i)
+                    #pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const double2 v = __ldcg(
+                            reinterpret_cast<const double2*>(w + (size_t)((i * 4 + j) * 2) * NTHREADS) + threadIdx.x);
+                        acc[i][j][0] = assign ? v.x : acc[i][j][0] + v.x;
+                        acc[i][j][1] = assign ? v.y : acc[i][j][1] + v.y;
+                    }
+            };
+            finish = false;
+            if (k0 == 0) {
+                // the k = 0 piece is the last work of its CTA and usually the last
+                // to arrive: when every other piece is already counted (parked),
+                // finish without parking it
                 if (threadIdx.x == 0) {
-                    volatile unsigned* f = ep.sk_flags + tile;
-                    while (*f < expect) __nanosleep(64);
-                    *f = 0;
+                    unsigned seen;
+                    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(ep.sk_flags + tile) : "memory");
+                    s_fin = (seen == others) ? 1 : 0;
                 }
                 __syncthreads();
-                __threadfence();
-                for (int c = (int)blockIdx.x + 1; c <= last; ++c) {
-                    const double* w = ep.sk_ws + (size_t)c * (BM * BN);
-                    #pragma unroll
-                    for (int i = 0; i < MI; ++i)
-                        #pragma unroll
-                        for (int j = 0; j < 4; ++j) {
-                            const int e = (i * 4 + j) * 2;
-                            const double2 v = __ldcg(reinterpret_cast<const double2*>(w + (size_t)e * NTHREADS) +
-                                                     threadIdx.x);
-                            acc[i][j][0] += v.x;
-                            acc[i][j][1] += v.y;
-                        }
-                }
+                finish = s_fin != 0;
             }
-            dot += tile_epilogue(acc, ep, M, N, m0, n0, wm, wn, g, t);
+            bool parked = false;
+            if (!finish) {
+                park();
+                parked = true;
+                __threadfence();
+                __syncthreads();
+                if (threadIdx.x == 0) s_fin = (atomicAdd(ep.sk_flags + tile, 1u) == others) ? 1 : 0;
+                __syncthreads();
+                finish = s_fin != 0;
+            }
+            if (finish) {
+                if (threadIdx.x == 0) ep.sk_flags[tile] = 0;  // ready for the next launch
+                __threadfence();
+                // sum the pieces in k order whoever finishes (bit-reproducible):
+                // the k = 0 piece first, then the continuations in CTA order
+                if (me != c_first) {
+                    if (!parked) park();  // our continuation is re-read in its place (same thread, L2)
+                    fold(c_first, 0, true);
+                }
+                for (int c = c_first + 1; c <= c_last; ++c) fold(c, 1, false);
+            }
+            __syncthreads();  // s_fin is rewritten by the next split piece
+        }
+        if (finish) {
+            const double d = tile_epilogue(acc, ep, M, N, m0, n0, wm, wn, g, t);
+            if (ep.mode == EPI_STORE_DOT) {  // one partial per tile: the sum order does not depend on who finished
+                const double part = block_sum<NTHREADS>(d, sh_dot);
+                if (threadIdx.x == 0) ep.partials[tile] = part;
+            }
         }
     }
 
     if (ep.mode == EPI_STORE_DOT) {
-        __shared__ double sh[NTHREADS / 32];
-        const double part = block_sum<NTHREADS>(dot, sh);
         const unsigned nblk = gridDim.x;
-        if (threadIdx.x == 0) ep.partials[blockIdx.x] = part;
         if (arrive_last(ep.counter, nblk)) {
-            const double tot = sum_partials<NTHREADS>(ep.partials, nblk, 1, sh);
+            const double tot = sum_partials<NTHREADS>(ep.partials, sc.tiles_total, 1, sh_dot);
             if (threadIdx.x == 0) {
                 *ep.counter = 0;
                 if (ep.pcg != nullptr) ep.pcg->rz_next = tot;
@@ -339,19 +377,15 @@ int launch_dgemm_nt(const double* A, int lda, const double* Bt, int ldb, int M, 
     sc.KT = (K + BK - 1) / BK;
     const int tiles = sc.tiles_n * ((M + BM - 1) / BM);
     sc.U = (long long)tiles * sc.KT;
+    sc.tiles_total = tiles;
     const bool have_ws = ep.sk_ws != nullptr && ep.sk_flags != nullptr;
     sc.G = gemm_grid_for(M, N, K, have_ws);
-    // Split tiles need all CTAs co-resident (a finishing CTA waits for the
-    // continuation pieces of later CTAs): the grid is at most one CTA per SM
-    // and each CTA fills an SM, so every CTA is resident once the previous
-    // kernel drains; continuation pieces are the first work of their CTA and
-    // never wait, so progress is guaranteed.
     return launch_kernel(dgemm_nt_kernel, dim3(sc.G), dim3(NTHREADS), SMEM_BYTES, stream, ma, mb, M, N, K, ep, sc);
 }
 
 int gemm_grid_blocks(int M, int N) { return ((N + BN - 1) / BN) * ((M + BM - 1) / BM); }
 
-size_t gemm_workspace_doubles() { return (size_t)num_sms() * BM * BN; }
+size_t gemm_workspace_doubles() { return (size_t)2 * num_sms() * BM * BN; }
 int gemm_max_tiles() { return 65536; }
 
 }  // namespace sfb

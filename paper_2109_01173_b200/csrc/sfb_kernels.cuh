@@ -30,7 +30,7 @@ struct GemmEpi {
     const double* sc = nullptr;
     const double* D = nullptr;
     int ldd = 0;
-    double* partials = nullptr;   // one per CTA (EPI_STORE_DOT)
+    double* partials = nullptr;   // one per output tile (EPI_STORE_DOT)
     unsigned* counter = nullptr;  // last-block counter (EPI_STORE_DOT)
     PcgState* pcg = nullptr;      // status gate; receives rz_next
     double* dot_out = nullptr;    // receives the dot total when non-null

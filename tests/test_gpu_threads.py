@@ -68,3 +68,43 @@ def test_concurrent_reduced_solves_and_imex():
     for tr in outs:
         assert np.array_equal(tr.final[0], ref.final[0]) and np.array_equal(tr.final[1], ref.final[1])
         assert np.array_equal(tr.iterations, ref.iterations)
+
+
+def test_concurrent_stream_k_gemms_at_full_width():
+    """At q >= 1024 every DMMA GEMM is a persistent stream-K grid of one CTA
+    per SM (148 CTAs).  Independent solver objects on their own streams, run
+    from a thread pool as the reference's harness does (harness.py:313-317),
+    launch such grids concurrently; split tiles are finished by their last
+    arriving piece, so no CTA waits on a CTA that cannot be scheduled.  Every
+    result must equal the sequential one bit for bit."""
+    work = []
+    for k, N, dom in ((1, 1025, pb.SQUARE), (2, 1040, WAVE), (1, 1100, WAVE)):
+        x, y = pb.build_direction_sets(dom, k, N, pb.BCKind.DIRICHLET)
+        op, rhs_of = pb.elliptic_operator(x, y, 1.0)
+        kind = "elliptic_xnormal" if dom is WAVE else "elliptic_square"
+        pre = pb.make_preconditioner(kind, x, y, mode="inverse")
+        assert min(op.shape) >= 1024
+        work.append(("pcg", op, pre, rhs_of(sine_source(N, N, 4))))
+    x, y = pb.build_direction_sets(pb.SQUARE, 1, 1200, pb.BCKind.DIRICHLET)
+    opr, rhs_of = pb.elliptic_operator(x, y, 1.0)
+    cache = pb.build_spectral_cache(opr)
+    rng = np.random.default_rng(11)
+    for _ in range(3):
+        work.append(("red", opr, cache, rng.standard_normal(opr.shape)))
+
+    def run(item):
+        kind, op, aux, rhs = item
+        if kind == "pcg":
+            rep = pb.mo_pcg(op, rhs, precond=aux, stop=pb.fixed_budget(), max_iter=25)
+            return rep.solution, rep.residual_history
+        return pb.solve_reduced(op, rhs, aux).solution, None
+
+    seq = [run(w) for w in work]
+    for _ in range(3):
+        with ThreadPoolExecutor(max_workers=len(work)) as pool:
+            par = list(pool.map(run, work * 2))
+        for i, (sol, hist) in enumerate(par):
+            s_sol, s_hist = seq[i % len(work)]
+            assert np.array_equal(sol, s_sol)
+            if hist is not None:
+                assert np.array_equal(hist, s_hist)
