@@ -279,6 +279,35 @@ int sfb_vec_dots(const double* A_dev, const double* B_dev, const double* C_dev,
                  const double* D_dev, int ld, int rows, int cols, double* out2_host,
                  void* stream);
 
+/* ---- device-resident sharded MO-PCG (distributed.py; reference solvers.py:
+ * 389-452 split over column shards).  The scalars live on the device: the
+ * communicator all-reduces the slot array in place (NCCL on the stream) and
+ * the host reads the state once per chunk of iterations with
+ * sfb_shard_result.  slots: [0] <W,Q>, [1] |Q|^2, [2] |R|^2, [3] <Z,R>,
+ * [4] beta.  Kernels that change the iterate are gated on the status, so
+ * iterations issued after the stop are no-ops. */
+typedef struct sfb_shard sfb_shard;
+int sfb_shard_create(int max_iter, int rule, double value, sfb_shard** out);
+int sfb_shard_destroy(sfb_shard* h);
+double* sfb_shard_slots(sfb_shard* h);
+/* slots[slot] = <A,B>, slots[slot+1] = <C,D> (C, D may be NULL) over the local block */
+int sfb_shard_dots(sfb_shard* h, const double* A_dev, int lda, const double* B_dev, int ldb,
+                   const double* C_dev, int ldc, const double* D_dev, int ldd, int rows, int cols,
+                   int slot, void* stream);
+/* after the all-reduce of slots[2..3] = {|R_0|^2, <Z_0,R_0>}: res0, history[0], rz */
+int sfb_shard_start(sfb_shard* h, void* stream);
+/* alpha = rz / slots[0] (INDEFINITE when <= 0), U += alpha Q, R -= alpha W, slots[2] = local |R|^2 */
+int sfb_shard_update(sfb_shard* h, double* U_dev, int ldu, double* R_dev, int ldr, const double* Q_dev,
+                     int ldq, const double* W_dev, int ldw, int rows, int cols, void* stream);
+/* after the all-reduce of slots[2..3]: history, increment, stop test, beta = slots[4] */
+int sfb_shard_control(sfb_shard* h, void* stream);
+/* Q = Z + beta Q (first: Q = Z), gated on the status */
+int sfb_shard_xpby(sfb_shard* h, double* Q_dev, int ldq, const double* Z_dev, int ldz, int rows,
+                   int cols, int first, void* stream);
+/* status, iterations, bad value / iteration; history (iterations + 1) and increments (iterations) */
+int sfb_shard_result(sfb_shard* h, sfb_pcg_result* res, double* hist_host, double* incs_host,
+                     void* stream);
+
 /* ---- reductions for the IMEX drivers (timestepping.py:89-91, 155, 210-215) */
 /* out4_host = { |A - B|_F (B may be NULL), max|A|, #non-finite(A), |A|_F }. */
 int sfb_diff_norm(const double* A_dev, int lda, const double* B_dev, int ldb,

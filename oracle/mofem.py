@@ -28,6 +28,7 @@ __all__ = [
     "reduced_solve", "mo_pcg", "imex_heat", "imex_rds", "dib_params",
     "dib_rates", "initial_fields", "full_node_grid", "expand_full",
     "interior", "seeded_modes", "OracleError", "pgm_bytes", "csv_text",
+    "closed_form", "direct_solve", "perturbed_apply", "iteration_envelope",
 ]
 
 DIRICHLET, NEUMANN = "dirichlet", "neumann"
@@ -446,9 +447,122 @@ def reduced_solve(terms, rhs, cache=None):
     return U, rel, cache
 
 
+def closed_form(gamma, f_int, N):
+    """k = 1 Dirichlet unit square without an eigensolver (solvers.py:303-354):
+    eigenvalues ((12N^2-g) l + 6Ng) / (12N - 2l), l = 2N(1-cos(i pi/N)), and
+    the sine basis X with X^-1 = (2/N) X.  Returns (U, spectral residual)."""
+    f_int = np.asarray(f_int, float)
+    i = np.arange(1, N)
+    la = 2.0 * N * (1.0 - np.cos(i * np.pi / N))
+    lam = ((12.0 * N * N - gamma) * la + 6.0 * N * gamma) / (12.0 * N - 2.0 * la)
+    den = lam[:, None] + lam[None, :]
+    X = np.sin(np.outer(i, i) * np.pi / N)
+    c = 2.0 / N
+    fh = c * (X @ f_int @ X)
+    U = c * (X @ (fh / den) @ X)
+    return U, np.linalg.norm(den * (c * (X @ U @ X)) - fh) / max(np.linalg.norm(fh), 1e-300)
+
+
+def direct_solve(terms, rhs):
+    """The vec-form system sum_t G_t (x) H_t^T (row-major vec) solved densely
+    (solvers.py:524-554 solves the same system by sparse LU)."""
+    K = sum(np.kron(G, H.T) for G, H in terms)
+    rhs = np.asarray(rhs, float)
+    return np.linalg.solve(K, rhs.ravel()).reshape(rhs.shape)
+
+
+def perturbed_apply(terms, variant):
+    """The operator map with one deliberate change of rounding (test-side
+    envelope of SURVEY finding 6): "reassoc" evaluates G (U H) instead of
+    (G U) H, "reverse" accumulates the terms in reverse order."""
+    if variant == "reassoc":
+        def A(U):
+            out = np.zeros((terms[0][0].shape[0], terms[0][1].shape[0]))
+            for G, H in terms:
+                out += G @ (U @ H)
+            return out
+        return A
+    if variant == "reverse":
+        return lambda U: apply_terms(terms[::-1], U)
+    raise ValueError(variant)
+
+
+def _precond_forms(pre):
+    """The same preconditioner Z = P_L^-1 R P_R^-1 in three algebraic forms:
+    LU solves (the reference), Cholesky solves (the factorization the banded
+    SPIKE form is built on) and explicit inverses (the dense-GEMM form of
+    BASELINE's north star)."""
+    forms = {"lu": pre.inverse}
+    if pre.identity:
+        return forms
+    L, R = pre.left, pre.right
+    cl = sla.cho_factor(L) if L is not None else None
+    cr = sla.cho_factor(R) if R is not None else None
+
+    def chol(X):
+        Z = sla.cho_solve(cl, X) if cl is not None else np.array(X, copy=True)
+        return sla.cho_solve(cr, Z.T).T if cr is not None else Z
+    Li = np.linalg.inv(L) if L is not None else None
+    Ri = np.linalg.inv(R) if R is not None else None
+
+    def explicit(X):
+        Z = Li @ X if Li is not None else np.array(X, copy=True)
+        return Z @ Ri if Ri is not None else Z
+    forms["cholesky"], forms["inverse"] = chol, explicit
+    return forms
+
+
+def iteration_envelope(terms, rhs, pinv=None, rule=("residual", 1e-10), u0=None, max_iter=1000, ulp_seeds=3):
+    """The reference's iteration count and the range it spans under changes
+    of rounding alone (SURVEY finding 6): (iterations, lo, hi) over
+    (a) G (U H) instead of (G U) H, (b) reversed term order and (c) the rhs
+    perturbed by ~1 ulp (relative N(0, eps) noise, `ulp_seeds` seeds), the
+    latter for every algebraic form of the preconditioner (LU / Cholesky /
+    explicit inverse, when ``pinv`` is an ``LUPrecond`` or its bound
+    ``inverse``).  A faithful implementation lands within hi - lo (+1) of
+    the reference's count."""
+    pre = getattr(pinv, "__self__", pinv) if pinv is not None else None
+    forms = _precond_forms(pre) if isinstance(pre, LUPrecond) else {"lu": pinv}
+    rhs = np.asarray(rhs, float)
+
+    def run(b, P, **kw):
+        return mo_pcg(terms, b, P, rule, u0=u0, max_iter=max_iter, **kw)["iterations"]
+    base = run(rhs, forms["lu"])
+    its = [base] + [run(rhs, forms["lu"], apply=perturbed_apply(terms, v)) for v in ("reassoc", "reverse")]
+    for P in forms.values():
+        for sd in range(ulp_seeds):
+            xi = np.random.default_rng(1000 + sd).standard_normal(rhs.shape)
+            its.append(run(rhs * (1.0 + np.finfo(float).eps * xi), P))
+    return base, min(its), max(its)
+
+
 # ---------------------------------------------------------------------------
 # MO-PCG (solvers.py:361-453)
 # ---------------------------------------------------------------------------
+
+_SMALL = 512 * 512
+_ONE = {"depth": 0}
+
+
+class _one_thread:
+    """Single-threaded BLAS for small grids (re-entrant; no-op without threadpoolctl)."""
+
+    def __enter__(self):
+        self.ctx = None
+        if _ONE["depth"] == 0:
+            try:
+                from threadpoolctl import threadpool_limits
+                self.ctx = threadpool_limits(limits=1)
+            except ImportError:
+                pass
+        _ONE["depth"] += 1
+        return self
+
+    def __exit__(self, *exc):
+        _ONE["depth"] -= 1
+        if self.ctx is not None:
+            self.ctx.unregister()
+
 
 def mo_pcg(terms, rhs, pinv=None, rule=("residual", 1e-10), u0=None,
            max_iter=1000, record=False, apply=None):
@@ -460,10 +574,13 @@ def mo_pcg(terms, rhs, pinv=None, rule=("residual", 1e-10), u0=None,
     ``apply`` overrides the operator map (used for the CPU baseline timing
     of alternative operator evaluations).
     """
+    rhs = np.asarray(rhs, float)
+    if rhs.size < _SMALL and _ONE["depth"] == 0:  # many tiny GEMMs: BLAS threads only add latency
+        with _one_thread():
+            return mo_pcg(terms, rhs, pinv, rule, u0, max_iter, record, apply)
     A = (lambda V: apply_terms(terms, V)) if apply is None else apply
     P = (lambda V: np.array(V, copy=True)) if pinv is None else pinv
     t0 = time.perf_counter()
-    rhs = np.asarray(rhs, float)
     if u0 is None:
         U = np.zeros_like(rhs)
         R = rhs.copy()

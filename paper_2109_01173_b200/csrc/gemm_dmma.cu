@@ -25,7 +25,11 @@
 #include "sfb_launch.cuh"
 #include "sfb_tma.cuh"
 
+#include <cstdlib>
+
 namespace sfb {
+
+int num_sms();
 
 namespace {
 
@@ -35,19 +39,32 @@ namespace {
 #ifndef GEMM_EMPTY
 #define GEMM_EMPTY 1  // per-stage empty barriers (1) or a CTA barrier per k-tile (0)
 #endif
-constexpr int BM = 128, BN = 128, BK = 16, STAGES = GEMM_STAGES;
+constexpr int BK = 16, STAGES = GEMM_STAGES;
 // k-tiles in flight ahead of the one being consumed: with per-stage empty
 // barriers one slot of slack lets warps drift by a k-tile without stalling
 // the issuing thread
 constexpr int LOOKAHEAD = GEMM_EMPTY ? STAGES - 2 : STAGES - 1;
 #ifndef GEMM_WM
-#define GEMM_WM 32  // rows per warp: 32 (16 warps, 128 regs; measured +4 % at q = 2047) or 64 (8 warps, 255 regs)
+#define GEMM_WM 32  // rows per warp: 32 (128 regs; measured +4 % at q = 2047 over 64 rows / 255 regs)
 #endif
 constexpr int WM = GEMM_WM, MI = WM / 8;   // warp tile WM x 32: MI x 4 DMMA 8x8 blocks
-constexpr int NWARPS = (BM / WM) * 4;      // (BM/WM) x 4 warp grid
-constexpr int NTHREADS = NWARPS * 32;
-constexpr int TILE_BYTES = BM * BK * 8;     // 16 KB per operand per stage
-constexpr int SMEM_BYTES = 2 * STAGES * TILE_BYTES + 2 * STAGES * 8 + 1024;
+
+// CTA tile BM x BN: 128 x 128 with 16 warps (one CTA per SM) for large
+// GEMMs; 64 x 64 with 4 warps (two CTAs per SM) when the 128-tiles would not
+// fill the machine (at most 64 of them: q <= 1024, the cfg1 / cfg2 reduced
+// solves), so the stream-K pieces stay short and the fix-up traffic small.
+template <int BM_, int BN_>
+struct Tile {
+    static constexpr int BM = BM_, BN = BN_;
+    static constexpr int WARPS_N = BN / 32;
+    static constexpr int NWARPS = (BM / WM) * WARPS_N;
+    static constexpr int NTHREADS = NWARPS * 32;
+    static constexpr int CTAS_PER_SM = NWARPS >= 16 ? 1 : 2;
+    static constexpr int A_BYTES = BM * BK * 8, B_BYTES = BN * BK * 8;
+    static constexpr int SMEM_BYTES = STAGES * (A_BYTES + B_BYTES) + 2 * STAGES * 8 + 1024;
+};
+using BigTile = Tile<128, 128>;
+using SmallTile = Tile<64, 64>;
 
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -79,11 +96,13 @@ struct Sched {
 // Parking slot of a split tile's piece: a CTA holds at most one continuation
 // piece (k0 != 0, the first work of its range) and at most one split first
 // piece (k0 == 0, the last work of its range).
+template <class T>
 __device__ __forceinline__ size_t ws_slot(int cta, int k0) {
-    return ((size_t)2 * cta + (k0 == 0 ? 1 : 0)) * (BM * BN);
+    return ((size_t)2 * cta + (k0 == 0 ? 1 : 0)) * (T::BM * T::BN);
 }
 
-// Epilogue of one finished 128x128 tile (registers -> global).
+// Epilogue of one finished tile (registers -> global).
+template <class T>
 __device__ __forceinline__ double tile_epilogue(double (&acc)[MI][4][2], const GemmEpi& ep, int M, int N, int m0,
                                                 int n0, int wm, int wn, int g, int t) {
     double dot = 0.0;
@@ -152,19 +171,22 @@ __device__ __forceinline__ double tile_epilogue(double (&acc)[MI][4][2], const G
 // deadlock-free however many kernels share the GPU.  <C,D> partials are per
 // tile, so every sum is independent of who finished.  With ws == nullptr
 // every CTA owns whole tiles (grid = tile count).
-__global__ void __launch_bounds__(NTHREADS, 1)
+template <class T>
+__global__ void __launch_bounds__(T::NTHREADS, T::CTAS_PER_SM)
     dgemm_nt_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
                     int K, GemmEpi ep, Sched sc) {
+    constexpr int BM = T::BM, BN = T::BN, NWARPS = T::NWARPS, NTHREADS = T::NTHREADS;
+    constexpr int A_BYTES = T::A_BYTES, B_BYTES = T::B_BYTES;
     SFB_PDL_PROLOGUE();
     if (ep.pcg != nullptr && ep.pcg->status != SFB_PCG_RUNNING) return;  // uniform gate
 
     extern __shared__ uint8_t smem_raw[];
     const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
-    const uint32_t sA = base, sB = base + STAGES * TILE_BYTES, full = base + 2 * STAGES * TILE_BYTES;
+    const uint32_t sA = base, sB = base + STAGES * A_BYTES, full = sB + STAGES * B_BYTES;
     const uint32_t empty = full + 8 * STAGES;  // one arrive per warp when it is done reading a slot
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int wm = warp >> 2, wn = warp & 3;  // (BM/WM) x 4 warps, WM x 32 each
+    const int wm = warp / T::WARPS_N, wn = warp % T::WARPS_N;  // (BM/WM) x (BN/32) warps, WM x 32 each
     const int g = lane >> 2, t = lane & 3;
     const int KT = sc.KT;
     const long long beg = sc.start(blockIdx.x), fin = sc.start(blockIdx.x + 1);
@@ -175,9 +197,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const int tile = (int)(li / KT), kt = (int)(li - (long long)tile * KT);
         const int m0 = (tile / sc.tiles_n) * BM, n0 = (tile % sc.tiles_n) * BN;
         const int sl = it % STAGES;
-        mbar_expect_tx_u32(full + 8 * sl, 2 * TILE_BYTES);
-        tma_load_u32(sA + sl * TILE_BYTES, &tmA, full + 8 * sl, kt * BK, m0);
-        tma_load_u32(sB + sl * TILE_BYTES, &tmB, full + 8 * sl, kt * BK, n0);
+        mbar_expect_tx_u32(full + 8 * sl, A_BYTES + B_BYTES);
+        tma_load_u32(sA + sl * A_BYTES, &tmA, full + 8 * sl, kt * BK, m0);
+        tma_load_u32(sB + sl * B_BYTES, &tmB, full + 8 * sl, kt * BK, n0);
     };
 
     if (threadIdx.x == 0) {
@@ -219,8 +241,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             if (threadIdx.x == 0 && it + LOOKAHEAD < n_it) issue(it + LOOKAHEAD);
 #endif
             mbar_wait_u32(full + 8 * s, (it / STAGES) & 1);
-            const uint32_t a_base = sA + s * TILE_BYTES + (wm * WM + g) * 128;
-            const uint32_t b_base = sB + s * TILE_BYTES + (wn * 32 + g) * 128;
+            const uint32_t a_base = sA + s * A_BYTES + (wm * WM + g) * 128;
+            const uint32_t b_base = sB + s * B_BYTES + (wn * 32 + g) * 128;
             #pragma unroll
             for (int half = 0; half < 2; ++half) {
                 const uint32_t ch = ((2 * t + half) ^ g) << 4;  // SWIZZLE_128B: chunk ^= row & 7 (= g)
@@ -253,7 +275,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             const int me = (int)blockIdx.x;
             const unsigned others = (unsigned)(c_last - c_first);
             auto park = [&]() {
-                double* w = ep.sk_ws + ws_slot(me, k0);
+                double* w = ep.sk_ws + ws_slot<T>(me, k0);
                 #pragma unroll
                 for (int i = 0; i < MI; ++i)
                     #pragma unroll
@@ -262,7 +284,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                                make_double2(acc[i][j][0], acc[i][j][1]));
             };
             auto fold = [&](int c, int piece_k0, bool assign) {  // acc (=|+=) parked piece of CTA c
-                const double* w = ep.sk_ws + ws_slot(c, piece_k0);
+                const double* w = ep.sk_ws + ws_slot<T>(c, piece_k0);
                 #pragma unroll
                 for (int i = 0; i < MI; ++i)
                     #pragma unroll
@@ -310,7 +332,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             __syncthreads();  // s_fin is rewritten by the next split piece
         }
         if (finish) {
-            const double d = tile_epilogue(acc, ep, M, N, m0, n0, wm, wn, g, t);
+            const double d = tile_epilogue<T>(acc, ep, M, N, m0, n0, wm, wn, g, t);
             if (ep.mode == EPI_STORE_DOT) {  // one partial per tile: the sum order does not depend on who finished
                 const double part = block_sum<NTHREADS>(d, sh_dot);
                 if (threadIdx.x == 0) ep.partials[tile] = part;
@@ -331,16 +353,54 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
 }
 
-int make_map(CUtensorMap* map, const double* ptr, int rows, int cols, int ld) {
+int make_map(CUtensorMap* map, const double* ptr, int rows, int cols, int ld, int box_rows) {
     if (!tma_aligned(ptr, ld)) return arg_error("DMMA GEMM operands need 16-byte aligned rows (even leading dimension)");
     const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-    const cuuint32_t box[2] = {BK, BM};
+    const cuuint32_t box[2] = {BK, (cuuint32_t)box_rows};
     return tma_make_map(map, ptr, 2, dims, ld, box, CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
-}  // namespace
+inline int tiles_of(int M, int N, int bm, int bn) { return ((N + bn - 1) / bn) * ((M + bm - 1) / bm); }
 
-int gemm_smem_bytes() { return SMEM_BYTES; }
+// SYLFEM_B200_GEMM_TILE=128|64 forces one tile shape (measurement switch);
+// default: 64 x 64 tiles when the 128 x 128 tiles would not fill the SMs.
+int tile_mode() {
+    static const int m = [] {
+        const char* e = std::getenv("SYLFEM_B200_GEMM_TILE");
+        return e == nullptr ? 0 : std::atoi(e);
+    }();
+    return m;
+}
+
+template <class T>
+int launch_tile(const double* A, int lda, const double* Bt, int ldb, int M, int N, int K, const GemmEpi& ep,
+                cudaStream_t stream) {
+    SFB_TRY(ensure_dynamic_smem(dgemm_nt_kernel<T>, T::SMEM_BYTES));
+    CUtensorMap ma, mb;
+    SFB_TRY(make_map(&ma, A, M, K, lda, T::BM));
+    SFB_TRY(make_map(&mb, Bt, N, K, ldb, T::BN));
+    Sched sc;
+    sc.tiles_n = (N + T::BN - 1) / T::BN;
+    sc.KT = (K + BK - 1) / BK;
+    const int tiles = tiles_of(M, N, T::BM, T::BN);
+    sc.U = (long long)tiles * sc.KT;
+    sc.tiles_total = tiles;
+    const bool have_ws = ep.sk_ws != nullptr && ep.sk_flags != nullptr;
+    // stream-K grid: at most CTAS_PER_SM CTAs per SM and a few k-tiles of
+    // work per CTA; tile-aligned data-parallel grid when that already fills
+    // the machine evenly or no workspace is available
+    const int slots = num_sms() * T::CTAS_PER_SM;
+    if (!have_ws || tiles % slots == 0) {
+        sc.G = tiles;
+    } else {
+        const long long min_work = T::BM >= 128 ? 8 : 4;
+        sc.G = (int)std::max(1LL, std::min<long long>(slots, sc.U / min_work));
+    }
+    return launch_kernel(dgemm_nt_kernel<T>, dim3(sc.G), dim3(T::NTHREADS), T::SMEM_BYTES, stream, ma, mb, M, N, K,
+                         ep, sc);
+}
+
+}  // namespace
 
 int num_sms() {
     static const int n = [] {  // thread-safe one-time query (every device of the box is a B200)
@@ -352,40 +412,28 @@ int num_sms() {
     return n;
 }
 
-// Grid of the stream-K schedule (at most one CTA per SM, at least ~8 k-tiles
-// of work per CTA); tile-aligned data-parallel grid when that already fills
-// the machine evenly or no workspace is available.
-int gemm_grid_for(int M, int N, int K, bool have_ws) {
-    const int tiles = ((N + BN - 1) / BN) * ((M + BM - 1) / BM);
-    const int KT = (K + BK - 1) / BK;
-    const int sms = num_sms();
-    if (!have_ws || tiles % sms == 0) return tiles;
-    const long long U = (long long)tiles * KT;
-    return (int)std::max(1LL, std::min<long long>(sms, U / 8));
-}
-
 // C[M x N] = A[M x K] * Bt[N x K]^T, both row-major K-contiguous.
 int launch_dgemm_nt(const double* A, int lda, const double* Bt, int ldb, int M, int N, int K,
                     const GemmEpi& ep, cudaStream_t stream) {
-    SFB_TRY(ensure_dynamic_smem(dgemm_nt_kernel, SMEM_BYTES));
     if (M <= 0 || N <= 0 || K <= 0) return arg_error("empty GEMM");
-    CUtensorMap ma, mb;
-    SFB_TRY(make_map(&ma, A, M, K, lda));
-    SFB_TRY(make_map(&mb, Bt, N, K, ldb));
-    Sched sc;
-    sc.tiles_n = (N + BN - 1) / BN;
-    sc.KT = (K + BK - 1) / BK;
-    const int tiles = sc.tiles_n * ((M + BM - 1) / BM);
-    sc.U = (long long)tiles * sc.KT;
-    sc.tiles_total = tiles;
-    const bool have_ws = ep.sk_ws != nullptr && ep.sk_flags != nullptr;
-    sc.G = gemm_grid_for(M, N, K, have_ws);
-    return launch_kernel(dgemm_nt_kernel, dim3(sc.G), dim3(NTHREADS), SMEM_BYTES, stream, ma, mb, M, N, K, ep, sc);
+    const int mode = tile_mode();
+    // measured: 64-tiles win below ~64 128-tiles (q = 256: 22 vs 38 us; q = 512:
+    // 27 vs 38 us), tie at 64 (q = 1024), lose from ~100 (q = 1536: 240 vs 228 us)
+    const bool small = mode == 64 || (mode != 128 && tiles_of(M, N, 128, 128) <= 64);
+    return small ? launch_tile<SmallTile>(A, lda, Bt, ldb, M, N, K, ep, stream)
+                 : launch_tile<BigTile>(A, lda, Bt, ldb, M, N, K, ep, stream);
 }
 
-int gemm_grid_blocks(int M, int N) { return ((N + BN - 1) / BN) * ((M + BM - 1) / BM); }
+// Upper bound of the output tiles of any tile shape (one <C,D> partial each).
+int gemm_grid_blocks(int M, int N) { return tiles_of(M, N, SmallTile::BM, SmallTile::BN); }
 
-size_t gemm_workspace_doubles() { return (size_t)2 * num_sms() * BM * BN; }
+int gemm_smem_bytes() { return BigTile::SMEM_BYTES; }
+
+// Stream-K parking: two slots per CTA of the largest grid of either shape.
+size_t gemm_workspace_doubles() {
+    return std::max((size_t)2 * num_sms() * BigTile::CTAS_PER_SM * BigTile::BM * BigTile::BN,
+                    (size_t)2 * num_sms() * SmallTile::CTAS_PER_SM * SmallTile::BM * SmallTile::BN);
+}
 int gemm_max_tiles() { return 65536; }
 
 }  // namespace sfb

@@ -124,6 +124,15 @@ int launch_sh_update(double* U, double* R, const double* Q, const double* W, int
                      double alpha, double* partials, RedSlots* out, cudaStream_t s);
 int launch_sh_xpby(double* Q, int ldq, const double* Z, int ldz, int rows, int cols, double beta, int first,
                    cudaStream_t s);
+int launch_shard_dots(const double* A, int lda, const double* B, int ldb, const double* C, int ldc, const double* D,
+                      int ldd, int rows, int cols, double* partials, unsigned* counter, double* out0, double* out1,
+                      cudaStream_t s);
+int launch_shard_update(double* U, int ldu, double* R, int ldr, const double* Q, int ldq, const double* W, int ldw,
+                        int rows, int cols, PcgState* st, double* slots, double* partials, cudaStream_t s);
+int launch_shard_start(PcgState* st, double* slots, double* hist, cudaStream_t s);
+int launch_shard_control(PcgState* st, double* slots, double* hist, double* incs, cudaStream_t s);
+int launch_shard_xpby(double* Q, int ldq, const double* Z, int ldz, int rows, int cols, const PcgState* st,
+                      const double* slots, int first, cudaStream_t s);
 int launch_sh_dots(const double* A, const double* B, const double* C, const double* D, int ld, int rows, int cols,
                    double* partials, RedSlots* out, cudaStream_t s);
 

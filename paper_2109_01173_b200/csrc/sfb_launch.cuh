@@ -87,10 +87,11 @@ inline int ensure_dynamic_smem(void (*kernel)(KArgs...), size_t bytes) {
 template <typename... KArgs>
 inline void pin_carveout(void (*kernel)(KArgs...)) {
     if (first_launch(reinterpret_cast<const void*>(kernel))) {
+        // a hint only: its own failure is ignored without touching errors
+        // pending from earlier asynchronous work
         if (carveout_pinned())
-            cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                 (int)cudaSharedmemCarveoutMaxShared);
-        cudaGetLastError();
+            (void)cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                       (int)cudaSharedmemCarveoutMaxShared);
     }
 }
 

@@ -955,8 +955,8 @@ int sfb_reduced_create(const sfb_pre* pre, const sfb_op* op, sfb_reduced** out) 
                 c = pre_apply_impl(pre, r->B, r->ld, r->U, r->ld, r->T1, r->ldt1, r->T2, r->ld, r->parts, nullptr,
                                    r->red + 2, &r->gw, st);
             if (c == SFB_OK) c = op_apply_impl(op, r->U, r->ld, r->W, r->ld, r->T1, r->ldt1, &r->gw, st);
-            if (c == SFB_OK) c = launch_norms(r->W, r->ld, r->B, r->ld, r->qy, r->qx, r->parts, r->red, st);
-            if (c == SFB_OK) c = launch_norms(r->B, r->ld, nullptr, 0, r->qy, r->qx, r->parts, r->red + 1, st);
+            // one pass: red[0] = { |B - W|, max|B|, #non-finite, |B| }
+            if (c == SFB_OK) c = launch_norms(r->B, r->ld, r->W, r->ld, r->qy, r->qx, r->parts, r->red, st);
             const cudaError_t e = cudaStreamEndCapture(st, &graph);
             rc = c != SFB_OK ? c : (e == cudaSuccess ? SFB_OK : SFB_ERR_CUDA);
             if (rc == SFB_OK && cudaGraphInstantiate(&r->exec, graph, 0) != cudaSuccess) rc = SFB_ERR_CUDA;
@@ -986,11 +986,10 @@ int sfb_reduced_solve(sfb_reduced* r, const double* B, int ldb, double* U, int l
     SFB_CUDA_TRY(cudaMemcpy2DAsync(U, (size_t)ldu * 8, r->U, (size_t)r->ld * 8, (size_t)r->qx * 8, r->qy,
                                    cudaMemcpyDeviceToDevice, st));
     if (res2_host) {
-        SFB_CUDA_TRY(cudaMemcpyAsync(r->host, &r->red[0].v[0], 8, cudaMemcpyDeviceToHost, st));
-        SFB_CUDA_TRY(cudaMemcpyAsync(r->host + 1, &r->red[1].v[0], 8, cudaMemcpyDeviceToHost, st));
+        SFB_CUDA_TRY(cudaMemcpyAsync(r->host, &r->red[0].v[0], 4 * sizeof(double), cudaMemcpyDeviceToHost, st));
         SFB_CUDA_TRY(cudaStreamSynchronize(st));
-        res2_host[0] = r->host[0];
-        res2_host[1] = r->host[1];
+        res2_host[0] = r->host[0];  // |B - U|-residual numerator
+        res2_host[1] = r->host[3];  // |B|
     }
     SFB_CUDA_TRY(cudaEventRecord(r->ev_out, st));
     SFB_CUDA_TRY(cudaStreamWaitEvent(cs, r->ev_out, 0));
@@ -1342,15 +1341,16 @@ int sfb_copy2d(double* dst, int ldd, const double* src, int lds, int rows, int c
 // travels with the handle.
 int sfb_ipc_get_handle(const void* ptr, unsigned char* handle64, unsigned long long* offset) {
     if (!ptr || !handle64 || !offset) return arg_error("ipc handle: null argument");
-    static CUresult (*range)(CUdeviceptr*, size_t*, CUdeviceptr) = nullptr;
-    if (range == nullptr) {
+    using RangeFn = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+    static const RangeFn range = [] {  // thread-safe one-time lookup
         void* p = nullptr;
         cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) != cudaSuccess || !p) {
-            set_error("cuMemGetAddressRange entry point unavailable");
-            return SFB_ERR_CUDA;
-        }
-        range = reinterpret_cast<CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr)>(p);
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) != cudaSuccess) p = nullptr;
+        return reinterpret_cast<RangeFn>(p);
+    }();
+    if (range == nullptr) {
+        set_error("cuMemGetAddressRange entry point unavailable");
+        return SFB_ERR_CUDA;
     }
     CUdeviceptr base = 0;
     size_t size = 0;
@@ -1401,6 +1401,114 @@ int sfb_vec_dots(const double* A, const double* B, const double* C, const double
     return reduce_call(out2_host, 2, s, [&](double* parts, RedSlots* red) {
         return launch_sh_dots(A, B, C, D, ld, rows, cols, parts, red, s);
     });
+}
+
+// ---------------------------------- device-resident sharded MO-PCG state --
+// One object per sharded solve: the PcgState, the all-reduce slots and the
+// history live on the device; the host reads them once per chunk of
+// iterations (sfb_shard_result), never inside the iteration.
+struct sfb_shard {
+    PcgState* st = nullptr;
+    double* slots = nullptr;  // [8]: <W,Q>, |Q|^2, |R|^2, <Z,R>, beta (local sums, all-reduced in place)
+    double* hist = nullptr;   // [max_iter + 1]
+    double* incs = nullptr;   // [max(max_iter, 1)]
+    double* partials = nullptr;
+    unsigned* counter = nullptr;
+    int max_iter = 0;
+};
+
+int sfb_shard_destroy(sfb_shard* h) {
+    if (!h) return SFB_OK;
+    for (void* p : {(void*)h->st, (void*)h->slots, (void*)h->hist, (void*)h->incs, (void*)h->partials,
+                    (void*)h->counter})
+        cudaFree(p);
+    delete h;
+    return SFB_OK;
+}
+
+int sfb_shard_create(int max_iter, int rule, double value, sfb_shard** out) {
+    if (!out || max_iter < 0) return arg_error("shard state: bad argument");
+    if (rule != SFB_RULE_RESIDUAL && rule != SFB_RULE_INCREMENT && rule != SFB_RULE_BUDGET)
+        return arg_error("shard state: unknown stopping rule");
+    auto* h = new sfb_shard;
+    h->max_iter = max_iter;
+    int rc = talloc(&h->st, sizeof(PcgState));
+    if (rc == SFB_OK) rc = talloc(&h->slots, 8 * sizeof(double));
+    if (rc == SFB_OK) rc = talloc(&h->hist, (size_t)(max_iter + 1) * sizeof(double));
+    if (rc == SFB_OK) rc = talloc(&h->incs, (size_t)std::max(max_iter, 1) * sizeof(double));
+    if (rc == SFB_OK) rc = talloc(&h->partials, (size_t)2 * vector_grid_blocks() * sizeof(double));
+    if (rc == SFB_OK) rc = talloc(&h->counter, 4 * sizeof(unsigned));
+    if (rc == SFB_OK) {
+        PcgState st{};
+        st.status = SFB_PCG_RUNNING;
+        st.max_iter = max_iter;
+        st.rule = rule;
+        st.value = value;
+        st.recorded = -1;
+        if (cudaMemcpy(h->st, &st, sizeof(st), cudaMemcpyHostToDevice) != cudaSuccess ||
+            cudaMemset(h->slots, 0, 8 * sizeof(double)) != cudaSuccess ||
+            cudaMemset(h->counter, 0, 4 * sizeof(unsigned)) != cudaSuccess) {
+            set_error("shard state: initialisation failed");
+            rc = SFB_ERR_CUDA;
+        }
+    }
+    if (rc != SFB_OK) {
+        sfb_shard_destroy(h);
+        return rc;
+    }
+    *out = h;
+    return SFB_OK;
+}
+
+double* sfb_shard_slots(sfb_shard* h) { return h ? h->slots : nullptr; }
+
+int sfb_shard_dots(sfb_shard* h, const double* A, int lda, const double* B, int ldb, const double* C, int ldc,
+                   const double* D, int ldd, int rows, int cols, int slot, void* stream) {
+    if (!h || !A || !B || slot < 0 || slot + (C ? 1 : 0) > 7) return arg_error("shard dots: bad argument");
+    return launch_shard_dots(A, lda, B, ldb, C, ldc, D, ldd, rows, cols, h->partials, h->counter, h->slots + slot,
+                             C ? h->slots + slot + 1 : nullptr, (cudaStream_t)stream);
+}
+
+int sfb_shard_start(sfb_shard* h, void* stream) {
+    if (!h) return arg_error("shard start: null state");
+    return launch_shard_start(h->st, h->slots, h->hist, (cudaStream_t)stream);
+}
+
+int sfb_shard_update(sfb_shard* h, double* U, int ldu, double* R, int ldr, const double* Q, int ldq, const double* W,
+                     int ldw, int rows, int cols, void* stream) {
+    if (!h || !U || !R || !Q || !W) return arg_error("shard update: null argument");
+    return launch_shard_update(U, ldu, R, ldr, Q, ldq, W, ldw, rows, cols, h->st, h->slots, h->partials,
+                               (cudaStream_t)stream);
+}
+
+int sfb_shard_control(sfb_shard* h, void* stream) {
+    if (!h) return arg_error("shard control: null state");
+    return launch_shard_control(h->st, h->slots, h->hist, h->incs, (cudaStream_t)stream);
+}
+
+int sfb_shard_xpby(sfb_shard* h, double* Q, int ldq, const double* Z, int ldz, int rows, int cols, int first,
+                   void* stream) {
+    if (!h || !Q || !Z) return arg_error("shard xpby: null argument");
+    return launch_shard_xpby(Q, ldq, Z, ldz, rows, cols, h->st, h->slots, first, (cudaStream_t)stream);
+}
+
+int sfb_shard_result(sfb_shard* h, sfb_pcg_result* res, double* hist_host, double* incs_host, void* stream) {
+    if (!h || !res) return arg_error("shard result: null argument");
+    cudaStream_t s = (cudaStream_t)stream;
+    PcgState st;
+    SFB_CUDA_TRY(cudaMemcpyAsync(&st, h->st, sizeof(st), cudaMemcpyDeviceToHost, s));
+    SFB_CUDA_TRY(cudaStreamSynchronize(s));
+    res->iterations = st.iter;
+    res->stop_reason = st.status;
+    res->bad_iter = st.bad_iter;
+    res->bad_value = st.bad_value;
+    res->res0 = st.res0;
+    res->chunks = 0;
+    res->device_ms = 0.0;
+    if (hist_host) SFB_CUDA_TRY(cudaMemcpy(hist_host, h->hist, (size_t)(st.iter + 1) * 8, cudaMemcpyDeviceToHost));
+    if (incs_host && st.iter > 0)
+        SFB_CUDA_TRY(cudaMemcpy(incs_host, h->incs, (size_t)st.iter * 8, cudaMemcpyDeviceToHost));
+    return SFB_OK;
 }
 
 // ------------------------------------------------------------ reductions --

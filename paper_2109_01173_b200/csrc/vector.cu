@@ -384,9 +384,15 @@ __global__ void __launch_bounds__(VT) norms_kernel(const double* A, int lda, con
         const double t0 = sum_partials<VT>(partials, nb, 1, sh);
         const double t2 = sum_partials<VT>(partials + 2 * nb, nb, 1, sh);
         const double t3 = sum_partials<VT>(partials + 3 * nb, nb, 1, sh);
+        double m = 0.0;  // max over the block maxima, by the whole block (a serial
+        for (unsigned i = threadIdx.x; i < nb; i += VT) m = fmax(m, __ldcg(partials + nb + i));  // loop cost ~50 us)
+        #pragma unroll
+        for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+        __syncthreads();
+        if ((threadIdx.x & 31) == 0) smx[threadIdx.x >> 5] = m;
+        __syncthreads();
         if (threadIdx.x == 0) {
-            double m = 0.0;
-            for (unsigned i = 0; i < nb; ++i) m = fmax(m, __ldcg(partials + nb + i));
+            for (int i = 0; i < VT / 32; ++i) m = fmax(m, smx[i]);
             out->counter[0] = 0;
             out->v[0] = sqrt(t0);
             out->v[1] = m;
@@ -459,7 +465,151 @@ __global__ void __launch_bounds__(VT) sh_dots_kernel(const double* A, const doub
     }
 }
 
+// ---- device-resident sharded MO-PCG (no host round trip per iteration) ----
+// The scalars of the column-sharded iteration live on the device: a PcgState
+// (status, alpha, rz, ...) plus a slot array whose local sums are all-reduced
+// in place by the communicator (NCCL on the stream).  Every kernel that
+// changes the iterate is gated on the status, so a host that only looks at
+// the status every few iterations sees exactly the reference trajectory.
+//   slots[0] <W,Q>  slots[1] |Q|^2  slots[2] |R|^2  slots[3] <Z,R>  slots[4] beta
+__global__ void __launch_bounds__(VT) shard_dots_kernel(const double* A, int lda, const double* B, int ldb,
+                                                        const double* C, int ldc, const double* D, int ldd,
+                                                        int rows, int cols, double* partials, unsigned* counter,
+                                                        double* out0, double* out1) {
+    SFB_PDL_PROLOGUE();
+    double ab = 0.0, cd = 0.0;
+    ROW_LOOP(rows, cols) {
+        ab = fma(A[(size_t)r * lda + cc], B[(size_t)r * ldb + cc], ab);
+        if (C) cd = fma(C[(size_t)r * ldc + cc], D[(size_t)r * ldd + cc], cd);
+    }
+    __shared__ double sh[VT / 32];
+    const double p0 = block_sum<VT>(ab, sh);
+    const double p1 = block_sum<VT>(cd, sh);
+    if (threadIdx.x == 0) {
+        partials[blockIdx.x] = p0;
+        partials[gridDim.x + blockIdx.x] = p1;
+    }
+    if (arrive_last(counter, gridDim.x)) {
+        const double t0 = sum_partials<VT>(partials, gridDim.x, 1, sh);
+        const double t1 = sum_partials<VT>(partials + gridDim.x, gridDim.x, 1, sh);
+        if (threadIdx.x == 0) {
+            *counter = 0;
+            *out0 = t0;
+            if (out1) *out1 = t1;
+        }
+    }
+}
+
+// alpha = rz / <W,Q> (global), U += alpha Q, R -= alpha W, local |R|^2 -> slots[2]
+__global__ void __launch_bounds__(VT) shard_update_kernel(double* U, int ldu, double* R, int ldr, const double* Q,
+                                                          int ldq, const double* W, int ldw, int rows, int cols,
+                                                          PcgState* st, double* slots, double* partials) {
+    SFB_PDL_PROLOGUE();
+    if (st->status != SFB_PCG_RUNNING) return;  // uniform gate
+    const double wq = slots[0];
+    const bool ok = wq > 0.0;
+    const double alpha = st->rz / wq;
+    double rr = 0.0;
+    if (ok) {
+        ROW_LOOP(rows, cols) {
+            double* u = U + (size_t)r * ldu + cc;
+            double* rp = R + (size_t)r * ldr + cc;
+            *u = __dadd_rn(*u, __dmul_rn(alpha, Q[(size_t)r * ldq + cc]));
+            const double rv = __dsub_rn(*rp, __dmul_rn(alpha, W[(size_t)r * ldw + cc]));
+            *rp = rv;
+            rr = fma(rv, rv, rr);
+        }
+    }
+    __shared__ double sh[VT / 32];
+    const double p = block_sum<VT>(rr, sh);
+    if (threadIdx.x == 0) partials[blockIdx.x] = p;
+    if (arrive_last(&st->counter[5], gridDim.x)) {
+        const double t = sum_partials<VT>(partials, gridDim.x, 1, sh);
+        if (threadIdx.x == 0) {
+            st->counter[5] = 0;
+            if (!ok) {  // solvers.py:426-429
+                st->status = SFB_PCG_INDEFINITE;
+                st->bad_value = wq;
+                st->bad_iter = st->iter;
+            } else {
+                st->alpha = alpha;
+                st->qq = slots[1];
+                slots[2] = t;
+            }
+        }
+    }
+}
+
+// after the all-reduce of {|R_0|^2, <Z_0,R_0>}: res0, history[0], rz
+__global__ void shard_start_kernel(PcgState* st, double* slots, double* hist) {
+    const double res0 = sqrt(slots[2]);
+    st->res0 = res0;
+    st->rz = slots[3];
+    hist[0] = res0;
+    st->status = res0 == 0.0 ? SFB_PCG_TOLERANCE : (st->max_iter <= 0 ? SFB_PCG_MAX_ITER : SFB_PCG_RUNNING);
+}
+
+// after the all-reduce of {|R|^2, <Z,R>}: history, increment, stop test, beta
+__global__ void shard_control_kernel(PcgState* st, double* slots, double* hist, double* incs) {
+    if (st->status != SFB_PCG_RUNNING) return;
+    pcg_finish_update(st, slots[2], hist, incs);
+    const double rz_new = slots[3];
+    slots[4] = rz_new / st->rz;
+    st->rz = rz_new;
+}
+
+// Q = Z + beta Q (first: Q = Z), gated
+__global__ void __launch_bounds__(VT) shard_xpby_kernel(double* Q, int ldq, const double* Z, int ldz, int rows,
+                                                        int cols, const PcgState* st, const double* slots,
+                                                        int first) {
+    SFB_PDL_PROLOGUE();
+    if (st->status != SFB_PCG_RUNNING) return;
+    const double beta = slots[4];
+    ROW_LOOP(rows, cols) {
+        const double z = Z[(size_t)r * ldz + cc];
+        double* q = Q + (size_t)r * ldq + cc;
+        *q = first ? z : __dadd_rn(__dmul_rn(beta, *q), z);
+    }
+}
+
 }  // namespace
+
+int launch_shard_dots(const double* A, int lda, const double* B, int ldb, const double* C, int ldc, const double* D,
+                      int ldd, int rows, int cols, double* partials, unsigned* counter, double* out0, double* out1,
+                      cudaStream_t s) {
+    SFB_TRY(launch_kernel(shard_dots_kernel, dim3(std::max(1, std::min(VB, rows))), dim3(VT), 0, s, A, lda, B, ldb,
+                          C, ldc, D, ldd, rows, cols, partials, counter, out0, out1));
+    SFB_CHECK_LAUNCH();
+    return SFB_OK;
+}
+
+int launch_shard_update(double* U, int ldu, double* R, int ldr, const double* Q, int ldq, const double* W, int ldw,
+                        int rows, int cols, PcgState* st, double* slots, double* partials, cudaStream_t s) {
+    SFB_TRY(launch_kernel(shard_update_kernel, dim3(std::max(1, std::min(VB, rows))), dim3(VT), 0, s, U, ldu, R, ldr,
+                          Q, ldq, W, ldw, rows, cols, st, slots, partials));
+    SFB_CHECK_LAUNCH();
+    return SFB_OK;
+}
+
+int launch_shard_start(PcgState* st, double* slots, double* hist, cudaStream_t s) {
+    shard_start_kernel<<<1, 1, 0, s>>>(st, slots, hist);
+    SFB_CHECK_LAUNCH();
+    return SFB_OK;
+}
+
+int launch_shard_control(PcgState* st, double* slots, double* hist, double* incs, cudaStream_t s) {
+    shard_control_kernel<<<1, 1, 0, s>>>(st, slots, hist, incs);
+    SFB_CHECK_LAUNCH();
+    return SFB_OK;
+}
+
+int launch_shard_xpby(double* Q, int ldq, const double* Z, int ldz, int rows, int cols, const PcgState* st,
+                      const double* slots, int first, cudaStream_t s) {
+    SFB_TRY(launch_kernel(shard_xpby_kernel, dim3(std::max(1, std::min(VB, rows))), dim3(VT), 0, s, Q, ldq, Z, ldz,
+                          rows, cols, st, slots, first));
+    SFB_CHECK_LAUNCH();
+    return SFB_OK;
+}
 
 // dst = src^T (rows x cols -> cols x rows) through 32 x 33 shared tiles.
 __global__ void transpose_kernel(const double* __restrict__ src, int lds, double* __restrict__ dst, int ldd,
@@ -553,7 +703,9 @@ int launch_loop_ctl(PcgState* st, unsigned long long handle, int use_handle, cud
 
 int launch_norms(const double* A, int lda, const double* B, int ldb, int rows, int cols, double* partials,
                  RedSlots* out, cudaStream_t s) {
-    SFB_TRY(launch_kernel(norms_kernel, dim3(VB), dim3(VT), 0, s, A, lda, B, ldb, rows, cols, partials, out));
+    // one block per row (ROW_LOOP): no more blocks than rows
+    SFB_TRY(launch_kernel(norms_kernel, dim3(std::max(1, std::min(VB, rows))), dim3(VT), 0, s, A, lda, B, ldb, rows,
+                          cols, partials, out));
     SFB_CHECK_LAUNCH();
     return SFB_OK;
 }

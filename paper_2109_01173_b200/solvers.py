@@ -121,7 +121,10 @@ def _lapack_band(m: Band):
 
 
 def _rcond(mat) -> float:
-    """1-norm reciprocal condition number (estimate for banded factors)."""
+    """1-norm reciprocal condition number: LAPACK's banded estimate for band
+    factors, the exact value of the reference (np.linalg.cond(., 1),
+    solvers.py:90-100) whenever the estimate lands within 100x of the guard
+    (the estimate may overstate rcond) and for dense factors."""
     if isinstance(mat, Band) and mat.half_bandwidth() <= 16:
         ab, kl, ku = _lapack_band(mat)
         anorm = float(np.max(np.asarray(abs(mat.sparse).sum(axis=0)).ravel()))
@@ -129,7 +132,10 @@ def _rcond(mat) -> float:
         if info > 0:
             return 0.0
         rc, info = lapack.dgbcon(kl, ku, lu, ipiv, anorm)
-        return float(rc) if np.isfinite(rc) else 0.0
+        rc = float(rc) if np.isfinite(rc) else 0.0
+        if rc > 100.0 * RCOND_GUARD:
+            return rc
+        mat = mat.toarray()
     try:
         c = np.linalg.cond(np.asarray(mat, dtype=float), 1)
     except np.linalg.LinAlgError:
@@ -279,6 +285,10 @@ class Preconditioner:
         if m is None:
             return np.ones(q), np.eye(q)
         A = np.asarray(m, dtype=float)
+        # the reference solves with the factor itself (LU); the spectral form
+        # is only the same preconditioner for a symmetric factor
+        if np.max(np.abs(A - A.T)) > 1e-12 * max(np.max(np.abs(A)), 1e-300):
+            raise SolverError("spectral preconditioner form needs symmetric factors; use mode='inverse'")
         lam, V = sla.eigh(0.5 * (A + A.T), driver="evd")
         return np.ascontiguousarray(lam), np.ascontiguousarray(V)
 
@@ -744,6 +754,9 @@ def pcg_pass_times(op: SylvesterOperator, precond: Preconditioner | None = None,
     return {"operator_ms": float(ms[0]), "update_ms": float(ms[1]), "preconditioner_ms": float(ms[2])}
 
 
+_ITERATES_FIRST = 64  # record_iterates: slots of the first attempt
+
+
 def mo_pcg(op: SylvesterOperator, rhs, precond: Preconditioner | None = None,
            stop: StoppingRule | None = None, u0=None, max_iter: int = DEFAULT_MAX_ITER,
            record_iterates: bool = False) -> SolveReport:
@@ -772,15 +785,28 @@ def mo_pcg(op: SylvesterOperator, rhs, precond: Preconditioner | None = None,
     U = t.empty((qy, qx), dtype=t.float64, device="cuda")
     hist = np.zeros(max_iter + 1)
     incs = np.zeros(max(max_iter, 1))
-    its = t.empty((max_iter + 1, qy, qx), dtype=t.float64, device="cuda") if record_iterates else None
-    res = nat.PcgResult()
     rule = stop.native_kind
-    nat.check(nat.lib().sfb_pcg_solve(
-        solver.handle.p, nat.ptr(B), qx, nat.ptr(U0) if U0 is not None else None, qx, nat.ptr(U), qx,
-        rule, float(stop.value), int(max_iter), nat.dptr(hist), nat.dptr(incs),
-        nat.ptr(its) if its is not None else None, max_iter + 1 if its is not None else 0,
-        nat.C.byref(res), nat.stream()), "mo_pcg")
+
+    def solve(cap):
+        its = t.empty((cap, qy, qx), dtype=t.float64, device="cuda") if cap else None
+        res = nat.PcgResult()
+        nat.check(nat.lib().sfb_pcg_solve(
+            solver.handle.p, nat.ptr(B), qx, nat.ptr(U0) if U0 is not None else None, qx, nat.ptr(U), qx,
+            rule, float(stop.value), int(max_iter), nat.dptr(hist), nat.dptr(incs),
+            nat.ptr(its) if its is not None else None, cap, nat.C.byref(res), nat.stream()), "mo_pcg")
+        return res, its
+
+    # record_iterates: the reference appends only the iterates it computes
+    # (solvers.py:400, 441-442).  Record into a modest buffer first; a longer
+    # solve is re-run with exactly n + 1 slots (every reduction is
+    # deterministic, so the second run retraces the first bit for bit).
+    cap = min(max_iter + 1, _ITERATES_FIRST) if record_iterates else 0
+    res, its = solve(cap)
     n = res.iterations
+    if record_iterates and n + 1 > cap:
+        del its
+        res, its = solve(n + 1)
+        n = res.iterations
     if res.stop_reason == nat.PCG_INDEFINITE:
         raise OperatorError("operator is not positive definite along a search direction "
                             f"(<L(Q), Q> = {res.bad_value:.3e} at iteration {res.bad_iter})")

@@ -62,6 +62,19 @@ def cosine_source_rect(N, seed):
                for m in range(8))
 
 
+def desk_cases():
+    """(k, N, domain, bc) of the reference's desk matrix (tests/conftest.py:12-22)."""
+    out = []
+    for k in (1, 2, 3, 4):
+        for n in (8, 16, 24):
+            if n % k:
+                continue
+            for name in ("square", "cap", "jar"):
+                for bc in ("d", "n"):
+                    out.append((k, n, name, bc))
+    return out
+
+
 def main():
     g = {}
     rng = np.random.default_rng(20260)
@@ -177,6 +190,49 @@ def main():
     fv, gv = sf.dib_kinetics(ee, tt, p)
     g["kin/eta"], g["kin/theta"], g["kin/f"], g["kin/g"] = ee, tt, fv, gv
     g["init/eta"], g["init/theta"] = sf.initial_fields((6, 5), sf.InitialData(amplitude=1e-3, seed=7))
+
+    # -- closed-form reduced solve, k = 1 Dirichlet square (solvers.py:303-354)
+    for gamma in (0.0, 1.0):
+        n = 16
+        x, y = sf.build_direction_sets(sf.SQUARE, 1, n, D)
+        F = sine_source(n, n, 6)
+        rep = sf.solve_reduced_closed_form(gamma, sf.interior_values(F, x, y), n)
+        tag = f"closed/g{int(gamma)}"
+        g[f"{tag}/F"], g[f"{tag}/U"] = F, rep.solution
+        g[f"{tag}/res"] = rep.residual_history
+
+    # -- the acceptance desk matrix (tests/test_acceptance.py:109-154 with
+    #    tests/conftest.py:12-30): per case a random apply, the direct
+    #    solution, the reduced and closed-form solutions where they apply and
+    #    the MO-PCG solve (reference preconditioner for Dirichlet, identity
+    #    for Neumann) ---------------------------------------------------------
+    for i, (k, n, name, bc) in enumerate(desk_cases()):
+        drng = np.random.default_rng(1234 + i)
+        bck = BCS[bc]
+        x, y = sf.build_direction_sets(sf.domain_from_name(name), k, n, bck, lumped=k == 1)
+        gamma = 0.0 if bck is D else 1.0
+        op, rhs_of = sf.elliptic_operator(x, y, gamma)
+        tag = f"desk/{i}"
+        U = drng.standard_normal(op.shape)
+        F = drng.standard_normal((y.basis.n_sub + 1, x.basis.n_sub + 1))
+        rhs = rhs_of(F)
+        g[f"{tag}/U"], g[f"{tag}/AU"] = U, op.apply(U)
+        g[f"{tag}/F"], g[f"{tag}/rhs"] = F, rhs
+        g[f"{tag}/nterms"] = np.array(len(op.terms))
+        g[f"{tag}/direct"] = sf.solve_direct(op, rhs).solution
+        if len(op.terms) == 2:
+            g[f"{tag}/reduced"] = sf.solve_reduced(op, rhs).solution
+            if k == 1 and bck is D and name == "square":
+                F0 = F.copy()
+                F0[0, :] = F0[-1, :] = F0[:, 0] = F0[:, -1] = 0.0
+                g[f"{tag}/reduced0"] = sf.solve_reduced(op, rhs_of(F0)).solution
+                g[f"{tag}/closed"] = sf.solve_reduced_closed_form(gamma, sf.interior_values(F0, x, y), n).solution
+        if bck is D:
+            pre = sf.make_preconditioner("elliptic_square" if name == "square" else "elliptic_xnormal", x, y)
+        else:
+            pre = sf.make_preconditioner("identity", x, y)
+        rep = sf.mo_pcg(op, rhs, precond=pre, stop=sf.relative_residual(1e-12), max_iter=5000)
+        g[f"{tag}/pcg"], g[f"{tag}/pcg_iters"] = rep.solution, np.array(rep.iterations)
 
     np.savez_compressed(OUT, **g)
     print(f"wrote {len(g)} arrays to {OUT} ({os.path.getsize(OUT) / 1024:.0f} KiB)")

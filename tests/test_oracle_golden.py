@@ -5,7 +5,7 @@ import numpy as np
 import pytest
 
 import oracle as orc
-from _cases import (ASM_CASES, OBC, ODOMS, OP_CASES, cosine_source_rect,
+from _cases import (ASM_CASES, DESK_CASES, OBC, ODOMS, OP_CASES, cosine_source_rect, desk_oracle,
                     sine_source)
 from conftest import relerr
 
@@ -135,3 +135,41 @@ def test_known_answers():
     Z = np.diag([2.0, 3.0])
     U, _, _ = orc.reduced_solve([(Z, np.eye(2)), (np.eye(2), Z)], np.ones((2, 2)))
     assert np.allclose(U, [[1 / 4, 1 / 5], [1 / 5, 1 / 6]], atol=1e-14)
+
+
+@pytest.mark.parametrize("gamma", [0, 1])
+def test_closed_form_matches_reference(golden, gamma):
+    tag = f"closed/g{gamma}"
+    F = golden[f"{tag}/F"]
+    U, res = orc.closed_form(float(gamma), F[1:-1, 1:-1], 16)
+    assert relerr(U, golden[f"{tag}/U"]) <= 1e-13
+    assert res <= 1e-13
+
+
+@pytest.mark.parametrize("i", range(len(DESK_CASES)), ids=lambda i: str(DESK_CASES[i]))
+def test_desk_matrix_matches_reference(golden, i):
+    """reference tests/test_acceptance.py:109-148 on the oracle: apply,
+    direct, reduced, closed form and MO-PCG against the reference's own
+    outputs on the same seeded inputs."""
+    k, n, name, bc = DESK_CASES[i]
+    x, y, gamma, terms, rhs_of, pinv = desk_oracle(i)
+    tag = f"desk/{i}"
+    assert len(terms) == int(golden[f"{tag}/nterms"])
+    assert relerr(orc.apply_terms(terms, golden[f"{tag}/U"]), golden[f"{tag}/AU"]) <= 1e-13
+    rhs = rhs_of(golden[f"{tag}/F"])
+    assert relerr(rhs, golden[f"{tag}/rhs"]) <= 1e-13
+    direct = orc.direct_solve(terms, rhs)
+    assert relerr(direct, golden[f"{tag}/direct"]) <= 1e-10
+    if len(terms) == 2:
+        U, _, _ = orc.reduced_solve(terms, rhs)
+        assert relerr(U, golden[f"{tag}/reduced"]) <= 1e-10
+        if f"{tag}/closed" in golden:
+            F0 = golden[f"{tag}/F"].copy()
+            F0[0, :] = F0[-1, :] = F0[:, 0] = F0[:, -1] = 0.0
+            Uc, _ = orc.closed_form(gamma, F0[1:-1, 1:-1], n)
+            assert relerr(Uc, golden[f"{tag}/closed"]) <= 1e-10
+    it, lo, hi = orc.iteration_envelope(terms, rhs, pinv, ("residual", 1e-12), max_iter=5000)
+    r = orc.mo_pcg(terms, rhs, pinv, ("residual", 1e-12), max_iter=5000)
+    assert r["iterations"] == it and lo <= it <= hi
+    assert abs(int(golden[f"{tag}/pcg_iters"]) - it) <= hi - lo + 1
+    assert relerr(r["solution"], golden[f"{tag}/pcg"]) <= 1e-10
