@@ -21,6 +21,14 @@ So two scalar allreduces, one halo exchange and two all-to-alls per
 iteration.  The collectives are ``torch.distributed`` (NCCL over NVLink on
 GPUs, gloo in the CPU tests); the local compute is a ``Backend`` — the CUDA
 one below (C ABI), or a numpy one in the tests.
+
+The iteration is device-resident: alpha, beta, the residual history and the
+stop test live in a device state (``sfb_shard_*``), the scalar all-reduces
+run in place on device slots (NCCL on the stream), and every kernel that
+changes the iterate is gated on the device status.  The host issues
+``check_every`` iterations back to back and reads the status once per
+chunk, so no iteration waits on the host; iterations issued after the stop
+are no-ops and the result is the per-iteration loop's.
 """
 
 from __future__ import annotations
@@ -91,6 +99,42 @@ class Comm:
         if self.L.world > 1:
             self.dist.all_reduce(t, group=self.group)
         return [float(v) for v in t.tolist()]
+
+    def allreduce_(self, t):
+        """In-place sum over the group of a (device) tensor, stream-ordered:
+        no host synchronisation with NCCL."""
+        if self.L.world > 1:
+            self.dist.all_reduce(t, group=self.group)
+        return t
+
+    def halo_(self, Xe, n: int, b: int):
+        """Fill the b-column halos of the extended block Xe = [left | X | right]
+        (q_y x (n + 2b)) from the neighbours, in place (zero at the domain ends)."""
+        L = self.L
+        if b == 0 or L.world == 1:
+            return Xe
+        if n < b:
+            raise SolverError(f"column shard of {n} columns is narrower than the halo {b}")
+        t = self.t
+        ops, recv = [], []
+        left, right = L.rank - 1, L.rank + 1
+        if left >= 0:
+            r = t.empty((Xe.shape[0], b), dtype=Xe.dtype, device=Xe.device)
+            ops.append(self.dist.P2POp(self.dist.isend, Xe[:, b:2 * b].contiguous(), self.ranks[left],
+                                       group=self.group))
+            ops.append(self.dist.P2POp(self.dist.irecv, r, self.ranks[left], group=self.group))
+            recv.append((slice(0, b), r))
+        if right < L.world:
+            r = t.empty((Xe.shape[0], b), dtype=Xe.dtype, device=Xe.device)
+            ops.append(self.dist.P2POp(self.dist.isend, Xe[:, n:n + b].contiguous(), self.ranks[right],
+                                       group=self.group))
+            ops.append(self.dist.P2POp(self.dist.irecv, r, self.ranks[right], group=self.group))
+            recv.append((slice(n + b, n + 2 * b), r))
+        for req in self.dist.batch_isend_irecv(ops):
+            req.wait()  # NCCL: the current stream waits, the host does not
+        for sl, r in recv:
+            Xe[:, sl] = r
+        return Xe
 
     def sendrecv(self, X, peer: int):
         """Swap X with the rank ``peer`` (global rank, default group)."""
@@ -274,9 +318,33 @@ class PeerTransposes:
         return self.colsT
 
 
+class _DeviceSlots:
+    """A device array owned by the library, seen by torch (in-place NCCL)."""
+
+    def __init__(self, ptr: int, n: int):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f8", "data": (ptr, False), "version": 3,
+                                         "strides": None}
+
+
+class ShardState:
+    """Device scalars of one sharded solve (sfb_shard_*): PcgState, history
+    and the all-reduce slots [<W,Q>, |Q|^2, |R|^2, <Z,R>, beta]."""
+
+    def __init__(self, max_iter: int, stop: StoppingRule):
+        import torch
+        L = nat.lib()
+        out = nat.C.c_void_p()
+        nat.check(L.sfb_shard_create(int(max_iter), stop.native_kind, float(stop.value), nat.C.byref(out)),
+                  "shard state")
+        self.handle = nat.Handle(out.value, L.sfb_shard_destroy)
+        self.max_iter = max_iter
+        self.slots = torch.as_tensor(_DeviceSlots(L.sfb_shard_slots(self.handle.p), 8), device="cuda")
+        self.host_reads = 0
+
+
 class CudaBackend:
     """Local compute of one rank through the C ABI (banded block operator,
-    DMMA GEMMs, fused vector passes)."""
+    DMMA GEMMs, fused vector passes, device-resident iteration state)."""
 
     def __init__(self, op, precond, layout: Layout):
         import torch
@@ -338,7 +406,7 @@ class CudaBackend:
     def apply_ext(self, ext):
         L = self.L
         W = self._padded(L.qy, L.n)
-        e = ext.contiguous()
+        e = ext if ext.stride(1) == 1 else ext.contiguous()  # row-strided blocks are read in place
         nat.check(nat.lib().sfb_op_apply(self._op.p, e.data_ptr(), e.stride(0), W.data_ptr(), W.stride(0),
                                          nat.stream()), "apply")
         return W
@@ -375,41 +443,87 @@ class CudaBackend:
     def to_host(self, X):
         return X.cpu().numpy()
 
+    # -- device-resident iteration state (no host round trip) -----------------
+    def state(self, max_iter, stop):
+        return ShardState(max_iter, stop)
+
+    def sdots(self, st, A, B, C=None, D=None, slot=0):
+        nat.check(nat.lib().sfb_shard_dots(
+            st.handle.p, A.data_ptr(), A.stride(0), B.data_ptr(), B.stride(0),
+            C.data_ptr() if C is not None else None, C.stride(0) if C is not None else 0,
+            D.data_ptr() if D is not None else None, D.stride(0) if D is not None else 0,
+            A.shape[0], A.shape[1], int(slot), nat.stream()), "shard dots")
+
+    def sstart(self, st):
+        nat.check(nat.lib().sfb_shard_start(st.handle.p, nat.stream()), "shard start")
+
+    def supdate(self, st, U, R, Q, W):
+        nat.check(nat.lib().sfb_shard_update(st.handle.p, U.data_ptr(), U.stride(0), R.data_ptr(), R.stride(0),
+                                             Q.data_ptr(), Q.stride(0), W.data_ptr(), W.stride(0), U.shape[0],
+                                             U.shape[1], nat.stream()), "shard update")
+
+    def scontrol(self, st):
+        nat.check(nat.lib().sfb_shard_control(st.handle.p, nat.stream()), "shard control")
+
+    def sxpby(self, st, Q, Z, first=False):
+        nat.check(nat.lib().sfb_shard_xpby(st.handle.p, Q.data_ptr(), Q.stride(0), Z.data_ptr(), Z.stride(0),
+                                           Q.shape[0], Q.shape[1], int(first), nat.stream()), "shard xpby")
+
+    def sresult(self, st, history=False):
+        """(status, iterations, bad_iter, bad_value[, history, increments]):
+        the one host synchronisation of a chunk."""
+        res = nat.PcgResult()
+        h = np.zeros(st.max_iter + 1) if history else None
+        i = np.zeros(max(st.max_iter, 1)) if history else None
+        nat.check(nat.lib().sfb_shard_result(st.handle.p, nat.C.byref(res), nat.dptr(h) if history else None,
+                                             nat.dptr(i) if history else None, nat.stream()), "shard result")
+        st.host_reads += 1
+        out = (res.stop_reason, res.iterations, res.bad_iter, res.bad_value)
+        if history:
+            out += (h[:res.iterations + 1], i[:res.iterations])
+        return out
+
+
+_STATUS = {nat.PCG_TOLERANCE: "tolerance", nat.PCG_INCREMENT: "increment", nat.PCG_MAX_ITER: "max_iter"}
+
 
 def sharded_mo_pcg(backend, comm: Comm, rhs_local, stop: StoppingRule | None = None, u0_local=None,
                    max_iter: int = 1000, identity: bool = False, keep_on_device: bool = False,
-                   peer: PeerTransposes | None = None) -> SolveReport:
+                   peer: PeerTransposes | None = None, check_every: int = 16,
+                   graph: bool = False) -> SolveReport:
     """MO-PCG over column shards; same recurrences, stop logic and report as
     solvers.mo_pcg (solvers.py:365-453).  Returns this rank's columns.
     With ``peer`` the preconditioner's transposes go over peer memory
-    (PeerTransposes) instead of the all-to-alls of ``comm``."""
+    (PeerTransposes) instead of the all-to-alls of ``comm``.
+
+    Device-resident: alpha, beta, the history and the stop test stay in the
+    backend's state, the scalar all-reduces run in place on its slots, and
+    the host reads the status once every ``check_every`` iterations
+    (``diagnostics["host_reads"]``); iterations issued after the stop are
+    gated no-ops, so the trajectory is the per-iteration loop's.  With
+    ``graph=True`` (CUDA backend with NCCL or peer-memory collectives) a
+    chunk is captured once into a CUDA graph — kernels and NCCL calls — and
+    replayed: capture would fail on any host synchronisation inside it."""
     stop = stop or relative_residual()
     t0 = time.perf_counter()
     L = comm.L
     b = getattr(backend, "b", 0)
+    n = L.n
+    st = backend.state(max_iter, stop)
     B = backend.from_host(rhs_local)
     R = backend.copy(B)
-    U = backend.zeros(L.qy, L.n)
     if u0_local is not None:
-        U = backend.from_host(u0_local)
-        W0 = backend.apply_ext(comm.halo(U, b))
-        scratch = backend.zeros(L.qy, L.n)
-        backend.update(scratch, R, backend.zeros(L.qy, L.n), W0, 1.0)  # R = rhs - L(U0)
-    rr_loc, _ = backend.dots(R, R)
-    res0 = math.sqrt(comm.allreduce([rr_loc])[0])
-    hist, incs = [res0], []
-
-    def report(n, why):
-        return SolveReport(solution=U if keep_on_device else backend.to_host(U), method="mo-pcg-sharded",
-                           iterations=n,
-                           residual_history=np.asarray(hist), stop_reason=why,
-                           wall_time=time.perf_counter() - t0,
-                           diagnostics={"dense_grid_matrices": 5, "increments": np.asarray(incs),
-                                        "stopping_rule": stop.describe(), "world": L.world,
-                                        "columns": (L.c0, L.c0 + L.n)})
-
-    if res0 == 0.0:
-        return report(0, "tolerance")
+        Ue = backend.zeros(L.qy, n + 2 * b)
+        Ue[:, b:b + n] = backend.from_host(u0_local)
+        W0 = backend.apply_ext(comm.halo_(Ue, n, b))
+        U = backend.copy(Ue[:, b:b + n])
+        scratch = backend.zeros(L.qy, n)
+        backend.update(scratch, R, backend.zeros(L.qy, n), W0, 1.0)  # R = rhs - L(U0) (setup, not the loop)
+        del Ue, W0, scratch
+    else:
+        U = backend.zeros(L.qy, n)
+    Qe = backend.zeros(L.qy, n + 2 * b)  # the direction lives inside its halo-extended block
+    Q = Qe[:, b:b + n]
 
     def precond(Rk):
         if identity:
@@ -419,33 +533,52 @@ def sharded_mo_pcg(backend, comm: Comm, rhs_local, stop: StoppingRule | None = N
         XrT = backend.right_T(comm.cols_to_rows(Rk))
         return backend.left(comm.rowsT_to_colsT(XrT))
 
+    # setup (solvers.py:389-420): |R_0|, Z_0, <Z_0, R_0>, Q_0 = Z_0
     Z = precond(R)
-    rz = comm.allreduce([backend.dots(Z, R)[0]])[0]
-    Q = backend.zeros(L.qy, L.n)
-    backend.xpby(Q, Z, 0.0, first=True)
-    for s in range(max_iter):
-        W = backend.apply_ext(comm.halo(Q, b))
-        wq, qq = comm.allreduce(list(backend.dots(W, Q, Q, Q)))
-        if wq <= 0.0:
-            raise OperatorError("operator is not positive definite along a search direction "
-                                f"(<L(Q), Q> = {wq:.3e} at iteration {s})")
-        alpha = rz / wq
-        rr_loc = backend.update(U, R, Q, W, alpha)
-        Z = precond(R)
-        rr, rz_new = comm.allreduce([rr_loc, backend.dots(Z, R)[0]])
-        res = math.sqrt(rr)
-        if not math.isfinite(res):
-            raise SolverError(f"mo_pcg residual became non-finite at iteration {s}")
-        hist.append(res)
-        incs.append(abs(alpha) * math.sqrt(qq))
-        if stop.kind == "residual" and res <= stop.value * res0:
-            return report(s + 1, "tolerance")
-        if stop.kind == "increment" and incs[-1] <= stop.value:
-            return report(s + 1, "increment")
-        beta = rz_new / rz
-        rz = rz_new
-        backend.xpby(Q, Z, beta)
-    return report(max_iter, "max_iter")
+    backend.sdots(st, R, R, Z, R, slot=2)
+    comm.allreduce_(st.slots[2:4])
+    backend.sstart(st)
+    backend.sxpby(st, Q, Z, first=True)
+    def chunk():
+        for _ in range(max(1, check_every)):
+            W = backend.apply_ext(comm.halo_(Qe, n, b))
+            backend.sdots(st, W, Q, Q, Q, slot=0)  # <W,Q>, |Q|^2
+            comm.allreduce_(st.slots[0:2])
+            backend.supdate(st, U, R, Q, W)  # alpha; U, R; |R|^2 -> slot 2
+            Z = precond(R)  # computed before the stop test: result-identical
+            backend.sdots(st, Z, R, slot=3)
+            comm.allreduce_(st.slots[2:4])
+            backend.scontrol(st)  # history, increment, stop test, beta
+            backend.sxpby(st, Q, Z)
+
+    status = backend.sresult(st)[0]
+    replay = None
+    while status == nat.PCG_RUNNING:
+        if replay is not None:
+            replay.replay()
+        else:
+            chunk()  # the first chunk runs eagerly (first-launch setup of every kernel)
+            if graph:
+                import torch
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    chunk()  # captured, not executed
+                replay = g
+                g.replay()
+        status = backend.sresult(st)[0]
+    status, iters, bad_iter, bad_value, hist, incs = backend.sresult(st, history=True)
+    if status == nat.PCG_INDEFINITE:
+        raise OperatorError("operator is not positive definite along a search direction "
+                            f"(<L(Q), Q> = {bad_value:.3e} at iteration {bad_iter})")
+    if status == nat.PCG_NONFINITE:
+        raise SolverError(f"mo_pcg residual became non-finite at iteration {bad_iter}")
+    return SolveReport(solution=U if keep_on_device else backend.to_host(U), method="mo-pcg-sharded",
+                       iterations=iters, residual_history=np.asarray(hist), stop_reason=_STATUS[status],
+                       wall_time=time.perf_counter() - t0,
+                       diagnostics={"dense_grid_matrices": 5, "increments": np.asarray(incs),
+                                    "stopping_rule": stop.describe(), "world": L.world,
+                                    "columns": (L.c0, L.c0 + L.n), "host_reads": st.host_reads,
+                                    "check_every": check_every, "graph": replay is not None})
 
 
 # =========================================================================

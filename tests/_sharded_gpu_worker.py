@@ -29,6 +29,18 @@ class HostStagedComm:
     def allreduce(self, vals):
         return self.inner.allreduce(vals)
 
+    def allreduce_(self, t):
+        h = t.cpu()
+        self.inner.allreduce_(h)
+        t.copy_(h)
+        return t
+
+    def halo_(self, Xe, n, b):
+        h = Xe.cpu()
+        self.inner.halo_(h, n, b)
+        Xe.copy_(h)
+        return Xe
+
     def halo(self, X, b):
         return self.inner.halo(X.cpu(), b).to(X.device)
 

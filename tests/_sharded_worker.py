@@ -66,6 +66,88 @@ class NumpyBackend:
     def to_host(self, X):
         return X.numpy().copy()
 
+    # -- the device-resident state protocol of sharded_mo_pcg, on the host
+    #    (the same arithmetic as the sfb_shard_* kernels) -------------------
+    def state(self, max_iter, stop):
+        return HostShardState(max_iter, stop)
+
+    def sdots(self, st, A, B, C=None, D=None, slot=0):
+        st.slots[slot] = float((A * B).sum())
+        if C is not None:
+            st.slots[slot + 1] = float((C * D).sum())
+
+    def sstart(self, st):
+        st.start()
+
+    def supdate(self, st, U, R, Q, W):
+        if st.status != 0:
+            return
+        wq = float(st.slots[0])
+        if not wq > 0.0:
+            st.status, st.bad_value, st.bad_iter = 3, wq, st.iter
+            return
+        st.alpha = st.rz / wq
+        st.qq = float(st.slots[1])
+        U += st.alpha * Q
+        R -= st.alpha * W
+        st.slots[2] = float((R * R).sum())
+
+    def scontrol(self, st):
+        st.control()
+
+    def sxpby(self, st, Q, Z, first=False):
+        if st.status != 0:
+            return
+        if first:
+            Q.copy_(Z)
+        else:
+            Q.mul_(float(st.slots[4])).add_(Z)
+
+    def sresult(self, st, history=False):
+        st.host_reads += 1
+        out = (st.status, st.iter, st.bad_iter, st.bad_value)
+        if history:
+            out += (np.asarray(st.hist), np.asarray(st.incs))
+        return out
+
+
+class HostShardState:
+    """Host twin of the sfb_shard_* device state (status codes of the C ABI)."""
+
+    def __init__(self, max_iter, stop):
+        self.slots = torch.zeros(8, dtype=torch.float64)
+        self.max_iter, self.kind, self.value = max_iter, stop.kind, stop.value
+        self.status, self.iter, self.bad_iter, self.bad_value = 0, 0, -1, 0.0
+        self.rz = self.alpha = self.qq = self.res0 = 0.0
+        self.hist, self.incs, self.host_reads = [], [], 0
+
+    def start(self):
+        self.res0 = float(np.sqrt(float(self.slots[2])))
+        self.rz = float(self.slots[3])
+        self.hist = [self.res0]
+        self.status = 1 if self.res0 == 0.0 else (5 if self.max_iter <= 0 else 0)
+
+    def control(self):
+        if self.status != 0:
+            return
+        res = float(np.sqrt(float(self.slots[2])))
+        if not np.isfinite(res):
+            self.status, self.bad_iter = 4, self.iter
+            return
+        self.hist.append(res)
+        inc = abs(self.alpha) * float(np.sqrt(self.qq))
+        self.incs.append(inc)
+        self.iter += 1
+        if self.kind == "residual" and res <= self.value * self.res0:
+            self.status = 1
+        elif self.kind == "increment" and inc <= self.value:
+            self.status = 2
+        elif self.iter >= self.max_iter:
+            self.status = 5
+        rz_new = float(self.slots[3])
+        self.slots[4] = rz_new / self.rz
+        self.rz = rz_new
+
 
 def problem(N, k=2):
     x, y = orc.direction_sets(orc.wave_domain(), k, N, orc.DIRICHLET)
@@ -106,7 +188,8 @@ def worker(rank, world, port, N, out_dir, warm):
         rep = sharded_mo_pcg(be, comm, rhs[:, lay.c0:lay.c0 + lay.n],
                              stop=orc_stop(), u0_local=u0, max_iter=5000)
         np.savez(os.path.join(out_dir, f"rank{rank}.npz"), U=rep.solution, iters=rep.iterations,
-                 hist=rep.residual_history, c0=lay.c0, n=lay.n)
+                 hist=rep.residual_history, c0=lay.c0, n=lay.n, host_reads=rep.diagnostics["host_reads"],
+                 check_every=rep.diagnostics["check_every"])
     finally:
         dist.destroy_process_group()
 

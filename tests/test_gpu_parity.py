@@ -321,6 +321,18 @@ def test_sharded_cuda_backend_single_rank_matches_mo_pcg():
                               max_iter=5000, peer=pt)
         assert rep2.iterations == rep.iterations
         assert relerr(rep2.solution, rep.solution) <= 1e-13
+        # device-resident: one host read per chunk of iterations; with graph=True
+        # a chunk (kernels + the NCCL call) is captured once and replayed --
+        # capture itself proves there is no host synchronisation inside it
+        for r in (rep, rep2):
+            assert r.diagnostics["host_reads"] <= -(-r.iterations // r.diagnostics["check_every"]) + 2
+        rep3 = sharded_mo_pcg(be, Comm(lay, torch.device("cuda")), rhs, stop=pb.relative_residual(1e-12),
+                              max_iter=5000, peer=pt, check_every=8, graph=True)
+        assert rep3.diagnostics["graph"] is True
+        assert rep3.iterations == rep2.iterations
+        assert np.array_equal(rep3.solution, rep2.solution)
+        assert np.array_equal(rep3.residual_history, rep2.residual_history)
+        assert rep3.diagnostics["host_reads"] <= -(-rep3.iterations // 8) + 3
     finally:
         dist.destroy_process_group()
 

@@ -35,5 +35,10 @@ def test_sharded_mo_pcg_matches_single_process(world, warm):
     pre = orc.LUPrecond(PL, PR)
     u0 = 1e-2 * np.random.default_rng(4).standard_normal(rhs.shape) if warm else None
     ref = orc.mo_pcg(terms, rhs, pre.inverse, ("residual", 1e-12), u0=u0, max_iter=5000)
-    assert abs(iters.pop() - ref["iterations"]) <= 1
+    it = iters.pop()
+    assert abs(it - ref["iterations"]) <= 1
     assert relerr(U, ref["solution"]) <= 1e-10
+    # device-resident loop: the host reads the state once per chunk of
+    # iterations (+ setup and the final report), never per iteration
+    for p in parts:
+        assert int(p["host_reads"]) <= -(-it // int(p["check_every"])) + 2
