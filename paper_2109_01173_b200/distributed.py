@@ -201,6 +201,13 @@ class Comm:
         parts = self._all_to_all(send, [(L.m, L.col_counts[s]) for s in range(L.world)], Xc.dtype, Xc.device)
         return self.t.cat([p.reshape(L.m, L.col_counts[s]) for s, p in enumerate(parts)], dim=1)
 
+    def rows_to_cols(self, Xr):
+        """m x q_x (row shard) -> q_y x n (column shard)."""
+        L = self.L
+        send = [Xr[:, L.col_offs[s]:L.col_offs[s] + L.col_counts[s]] for s in range(L.world)]
+        parts = self._all_to_all(send, [(L.row_counts[s], L.n) for s in range(L.world)], Xr.dtype, Xr.device)
+        return self.t.cat([p.reshape(L.row_counts[s], L.n) for s, p in enumerate(parts)], dim=0)
+
     def rowsT_to_colsT(self, XrT):
         """q_x x m (transposed row shard) -> n x q_y (transposed column shard)."""
         L = self.L
@@ -241,19 +248,22 @@ class PeerTransposes:
         # receive buffers: row shard of R (m x q_x) and transposed column shard (n x q_y)
         self.rows = backend.zeros(L.m, L.qx)
         self.colsT = backend.zeros(L.n, L.qy)
-        mine = [self._handle(self.rows), self._handle(self.colsT)]
+        self.cols = backend.zeros(L.qy, L.n)  # banded form: rows -> cols without a transpose
+        mine = [self._handle(self.rows), self._handle(self.colsT), self._handle(self.cols)]
         allh = [None] * L.world
         dist.all_gather_object(allh, mine, group=group)
         self._bases = []
-        self.peer_rows, self.peer_colsT = [], []
+        self.peer_rows, self.peer_colsT, self.peer_cols = [], [], []
         for r in range(L.world):
             if r == L.rank:
                 self.peer_rows.append((self.rows.data_ptr(), self.rows.stride(0)))
                 self.peer_colsT.append((self.colsT.data_ptr(), self.colsT.stride(0)))
+                self.peer_cols.append((self.cols.data_ptr(), self.cols.stride(0)))
                 continue
-            (hr, orr, ldr), (hc, oc, ldc) = allh[r]
+            (hr, orr, ldr), (hc, oc, ldc), (hk, ok, ldk) = allh[r]
             self.peer_rows.append((self._open(hr, orr), ldr))
             self.peer_colsT.append((self._open(hc, oc), ldc))
+            self.peer_cols.append((self._open(hk, ok), ldk))
         self._flag = torch.zeros(1, dtype=torch.float64, device="cuda") if sync == "stream" else None
 
     def _handle(self, X):
@@ -300,6 +310,19 @@ class PeerTransposes:
                                            nat.stream()), "peer copy")
         self.sync()
         return self.rows
+
+    def rows_to_cols(self, Xr):
+        """Push every rank's column block of this row shard into its column
+        buffer at this rank's row offset (P2P copies)."""
+        L = self.L
+        Xr = Xr if Xr.stride(1) == 1 else Xr.contiguous()
+        for s in range(L.world):
+            dst, ldd = self.peer_cols[s]
+            src = Xr[:, L.col_offs[s]:L.col_offs[s] + L.col_counts[s]]
+            nat.check(nat.lib().sfb_copy2d(dst + 8 * L.r0 * ldd, ldd, src.data_ptr(), Xr.stride(0), L.m,
+                                           L.col_counts[s], nat.stream()), "peer copy")
+        self.sync()
+        return self.cols
 
     def right_T_scatter(self, RinvT, R_rows):
         """X^T = P_R^-T R_rows^T with each output row stored straight into
@@ -360,8 +383,23 @@ class CudaBackend:
         nat.check(L.sfb_op_create_block(layout.qy, layout.n, layout.n + 2 * self.b, len(op.terms), w, off,
                                         nat.host_ptr(g), 0, nat.host_ptr(hl), nat.C.byref(out)), "block op")
         self._op = nat.Handle(out.value, L.sfb_op_destroy)
+        self.banded = False
         if precond.is_identity:
             self.Linv = self.RinvT = None
+        elif precond.mode == "banded":
+            # SPIKE solves on the shards: the right factor along the rows of a
+            # row shard (after the first transpose), the left factor along the
+            # columns of a column shard (reference solvers.py:134-143)
+            from .solvers import _cholesky_band
+            qy, qx = layout.qy, layout.qx
+            cl, cr = _cholesky_band(precond.left, qy), _cholesky_band(precond.right, qx)
+            if cl is None or cr is None:
+                raise SolverError("banded preconditioner mode needs symmetric positive definite "
+                                  "factors with half-bandwidth <= 4")
+            self.banded = True
+            self.Linv = self.RinvT = None
+            self._pre_rows = self._banded_pre(layout.m, qx, (0, np.ones((layout.m, 1))), cr)
+            self._pre_cols = self._banded_pre(qy, layout.n, cl, (0, np.ones((layout.n, 1))))
         else:
             qy, qx = layout.qy, layout.qx
             # formed on the device and kept there (no host round trip)
@@ -369,6 +407,27 @@ class CudaBackend:
             self.RinvT = self.from_host(precond._inverse(precond.right, qx, left=False).T)
 
     # -- helpers ------------------------------------------------------------
+    @staticmethod
+    def _banded_pre(rows, cols, left, right):
+        L = nat.lib()
+        out = nat.C.c_void_p()
+        nat.check(L.sfb_pre_create_banded(rows, cols, left[0], nat.host_ptr(np.ascontiguousarray(left[1])),
+                                          right[0], nat.host_ptr(np.ascontiguousarray(right[1])),
+                                          nat.C.byref(out)), "banded shard preconditioner")
+        return nat.Handle(out.value, L.sfb_pre_destroy)
+
+    def _pre(self, h, X, rows, cols):
+        Z = self._padded(rows, cols)
+        nat.check(nat.lib().sfb_pre_apply(h.p, X.data_ptr(), X.stride(0), Z.data_ptr(), Z.stride(0), nat.stream()),
+                  "banded shard preconditioner")
+        return Z
+
+    def right_rows(self, Xr):  # Xr P_R^-1 on a row shard (m x q_x)
+        return self._pre(self._pre_rows, Xr, self.L.m, self.L.qx)
+
+    def left_cols(self, Xc):  # P_L^-1 Xc on a column shard (q_y x n)
+        return self._pre(self._pre_cols, Xc, self.L.qy, self.L.n)
+
     def _padded(self, rows, cols):
         t = self.t
         buf = t.zeros((rows, cols + (cols % 2)), dtype=t.float64, device="cuda")
@@ -528,6 +587,9 @@ def sharded_mo_pcg(backend, comm: Comm, rhs_local, stop: StoppingRule | None = N
     def precond(Rk):
         if identity:
             return backend.copy(Rk)
+        if getattr(backend, "banded", False):  # SPIKE form: right solves on rows, left solves on columns
+            ex = peer if peer is not None else comm
+            return backend.left_cols(ex.rows_to_cols(backend.right_rows(ex.cols_to_rows(Rk))))
         if peer is not None:  # transposes over peer memory, the second fused into the GEMM
             return backend.left(peer.right_T_scatter(backend.RinvT, peer.cols_to_rows(Rk)))
         XrT = backend.right_T(comm.cols_to_rows(Rk))
@@ -579,6 +641,140 @@ def sharded_mo_pcg(backend, comm: Comm, rhs_local, stop: StoppingRule | None = N
                                     "stopping_rule": stop.describe(), "world": L.world,
                                     "columns": (L.c0, L.c0 + L.n), "host_reads": st.host_reads,
                                     "check_every": check_every, "graph": replay is not None})
+
+
+# =========================================================================
+# Column-sharded IMEX heat (cfg4 across GPUs, SURVEY §8 e)
+# =========================================================================
+#
+# imex_euler_heat (reference timestepping.py:126-159) with U column-sharded.
+# Per step: the b_rhs-column halo of U; the block rhs map W = expand(U) +
+# tau g(t_k) F (the fused heat loader of the banded map kernel on the
+# halo-extended block, with this rank's static slice of F); the blow-up
+# checks reduced over the ranks; the sharded MO-PCG warm-started from U; the
+# increment norm reduced over the ranks.  Block coordinates: input column k'
+# of the map is full-grid column c0 + cs - b + k' (cs = 1 for Dirichlet),
+# i.e. interior column c0 - b + k', so the halo-extended block of U is read
+# with no column shift and zero halos at the domain ends.
+
+
+class CudaShardedHeatStepper:
+    """Local compute of the column-sharded heat step through the C ABI."""
+
+    def __init__(self, x, y, d_u, tau, lumped, inner, source, layout: Layout):
+        from .fem1d import BCKind
+        from .operators import parabolic_operator
+        from .timestepping import SeparableSource, _parabolic_precond
+        if not isinstance(source, SeparableSource):
+            raise ConfigError("the column-sharded heat driver evaluates the source on the device: "
+                              "pass a SeparableSource")
+        if inner.method != "mo-pcg" or inner.precond == "two_term":
+            raise ConfigError("the column-sharded heat driver runs MO-PCG with the reference preconditioner")
+        import torch
+        self.t, self.L = torch, layout
+        op, rhs_of = parabolic_operator(x, y, d_u, tau, lumped=lumped)
+        pre = _parabolic_precond(x, y, d_u, tau, lumped, inner, op)
+        self.backend = CudaBackend(op, pre, layout)
+        self.g = source.time_factor
+        F = np.asarray(source.F, dtype=float)
+        if F.shape != rhs_of.in_shape:
+            raise ConfigError(f"separable source must cover the full node grid {rhs_of.in_shape}")
+        self.rs = 1 if y.basis.bc is BCKind.DIRICHLET else 0
+        cs = 1 if x.basis.bc is BCKind.DIRICHLET else 0
+        w, goff, g, hoff, h = rhs_of.layout()
+        self.b = max(0, cs - hoff, hoff - cs + w - 1)
+        n, c0, b = layout.n, layout.c0, self.b
+        ncols = n + 2 * b
+        Fb = np.zeros((F.shape[0], ncols))  # full-grid columns c0 + cs - b ... (zero outside the grid)
+        lo = c0 + cs - b
+        a0, a1 = max(lo, 0), min(lo + ncols, F.shape[1])
+        Fb[:, a0 - lo:a1 - lo] = F[:, a0:a1]
+        self.F = self.backend.from_host(Fb)
+        hl = np.ascontiguousarray(h[c0:c0 + n])
+        out = nat.C.c_void_p()
+        nat.check(nat.lib().sfb_map_create(layout.qy, n, F.shape[0], ncols, w, goff,
+                                           nat.host_ptr(np.ascontiguousarray(g)), w, hoff - cs + b,
+                                           nat.host_ptr(hl), nat.C.byref(out)), "block rhs map")
+        self._map = nat.Handle(out.value, nat.lib().sfb_map_destroy)
+
+    def to_local(self, a):
+        L = self.L
+        if nat.is_device(a):
+            return self.backend.from_host(a[:, L.c0:L.c0 + L.n])
+        return self.backend.from_host(np.asarray(a, dtype=float)[:, L.c0:L.c0 + L.n])
+
+    def rhs(self, Ue, c):
+        """local rhs of W = expand(U) + c F and local [max|W|, #non-finite(W)]."""
+        out = self.backend.zeros(self.L.qy, self.L.n)
+        chk = np.zeros(2)
+        nat.check(nat.lib().sfb_map_apply_heat(self._map.p, Ue.data_ptr(), Ue.stride(0), self.rs, 0, float(c),
+                                               self.F.data_ptr(), self.F.stride(0), out.data_ptr(), out.stride(0),
+                                               nat.dptr(chk), nat.stream()), "heat rhs")
+        return out, chk
+
+    def norms(self, A, B):
+        """local {sum (A-B)^2, max|A|, #non-finite(A), sum A^2}."""
+        out = np.zeros(4)
+        nat.check(nat.lib().sfb_diff_norm(A.data_ptr(), A.stride(0), B.data_ptr(), B.stride(0), A.shape[0],
+                                          A.shape[1], nat.dptr(out), nat.stream()), "norm")
+        return [out[0] ** 2, out[1], out[2], out[3] ** 2]
+
+    def host(self, X):
+        return nat.to_host(X)
+
+
+def sharded_imex_heat(domain, x, y, d_u: float, source, u0, grid, inner=None, lumped: bool = False,
+                      comm: Comm | None = None, stepper=None, peer_sync: str | None = None,
+                      graph: bool = False):
+    """imex_euler_heat (timestepping.py:126-159) with U column-sharded over
+    the ranks of ``comm`` (SURVEY §8 e; cfg4 at 1/2/4/8 GPUs).  ``u0`` is the
+    full initial state (each rank keeps its columns); ``source`` a
+    SeparableSource.  Returns this rank's columns in ``final``; increments
+    and iteration counts are global and equal on all ranks.  ``peer_sync``
+    ("stream" for one GPU per rank) routes the preconditioner's transposes
+    over peer memory."""
+    from .timestepping import BLOWUP_LIMIT, BlowUpError, InnerSolver, Trajectory, _step_setup
+    inner = inner or InnerSolver()
+    _step_setup(inner)
+    tau = grid.tau
+    if comm is None:
+        import torch.distributed as dist
+        comm = Comm(Layout(y.q, x.q, dist.get_world_size(), dist.get_rank()), "cuda")
+    L = comm.L
+    st = stepper or CudaShardedHeatStepper(x, y, d_u, tau, lumped, inner, source, L)
+    be = st.backend
+    peer = PeerTransposes(L, be, sync=peer_sync) if peer_sync else None
+    stop = inner.stopping(tau)
+    U = st.to_local(u0)
+    Ue = be.zeros(L.qy, L.n + 2 * st.b)
+    n = grid.n_steps
+    incs = np.empty(n)
+    iters = np.empty(n, dtype=int)
+    try:
+        for k in range(n):
+            Ue[:, st.b:st.b + L.n] = U
+            rhs, chk = st.rhs(comm.halo_(Ue, L.n, st.b), tau * float(st.g(k * tau)))
+            mx, = _allreduce_max(comm, [chk[0]])
+            cnt, = comm.allreduce([chk[1]])
+            if cnt > 0 or mx > BLOWUP_LIMIT:
+                raise BlowUpError(k, "u", st.host(U))
+            rep = sharded_mo_pcg(be, comm, rhs, stop=stop, u0_local=U, max_iter=inner.max_iter,
+                                 keep_on_device=True, peer=peer, graph=graph)
+            if rep.stop_reason == "max_iter" and stop.kind != "budget":
+                raise SolverError(f"inner PCG did not converge in {inner.max_iter} iterations")
+            loc = st.norms(rep.solution, U)
+            dd, bad = comm.allreduce([loc[0], loc[2]])
+            mx, = _allreduce_max(comm, [loc[1]])
+            if bad > 0 or mx > BLOWUP_LIMIT:
+                raise BlowUpError(k, "u", st.host(U))
+            incs[k] = math.sqrt(dd)
+            iters[k] = rep.iterations
+            U = rep.solution
+    finally:
+        if peer is not None:
+            peer.close()
+    return Trajectory(final=(st.host(U),), increments=incs, iterations=iters, times=(1 + np.arange(n)) * tau,
+                      diagnostics={"world": L.world, "columns": (L.c0, L.c0 + L.n)})
 
 
 # =========================================================================

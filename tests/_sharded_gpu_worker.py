@@ -47,6 +47,9 @@ class HostStagedComm:
     def cols_to_rows(self, Xc):
         return self.inner.cols_to_rows(Xc.cpu()).to(Xc.device)
 
+    def rows_to_cols(self, Xr):
+        return self.inner.rows_to_cols(Xr.cpu()).to(Xr.device)
+
     def rowsT_to_colsT(self, XrT):
         return self.inner.rowsT_to_colsT(XrT.cpu()).to(XrT.device)
 
@@ -57,20 +60,20 @@ class HostStagedComm:
         return self.inner.gather_world(vals)
 
 
-def problem(N):
+def problem(N, mode="inverse"):
     x, y = pb.build_direction_sets(WAVE, 2, N, pb.BCKind.DIRICHLET)
     op, rhs_of = pb.elliptic_operator(x, y, 1.0)
-    pre = pb.make_preconditioner("elliptic_xnormal", x, y, mode="inverse")
+    pre = pb.make_preconditioner("elliptic_xnormal", x, y, mode=mode)
     return op, pre, rhs_of(sine_source(N, N, 3))
 
 
-def worker(rank, world, port, N, out_dir, peer=False):
+def worker(rank, world, port, N, out_dir, peer=False, mode="inverse"):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         torch.cuda.set_device(0)
-        op, pre, rhs = problem(N)
+        op, pre, rhs = problem(N, mode)
         qy, qx = rhs.shape
         lay = Layout(qy, qx, world, rank)
         be = CudaBackend(op, pre, lay)
@@ -86,5 +89,32 @@ def worker(rank, world, port, N, out_dir, peer=False):
             pt.close()
         np.savez(os.path.join(out_dir, f"rank{rank}.npz"), U=rep.solution, iters=rep.iterations,
                  hist=rep.residual_history)
+    finally:
+        dist.destroy_process_group()
+
+
+def heat_case(N=24, k=4):
+    """cfg4-type: heat on the wave domain, P_k, Dirichlet, separable source."""
+    x, y = pb.build_direction_sets(WAVE, k, N, pb.BCKind.DIRICHLET)
+    F = sine_source(N, N, 4)
+    u0 = 1e-2 * np.random.default_rng(4).standard_normal((y.q, x.q))
+    src = pb.SeparableSource(F, lambda t: float(np.exp(-t)))
+    inner = pb.InnerSolver(rule="residual", tol=1e-12, max_iter=5000)
+    return x, y, src, u0, pb.TimeGrid(1e-3, 4e-3), inner
+
+
+def heat_worker(rank, world, port, N, out_dir, mode="inverse"):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2109_01173_b200.distributed import sharded_imex_heat
+        torch.cuda.set_device(0)
+        x, y, src, u0, grid, inner = heat_case(N)
+        inner = pb.InnerSolver(rule="residual", tol=1e-12, max_iter=5000, precond_mode=mode)
+        lay = Layout(y.q, x.q, world, rank)
+        tr = sharded_imex_heat(WAVE, x, y, 1.0, src, u0, grid, inner=inner, comm=HostStagedComm(lay))
+        np.savez(os.path.join(out_dir, f"rank{rank}.npz"), U=tr.final[0], iters=tr.iterations,
+                 incs=tr.increments)
     finally:
         dist.destroy_process_group()

@@ -16,8 +16,9 @@ from paper_2109_01173_b200.distributed import Comm, Layout, sharded_mo_pcg
 
 
 class NumpyBackend:
-    def __init__(self, terms, Linv, RinvT, layout, b):
+    def __init__(self, terms, Linv, RinvT, layout, b, banded=False):
         self.L, self.b = layout, b
+        self.banded = banded  # the SPIKE route: right solves on row shards, left solves on column shards
         self.terms = terms
         self.Linv, self.RinvT = Linv, RinvT
         qx, n, c0 = layout.qx, layout.n, layout.c0
@@ -48,6 +49,12 @@ class NumpyBackend:
 
     def left(self, XcT):
         return torch.from_numpy(self.Linv @ XcT.numpy().T)
+
+    def right_rows(self, Xr):  # Xr P_R^-1
+        return torch.from_numpy(Xr.numpy() @ self.RinvT.T)
+
+    def left_cols(self, Xc):  # P_L^-1 Xc
+        return torch.from_numpy(self.Linv @ Xc.numpy())
 
     def update(self, U, R, Q, W, alpha):
         U += alpha * Q
@@ -156,7 +163,7 @@ def problem(N, k=2):
     return x, y, terms, rhs_of(sine_source(N, N, 3)), L, R
 
 
-def worker(rank, world, port, N, out_dir, warm):
+def worker(rank, world, port, N, out_dir, warm, banded=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -165,7 +172,7 @@ def worker(rank, world, port, N, out_dir, warm):
         qy, qx = rhs.shape
         lay = Layout(qy, qx, world, rank)
         b = 2
-        be = NumpyBackend(terms, np.linalg.inv(PL), np.linalg.inv(PR).T, lay, b)
+        be = NumpyBackend(terms, np.linalg.inv(PL), np.linalg.inv(PR).T, lay, b, banded=banded)
         comm = Comm(lay, "cpu")
         # collective unit checks
         rng = np.random.default_rng(7)
@@ -182,6 +189,8 @@ def worker(rank, world, port, N, out_dir, warm):
         assert np.array_equal(rows, full[lay.r0:lay.r0 + lay.m, :])
         colsT = comm.rowsT_to_colsT(torch.from_numpy(full.T[:, lay.r0:lay.r0 + lay.m].copy())).numpy()
         assert np.array_equal(colsT, full.T[lay.c0:lay.c0 + lay.n, :])
+        cols = comm.rows_to_cols(torch.from_numpy(full[lay.r0:lay.r0 + lay.m, :].copy())).numpy()
+        assert np.array_equal(cols, full[:, lay.c0:lay.c0 + lay.n])
         u0 = None
         if warm:
             u0 = 1e-2 * np.random.default_rng(4).standard_normal((qy, qx))[:, lay.c0:lay.c0 + lay.n]

@@ -13,16 +13,20 @@ import paper_2109_01173_b200 as pb
 from _cases import wave_oracle
 from _sharded_gpu_worker import worker
 from conftest import relerr
+from test_host_logic import WAVE
 from test_sharded_cpu import free_port
 
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("world,peer", [(2, False), (3, False), (2, True), (3, True)])
-def test_sharded_cuda_backend_multirank_matches_mo_pcg(world, peer):
+@pytest.mark.parametrize("world,peer,mode", [(2, False, "inverse"), (3, False, "inverse"), (2, True, "inverse"),
+                                             (3, True, "inverse"), (2, False, "banded"), (3, True, "banded")])
+def test_sharded_cuda_backend_multirank_matches_mo_pcg(world, peer, mode):
+    """mode banded: SPIKE solves on the shards (right factor on row shards,
+    left factor on column shards) with the rows -> cols exchange."""
     N = 40
     with tempfile.TemporaryDirectory() as d:
-        mp.spawn(worker, args=(world, free_port(), N, d, peer), nprocs=world, join=True)
+        mp.spawn(worker, args=(world, free_port(), N, d, peer, mode), nprocs=world, join=True)
         parts = [np.load(os.path.join(d, f"rank{r}.npz")) for r in range(world)]
     U = np.concatenate([p["U"] for p in parts], axis=1)
     iters = {int(p["iters"]) for p in parts}
@@ -63,3 +67,48 @@ def test_scatter_gemm_places_rows_like_the_transpose():
         c0, n = lay.col_offs[s], lay.col_counts[s]
         assert np.allclose(got[:, off:off + m], ref[c0:c0 + n, :], rtol=1e-13, atol=1e-12)
         assert np.all(np.isnan(got[:, :off])) and np.all(np.isnan(got[:, off + m:]))  # nothing outside the block
+
+
+@pytest.mark.parametrize("world,mode", [(2, "inverse"), (3, "banded")])
+def test_sharded_imex_heat_matches_single_gpu_driver(world, mode):
+    """cfg4-type heat (P4, wave domain, Dirichlet) with U column-sharded:
+    block rhs map over the halo-extended block (fused heat loader), the
+    sharded MO-PCG per step; against imex_euler_heat on one GPU."""
+    from _sharded_gpu_worker import heat_case, heat_worker
+    N = 24
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(heat_worker, args=(world, free_port(), N, d, mode), nprocs=world, join=True)
+        parts = [np.load(os.path.join(d, f"rank{r}.npz")) for r in range(world)]
+        U = np.concatenate([p["U"] for p in parts], axis=1)
+        iters = parts[0]["iters"]
+        incs = parts[0]["incs"]
+    x, y, src, u0, grid, inner = heat_case(N)
+    inner = pb.InnerSolver(rule="residual", tol=1e-12, max_iter=5000, precond_mode=mode)
+    ref = pb.imex_euler_heat(WAVE, x, y, 1.0, src, u0, grid, inner=inner)
+    assert np.all(np.abs(iters - ref.iterations) <= 2)
+    assert relerr(U, ref.final[0]) <= 1e-10
+    assert np.allclose(incs, ref.increments, rtol=1e-8)
+
+
+def test_sharded_imex_heat_single_rank_nccl_peer_graph():
+    """World 1 over NCCL with the peer-memory transposes (stream sync) and
+    CUDA-graph chunks: the configuration bench.py uses on one GPU per rank."""
+    import socket
+
+    import torch.distributed as dist
+
+    from _sharded_gpu_worker import heat_case
+    from paper_2109_01173_b200.distributed import sharded_imex_heat
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        x, y, src, u0, grid, inner = heat_case(24)
+        tr = sharded_imex_heat(WAVE, x, y, 1.0, src, u0, grid, inner=inner, peer_sync="stream", graph=True)
+        ref = pb.imex_euler_heat(WAVE, x, y, 1.0, src, u0, grid, inner=inner)
+        assert np.all(np.abs(tr.iterations - ref.iterations) <= 2)
+        assert relerr(tr.final[0], ref.final[0]) <= 1e-10
+    finally:
+        dist.destroy_process_group()

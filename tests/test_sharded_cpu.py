@@ -22,11 +22,13 @@ def free_port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("world,warm", [(2, False), (3, True)])
-def test_sharded_mo_pcg_matches_single_process(world, warm):
+@pytest.mark.parametrize("world,warm,banded", [(2, False, False), (3, True, False), (3, False, True)])
+def test_sharded_mo_pcg_matches_single_process(world, warm, banded):
+    """banded: the SPIKE form's route (right solves on row shards, rows -> cols
+    all-to-all, left solves on column shards)."""
     N = 24
     with tempfile.TemporaryDirectory() as d:
-        mp.spawn(worker, args=(world, free_port(), N, d, warm), nprocs=world, join=True)
+        mp.spawn(worker, args=(world, free_port(), N, d, warm, banded), nprocs=world, join=True)
         parts = [np.load(os.path.join(d, f"rank{r}.npz")) for r in range(world)]
         U = np.concatenate([p["U"] for p in parts], axis=1)
         iters = {int(p["iters"]) for p in parts}
