@@ -60,8 +60,14 @@ constexpr int NS = BAND_NS;
 constexpr int kMUnroll = BAND_MUNROLL;  // unroll of the chunk's W-row groups                       // TMA ring stages
 // CTAs per SM (2 x 5 warps: 168 registers per thread keep the 5-term band
 // in registers; measured faster than 3 CTAs at 128 registers)
+#ifndef BAND_MINB_WIDE
+#define BAND_MINB_WIDE 2
+#endif
+#ifndef BAND_PCG_XF_MINW
+#define BAND_PCG_XF_MINW 7  // MO-PCG direction update as a shared-memory pass from this band width on
+#endif
 template <int W>
-constexpr int band_minb() { return W >= 7 ? 2 : BAND_MINB; }
+constexpr int band_minb() { return W >= 7 ? BAND_MINB_WIDE : BAND_MINB; }
 constexpr int RY_MIN = 32;
 
 // Ring shape: NS stages of chunk_rows<W>() rows, or with FINE (MO-PCG pass of
@@ -220,7 +226,12 @@ __global__ void __launch_bounds__(TX + 32, band_minb<W>()) band_kernel(BandArgs 
             // in the grid and in this CTA's halo (the box's extra columns stay out of the checks)
             mdom[j] = pp < NPAIR ? (pm(gx, a.in_cols) & pm(2 * pp - shA, C::HC)) : 0u;
         }
-        constexpr bool smem_pass = mode == LD_HEAT || mode == LD_DIB;
+        // wide bands (W >= 7): the MO-PCG direction update Q = Z + beta Q_prev
+        // is applied once per halo element in shared memory instead of inline
+        // in each of the W taps that read it (W x fewer updates and Q_prev
+        // reads; measured slower for W = 5)
+        constexpr bool pcg_xf = mode == LD_PCG && W >= BAND_PCG_XF_MINW;
+        constexpr bool smem_pass = mode == LD_HEAT || mode == LD_DIB || pcg_xf;
         // visit this thread's pairs of a landed chunk: f(gr, j, double2* a_pair, const double* b_elems),
         // b_elems = B at the same full-grid columns (16-byte aligned unless shA != shB: heat only)
         auto for_pairs = [&](double* A, int r0, auto&& f) {
@@ -316,6 +327,14 @@ __global__ void __launch_bounds__(TX + 32, band_minb<W>()) band_kernel(BandArgs 
                     *ap = make_double2(v[0], v[1]);
                 });
             }
+            if constexpr (pcg_xf) {
+                if (upd) {
+                    for_pairs(A, r0, [&](int, int, double2* ap, const double* bp) {
+                        const double2 z = *ap, qp = *reinterpret_cast<const double2*>(bp);
+                        *ap = make_double2(__dadd_rn(__dmul_rn(beta, qp.x), z.x), __dadd_rn(__dmul_rn(beta, qp.y), z.y));
+                    });
+                }
+            }
             if constexpr (smem_pass)
                 asm volatile("bar.sync 1, %0;" ::"n"(TX) : "memory");  // transformed chunk visible
 
@@ -334,7 +353,7 @@ __global__ void __launch_bounds__(TX + 32, band_minb<W>()) band_kernel(BandArgs 
                     for (int e = 0; e < W; ++e) {
                         const double z = A[rr * HCB + shA + c + e];
                         double q = z;
-                        if constexpr (mode == LD_PCG)  // Q*=beta; Q+=Z (solvers.py:448-452), inline
+                        if constexpr (mode == LD_PCG && !pcg_xf)  // Q*=beta; Q+=Z (solvers.py:448-452), inline
                             q = upd ? __dadd_rn(__dmul_rn(beta, Bs[rr * HCB + shA + c + e]), z) : z;
                         if (e == (W - 1) / 2) cen[u] = q;
                         #pragma unroll
