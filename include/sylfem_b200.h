@@ -333,6 +333,17 @@ int sfb_frame_pgm16(const double* A_dev, int lda, int rows, int cols,
 
 /* ---- sparse vec-form matrices for the Kronecker cross-check path
  *      (operators.py:141-155 to_kronecker; vector_pcg, solvers.py:456-517) */
+/* ---- vector_pcg with a generic sparse preconditioner (solvers.py:473:
+ * spla.splu(P).solve): P factored once on the host as Pr P Pc = L U
+ * (CSR, 0-based; L unit or not, U upper), solved on the device level by
+ * level in one CTA.  z = P^-1 r for device vectors of length n. */
+typedef struct sfb_lu sfb_lu;
+int sfb_lu_create(int n, long long nnz_l, const long long* Lp, const int* Li, const double* Lv,
+                  long long nnz_u, const long long* Up, const int* Ui, const double* Uv,
+                  const int* perm_r, const int* perm_c, sfb_lu** out);
+int sfb_lu_solve(sfb_lu* h, const double* r_dev, double* z_dev, void* stream);
+int sfb_lu_destroy(sfb_lu* h);
+
 /* K (n x n) in CSR from host arrays: indptr n+1 (int64), indices nnz (int32,
  * column indices), data nnz (fp64); copied once. */
 int sfb_csr_create(int n, long long nnz, const long long* indptr_host, const int* indices_host,

@@ -44,6 +44,9 @@ constexpr int BK = 16, STAGES = GEMM_STAGES;
 // barriers one slot of slack lets warps drift by a k-tile without stalling
 // the issuing thread
 constexpr int LOOKAHEAD = GEMM_EMPTY ? STAGES - 2 : STAGES - 1;
+#ifndef GEMM_GROUP_M
+#define GEMM_GROUP_M 0  // tile raster: bands of GROUP_M tile rows (0: row-major)
+#endif
 #ifndef GEMM_WM
 #define GEMM_WM 32  // rows per warp: 32 (128 regs; measured +4 % at q = 2047 over 64 rows / 255 regs)
 #endif
@@ -85,6 +88,20 @@ struct Sched {
     int G;               // CTAs
     int tiles_total;     // output tiles (one <C,D> partial each)
     __device__ long long start(int c) const { return (long long)c * U / G; }
+    // tile -> output origin: tiles run down GROUP_M-row bands column by column,
+    // so the CTAs in flight share A and B panels in L2 (plain row-major with 0)
+    __device__ void origin(int tile, int bm, int bn, int& m0, int& n0) const {
+#if GEMM_GROUP_M > 0
+        const int tiles_m = tiles_total / tiles_n;
+        const int band = tile / (GEMM_GROUP_M * tiles_n), first = band * GEMM_GROUP_M;
+        const int gm = min(tiles_m - first, GEMM_GROUP_M), in = tile - band * GEMM_GROUP_M * tiles_n;
+        m0 = (first + in % gm) * bm;
+        n0 = (in / gm) * bn;
+#else
+        m0 = (tile / tiles_n) * bm;
+        n0 = (tile % tiles_n) * bn;
+#endif
+    }
     __device__ int owner(long long i) const {  // CTA whose range holds linear iteration i
         int c = (int)((i * G) / U);
         while (c + 1 < G && start(c + 1) <= i) ++c;
@@ -195,7 +212,8 @@ __global__ void __launch_bounds__(T::NTHREADS, T::CTAS_PER_SM)
     auto issue = [&](int it) {  // TMA for local iteration `it` into its ring slot
         const long long li = beg + it;
         const int tile = (int)(li / KT), kt = (int)(li - (long long)tile * KT);
-        const int m0 = (tile / sc.tiles_n) * BM, n0 = (tile % sc.tiles_n) * BN;
+        int m0, n0;
+        sc.origin(tile, BM, BN, m0, n0);
         const int sl = it % STAGES;
         mbar_expect_tx_u32(full + 8 * sl, A_BYTES + B_BYTES);
         tma_load_u32(sA + sl * A_BYTES, &tmA, full + 8 * sl, kt * BK, m0);
@@ -266,7 +284,8 @@ __global__ void __launch_bounds__(T::NTHREADS, T::CTAS_PER_SM)
 #endif
         }
 
-        const int m0 = (tile / sc.tiles_n) * BM, n0 = (tile % sc.tiles_n) * BN;
+        int m0, n0;
+        sc.origin(tile, BM, BN, m0, n0);
         bool finish = true;
         if (k0 != 0 || kl != KT - 1) {
             // split tile: the last piece to arrive finishes it (no CTA ever

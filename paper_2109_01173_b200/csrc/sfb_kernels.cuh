@@ -168,6 +168,10 @@ int launch_spike_pre(const SpikeFactor& L, const SpikeFactor& R, const double* R
                      const SegDot* dot, double* svL, double* svR, const PcgState* gate, cudaStream_t s);
 
 // ------------------------------------------------------------ sparse -----
+int launch_lu_solve(int n, const long long* Lp, const int* Li, const double* Lv, const int* Llp, const int* Llr,
+                    int nlL, const long long* Up, const int* Ui, const double* Uv, const int* Ulp, const int* Ulr,
+                    int nlU, const int* perm_r, const int* perm_c, const double* r, double* z, double* y,
+                    cudaStream_t s);
 int launch_csr_spmv(int n, const long long* indptr, const int* indices, const double* data, const double* x,
                     double* y, cudaStream_t s);
 

@@ -1532,6 +1532,100 @@ int sfb_diff_norm(const double* A, int lda, const double* B, int ldb, int rows, 
 }  // extern "C"
 
 // --------------------------------------------------------------- sparse ---
+// ---------------------- sparse LU of a generic vector_pcg preconditioner --
+struct sfb_lu {
+    int n = 0, nlev_l = 0, nlev_u = 0;
+    long long *Lp = nullptr, *Up = nullptr;
+    int *Li = nullptr, *Ui = nullptr, *Llp = nullptr, *Llr = nullptr, *Ulp = nullptr, *Ulr = nullptr;
+    int *perm_r = nullptr, *perm_c = nullptr;
+    double *Lv = nullptr, *Uv = nullptr, *y = nullptr;
+};
+
+int sfb_lu_destroy(sfb_lu* h) {
+    if (!h) return SFB_OK;
+    for (void* p : {(void*)h->Lp, (void*)h->Up, (void*)h->Li, (void*)h->Ui, (void*)h->Llp, (void*)h->Llr,
+                    (void*)h->Ulp, (void*)h->Ulr, (void*)h->perm_r, (void*)h->perm_c, (void*)h->Lv, (void*)h->Uv,
+                    (void*)h->y})
+        cudaFree(p);
+    delete h;
+    return SFB_OK;
+}
+
+namespace {
+// dependency levels of a triangular CSR factor (lower: rows in increasing
+// order, upper: decreasing); rows grouped by level
+int tri_levels(int n, const long long* ptr, const int* ind, bool lower, std::vector<int>& lev_ptr,
+               std::vector<int>& lev_rows) {
+    std::vector<int> lev(n, 0);
+    int nlev = 0;
+    for (int k = 0; k < n; ++k) {
+        const int i = lower ? k : n - 1 - k;
+        int l = 0;
+        for (long long p = ptr[i]; p < ptr[i + 1]; ++p) {
+            const int j = ind[p];
+            if (j < 0 || j >= n || (lower ? j > i : j < i)) return -1;
+            if (j != i) l = std::max(l, lev[j] + 1);
+        }
+        lev[i] = l;
+        nlev = std::max(nlev, l + 1);
+    }
+    lev_ptr.assign(nlev + 1, 0);
+    for (int i = 0; i < n; ++i) ++lev_ptr[lev[i] + 1];
+    for (int l = 0; l < nlev; ++l) lev_ptr[l + 1] += lev_ptr[l];
+    lev_rows.assign(n, 0);
+    std::vector<int> fill(lev_ptr.begin(), lev_ptr.end() - 1);
+    for (int i = 0; i < n; ++i) lev_rows[fill[lev[i]]++] = i;
+    return nlev;
+}
+}  // namespace
+
+int sfb_lu_create(int n, long long nnz_l, const long long* Lp, const int* Li, const double* Lv, long long nnz_u,
+                  const long long* Up, const int* Ui, const double* Uv, const int* perm_r, const int* perm_c,
+                  sfb_lu** out) {
+    if (n <= 0 || !Lp || !Up || !perm_r || !perm_c || !out) return arg_error("sparse LU: bad argument");
+    std::vector<int> llp, llr, ulp, ulr;
+    const int nl = tri_levels(n, Lp, Li, true, llp, llr), nu = tri_levels(n, Up, Ui, false, ulp, ulr);
+    if (nl < 0 || nu < 0) return arg_error("sparse LU: factors are not triangular CSR");
+    auto* h = new sfb_lu;
+    h->n = n;
+    h->nlev_l = nl;
+    h->nlev_u = nu;
+    int rc = SFB_OK;
+    auto up = [&](auto** dst, const void* src, size_t bytes) {
+        if (rc != SFB_OK) return;
+        if (cudaMalloc(reinterpret_cast<void**>(dst), bytes ? bytes : 8) != cudaSuccess ||
+            (src && bytes && cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice) != cudaSuccess)) {
+            set_error("uploading the sparse LU factors failed");
+            rc = SFB_ERR_NOMEM;
+        }
+    };
+    up(&h->Lp, Lp, (size_t)(n + 1) * 8);
+    up(&h->Li, Li, (size_t)nnz_l * 4);
+    up(&h->Lv, Lv, (size_t)nnz_l * 8);
+    up(&h->Up, Up, (size_t)(n + 1) * 8);
+    up(&h->Ui, Ui, (size_t)nnz_u * 4);
+    up(&h->Uv, Uv, (size_t)nnz_u * 8);
+    up(&h->Llp, llp.data(), llp.size() * 4);
+    up(&h->Llr, llr.data(), llr.size() * 4);
+    up(&h->Ulp, ulp.data(), ulp.size() * 4);
+    up(&h->Ulr, ulr.data(), ulr.size() * 4);
+    up(&h->perm_r, perm_r, (size_t)n * 4);
+    up(&h->perm_c, perm_c, (size_t)n * 4);
+    up(&h->y, nullptr, (size_t)n * 8);
+    if (rc != SFB_OK) {
+        sfb_lu_destroy(h);
+        return rc;
+    }
+    *out = h;
+    return SFB_OK;
+}
+
+int sfb_lu_solve(sfb_lu* h, const double* r, double* z, void* stream) {
+    if (!h || !r || !z) return arg_error("sparse LU solve: null argument");
+    return launch_lu_solve(h->n, h->Lp, h->Li, h->Lv, h->Llp, h->Llr, h->nlev_l, h->Up, h->Ui, h->Uv, h->Ulp, h->Ulr,
+                           h->nlev_u, h->perm_r, h->perm_c, r, z, h->y, (cudaStream_t)stream);
+}
+
 struct sfb_csr {
     int n = 0;
     long long nnz = 0;

@@ -42,7 +42,56 @@ __global__ void __launch_bounds__(CT) csr_spmv_kernel(int n, const long long* __
     }
 }
 
+// Sparse LU solve z = P^-1 r of a generic sparse preconditioner, factored
+// once on the host as Pr P Pc = L U (SuperLU, like the reference's
+// spla.splu(P).solve, solvers.py:473).  One CTA: y = Pr r, forward
+// substitution with L level by level, backward substitution with U level by
+// level (rows of one level are independent; a CTA barrier separates
+// levels), z = Pc x.  Each row sums its entries in CSR order, so the solve
+// is deterministic.  Meant for the cross-check sizes vector_pcg runs at.
+constexpr int LU_T = 1024;
+
+__device__ __forceinline__ void tri_level_sweep(const long long* __restrict__ ptr, const int* __restrict__ ind,
+                                                const double* __restrict__ val, const int* __restrict__ lev_ptr,
+                                                const int* __restrict__ lev_rows, int nlev, double* y) {
+    for (int l = 0; l < nlev; ++l) {
+        for (int k = lev_ptr[l] + threadIdx.x; k < lev_ptr[l + 1]; k += LU_T) {
+            const int i = lev_rows[k];
+            double s = y[i], d = 1.0;
+            for (long long p = ptr[i]; p < ptr[i + 1]; ++p) {
+                const int j = ind[p];
+                if (j == i) d = val[p];
+                else s = fma(-val[p], y[j], s);
+            }
+            y[i] = s / d;
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(LU_T) lu_solve_kernel(int n, const long long* Lp, const int* Li, const double* Lv,
+                                                       const int* Llp, const int* Llr, int nlL, const long long* Up,
+                                                       const int* Ui, const double* Uv, const int* Ulp,
+                                                       const int* Ulr, int nlU, const int* perm_r,
+                                                       const int* perm_c, const double* r, double* z, double* y) {
+    for (int i = threadIdx.x; i < n; i += LU_T) y[perm_r[i]] = r[i];  // Pr r
+    __syncthreads();
+    tri_level_sweep(Lp, Li, Lv, Llp, Llr, nlL, y);
+    tri_level_sweep(Up, Ui, Uv, Ulp, Ulr, nlU, y);
+    for (int i = threadIdx.x; i < n; i += LU_T) z[i] = y[perm_c[i]];  // Pc x: (Pc x)[i] = x[perm_c[i]]
+}
+
 }  // namespace
+
+int launch_lu_solve(int n, const long long* Lp, const int* Li, const double* Lv, const int* Llp, const int* Llr,
+                    int nlL, const long long* Up, const int* Ui, const double* Uv, const int* Ulp, const int* Ulr,
+                    int nlU, const int* perm_r, const int* perm_c, const double* r, double* z, double* y,
+                    cudaStream_t s) {
+    lu_solve_kernel<<<1, LU_T, 0, s>>>(n, Lp, Li, Lv, Llp, Llr, nlL, Up, Ui, Uv, Ulp, Ulr, nlU, perm_r, perm_c, r,
+                                       z, y);
+    SFB_CHECK_LAUNCH();
+    return SFB_OK;
+}
 
 int launch_csr_spmv(int n, const long long* indptr, const int* indices, const double* data, const double* x,
                     double* y, cudaStream_t s) {

@@ -851,6 +851,42 @@ class _DeviceCSR:
         nat.check(nat.lib().sfb_csr_spmv(self.handle.p, nat.ptr(x), nat.ptr(y), nat.stream()), "spmv")
 
 
+class _DeviceLU:
+    """A generic sparse preconditioner P factored once on the host like the
+    reference (SuperLU: Pr P Pc = L U, solvers.py:473) and solved on the
+    device (sfb_lu_solve: permutations and level-scheduled triangular
+    sweeps in one kernel)."""
+
+    def __init__(self, P, n: int):
+        import scipy.sparse.linalg as spla
+        P = sp.csc_matrix(P, dtype=float)
+        if P.shape != (n, n):
+            raise OperatorError(f"preconditioner of shape {P.shape} does not match the {n} unknowns")
+        try:
+            f = spla.splu(P)
+        except RuntimeError as exc:  # singular factor
+            raise SolverError(f"preconditioner factorisation failed: {exc}") from None
+        Lc, Uc = sp.csr_matrix(f.L), sp.csr_matrix(f.U)
+        arrs = []
+        for M in (Lc, Uc):
+            M.sort_indices()
+            arrs.append((np.ascontiguousarray(M.indptr, dtype=np.int64), np.ascontiguousarray(M.indices, np.int32),
+                         np.ascontiguousarray(M.data, dtype=float)))
+        # P^-1 r = Pc U^-1 L^-1 Pr r: (Pr r)[perm_r[i]] = r[i], (Pc x)[i] = x[perm_c[i]]
+        pr = np.ascontiguousarray(f.perm_r, dtype=np.int32)
+        pc = np.ascontiguousarray(f.perm_c, dtype=np.int32)
+        L = nat.lib()
+        out = nat.C.c_void_p()
+        (lp, li, lv), (up, ui, uv) = arrs
+        nat.check(L.sfb_lu_create(n, int(lv.size), nat.host_ptr(lp), nat.host_ptr(li), nat.host_ptr(lv), int(uv.size),
+                                  nat.host_ptr(up), nat.host_ptr(ui), nat.host_ptr(uv), nat.host_ptr(pr),
+                                  nat.host_ptr(pc), nat.C.byref(out)), "sparse LU")
+        self.handle = nat.Handle(out.value, L.sfb_lu_destroy)
+
+    def solve(self, r, z):
+        nat.check(nat.lib().sfb_lu_solve(self.handle.p, nat.ptr(r), nat.ptr(z), nat.stream()), "sparse LU solve")
+
+
 def _vec_ops(n):
     """Host-synchronous vector passes (the sharded MO-PCG blocks) on 1 x n rows."""
     L = nat.lib()
@@ -891,18 +927,20 @@ def vector_pcg(K, b, P=None, stop: StoppingRule | None = None, x0=None, max_iter
     bh = np.asarray(b, dtype=float).reshape(-1)
     if bh.size != n:
         raise OperatorError(f"right-hand side of length {bh.size} does not match the {n} x {n} matrix")
-    if P is None:
-        pre = None
-    else:
+    pre = lu = None
+    if P is not None:
         pre = getattr(P, "sfb_pre", None)
-        if pre is None:
-            raise SolverError("vector_pcg applies its preconditioner with the device kernels: pass "
-                              "P = Preconditioner.as_kronecker(shape) (or None)")
-        qy, qx = P.sfb_shape
-        if qy * qx != n:
-            raise OperatorError(f"preconditioner of grid {P.sfb_shape} does not match the {n} unknowns")
+        if pre is not None:  # Kronecker-structured: the preconditioner's own device kernels
+            qy, qx = P.sfb_shape
+            if qy * qx != n:
+                raise OperatorError(f"preconditioner of grid {P.sfb_shape} does not match the {n} unknowns")
+        else:  # any sparse P: factored once (solvers.py:473), solved on the device
+            lu = _DeviceLU(P, n)
 
     def solve_p(r, z):
+        if lu is not None:
+            lu.solve(r, z)
+            return
         if pre is None:
             z.copy_(r)
             return

@@ -87,8 +87,11 @@ def test_vector_pcg_identity_warm_start_increment_rule_and_errors():
     r2 = pb.vector_pcg(K, b, stop=pb.increment_threshold(1e-10), max_iter=5000)
     assert r2.stop_reason == "increment"
     assert pb.vector_pcg(K, np.zeros_like(b)).iterations == 0
-    with pytest.raises(pb.SolverError, match="as_kronecker"):
-        pb.vector_pcg(K, b, P=sp.identity(b.size, format="csr"))
+    # a plain sparse P (not from as_kronecker) is factored like the reference's splu
+    r3 = pb.vector_pcg(K, b, P=sp.identity(b.size, format="csr"), stop=pb.relative_residual(1e-12), max_iter=5000)
+    assert r3.iterations == pb.vector_pcg(K, b, stop=pb.relative_residual(1e-12), max_iter=5000).iterations
+    with pytest.raises(pb.OperatorError, match="does not match"):
+        pb.vector_pcg(K, b, P=sp.identity(b.size + 1, format="csr"))
     with pytest.raises(pb.OperatorError, match="not positive definite"):
         pb.vector_pcg(-K, b, max_iter=10)
 
@@ -125,3 +128,61 @@ def test_vector_imex_drivers_match_reference_trajectories(golden):
                             (golden["dib/eta0"], golden["dib/theta0"]), pb.TimeGrid(tau, 6 * tau), lumped=True)
     assert relerr(tv.final[0], golden["dib/t12/U"]) <= 1e-10
     assert relerr(tv.final[1], golden["dib/t12/V"]) <= 1e-10
+
+
+@pytest.mark.gpu
+def test_vector_pcg_generic_sparse_preconditioner_vs_reference_algorithm():
+    """A P that is not Kronecker-structured (here: an incomplete-Cholesky-like
+    sparse SPD matrix, the Kronecker matrix's own tridiagonal-block part):
+    factored once like the reference (spla.splu(P), solvers.py:473) and solved
+    on the device (sfb_lu_solve).  Iterates against the reference recurrence
+    with the host LU solve on the same inputs."""
+    import scipy.sparse.linalg as spla
+    N = 12
+    x, y = pb.build_direction_sets(WAVE, 2, N, D)
+    op, rhs_of = pb.elliptic_operator(x, y, 1.0)
+    K = sp.csr_matrix(pb.to_kronecker(op))
+    # a generic SPD preconditioner: K without its far off-diagonal couplings
+    C = K.tocoo()
+    keep = np.abs(C.row - C.col) <= 2
+    P = sp.csr_matrix((C.data[keep], (C.row[keep], C.col[keep])), shape=K.shape)
+    P = 0.5 * (P + P.T) + sp.diags(np.abs(P).sum(axis=1).A.ravel())  # diagonally dominant SPD
+    b = pb.vec(rhs_of(sine_source(N, N, 3)))
+    stop = pb.relative_residual(1e-10)
+    rep = pb.vector_pcg(K, b, P=P, stop=stop, record_iterates=True)
+    # the reference recurrence (solvers.py:456-517) with SuperLU on the host (checker)
+    solve = spla.splu(sp.csc_matrix(P)).solve
+    xr = np.zeros_like(b)
+    r = b.copy()
+    z = solve(r)
+    q = z.copy()
+    rz = r @ z
+    its = [xr.copy()]
+    res0 = np.linalg.norm(r)
+    n_it = 0
+    for s in range(1000):
+        w = K @ q
+        a = rz / (q @ w)
+        xr += a * q
+        r -= a * w
+        its.append(xr.copy())
+        n_it = s + 1
+        if np.linalg.norm(r) <= 1e-10 * res0:
+            break
+        z = solve(r)
+        rzn = r @ z
+        q = z + (rzn / rz) * q
+        rz = rzn
+    assert rep.stop_reason == "tolerance"
+    assert abs(rep.iterations - n_it) <= 1
+    for a_, b_ in list(zip(rep.diagnostics["iterates"], its))[1:10]:
+        assert relerr(a_, b_) <= 1e-10
+    assert relerr(rep.solution, its[-1]) <= 1e-9
+    # the device LU solve itself
+    from paper_2109_01173_b200.solvers import _DeviceLU
+    import torch
+    lu = _DeviceLU(P, P.shape[0])
+    rr = np.random.default_rng(2).standard_normal(P.shape[0])
+    zd = torch.empty((1, P.shape[0]), dtype=torch.float64, device="cuda")
+    lu.solve(torch.from_numpy(rr.reshape(1, -1)).cuda(), zd)
+    assert relerr(zd.cpu().numpy().ravel(), solve(rr)) <= 1e-13
