@@ -8,11 +8,12 @@
 //
 // sm_100a has no FP64 tcgen05 kind, so the FP64 tensor path is the warp-level
 // DMMA.8x8x4 (mma.sync m8n8k4 f64).  Tiles are staged by TMA
-// (cp.async.bulk.tensor, SWIZZLE_128B) into a 5-stage shared-memory ring
-// guarded by full/empty mbarriers; one thread issues the copies three k-tiles
-// ahead (after the slot's empty barrier completes: every warp released it)
-// and sixteen warps (four per SM sub-partition, 32 x 32 warp tiles, 128
-// registers) issue DMMA.
+// (cp.async.bulk.tensor, SWIZZLE_128B, 16-wide k boxes) into a shared-memory
+// ring guarded by full/empty mbarriers — 128 x 128 tiles: 3 stages of 32 k
+// (two boxes per operand, 64 KB), two k-tiles ahead; 64 x 64 tiles: 5 stages
+// of 16 k, three ahead — one thread issues the copies once the slot's empty
+// barrier completes (every warp released it), and the warps (four per SM
+// sub-partition for 128 x 128, 32 x 32 warp tiles, 128 registers) issue DMMA.
 // Both operands are K-contiguous ("NT"), which lets every fragment load be a
 // conflict-free LDS.128: thread t of a quad owns the
 // physical k = 4t+s for mma step s, so A[row][4t..4t+3] and Bt[col][4t..4t+3]
@@ -33,19 +34,15 @@ int num_sms();
 
 namespace {
 
-#ifndef GEMM_STAGES
-#define GEMM_STAGES 5
-#endif
 #ifndef GEMM_EMPTY
 #define GEMM_EMPTY 1  // per-stage empty barriers (1) or a CTA barrier per k-tile (0)
 #endif
-constexpr int BK = 16, STAGES = GEMM_STAGES;
-// k-tiles in flight ahead of the one being consumed: with per-stage empty
-// barriers one slot of slack lets warps drift by a k-tile without stalling
-// the issuing thread
-constexpr int LOOKAHEAD = GEMM_EMPTY ? STAGES - 2 : STAGES - 1;
+constexpr int KBOX = 16;  // doubles per 128-byte swizzled TMA box row (one box per operand and 16 k)
 #ifndef GEMM_GROUP_M
 #define GEMM_GROUP_M 0  // tile raster: bands of GROUP_M tile rows (0: row-major)
+#endif
+#ifndef GEMM_SMALL_MINWORK
+#define GEMM_SMALL_MINWORK 4  // k-tiles per CTA at least, 64x64 tiles
 #endif
 #ifndef GEMM_WM
 #define GEMM_WM 32  // rows per warp: 32 (128 regs; measured +4 % at q = 2047 over 64 rows / 255 regs)
@@ -56,9 +53,15 @@ constexpr int WM = GEMM_WM, MI = WM / 8;   // warp tile WM x 32: MI x 4 DMMA 8x8
 // GEMMs; 64 x 64 with 4 warps (two CTAs per SM) when the 128-tiles would not
 // fill the machine (at most 64 of them: q <= 1024, the cfg1 / cfg2 reduced
 // solves), so the stream-K pieces stay short and the fix-up traffic small.
-template <int BM_, int BN_>
+template <int BM_, int BN_, int BK_, int STAGES_>
 struct Tile {
-    static constexpr int BM = BM_, BN = BN_;
+    static constexpr int BM = BM_, BN = BN_, BK = BK_, STAGES = STAGES_;
+    static_assert(BK % KBOX == 0, "k-tile must be a multiple of the TMA box width");
+    // k-tiles in flight ahead of the one being consumed: all but one slot with
+    // few deep stages (the refill then waits for the slowest warp's previous
+    // k-tile: measured +0.1-0.3 % for 3 x 64 KB), else one slot of slack so
+    // warps drift by a k-tile without stalling the issuing thread
+    static constexpr int LOOKAHEAD = (GEMM_EMPTY && STAGES > 3) ? STAGES - 2 : STAGES - 1;
     static constexpr int WARPS_N = BN / 32;
     static constexpr int NWARPS = (BM / WM) * WARPS_N;
     static constexpr int NTHREADS = NWARPS * 32;
@@ -66,8 +69,14 @@ struct Tile {
     static constexpr int A_BYTES = BM * BK * 8, B_BYTES = BN * BK * 8;
     static constexpr int SMEM_BYTES = STAGES * (A_BYTES + B_BYTES) + 2 * STAGES * 8 + 1024;
 };
-using BigTile = Tile<128, 128>;
-using SmallTile = Tile<64, 64>;
+#ifndef GEMM_BIG_BK
+#define GEMM_BIG_BK 32  // measured: 36.3 vs 35.4 TF/s at q = 8192 (3 x 64 KB stages vs 5 x 32 KB)
+#endif
+#ifndef GEMM_BIG_STAGES
+#define GEMM_BIG_STAGES (GEMM_BIG_BK == 32 ? 3 : 5)
+#endif
+using BigTile = Tile<128, 128, GEMM_BIG_BK, GEMM_BIG_STAGES>;
+using SmallTile = Tile<64, 64, 16, 5>;
 
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -193,6 +202,7 @@ __global__ void __launch_bounds__(T::NTHREADS, T::CTAS_PER_SM)
     dgemm_nt_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
                     int K, GemmEpi ep, Sched sc) {
     constexpr int BM = T::BM, BN = T::BN, NWARPS = T::NWARPS, NTHREADS = T::NTHREADS;
+    constexpr int BK = T::BK, STAGES = T::STAGES, LOOKAHEAD = T::LOOKAHEAD;
     constexpr int A_BYTES = T::A_BYTES, B_BYTES = T::B_BYTES;
     SFB_PDL_PROLOGUE();
     if (ep.pcg != nullptr && ep.pcg->status != SFB_PCG_RUNNING) return;  // uniform gate
@@ -216,8 +226,11 @@ __global__ void __launch_bounds__(T::NTHREADS, T::CTAS_PER_SM)
         sc.origin(tile, BM, BN, m0, n0);
         const int sl = it % STAGES;
         mbar_expect_tx_u32(full + 8 * sl, A_BYTES + B_BYTES);
-        tma_load_u32(sA + sl * A_BYTES, &tmA, full + 8 * sl, kt * BK, m0);
-        tma_load_u32(sB + sl * B_BYTES, &tmB, full + 8 * sl, kt * BK, n0);
+        #pragma unroll
+        for (int kb = 0; kb < BK / KBOX; ++kb) {
+            tma_load_u32(sA + sl * A_BYTES + kb * BM * KBOX * 8, &tmA, full + 8 * sl, kt * BK + kb * KBOX, m0);
+            tma_load_u32(sB + sl * B_BYTES + kb * BN * KBOX * 8, &tmB, full + 8 * sl, kt * BK + kb * KBOX, n0);
+        }
     };
 
     if (threadIdx.x == 0) {
@@ -259,10 +272,11 @@ __global__ void __launch_bounds__(T::NTHREADS, T::CTAS_PER_SM)
             if (threadIdx.x == 0 && it + LOOKAHEAD < n_it) issue(it + LOOKAHEAD);
 #endif
             mbar_wait_u32(full + 8 * s, (it / STAGES) & 1);
-            const uint32_t a_base = sA + s * A_BYTES + (wm * WM + g) * 128;
-            const uint32_t b_base = sB + s * B_BYTES + (wn * 32 + g) * 128;
             #pragma unroll
-            for (int half = 0; half < 2; ++half) {
+            for (int hh = 0; hh < 2 * (BK / KBOX); ++hh) {
+                const int half = hh & 1, kb = hh >> 1;  // box kb of the stage, 8-double half of its row
+                const uint32_t a_base = sA + s * A_BYTES + kb * BM * KBOX * 8 + (wm * WM + g) * 128;
+                const uint32_t b_base = sB + s * B_BYTES + kb * BN * KBOX * 8 + (wn * 32 + g) * 128;
                 const uint32_t ch = ((2 * t + half) ^ g) << 4;  // SWIZZLE_128B: chunk ^= row & 7 (= g)
                 double2 a[MI], b[4];
                 #pragma unroll
@@ -375,7 +389,7 @@ __global__ void __launch_bounds__(T::NTHREADS, T::CTAS_PER_SM)
 int make_map(CUtensorMap* map, const double* ptr, int rows, int cols, int ld, int box_rows) {
     if (!tma_aligned(ptr, ld)) return arg_error("DMMA GEMM operands need 16-byte aligned rows (even leading dimension)");
     const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-    const cuuint32_t box[2] = {BK, (cuuint32_t)box_rows};
+    const cuuint32_t box[2] = {KBOX, (cuuint32_t)box_rows};
     return tma_make_map(map, ptr, 2, dims, ld, box, CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
@@ -400,7 +414,7 @@ int launch_tile(const double* A, int lda, const double* Bt, int ldb, int M, int 
     SFB_TRY(make_map(&mb, Bt, N, K, ldb, T::BN));
     Sched sc;
     sc.tiles_n = (N + T::BN - 1) / T::BN;
-    sc.KT = (K + BK - 1) / BK;
+    sc.KT = (K + T::BK - 1) / T::BK;
     const int tiles = tiles_of(M, N, T::BM, T::BN);
     sc.U = (long long)tiles * sc.KT;
     sc.tiles_total = tiles;
@@ -412,7 +426,7 @@ int launch_tile(const double* A, int lda, const double* Bt, int ldb, int M, int 
     if (!have_ws || tiles % slots == 0) {
         sc.G = tiles;
     } else {
-        const long long min_work = T::BM >= 128 ? 8 : 4;
+        const long long min_work = T::BM >= 128 ? 8 : GEMM_SMALL_MINWORK;
         sc.G = (int)std::max(1LL, std::min<long long>(slots, sc.U / min_work));
     }
     return launch_kernel(dgemm_nt_kernel<T>, dim3(sc.G), dim3(T::NTHREADS), T::SMEM_BYTES, stream, ma, mb, M, N, K,
