@@ -45,24 +45,28 @@ constexpr int KBOX = 16;  // doubles per 128-byte swizzled TMA box row (one box 
 #define GEMM_SMALL_MINWORK 4  // k-tiles per CTA at least, 64x64 tiles
 #endif
 #ifndef GEMM_WM
-#define GEMM_WM 32  // rows per warp: 32 (128 regs; measured +4 % at q = 2047 over 64 rows / 255 regs)
+#define GEMM_WM 32  // rows per warp, 128 x 128 tiles: 32 (128 regs; measured +4 % at q = 2047 over 64 rows / 255 regs)
 #endif
-constexpr int WM = GEMM_WM, MI = WM / 8;   // warp tile WM x 32: MI x 4 DMMA 8x8 blocks
+
 
 // CTA tile BM x BN: 128 x 128 with 16 warps (one CTA per SM) for large
 // GEMMs; 64 x 64 with 4 warps (two CTAs per SM) when the 128-tiles would not
 // fill the machine (at most 64 of them: q <= 1024, the cfg1 / cfg2 reduced
-// solves), so the stream-K pieces stay short and the fix-up traffic small.
-template <int BM_, int BN_, int BK_, int STAGES_>
+// solves), so the stream-K pieces stay short and the fix-up traffic small;
+// 64 x 64 with 16 warps of 16 x 16 at <= 16 128-tiles (q <= 512), where one
+// warp per SM sub-partition cannot hide the DMMA dependency latency.
+template <int BM_, int BN_, int BK_, int STAGES_, int WM_ = 32, int WN_ = 32>
 struct Tile {
     static constexpr int BM = BM_, BN = BN_, BK = BK_, STAGES = STAGES_;
+    static constexpr int WM = WM_, WN = WN_;          // warp tile WM x WN
+    static constexpr int MI = WM / 8, NJ = WN / 8;    // MI x NJ DMMA 8x8 blocks per warp
     static_assert(BK % KBOX == 0, "k-tile must be a multiple of the TMA box width");
     // k-tiles in flight ahead of the one being consumed: all but one slot with
     // few deep stages (the refill then waits for the slowest warp's previous
     // k-tile: measured +0.1-0.3 % for 3 x 64 KB), else one slot of slack so
     // warps drift by a k-tile without stalling the issuing thread
     static constexpr int LOOKAHEAD = (GEMM_EMPTY && STAGES > 3) ? STAGES - 2 : STAGES - 1;
-    static constexpr int WARPS_N = BN / 32;
+    static constexpr int WARPS_N = BN / WN;
     static constexpr int NWARPS = (BM / WM) * WARPS_N;
     static constexpr int NTHREADS = NWARPS * 32;
     static constexpr int CTAS_PER_SM = NWARPS >= 16 ? 1 : 2;
@@ -75,8 +79,9 @@ struct Tile {
 #ifndef GEMM_BIG_STAGES
 #define GEMM_BIG_STAGES (GEMM_BIG_BK == 32 ? 3 : 5)
 #endif
-using BigTile = Tile<128, 128, GEMM_BIG_BK, GEMM_BIG_STAGES>;
-using SmallTile = Tile<64, 64, 16, 5>;
+using BigTile = Tile<128, 128, GEMM_BIG_BK, GEMM_BIG_STAGES, GEMM_WM, 32>;
+using SmallTile = Tile<64, 64, 16, 5, 32, 32>;  // 4 warps, 2 CTAs/SM
+using TinyTile = Tile<64, 64, 16, 5, 16, 16>;   // 16 warps of 16 x 16: latency-bound sizes
 
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -129,16 +134,17 @@ __device__ __forceinline__ size_t ws_slot(int cta, int k0) {
 
 // Epilogue of one finished tile (registers -> global).
 template <class T>
-__device__ __forceinline__ double tile_epilogue(double (&acc)[MI][4][2], const GemmEpi& ep, int M, int N, int m0,
+__device__ __forceinline__ double tile_epilogue(double (&acc)[T::MI][T::NJ][2], const GemmEpi& ep, int M, int N, int m0,
                                                 int n0, int wm, int wn, int g, int t) {
+    constexpr int MI = T::MI, NJ = T::NJ;
     double dot = 0.0;
     #pragma unroll
     for (int i = 0; i < MI; ++i) {
-        const int m = m0 + wm * WM + i * 8 + g;
+        const int m = m0 + wm * T::WM + i * 8 + g;
         if (m >= M) continue;
         #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int n = n0 + wn * 32 + j * 8 + 2 * t;
+        for (int j = 0; j < NJ; ++j) {
+            const int n = n0 + wn * T::WN + j * 8 + 2 * t;
             double v0 = acc[i][j][0], v1 = acc[i][j][1];
             const bool ok0 = n < N, ok1 = n + 1 < N;
             switch (ep.mode) {
@@ -213,7 +219,8 @@ __global__ void __launch_bounds__(T::NTHREADS, T::CTAS_PER_SM)
     const uint32_t empty = full + 8 * STAGES;  // one arrive per warp when it is done reading a slot
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int wm = warp / T::WARPS_N, wn = warp % T::WARPS_N;  // (BM/WM) x (BN/32) warps, WM x 32 each
+    const int wm = warp / T::WARPS_N, wn = warp % T::WARPS_N;  // (BM/WM) x (BN/WN) warps, WM x WN each
+    constexpr int MI = T::MI, NJ = T::NJ, WM = T::WM, WN = T::WN;
     const int g = lane >> 2, t = lane & 3;
     const int KT = sc.KT;
     const long long beg = sc.start(blockIdx.x), fin = sc.start(blockIdx.x + 1);
@@ -247,7 +254,7 @@ __global__ void __launch_bounds__(T::NTHREADS, T::CTAS_PER_SM)
 
     __shared__ int s_fin;
     __shared__ double sh_dot[NTHREADS / 32];
-    double acc[MI][4][2];
+    double acc[MI][NJ][2];
     int it = 0;
     while (it < n_it) {
         const long long li0 = beg + it;
@@ -257,7 +264,7 @@ __global__ void __launch_bounds__(T::NTHREADS, T::CTAS_PER_SM)
         #pragma unroll
         for (int i = 0; i < MI; ++i)
             #pragma unroll
-            for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+            for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
         for (; it < seg_end; ++it) {
             const int s = it % STAGES;
@@ -276,21 +283,21 @@ __global__ void __launch_bounds__(T::NTHREADS, T::CTAS_PER_SM)
             for (int hh = 0; hh < 2 * (BK / KBOX); ++hh) {
                 const int half = hh & 1, kb = hh >> 1;  // box kb of the stage, 8-double half of its row
                 const uint32_t a_base = sA + s * A_BYTES + kb * BM * KBOX * 8 + (wm * WM + g) * 128;
-                const uint32_t b_base = sB + s * B_BYTES + kb * BN * KBOX * 8 + (wn * 32 + g) * 128;
+                const uint32_t b_base = sB + s * B_BYTES + kb * BN * KBOX * 8 + (wn * WN + g) * 128;
                 const uint32_t ch = ((2 * t + half) ^ g) << 4;  // SWIZZLE_128B: chunk ^= row & 7 (= g)
-                double2 a[MI], b[4];
+                double2 a[MI], b[NJ];
                 #pragma unroll
                 for (int i = 0; i < MI; ++i) a[i] = lds128(a_base + i * 1024 + ch);
                 #pragma unroll
-                for (int j = 0; j < 4; ++j) b[j] = lds128(b_base + j * 1024 + ch);
+                for (int j = 0; j < NJ; ++j) b[j] = lds128(b_base + j * 1024 + ch);
                 #pragma unroll
                 for (int i = 0; i < MI; ++i)
                     #pragma unroll
-                    for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i].x, b[j].x);
+                    for (int j = 0; j < NJ; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i].x, b[j].x);
                 #pragma unroll
                 for (int i = 0; i < MI; ++i)
                     #pragma unroll
-                    for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i].y, b[j].y);
+                    for (int j = 0; j < NJ; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i].y, b[j].y);
             }
 #if GEMM_EMPTY
             __syncwarp();
@@ -312,8 +319,8 @@ __global__ void __launch_bounds__(T::NTHREADS, T::CTAS_PER_SM)
                 #pragma unroll
                 for (int i = 0; i < MI; ++i)
                     #pragma unroll
-                    for (int j = 0; j < 4; ++j)
-                        __stcg(reinterpret_cast<double2*>(w + (size_t)((i * 4 + j) * 2) * NTHREADS) + threadIdx.x,
+                    for (int j = 0; j < NJ; ++j)
+                        __stcg(reinterpret_cast<double2*>(w + (size_t)((i * NJ + j) * 2) * NTHREADS) + threadIdx.x,
                                make_double2(acc[i][j][0], acc[i][j][1]));
             };
             auto fold = [&](int c, int piece_k0, bool assign) {  // acc (=|+=) parked piece of CTA c
@@ -321,9 +328,9 @@ __global__ void __launch_bounds__(T::NTHREADS, T::CTAS_PER_SM)
                 #pragma unroll
                 for (int i = 0; i < MI; ++i)
                     #pragma unroll
-                    for (int j = 0; j < 4; ++j) {
+                    for (int j = 0; j < NJ; ++j) {
                         const double2 v = __ldcg(
-                            reinterpret_cast<const double2*>(w + (size_t)((i * 4 + j) * 2) * NTHREADS) + threadIdx.x);
+                            reinterpret_cast<const double2*>(w + (size_t)((i * NJ + j) * 2) * NTHREADS) + threadIdx.x);
                         acc[i][j][0] = assign ? v.x : acc[i][j][0] + v.x;
                         acc[i][j][1] = assign ? v.y : acc[i][j][1] + v.y;
                     }
@@ -395,7 +402,8 @@ int make_map(CUtensorMap* map, const double* ptr, int rows, int cols, int ld, in
 
 inline int tiles_of(int M, int N, int bm, int bn) { return ((N + bn - 1) / bn) * ((M + bm - 1) / bm); }
 
-// SYLFEM_B200_GEMM_TILE=128|64 forces one tile shape (measurement switch);
+// SYLFEM_B200_GEMM_TILE=128|64|16 forces one tile shape (measurement switch: 16 =
+// 64 x 64 tiles with 16 x 16 warp tiles);
 // default: 64 x 64 tiles when the 128 x 128 tiles would not fill the SMs.
 int tile_mode() {
     static const int m = [] {
@@ -451,8 +459,13 @@ int launch_dgemm_nt(const double* A, int lda, const double* Bt, int ldb, int M, 
     if (M <= 0 || N <= 0 || K <= 0) return arg_error("empty GEMM");
     const int mode = tile_mode();
     // measured: 64-tiles win below ~64 128-tiles (q = 256: 22 vs 38 us; q = 512:
-    // 27 vs 38 us), tie at 64 (q = 1024), lose from ~100 (q = 1536: 240 vs 228 us)
-    const bool small = mode == 64 || (mode != 128 && tiles_of(M, N, 128, 128) <= 64);
+    // 27 vs 38 us), tie at 64 (q = 1024), lose from ~100 (q = 1536: 240 vs 228 us);
+    // at <= 16 128-tiles (q <= 512) the DMMA pipe is latency bound with one warp
+    // per SM sub-partition and 16 warps of 16 x 16 win (q = 256: 18.4 vs 21.6 us,
+    // q = 512: 23.6 vs 27.1 us; q = 1024: 85.2 vs 84.2 us)
+    const int t128 = tiles_of(M, N, 128, 128);
+    if (mode == 16 || (mode == 0 && t128 <= 16)) return launch_tile<TinyTile>(A, lda, Bt, ldb, M, N, K, ep, stream);
+    const bool small = mode == 64 || (mode != 128 && t128 <= 64);
     return small ? launch_tile<SmallTile>(A, lda, Bt, ldb, M, N, K, ep, stream)
                  : launch_tile<BigTile>(A, lda, Bt, ldb, M, N, K, ep, stream);
 }
