@@ -275,7 +275,7 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": DATA,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": DATA,
         "config": {"workload": wl_name, "step": "one MO-PCG iteration of a step-0 system"
                    + (" (species alternate)" if len(systems) > 1 else ""),
                    "parallelism": "host BLAS threads", "setup_s": round(setup, 1)},
@@ -553,7 +553,7 @@ def run_cfg5(args):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * elapsed / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": DATA,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": DATA,
         "config": {"workload": cfg5_name(args, qy, qx), "iterations_per_step": 2 * K,
                    "inner": f"InnerSolver(rule='budget', max_iter={K}, precond_mode='{args.precond_mode}') per species",
                    "preconditioner_mode": args.precond_mode,
@@ -721,7 +721,7 @@ def run_cfg3(args):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * elapsed / args.steps, "higher_is_better": True,
-        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64", "data": DATA,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": DATA,
         "config": {"workload": f"cfg3 (BASELINE configs[2]): wave domain, P2, Dirichlet, N={args.N}, "
                                f"q={qy}x{qx}, {len(op)}-term operator, MO-PCG with elliptic_xnormal "
                                f"preconditioner ({args.precond_mode})",
