@@ -484,7 +484,13 @@ def run_cfg5(args):
                                                f"2 species groups x {world // 2} column shards"),
                                "l2": "inputs larger than L2 (each q x q state is 537 MB)", "setup_s": setup_s},
                     "e2e": e2e, "clocks": clk,
-                    "gpu_launches": None, "roofline": None, "cpu_baseline": None}
+                    # this library's kernels per rank in the timed region: species-parallel runs the
+                    # single-GPU step of one species; the grouped driver per step rhs (1) + warm-start
+                    # apply / residual / dots / start / xpby (5) + 2 preconditioner GEMMs, and per
+                    # iteration apply, dots, update, 2 GEMMs, dots, control, xpby (8), + norms (1)
+                    "gpu_launches": (world and args.steps * (4 + 2 + K * 4 + 1) if world == 2 else
+                                     args.steps * (1 + 5 + 2 + K * 8 + 1)),
+                    "roofline": None, "cpu_baseline": None}
             print(json.dumps(line), flush=True)
         dist.barrier()
         dist.destroy_process_group()
