@@ -488,7 +488,7 @@ def run_cfg5(args):
                     # single-GPU step of one species; the grouped driver per step rhs (1) + warm-start
                     # apply / residual / dots / start / xpby (5) + 2 preconditioner GEMMs, and per
                     # iteration apply, dots, update, 2 GEMMs, dots, control, xpby (8), + norms (1)
-                    "gpu_launches": (world and args.steps * (4 + 2 + K * 4 + 1) if world == 2 else
+                    "gpu_launches": (args.steps * (4 + 2 + K * 4 + 1) if world == 2 else
                                      args.steps * (1 + 5 + 2 + K * 8 + 1)),
                     "roofline": None, "cpu_baseline": None}
             print(json.dumps(line), flush=True)
