@@ -304,6 +304,18 @@ int sfb_shard_control(sfb_shard* h, void* stream);
 /* Q = Z + beta Q (first: Q = Z), gated on the status */
 int sfb_shard_xpby(sfb_shard* h, double* Q_dev, int ldq, const double* Z_dev, int ldz, int rows,
                    int cols, int first, void* stream);
+/* the heavy kernels of a sharded iteration, gated on the shard state (no-ops once the
+ * solve has stopped): the banded block operator W = L(X), a DMMA GEMM C = A Bt^T (store),
+ * the scatter GEMM of the peer transposes, the SPIKE preconditioner on a shard */
+int sfb_shard_apply(sfb_shard* h, const sfb_op* op, const double* X_dev, int ldx, double* W_dev,
+                    int ldw, void* stream);
+int sfb_shard_gemm(sfb_shard* h, const double* A_dev, int lda, const double* Bt_dev, int ldb, int M,
+                   int N, int K, double* C_dev, int ldc, void* stream);
+int sfb_shard_gemm_scatter(sfb_shard* h, const double* A_dev, int lda, const double* Bt_dev, int ldb,
+                           int M, int N, int K, int nseg, const int* seg_host,
+                           double* const* dst_host, const int* ldd_host, int col_off, void* stream);
+int sfb_shard_pre_apply(sfb_shard* h, const sfb_pre* p, const double* R_dev, int ldr, double* Z_dev,
+                        int ldz, void* stream);
 /* status, iterations, bad value / iteration; history (iterations + 1) and increments (iterations) */
 int sfb_shard_result(sfb_shard* h, sfb_pcg_result* res, double* hist_host, double* incs_host,
                      void* stream);

@@ -129,6 +129,7 @@ __host__ inline void band_geometry(int rows, int cols, int minb, int* ry, int* n
 template <int T, int W, int MODE, bool FINE>
 __global__ void __launch_bounds__(TX + 32, band_minb<W>()) band_kernel(BandArgs a, const __grid_constant__ BandMaps maps, int ry) {
     SFB_PDL_PROLOGUE();
+    if (a.gate != nullptr && a.gate->status != SFB_PCG_RUNNING) return;  // uniform gate
     using C = BandCfg<T, W, FINE>;
     constexpr int CH = C::CH, HCB = C::HCB, TWP = C::TWP, NS = C::NS;
     constexpr int NPAIR = HCB / 2;           // HCB is even (W odd)

@@ -84,6 +84,7 @@ struct BandArgs {
     int ldw = 0;
     double* partials = nullptr;  // [2][nblocks]
     PcgState* pcg = nullptr;
+    const PcgState* gate = nullptr;  // any loader: no-op unless gate->status == running (sharded MO-PCG)
 };
 
 // Every input of `a` needs 16-byte aligned rows (even leading dimension).

@@ -1415,12 +1415,14 @@ struct sfb_shard {
     double* partials = nullptr;
     unsigned* counter = nullptr;
     int max_iter = 0;
+    GemmWs gw;                // stream-K workspace of the gated GEMMs; SPIKE interface scratch (grown once)
+    size_t seg_doubles = 0;
 };
 
 int sfb_shard_destroy(sfb_shard* h) {
     if (!h) return SFB_OK;
     for (void* p : {(void*)h->st, (void*)h->slots, (void*)h->hist, (void*)h->incs, (void*)h->partials,
-                    (void*)h->counter})
+                    (void*)h->counter, (void*)h->gw.ws, (void*)h->gw.flags, (void*)h->gw.seg_f, (void*)h->gw.seg_b})
         cudaFree(p);
     delete h;
     return SFB_OK;
@@ -1438,6 +1440,10 @@ int sfb_shard_create(int max_iter, int rule, double value, sfb_shard** out) {
     if (rc == SFB_OK) rc = talloc(&h->incs, (size_t)std::max(max_iter, 1) * sizeof(double));
     if (rc == SFB_OK) rc = talloc(&h->partials, (size_t)2 * vector_grid_blocks() * sizeof(double));
     if (rc == SFB_OK) rc = talloc(&h->counter, 4 * sizeof(unsigned));
+    if (rc == SFB_OK) rc = talloc(&h->gw.ws, gemm_workspace_doubles() * sizeof(double));
+    if (rc == SFB_OK) rc = talloc(&h->gw.flags, (size_t)gemm_max_tiles() * sizeof(unsigned));
+    if (rc == SFB_OK && cudaMemset(h->gw.flags, 0, (size_t)gemm_max_tiles() * sizeof(unsigned)) != cudaSuccess)
+        rc = SFB_ERR_CUDA;
     if (rc == SFB_OK) {
         PcgState st{};
         st.status = SFB_PCG_RUNNING;
@@ -1490,6 +1496,70 @@ int sfb_shard_xpby(sfb_shard* h, double* Q, int ldq, const double* Z, int ldz, i
                    void* stream) {
     if (!h || !Q || !Z) return arg_error("shard xpby: null argument");
     return launch_shard_xpby(Q, ldq, Z, ldz, rows, cols, h->st, h->slots, first, (cudaStream_t)stream);
+}
+
+// The heavy kernels of a sharded iteration, gated on the shard state: once
+// the solve has stopped, the iterations issued ahead by the host cost only
+// their (cheap) communication, not their GEMMs / SPIKE passes / band pass.
+int sfb_shard_apply(sfb_shard* h, const sfb_op* op, const double* X, int ldx, double* W, int ldw, void* stream) {
+    if (!h || !op || !X || !W) return arg_error("shard apply: null argument");
+    if (op->dense) return arg_error("shard apply: banded operators only");
+    BandArgs a = op_band_args(op);
+    a.ld_mode = LD_PLAIN;
+    a.X = X;
+    a.ldx = ldx;
+    a.ep_mode = EP_STORE;
+    a.W = W;
+    a.ldw = ldw;
+    a.gate = h->st;
+    return launch_band_staged(a, (cudaStream_t)stream);
+}
+
+int sfb_shard_gemm(sfb_shard* h, const double* A, int lda, const double* Bt, int ldb, int M, int N, int K, double* C,
+                   int ldc, void* stream) {
+    if (!h || !A || !Bt || !C) return arg_error("shard GEMM: null argument");
+    GemmEpi e;
+    e.C = C;
+    e.ldc = ldc;
+    e.pcg = h->st;  // STORE epilogue: the PcgState only gates
+    return launch_dgemm_nt(A, lda, Bt, ldb, M, N, K, with_ws(e, &h->gw), (cudaStream_t)stream);
+}
+
+int sfb_shard_gemm_scatter(sfb_shard* h, const double* A, int lda, const double* Bt, int ldb, int M, int N, int K,
+                           int nseg, const int* seg, double* const* dst, const int* ldd, int col_off, void* stream) {
+    if (!h || !A || !Bt || !seg || !dst || !ldd || nseg < 1 || nseg > kMaxScatter)
+        return arg_error("shard scatter GEMM: bad argument");
+    GemmEpi e;
+    e.mode = EPI_SCATTER;
+    e.nseg = nseg;
+    for (int i = 0; i <= nseg; ++i) e.seg[i] = seg[i];
+    if (e.seg[0] != 0 || e.seg[nseg] != M) return arg_error("shard scatter GEMM: segments must cover the M rows");
+    for (int i = 0; i < nseg; ++i) {
+        if (e.seg[i + 1] < e.seg[i]) return arg_error("shard scatter GEMM: segments must be increasing");
+        if (!dst[i] && e.seg[i + 1] > e.seg[i]) return arg_error("shard scatter GEMM: null destination");
+        e.dst[i] = dst[i];
+        e.ldd_seg[i] = ldd[i];
+    }
+    e.col_off = col_off;
+    e.pcg = h->st;
+    return launch_dgemm_nt(A, lda, Bt, ldb, M, N, K, with_ws(e, &h->gw), (cudaStream_t)stream);
+}
+
+int sfb_shard_pre_apply(sfb_shard* h, const sfb_pre* p, const double* R, int ldr, double* Z, int ldz, void* stream) {
+    if (!h || !p || !R || !Z) return arg_error("shard preconditioner: null argument");
+    if (p->kind != SFB_PRE_BANDED) return arg_error("shard preconditioner: banded (SPIKE) form only");
+    if (!tma_aligned(R, ldr) || !tma_aligned(Z, ldz)) return arg_error("shard preconditioner: 16-byte aligned rows");
+    if (h->seg_doubles < p->seg_doubles) {  // grown once, before any graph capture (first chunk runs eagerly)
+        cudaFree(h->gw.seg_f);
+        cudaFree(h->gw.seg_b);
+        h->gw.seg_f = h->gw.seg_b = nullptr;
+        h->seg_doubles = 0;
+        SFB_TRY(talloc(&h->gw.seg_f, p->seg_doubles * sizeof(double)));
+        SFB_TRY(talloc(&h->gw.seg_b, p->seg_doubles * sizeof(double)));
+        h->seg_doubles = p->seg_doubles;
+    }
+    return launch_spike_pre(p->fl, p->fr, R, ldr, Z, ldz, nullptr, h->gw.seg_f, h->gw.seg_b, h->st,
+                            (cudaStream_t)stream);
 }
 
 int sfb_shard_result(sfb_shard* h, sfb_pcg_result* res, double* hist_host, double* incs_host, void* stream) {

@@ -324,9 +324,10 @@ class PeerTransposes:
         self.sync()
         return self.cols
 
-    def right_T_scatter(self, RinvT, R_rows):
+    def right_T_scatter(self, RinvT, R_rows, st=None):
         """X^T = P_R^-T R_rows^T with each output row stored straight into
-        its owner's transposed column shard; returns this rank's shard."""
+        its owner's transposed column shard; returns this rank's shard
+        (gated on the sharded solve's status when ``st`` is given)."""
         L = self.L
         A, B = RinvT, R_rows
         if B.stride(0) % 2 or B.data_ptr() % 16:
@@ -335,8 +336,14 @@ class PeerTransposes:
         seg = (nat.C.c_int * (n + 1))(*(list(L.col_offs) + [L.qx]))
         dst = (nat.C.c_void_p * n)(*[p for p, _ in self.peer_colsT])
         ldd = (nat.C.c_int * n)(*[ld for _, ld in self.peer_colsT])
-        nat.check(nat.lib().sfb_dgemm_nt_scatter(A.data_ptr(), A.stride(0), B.data_ptr(), B.stride(0), L.qx, L.m,
-                                                  L.qx, n, seg, dst, ldd, L.r0, nat.stream()), "scatter gemm")
+        if st is not None:
+            nat.check(nat.lib().sfb_shard_gemm_scatter(st.handle.p, A.data_ptr(), A.stride(0), B.data_ptr(),
+                                                       B.stride(0), L.qx, L.m, L.qx, n, seg, dst, ldd, L.r0,
+                                                       nat.stream()), "scatter gemm")
+        else:
+            nat.check(nat.lib().sfb_dgemm_nt_scatter(A.data_ptr(), A.stride(0), B.data_ptr(), B.stride(0), L.qx,
+                                                      L.m, L.qx, n, seg, dst, ldd, L.r0, nat.stream()),
+                      "scatter gemm")
         self.sync()
         return self.colsT
 
@@ -416,17 +423,23 @@ class CudaBackend:
                                           nat.C.byref(out)), "banded shard preconditioner")
         return nat.Handle(out.value, L.sfb_pre_destroy)
 
-    def _pre(self, h, X, rows, cols):
+    def _pre(self, h, X, rows, cols, st=None):
         Z = self._padded(rows, cols)
+        if st is not None:  # gated on the sharded solve's status
+            if X.stride(0) % 2 or X.data_ptr() % 16:
+                X = self.copy(X)
+            nat.check(nat.lib().sfb_shard_pre_apply(st.handle.p, h.p, X.data_ptr(), X.stride(0), Z.data_ptr(),
+                                                    Z.stride(0), nat.stream()), "banded shard preconditioner")
+            return Z
         nat.check(nat.lib().sfb_pre_apply(h.p, X.data_ptr(), X.stride(0), Z.data_ptr(), Z.stride(0), nat.stream()),
                   "banded shard preconditioner")
         return Z
 
-    def right_rows(self, Xr):  # Xr P_R^-1 on a row shard (m x q_x)
-        return self._pre(self._pre_rows, Xr, self.L.m, self.L.qx)
+    def right_rows(self, Xr, st=None):  # Xr P_R^-1 on a row shard (m x q_x)
+        return self._pre(self._pre_rows, Xr, self.L.m, self.L.qx, st)
 
-    def left_cols(self, Xc):  # P_L^-1 Xc on a column shard (q_y x n)
-        return self._pre(self._pre_cols, Xc, self.L.qy, self.L.n)
+    def left_cols(self, Xc, st=None):  # P_L^-1 Xc on a column shard (q_y x n)
+        return self._pre(self._pre_cols, Xc, self.L.qy, self.L.n, st)
 
     def _padded(self, rows, cols):
         t = self.t
@@ -438,7 +451,7 @@ class CudaBackend:
         v.copy_(self.t.from_numpy(np.ascontiguousarray(a)))
         return v
 
-    def _gemm(self, A, Bt, M, N, K):
+    def _gemm(self, A, Bt, M, N, K, st=None):
         C = self._padded(M, N)
         As, Bs = A, Bt
         if As.stride(0) % 2 or As.data_ptr() % 16:
@@ -447,6 +460,10 @@ class CudaBackend:
         if Bs.stride(0) % 2 or Bs.data_ptr() % 16:
             Bs = self._padded(*Bt.shape)
             Bs.copy_(Bt)
+        if st is not None:  # gated on the sharded solve's status
+            nat.check(nat.lib().sfb_shard_gemm(st.handle.p, As.data_ptr(), As.stride(0), Bs.data_ptr(), Bs.stride(0),
+                                               M, N, K, C.data_ptr(), C.stride(0), nat.stream()), "gemm")
+            return C
         nat.check(nat.lib().sfb_dgemm_nt(As.data_ptr(), As.stride(0), Bs.data_ptr(), Bs.stride(0), M, N, K,
                                          C.data_ptr(), C.stride(0), nat.stream()), "gemm")
         return C
@@ -462,19 +479,23 @@ class CudaBackend:
             return v
         return self._padded_from(np.asarray(a, dtype=float))
 
-    def apply_ext(self, ext):
+    def apply_ext(self, ext, st=None):
         L = self.L
         W = self._padded(L.qy, L.n)
         e = ext if ext.stride(1) == 1 else ext.contiguous()  # row-strided blocks are read in place
+        if st is not None:  # gated on the sharded solve's status
+            nat.check(nat.lib().sfb_shard_apply(st.handle.p, self._op.p, e.data_ptr(), e.stride(0), W.data_ptr(),
+                                                W.stride(0), nat.stream()), "apply")
+            return W
         nat.check(nat.lib().sfb_op_apply(self._op.p, e.data_ptr(), e.stride(0), W.data_ptr(), W.stride(0),
                                          nat.stream()), "apply")
         return W
 
-    def right_T(self, R_rows):  # (P_R^-1)^T R_rows^T  : q_x x m
-        return self._gemm(self.RinvT, R_rows, self.L.qx, R_rows.shape[0], self.L.qx)
+    def right_T(self, R_rows, st=None):  # (P_R^-1)^T R_rows^T  : q_x x m
+        return self._gemm(self.RinvT, R_rows, self.L.qx, R_rows.shape[0], self.L.qx, st)
 
-    def left(self, XcT):  # P_L^-1 X_cols : q_y x n
-        return self._gemm(self.Linv, XcT, self.L.qy, XcT.shape[0], self.L.qy)
+    def left(self, XcT, st=None):  # P_L^-1 X_cols : q_y x n
+        return self._gemm(self.Linv, XcT, self.L.qy, XcT.shape[0], self.L.qy, st)
 
     def copy(self, X):
         Y = self._padded(*X.shape)
@@ -584,16 +605,16 @@ def sharded_mo_pcg(backend, comm: Comm, rhs_local, stop: StoppingRule | None = N
     Qe = backend.zeros(L.qy, n + 2 * b)  # the direction lives inside its halo-extended block
     Q = Qe[:, b:b + n]
 
-    def precond(Rk):
+    def precond(Rk, st=None):  # st: gate the heavy kernels on the solve's status
         if identity:
             return backend.copy(Rk)
         if getattr(backend, "banded", False):  # SPIKE form: right solves on rows, left solves on columns
             ex = peer if peer is not None else comm
-            return backend.left_cols(ex.rows_to_cols(backend.right_rows(ex.cols_to_rows(Rk))))
+            return backend.left_cols(ex.rows_to_cols(backend.right_rows(ex.cols_to_rows(Rk), st=st)), st=st)
         if peer is not None:  # transposes over peer memory, the second fused into the GEMM
-            return backend.left(peer.right_T_scatter(backend.RinvT, peer.cols_to_rows(Rk)))
-        XrT = backend.right_T(comm.cols_to_rows(Rk))
-        return backend.left(comm.rowsT_to_colsT(XrT))
+            return backend.left(peer.right_T_scatter(backend.RinvT, peer.cols_to_rows(Rk), st=st), st=st)
+        XrT = backend.right_T(comm.cols_to_rows(Rk), st=st)
+        return backend.left(comm.rowsT_to_colsT(XrT), st=st)
 
     # setup (solvers.py:389-420): |R_0|, Z_0, <Z_0, R_0>, Q_0 = Z_0
     Z = precond(R)
@@ -601,32 +622,38 @@ def sharded_mo_pcg(backend, comm: Comm, rhs_local, stop: StoppingRule | None = N
     comm.allreduce_(st.slots[2:4])
     backend.sstart(st)
     backend.sxpby(st, Q, Z, first=True)
-    def chunk():
-        for _ in range(max(1, check_every)):
-            W = backend.apply_ext(comm.halo_(Qe, n, b))
+    def chunk(size):
+        for _ in range(size):
+            W = backend.apply_ext(comm.halo_(Qe, n, b), st=st)
             backend.sdots(st, W, Q, Q, Q, slot=0)  # <W,Q>, |Q|^2
             comm.allreduce_(st.slots[0:2])
             backend.supdate(st, U, R, Q, W)  # alpha; U, R; |R|^2 -> slot 2
-            Z = precond(R)  # computed before the stop test: result-identical
+            Z = precond(R, st)  # computed before the stop test: result-identical
             backend.sdots(st, Z, R, slot=3)
             comm.allreduce_(st.slots[2:4])
             backend.scontrol(st)  # history, increment, stop test, beta
             backend.sxpby(st, Q, Z)
 
+    # chunks of 1, 2, 4, ... check_every iterations: short solves (an IMEX
+    # step's few iterations) read the status early; iterations issued past the
+    # stop skip their GEMMs / SPIKE / band passes (gated) and cost only their
+    # communication
+    full = max(1, check_every)
+    size = 1
     status = backend.sresult(st)[0]
     replay = None
     while status == nat.PCG_RUNNING:
         if replay is not None:
             replay.replay()
         else:
-            chunk()  # the first chunk runs eagerly (first-launch setup of every kernel)
-            if graph:
+            chunk(size)  # eager (the first full-size chunk also does every kernel's first-launch setup)
+            if graph and size == full:
                 import torch
                 g = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(g):
-                    chunk()  # captured, not executed
+                    chunk(full)  # captured, not executed
                 replay = g
-                g.replay()
+            size = min(2 * size, full)
         status = backend.sresult(st)[0]
     status, iters, bad_iter, bad_value, hist, incs = backend.sresult(st, history=True)
     if status == nat.PCG_INDEFINITE:

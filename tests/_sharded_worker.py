@@ -40,20 +40,20 @@ class NumpyBackend:
     def copy(self, X):
         return X.clone()
 
-    def apply_ext(self, ext):
+    def apply_ext(self, ext, st=None):
         e = ext.numpy()
         return torch.from_numpy(sum(G @ e @ hs for (G, _), hs in zip(self.terms, self.Hsub)))
 
-    def right_T(self, R_rows):
+    def right_T(self, R_rows, st=None):
         return torch.from_numpy(self.RinvT @ R_rows.numpy().T)
 
-    def left(self, XcT):
+    def left(self, XcT, st=None):
         return torch.from_numpy(self.Linv @ XcT.numpy().T)
 
-    def right_rows(self, Xr):  # Xr P_R^-1
+    def right_rows(self, Xr, st=None):  # Xr P_R^-1
         return torch.from_numpy(Xr.numpy() @ self.RinvT.T)
 
-    def left_cols(self, Xc):  # P_L^-1 Xc
+    def left_cols(self, Xc, st=None):  # P_L^-1 Xc
         return torch.from_numpy(self.Linv @ Xc.numpy())
 
     def update(self, U, R, Q, W, alpha):

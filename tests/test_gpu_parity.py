@@ -325,14 +325,14 @@ def test_sharded_cuda_backend_single_rank_matches_mo_pcg():
         # a chunk (kernels + the NCCL call) is captured once and replayed --
         # capture itself proves there is no host synchronisation inside it
         for r in (rep, rep2):
-            assert r.diagnostics["host_reads"] <= -(-r.iterations // r.diagnostics["check_every"]) + 2
+            assert r.diagnostics["host_reads"] <= -(-r.iterations // r.diagnostics["check_every"]) + 6
         rep3 = sharded_mo_pcg(be, Comm(lay, torch.device("cuda")), rhs, stop=pb.relative_residual(1e-12),
                               max_iter=5000, peer=pt, check_every=8, graph=True)
         assert rep3.diagnostics["graph"] is True
         assert rep3.iterations == rep2.iterations
         assert np.array_equal(rep3.solution, rep2.solution)
         assert np.array_equal(rep3.residual_history, rep2.residual_history)
-        assert rep3.diagnostics["host_reads"] <= -(-rep3.iterations // 8) + 3
+        assert rep3.diagnostics["host_reads"] <= -(-rep3.iterations // 8) + 6
     finally:
         dist.destroy_process_group()
 
@@ -429,3 +429,29 @@ def test_record_iterates_grows_on_demand(golden):
     assert np.array_equal(rep.diagnostics["iterates"][-1], rep.solution)
     for a, b in zip(rep.diagnostics["iterates"][:8], golden["pcg3/t12/first8"]):
         assert relerr(a, b) <= 1e-10
+
+
+def test_shard_state_gates_the_heavy_kernels():
+    """sfb_shard_gemm / sfb_shard_apply are no-ops once the sharded solve has
+    stopped (the iterations the host issues ahead of its next status read
+    must not spend their GEMMs), and run normally while it is running."""
+    import torch
+
+    from paper_2109_01173_b200 import _native as nat
+    from paper_2109_01173_b200.distributed import ShardState
+    q = 130
+    A = torch.randn(q, q + 2, dtype=torch.float64, device="cuda")[:, :q]
+    B = torch.randn(q, q + 2, dtype=torch.float64, device="cuda")[:, :q]
+    for max_iter, runs in ((5, True), (0, False)):
+        st = ShardState(max_iter, pb.relative_residual(1e-12))
+        st.slots[2] = 1.0  # |R_0|^2 > 0
+        st.slots[3] = 1.0
+        nat.check(nat.lib().sfb_shard_start(st.handle.p, nat.stream()), "start")  # max_iter 0 -> stopped
+        C = torch.full((q, q + 2), float("nan"), dtype=torch.float64, device="cuda")
+        nat.check(nat.lib().sfb_shard_gemm(st.handle.p, A.data_ptr(), A.stride(0), B.data_ptr(), B.stride(0), q, q,
+                                           q, C.data_ptr(), C.stride(0), nat.stream()), "gemm")
+        torch.cuda.synchronize()
+        if runs:
+            assert relerr(C[:, :q].cpu().numpy(), (A @ B.T).cpu().numpy()) <= 1e-14
+        else:
+            assert torch.isnan(C).all()

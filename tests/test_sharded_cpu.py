@@ -43,4 +43,4 @@ def test_sharded_mo_pcg_matches_single_process(world, warm, banded):
     # device-resident loop: the host reads the state once per chunk of
     # iterations (+ setup and the final report), never per iteration
     for p in parts:
-        assert int(p["host_reads"]) <= -(-it // int(p["check_every"])) + 2
+        assert int(p["host_reads"]) <= -(-it // int(p["check_every"])) + 6  # + the 1, 2, 4, 8 ramp
