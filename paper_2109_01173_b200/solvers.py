@@ -999,27 +999,37 @@ def vector_pcg(K, b, P=None, stop: StoppingRule | None = None, x0=None, max_iter
 def solve_direct(op: SylvesterOperator, rhs) -> SolveReport:
     """Solution of the Kronecker system to round-off (solvers.py:521-555).
 
-    The reference factors to_kronecker(op) with sparse LU.  Here the system is
-    solved on the device: the spectral reduced solve for two-term operators,
-    otherwise MO-PCG to a 1e-14 relative residual with the two-term spectral
-    preconditioner of the operator's first two terms; the reference's
-    Kronecker guard, relative-residual check (> 1e-9 -> SolverError) and report
-    fields are kept.  Symmetric positive definite operators only."""
+    The reference factors to_kronecker(op) with sparse LU.  Here symmetric
+    positive definite operators are solved entirely on the device: the
+    spectral reduced solve for two-term operators, otherwise MO-PCG to a
+    1e-14 relative residual with the two-term spectral preconditioner of the
+    operator's first two terms.  Any other operator takes the reference's
+    own route — SuperLU factors of the Kronecker matrix (host, once), the
+    triangular solves on the device (sfb_lu_solve); an exactly singular
+    factor raises SolverError like the reference.  The reference's Kronecker
+    guard, relative-residual check (> 1e-9 -> SolverError) and report fields
+    are kept."""
     t0 = time.perf_counter()
     rhs = np.asarray(rhs, dtype=float)
     K = to_kronecker(op)  # the reference's guard and the residual check below
-    if not (op.symmetric and op.positive_definite):
-        raise SolverError("the device direct solve needs an operator flagged symmetric positive definite")
     if tuple(rhs.shape) != tuple(op.shape):
         raise OperatorError(f"grid shape {rhs.shape} does not match operator {op.shape}")
-    try:
-        if len(op.terms) == 2:
-            U = solve_reduced(op, rhs).solution
-        else:
-            pre = two_term_preconditioner(op)
-            U = mo_pcg(op, rhs, precond=pre, stop=relative_residual(1e-14), max_iter=100000).solution
-    except (SolverError, np.linalg.LinAlgError):
-        U = mo_pcg(op, rhs, stop=relative_residual(1e-14), max_iter=100000).solution
+    if not (op.symmetric and op.positive_definite):
+        t = nat.torch()
+        n = K.shape[0]
+        lu = _DeviceLU(K, n)
+        zd = t.empty((1, n), dtype=t.float64, device="cuda")
+        lu.solve(t.from_numpy(np.ascontiguousarray(vec(rhs)).reshape(1, n)).cuda(), zd)
+        U = unvec(nat.to_host(zd).reshape(-1), op.shape)
+    else:
+        try:
+            if len(op.terms) == 2:
+                U = solve_reduced(op, rhs).solution
+            else:
+                pre = two_term_preconditioner(op)
+                U = mo_pcg(op, rhs, precond=pre, stop=relative_residual(1e-14), max_iter=100000).solution
+        except (SolverError, np.linalg.LinAlgError):
+            U = mo_pcg(op, rhs, stop=relative_residual(1e-14), max_iter=100000).solution
     b = vec(rhs)
     Kd = _DeviceCSR(K)
     t = nat.torch()

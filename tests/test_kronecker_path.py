@@ -112,6 +112,32 @@ def test_solve_direct_matches_dense_solve(k, N):
 
 
 @pytest.mark.gpu
+def test_solve_direct_non_spd_and_singular_operators():
+    """Operators not flagged SPD take the reference's route (SuperLU factors
+    of the Kronecker matrix, solved on the device); reference
+    tests/test_solvers.py:295-330: identity returns the rhs, a singular
+    operator raises SolverError."""
+    rng = np.random.default_rng(9)
+    q = 9
+    G = np.eye(q) * 4 + np.diag(np.ones(q - 1), 1) * 1.5 - np.diag(np.ones(q - 1), -1) * 0.5  # non-symmetric
+    H = np.eye(q) * 3 + np.diag(np.ones(q - 1), -1)
+    op = pb.SylvesterOperator([(G, H), (np.eye(q), np.diag(np.arange(1.0, q + 1)))])
+    rhs = rng.standard_normal((q, q))
+    rep = pb.solve_direct(op, rhs)
+    K = pb.to_kronecker(op).toarray()
+    assert relerr(rep.solution, pb.unvec(np.linalg.solve(K, pb.vec(rhs)), op.shape)) <= 1e-12
+    assert rep.residual_history[0] <= 1e-12
+    ident = pb.SylvesterOperator([(np.eye(5), np.eye(5))])
+    r5 = rng.standard_normal((5, 5))
+    assert np.allclose(pb.solve_direct(ident, r5).solution, r5, atol=1e-13)
+    x, y = pb.build_direction_sets(pb.SQUARE, 1, 8, pb.BCKind.NEUMANN)
+    A, M = np.asarray(x.mats.A), np.asarray(x.mats.M)
+    sing = pb.SylvesterOperator([(A, M), (M, A)], symmetric=True, positive_definite=False)
+    with pytest.raises(pb.SolverError):
+        pb.solve_direct(sing, np.ones(sing.shape))
+
+
+@pytest.mark.gpu
 def test_vector_imex_drivers_match_reference_trajectories(golden):
     # heat, cfg4-type (5-term step operator: MO-PCG to round-off per step)
     x, y = pb.build_direction_sets(WAVE, 4, 8, D)
