@@ -41,6 +41,9 @@ constexpr int KBOX = 16;  // doubles per 128-byte swizzled TMA box row (one box 
 #ifndef GEMM_GROUP_M
 #define GEMM_GROUP_M 0  // tile raster: bands of GROUP_M tile rows (0: row-major)
 #endif
+#ifndef GEMM_HYBRID
+#define GEMM_HYBRID 1  // full waves data parallel + stream-K tail (0: stream-K over all tiles)
+#endif
 #ifndef GEMM_SMALL_MINWORK
 #define GEMM_SMALL_MINWORK 4  // k-tiles per CTA at least, 64x64 tiles
 #endif
@@ -95,12 +98,19 @@ __device__ __forceinline__ double2 lds128(uint32_t addr) {
     return v;
 }
 
+// Hybrid schedule: `waves` full waves of whole tiles in data-parallel order
+// (CTA c takes tiles c, c + G, c + 2G, ...: the CTAs of a wave walk k in
+// lockstep over neighbouring tiles and share their A / B k-slices in L2),
+// then the remaining tiles' (tile, k-tile) iterations split stream-K over
+// all G CTAs (CTA c owns tail iterations [c U / G, (c+1) U / G)), which
+// balances the last partial wave.
 struct Sched {
     int tiles_n;         // tiles along N
     int KT;              // k-tiles per output tile
-    long long U;         // total (tile, k-tile) iterations
+    long long U;         // stream-K (tail) iterations
     int G;               // CTAs
     int tiles_total;     // output tiles (one <C,D> partial each)
+    int waves;           // data-parallel full waves (tiles 0 .. waves * G - 1)
     __device__ long long start(int c) const { return (long long)c * U / G; }
     // tile -> output origin: tiles run down GROUP_M-row bands column by column,
     // so the CTAs in flight share A and B panels in L2 (plain row-major with 0)
@@ -116,7 +126,7 @@ struct Sched {
         n0 = (tile % tiles_n) * bn;
 #endif
     }
-    __device__ int owner(long long i) const {  // CTA whose range holds linear iteration i
+    __device__ int owner(long long i) const {  // CTA whose tail range holds tail iteration i
         int c = (int)((i * G) / U);
         while (c + 1 < G && start(c + 1) <= i) ++c;
         while (c > 0 && start(c) > i) --c;
@@ -223,12 +233,25 @@ __global__ void __launch_bounds__(T::NTHREADS, T::CTAS_PER_SM)
     constexpr int MI = T::MI, NJ = T::NJ, WM = T::WM, WN = T::WN;
     const int g = lane >> 2, t = lane & 3;
     const int KT = sc.KT;
-    const long long beg = sc.start(blockIdx.x), fin = sc.start(blockIdx.x + 1);
-    const int n_it = (int)(fin - beg);
+    const long long beg = sc.start(blockIdx.x), fin = sc.start(blockIdx.x + 1);  // tail range
+    const int n_dp = sc.waves * KT;               // data-parallel iterations of this CTA
+    const int n_it = n_dp + (int)(fin - beg);
+    const int tail0 = sc.waves * sc.G;            // first tail tile
+    // local iteration -> (tile, k-tile)
+    auto locate = [&](int it, int& tile, int& kt) {
+        if (it < n_dp) {
+            tile = (int)blockIdx.x + (it / KT) * sc.G;
+            kt = it % KT;
+        } else {
+            const long long li = beg + (it - n_dp);
+            tile = tail0 + (int)(li / KT);
+            kt = (int)(li - (long long)(tile - tail0) * KT);
+        }
+    };
 
     auto issue = [&](int it) {  // TMA for local iteration `it` into its ring slot
-        const long long li = beg + it;
-        const int tile = (int)(li / KT), kt = (int)(li - (long long)tile * KT);
+        int tile, kt;
+        locate(it, tile, kt);
         int m0, n0;
         sc.origin(tile, BM, BN, m0, n0);
         const int sl = it % STAGES;
@@ -257,8 +280,8 @@ __global__ void __launch_bounds__(T::NTHREADS, T::CTAS_PER_SM)
     double acc[MI][NJ][2];
     int it = 0;
     while (it < n_it) {
-        const long long li0 = beg + it;
-        const int tile = (int)(li0 / KT), k0 = (int)(li0 - (long long)tile * KT);
+        int tile, k0;
+        locate(it, tile, k0);
         const int seg_end = (int)min((long long)n_it, (long long)it + (KT - k0));
         const int kl = k0 + (seg_end - it) - 1;  // last k-tile of this piece
         #pragma unroll
@@ -311,7 +334,9 @@ __global__ void __launch_bounds__(T::NTHREADS, T::CTAS_PER_SM)
         if (k0 != 0 || kl != KT - 1) {
             // split tile: the last piece to arrive finishes it (no CTA ever
             // waits on another, so any residency order makes progress)
-            const int c_first = sc.owner((long long)tile * KT), c_last = sc.owner((long long)(tile + 1) * KT - 1);
+            // (only tail tiles are split)
+            const long long t0 = (long long)(tile - tail0) * KT;
+            const int c_first = sc.owner(t0), c_last = sc.owner(t0 + KT - 1);
             const int me = (int)blockIdx.x;
             const unsigned others = (unsigned)(c_last - c_first);
             auto park = [&]() {
@@ -424,17 +449,25 @@ int launch_tile(const double* A, int lda, const double* Bt, int ldb, int M, int 
     sc.tiles_n = (N + T::BN - 1) / T::BN;
     sc.KT = (K + T::BK - 1) / T::BK;
     const int tiles = tiles_of(M, N, T::BM, T::BN);
-    sc.U = (long long)tiles * sc.KT;
     sc.tiles_total = tiles;
+    sc.waves = 0;
     const bool have_ws = ep.sk_ws != nullptr && ep.sk_flags != nullptr;
-    // stream-K grid: at most CTAS_PER_SM CTAs per SM and a few k-tiles of
-    // work per CTA; tile-aligned data-parallel grid when that already fills
-    // the machine evenly or no workspace is available
+    // grid: at most CTAS_PER_SM CTAs per SM.  Without a workspace, or when the
+    // tiles fill whole waves, one CTA per tile (data parallel).  Otherwise the
+    // full waves of whole tiles run data parallel and the rest stream-K (at
+    // least a few k-tiles per CTA), so the last partial wave is balanced.
     const int slots = num_sms() * T::CTAS_PER_SM;
     if (!have_ws || tiles % slots == 0) {
         sc.G = tiles;
+        sc.waves = 1;  // CTA c: tile c, whole
+        sc.U = 0;
+    } else if (tiles > slots && GEMM_HYBRID) {
+        sc.G = slots;
+        sc.waves = tiles / slots - 1;  // keep one wave + the remainder in the stream-K tail
+        sc.U = (long long)(tiles - sc.waves * slots) * sc.KT;
     } else {
         const long long min_work = T::BM >= 128 ? 8 : GEMM_SMALL_MINWORK;
+        sc.U = (long long)tiles * sc.KT;
         sc.G = (int)std::max(1LL, std::min<long long>(slots, sc.U / min_work));
     }
     return launch_kernel(dgemm_nt_kernel<T>, dim3(sc.G), dim3(T::NTHREADS), T::SMEM_BYTES, stream, ma, mb, M, N, K,
