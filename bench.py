@@ -353,8 +353,8 @@ def hbm_passes(op, pre, reps=20):
     band = 6 * n2 / (pt["operator_ms"] * 1e-3) / 1e9
     upd = 3 * n2 / (pt["update_ms"] * 1e-3) / 1e9
     w = 2 * op.half_bandwidth + 1
-    tr = profile_json("ncu_passes_r02.json") or profile_json("ncu_passes_r01.json")
-    key = f"band_kernel<{len(op)},{w},PCG>"
+    tr = profile_json("ncu_passes_r02.json")
+    key = f"band_kernel<{len(op)},{w},PCG>@q{qy}"
     return {"bound": "hbm", "unit": "GB/s", "peak": peak, "peak_source": src, "q": [qy, qx],
             "banded_operator_pass": {
                 "kernel": f"band_kernel<{len(op)} terms, W={w}> (LD_PCG)", "achieved": band, "frac": band / peak,
@@ -364,7 +364,8 @@ def hbm_passes(op, pre, reps=20):
                         "previous iteration's deferred U += alpha Q)"},
             "vector_update_pass": {
                 "kernel": "pcg_rupdate_kernel", "achieved": upd, "frac": upd / peak, "launch_ms": pt["update_ms"],
-                "algorithmic_bytes": 3 * n2, "traffic": tr.get("pcg_rupdate_kernel", {}).get("dram_bytes_per_launch"),
+                "algorithmic_bytes": 3 * n2,
+                "traffic": tr.get(f"pcg_rupdate_kernel@q{qy}", {}).get("dram_bytes_per_launch"),
                 "note": "read R, W; write R (+ |R|^2, stop test)"},
             "preconditioner_ms": pt["preconditioner_ms"]}
 
@@ -552,7 +553,7 @@ def run_cfg5(args):
     n_gemm = 2 if args.precond_mode == "inverse" else (4 if args.precond_mode == "spectral" else 0)
     roof.update({"share_of_iteration": n_gemm * roof["launch_ms"] / iter_ms if n_gemm else 0.0,
                  "iteration_ms": iter_ms,
-                 "traffic": (profile_json("ncu_dgemm_r02.json") or {}).get("dram_bytes_per_launch")})
+                 "traffic": (profile_json("ncu_dgemm_r02.json").get(f"q{qy}") or {}).get("dram_bytes_per_launch")})
     if args.precond_mode == "banded":
         bp = hbm["banded_operator_pass"]
         roof = {"bound": "hbm", "kernel": bp["kernel"], "achieved": bp["achieved"], "peak": hbm["peak"],
@@ -632,6 +633,7 @@ def cfg3_block(args, steps=5, K=200):
            "value": qy * qx * its / el, "unit": UNIT, "iterations_per_step": K, "ms_per_step": 1e3 * el / steps}
     out["roofline_hbm"] = hbm_passes(op, pre)
     out["roofline"] = gemm_roofline(qy)
+    out["roofline"]["traffic"] = (profile_json("ncu_dgemm_r02.json").get(f"q{qy}") or {}).get("dram_bytes_per_launch")
     if not args.no_full:
         pre_b = pb.make_preconditioner("elliptic_xnormal", w.x, w.y, mode="banded")
         pb.mo_pcg(op, rhs, precond=pre_b, stop=stop, max_iter=10)
