@@ -198,3 +198,36 @@ def test_spectral_cache_host_route(golden):
     bad = pb.SylvesterOperator([(Z, np.eye(2)), (np.eye(2), np.diag([-1.0, 3.0]))])
     with pytest.raises(pb.SolverError, match="singular"):
         pb.build_spectral_cache(bad).check_pencils()
+
+
+def test_rcond_guard_uses_the_exact_condition_near_the_threshold():
+    """solvers.py:90-100 guards with the exact 1-norm condition number; the
+    banded LAPACK estimate is only trusted far from the 1e-14 threshold."""
+    import scipy.sparse as sp
+
+    from paper_2109_01173_b200.banded import Band
+    from paper_2109_01173_b200.solvers import RCOND_GUARD, _rcond, _rcond_guard
+    n = 40
+    for eps in (1e-17, 3e-15, 1e-13, 1e-6):
+        d = np.ones(n)
+        d[7] = eps
+        A = sp.diags([d], [0]).tocsr()
+        exact = 1.0 / np.linalg.cond(A.toarray(), 1)
+        assert _rcond(Band(A)) == pytest.approx(exact, rel=1e-12)
+        if exact < RCOND_GUARD:
+            with pytest.raises(pb.SolverError, match="singular"):
+                _rcond_guard(Band(A), "P_L")
+        else:
+            _rcond_guard(Band(A), "P_L")
+
+
+def test_spectral_form_rejects_non_symmetric_factors():
+    """The spectral form of the preconditioner is the reference's LU solve
+    only for symmetric factors: a non-symmetric one raises instead of being
+    silently symmetrised."""
+    from paper_2109_01173_b200.solvers import Preconditioner
+    F = np.eye(6) * 4 + np.diag(np.ones(5), 1)
+    with pytest.raises(pb.SolverError, match="symmetric"):
+        Preconditioner._eigh(F, 6)
+    lam, V = Preconditioner._eigh(F + F.T, 6)
+    assert np.allclose(V @ np.diag(lam) @ V.T, F + F.T)
