@@ -861,8 +861,6 @@ class CudaSpeciesStepper:
 
     def __init__(self, x, y, d, tau, rho, kinetics, inner, lumped, species):
         from .models import DIBKinetics
-        from .operators import parabolic_operator
-        from .timestepping import _parabolic_precond
         from .timestepping import _step_system
         self.species = species
         self.tau, self.rho = tau, rho
