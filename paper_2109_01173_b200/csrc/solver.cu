@@ -952,8 +952,9 @@ int sfb_reduced_create(const sfb_pre* pre, const sfb_op* op, sfb_reduced** out) 
         } else {
             int c = cudaMemsetAsync(r->red, 0, 3 * sizeof(RedSlots), st) == cudaSuccess ? SFB_OK : SFB_ERR_CUDA;
             if (c == SFB_OK)
+                // plain store epilogue: the reduced solve needs no <U,B>
                 c = pre_apply_impl(pre, r->B, r->ld, r->U, r->ld, r->T1, r->ldt1, r->T2, r->ld, r->parts, nullptr,
-                                   r->red + 2, &r->gw, st);
+                                   nullptr, &r->gw, st);
             if (c == SFB_OK) c = op_apply_impl(op, r->U, r->ld, r->W, r->ld, r->T1, r->ldt1, &r->gw, st);
             // one pass: red[0] = { |B - W|, max|B|, #non-finite, |B| }
             if (c == SFB_OK) c = launch_norms(r->B, r->ld, r->W, r->ld, r->qy, r->qx, r->parts, r->red, st);
