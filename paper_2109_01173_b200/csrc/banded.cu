@@ -194,7 +194,8 @@ __global__ void __launch_bounds__(TX + 32, band_minb<W>()) band_kernel(BandArgs 
     }
     __syncthreads();
 
-    double pdot = 0.0, pqq = 0.0;
+    double pdot = 0.0, pqq = 0.0;  // MO-PCG: <W,Q>, |Q|^2; residual epilogue: |B - W|^2, |B|^2
+    const bool resid = mode == LD_PLAIN && a.ep_mode == EP_RESID;
     bool flag = false;
     double vmax = 0.0;
     if (producer) {
@@ -402,7 +403,14 @@ __global__ void __launch_bounds__(TX + 32, band_minb<W>()) band_kernel(BandArgs 
 #else
                     const double w = acc[slot];
 #endif
-                    if (store) Wout[(size_t)(y0 + i) * ldw + gc] = w;
+                    if (resid) {  // the residual of a reduced solve: no W store
+                        const double bv = store ? a.B[(size_t)(y0 + i) * a.ldb + gc] : 0.0;
+                        const double rv = store ? bv - w : 0.0;
+                        pdot = fma(rv, rv, pdot);
+                        pqq = fma(bv, bv, pqq);
+                    } else if (store) {
+                        Wout[(size_t)(y0 + i) * ldw + gc] = w;
+                    }
                     if constexpr (pcg_ep) {
                         // Q at (y0 + i, gc): centre of halo row i - goff = r - (W-1)/2
                         const double q = store ? cen[(u - (W - 1) / 2 + W) % W] : 0.0;
@@ -423,6 +431,26 @@ __global__ void __launch_bounds__(TX + 32, band_minb<W>()) band_kernel(BandArgs 
         if (vmax > 0.0) atomicMax(a.check, (unsigned long long)__double_as_longlong(vmax));
     }
 
+    if (mode == LD_PLAIN && a.ep_mode == EP_RESID) {  // uniform: sum in fixed order, last block finishes
+        __shared__ double shr[NTH / 32];
+        const unsigned nblk = gridDim.x * gridDim.y;
+        const unsigned bid = blockIdx.y * gridDim.x + blockIdx.x;
+        const double p0 = block_sum<NTH>(pdot, shr);
+        const double p1 = block_sum<NTH>(pqq, shr);
+        if (threadIdx.x == 0) {
+            a.partials[bid] = p0;
+            a.partials[nblk + bid] = p1;
+        }
+        if (arrive_last(&a.res->counter[0], nblk)) {
+            const double rr = sum_partials<NTH>(a.partials, nblk, 1, shr);
+            const double bb = sum_partials<NTH>(a.partials + nblk, nblk, 1, shr);
+            if (threadIdx.x == 0) {
+                a.res->counter[0] = 0;
+                a.res->v[0] = sqrt(rr);
+                a.res->v[3] = sqrt(bb);
+            }
+        }
+    }
     if constexpr (pcg_ep) {
         __shared__ double sh[NTH / 32];
         const unsigned nblk = gridDim.x * gridDim.y;
@@ -553,6 +581,8 @@ int launch_band(const BandArgs& a, cudaStream_t stream) {
     }
     if (a.out_rows <= 0 || a.out_cols <= 0) return SFB_OK;
     if ((a.ep_mode == EP_PCG) != (a.ld_mode == LD_PCG)) return arg_error("banded kernel: MO-PCG loader without its epilogue");
+    if (a.ep_mode == EP_RESID && (a.ld_mode != LD_PLAIN || !a.B || !a.res || !a.partials))
+        return arg_error("banded kernel: the residual epilogue needs the plain loader, B, partials and a result slot");
     if (a.ep_mode == EP_PCG && (a.goff != -(a.width - 1) / 2 || a.hoff != -(a.width - 1) / 2)) {
         set_error("banded kernel: the MO-PCG epilogue needs a centred square operator");
         return SFB_ERR_UNSUPPORTED;

@@ -53,7 +53,7 @@ int gemm_max_tiles();
 
 // ----------------------------------------------------------- banded -------
 enum BandLoad { LD_PLAIN = 0, LD_PCG = 1, LD_HEAT = 2, LD_DIB = 3 };
-enum BandEpi { EP_STORE = 0, EP_PCG = 1 };
+enum BandEpi { EP_STORE = 0, EP_PCG = 1, EP_RESID = 2 };  // EP_RESID: |B - L(X)|, |B| (no store)
 
 struct BandArgs {
     int out_rows = 0, out_cols = 0, in_rows = 0, in_cols = 0;
@@ -85,6 +85,10 @@ struct BandArgs {
     double* partials = nullptr;  // [2][nblocks]
     PcgState* pcg = nullptr;
     const PcgState* gate = nullptr;  // any loader: no-op unless gate->status == running (sharded MO-PCG)
+    // EP_RESID (plain loader): res->v[0] = |B - W|_F, res->v[3] = |B|_F, W not stored
+    const double* B = nullptr;
+    int ldb = 0;
+    RedSlots* res = nullptr;
 };
 
 // Every input of `a` needs 16-byte aligned rows (even leading dimension).

@@ -955,9 +955,23 @@ int sfb_reduced_create(const sfb_pre* pre, const sfb_op* op, sfb_reduced** out) 
                 // plain store epilogue: the reduced solve needs no <U,B>
                 c = pre_apply_impl(pre, r->B, r->ld, r->U, r->ld, r->T1, r->ldt1, r->T2, r->ld, r->parts, nullptr,
                                    nullptr, &r->gw, st);
-            if (c == SFB_OK) c = op_apply_impl(op, r->U, r->ld, r->W, r->ld, r->T1, r->ldt1, &r->gw, st);
-            // one pass: red[0] = { |B - W|, max|B|, #non-finite, |B| }
-            if (c == SFB_OK) c = launch_norms(r->B, r->ld, r->W, r->ld, r->qy, r->qx, r->parts, r->red, st);
+            if (c == SFB_OK && !op->dense) {
+                // banded operator: the residual |B - L(U)|, |B| in the operator pass itself
+                BandArgs a = op_band_args(op);
+                a.ld_mode = LD_PLAIN;
+                a.X = r->U;
+                a.ldx = r->ld;
+                a.ep_mode = EP_RESID;
+                a.B = r->B;
+                a.ldb = r->ld;
+                a.res = r->red;
+                a.partials = r->parts;
+                c = launch_band(a, st);
+            } else if (c == SFB_OK) {
+                c = op_apply_impl(op, r->U, r->ld, r->W, r->ld, r->T1, r->ldt1, &r->gw, st);
+                // one pass: red[0] = { |B - W|, max|B|, #non-finite, |B| }
+                if (c == SFB_OK) c = launch_norms(r->B, r->ld, r->W, r->ld, r->qy, r->qx, r->parts, r->red, st);
+            }
             const cudaError_t e = cudaStreamEndCapture(st, &graph);
             rc = c != SFB_OK ? c : (e == cudaSuccess ? SFB_OK : SFB_ERR_CUDA);
             if (rc == SFB_OK && cudaGraphInstantiate(&r->exec, graph, 0) != cudaSuccess) rc = SFB_ERR_CUDA;
@@ -991,6 +1005,7 @@ int sfb_reduced_solve(sfb_reduced* r, const double* B, int ldb, double* U, int l
         SFB_CUDA_TRY(cudaStreamSynchronize(st));
         res2_host[0] = r->host[0];  // |B - U|-residual numerator
         res2_host[1] = r->host[3];  // |B|
+        return SFB_OK;              // everything is complete: the caller's stream needs no edge
     }
     SFB_CUDA_TRY(cudaEventRecord(r->ev_out, st));
     SFB_CUDA_TRY(cudaStreamWaitEvent(cs, r->ev_out, 0));
