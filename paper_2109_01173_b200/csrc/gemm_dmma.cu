@@ -53,11 +53,11 @@ constexpr int KBOX = 16;  // doubles per 128-byte swizzled TMA box row (one box 
 
 
 // CTA tile BM x BN: 128 x 128 with 16 warps (one CTA per SM) for large
-// GEMMs; 64 x 64 with 4 warps (two CTAs per SM) when the 128-tiles would not
-// fill the machine (at most 64 of them: q <= 1024, the cfg1 / cfg2 reduced
-// solves), so the stream-K pieces stay short and the fix-up traffic small;
-// 64 x 64 with 16 warps of 16 x 16 at <= 16 128-tiles (q <= 512), where one
-// warp per SM sub-partition cannot hide the DMMA dependency latency.
+// GEMMs; 64 x 64 when the 128-tiles would not fill the machine (fewer than
+// 64 of them: q < 1024), so the stream-K pieces stay short and the fix-up
+// traffic small — with 16 warps of 16 x 16 at <= 40 128-tiles (q <= 768,
+// the cfg1 reduced solve), where one warp per SM sub-partition cannot hide
+// the DMMA dependency latency, else 4 warps of 32 x 32 (two CTAs per SM).
 template <int BM_, int BN_, int BK_, int STAGES_, int WM_ = 32, int WN_ = 32>
 struct Tile {
     static constexpr int BM = BM_, BN = BN_, BK = BK_, STAGES = STAGES_;
@@ -491,14 +491,14 @@ int launch_dgemm_nt(const double* A, int lda, const double* Bt, int ldb, int M, 
                     const GemmEpi& ep, cudaStream_t stream) {
     if (M <= 0 || N <= 0 || K <= 0) return arg_error("empty GEMM");
     const int mode = tile_mode();
-    // measured: 64-tiles win below ~64 128-tiles (q = 256: 22 vs 38 us; q = 512:
-    // 27 vs 38 us), tie at 64 (q = 1024), lose from ~100 (q = 1536: 240 vs 228 us);
-    // at <= 16 128-tiles (q <= 512) the DMMA pipe is latency bound with one warp
-    // per SM sub-partition and 16 warps of 16 x 16 win (q = 256: 18.4 vs 21.6 us,
-    // q = 512: 23.6 vs 27.1 us; q = 1024: 85.2 vs 84.2 us)
+    // measured (128 x 128 tiles with 32-deep stages): 64-tiles win below 64
+    // 128-tiles (q = 256: 22 vs 38 us; q = 512: 27 vs 55 us; q = 768: 47 vs 55 us)
+    // and lose from 64 (q = 1024: 84.3 vs 81.6 us); below ~40 of them the DMMA pipe
+    // is latency bound with one warp per SM sub-partition and 16 warps of 16 x 16
+    // win (q = 256: 18.4 vs 21.6 us, q = 768: 45.7 vs 47.0 us)
     const int t128 = tiles_of(M, N, 128, 128);
-    if (mode == 16 || (mode == 0 && t128 <= 16)) return launch_tile<TinyTile>(A, lda, Bt, ldb, M, N, K, ep, stream);
-    const bool small = mode == 64 || (mode != 128 && t128 <= 64);
+    if (mode == 16 || (mode == 0 && t128 <= 40)) return launch_tile<TinyTile>(A, lda, Bt, ldb, M, N, K, ep, stream);
+    const bool small = mode == 64 || (mode != 128 && t128 < 64);
     return small ? launch_tile<SmallTile>(A, lda, Bt, ldb, M, N, K, ep, stream)
                  : launch_tile<BigTile>(A, lda, Bt, ldb, M, N, K, ep, stream);
 }
