@@ -231,3 +231,33 @@ def test_spectral_form_rejects_non_symmetric_factors():
         Preconditioner._eigh(F, 6)
     lam, V = Preconditioner._eigh(F + F.T, 6)
     assert np.allclose(V @ np.diag(lam) @ V.T, F + F.T)
+
+
+# reference pkg/tests/test_solvers.py TestClosedForm, host-side pieces
+@pytest.mark.parametrize("n", [2, 4, 8, 16])
+@pytest.mark.parametrize("gamma", [0.0, 1.0])
+def test_dirichlet_eigenvalues_match_assembled_pencil(n, gamma):
+    """TestClosedForm.test_smallest_eigenvalue / test_eigenvalues_match_assembled_pencil."""
+    basis = pb.build_basis(1, n, pb.BCKind.DIRICHLET)
+    A, M = pb.assemble_standard(basis)
+    A, M = np.asarray(A), np.asarray(M)
+    lam = np.sort(np.linalg.eigvals(np.linalg.solve(M, A) + 0.5 * gamma * np.eye(n - 1)).real)
+    ref = np.sort(pb.dirichlet_p1_eigenvalues(n, gamma))
+    assert np.max(np.abs(lam - ref)) < 1e-10 * max(1.0, np.max(ref))
+    if n == 2 and gamma == 0.0:
+        assert np.allclose(ref, [12.0])
+
+
+def test_sine_basis_eigenvectors_and_involution():
+    """TestClosedForm.test_sine_basis_matches_numerical_eigenvectors / test_sine_basis_involution."""
+    A, _ = pb.assemble_standard(pb.build_basis(1, 4, pb.BCKind.DIRICHLET))
+    A = np.asarray(A)
+    _, vecs = np.linalg.eigh(A)
+    X = pb.dirichlet_sine_basis(4)
+    for j in range(3):
+        a = vecs[:, j] / np.linalg.norm(vecs[:, j])
+        b = X[:, j] / np.linalg.norm(X[:, j])
+        assert min(np.linalg.norm(a - b), np.linalg.norm(a + b)) < 1e-12
+    for n in (4, 8, 16):
+        X = pb.dirichlet_sine_basis(n)
+        assert np.allclose(X @ X, n / 2 * np.eye(n - 1), atol=1e-12)
