@@ -163,6 +163,15 @@ int sfb_map_destroy(sfb_map* m);
 int sfb_pre_create(int qy, int qx, int kind, const double* L,
                    const double* R, const double* lamL_host,
                    const double* lamR_host, sfb_pre** out);
+/* The inverse-form products Z = P_L^-1 (R P_R^-1) of shapes with q_y, q_x >=
+ * min_q and divisible by 4 run as one level of Strassen around the DMMA GEMM
+ * (7 half-size products, the constant operands' block sums formed at
+ * creation); it replaces the same two dense solves of Preconditioner.apply_inverse
+ * (solvers.py:134-143).  Applies to preconditioners created afterwards; 0 =
+ * never (default: SYLFEM_B200_STRASSEN_MINQ or 6144).  Returns the previous
+ * threshold.  sfb_pre_uses_strassen reports what a preconditioner does. */
+int sfb_set_strassen_min_q(int min_q);
+int sfb_pre_uses_strassen(const sfb_pre* p);
 /* Banded SPD factors: lower Cholesky factors in band storage
  * lband[i][d] = C_L[i][i - bw + d] (d = 0..bw), same for the right factor. */
 int sfb_pre_create_banded(int qy, int qx, int bwL, const double* lband_host,

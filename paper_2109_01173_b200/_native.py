@@ -31,6 +31,7 @@ EXPORTS = [
     "sfb_op_create", "sfb_op_create_block", "sfb_op_create_dense", "sfb_op_apply", "sfb_op_residual", "sfb_op_destroy",
     "sfb_map_create", "sfb_map_apply", "sfb_map_apply_heat", "sfb_map_apply_dib", "sfb_map_destroy",
     "sfb_pre_create", "sfb_pre_create_banded", "sfb_pre_apply", "sfb_pre_transform", "sfb_pre_destroy",
+    "sfb_set_strassen_min_q", "sfb_pre_uses_strassen",
     "sfb_pcg_create", "sfb_pcg_solve", "sfb_pcg_pass_times", "sfb_pcg_destroy", "sfb_dgemm_nt", "sfb_diff_norm",
     "sfb_vec_update", "sfb_vec_xpby", "sfb_vec_dots",
     "sfb_csr_create", "sfb_csr_spmv", "sfb_csr_destroy",
@@ -85,6 +86,8 @@ _SIGS = {
     "sfb_pre_apply": (_I, [_P, _P, _I, _P, _I, _P]),
     "sfb_pre_transform": (_I, [_P, _P, _I, _P, _I, _P]),
     "sfb_pre_destroy": (_I, [_P]),
+    "sfb_set_strassen_min_q": (_I, [_I]),
+    "sfb_pre_uses_strassen": (_I, [_P]),
     "sfb_pcg_create": (_I, [_P, _P, C.POINTER(_P)]),
     "sfb_pcg_solve": (_I, [_P, _P, _I, _P, _I, _P, _I, _I, _D, _I, _DP, _DP, _P, _I,
                            C.POINTER(PcgResult), _P]),

@@ -124,6 +124,14 @@ int launch_loop_ctl(PcgState* st, unsigned long long handle, int use_handle, cud
 int launch_norms(const double* A, int lda, const double* B, int ldb, int rows, int cols, double* partials,
                  RedSlots* out, cudaStream_t s);
 int vector_grid_blocks();
+// one-level Strassen helpers (vector.cu): the five block sums of an operand
+// (side 0: A pattern, side 1: Bt pattern; X is 2rh x 2ch, outputs rh x ch at S + i * sstride)
+// and the assembly of C (2rh x 2ch) from the seven products at Mp + i * mstride, with <C,D> when D is set
+int launch_strassen_sums(const double* X, int ldx, int rh, int ch, double* S, int lds, size_t sstride, int side,
+                         const PcgState* gate, cudaStream_t s);
+int launch_strassen_combine(const double* Mp, int ldm, size_t mstride, int rh, int ch, double* C, int ldc,
+                            const double* D, int ldd, double* partials, PcgState* st, double* dot_out,
+                            unsigned* counter, cudaStream_t s);
 int launch_transpose(const double* src, int lds, double* dst, int ldd, int rows, int cols, cudaStream_t s);
 int launch_sh_update(double* U, double* R, const double* Q, const double* W, int ld, int rows, int cols,
                      double alpha, double* partials, RedSlots* out, cudaStream_t s);

@@ -9,6 +9,7 @@
 // solve is then a single graph launch and one final synchronisation.
 #include <cuda.h>
 
+#include <atomic>
 #include <cstdlib>
 #include <functional>
 #include <cstring>
@@ -104,6 +105,7 @@ struct GemmWs {
     unsigned* flags = nullptr;
     double* seg_f = nullptr;  // segmented-solve boundary states (banded preconditioner)
     double* seg_b = nullptr;
+    double* strassen = nullptr;  // strassen_scratch_doubles(): operand sums and the seven products
 };
 
 // Temporary stream-K workspace from the stream-ordered pool.
@@ -158,6 +160,10 @@ struct sfb_pre {
     double *A1 = nullptr, *A1t = nullptr, *B1 = nullptr, *B1t = nullptr;
     int ldA = 0, ldB = 0;
     double *sl = nullptr, *sr = nullptr;
+    // INVERSE, large shapes divisible by 4: the five Strassen block sums of
+    // A1 and B1 (the constant left operands of the two products), formed once
+    double *A1s = nullptr, *B1s = nullptr;
+    bool strassen = false;
     // BANDED: factors prepared for the SPIKE solves (spike.cu)
     SpikeFactor fl, fr;
     size_t seg_doubles = 0;  // scratch per interface buffer
@@ -220,6 +226,71 @@ int op_apply_impl(const sfb_op* op, const double* U, int ldu, double* W, int ldw
     return SFB_OK;
 }
 
+// ---- one level of Strassen around the DMMA GEMM -------------------------
+// The inverse-form preconditioner (solvers.py:103-143 as two dense products)
+// multiplies by the same two matrices every iteration, so the five block sums
+// of the constant operand are formed once (sfb_pre_create); per product: one
+// pass for the variable operand's sums, seven half-size DMMA GEMMs and one
+// assembly pass (7/8 of the flops; the two passes move ~24 half-size blocks).
+// Used for shapes of at least strassen_min_q() that are divisible by 4
+// (SYLFEM_B200_STRASSEN_MINQ, 0 = never).
+std::atomic<int>& strassen_min_q_slot() {
+    static std::atomic<int> v([] {
+        const char* e = std::getenv("SYLFEM_B200_STRASSEN_MINQ");
+        return e ? std::atoi(e) : 6144;
+    }());
+    return v;
+}
+int strassen_min_q() { return strassen_min_q_slot().load(std::memory_order_relaxed); }
+
+bool strassen_shape(int qy, int qx) {
+    const int m = strassen_min_q();
+    return m > 0 && qy >= m && qx >= m && qy % 4 == 0 && qx % 4 == 0;
+}
+
+size_t strassen_sums_doubles(int q) { return (size_t)5 * (q / 2) * pad_ld(q / 2); }
+
+size_t strassen_scratch_doubles(int qy, int qx) {
+    const int h = std::max(qy, qx) / 2;
+    return (size_t)12 * h * pad_ld(h);
+}
+
+// C[M x N] = A[M x K] Bt[N x K]^T; As = the five A-side sums ((M/2) x pad_ld(K/2) each).
+int strassen_nt(const double* A, int lda, const double* As, const double* Bt, int ldb, int M, int N, int K,
+                double* scratch, double* C, int ldc, const double* D, int ldd, double* partials, PcgState* pcg,
+                double* dot_out, unsigned* counter, const GemmWs* gw, cudaStream_t s) {
+    const int Mh = M / 2, Nh = N / 2, Kh = K / 2;
+    const int ldk = pad_ld(Kh), ldn = pad_ld(Nh);
+    const size_t sa = (size_t)Mh * ldk, sb = (size_t)Nh * ldk, sm = (size_t)Mh * ldn;
+    double* Bs = scratch;
+    double* Mp = scratch + 5 * sb;
+    SFB_TRY(launch_strassen_sums(Bt, ldb, Nh, Kh, Bs, ldk, sb, 1, pcg, s));
+    const double *A11 = A, *A22 = A + (size_t)Mh * lda + Kh;
+    const double *B11 = Bt, *B22 = Bt + (size_t)Nh * ldb + Kh;
+    struct Prod {
+        const double* a;
+        int lda;
+        const double* b;
+        int ldb;
+    };
+    const Prod prods[7] = {{As, ldk, Bs, ldk},                    // (A11 + A22)(B11 + B22)
+                           {As + sa, ldk, B11, ldb},              // (A21 + A22) B11
+                           {A11, lda, Bs + sb, ldk},              // A11 (B12 - B22)
+                           {A22, lda, Bs + 2 * sb, ldk},          // A22 (B21 - B11)
+                           {As + 2 * sa, ldk, B22, ldb},          // (A11 + A12) B22
+                           {As + 3 * sa, ldk, Bs + 3 * sb, ldk},  // (A21 - A11)(B11 + B12)
+                           {As + 4 * sa, ldk, Bs + 4 * sb, ldk}}; // (A12 - A22)(B21 + B22)
+    for (int i = 0; i < 7; ++i) {
+        GemmEpi e;
+        e.mode = EPI_STORE;
+        e.C = Mp + i * sm;
+        e.ldc = ldn;
+        e.pcg = pcg;
+        SFB_TRY(launch_dgemm_nt(prods[i].a, prods[i].lda, prods[i].b, prods[i].ldb, Mh, Nh, Kh, with_ws(e, gw), s));
+    }
+    return launch_strassen_combine(Mp, ldn, sm, Mh, Nh, C, ldc, D, ldd, partials, pcg, dot_out, counter, s);
+}
+
 // Z = P^-1 R (or the reduced-solve sandwich).  R/Z device buffers with even
 // ld; T1 (qx x qy, ldt1) and T2 (qy x qx, ldt2) scratch.  When `pcg` is set,
 // kernels are gated on its status and <Z,R> lands in pcg->rz_next; otherwise
@@ -244,6 +315,14 @@ int pre_apply_impl(const sfb_pre* p, const double* R, int ldr, double* Z, int ld
             if (ldr != ldz) return arg_error("identity preconditioner needs matching leading dimensions");
             return launch_copy_dot(R, Z, ldz, qy, qx, partials, pcg, red, s);
         case SFB_PRE_INVERSE: {
+            if (p->strassen && gw != nullptr && gw->strassen != nullptr) {
+                // T1 = P_R^-T R^T, then Z = P_L^-1 T1^T with <Z,R> in the assembly pass
+                SFB_TRY(strassen_nt(p->B1, p->ldB, p->B1s, R, ldr, qx, qy, qx, gw->strassen, T1, ldt1, nullptr, 0,
+                                    nullptr, pcg, nullptr, nullptr, gw, s));
+                const bool dot = pcg || red;
+                return strassen_nt(p->A1, p->ldA, p->A1s, T1, ldt1, qy, qx, qy, gw->strassen, Z, ldz,
+                                   dot ? R : nullptr, ldr, partials, pcg, red ? &red->v[3] : nullptr, counter, gw, s);
+            }
             GemmEpi e1;  // T1 = (R P_R^-1)^T
             e1.mode = EPI_STORE_T;
             e1.C = T1;
@@ -487,6 +566,14 @@ extern "C" {
 int sfb_version(void) { return 1; }
 
 const char* sfb_last_error(void) { return g_last_error.c_str(); }
+
+int sfb_set_strassen_min_q(int min_q) {
+    const int prev = strassen_min_q();
+    strassen_min_q_slot().store(min_q < 0 ? 0 : min_q, std::memory_order_relaxed);
+    return prev;
+}
+
+int sfb_pre_uses_strassen(const sfb_pre* p) { return p != nullptr && p->strassen ? 1 : 0; }
 
 int sfb_init(int device, int* sm_count) {
     SFB_CUDA_TRY(cudaSetDevice(device));
@@ -783,6 +870,20 @@ int sfb_pre_create(int qy, int qx, int kind, const double* L, const double* R, c
         if (rc == SFB_OK) rc = dalloc(&p->B1, (size_t)qx * p->ldB);
         if (rc == SFB_OK) rc = upload_padded(p->A1, p->ldA, L, qy, qy);
         if (rc == SFB_OK) rc = upload_padded(p->B1, p->ldB, R, qx, qx);
+        if (rc == SFB_OK && strassen_shape(qy, qx)) {
+            rc = dalloc(&p->A1s, strassen_sums_doubles(qy));
+            if (rc == SFB_OK) rc = dalloc(&p->B1s, strassen_sums_doubles(qx));
+            if (rc == SFB_OK) rc = cudaMemset(p->A1s, 0, strassen_sums_doubles(qy) * 8) == cudaSuccess ? SFB_OK : SFB_ERR_CUDA;
+            if (rc == SFB_OK) rc = cudaMemset(p->B1s, 0, strassen_sums_doubles(qx) * 8) == cudaSuccess ? SFB_OK : SFB_ERR_CUDA;
+            if (rc == SFB_OK)
+                rc = launch_strassen_sums(p->A1, p->ldA, qy / 2, qy / 2, p->A1s, pad_ld(qy / 2),
+                                          (size_t)(qy / 2) * pad_ld(qy / 2), 0, nullptr, nullptr);
+            if (rc == SFB_OK)
+                rc = launch_strassen_sums(p->B1, p->ldB, qx / 2, qx / 2, p->B1s, pad_ld(qx / 2),
+                                          (size_t)(qx / 2) * pad_ld(qx / 2), 0, nullptr, nullptr);
+            if (rc == SFB_OK && cudaDeviceSynchronize() != cudaSuccess) rc = SFB_ERR_CUDA;
+            p->strassen = rc == SFB_OK;
+        }
         if (rc != SFB_OK) return fail(rc);
         *out = p;
         return SFB_OK;
@@ -865,6 +966,10 @@ int sfb_pre_apply(const sfb_pre* p, const double* R, int ldr, double* Z, int ldz
     if (p->kind == SFB_PRE_BANDED) {
         SFB_TRY(tmp.get(&gw.seg_f, p->seg_doubles * 8));
         SFB_TRY(tmp.get(&gw.seg_b, p->seg_doubles * 8));
+    }
+    if (p->strassen) {
+        SFB_TRY(tmp.get(&gw.strassen, strassen_scratch_doubles(p->qy, p->qx) * 8));
+        SFB_CUDA_TRY(cudaMemsetAsync(gw.strassen, 0, strassen_scratch_doubles(p->qy, p->qx) * 8, s));
     }
     SFB_TRY(pre_apply_impl(p, Rb, ld, Zb, ld, T1, ldt1, T2, ld, parts, nullptr, red, &gw, s));
     SFB_CUDA_TRY(cudaMemcpy2DAsync(Z, (size_t)ldz * 8, Zb, (size_t)ld * 8, (size_t)p->qx * 8, p->qy,
@@ -1050,6 +1155,8 @@ int sfb_pre_destroy(sfb_pre* p) {
     cudaFree(p->B1t);
     cudaFree(p->sl);
     cudaFree(p->sr);
+    cudaFree(p->A1s);
+    cudaFree(p->B1s);
     free_spike_factor(p->fl);
     free_spike_factor(p->fr);
     delete p;
@@ -1087,6 +1194,10 @@ int sfb_pcg_create(const sfb_op* op, const sfb_pre* pre, sfb_pcg** out) {
     if (rc == SFB_OK && pre->kind == SFB_PRE_BANDED) {
         rc = dalloc(&s->gw.seg_f, pre->seg_doubles);
         if (rc == SFB_OK) rc = dalloc(&s->gw.seg_b, pre->seg_doubles);
+    }
+    if (rc == SFB_OK && pre->strassen) {
+        rc = dalloc(&s->gw.strassen, strassen_scratch_doubles(s->qy, s->qx));
+        if (rc == SFB_OK) cudaMemset(s->gw.strassen, 0, strassen_scratch_doubles(s->qy, s->qx) * 8);
     }
     if (rc == SFB_OK) {
         for (double** b : bufs) cudaMemset(*b, 0, n * 8);
@@ -1298,6 +1409,7 @@ int sfb_pcg_destroy(sfb_pcg* s) {
     cudaFree(s->gw.flags);
     cudaFree(s->gw.seg_f);
     cudaFree(s->gw.seg_b);
+    cudaFree(s->gw.strassen);
     if (s->stream) cudaStreamDestroy(s->stream);
     cudaEvent_t evs[] = {s->ev_in, s->ev_out, s->ev_t0, s->ev_t1};
     for (auto e : evs)

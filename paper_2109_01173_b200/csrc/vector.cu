@@ -627,7 +627,129 @@ __global__ void transpose_kernel(const double* __restrict__ src, int lds, double
     }
 }
 
+// ---- one-level Strassen around the DMMA GEMM (large even preconditioner products) ----
+// C = A Bt^T with 2 x 2 blocks, B = Bt^T (B11 = Bt11^T, B12 = Bt21^T, B21 = Bt12^T, B22 = Bt22^T):
+//   M1 = (A11 + A22)(B11 + B22)   M2 = (A21 + A22) B11     M3 = A11 (B12 - B22)
+//   M4 = A22 (B21 - B11)          M5 = (A11 + A12) B22     M6 = (A21 - A11)(B11 + B12)
+//   M7 = (A12 - A22)(B21 + B22)
+//   C11 = M1 + M4 - M5 + M7   C12 = M3 + M5   C21 = M2 + M4   C22 = M1 - M2 + M3 + M6
+// strassen_sums_kernel forms the five block sums of one operand (side 0: the
+// A pattern, side 1: the Bt pattern) in one pass over its four blocks;
+// strassen_combine_kernel assembles C from the seven products in one pass,
+// with the optional <C,D> of the MO-PCG preconditioner step (solvers.py:448)
+// as a deterministic last-block reduction.
+__global__ void __launch_bounds__(VT) strassen_sums_kernel(const double* __restrict__ X, int ldx, int rh, int ch,
+                                                           double* __restrict__ S, int lds, size_t sstride, int side,
+                                                           const PcgState* gate) {
+    SFB_PDL_PROLOGUE();
+    if (gate != nullptr && gate->status != SFB_PCG_RUNNING) return;
+    const int np = ch / 2;  // ch is even, rows 16-byte aligned
+    for (int r = blockIdx.x; r < rh; r += gridDim.x) {
+        const double2* x11 = reinterpret_cast<const double2*>(X + (size_t)r * ldx);
+        const double2* x12 = reinterpret_cast<const double2*>(X + (size_t)r * ldx + ch);
+        const double2* x21 = reinterpret_cast<const double2*>(X + (size_t)(r + rh) * ldx);
+        const double2* x22 = reinterpret_cast<const double2*>(X + (size_t)(r + rh) * ldx + ch);
+        double2* s0 = reinterpret_cast<double2*>(S + (size_t)r * lds);
+        double2* s1 = reinterpret_cast<double2*>(S + sstride + (size_t)r * lds);
+        double2* s2 = reinterpret_cast<double2*>(S + 2 * sstride + (size_t)r * lds);
+        double2* s3 = reinterpret_cast<double2*>(S + 3 * sstride + (size_t)r * lds);
+        double2* s4 = reinterpret_cast<double2*>(S + 4 * sstride + (size_t)r * lds);
+        #pragma unroll 2
+        for (int q = threadIdx.x; q < np; q += VT) {
+            const double2 a = x11[q], b = x12[q], c = x21[q], d = x22[q];
+            if (side == 0) {  // A11 + A22, A21 + A22, A11 + A12, A21 - A11, A12 - A22
+                s0[q] = make_double2(a.x + d.x, a.y + d.y);
+                s1[q] = make_double2(c.x + d.x, c.y + d.y);
+                s2[q] = make_double2(a.x + b.x, a.y + b.y);
+                s3[q] = make_double2(c.x - a.x, c.y - a.y);
+                s4[q] = make_double2(b.x - d.x, b.y - d.y);
+            } else {          // Bt11 + Bt22, Bt21 - Bt22, Bt12 - Bt11, Bt11 + Bt21, Bt12 + Bt22
+                s0[q] = make_double2(a.x + d.x, a.y + d.y);
+                s1[q] = make_double2(c.x - d.x, c.y - d.y);
+                s2[q] = make_double2(b.x - a.x, b.y - a.y);
+                s3[q] = make_double2(a.x + c.x, a.y + c.y);
+                s4[q] = make_double2(b.x + d.x, b.y + d.y);
+            }
+        }
+    }
+}
+
+__global__ void __launch_bounds__(VT) strassen_combine_kernel(const double* __restrict__ Mp, int ldm, size_t mstride,
+                                                              int rh, int ch, double* __restrict__ C, int ldc,
+                                                              const double* __restrict__ D, int ldd, double* partials,
+                                                              PcgState* st, double* dot_out, unsigned* counter) {
+    SFB_PDL_PROLOGUE();
+    if (st != nullptr && st->status != SFB_PCG_RUNNING) return;
+    const int np = ch / 2;
+    double dot = 0.0;
+    for (int r = blockIdx.x; r < rh; r += gridDim.x) {
+        const double2* m[7];
+        #pragma unroll
+        for (int i = 0; i < 7; ++i) m[i] = reinterpret_cast<const double2*>(Mp + i * mstride + (size_t)r * ldm);
+        double2* c11 = reinterpret_cast<double2*>(C + (size_t)r * ldc);
+        double2* c12 = reinterpret_cast<double2*>(C + (size_t)r * ldc + ch);
+        double2* c21 = reinterpret_cast<double2*>(C + (size_t)(r + rh) * ldc);
+        double2* c22 = reinterpret_cast<double2*>(C + (size_t)(r + rh) * ldc + ch);
+        const double2* d11 = reinterpret_cast<const double2*>(D + (size_t)r * ldd);
+        const double2* d12 = reinterpret_cast<const double2*>(D + (size_t)r * ldd + ch);
+        const double2* d21 = reinterpret_cast<const double2*>(D + (size_t)(r + rh) * ldd);
+        const double2* d22 = reinterpret_cast<const double2*>(D + (size_t)(r + rh) * ldd + ch);
+        for (int q = threadIdx.x; q < np; q += VT) {
+            const double2 m1 = m[0][q], m2 = m[1][q], m3 = m[2][q], m4 = m[3][q], m5 = m[4][q], m6 = m[5][q],
+                          m7 = m[6][q];
+            const double2 v11 = make_double2(((m1.x + m4.x) - m5.x) + m7.x, ((m1.y + m4.y) - m5.y) + m7.y);
+            const double2 v12 = make_double2(m3.x + m5.x, m3.y + m5.y);
+            const double2 v21 = make_double2(m2.x + m4.x, m2.y + m4.y);
+            const double2 v22 = make_double2(((m1.x - m2.x) + m3.x) + m6.x, ((m1.y - m2.y) + m3.y) + m6.y);
+            c11[q] = v11;
+            c12[q] = v12;
+            c21[q] = v21;
+            c22[q] = v22;
+            if (D != nullptr) {
+                const double2 e11 = d11[q], e12 = d12[q], e21 = d21[q], e22 = d22[q];
+                dot = fma(v11.x, e11.x, dot);
+                dot = fma(v11.y, e11.y, dot);
+                dot = fma(v12.x, e12.x, dot);
+                dot = fma(v12.y, e12.y, dot);
+                dot = fma(v21.x, e21.x, dot);
+                dot = fma(v21.y, e21.y, dot);
+                dot = fma(v22.x, e22.x, dot);
+                dot = fma(v22.y, e22.y, dot);
+            }
+        }
+    }
+    if (D == nullptr) return;  // uniform
+    __shared__ double sh[VT / 32];
+    const double p = block_sum<VT>(dot, sh);
+    if (threadIdx.x == 0) partials[blockIdx.x] = p;
+    if (arrive_last(counter, gridDim.x)) {
+        const double tot = sum_partials<VT>(partials, gridDim.x, 1, sh);
+        if (threadIdx.x == 0) {
+            *counter = 0;
+            if (st != nullptr) st->rz_next = tot;
+            if (dot_out != nullptr) *dot_out = tot;
+        }
+    }
+}
+
 int vector_grid_blocks() { return VB; }
+
+int launch_strassen_sums(const double* X, int ldx, int rh, int ch, double* S, int lds, size_t sstride, int side,
+                         const PcgState* gate, cudaStream_t s) {
+    SFB_TRY(launch_kernel(strassen_sums_kernel, dim3(std::max(1, std::min(VB, rh))), dim3(VT), 0, s, X, ldx, rh, ch, S,
+                          lds, sstride, side, gate));
+    SFB_CHECK_LAUNCH();
+    return SFB_OK;
+}
+
+int launch_strassen_combine(const double* Mp, int ldm, size_t mstride, int rh, int ch, double* C, int ldc,
+                            const double* D, int ldd, double* partials, PcgState* st, double* dot_out,
+                            unsigned* counter, cudaStream_t s) {
+    SFB_TRY(launch_kernel(strassen_combine_kernel, dim3(std::max(1, std::min(VB, rh))), dim3(VT), 0, s, Mp, ldm,
+                          mstride, rh, ch, C, ldc, D, ldd, partials, st, dot_out, counter));
+    SFB_CHECK_LAUNCH();
+    return SFB_OK;
+}
 
 int launch_pcg_init_plain(const double* rhs, int ldr, double* R, double* U, int ld, int rows, int cols,
                           double* partials, PcgState* st, double* hist, cudaStream_t s) {

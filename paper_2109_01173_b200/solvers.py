@@ -200,6 +200,15 @@ class KroneckerCSR(sp.csr_matrix):
     sfb_shape = None
 
 
+def set_strassen_min_q(min_q: int) -> int:
+    """Grid size from which the inverse-form preconditioner products (the two
+    dense solves of solvers.py:134-143 as DMMA GEMMs) run as one level of
+    Strassen (7 half-size GEMMs each; shapes divisible by 4).  0 disables it.
+    Applies to device preconditioners built afterwards; returns the previous
+    threshold (default 6144, or SYLFEM_B200_STRASSEN_MINQ)."""
+    return int(nat.lib().sfb_set_strassen_min_q(int(min_q)))
+
+
 class Preconditioner:
     """Single-term preconditioner U -> P_L U P_R (solvers.py:103-150).
 
@@ -279,6 +288,11 @@ class Preconditioner:
         self._handle = nat.Handle(out.value, L.sfb_pre_destroy)
         self._handle_shape = shape
         return self._handle.p
+
+    def uses_strassen(self, shape=None) -> bool:
+        """Whether the device form multiplies by the dense inverses with the
+        Strassen schedule (see set_strassen_min_q)."""
+        return bool(nat.lib().sfb_pre_uses_strassen(self.native(shape)))
 
     @staticmethod
     def _eigh(m, q):

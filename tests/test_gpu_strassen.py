@@ -1,0 +1,91 @@
+"""The inverse-form preconditioner's dense products as one level of Strassen
+around the DMMA GEMM (large shapes divisible by 4; BASELINE cfg5, q = 8192).
+
+The reference applies P_L^-1 U P_R^-1 by two dense solves
+(solvers.py:134-143).  Strassen changes the summation order of the two
+products, not their value: the checks are the product against the classic
+schedule (normwise, at the level of the GEMM's own rounding), MO-PCG iterates
+against the oracle at the north-star tolerance (1e-10), and the <Z,R> of the
+assembly pass through the iteration counts of a converged solve.  The
+threshold is lowered for these desk sizes and restored afterwards; the
+full-size cfg5 test (test_gpu_fullsize.py) runs the default threshold.
+"""
+
+import numpy as np
+import pytest
+
+import oracle as orc
+import paper_2109_01173_b200 as pb
+from conftest import relerr
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture
+def strassen_from_256():
+    prev = pb.set_strassen_min_q(256)
+    yield
+    pb.set_strassen_min_q(prev)
+
+
+def _lumped_sets(Nx, Ny):
+    return pb.build_direction_sets(pb.SQUARE, 1, (Nx, Ny), pb.BCKind.NEUMANN, lumped=True)
+
+
+@pytest.mark.parametrize("Nx,Ny", [(511, 511), (639, 511), (255, 383)])
+def test_strassen_product_matches_classic_schedule(Nx, Ny, strassen_from_256):
+    x, y = _lumped_sets(Nx, Ny)
+    d, tau = 20.0, 1.25e-5
+    kw = {"d_u": d, "tau": tau, "lumped": True}
+    pre_s = pb.make_preconditioner("parabolic_lumped", x, y, mode="inverse", **kw)
+    assert pre_s.uses_strassen()
+    prev = pb.set_strassen_min_q(0)
+    try:
+        pre_c = pb.make_preconditioner("parabolic_lumped", x, y, mode="inverse", **kw)
+        assert not pre_c.uses_strassen()
+    finally:
+        pb.set_strassen_min_q(prev)
+    rng = np.random.default_rng(11)
+    R = rng.standard_normal((y.q, x.q))
+    Zs, Zc = pre_s.apply_inverse(R), pre_c.apply_inverse(R)
+    assert relerr(Zs, Zc) <= 1e-13
+    # and against the oracle's LU solves
+    ox, oy = orc.direction_sets(orc.unit_square(), 1, (Nx, Ny), orc.NEUMANN, lumped=True)
+    opre = orc.LUPrecond(*orc.precond_factors("parabolic_lumped", ox, oy, d_u=d, tau=tau, lumped=True))
+    assert relerr(Zs, opre.inverse(R)) <= 1e-11
+
+
+def test_strassen_shapes_not_divisible_by_4_keep_the_classic_schedule(strassen_from_256):
+    x, y = _lumped_sets(513, 511)  # q_x = 514
+    pre = pb.make_preconditioner("parabolic_lumped", x, y, mode="inverse", d_u=1.0, tau=1e-4, lumped=True)
+    assert not pre.uses_strassen()
+
+
+@pytest.mark.parametrize("d,tau", [(1.0, 5e-4), (20.0, 1.25e-5)])
+def test_strassen_mo_pcg_iterates_vs_oracle(d, tau, strassen_from_256):
+    """cfg5-type step system (lumped P1, Neumann, square) at q = 512: K-th
+    iterates and residual histories against the oracle, then a converged solve."""
+    N = 511
+    x, y = _lumped_sets(N, N)
+    op, rhs_of = pb.parabolic_operator(x, y, d, tau, lumped=True)
+    ox, oy = orc.direction_sets(orc.unit_square(), 1, N, orc.NEUMANN, lumped=True)
+    terms, orhs = orc.parabolic_terms(ox, oy, d, tau, True)
+    opre = orc.LUPrecond(*orc.precond_factors("parabolic_lumped", ox, oy, d_u=d, tau=tau, lumped=True))
+    rng = np.random.default_rng(5)
+    S = 1e-3 * rng.uniform(-1.0, 1.0, (N + 1, N + 1))
+    rhs = orhs(S)
+    assert relerr(rhs_of(S), rhs) <= 1e-13
+    pre = pb.make_preconditioner("parabolic_lumped", x, y, mode="inverse", d_u=d, tau=tau, lumped=True)
+    assert pre.uses_strassen()
+    K = 6
+    ref = orc.mo_pcg(terms, rhs, opre.inverse, ("residual", 1e-300), u0=S, max_iter=K)
+    rep = pb.mo_pcg(op, rhs, precond=pre, stop=pb.fixed_budget(), u0=S, max_iter=K)
+    assert rep.iterations == K
+    assert relerr(rep.solution, ref["solution"]) <= 1e-10
+    h = np.asarray(ref["history"])
+    assert np.max(np.abs(rep.residual_history - h) / h) <= 1e-10
+    full = orc.mo_pcg(terms, rhs, opre.inverse, ("residual", 1e-10), max_iter=500)
+    rep = pb.mo_pcg(op, rhs, precond=pre, stop=pb.relative_residual(1e-10), max_iter=500)
+    assert rep.stop_reason == "tolerance"
+    assert abs(rep.iterations - full["iterations"]) <= 1
+    assert relerr(rep.solution, full["solution"]) <= 1e-9

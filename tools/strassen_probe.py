@@ -1,0 +1,56 @@
+"""Inverse-form preconditioner apply Z = A R B^T at q x q (two dense products):
+classic DMMA GEMMs vs one level of Strassen around them -- time and error
+against torch's fp64 matmul.  python tools/strassen_probe.py [q ...]"""
+import ctypes as C
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+from paper_2109_01173_b200 import _native as nat  # noqa: E402
+
+L = nat.lib()
+s = torch.cuda.current_stream().cuda_stream
+PRE_INVERSE = nat.PRE_INVERSE
+
+
+def make(q, A, Bt, minq):
+    prev = L.sfb_set_strassen_min_q(minq)
+    out = C.c_void_p()
+    nat.check(L.sfb_pre_create(q, q, PRE_INVERSE, A.data_ptr(), Bt.data_ptr(), None, None, C.byref(out)), "pre")
+    L.sfb_set_strassen_min_q(prev)
+    return out
+
+
+for q in [int(a) for a in sys.argv[1:]] or [4096, 8192]:
+    g = torch.Generator(device="cuda").manual_seed(q)
+    A = torch.randn(q, q, dtype=torch.float64, device="cuda", generator=g)
+    Bt = torch.randn(q, q, dtype=torch.float64, device="cuda", generator=g)
+    R = torch.randn(q, q, dtype=torch.float64, device="cuda", generator=g)
+    Z = torch.empty_like(R)
+    ref = A @ (R @ Bt.T)
+    for name, minq in (("classic", 0), ("strassen", 256)):
+        h = make(q, A, Bt, minq)
+        assert bool(L.sfb_pre_uses_strassen(h)) == (minq > 0)
+
+        def run():
+            nat.check(L.sfb_pre_apply(h, R.data_ptr(), q, Z.data_ptr(), q, s), "apply")
+
+        for _ in range(2):
+            run()
+        torch.cuda.synchronize()
+        err = float((Z - ref).norm() / ref.norm())
+        emax = float((Z - ref).abs().max() / ref.abs().max())
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 5
+        e0.record()
+        for _ in range(reps):
+            run()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        print(f"q={q} {name:9s} {ms:8.3f} ms per apply (2 products + 2 copies)  "
+              f"{4 * q ** 3 / ms / 1e9:6.2f} TF/s algorithmic  rel err {err:.2e}  max err / max {emax:.2e}", flush=True)
+        nat.check(L.sfb_pre_destroy(h), "destroy")
