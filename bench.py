@@ -67,6 +67,10 @@ def parse():
     ap.add_argument("--iters-per-step", type=int, default=None,
                     help="MO-PCG budget per solve (cfg5: per species and step, default 20; cfg3: default 200)")
     ap.add_argument("--precond-mode", default="inverse", choices=["inverse", "spectral", "banded"])
+    ap.add_argument("--strassen-levels", type=int, default=None,
+                    help="Strassen levels of the inverse-form preconditioner products (default: the library's, "
+                         "3 at q = 8192; 0 = classic GEMMs)")
+    ap.add_argument("--no-classic", action="store_true", help="skip the classic-GEMM-schedule comparison block")
     ap.add_argument("--cpu-iters", type=int, default=2, help="oracle iterations per system in cpu_baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -290,7 +294,7 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------ GPU pieces ----
-def gemm_roofline(q: int):
+def gemm_roofline(q: int, levels: int = 0):
     """Dominant kernel: the q x q x q DMMA GEMM (C = A Bt^T), live CUDA
     events on the launching stream, against cuBLAS DGEMM 8192^3 measured in
     the same process."""
@@ -336,9 +340,39 @@ def gemm_roofline(q: int):
     del a8, b8
     torch.cuda.empty_cache()
     tf = 2.0 * q ** 3 / t_gemm / 1e12
-    return {"bound": "tensor", "kernel": "dgemm_nt (DMMA.8x8x4 + TMA, stream-K)", "achieved": tf, "peak": peak,
+    roof = {"bound": "tensor", "kernel": "dgemm_nt (DMMA.8x8x4 + TMA, stream-K)", "achieved": tf, "peak": peak,
             "unit": "TFLOP/s", "frac": tf / peak, "flops_per_launch": 2.0 * q ** 3, "launch_ms": t_gemm * 1e3,
             "peak_source": "cuBLAS DGEMM 8192^3 measured in this run", "cublas_same_shape_tflops": cublas_same}
+    if levels > 0:
+        # the dominant kernel of the Strassen schedule: one batched launch of the
+        # seven leaf products (its own flops, not the algorithmic 2 q^3)
+        import ctypes as C
+        h = q >> levels
+        A = [torch.randn(h, h, dtype=torch.float64, device="cuda") for _ in range(7)]
+        B = [torch.randn(h, h, dtype=torch.float64, device="cuda") for _ in range(7)]
+        out = torch.empty(7, h, h, dtype=torch.float64, device="cuda")
+        pa = (C.c_void_p * 7)(*[a.data_ptr() for a in A])
+        pb_ = (C.c_void_p * 7)(*[b.data_ptr() for b in B])
+        ld7 = (C.c_int * 7)(*([h] * 7))
+
+        def leaf():
+            nat.check(L.sfb_dgemm_nt_batch7(pa, ld7, pb_, ld7, h, h, h, out.data_ptr(), h, h * h, s.cuda_stream))
+
+        t_leaf = timed(leaf, 20)
+        tfl = 14.0 * h ** 3 / t_leaf / 1e12
+        roof = {"bound": "tensor",
+                "kernel": f"dgemm_nt batched (7 x {h}^3 per launch: the leaf products of {levels} Strassen levels; "
+                          f"DMMA.8x8x4 + TMA, hybrid data-parallel + stream-K)",
+                "achieved": tfl, "peak": peak, "unit": "TFLOP/s", "frac": tfl / peak,
+                "flops_per_launch": 14.0 * h ** 3, "launch_ms": t_leaf * 1e3,
+                "launches_per_product": 7 ** (levels - 1),
+                "peak_source": "cuBLAS DGEMM 8192^3 measured in this run",
+                "classic_gemm": {"kernel": "dgemm_nt, one q^3 product per launch", "achieved": tf, "frac": tf / peak,
+                                 "launch_ms": t_gemm * 1e3, "flops_per_launch": 2.0 * q ** 3,
+                                 "cublas_same_shape_tflops": cublas_same}}
+        del A, B, out
+        torch.cuda.empty_cache()
+    return roof
 
 
 def hbm_passes(op, pre, reps=20):
@@ -408,6 +442,8 @@ def run_cfg5(args):
         return float(t.item())
 
     K = args.iters_per_step
+    if args.strassen_levels is not None:
+        pb.set_strassen_levels(args.strassen_levels)
     t_setup = time.perf_counter()
     w, ex, run = cfg5_setup(args, args.precond_mode)
     qy, qx = w.op.shape
@@ -520,8 +556,38 @@ def run_cfg5(args):
 
     # ---- per-pass timing of the headline iteration (q = 8192) ----
     op_u, _, pre_u = _step_system(w.x, w.y, 1.0, tau, True, run["inner"])
+    levels = pre_u.uses_strassen() if args.precond_mode == "inverse" else 0
     hbm = hbm_passes(op_u, pre_u)
     iter_ms = 1e3 * elapsed / args.steps / (2 * K)
+
+    # ---- the same steps with the classic schedule (one q^3 DMMA GEMM per product) ----
+    classic = None
+    if levels > 0 and not args.no_classic:
+        pb.clear_step_cache()
+        del op_u, pre_u
+        torch.cuda.empty_cache()
+        prev_levels = pb.set_strassen_levels(0)
+        stc = tuple(s.clone() for s in state)
+        stc = step(stc).final
+        barrier()
+        e0.record()
+        its_c = 0
+        n_c = min(args.steps, 3)
+        for _ in range(n_c):
+            tr = step(stc)
+            stc = tr.final
+            its_c += int(np.sum(tr.iterations))
+        e1.record()
+        barrier()
+        el_c = e0.elapsed_time(e1) / 1e3
+        classic = {"value": qy * qx * its_c / el_c, "unit": UNIT, "steps": n_c, "ms_per_step": 1e3 * el_c / n_c,
+                   "iteration_ms": 1e3 * el_c / its_c,
+                   "note": "the same IMEX steps with each preconditioner product as one q^3 DMMA GEMM "
+                           "(set_strassen_levels(0))"}
+        del stc
+        pb.clear_step_cache()
+        pb.set_strassen_levels(prev_levels)
+        torch.cuda.empty_cache()
 
     # ---- the same steps with the f1 banded preconditioner ----
     alt = None
@@ -549,11 +615,21 @@ def run_cfg5(args):
 
     del state
     torch.cuda.empty_cache()
-    roof = gemm_roofline(qy)
+    roof = gemm_roofline(qy, levels)
     n_gemm = 2 if args.precond_mode == "inverse" else (4 if args.precond_mode == "spectral" else 0)
-    roof.update({"share_of_iteration": n_gemm * roof["launch_ms"] / iter_ms if n_gemm else 0.0,
+    n_launch = n_gemm * (7 ** (levels - 1) if levels > 0 else 1)  # dominant-kernel launches per iteration
+    tkey = f"q{qy >> levels}x7" if levels > 0 else f"q{qy}"
+    roof.update({"share_of_iteration": n_launch * roof["launch_ms"] / iter_ms if n_gemm else 0.0,
                  "iteration_ms": iter_ms,
-                 "traffic": (profile_json("ncu_dgemm_r02.json").get(f"q{qy}") or {}).get("dram_bytes_per_launch")})
+                 "traffic": (profile_json("ncu_dgemm_r02.json").get(tkey) or {}).get("dram_bytes_per_launch")})
+    if levels > 0:
+        # the two dense products of one preconditioner application, as a whole
+        roof["preconditioner_application"] = {
+            "ms": hbm["preconditioner_ms"], "algorithmic_flops": 4.0 * qy ** 3,
+            "algorithmic_tflops": 4.0 * qy ** 3 / (hbm["preconditioner_ms"] * 1e-3) / 1e12,
+            "executed_flops": 4.0 * qy ** 3 * (7.0 / 8.0) ** levels,
+            "note": f"{levels} Strassen levels: per product {(7 ** levels - 1) // 6} operand-sum passes, "
+                    f"{7 ** (levels - 1)} batched leaf launches, {(7 ** levels - 1) // 6} assembly passes"}
     if args.precond_mode == "banded":
         bp = hbm["banded_operator_pass"]
         roof = {"bound": "hbm", "kernel": bp["kernel"], "achieved": bp["achieved"], "peak": hbm["peak"],
@@ -577,6 +653,8 @@ def run_cfg5(args):
     # first preconditioner (n_pre), K x (banded pass + R update + preconditioner),
     # deferred U update (1), increment norms (1)
     n_pre = n_gemm if n_gemm else 5
+    if levels > 0:  # per product: sums + batched leaves + assemblies
+        n_pre = 2 * (2 * ((7 ** levels - 1) // 6) + 7 ** (levels - 1))
     per_species = 4 + n_pre + K * (2 + n_pre) + 1
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -585,8 +663,11 @@ def run_cfg5(args):
         "config": {"workload": cfg5_name(args, qy, qx), "iterations_per_step": 2 * K,
                    "inner": f"InnerSolver(rule='budget', max_iter={K}, precond_mode='{args.precond_mode}') per species",
                    "preconditioner_mode": args.precond_mode,
+                   "gemm_schedule": (f"{levels} Strassen levels over batched DMMA GEMMs ({qy >> levels}^3 leaves)"
+                                     if levels > 0 else "classic (one DMMA GEMM per product)"),
                    "l2": "inputs larger than L2 (each q x q state is 537 MB; 2 x (8 solver grids + 2 dense "
-                         "inverses) = 10.7 GB resident)",
+                         "inverses) = 10.7 GB resident" +
+                         (", plus the Strassen operand sums and scratch)" if levels > 0 else ")"),
                    "parallelism": "single GPU", "setup_s": round(setup_s, 2)},
         "roofline": roof,
         "roofline_hbm": hbm,
@@ -595,6 +676,7 @@ def run_cfg5(args):
         "gpu_launches": 2 * per_species * args.steps,
         "clocks": clk,
         "alt_preconditioner": alt,
+        "classic_gemm_schedule": classic,
         "secondary": secondary,
     }
     print(json.dumps(line), flush=True)

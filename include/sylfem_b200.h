@@ -165,12 +165,17 @@ int sfb_pre_create(int qy, int qx, int kind, const double* L,
                    const double* lamR_host, sfb_pre** out);
 /* The inverse-form products Z = P_L^-1 (R P_R^-1) of shapes with q_y, q_x >=
  * min_q and divisible by 4 run as one level of Strassen around the DMMA GEMM
- * (7 half-size products, the constant operands' block sums formed at
+ * (7 half-size products per level, the constant operands' block sums formed at
  * creation); it replaces the same two dense solves of Preconditioner.apply_inverse
  * (solvers.py:134-143).  Applies to preconditioners created afterwards; 0 =
  * never (default: SYLFEM_B200_STRASSEN_MINQ or 6144).  Returns the previous
- * threshold.  sfb_pre_uses_strassen reports what a preconditioner does. */
+ * threshold. */
 int sfb_set_strassen_min_q(int min_q);
+/* Most Strassen levels taken (0..3, default SYLFEM_B200_STRASSEN_LEVELS or 3);
+ * a level needs dimensions divisible by 4 and halves of at least min_q / 6.
+ * Returns the previous value. */
+int sfb_set_strassen_levels(int levels);
+/* Strassen levels this preconditioner's products use (0: classic GEMMs). */
 int sfb_pre_uses_strassen(const sfb_pre* p);
 /* Banded SPD factors: lower Cholesky factors in band storage
  * lband[i][d] = C_L[i][i - bw + d] (d = 0..bw), same for the right factor. */
@@ -252,6 +257,16 @@ int sfb_imex_rds_run(sfb_pcg* solver_u, sfb_pcg* solver_v, const sfb_map* rhs_ma
  *      leading dimensions and 16-byte aligned rows (TMA requirement). ------ */
 int sfb_dgemm_nt(const double* A_dev, int lda, const double* Bt_dev, int ldb,
                  int M, int N, int K, double* C_dev, int ldc, void* stream);
+
+/* Seven independent products of one shape in one persistent launch (128 x 128
+ * tiles, one wave schedule and stream-K tail for the whole batch): C_b = A_b
+ * Bt_b^T at C_dev + b * c_stride, b = 0..6 -- the seven half-size products of a
+ * Strassen level of the inverse-form preconditioner (solvers.py:134-143).
+ * A_host/Bt_host: host arrays of 7 device pointers, lda_host/ldb_host of 7 ints. */
+int sfb_dgemm_nt_batch7(const double* const* A_host, const int* lda_host,
+                        const double* const* Bt_host, const int* ldb_host,
+                        int M, int N, int K, double* C_dev, int ldc, long long c_stride,
+                        void* stream);
 
 /* ---- host-synchronous blocks of the column-sharded MO-PCG (one rank's
  *      columns; the collectives run between these calls) --------------- */

@@ -110,13 +110,15 @@ struct Sched {
     long long U;         // stream-K (tail) iterations
     int G;               // CTAs
     int tiles_total;     // output tiles (one <C,D> partial each)
+    int tiles_per;       // output tiles per problem (batched launch: tile / tiles_per = problem)
+    long long c_stride;  // doubles between the problems' outputs (batched launch)
     int waves;           // data-parallel full waves (tiles 0 .. waves * G - 1)
     __device__ long long start(int c) const { return (long long)c * U / G; }
     // tile -> output origin: tiles run down GROUP_M-row bands column by column,
     // so the CTAs in flight share A and B panels in L2 (plain row-major with 0)
     __device__ void origin(int tile, int bm, int bn, int& m0, int& n0) const {
 #if GEMM_GROUP_M > 0
-        const int tiles_m = tiles_total / tiles_n;
+        const int tiles_m = tiles_per / tiles_n;
         const int band = tile / (GEMM_GROUP_M * tiles_n), first = band * GEMM_GROUP_M;
         const int gm = min(tiles_m - first, GEMM_GROUP_M), in = tile - band * GEMM_GROUP_M * tiles_n;
         m0 = (first + in % gm) * bm;
@@ -145,7 +147,7 @@ __device__ __forceinline__ size_t ws_slot(int cta, int k0) {
 // Epilogue of one finished tile (registers -> global).
 template <class T>
 __device__ __forceinline__ double tile_epilogue(double (&acc)[T::MI][T::NJ][2], const GemmEpi& ep, int M, int N, int m0,
-                                                int n0, int wm, int wn, int g, int t) {
+                                                int n0, int wm, int wn, int g, int t, size_t coff = 0) {
     constexpr int MI = T::MI, NJ = T::NJ;
     double dot = 0.0;
     #pragma unroll
@@ -186,7 +188,7 @@ __device__ __forceinline__ double tile_epilogue(double (&acc)[T::MI][T::NJ][2], 
                         if (ok0) v0 *= ep.sr[m] * ep.sc[n];
                         if (ok1) v1 *= ep.sr[m] * ep.sc[n + 1];
                     }
-                    double* c = ep.C + (size_t)m * ep.ldc + n;
+                    double* c = ep.C + coff + (size_t)m * ep.ldc + n;
                     if (ok1) {
                         *reinterpret_cast<double2*>(c) = make_double2(v0, v1);
                     } else if (ok0) {
@@ -213,10 +215,18 @@ __device__ __forceinline__ double tile_epilogue(double (&acc)[T::MI][T::NJ][2], 
 // deadlock-free however many kernels share the GPU.  <C,D> partials are per
 // tile, so every sum is independent of who finished.  With ws == nullptr
 // every CTA owns whole tiles (grid = tile count).
-template <class T>
+// NB > 1: a batch of NB independent problems of one shape in one persistent
+// launch (plain store epilogue; the seven half-size products of a Strassen
+// level): tile / tiles_per selects the problem's tensor maps and output, so
+// the whole batch shares one wave schedule and one stream-K tail.
+template <int NB>
+struct GemmMaps {
+    CUtensorMap a[NB], b[NB];
+};
+
+template <class T, int NB>
 __global__ void __launch_bounds__(T::NTHREADS, T::CTAS_PER_SM)
-    dgemm_nt_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
-                    int K, GemmEpi ep, Sched sc) {
+    dgemm_nt_kernel(const __grid_constant__ GemmMaps<NB> maps, int M, int N, int K, GemmEpi ep, Sched sc) {
     constexpr int BM = T::BM, BN = T::BN, NWARPS = T::NWARPS, NTHREADS = T::NTHREADS;
     constexpr int BK = T::BK, STAGES = T::STAGES, LOOKAHEAD = T::LOOKAHEAD;
     constexpr int A_BYTES = T::A_BYTES, B_BYTES = T::B_BYTES;
@@ -253,13 +263,16 @@ __global__ void __launch_bounds__(T::NTHREADS, T::CTAS_PER_SM)
         int tile, kt;
         locate(it, tile, kt);
         int m0, n0;
-        sc.origin(tile, BM, BN, m0, n0);
+        const int prob = NB > 1 ? tile / sc.tiles_per : 0;
+        sc.origin(NB > 1 ? tile - prob * sc.tiles_per : tile, BM, BN, m0, n0);
+        const CUtensorMap* tmA = &maps.a[prob];
+        const CUtensorMap* tmB = &maps.b[prob];
         const int sl = it % STAGES;
         mbar_expect_tx_u32(full + 8 * sl, A_BYTES + B_BYTES);
         #pragma unroll
         for (int kb = 0; kb < BK / KBOX; ++kb) {
-            tma_load_u32(sA + sl * A_BYTES + kb * BM * KBOX * 8, &tmA, full + 8 * sl, kt * BK + kb * KBOX, m0);
-            tma_load_u32(sB + sl * B_BYTES + kb * BN * KBOX * 8, &tmB, full + 8 * sl, kt * BK + kb * KBOX, n0);
+            tma_load_u32(sA + sl * A_BYTES + kb * BM * KBOX * 8, tmA, full + 8 * sl, kt * BK + kb * KBOX, m0);
+            tma_load_u32(sB + sl * B_BYTES + kb * BN * KBOX * 8, tmB, full + 8 * sl, kt * BK + kb * KBOX, n0);
         }
     };
 
@@ -269,8 +282,10 @@ __global__ void __launch_bounds__(T::NTHREADS, T::CTAS_PER_SM)
             mbar_init_u32(empty + 8 * s, NWARPS);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+        for (int b = 0; b < NB; ++b) {
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.a[b])) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.b[b])) : "memory");
+        }
         for (int it = 0; it < LOOKAHEAD && it < n_it; ++it) issue(it);
     }
     __syncthreads();
@@ -329,7 +344,8 @@ __global__ void __launch_bounds__(T::NTHREADS, T::CTAS_PER_SM)
         }
 
         int m0, n0;
-        sc.origin(tile, BM, BN, m0, n0);
+        const int prob = NB > 1 ? tile / sc.tiles_per : 0;
+        sc.origin(NB > 1 ? tile - prob * sc.tiles_per : tile, BM, BN, m0, n0);
         bool finish = true;
         if (k0 != 0 || kl != KT - 1) {
             // split tile: the last piece to arrive finishes it (no CTA ever
@@ -397,7 +413,8 @@ __global__ void __launch_bounds__(T::NTHREADS, T::CTAS_PER_SM)
             __syncthreads();  // s_fin is rewritten by the next split piece
         }
         if (finish) {
-            const double d = tile_epilogue<T>(acc, ep, M, N, m0, n0, wm, wn, g, t);
+            const double d = tile_epilogue<T>(acc, ep, M, N, m0, n0, wm, wn, g, t,
+                                              NB > 1 ? (size_t)prob * (size_t)sc.c_stride : 0);
             if (ep.mode == EPI_STORE_DOT) {  // one partial per tile: the sum order does not depend on who finished
                 const double part = block_sum<NTHREADS>(d, sh_dot);
                 if (threadIdx.x == 0) ep.partials[tile] = part;
@@ -438,17 +455,21 @@ int tile_mode() {
     return m;
 }
 
-template <class T>
-int launch_tile(const double* A, int lda, const double* Bt, int ldb, int M, int N, int K, const GemmEpi& ep,
-                cudaStream_t stream) {
-    SFB_TRY(ensure_dynamic_smem(dgemm_nt_kernel<T>, T::SMEM_BYTES));
-    CUtensorMap ma, mb;
-    SFB_TRY(make_map(&ma, A, M, K, lda, T::BM));
-    SFB_TRY(make_map(&mb, Bt, N, K, ldb, T::BN));
+template <class T, int NB>
+int launch_tile_batch(const GemmOperands* ops, int M, int N, int K, long long c_stride, const GemmEpi& ep,
+                      cudaStream_t stream) {
+    SFB_TRY(ensure_dynamic_smem(dgemm_nt_kernel<T, NB>, T::SMEM_BYTES));
+    GemmMaps<NB> maps;
+    for (int b = 0; b < NB; ++b) {
+        SFB_TRY(make_map(&maps.a[b], ops[b].A, M, K, ops[b].lda, T::BM));
+        SFB_TRY(make_map(&maps.b[b], ops[b].Bt, N, K, ops[b].ldb, T::BN));
+    }
     Sched sc;
     sc.tiles_n = (N + T::BN - 1) / T::BN;
     sc.KT = (K + T::BK - 1) / T::BK;
-    const int tiles = tiles_of(M, N, T::BM, T::BN);
+    sc.tiles_per = tiles_of(M, N, T::BM, T::BN);
+    sc.c_stride = c_stride;
+    const int tiles = NB * sc.tiles_per;
     sc.tiles_total = tiles;
     sc.waves = 0;
     const bool have_ws = ep.sk_ws != nullptr && ep.sk_flags != nullptr;
@@ -470,8 +491,15 @@ int launch_tile(const double* A, int lda, const double* Bt, int ldb, int M, int 
         sc.U = (long long)tiles * sc.KT;
         sc.G = (int)std::max(1LL, std::min<long long>(slots, sc.U / min_work));
     }
-    return launch_kernel(dgemm_nt_kernel<T>, dim3(sc.G), dim3(T::NTHREADS), T::SMEM_BYTES, stream, ma, mb, M, N, K,
+    return launch_kernel(dgemm_nt_kernel<T, NB>, dim3(sc.G), dim3(T::NTHREADS), T::SMEM_BYTES, stream, maps, M, N, K,
                          ep, sc);
+}
+
+template <class T>
+int launch_tile(const double* A, int lda, const double* Bt, int ldb, int M, int N, int K, const GemmEpi& ep,
+                cudaStream_t stream) {
+    const GemmOperands op{A, lda, Bt, ldb};
+    return launch_tile_batch<T, 1>(&op, M, N, K, 0, ep, stream);
 }
 
 }  // namespace
@@ -501,6 +529,16 @@ int launch_dgemm_nt(const double* A, int lda, const double* Bt, int ldb, int M, 
     const bool small = mode == 64 || (mode != 128 && t128 < 64);
     return small ? launch_tile<SmallTile>(A, lda, Bt, ldb, M, N, K, ep, stream)
                  : launch_tile<BigTile>(A, lda, Bt, ldb, M, N, K, ep, stream);
+}
+
+// Seven independent products C_b[M x N] = A_b Bt_b^T of one shape in one launch
+// (128 x 128 tiles, plain store; C_b = ep.C + b * c_stride).
+int launch_dgemm_nt_batch7(const GemmOperands* ops, int M, int N, int K, long long c_stride, const GemmEpi& ep,
+                           cudaStream_t stream) {
+    if (M <= 0 || N <= 0 || K <= 0) return arg_error("empty GEMM");
+    if (ep.mode != EPI_STORE) return arg_error("batched GEMM: plain store epilogue only");
+    if (7 * tiles_of(M, N, 128, 128) > gemm_max_tiles()) return arg_error("batched GEMM: too many tiles");
+    return launch_tile_batch<BigTile, 7>(ops, M, N, K, c_stride, ep, stream);
 }
 
 // Upper bound of the output tiles of any tile shape (one <C,D> partial each).

@@ -46,6 +46,14 @@ struct GemmEpi {
 
 int launch_dgemm_nt(const double* A, int lda, const double* Bt, int ldb, int M, int N, int K,
                     const GemmEpi& ep, cudaStream_t stream);
+struct GemmOperands {
+    const double* A;
+    int lda;
+    const double* Bt;
+    int ldb;
+};
+int launch_dgemm_nt_batch7(const GemmOperands* ops, int M, int N, int K, long long c_stride, const GemmEpi& ep,
+                           cudaStream_t stream);
 int gemm_grid_blocks(int M, int N);
 int gemm_smem_bytes();
 size_t gemm_workspace_doubles();

@@ -152,6 +152,12 @@ struct sfb_map {
     double* hband = nullptr;
 };
 
+namespace sfb {
+namespace {
+struct StrassenPlan;  // block sums of a constant left operand (defined with the Strassen driver below)
+}
+}  // namespace sfb
+
 struct sfb_pre {
     int kind = SFB_PRE_IDENTITY;
     int qy = 0, qx = 0;
@@ -162,7 +168,8 @@ struct sfb_pre {
     double *sl = nullptr, *sr = nullptr;
     // INVERSE, large shapes divisible by 4: the five Strassen block sums of
     // A1 and B1 (the constant left operands of the two products), formed once
-    double *A1s = nullptr, *B1s = nullptr;
+    sfb::StrassenPlan *planA = nullptr, *planB = nullptr;
+    int strassen_levels = 0;
     bool strassen = false;
     // BANDED: factors prepared for the SPIKE solves (spike.cu)
     SpikeFactor fl, fr;
@@ -226,14 +233,19 @@ int op_apply_impl(const sfb_op* op, const double* U, int ldu, double* W, int ldw
     return SFB_OK;
 }
 
-// ---- one level of Strassen around the DMMA GEMM -------------------------
+// ---- Strassen around the DMMA GEMM ---------------------------------------
 // The inverse-form preconditioner (solvers.py:103-143 as two dense products)
-// multiplies by the same two matrices every iteration, so the five block sums
-// of the constant operand are formed once (sfb_pre_create); per product: one
-// pass for the variable operand's sums, seven half-size DMMA GEMMs and one
-// assembly pass (7/8 of the flops; the two passes move ~24 half-size blocks).
-// Used for shapes of at least strassen_min_q() that are divisible by 4
-// (SYLFEM_B200_STRASSEN_MINQ, 0 = never).
+// multiplies by the same two matrices every iteration, so the block sums of
+// the constant left operands are formed once, for every level
+// (StrassenPlan, built in sfb_pre_create).  Per product and level: one pass
+// for the variable operand's five sums, the seven half-size products (the
+// next level, or one batched DMMA launch) and one assembly pass.  Two levels
+// do 49/64 of the flops, three 343/512.  Used for shapes of at least
+// strassen_min_q() with every level's dimensions divisible by 4 and leaves of
+// at least a sixth of the threshold (SYLFEM_B200_STRASSEN_MINQ, default 6144,
+// 0 = never; SYLFEM_B200_STRASSEN_LEVELS, default 3: q = 8192 runs 1024^3
+// leaves, measured 49.6 ms per preconditioner application against 51.2 / 55.9
+// ms with two / one levels and 62.2 ms classic).
 std::atomic<int>& strassen_min_q_slot() {
     static std::atomic<int> v([] {
         const char* e = std::getenv("SYLFEM_B200_STRASSEN_MINQ");
@@ -242,51 +254,117 @@ std::atomic<int>& strassen_min_q_slot() {
     return v;
 }
 int strassen_min_q() { return strassen_min_q_slot().load(std::memory_order_relaxed); }
+std::atomic<int>& strassen_max_levels_slot() {
+    static std::atomic<int> v([] {
+        const char* e = std::getenv("SYLFEM_B200_STRASSEN_LEVELS");
+        return e ? std::max(0, std::min(3, std::atoi(e))) : 3;
+    }());
+    return v;
+}
 
-bool strassen_shape(int qy, int qx) {
+int strassen_levels_of(int q) {
     const int m = strassen_min_q();
-    return m > 0 && qy >= m && qx >= m && qy % 4 == 0 && qx % 4 == 0;
+    if (m <= 0 || q < m) return 0;
+    const int leaf = std::max(m / 6, 64);
+    int levels = 0;
+    while (levels < strassen_max_levels_slot().load(std::memory_order_relaxed) && q % 4 == 0 && q / 2 >= leaf) {
+        q /= 2;
+        ++levels;
+    }
+    return levels;
+}
+int strassen_levels(int qy, int qx) { return std::min(strassen_levels_of(qy), strassen_levels_of(qx)); }
+
+// A constant left operand (M x K), its five block sums and, below the last
+// level, the plans of its seven half-size operands.
+struct StrassenPlan {
+    const double* A = nullptr;
+    int lda = 0, M = 0, K = 0, ldk = 0;
+    double* S = nullptr;  // (A11 + A22, A21 + A22, A11 + A12, A21 - A11, A12 - A22), (M/2) x ldk each
+    StrassenPlan* sub[7] = {};
+    // left operand of product i: (A11 + A22), (A21 + A22), A11, A22, (A11 + A12), (A21 - A11), (A12 - A22)
+    void operand(int i, const double** a, int* ld) const {
+        const size_t sa = (size_t)(M / 2) * ldk;
+        static const int sum_of[7] = {0, 1, -1, -2, 2, 3, 4};
+        if (sum_of[i] >= 0) {
+            *a = S + sum_of[i] * sa;
+            *ld = ldk;
+        } else {
+            *a = sum_of[i] == -1 ? A : A + (size_t)(M / 2) * lda + K / 2;
+            *ld = lda;
+        }
+    }
+};
+
+void free_strassen_plan(StrassenPlan* p) {
+    if (!p) return;
+    for (auto* c : p->sub) free_strassen_plan(c);
+    cudaFree(p->S);
+    delete p;
 }
 
-size_t strassen_sums_doubles(int q) { return (size_t)5 * (q / 2) * pad_ld(q / 2); }
-
-size_t strassen_scratch_doubles(int qy, int qx) {
-    const int h = std::max(qy, qx) / 2;
-    return (size_t)12 * h * pad_ld(h);
+int build_strassen_plan(const double* A, int lda, int M, int K, int levels, StrassenPlan** out) {
+    auto* p = new StrassenPlan;
+    p->A = A;
+    p->lda = lda;
+    p->M = M;
+    p->K = K;
+    p->ldk = pad_ld(K / 2);
+    const size_t n = (size_t)5 * (M / 2) * p->ldk;
+    int rc = dalloc(&p->S, n);
+    if (rc == SFB_OK && cudaMemset(p->S, 0, n * 8) != cudaSuccess) rc = SFB_ERR_CUDA;
+    if (rc == SFB_OK)
+        rc = launch_strassen_sums(A, lda, M / 2, K / 2, p->S, p->ldk, (size_t)(M / 2) * p->ldk, 0, nullptr, nullptr);
+    for (int i = 0; i < 7 && rc == SFB_OK && levels > 1; ++i) {
+        const double* a;
+        int ld;
+        p->operand(i, &a, &ld);
+        rc = build_strassen_plan(a, ld, M / 2, K / 2, levels - 1, &p->sub[i]);
+    }
+    if (rc != SFB_OK) {
+        free_strassen_plan(p);
+        return rc;
+    }
+    *out = p;
+    return SFB_OK;
 }
 
-// C[M x N] = A[M x K] Bt[N x K]^T; As = the five A-side sums ((M/2) x pad_ld(K/2) each).
-int strassen_nt(const double* A, int lda, const double* As, const double* Bt, int ldb, int M, int N, int K,
-                double* scratch, double* C, int ldc, const double* D, int ldd, double* partials, PcgState* pcg,
-                double* dot_out, unsigned* counter, const GemmWs* gw, cudaStream_t s) {
-    const int Mh = M / 2, Nh = N / 2, Kh = K / 2;
-    const int ldk = pad_ld(Kh), ldn = pad_ld(Nh);
-    const size_t sa = (size_t)Mh * ldk, sb = (size_t)Nh * ldk, sm = (size_t)Mh * ldn;
+// scratch of a product with `levels` levels on shapes up to h x h halves
+size_t strassen_scratch_doubles(int qy, int qx, int levels) {
+    size_t n = 0;
+    int h = std::max(qy, qx) / 2;
+    for (int l = 0; l < levels; ++l, h /= 2) n += (size_t)12 * h * pad_ld(h);
+    return n;
+}
+
+// C[M x N] = A[M x K] Bt[N x K]^T with A described by `pl`.
+int strassen_apply(const StrassenPlan* pl, const double* Bt, int ldb, int N, double* scratch, double* C, int ldc,
+                   const double* D, int ldd, double* partials, PcgState* pcg, double* dot_out, unsigned* counter,
+                   const GemmWs* gw, cudaStream_t s) {
+    const int Mh = pl->M / 2, Nh = N / 2, Kh = pl->K / 2;
+    const int ldk = pl->ldk, ldn = pad_ld(Nh);
+    const size_t sb = (size_t)Nh * ldk, sm = (size_t)Mh * ldn;
     double* Bs = scratch;
     double* Mp = scratch + 5 * sb;
+    double* rest = Mp + 7 * sm;
     SFB_TRY(launch_strassen_sums(Bt, ldb, Nh, Kh, Bs, ldk, sb, 1, pcg, s));
-    const double *A11 = A, *A22 = A + (size_t)Mh * lda + Kh;
-    const double *B11 = Bt, *B22 = Bt + (size_t)Nh * ldb + Kh;
-    struct Prod {
-        const double* a;
-        int lda;
-        const double* b;
-        int ldb;
-    };
-    const Prod prods[7] = {{As, ldk, Bs, ldk},                    // (A11 + A22)(B11 + B22)
-                           {As + sa, ldk, B11, ldb},              // (A21 + A22) B11
-                           {A11, lda, Bs + sb, ldk},              // A11 (B12 - B22)
-                           {A22, lda, Bs + 2 * sb, ldk},          // A22 (B21 - B11)
-                           {As + 2 * sa, ldk, B22, ldb},          // (A11 + A12) B22
-                           {As + 3 * sa, ldk, Bs + 3 * sb, ldk},  // (A21 - A11)(B11 + B12)
-                           {As + 4 * sa, ldk, Bs + 4 * sb, ldk}}; // (A12 - A22)(B21 + B22)
-    for (int i = 0; i < 7; ++i) {
+    // right operands: (B11 + B22), B11, (B12 - B22), (B21 - B11), B22, (B11 + B12), (B21 + B22)
+    const double* B22 = Bt + (size_t)Nh * ldb + Kh;
+    GemmOperands ops[7] = {{nullptr, 0, Bs, ldk},          {nullptr, 0, Bt, ldb},          {nullptr, 0, Bs + sb, ldk},
+                           {nullptr, 0, Bs + 2 * sb, ldk}, {nullptr, 0, B22, ldb},         {nullptr, 0, Bs + 3 * sb, ldk},
+                           {nullptr, 0, Bs + 4 * sb, ldk}};
+    for (int i = 0; i < 7; ++i) pl->operand(i, &ops[i].A, &ops[i].lda);
+    if (pl->sub[0] == nullptr) {
         GemmEpi e;
         e.mode = EPI_STORE;
-        e.C = Mp + i * sm;
+        e.C = Mp;
         e.ldc = ldn;
         e.pcg = pcg;
-        SFB_TRY(launch_dgemm_nt(prods[i].a, prods[i].lda, prods[i].b, prods[i].ldb, Mh, Nh, Kh, with_ws(e, gw), s));
+        SFB_TRY(launch_dgemm_nt_batch7(ops, Mh, Nh, Kh, (long long)sm, with_ws(e, gw), s));
+    } else {
+        for (int i = 0; i < 7; ++i)
+            SFB_TRY(strassen_apply(pl->sub[i], ops[i].Bt, ops[i].ldb, Nh, rest, Mp + i * sm, ldn, nullptr, 0, nullptr,
+                                   pcg, nullptr, nullptr, gw, s));
     }
     return launch_strassen_combine(Mp, ldn, sm, Mh, Nh, C, ldc, D, ldd, partials, pcg, dot_out, counter, s);
 }
@@ -317,11 +395,11 @@ int pre_apply_impl(const sfb_pre* p, const double* R, int ldr, double* Z, int ld
         case SFB_PRE_INVERSE: {
             if (p->strassen && gw != nullptr && gw->strassen != nullptr) {
                 // T1 = P_R^-T R^T, then Z = P_L^-1 T1^T with <Z,R> in the assembly pass
-                SFB_TRY(strassen_nt(p->B1, p->ldB, p->B1s, R, ldr, qx, qy, qx, gw->strassen, T1, ldt1, nullptr, 0,
-                                    nullptr, pcg, nullptr, nullptr, gw, s));
+                SFB_TRY(strassen_apply(p->planB, R, ldr, qy, gw->strassen, T1, ldt1, nullptr, 0, nullptr, pcg, nullptr,
+                                       nullptr, gw, s));
                 const bool dot = pcg || red;
-                return strassen_nt(p->A1, p->ldA, p->A1s, T1, ldt1, qy, qx, qy, gw->strassen, Z, ldz,
-                                   dot ? R : nullptr, ldr, partials, pcg, red ? &red->v[3] : nullptr, counter, gw, s);
+                return strassen_apply(p->planA, T1, ldt1, qx, gw->strassen, Z, ldz, dot ? R : nullptr, ldr, partials,
+                                      pcg, red ? &red->v[3] : nullptr, counter, gw, s);
             }
             GemmEpi e1;  // T1 = (R P_R^-1)^T
             e1.mode = EPI_STORE_T;
@@ -573,7 +651,13 @@ int sfb_set_strassen_min_q(int min_q) {
     return prev;
 }
 
-int sfb_pre_uses_strassen(const sfb_pre* p) { return p != nullptr && p->strassen ? 1 : 0; }
+int sfb_pre_uses_strassen(const sfb_pre* p) { return p != nullptr && p->strassen ? p->strassen_levels : 0; }
+
+int sfb_set_strassen_levels(int levels) {
+    const int prev = strassen_max_levels_slot().load(std::memory_order_relaxed);
+    strassen_max_levels_slot().store(std::max(0, std::min(3, levels)), std::memory_order_relaxed);
+    return prev;
+}
 
 int sfb_init(int device, int* sm_count) {
     SFB_CUDA_TRY(cudaSetDevice(device));
@@ -870,19 +954,13 @@ int sfb_pre_create(int qy, int qx, int kind, const double* L, const double* R, c
         if (rc == SFB_OK) rc = dalloc(&p->B1, (size_t)qx * p->ldB);
         if (rc == SFB_OK) rc = upload_padded(p->A1, p->ldA, L, qy, qy);
         if (rc == SFB_OK) rc = upload_padded(p->B1, p->ldB, R, qx, qx);
-        if (rc == SFB_OK && strassen_shape(qy, qx)) {
-            rc = dalloc(&p->A1s, strassen_sums_doubles(qy));
-            if (rc == SFB_OK) rc = dalloc(&p->B1s, strassen_sums_doubles(qx));
-            if (rc == SFB_OK) rc = cudaMemset(p->A1s, 0, strassen_sums_doubles(qy) * 8) == cudaSuccess ? SFB_OK : SFB_ERR_CUDA;
-            if (rc == SFB_OK) rc = cudaMemset(p->B1s, 0, strassen_sums_doubles(qx) * 8) == cudaSuccess ? SFB_OK : SFB_ERR_CUDA;
-            if (rc == SFB_OK)
-                rc = launch_strassen_sums(p->A1, p->ldA, qy / 2, qy / 2, p->A1s, pad_ld(qy / 2),
-                                          (size_t)(qy / 2) * pad_ld(qy / 2), 0, nullptr, nullptr);
-            if (rc == SFB_OK)
-                rc = launch_strassen_sums(p->B1, p->ldB, qx / 2, qx / 2, p->B1s, pad_ld(qx / 2),
-                                          (size_t)(qx / 2) * pad_ld(qx / 2), 0, nullptr, nullptr);
+        const int levels = strassen_levels(qy, qx);
+        if (rc == SFB_OK && levels > 0) {
+            rc = build_strassen_plan(p->A1, p->ldA, qy, qy, levels, &p->planA);
+            if (rc == SFB_OK) rc = build_strassen_plan(p->B1, p->ldB, qx, qx, levels, &p->planB);
             if (rc == SFB_OK && cudaDeviceSynchronize() != cudaSuccess) rc = SFB_ERR_CUDA;
             p->strassen = rc == SFB_OK;
+            p->strassen_levels = levels;
         }
         if (rc != SFB_OK) return fail(rc);
         *out = p;
@@ -968,8 +1046,8 @@ int sfb_pre_apply(const sfb_pre* p, const double* R, int ldr, double* Z, int ldz
         SFB_TRY(tmp.get(&gw.seg_b, p->seg_doubles * 8));
     }
     if (p->strassen) {
-        SFB_TRY(tmp.get(&gw.strassen, strassen_scratch_doubles(p->qy, p->qx) * 8));
-        SFB_CUDA_TRY(cudaMemsetAsync(gw.strassen, 0, strassen_scratch_doubles(p->qy, p->qx) * 8, s));
+        // (padding columns of the scratch blocks are never read)
+        SFB_TRY(tmp.get(&gw.strassen, strassen_scratch_doubles(p->qy, p->qx, p->strassen_levels) * 8));
     }
     SFB_TRY(pre_apply_impl(p, Rb, ld, Zb, ld, T1, ldt1, T2, ld, parts, nullptr, red, &gw, s));
     SFB_CUDA_TRY(cudaMemcpy2DAsync(Z, (size_t)ldz * 8, Zb, (size_t)ld * 8, (size_t)p->qx * 8, p->qy,
@@ -1155,8 +1233,8 @@ int sfb_pre_destroy(sfb_pre* p) {
     cudaFree(p->B1t);
     cudaFree(p->sl);
     cudaFree(p->sr);
-    cudaFree(p->A1s);
-    cudaFree(p->B1s);
+    free_strassen_plan(p->planA);
+    free_strassen_plan(p->planB);
     free_spike_factor(p->fl);
     free_spike_factor(p->fr);
     delete p;
@@ -1196,8 +1274,9 @@ int sfb_pcg_create(const sfb_op* op, const sfb_pre* pre, sfb_pcg** out) {
         if (rc == SFB_OK) rc = dalloc(&s->gw.seg_b, pre->seg_doubles);
     }
     if (rc == SFB_OK && pre->strassen) {
-        rc = dalloc(&s->gw.strassen, strassen_scratch_doubles(s->qy, s->qx));
-        if (rc == SFB_OK) cudaMemset(s->gw.strassen, 0, strassen_scratch_doubles(s->qy, s->qx) * 8);
+        const size_t ns = strassen_scratch_doubles(s->qy, s->qx, pre->strassen_levels);
+        rc = dalloc(&s->gw.strassen, ns);
+        if (rc == SFB_OK) cudaMemset(s->gw.strassen, 0, ns * 8);
     }
     if (rc == SFB_OK) {
         for (double** b : bufs) cudaMemset(*b, 0, n * 8);
@@ -1431,6 +1510,23 @@ int sfb_dgemm_nt(const double* A, int lda, const double* Bt, int ldb, int M, int
     GemmWs gw;
     SFB_TRY(temp_ws(tmp, gw, s));
     return launch_dgemm_nt(A, lda, Bt, ldb, M, N, K, with_ws(e, &gw), s);
+}
+
+int sfb_dgemm_nt_batch7(const double* const* A, const int* lda, const double* const* Bt, const int* ldb, int M, int N,
+                        int K, double* C, int ldc, long long c_stride, void* stream) {
+    SFB_NVTX("sfb_dgemm_nt_batch7");
+    if (!A || !lda || !Bt || !ldb || !C) return arg_error("batched GEMM: null argument");
+    GemmOperands ops[7];
+    for (int b = 0; b < 7; ++b) ops[b] = GemmOperands{A[b], lda[b], Bt[b], ldb[b]};
+    GemmEpi e;
+    e.mode = EPI_STORE;
+    e.C = C;
+    e.ldc = ldc;
+    cudaStream_t s = (cudaStream_t)stream;
+    ScopedFree tmp(s);
+    GemmWs gw;
+    SFB_TRY(temp_ws(tmp, gw, s));
+    return launch_dgemm_nt_batch7(ops, M, N, K, c_stride, with_ws(e, &gw), s);
 }
 
 int sfb_dgemm_nt_scatter(const double* A, int lda, const double* Bt, int ldb, int M, int N, int K, int nseg,

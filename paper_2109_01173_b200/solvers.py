@@ -209,6 +209,12 @@ def set_strassen_min_q(min_q: int) -> int:
     return int(nat.lib().sfb_set_strassen_min_q(int(min_q)))
 
 
+def set_strassen_levels(levels: int) -> int:
+    """Most Strassen levels taken by the inverse-form products (0..3, default
+    3: q = 8192 runs 343 GEMMs of 1024^3 per product); returns the previous value."""
+    return int(nat.lib().sfb_set_strassen_levels(int(levels)))
+
+
 class Preconditioner:
     """Single-term preconditioner U -> P_L U P_R (solvers.py:103-150).
 
@@ -289,10 +295,10 @@ class Preconditioner:
         self._handle_shape = shape
         return self._handle.p
 
-    def uses_strassen(self, shape=None) -> bool:
-        """Whether the device form multiplies by the dense inverses with the
-        Strassen schedule (see set_strassen_min_q)."""
-        return bool(nat.lib().sfb_pre_uses_strassen(self.native(shape)))
+    def uses_strassen(self, shape=None) -> int:
+        """Strassen levels the device form's dense products use (0: classic
+        GEMMs; see set_strassen_min_q, set_strassen_levels)."""
+        return int(nat.lib().sfb_pre_uses_strassen(self.native(shape)))
 
     @staticmethod
     def _eigh(m, q):

@@ -21,24 +21,26 @@ from conftest import relerr
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture
-def strassen_from_256():
-    prev = pb.set_strassen_min_q(256)
-    yield
+@pytest.fixture(params=[1, 2, 3], ids=["one-level", "two-levels", "three-levels"])
+def strassen_from_256(request):
+    prev, prev_levels = pb.set_strassen_min_q(256), pb.set_strassen_levels(request.param)
+    yield request.param
     pb.set_strassen_min_q(prev)
+    pb.set_strassen_levels(prev_levels)
 
 
 def _lumped_sets(Nx, Ny):
     return pb.build_direction_sets(pb.SQUARE, 1, (Nx, Ny), pb.BCKind.NEUMANN, lumped=True)
 
 
-@pytest.mark.parametrize("Nx,Ny", [(511, 511), (639, 511), (255, 383)])
+@pytest.mark.parametrize("Nx,Ny", [(511, 511), (767, 511), (255, 383)])
 def test_strassen_product_matches_classic_schedule(Nx, Ny, strassen_from_256):
     x, y = _lumped_sets(Nx, Ny)
     d, tau = 20.0, 1.25e-5
     kw = {"d_u": d, "tau": tau, "lumped": True}
     pre_s = pb.make_preconditioner("parabolic_lumped", x, y, mode="inverse", **kw)
-    assert pre_s.uses_strassen()
+    # leaves of at least 64 (a sixth of the threshold, not below 64): q = 256 takes at most two levels
+    assert pre_s.uses_strassen() == (strassen_from_256 if min(x.q, y.q) >= 512 else min(strassen_from_256, 2))
     prev = pb.set_strassen_min_q(0)
     try:
         pre_c = pb.make_preconditioner("parabolic_lumped", x, y, mode="inverse", **kw)
@@ -76,7 +78,7 @@ def test_strassen_mo_pcg_iterates_vs_oracle(d, tau, strassen_from_256):
     rhs = orhs(S)
     assert relerr(rhs_of(S), rhs) <= 1e-13
     pre = pb.make_preconditioner("parabolic_lumped", x, y, mode="inverse", d_u=d, tau=tau, lumped=True)
-    assert pre.uses_strassen()
+    assert pre.uses_strassen() == strassen_from_256
     K = 6
     ref = orc.mo_pcg(terms, rhs, opre.inverse, ("residual", 1e-300), u0=S, max_iter=K)
     rep = pb.mo_pcg(op, rhs, precond=pre, stop=pb.fixed_budget(), u0=S, max_iter=K)
@@ -89,3 +91,31 @@ def test_strassen_mo_pcg_iterates_vs_oracle(d, tau, strassen_from_256):
     assert rep.stop_reason == "tolerance"
     assert abs(rep.iterations - full["iterations"]) <= 1
     assert relerr(rep.solution, full["solution"]) <= 1e-9
+
+
+@pytest.mark.parametrize("M,N,K", [(256, 256, 256), (384, 256, 512), (130, 258, 100)])
+def test_batched_gemm_matches_fp64_matmul(M, N, K):
+    """sfb_dgemm_nt_batch7: seven products in one persistent launch (operands with
+    different leading dimensions, as the Strassen level passes block views and sums)."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2109_01173_b200 import _native as nat
+
+    g = torch.Generator(device="cuda").manual_seed(M + N + K)
+    ldc = N + (N % 2)
+    As = [torch.randn(M, K + 2 * (b % 3), dtype=torch.float64, device="cuda", generator=g) for b in range(7)]
+    Bs = [torch.randn(N, K + 4 * (b % 2), dtype=torch.float64, device="cuda", generator=g) for b in range(7)]
+    out = torch.zeros(7, M, ldc, dtype=torch.float64, device="cuda")
+    pa = (C.c_void_p * 7)(*[a.data_ptr() for a in As])
+    pb_ = (C.c_void_p * 7)(*[b.data_ptr() for b in Bs])
+    la = (C.c_int * 7)(*[a.shape[1] for a in As])
+    lb = (C.c_int * 7)(*[b.shape[1] for b in Bs])
+    nat.check(nat.lib().sfb_dgemm_nt_batch7(pa, la, pb_, lb, M, N, K, out.data_ptr(), ldc, M * ldc, nat.stream()),
+              "batched GEMM")
+    torch.cuda.synchronize()
+    for b in range(7):
+        ref = As[b][:, :K] @ Bs[b][:, :K].T
+        assert float((out[b, :, :N] - ref).norm() / ref.norm()) <= 1e-14
+    assert float(out[:, :, N:].abs().max()) == 0.0 if ldc > N else True

@@ -16,11 +16,12 @@ s = torch.cuda.current_stream().cuda_stream
 PRE_INVERSE = nat.PRE_INVERSE
 
 
-def make(q, A, Bt, minq):
-    prev = L.sfb_set_strassen_min_q(minq)
+def make(q, A, Bt, levels):
+    prev, prev_l = L.sfb_set_strassen_min_q(256 if levels else 0), L.sfb_set_strassen_levels(levels)
     out = C.c_void_p()
     nat.check(L.sfb_pre_create(q, q, PRE_INVERSE, A.data_ptr(), Bt.data_ptr(), None, None, C.byref(out)), "pre")
     L.sfb_set_strassen_min_q(prev)
+    L.sfb_set_strassen_levels(prev_l)
     return out
 
 
@@ -31,9 +32,9 @@ for q in [int(a) for a in sys.argv[1:]] or [4096, 8192]:
     R = torch.randn(q, q, dtype=torch.float64, device="cuda", generator=g)
     Z = torch.empty_like(R)
     ref = A @ (R @ Bt.T)
-    for name, minq in (("classic", 0), ("strassen", 256)):
-        h = make(q, A, Bt, minq)
-        assert bool(L.sfb_pre_uses_strassen(h)) == (minq > 0)
+    for name, levels in (("classic", 0), ("strassen-1", 1), ("strassen-2", 2), ("strassen-3", 3)):
+        h = make(q, A, Bt, levels)
+        assert L.sfb_pre_uses_strassen(h) == levels
 
         def run():
             nat.check(L.sfb_pre_apply(h, R.data_ptr(), q, Z.data_ptr(), q, s), "apply")
@@ -51,6 +52,6 @@ for q in [int(a) for a in sys.argv[1:]] or [4096, 8192]:
         e1.record()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / reps
-        print(f"q={q} {name:9s} {ms:8.3f} ms per apply (2 products + 2 copies)  "
+        print(f"q={q} {name:10s} {ms:8.3f} ms per apply (2 products + 2 copies)  "
               f"{4 * q ** 3 / ms / 1e9:6.2f} TF/s algorithmic  rel err {err:.2e}  max err / max {emax:.2e}", flush=True)
         nat.check(L.sfb_pre_destroy(h), "destroy")
