@@ -258,15 +258,16 @@ int sfb_imex_rds_run(sfb_pcg* solver_u, sfb_pcg* solver_v, const sfb_map* rhs_ma
 int sfb_dgemm_nt(const double* A_dev, int lda, const double* Bt_dev, int ldb,
                  int M, int N, int K, double* C_dev, int ldc, void* stream);
 
-/* Seven independent products of one shape in one persistent launch (128 x 128
- * tiles, one wave schedule and stream-K tail for the whole batch): C_b = A_b
- * Bt_b^T at C_dev + b * c_stride, b = 0..6 -- the seven half-size products of a
- * Strassen level of the inverse-form preconditioner (solvers.py:134-143).
- * A_host/Bt_host: host arrays of 7 device pointers, lda_host/ldb_host of 7 ints. */
-int sfb_dgemm_nt_batch7(const double* const* A_host, const int* lda_host,
-                        const double* const* Bt_host, const int* ldb_host,
-                        int M, int N, int K, double* C_dev, int ldc, long long c_stride,
-                        void* stream);
+/* nb = 7 or 49 independent products of one shape in one persistent launch
+ * (128 x 128 tiles, one wave schedule and stream-K tail for the whole batch):
+ * C_b = A_b Bt_b^T at C_dev + b * c_stride -- the leaf products of one Strassen
+ * node, or of a node's seven children, of the inverse-form preconditioner
+ * (solvers.py:134-143).  A_host/Bt_host: host arrays of nb device pointers,
+ * lda_host/ldb_host of nb ints. */
+int sfb_dgemm_nt_batch(int nb, const double* const* A_host, const int* lda_host,
+                       const double* const* Bt_host, const int* ldb_host,
+                       int M, int N, int K, double* C_dev, int ldc, long long c_stride,
+                       void* stream);
 
 /* ---- host-synchronous blocks of the column-sharded MO-PCG (one rank's
  *      columns; the collectives run between these calls) --------------- */

@@ -36,7 +36,7 @@ EXPORTS = [
     "sfb_vec_update", "sfb_vec_xpby", "sfb_vec_dots",
     "sfb_csr_create", "sfb_csr_spmv", "sfb_csr_destroy",
     "sfb_pcg_shape", "sfb_imex_heat_run", "sfb_imex_rds_run",
-    "sfb_dgemm_nt_scatter", "sfb_dgemm_nt_batch7", "sfb_copy2d", "sfb_ipc_get_handle", "sfb_ipc_open", "sfb_ipc_close",
+    "sfb_dgemm_nt_scatter", "sfb_dgemm_nt_batch", "sfb_copy2d", "sfb_ipc_get_handle", "sfb_ipc_open", "sfb_ipc_close",
     "sfb_frame_pgm16", "sfb_geigh", "sfb_reduced_create", "sfb_reduced_solve", "sfb_reduced_destroy",
     "sfb_shard_create", "sfb_shard_destroy", "sfb_shard_slots", "sfb_shard_dots", "sfb_shard_start",
     "sfb_shard_update", "sfb_shard_control", "sfb_shard_xpby", "sfb_shard_result",
@@ -101,7 +101,7 @@ _SIGS = {
     "sfb_diff_norm": (_I, [_P, _I, _P, _I, _I, _I, _DP, _P]),
     "sfb_pcg_shape": (_I, [_P, C.POINTER(_I), C.POINTER(_I)]),
     "sfb_dgemm_nt_scatter": (_I, [_P, _I, _P, _I, _I, _I, _I, _I, _P, _P, _P, _I, _P]),
-    "sfb_dgemm_nt_batch7": (_I, [_P, _P, _P, _P, _I, _I, _I, _P, _I, C.c_longlong, _P]),
+    "sfb_dgemm_nt_batch": (_I, [_I, _P, _P, _P, _P, _I, _I, _I, _P, _I, C.c_longlong, _P]),
     "sfb_copy2d": (_I, [_P, _I, _P, _I, _I, _I, _P]),
     "sfb_ipc_get_handle": (_I, [_P, _P, C.POINTER(C.c_ulonglong)]),
     "sfb_ipc_open": (_I, [_P, C.c_ulonglong, C.POINTER(_P), C.POINTER(_P)]),

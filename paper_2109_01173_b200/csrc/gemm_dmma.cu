@@ -531,14 +531,18 @@ int launch_dgemm_nt(const double* A, int lda, const double* Bt, int ldb, int M, 
                  : launch_tile<BigTile>(A, lda, Bt, ldb, M, N, K, ep, stream);
 }
 
-// Seven independent products C_b[M x N] = A_b Bt_b^T of one shape in one launch
-// (128 x 128 tiles, plain store; C_b = ep.C + b * c_stride).
-int launch_dgemm_nt_batch7(const GemmOperands* ops, int M, int N, int K, long long c_stride, const GemmEpi& ep,
-                           cudaStream_t stream) {
+// nb = 7 or 49 independent products C_b[M x N] = A_b Bt_b^T of one shape in one
+// launch (128 x 128 tiles, plain store; C_b = ep.C + b * c_stride): the leaf
+// products of one Strassen node, or of its seven children together (98 tensor
+// maps = 12.5 KB of kernel parameters).
+int launch_dgemm_nt_batch(const GemmOperands* ops, int nb, int M, int N, int K, long long c_stride, const GemmEpi& ep,
+                          cudaStream_t stream) {
     if (M <= 0 || N <= 0 || K <= 0) return arg_error("empty GEMM");
     if (ep.mode != EPI_STORE) return arg_error("batched GEMM: plain store epilogue only");
-    if (7 * tiles_of(M, N, 128, 128) > gemm_max_tiles()) return arg_error("batched GEMM: too many tiles");
-    return launch_tile_batch<BigTile, 7>(ops, M, N, K, c_stride, ep, stream);
+    if (nb != 7 && nb != 49) return arg_error("batched GEMM: 7 or 49 problems");
+    if ((long long)nb * tiles_of(M, N, 128, 128) > gemm_max_tiles()) return arg_error("batched GEMM: too many tiles");
+    return nb == 7 ? launch_tile_batch<BigTile, 7>(ops, M, N, K, c_stride, ep, stream)
+                   : launch_tile_batch<BigTile, 49>(ops, M, N, K, c_stride, ep, stream);
 }
 
 // Upper bound of the output tiles of any tile shape (one <C,D> partial each).

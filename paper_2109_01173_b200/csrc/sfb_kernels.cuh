@@ -52,8 +52,8 @@ struct GemmOperands {
     const double* Bt;
     int ldb;
 };
-int launch_dgemm_nt_batch7(const GemmOperands* ops, int M, int N, int K, long long c_stride, const GemmEpi& ep,
-                           cudaStream_t stream);
+int launch_dgemm_nt_batch(const GemmOperands* ops, int nb, int M, int N, int K, long long c_stride, const GemmEpi& ep,
+                          cudaStream_t stream);
 int gemm_grid_blocks(int M, int N);
 int gemm_smem_bytes();
 size_t gemm_workspace_doubles();

@@ -329,12 +329,33 @@ int build_strassen_plan(const double* A, int lda, int M, int K, int levels, Stra
     return SFB_OK;
 }
 
-// scratch of a product with `levels` levels on shapes up to h x h halves
+// scratch of a product with `levels` levels on shapes up to h x h halves:
+// five operand sums and seven products per node; the nodes of the last level
+// under one parent are live together (their 49 leaf products are one launch)
 size_t strassen_scratch_doubles(int qy, int qx, int levels) {
     size_t n = 0;
     int h = std::max(qy, qx) / 2;
-    for (int l = 0; l < levels; ++l, h /= 2) n += (size_t)12 * h * pad_ld(h);
+    for (int l = 0; l < levels; ++l, h /= 2) n += (size_t)(l > 0 && l == levels - 1 ? 84 : 12) * h * pad_ld(h);
     return n;
+}
+
+// The seven (A_i, B_i) of node `pl` applied to Bt (N x K): the variable
+// operand's sums go to Bs (one pass).
+int strassen_operands(const StrassenPlan* pl, const double* Bt, int ldb, int N, double* Bs, GemmOperands* ops,
+                      const PcgState* gate, cudaStream_t s) {
+    const int Nh = N / 2, Kh = pl->K / 2, ldk = pl->ldk;
+    const size_t sb = (size_t)Nh * ldk;
+    SFB_TRY(launch_strassen_sums(Bt, ldb, Nh, Kh, Bs, ldk, sb, 1, gate, s));
+    // right operands: (B11 + B22), B11, (B12 - B22), (B21 - B11), B22, (B11 + B12), (B21 + B22)
+    const double* B22 = Bt + (size_t)Nh * ldb + Kh;
+    const GemmOperands b[7] = {{nullptr, 0, Bs, ldk},          {nullptr, 0, Bt, ldb},  {nullptr, 0, Bs + sb, ldk},
+                               {nullptr, 0, Bs + 2 * sb, ldk}, {nullptr, 0, B22, ldb}, {nullptr, 0, Bs + 3 * sb, ldk},
+                               {nullptr, 0, Bs + 4 * sb, ldk}};
+    for (int i = 0; i < 7; ++i) {
+        ops[i] = b[i];
+        pl->operand(i, &ops[i].A, &ops[i].lda);
+    }
+    return SFB_OK;
 }
 
 // C[M x N] = A[M x K] Bt[N x K]^T with A described by `pl`.
@@ -347,20 +368,30 @@ int strassen_apply(const StrassenPlan* pl, const double* Bt, int ldb, int N, dou
     double* Bs = scratch;
     double* Mp = scratch + 5 * sb;
     double* rest = Mp + 7 * sm;
-    SFB_TRY(launch_strassen_sums(Bt, ldb, Nh, Kh, Bs, ldk, sb, 1, pcg, s));
-    // right operands: (B11 + B22), B11, (B12 - B22), (B21 - B11), B22, (B11 + B12), (B21 + B22)
-    const double* B22 = Bt + (size_t)Nh * ldb + Kh;
-    GemmOperands ops[7] = {{nullptr, 0, Bs, ldk},          {nullptr, 0, Bt, ldb},          {nullptr, 0, Bs + sb, ldk},
-                           {nullptr, 0, Bs + 2 * sb, ldk}, {nullptr, 0, B22, ldb},         {nullptr, 0, Bs + 3 * sb, ldk},
-                           {nullptr, 0, Bs + 4 * sb, ldk}};
-    for (int i = 0; i < 7; ++i) pl->operand(i, &ops[i].A, &ops[i].lda);
+    GemmOperands ops[7];
+    SFB_TRY(strassen_operands(pl, Bt, ldb, N, Bs, ops, pcg, s));
+    GemmEpi e;
+    e.mode = EPI_STORE;
+    e.ldc = ldn;
+    e.pcg = pcg;
     if (pl->sub[0] == nullptr) {
-        GemmEpi e;
-        e.mode = EPI_STORE;
         e.C = Mp;
-        e.ldc = ldn;
-        e.pcg = pcg;
-        SFB_TRY(launch_dgemm_nt_batch7(ops, Mh, Nh, Kh, (long long)sm, with_ws(e, gw), s));
+        SFB_TRY(launch_dgemm_nt_batch(ops, 7, Mh, Nh, Kh, (long long)sm, with_ws(e, gw), s));
+    } else if (pl->sub[0]->sub[0] == nullptr) {
+        // the children are last-level nodes: their 49 leaf products in one launch
+        const int Mq = Mh / 2, Nq = Nh / 2, Kq = Kh / 2, ldq = pad_ld(Nq);
+        const size_t sb2 = (size_t)Nq * pl->sub[0]->ldk, sm2 = (size_t)Mq * ldq;
+        double* Bs2 = rest;
+        double* Mp2 = rest + 35 * sb2;
+        GemmOperands all[49];
+        for (int i = 0; i < 7; ++i)
+            SFB_TRY(strassen_operands(pl->sub[i], ops[i].Bt, ops[i].ldb, Nh, Bs2 + 5 * i * sb2, all + 7 * i, pcg, s));
+        e.C = Mp2;
+        e.ldc = ldq;
+        SFB_TRY(launch_dgemm_nt_batch(all, 49, Mq, Nq, Kq, (long long)sm2, with_ws(e, gw), s));
+        for (int i = 0; i < 7; ++i)
+            SFB_TRY(launch_strassen_combine(Mp2 + 7 * i * sm2, ldq, sm2, Mq, Nq, Mp + i * sm, ldn, nullptr, 0, nullptr,
+                                            pcg, nullptr, nullptr, s));
     } else {
         for (int i = 0; i < 7; ++i)
             SFB_TRY(strassen_apply(pl->sub[i], ops[i].Bt, ops[i].ldb, Nh, rest, Mp + i * sm, ldn, nullptr, 0, nullptr,
@@ -1512,12 +1543,13 @@ int sfb_dgemm_nt(const double* A, int lda, const double* Bt, int ldb, int M, int
     return launch_dgemm_nt(A, lda, Bt, ldb, M, N, K, with_ws(e, &gw), s);
 }
 
-int sfb_dgemm_nt_batch7(const double* const* A, const int* lda, const double* const* Bt, const int* ldb, int M, int N,
-                        int K, double* C, int ldc, long long c_stride, void* stream) {
-    SFB_NVTX("sfb_dgemm_nt_batch7");
+int sfb_dgemm_nt_batch(int nb, const double* const* A, const int* lda, const double* const* Bt, const int* ldb, int M,
+                       int N, int K, double* C, int ldc, long long c_stride, void* stream) {
+    SFB_NVTX("sfb_dgemm_nt_batch");
     if (!A || !lda || !Bt || !ldb || !C) return arg_error("batched GEMM: null argument");
-    GemmOperands ops[7];
-    for (int b = 0; b < 7; ++b) ops[b] = GemmOperands{A[b], lda[b], Bt[b], ldb[b]};
+    if (nb != 7 && nb != 49) return arg_error("batched GEMM: 7 or 49 problems");
+    GemmOperands ops[49];
+    for (int b = 0; b < nb; ++b) ops[b] = GemmOperands{A[b], lda[b], Bt[b], ldb[b]};
     GemmEpi e;
     e.mode = EPI_STORE;
     e.C = C;
@@ -1526,7 +1558,7 @@ int sfb_dgemm_nt_batch7(const double* const* A, const int* lda, const double* co
     ScopedFree tmp(s);
     GemmWs gw;
     SFB_TRY(temp_ws(tmp, gw, s));
-    return launch_dgemm_nt_batch7(ops, M, N, K, c_stride, with_ws(e, &gw), s);
+    return launch_dgemm_nt_batch(ops, nb, M, N, K, c_stride, with_ws(e, &gw), s);
 }
 
 int sfb_dgemm_nt_scatter(const double* A, int lda, const double* Bt, int ldb, int M, int N, int K, int nseg,

@@ -93,10 +93,11 @@ def test_strassen_mo_pcg_iterates_vs_oracle(d, tau, strassen_from_256):
     assert relerr(rep.solution, full["solution"]) <= 1e-9
 
 
+@pytest.mark.parametrize("nb", [7, 49])
 @pytest.mark.parametrize("M,N,K", [(256, 256, 256), (384, 256, 512), (130, 258, 100)])
-def test_batched_gemm_matches_fp64_matmul(M, N, K):
-    """sfb_dgemm_nt_batch7: seven products in one persistent launch (operands with
-    different leading dimensions, as the Strassen level passes block views and sums)."""
+def test_batched_gemm_matches_fp64_matmul(M, N, K, nb):
+    """sfb_dgemm_nt_batch: 7 or 49 products in one persistent launch (operands with
+    different leading dimensions, as the Strassen levels pass block views and sums)."""
     import ctypes as C
 
     import torch
@@ -105,17 +106,18 @@ def test_batched_gemm_matches_fp64_matmul(M, N, K):
 
     g = torch.Generator(device="cuda").manual_seed(M + N + K)
     ldc = N + (N % 2)
-    As = [torch.randn(M, K + 2 * (b % 3), dtype=torch.float64, device="cuda", generator=g) for b in range(7)]
-    Bs = [torch.randn(N, K + 4 * (b % 2), dtype=torch.float64, device="cuda", generator=g) for b in range(7)]
-    out = torch.zeros(7, M, ldc, dtype=torch.float64, device="cuda")
-    pa = (C.c_void_p * 7)(*[a.data_ptr() for a in As])
-    pb_ = (C.c_void_p * 7)(*[b.data_ptr() for b in Bs])
-    la = (C.c_int * 7)(*[a.shape[1] for a in As])
-    lb = (C.c_int * 7)(*[b.shape[1] for b in Bs])
-    nat.check(nat.lib().sfb_dgemm_nt_batch7(pa, la, pb_, lb, M, N, K, out.data_ptr(), ldc, M * ldc, nat.stream()),
+    As = [torch.randn(M, K + 2 * (b % 3), dtype=torch.float64, device="cuda", generator=g) for b in range(nb)]
+    Bs = [torch.randn(N, K + 4 * (b % 2), dtype=torch.float64, device="cuda", generator=g) for b in range(nb)]
+    out = torch.zeros(nb, M, ldc, dtype=torch.float64, device="cuda")
+    pa = (C.c_void_p * nb)(*[a.data_ptr() for a in As])
+    pb_ = (C.c_void_p * nb)(*[b.data_ptr() for b in Bs])
+    la = (C.c_int * nb)(*[a.shape[1] for a in As])
+    lb = (C.c_int * nb)(*[b.shape[1] for b in Bs])
+    nat.check(nat.lib().sfb_dgemm_nt_batch(nb, pa, la, pb_, lb, M, N, K, out.data_ptr(), ldc, M * ldc, nat.stream()),
               "batched GEMM")
     torch.cuda.synchronize()
-    for b in range(7):
+    for b in range(nb):
         ref = As[b][:, :K] @ Bs[b][:, :K].T
         assert float((out[b, :, :N] - ref).norm() / ref.norm()) <= 1e-14
-    assert float(out[:, :, N:].abs().max()) == 0.0 if ldc > N else True
+    if ldc > N:
+        assert float(out[:, :, N:].abs().max()) == 0.0
