@@ -346,27 +346,24 @@ def gemm_roofline(q: int, levels: int = 0):
     if levels > 0:
         # the dominant kernel of the Strassen schedule: one batched launch of the
         # seven leaf products (its own flops, not the algorithmic 2 q^3)
-        import ctypes as C
         h = q >> levels
-        nb = 7 if levels == 1 else 49  # the last two levels share one launch
-        A = [torch.randn(h, h, dtype=torch.float64, device="cuda") for _ in range(nb)]
-        B = [torch.randn(h, h, dtype=torch.float64, device="cuda") for _ in range(nb)]
+        nb = 7 ** levels  # all leaf products of a preconditioner product are one strided-batch launch
+        A = torch.randn(nb, h, h, dtype=torch.float64, device="cuda")
+        B = torch.randn(nb, h, h, dtype=torch.float64, device="cuda")
         out = torch.empty(nb, h, h, dtype=torch.float64, device="cuda")
-        pa = (C.c_void_p * nb)(*[a.data_ptr() for a in A])
-        pb_ = (C.c_void_p * nb)(*[b.data_ptr() for b in B])
-        ldn = (C.c_int * nb)(*([h] * nb))
 
         def leaf():
-            nat.check(L.sfb_dgemm_nt_batch(nb, pa, ldn, pb_, ldn, h, h, h, out.data_ptr(), h, h * h, s.cuda_stream))
+            nat.check(L.sfb_dgemm_nt_batch(nb, A.data_ptr(), h, B.data_ptr(), h, h, h, h, out.data_ptr(), h, h * h,
+                                           s.cuda_stream))
 
-        t_leaf = timed(leaf, 20)
+        t_leaf = timed(leaf, 10)
         tfl = 2.0 * nb * h ** 3 / t_leaf / 1e12
         roof = {"bound": "tensor",
-                "kernel": f"dgemm_nt batched ({nb} x {h}^3 per launch: leaf products of {levels} Strassen levels; "
-                          f"DMMA.8x8x4 + TMA, hybrid data-parallel + stream-K)",
+                "kernel": f"dgemm_nt strided batch ({nb} x {h}^3 per launch: the leaf products of {levels} Strassen "
+                          f"levels; DMMA.8x8x4 + rank-3 TMA maps, hybrid data-parallel + stream-K)",
                 "achieved": tfl, "peak": peak, "unit": "TFLOP/s", "frac": tfl / peak,
                 "flops_per_launch": 2.0 * nb * h ** 3, "launch_ms": t_leaf * 1e3,
-                "launches_per_product": 7 ** levels // nb,
+                "launches_per_product": 1,
                 "peak_source": "cuBLAS DGEMM 8192^3 measured in this run",
                 "classic_gemm": {"kernel": "dgemm_nt, one q^3 product per launch", "achieved": tf, "frac": tf / peak,
                                  "launch_ms": t_gemm * 1e3, "flops_per_launch": 2.0 * q ** 3,
@@ -619,7 +616,7 @@ def run_cfg5(args):
     roof = gemm_roofline(qy, levels)
     n_gemm = 2 if args.precond_mode == "inverse" else (4 if args.precond_mode == "spectral" else 0)
     n_launch = n_gemm * roof.get("launches_per_product", 1)  # dominant-kernel launches per iteration
-    tkey = f"q{qy >> levels}x{7 if levels == 1 else 49}" if levels > 0 else f"q{qy}"
+    tkey = f"q{qy >> levels}x{7 ** levels}" if levels > 0 else f"q{qy}"
     roof.update({"share_of_iteration": n_launch * roof["launch_ms"] / iter_ms if n_gemm else 0.0,
                  "iteration_ms": iter_ms,
                  "traffic": (profile_json("ncu_dgemm_r02.json").get(tkey) or {}).get("dram_bytes_per_launch")})
@@ -629,8 +626,8 @@ def run_cfg5(args):
             "ms": hbm["preconditioner_ms"], "algorithmic_flops": 4.0 * qy ** 3,
             "algorithmic_tflops": 4.0 * qy ** 3 / (hbm["preconditioner_ms"] * 1e-3) / 1e12,
             "executed_flops": 4.0 * qy ** 3 * (7.0 / 8.0) ** levels,
-            "note": f"{levels} Strassen levels: per product {(7 ** levels - 1) // 6} operand-sum passes, "
-                    f"{roof['launches_per_product']} batched leaf launches, {(7 ** levels - 1) // 6} assembly passes"}
+            "note": f"{levels} Strassen levels: per product one pass forming the {7 ** levels} leaf operands of the "
+                    f"variable factor, one strided-batch launch of the leaf products, one assembly pass"}
     if args.precond_mode == "banded":
         bp = hbm["banded_operator_pass"]
         roof = {"bound": "hbm", "kernel": bp["kernel"], "achieved": bp["achieved"], "peak": hbm["peak"],
@@ -654,8 +651,8 @@ def run_cfg5(args):
     # first preconditioner (n_pre), K x (banded pass + R update + preconditioner),
     # deferred U update (1), increment norms (1)
     n_pre = n_gemm if n_gemm else 5
-    if levels > 0:  # per product: sums + batched leaves + assemblies
-        n_pre = 2 * (2 * ((7 ** levels - 1) // 6) + roof["launches_per_product"])
+    if levels > 0:
+        n_pre = 2 * 3  # per product: leaf operands, leaf products, assembly
     per_species = 4 + n_pre + K * (2 + n_pre) + 1
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

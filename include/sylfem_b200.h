@@ -164,15 +164,17 @@ int sfb_pre_create(int qy, int qx, int kind, const double* L,
                    const double* R, const double* lamL_host,
                    const double* lamR_host, sfb_pre** out);
 /* The inverse-form products Z = P_L^-1 (R P_R^-1) of shapes with q_y, q_x >=
- * min_q and divisible by 4 run as one level of Strassen around the DMMA GEMM
- * (7 half-size products per level, the constant operands' block sums formed at
- * creation); it replaces the same two dense solves of Preconditioner.apply_inverse
- * (solvers.py:134-143).  Applies to preconditioners created afterwards; 0 =
- * never (default: SYLFEM_B200_STRASSEN_MINQ or 6144).  Returns the previous
- * threshold. */
+ * min_q run as up to three levels of Strassen around the DMMA GEMM (every
+ * level's dimensions divisible by 4): one pass forms the 7^L leaf operands of
+ * the variable factor (those of the constant factors are formed at creation),
+ * one strided-batch DMMA launch does the 7^L leaf products, one pass
+ * assembles Z (and <Z,R>).  Same value as the two dense solves of
+ * Preconditioner.apply_inverse (solvers.py:134-143), other summation order.
+ * Applies to preconditioners created afterwards; 0 = never (default:
+ * SYLFEM_B200_STRASSEN_MINQ or 4096).  Returns the previous threshold. */
 int sfb_set_strassen_min_q(int min_q);
 /* Most Strassen levels taken (0..3, default SYLFEM_B200_STRASSEN_LEVELS or 3);
- * a level needs dimensions divisible by 4 and halves of at least min_q / 6.
+ * a level needs dimensions divisible by 4 and halves of at least min_q / 8.
  * Returns the previous value. */
 int sfb_set_strassen_levels(int levels);
 /* Strassen levels this preconditioner's products use (0: classic GEMMs). */
@@ -258,14 +260,13 @@ int sfb_imex_rds_run(sfb_pcg* solver_u, sfb_pcg* solver_v, const sfb_map* rhs_ma
 int sfb_dgemm_nt(const double* A_dev, int lda, const double* Bt_dev, int ldb,
                  int M, int N, int K, double* C_dev, int ldc, void* stream);
 
-/* nb = 7 or 49 independent products of one shape in one persistent launch
- * (128 x 128 tiles, one wave schedule and stream-K tail for the whole batch):
- * C_b = A_b Bt_b^T at C_dev + b * c_stride -- the leaf products of one Strassen
- * node, or of a node's seven children, of the inverse-form preconditioner
- * (solvers.py:134-143).  A_host/Bt_host: host arrays of nb device pointers,
- * lda_host/ldb_host of nb ints. */
-int sfb_dgemm_nt_batch(int nb, const double* const* A_host, const int* lda_host,
-                       const double* const* Bt_host, const int* ldb_host,
+/* A strided batch of nb independent products of one shape in one persistent
+ * launch (128 x 128 tiles, one wave schedule and stream-K tail for the whole
+ * batch; rank-3 tensor maps): C_b = A_b Bt_b^T with A_b = A_dev + b * M * lda,
+ * Bt_b = Bt_dev + b * N * ldb, C_b = C_dev + b * c_stride -- the leaf products
+ * of the Strassen schedule of the inverse-form preconditioner
+ * (solvers.py:134-143).  nb * ceil(M/128) * ceil(N/128) <= 65536. */
+int sfb_dgemm_nt_batch(int nb, const double* A_dev, int lda, const double* Bt_dev, int ldb,
                        int M, int N, int K, double* C_dev, int ldc, long long c_stride,
                        void* stream);
 

@@ -101,7 +101,7 @@ _SIGS = {
     "sfb_diff_norm": (_I, [_P, _I, _P, _I, _I, _I, _DP, _P]),
     "sfb_pcg_shape": (_I, [_P, C.POINTER(_I), C.POINTER(_I)]),
     "sfb_dgemm_nt_scatter": (_I, [_P, _I, _P, _I, _I, _I, _I, _I, _P, _P, _P, _I, _P]),
-    "sfb_dgemm_nt_batch": (_I, [_I, _P, _P, _P, _P, _I, _I, _I, _P, _I, C.c_longlong, _P]),
+    "sfb_dgemm_nt_batch": (_I, [_I, _P, _I, _P, _I, _I, _I, _I, _P, _I, C.c_longlong, _P]),
     "sfb_copy2d": (_I, [_P, _I, _P, _I, _I, _I, _P]),
     "sfb_ipc_get_handle": (_I, [_P, _P, C.POINTER(C.c_ulonglong)]),
     "sfb_ipc_open": (_I, [_P, C.c_ulonglong, C.POINTER(_P), C.POINTER(_P)]),

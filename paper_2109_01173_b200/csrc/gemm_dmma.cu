@@ -215,18 +215,19 @@ __device__ __forceinline__ double tile_epilogue(double (&acc)[T::MI][T::NJ][2], 
 // deadlock-free however many kernels share the GPU.  <C,D> partials are per
 // tile, so every sum is independent of who finished.  With ws == nullptr
 // every CTA owns whole tiles (grid = tile count).
-// NB > 1: a batch of NB independent problems of one shape in one persistent
-// launch (plain store epilogue; the seven half-size products of a Strassen
-// level): tile / tiles_per selects the problem's tensor maps and output, so
-// the whole batch shares one wave schedule and one stream-K tail.
-template <int NB>
+// BATCH: a strided batch of independent problems of one shape in one
+// persistent launch (plain store epilogue; the leaf products of the Strassen
+// schedule): the operands are stacks of matrices behind rank-3 tensor maps,
+// tile / tiles_per is the problem (the maps' third coordinate, and the
+// output's offset), so the whole batch shares one wave schedule and one
+// stream-K tail.
 struct GemmMaps {
-    CUtensorMap a[NB], b[NB];
+    CUtensorMap a, b;
 };
 
-template <class T, int NB>
+template <class T, bool BATCH>
 __global__ void __launch_bounds__(T::NTHREADS, T::CTAS_PER_SM)
-    dgemm_nt_kernel(const __grid_constant__ GemmMaps<NB> maps, int M, int N, int K, GemmEpi ep, Sched sc) {
+    dgemm_nt_kernel(const __grid_constant__ GemmMaps maps, int M, int N, int K, GemmEpi ep, Sched sc) {
     constexpr int BM = T::BM, BN = T::BN, NWARPS = T::NWARPS, NTHREADS = T::NTHREADS;
     constexpr int BK = T::BK, STAGES = T::STAGES, LOOKAHEAD = T::LOOKAHEAD;
     constexpr int A_BYTES = T::A_BYTES, B_BYTES = T::B_BYTES;
@@ -263,16 +264,20 @@ __global__ void __launch_bounds__(T::NTHREADS, T::CTAS_PER_SM)
         int tile, kt;
         locate(it, tile, kt);
         int m0, n0;
-        const int prob = NB > 1 ? tile / sc.tiles_per : 0;
-        sc.origin(NB > 1 ? tile - prob * sc.tiles_per : tile, BM, BN, m0, n0);
-        const CUtensorMap* tmA = &maps.a[prob];
-        const CUtensorMap* tmB = &maps.b[prob];
+        const int prob = BATCH ? tile / sc.tiles_per : 0;
+        sc.origin(BATCH ? tile - prob * sc.tiles_per : tile, BM, BN, m0, n0);
         const int sl = it % STAGES;
         mbar_expect_tx_u32(full + 8 * sl, A_BYTES + B_BYTES);
         #pragma unroll
         for (int kb = 0; kb < BK / KBOX; ++kb) {
-            tma_load_u32(sA + sl * A_BYTES + kb * BM * KBOX * 8, tmA, full + 8 * sl, kt * BK + kb * KBOX, m0);
-            tma_load_u32(sB + sl * B_BYTES + kb * BN * KBOX * 8, tmB, full + 8 * sl, kt * BK + kb * KBOX, n0);
+            const uint32_t da = sA + sl * A_BYTES + kb * BM * KBOX * 8, db = sB + sl * B_BYTES + kb * BN * KBOX * 8;
+            if constexpr (BATCH) {
+                tma_load3_u32(da, &maps.a, full + 8 * sl, kt * BK + kb * KBOX, m0, prob);
+                tma_load3_u32(db, &maps.b, full + 8 * sl, kt * BK + kb * KBOX, n0, prob);
+            } else {
+                tma_load_u32(da, &maps.a, full + 8 * sl, kt * BK + kb * KBOX, m0);
+                tma_load_u32(db, &maps.b, full + 8 * sl, kt * BK + kb * KBOX, n0);
+            }
         }
     };
 
@@ -282,10 +287,8 @@ __global__ void __launch_bounds__(T::NTHREADS, T::CTAS_PER_SM)
             mbar_init_u32(empty + 8 * s, NWARPS);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        for (int b = 0; b < NB; ++b) {
-            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.a[b])) : "memory");
-            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.b[b])) : "memory");
-        }
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.a)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.b)) : "memory");
         for (int it = 0; it < LOOKAHEAD && it < n_it; ++it) issue(it);
     }
     __syncthreads();
@@ -344,8 +347,8 @@ __global__ void __launch_bounds__(T::NTHREADS, T::CTAS_PER_SM)
         }
 
         int m0, n0;
-        const int prob = NB > 1 ? tile / sc.tiles_per : 0;
-        sc.origin(NB > 1 ? tile - prob * sc.tiles_per : tile, BM, BN, m0, n0);
+        const int prob = BATCH ? tile / sc.tiles_per : 0;
+        sc.origin(BATCH ? tile - prob * sc.tiles_per : tile, BM, BN, m0, n0);
         bool finish = true;
         if (k0 != 0 || kl != KT - 1) {
             // split tile: the last piece to arrive finishes it (no CTA ever
@@ -414,7 +417,7 @@ __global__ void __launch_bounds__(T::NTHREADS, T::CTAS_PER_SM)
         }
         if (finish) {
             const double d = tile_epilogue<T>(acc, ep, M, N, m0, n0, wm, wn, g, t,
-                                              NB > 1 ? (size_t)prob * (size_t)sc.c_stride : 0);
+                                              BATCH ? (size_t)prob * (size_t)sc.c_stride : 0);
             if (ep.mode == EPI_STORE_DOT) {  // one partial per tile: the sum order does not depend on who finished
                 const double part = block_sum<NTHREADS>(d, sh_dot);
                 if (threadIdx.x == 0) ep.partials[tile] = part;
@@ -455,15 +458,27 @@ int tile_mode() {
     return m;
 }
 
-template <class T, int NB>
-int launch_tile_batch(const GemmOperands* ops, int M, int N, int K, long long c_stride, const GemmEpi& ep,
-                      cudaStream_t stream) {
-    SFB_TRY(ensure_dynamic_smem(dgemm_nt_kernel<T, NB>, T::SMEM_BYTES));
-    GemmMaps<NB> maps;
-    for (int b = 0; b < NB; ++b) {
-        SFB_TRY(make_map(&maps.a[b], ops[b].A, M, K, ops[b].lda, T::BM));
-        SFB_TRY(make_map(&maps.b[b], ops[b].Bt, N, K, ops[b].ldb, T::BN));
+int make_map3(CUtensorMap* map, const double* ptr, int rows, int cols, int ld, int box_rows, int nb) {
+    if (!tma_aligned(ptr, ld)) return arg_error("DMMA GEMM operands need 16-byte aligned rows (even leading dimension)");
+    const cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)rows, (cuuint64_t)nb};
+    const cuuint32_t box[3] = {KBOX, (cuuint32_t)box_rows, 1};
+    return tma_make_map(map, ptr, 3, dims, ld, box, CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
+// nb > 0: strided batch (A: nb stacked M x lda matrices, Bt: nb stacked N x ldb, C_b = ep.C + b * c_stride)
+template <class T, bool BATCH>
+int launch_tile_batch(const double* A, int lda, const double* Bt, int ldb, int nb, int M, int N, int K,
+                      long long c_stride, const GemmEpi& ep, cudaStream_t stream) {
+    SFB_TRY(ensure_dynamic_smem(dgemm_nt_kernel<T, BATCH>, T::SMEM_BYTES));
+    GemmMaps maps;
+    if (BATCH) {
+        SFB_TRY(make_map3(&maps.a, A, M, K, lda, T::BM, nb));
+        SFB_TRY(make_map3(&maps.b, Bt, N, K, ldb, T::BN, nb));
+    } else {
+        SFB_TRY(make_map(&maps.a, A, M, K, lda, T::BM));
+        SFB_TRY(make_map(&maps.b, Bt, N, K, ldb, T::BN));
     }
+    const int NB = BATCH ? nb : 1;
     Sched sc;
     sc.tiles_n = (N + T::BN - 1) / T::BN;
     sc.KT = (K + T::BK - 1) / T::BK;
@@ -491,15 +506,14 @@ int launch_tile_batch(const GemmOperands* ops, int M, int N, int K, long long c_
         sc.U = (long long)tiles * sc.KT;
         sc.G = (int)std::max(1LL, std::min<long long>(slots, sc.U / min_work));
     }
-    return launch_kernel(dgemm_nt_kernel<T, NB>, dim3(sc.G), dim3(T::NTHREADS), T::SMEM_BYTES, stream, maps, M, N, K,
-                         ep, sc);
+    return launch_kernel(dgemm_nt_kernel<T, BATCH>, dim3(sc.G), dim3(T::NTHREADS), T::SMEM_BYTES, stream, maps, M, N,
+                         K, ep, sc);
 }
 
 template <class T>
 int launch_tile(const double* A, int lda, const double* Bt, int ldb, int M, int N, int K, const GemmEpi& ep,
                 cudaStream_t stream) {
-    const GemmOperands op{A, lda, Bt, ldb};
-    return launch_tile_batch<T, 1>(&op, M, N, K, 0, ep, stream);
+    return launch_tile_batch<T, false>(A, lda, Bt, ldb, 1, M, N, K, 0, ep, stream);
 }
 
 }  // namespace
@@ -531,18 +545,17 @@ int launch_dgemm_nt(const double* A, int lda, const double* Bt, int ldb, int M, 
                  : launch_tile<BigTile>(A, lda, Bt, ldb, M, N, K, ep, stream);
 }
 
-// nb = 7 or 49 independent products C_b[M x N] = A_b Bt_b^T of one shape in one
-// launch (128 x 128 tiles, plain store; C_b = ep.C + b * c_stride): the leaf
-// products of one Strassen node, or of its seven children together (98 tensor
-// maps = 12.5 KB of kernel parameters).
-int launch_dgemm_nt_batch(const GemmOperands* ops, int nb, int M, int N, int K, long long c_stride, const GemmEpi& ep,
-                          cudaStream_t stream) {
-    if (M <= 0 || N <= 0 || K <= 0) return arg_error("empty GEMM");
+// nb independent products C_b[M x N] = A_b Bt_b^T of one shape in one launch
+// (128 x 128 tiles, plain store): A_b = A + b * M * lda, Bt_b = Bt + b * N * ldb
+// (stacked matrices behind rank-3 tensor maps), C_b = ep.C + b * c_stride.
+int gemm_batch_max(int M, int N) { return gemm_max_tiles() / tiles_of(M, N, 128, 128); }
+
+int launch_dgemm_nt_batch(const double* A, int lda, const double* Bt, int ldb, int nb, int M, int N, int K,
+                          long long c_stride, const GemmEpi& ep, cudaStream_t stream) {
+    if (M <= 0 || N <= 0 || K <= 0 || nb <= 0) return arg_error("empty GEMM");
     if (ep.mode != EPI_STORE) return arg_error("batched GEMM: plain store epilogue only");
-    if (nb != 7 && nb != 49) return arg_error("batched GEMM: 7 or 49 problems");
-    if ((long long)nb * tiles_of(M, N, 128, 128) > gemm_max_tiles()) return arg_error("batched GEMM: too many tiles");
-    return nb == 7 ? launch_tile_batch<BigTile, 7>(ops, M, N, K, c_stride, ep, stream)
-                   : launch_tile_batch<BigTile, 49>(ops, M, N, K, c_stride, ep, stream);
+    if (nb > gemm_batch_max(M, N)) return arg_error("batched GEMM: too many tiles for one launch");
+    return launch_tile_batch<BigTile, true>(A, lda, Bt, ldb, nb, M, N, K, c_stride, ep, stream);
 }
 
 // Upper bound of the output tiles of any tile shape (one <C,D> partial each).

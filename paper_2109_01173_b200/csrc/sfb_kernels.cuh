@@ -46,14 +46,10 @@ struct GemmEpi {
 
 int launch_dgemm_nt(const double* A, int lda, const double* Bt, int ldb, int M, int N, int K,
                     const GemmEpi& ep, cudaStream_t stream);
-struct GemmOperands {
-    const double* A;
-    int lda;
-    const double* Bt;
-    int ldb;
-};
-int launch_dgemm_nt_batch(const GemmOperands* ops, int nb, int M, int N, int K, long long c_stride, const GemmEpi& ep,
-                          cudaStream_t stream);
+// strided batch of nb products of one shape in one persistent launch (plain store)
+int launch_dgemm_nt_batch(const double* A, int lda, const double* Bt, int ldb, int nb, int M, int N, int K,
+                          long long c_stride, const GemmEpi& ep, cudaStream_t stream);
+int gemm_batch_max(int M, int N);  // most problems of this shape per launch
 int gemm_grid_blocks(int M, int N);
 int gemm_smem_bytes();
 size_t gemm_workspace_doubles();
@@ -132,14 +128,15 @@ int launch_loop_ctl(PcgState* st, unsigned long long handle, int use_handle, cud
 int launch_norms(const double* A, int lda, const double* B, int ldb, int rows, int cols, double* partials,
                  RedSlots* out, cudaStream_t s);
 int vector_grid_blocks();
-// one-level Strassen helpers (vector.cu): the five block sums of an operand
-// (side 0: A pattern, side 1: Bt pattern; X is 2rh x 2ch, outputs rh x ch at S + i * sstride)
-// and the assembly of C (2rh x 2ch) from the seven products at Mp + i * mstride, with <C,D> when D is set
-int launch_strassen_sums(const double* X, int ldx, int rh, int ch, double* S, int lds, size_t sstride, int side,
-                         const PcgState* gate, cudaStream_t s);
-int launch_strassen_combine(const double* Mp, int ldm, size_t mstride, int rh, int ch, double* C, int ldc,
-                            const double* D, int ldd, double* partials, PcgState* st, double* dot_out,
-                            unsigned* counter, cudaStream_t s);
+// Strassen schedule, `levels` levels flattened (vector.cu): all 7^levels leaf
+// operands of X ((rh 2^levels) x (ch 2^levels); side 0: left operand A, side 1:
+// right operand Bt) at S + l * sstride, and the assembly of C from the leaf
+// products at Mp + l * mstride, with <C,D> when D is set
+int launch_strassen_operands(int levels, int side, const double* X, int ldx, int rh, int ch, double* S, int lds,
+                             size_t sstride, const PcgState* gate, cudaStream_t s);
+int launch_strassen_assemble(int levels, const double* Mp, int ldm, size_t mstride, int rh, int ch, double* C, int ldc,
+                             const double* D, int ldd, double* partials, PcgState* st, double* dot_out,
+                             unsigned* counter, cudaStream_t s);
 int launch_transpose(const double* src, int lds, double* dst, int ldd, int rows, int cols, cudaStream_t s);
 int launch_sh_update(double* U, double* R, const double* Q, const double* W, int ld, int rows, int cols,
                      double alpha, double* partials, RedSlots* out, cudaStream_t s);

@@ -235,21 +235,21 @@ int op_apply_impl(const sfb_op* op, const double* U, int ldu, double* W, int ldw
 
 // ---- Strassen around the DMMA GEMM ---------------------------------------
 // The inverse-form preconditioner (solvers.py:103-143 as two dense products)
-// multiplies by the same two matrices every iteration, so the block sums of
-// the constant left operands are formed once, for every level
-// (StrassenPlan, built in sfb_pre_create).  Per product and level: one pass
-// for the variable operand's five sums, the seven half-size products (the
-// next level, or one batched DMMA launch) and one assembly pass.  Two levels
-// do 49/64 of the flops, three 343/512.  Used for shapes of at least
-// strassen_min_q() with every level's dimensions divisible by 4 and leaves of
-// at least a sixth of the threshold (SYLFEM_B200_STRASSEN_MINQ, default 6144,
-// 0 = never; SYLFEM_B200_STRASSEN_LEVELS, default 3: q = 8192 runs 1024^3
-// leaves, measured 49.6 ms per preconditioner application against 51.2 / 55.9
-// ms with two / one levels and 62.2 ms classic).
+// multiplies by the same two matrices every iteration, so the leaf operands
+// of the constant left factors are formed once (StrassenPlan, built in
+// sfb_pre_create).  Per product: one pass forms the variable operand's 7^L
+// leaf operands, one strided-batch DMMA launch does the 7^L leaf products,
+// one pass assembles the result (and <Z,R>).  Three levels do 343/512 of the
+// flops.  Used for shapes of at least strassen_min_q() with every level's
+// dimensions divisible by 4 and leaves of at least an eighth of the threshold
+// (SYLFEM_B200_STRASSEN_MINQ, default 4096, 0 = never;
+// SYLFEM_B200_STRASSEN_LEVELS, default 3: q = 8192 runs 343 leaves of 1024^3,
+// measured 45.5 ms per preconditioner application against 62.2 ms with one
+// 8192^3 DMMA GEMM per product; q = 4096: 6.3 against 8.0 ms).
 std::atomic<int>& strassen_min_q_slot() {
     static std::atomic<int> v([] {
         const char* e = std::getenv("SYLFEM_B200_STRASSEN_MINQ");
-        return e ? std::atoi(e) : 6144;
+        return e ? std::atoi(e) : 4096;
     }());
     return v;
 }
@@ -265,7 +265,7 @@ std::atomic<int>& strassen_max_levels_slot() {
 int strassen_levels_of(int q) {
     const int m = strassen_min_q();
     if (m <= 0 || q < m) return 0;
-    const int leaf = std::max(m / 6, 64);
+    const int leaf = std::max(m / 8, 64);
     int levels = 0;
     while (levels < strassen_max_levels_slot().load(std::memory_order_relaxed) && q % 4 == 0 && q / 2 >= leaf) {
         q /= 2;
@@ -275,52 +275,32 @@ int strassen_levels_of(int q) {
 }
 int strassen_levels(int qy, int qx) { return std::min(strassen_levels_of(qy), strassen_levels_of(qx)); }
 
-// A constant left operand (M x K), its five block sums and, below the last
-// level, the plans of its seven half-size operands.
+// The constant left operand of a product (M x K): its 7^levels leaf operands
+// ((M >> levels) x ldk each, stacked), formed once.
 struct StrassenPlan {
-    const double* A = nullptr;
-    int lda = 0, M = 0, K = 0, ldk = 0;
-    double* S = nullptr;  // (A11 + A22, A21 + A22, A11 + A12, A21 - A11, A12 - A22), (M/2) x ldk each
-    StrassenPlan* sub[7] = {};
-    // left operand of product i: (A11 + A22), (A21 + A22), A11, A22, (A11 + A12), (A21 - A11), (A12 - A22)
-    void operand(int i, const double** a, int* ld) const {
-        const size_t sa = (size_t)(M / 2) * ldk;
-        static const int sum_of[7] = {0, 1, -1, -2, 2, 3, 4};
-        if (sum_of[i] >= 0) {
-            *a = S + sum_of[i] * sa;
-            *ld = ldk;
-        } else {
-            *a = sum_of[i] == -1 ? A : A + (size_t)(M / 2) * lda + K / 2;
-            *ld = lda;
-        }
-    }
+    int levels = 0, M = 0, K = 0, ldk = 0, leaves = 0;
+    double* leaf = nullptr;
 };
 
 void free_strassen_plan(StrassenPlan* p) {
     if (!p) return;
-    for (auto* c : p->sub) free_strassen_plan(c);
-    cudaFree(p->S);
+    cudaFree(p->leaf);
     delete p;
 }
 
 int build_strassen_plan(const double* A, int lda, int M, int K, int levels, StrassenPlan** out) {
     auto* p = new StrassenPlan;
-    p->A = A;
-    p->lda = lda;
+    p->levels = levels;
     p->M = M;
     p->K = K;
-    p->ldk = pad_ld(K / 2);
-    const size_t n = (size_t)5 * (M / 2) * p->ldk;
-    int rc = dalloc(&p->S, n);
-    if (rc == SFB_OK && cudaMemset(p->S, 0, n * 8) != cudaSuccess) rc = SFB_ERR_CUDA;
-    if (rc == SFB_OK)
-        rc = launch_strassen_sums(A, lda, M / 2, K / 2, p->S, p->ldk, (size_t)(M / 2) * p->ldk, 0, nullptr, nullptr);
-    for (int i = 0; i < 7 && rc == SFB_OK && levels > 1; ++i) {
-        const double* a;
-        int ld;
-        p->operand(i, &a, &ld);
-        rc = build_strassen_plan(a, ld, M / 2, K / 2, levels - 1, &p->sub[i]);
-    }
+    p->leaves = 1;
+    for (int l = 0; l < levels; ++l) p->leaves *= 7;
+    const int mh = M >> levels, kh = K >> levels;
+    p->ldk = pad_ld(kh);
+    const size_t sa = (size_t)mh * p->ldk;
+    int rc = dalloc(&p->leaf, sa * p->leaves);
+    if (rc == SFB_OK && cudaMemset(p->leaf, 0, sa * p->leaves * 8) != cudaSuccess) rc = SFB_ERR_CUDA;
+    if (rc == SFB_OK) rc = launch_strassen_operands(levels, 0, A, lda, mh, kh, p->leaf, p->ldk, sa, nullptr, nullptr);
     if (rc != SFB_OK) {
         free_strassen_plan(p);
         return rc;
@@ -329,75 +309,38 @@ int build_strassen_plan(const double* A, int lda, int M, int K, int levels, Stra
     return SFB_OK;
 }
 
-// scratch of a product with `levels` levels on shapes up to h x h halves:
-// five operand sums and seven products per node; the nodes of the last level
-// under one parent are live together (their 49 leaf products are one launch)
+// scratch of a product: the variable operand's leaf operands and the leaf products
 size_t strassen_scratch_doubles(int qy, int qx, int levels) {
-    size_t n = 0;
-    int h = std::max(qy, qx) / 2;
-    for (int l = 0; l < levels; ++l, h /= 2) n += (size_t)(l > 0 && l == levels - 1 ? 84 : 12) * h * pad_ld(h);
-    return n;
+    const int h = std::max(qy, qx) >> levels;
+    size_t leaves = 1;
+    for (int l = 0; l < levels; ++l) leaves *= 7;
+    return 2 * leaves * (size_t)h * pad_ld(h);
 }
 
-// The seven (A_i, B_i) of node `pl` applied to Bt (N x K): the variable
-// operand's sums go to Bs (one pass).
-int strassen_operands(const StrassenPlan* pl, const double* Bt, int ldb, int N, double* Bs, GemmOperands* ops,
-                      const PcgState* gate, cudaStream_t s) {
-    const int Nh = N / 2, Kh = pl->K / 2, ldk = pl->ldk;
-    const size_t sb = (size_t)Nh * ldk;
-    SFB_TRY(launch_strassen_sums(Bt, ldb, Nh, Kh, Bs, ldk, sb, 1, gate, s));
-    // right operands: (B11 + B22), B11, (B12 - B22), (B21 - B11), B22, (B11 + B12), (B21 + B22)
-    const double* B22 = Bt + (size_t)Nh * ldb + Kh;
-    const GemmOperands b[7] = {{nullptr, 0, Bs, ldk},          {nullptr, 0, Bt, ldb},  {nullptr, 0, Bs + sb, ldk},
-                               {nullptr, 0, Bs + 2 * sb, ldk}, {nullptr, 0, B22, ldb}, {nullptr, 0, Bs + 3 * sb, ldk},
-                               {nullptr, 0, Bs + 4 * sb, ldk}};
-    for (int i = 0; i < 7; ++i) {
-        ops[i] = b[i];
-        pl->operand(i, &ops[i].A, &ops[i].lda);
-    }
-    return SFB_OK;
-}
-
-// C[M x N] = A[M x K] Bt[N x K]^T with A described by `pl`.
+// C[M x N] = A[M x K] Bt[N x K]^T with A's leaf operands in `pl`: one pass
+// for Bt's leaf operands, the leaf products as one strided-batch DMMA launch
+// (split only when they exceed the stream-K ticket array), one assembly pass.
 int strassen_apply(const StrassenPlan* pl, const double* Bt, int ldb, int N, double* scratch, double* C, int ldc,
                    const double* D, int ldd, double* partials, PcgState* pcg, double* dot_out, unsigned* counter,
                    const GemmWs* gw, cudaStream_t s) {
-    const int Mh = pl->M / 2, Nh = N / 2, Kh = pl->K / 2;
-    const int ldk = pl->ldk, ldn = pad_ld(Nh);
-    const size_t sb = (size_t)Nh * ldk, sm = (size_t)Mh * ldn;
-    double* Bs = scratch;
-    double* Mp = scratch + 5 * sb;
-    double* rest = Mp + 7 * sm;
-    GemmOperands ops[7];
-    SFB_TRY(strassen_operands(pl, Bt, ldb, N, Bs, ops, pcg, s));
+    const int L = pl->levels, mh = pl->M >> L, nh = N >> L, kh = pl->K >> L;
+    const int ldk = pl->ldk, ldn = pad_ld(nh);
+    const size_t sa = (size_t)mh * ldk, sb = (size_t)nh * ldk, sm = (size_t)mh * ldn;
+    double* Bl = scratch;
+    double* Mp = scratch + (size_t)pl->leaves * sb;
+    SFB_TRY(launch_strassen_operands(L, 1, Bt, ldb, nh, kh, Bl, ldk, sb, pcg, s));
     GemmEpi e;
     e.mode = EPI_STORE;
     e.ldc = ldn;
     e.pcg = pcg;
-    if (pl->sub[0] == nullptr) {
-        e.C = Mp;
-        SFB_TRY(launch_dgemm_nt_batch(ops, 7, Mh, Nh, Kh, (long long)sm, with_ws(e, gw), s));
-    } else if (pl->sub[0]->sub[0] == nullptr) {
-        // the children are last-level nodes: their 49 leaf products in one launch
-        const int Mq = Mh / 2, Nq = Nh / 2, Kq = Kh / 2, ldq = pad_ld(Nq);
-        const size_t sb2 = (size_t)Nq * pl->sub[0]->ldk, sm2 = (size_t)Mq * ldq;
-        double* Bs2 = rest;
-        double* Mp2 = rest + 35 * sb2;
-        GemmOperands all[49];
-        for (int i = 0; i < 7; ++i)
-            SFB_TRY(strassen_operands(pl->sub[i], ops[i].Bt, ops[i].ldb, Nh, Bs2 + 5 * i * sb2, all + 7 * i, pcg, s));
-        e.C = Mp2;
-        e.ldc = ldq;
-        SFB_TRY(launch_dgemm_nt_batch(all, 49, Mq, Nq, Kq, (long long)sm2, with_ws(e, gw), s));
-        for (int i = 0; i < 7; ++i)
-            SFB_TRY(launch_strassen_combine(Mp2 + 7 * i * sm2, ldq, sm2, Mq, Nq, Mp + i * sm, ldn, nullptr, 0, nullptr,
-                                            pcg, nullptr, nullptr, s));
-    } else {
-        for (int i = 0; i < 7; ++i)
-            SFB_TRY(strassen_apply(pl->sub[i], ops[i].Bt, ops[i].ldb, Nh, rest, Mp + i * sm, ldn, nullptr, 0, nullptr,
-                                   pcg, nullptr, nullptr, gw, s));
+    const int per = std::max(1, gemm_batch_max(mh, nh));
+    for (int l0 = 0; l0 < pl->leaves; l0 += per) {
+        const int nb = std::min(per, pl->leaves - l0);
+        e.C = Mp + (size_t)l0 * sm;
+        SFB_TRY(launch_dgemm_nt_batch(pl->leaf + (size_t)l0 * sa, ldk, Bl + (size_t)l0 * sb, ldk, nb, mh, nh, kh,
+                                      (long long)sm, with_ws(e, gw), s));
     }
-    return launch_strassen_combine(Mp, ldn, sm, Mh, Nh, C, ldc, D, ldd, partials, pcg, dot_out, counter, s);
+    return launch_strassen_assemble(L, Mp, ldn, sm, mh, nh, C, ldc, D, ldd, partials, pcg, dot_out, counter, s);
 }
 
 // Z = P^-1 R (or the reduced-solve sandwich).  R/Z device buffers with even
@@ -1543,13 +1486,10 @@ int sfb_dgemm_nt(const double* A, int lda, const double* Bt, int ldb, int M, int
     return launch_dgemm_nt(A, lda, Bt, ldb, M, N, K, with_ws(e, &gw), s);
 }
 
-int sfb_dgemm_nt_batch(int nb, const double* const* A, const int* lda, const double* const* Bt, const int* ldb, int M,
-                       int N, int K, double* C, int ldc, long long c_stride, void* stream) {
+int sfb_dgemm_nt_batch(int nb, const double* A, int lda, const double* Bt, int ldb, int M, int N, int K, double* C,
+                       int ldc, long long c_stride, void* stream) {
     SFB_NVTX("sfb_dgemm_nt_batch");
-    if (!A || !lda || !Bt || !ldb || !C) return arg_error("batched GEMM: null argument");
-    if (nb != 7 && nb != 49) return arg_error("batched GEMM: 7 or 49 problems");
-    GemmOperands ops[49];
-    for (int b = 0; b < nb; ++b) ops[b] = GemmOperands{A[b], lda[b], Bt[b], ldb[b]};
+    if (!A || !Bt || !C) return arg_error("batched GEMM: null argument");
     GemmEpi e;
     e.mode = EPI_STORE;
     e.C = C;
@@ -1558,7 +1498,7 @@ int sfb_dgemm_nt_batch(int nb, const double* const* A, const int* lda, const dou
     ScopedFree tmp(s);
     GemmWs gw;
     SFB_TRY(temp_ws(tmp, gw, s));
-    return launch_dgemm_nt_batch(ops, nb, M, N, K, c_stride, with_ws(e, &gw), s);
+    return launch_dgemm_nt_batch(A, lda, Bt, ldb, nb, M, N, K, c_stride, with_ws(e, &gw), s);
 }
 
 int sfb_dgemm_nt_scatter(const double* A, int lda, const double* Bt, int ldb, int M, int N, int K, int nseg,

@@ -627,103 +627,164 @@ __global__ void transpose_kernel(const double* __restrict__ src, int lds, double
     }
 }
 
-// ---- one-level Strassen around the DMMA GEMM (large even preconditioner products) ----
-// C = A Bt^T with 2 x 2 blocks, B = Bt^T (B11 = Bt11^T, B12 = Bt21^T, B21 = Bt12^T, B22 = Bt22^T):
-//   M1 = (A11 + A22)(B11 + B22)   M2 = (A21 + A22) B11     M3 = A11 (B12 - B22)
-//   M4 = A22 (B21 - B11)          M5 = (A11 + A12) B22     M6 = (A21 - A11)(B11 + B12)
-//   M7 = (A12 - A22)(B21 + B22)
-//   C11 = M1 + M4 - M5 + M7   C12 = M3 + M5   C21 = M2 + M4   C22 = M1 - M2 + M3 + M6
-// strassen_sums_kernel forms the five block sums of one operand (side 0: the
-// A pattern, side 1: the Bt pattern) in one pass over its four blocks;
-// strassen_combine_kernel assembles C from the seven products in one pass,
-// with the optional <C,D> of the MO-PCG preconditioner step (solvers.py:448)
-// as a deterministic last-block reduction.
-__global__ void __launch_bounds__(VT) strassen_sums_kernel(const double* __restrict__ X, int ldx, int rh, int ch,
-                                                           double* __restrict__ S, int lds, size_t sstride, int side,
-                                                           const PcgState* gate) {
+// ---- Strassen schedule around the DMMA GEMM, L levels flattened -----------
+// C = A Bt^T with 2 x 2 blocks per level, B = Bt^T (B11 = Bt11^T, B12 = Bt21^T,
+// B21 = Bt12^T, B22 = Bt22^T):
+//   M0 = (A11 + A22)(B11 + B22)   M1 = (A21 + A22) B11     M2 = A11 (B12 - B22)
+//   M3 = A22 (B21 - B11)          M4 = (A11 + A12) B22     M5 = (A21 - A11)(B11 + B12)
+//   M6 = (A12 - A22)(B21 + B22)
+//   C11 = M0 + M3 - M4 + M6   C12 = M2 + M4   C21 = M1 + M3   C22 = M0 - M1 + M2 + M5
+// L levels are one bilinear algorithm with 7^L leaf products of 2^-L-size
+// blocks: leaf l = (i_1 * 7 + i_2) * 7 + ... takes product i_1 at the top
+// level, i_2 below it, and so on.  strassen_operands_kernel forms all 7^L leaf
+// operands of one matrix in one pass (each thread holds the 4^L blocks' values
+// at one position and walks the levels depth-first in registers: read 4^L,
+// write 7^L blocks); strassen_assemble_kernel forms C from the 7^L leaf
+// products the same way (read 7^L, write 4^L blocks), with the optional <C,D>
+// of the MO-PCG preconditioner step (solvers.py:448) as a deterministic
+// last-block reduction.  Blocks are indexed by their quadrant digits
+// (q_1 ... q_L), q = 2 * (lower half) + (right half), most significant first.
+constexpr int ST = 128;  // threads per CTA of the Strassen passes (one position per thread and step)
+
+__host__ __device__ constexpr int pow_int(int b, int e) { return e == 0 ? 1 : b * pow_int(b, e - 1); }
+
+// product i of a level: first quadrant (coefficient +1), second quadrant or -1, its sign
+template <int SIDE>
+struct StrassenIn {
+    // SIDE 0 (A):  A11+A22, A21+A22, A11, A22, A11+A12, A21-A11, A12-A22
+    // SIDE 1 (Bt): Bt11+Bt22, Bt11, Bt21-Bt22, Bt12-Bt11, Bt22, Bt11+Bt21, Bt12+Bt22
+    __device__ static constexpr int qa(int i) {
+        constexpr int a0[7] = {0, 2, 0, 3, 0, 2, 1}, a1[7] = {0, 0, 2, 1, 3, 0, 1};
+        return SIDE == 0 ? a0[i] : a1[i];
+    }
+    __device__ static constexpr int qb(int i) {
+        constexpr int b0[7] = {3, 3, -1, -1, 1, 0, 3}, b1[7] = {3, -1, 3, 0, -1, 2, 3};
+        return SIDE == 0 ? b0[i] : b1[i];
+    }
+    __device__ static constexpr bool minus(int i) {
+        constexpr bool m0[7] = {false, false, false, false, false, true, true},
+                       m1[7] = {false, false, true, true, false, false, false};
+        return SIDE == 0 ? m0[i] : m1[i];
+    }
+};
+
+template <int L, int SIDE>
+struct StrassenDown {
+    template <class Store>
+    __device__ __forceinline__ static void run(const double (&x)[pow_int(4, L)], int prefix, Store&& st) {
+        constexpr int NS = pow_int(4, L - 1);
+        #pragma unroll
+        for (int i = 0; i < 7; ++i) {
+            double y[NS];
+            constexpr int dummy = 0;
+            (void)dummy;
+            const int qa = StrassenIn<SIDE>::qa(i), qb = StrassenIn<SIDE>::qb(i);
+            #pragma unroll
+            for (int m = 0; m < NS; ++m) {
+                if (qb < 0) y[m] = x[qa * NS + m];
+                else y[m] = StrassenIn<SIDE>::minus(i) ? x[qa * NS + m] - x[qb * NS + m] : x[qa * NS + m] + x[qb * NS + m];
+            }
+            if constexpr (L == 1) st(prefix * 7 + i, y[0]);
+            else StrassenDown<L - 1, SIDE>::run(y, prefix * 7 + i, st);
+        }
+    }
+};
+
+template <int L>
+struct StrassenUp {
+    // out[4^L] = the C blocks of the node whose leaves start at prefix * 7^L
+    template <class Load>
+    __device__ __forceinline__ static void run(double (&out)[pow_int(4, L)], int prefix, Load&& ld) {
+        constexpr int NS = pow_int(4, L - 1);
+        // product i adds into quadrant ca (+) and cb (sign sb; -1: none); the first writer of a quadrant assigns
+        constexpr int ca[7] = {0, 2, 1, 0, 1, 3, 0};     // +C11 +C21 +C12 +C11 +C12 +C22 +C11
+        constexpr int cb[7] = {3, 3, 3, 2, 0, -1, -1};   // +C22 -C22 +C22 +C21 -C11
+        constexpr bool mb[7] = {false, true, false, false, true, false, false};
+        #pragma unroll
+        for (int i = 0; i < 7; ++i) {
+            double y[NS];
+            if constexpr (L == 1) y[0] = ld(prefix * 7 + i);
+            else StrassenUp<L - 1>::run(y, prefix * 7 + i, ld);
+            #pragma unroll
+            for (int m = 0; m < NS; ++m) {
+                // i = 0 assigns C11, C22; i = 1 assigns C21; i = 2 assigns C12
+                if (i == 0) {
+                    out[0 * NS + m] = y[m];
+                    out[3 * NS + m] = y[m];
+                } else {
+                    if (i == 1 || i == 2) out[ca[i] * NS + m] = y[m];
+                    else out[ca[i] * NS + m] += y[m];
+                    if (cb[i] >= 0) out[cb[i] * NS + m] = mb[i] ? out[cb[i] * NS + m] - y[m] : out[cb[i] * NS + m] + y[m];
+                }
+            }
+        }
+    }
+};
+
+// block (q_1 ... q_L) -> its row / column block index
+template <int L>
+__host__ __device__ constexpr int quad_row(int idx) {
+    int r = 0;
+    for (int l = 0; l < L; ++l) r |= ((idx >> (2 * l + 1)) & 1) << l;
+    return r;
+}
+template <int L>
+__host__ __device__ constexpr int quad_col(int idx) {
+    int c = 0;
+    for (int l = 0; l < L; ++l) c |= ((idx >> (2 * l)) & 1) << l;
+    return c;
+}
+
+// X: (rh 2^L) x (ch 2^L), ldx; leaf operand l at S + l * sstride (rh x ch, lds)
+template <int L, int SIDE>
+__global__ void __launch_bounds__(ST) strassen_operands_kernel(const double* __restrict__ X, int ldx, int rh, int ch,
+                                                               double* __restrict__ S, int lds, size_t sstride,
+                                                               const PcgState* gate) {
     SFB_PDL_PROLOGUE();
     if (gate != nullptr && gate->status != SFB_PCG_RUNNING) return;
-    const int np = ch / 2;  // ch is even, rows 16-byte aligned
+    constexpr int NQ = pow_int(4, L);
     for (int r = blockIdx.x; r < rh; r += gridDim.x) {
-        const double2* x11 = reinterpret_cast<const double2*>(X + (size_t)r * ldx);
-        const double2* x12 = reinterpret_cast<const double2*>(X + (size_t)r * ldx + ch);
-        const double2* x21 = reinterpret_cast<const double2*>(X + (size_t)(r + rh) * ldx);
-        const double2* x22 = reinterpret_cast<const double2*>(X + (size_t)(r + rh) * ldx + ch);
-        double2* s0 = reinterpret_cast<double2*>(S + (size_t)r * lds);
-        double2* s1 = reinterpret_cast<double2*>(S + sstride + (size_t)r * lds);
-        double2* s2 = reinterpret_cast<double2*>(S + 2 * sstride + (size_t)r * lds);
-        double2* s3 = reinterpret_cast<double2*>(S + 3 * sstride + (size_t)r * lds);
-        double2* s4 = reinterpret_cast<double2*>(S + 4 * sstride + (size_t)r * lds);
-        #pragma unroll 2
-        for (int q = threadIdx.x; q < np; q += VT) {
-            const double2 a = x11[q], b = x12[q], c = x21[q], d = x22[q];
-            if (side == 0) {  // A11 + A22, A21 + A22, A11 + A12, A21 - A11, A12 - A22
-                s0[q] = make_double2(a.x + d.x, a.y + d.y);
-                s1[q] = make_double2(c.x + d.x, c.y + d.y);
-                s2[q] = make_double2(a.x + b.x, a.y + b.y);
-                s3[q] = make_double2(c.x - a.x, c.y - a.y);
-                s4[q] = make_double2(b.x - d.x, b.y - d.y);
-            } else {          // Bt11 + Bt22, Bt21 - Bt22, Bt12 - Bt11, Bt11 + Bt21, Bt12 + Bt22
-                s0[q] = make_double2(a.x + d.x, a.y + d.y);
-                s1[q] = make_double2(c.x - d.x, c.y - d.y);
-                s2[q] = make_double2(b.x - a.x, b.y - a.y);
-                s3[q] = make_double2(a.x + c.x, a.y + c.y);
-                s4[q] = make_double2(b.x + d.x, b.y + d.y);
-            }
+        for (int c = threadIdx.x; c < ch; c += ST) {
+            double x[NQ];
+            #pragma unroll
+            for (int q = 0; q < NQ; ++q)
+                x[q] = X[(size_t)(quad_row<L>(q) * rh + r) * ldx + quad_col<L>(q) * ch + c];
+            const size_t o = (size_t)r * lds + c;
+            StrassenDown<L, SIDE>::run(x, 0, [&](int leaf, double v) { S[leaf * sstride + o] = v; });
         }
     }
 }
 
-__global__ void __launch_bounds__(VT) strassen_combine_kernel(const double* __restrict__ Mp, int ldm, size_t mstride,
-                                                              int rh, int ch, double* __restrict__ C, int ldc,
-                                                              const double* __restrict__ D, int ldd, double* partials,
-                                                              PcgState* st, double* dot_out, unsigned* counter) {
+// leaf product l at Mp + l * mstride (rh x ch, ldm); C: (rh 2^L) x (ch 2^L), ldc
+template <int L>
+__global__ void __launch_bounds__(ST) strassen_assemble_kernel(const double* __restrict__ Mp, int ldm, size_t mstride,
+                                                               int rh, int ch, double* __restrict__ C, int ldc,
+                                                               const double* __restrict__ D, int ldd, double* partials,
+                                                               PcgState* st, double* dot_out, unsigned* counter) {
     SFB_PDL_PROLOGUE();
     if (st != nullptr && st->status != SFB_PCG_RUNNING) return;
-    const int np = ch / 2;
+    constexpr int NQ = pow_int(4, L);
     double dot = 0.0;
     for (int r = blockIdx.x; r < rh; r += gridDim.x) {
-        const double2* m[7];
-        #pragma unroll
-        for (int i = 0; i < 7; ++i) m[i] = reinterpret_cast<const double2*>(Mp + i * mstride + (size_t)r * ldm);
-        double2* c11 = reinterpret_cast<double2*>(C + (size_t)r * ldc);
-        double2* c12 = reinterpret_cast<double2*>(C + (size_t)r * ldc + ch);
-        double2* c21 = reinterpret_cast<double2*>(C + (size_t)(r + rh) * ldc);
-        double2* c22 = reinterpret_cast<double2*>(C + (size_t)(r + rh) * ldc + ch);
-        const double2* d11 = reinterpret_cast<const double2*>(D + (size_t)r * ldd);
-        const double2* d12 = reinterpret_cast<const double2*>(D + (size_t)r * ldd + ch);
-        const double2* d21 = reinterpret_cast<const double2*>(D + (size_t)(r + rh) * ldd);
-        const double2* d22 = reinterpret_cast<const double2*>(D + (size_t)(r + rh) * ldd + ch);
-        for (int q = threadIdx.x; q < np; q += VT) {
-            const double2 m1 = m[0][q], m2 = m[1][q], m3 = m[2][q], m4 = m[3][q], m5 = m[4][q], m6 = m[5][q],
-                          m7 = m[6][q];
-            const double2 v11 = make_double2(((m1.x + m4.x) - m5.x) + m7.x, ((m1.y + m4.y) - m5.y) + m7.y);
-            const double2 v12 = make_double2(m3.x + m5.x, m3.y + m5.y);
-            const double2 v21 = make_double2(m2.x + m4.x, m2.y + m4.y);
-            const double2 v22 = make_double2(((m1.x - m2.x) + m3.x) + m6.x, ((m1.y - m2.y) + m3.y) + m6.y);
-            c11[q] = v11;
-            c12[q] = v12;
-            c21[q] = v21;
-            c22[q] = v22;
-            if (D != nullptr) {
-                const double2 e11 = d11[q], e12 = d12[q], e21 = d21[q], e22 = d22[q];
-                dot = fma(v11.x, e11.x, dot);
-                dot = fma(v11.y, e11.y, dot);
-                dot = fma(v12.x, e12.x, dot);
-                dot = fma(v12.y, e12.y, dot);
-                dot = fma(v21.x, e21.x, dot);
-                dot = fma(v21.y, e21.y, dot);
-                dot = fma(v22.x, e22.x, dot);
-                dot = fma(v22.y, e22.y, dot);
+        for (int c = threadIdx.x; c < ch; c += ST) {
+            const size_t o = (size_t)r * ldm + c;
+            double out[NQ];
+            StrassenUp<L>::run(out, 0, [&](int leaf) { return __ldg(Mp + leaf * mstride + o); });
+            #pragma unroll
+            for (int q = 0; q < NQ; ++q) {
+                const size_t row = (size_t)(quad_row<L>(q) * rh + r);
+                const int col = quad_col<L>(q) * ch + c;
+                C[row * ldc + col] = out[q];
+                if (D != nullptr) dot = fma(out[q], D[row * ldd + col], dot);
             }
         }
     }
     if (D == nullptr) return;  // uniform
-    __shared__ double sh[VT / 32];
-    const double p = block_sum<VT>(dot, sh);
+    __shared__ double sh[ST / 32];
+    const double p = block_sum<ST>(dot, sh);
     if (threadIdx.x == 0) partials[blockIdx.x] = p;
     if (arrive_last(counter, gridDim.x)) {
-        const double tot = sum_partials<VT>(partials, gridDim.x, 1, sh);
+        const double tot = sum_partials<ST>(partials, gridDim.x, 1, sh);
         if (threadIdx.x == 0) {
             *counter = 0;
             if (st != nullptr) st->rz_next = tot;
@@ -734,21 +795,42 @@ __global__ void __launch_bounds__(VT) strassen_combine_kernel(const double* __re
 
 int vector_grid_blocks() { return VB; }
 
-int launch_strassen_sums(const double* X, int ldx, int rh, int ch, double* S, int lds, size_t sstride, int side,
-                         const PcgState* gate, cudaStream_t s) {
-    SFB_TRY(launch_kernel(strassen_sums_kernel, dim3(std::max(1, std::min(VB, rh))), dim3(VT), 0, s, X, ldx, rh, ch, S,
-                          lds, sstride, side, gate));
-    SFB_CHECK_LAUNCH();
-    return SFB_OK;
+int launch_strassen_operands(int levels, int side, const double* X, int ldx, int rh, int ch, double* S, int lds,
+                             size_t sstride, const PcgState* gate, cudaStream_t s) {
+    const dim3 grid(std::max(1, std::min(VB, rh))), block(ST);
+#define SFB_OPERANDS(L, SIDE)                                                                                      \
+    if (levels == L && side == SIDE) {                                                                             \
+        SFB_TRY(launch_kernel(strassen_operands_kernel<L, SIDE>, grid, block, 0, s, X, ldx, rh, ch, S, lds, sstride, \
+                              gate));                                                                              \
+        SFB_CHECK_LAUNCH();                                                                                        \
+        return SFB_OK;                                                                                             \
+    }
+    SFB_OPERANDS(1, 0)
+    SFB_OPERANDS(1, 1)
+    SFB_OPERANDS(2, 0)
+    SFB_OPERANDS(2, 1)
+    SFB_OPERANDS(3, 0)
+    SFB_OPERANDS(3, 1)
+#undef SFB_OPERANDS
+    return arg_error("Strassen operands: 1 to 3 levels, side 0 or 1");
 }
 
-int launch_strassen_combine(const double* Mp, int ldm, size_t mstride, int rh, int ch, double* C, int ldc,
-                            const double* D, int ldd, double* partials, PcgState* st, double* dot_out,
-                            unsigned* counter, cudaStream_t s) {
-    SFB_TRY(launch_kernel(strassen_combine_kernel, dim3(std::max(1, std::min(VB, rh))), dim3(VT), 0, s, Mp, ldm,
-                          mstride, rh, ch, C, ldc, D, ldd, partials, st, dot_out, counter));
-    SFB_CHECK_LAUNCH();
-    return SFB_OK;
+int launch_strassen_assemble(int levels, const double* Mp, int ldm, size_t mstride, int rh, int ch, double* C, int ldc,
+                             const double* D, int ldd, double* partials, PcgState* st, double* dot_out,
+                             unsigned* counter, cudaStream_t s) {
+    const dim3 grid(std::max(1, std::min(VB, rh))), block(ST);
+#define SFB_ASSEMBLE(L)                                                                                          \
+    if (levels == L) {                                                                                           \
+        SFB_TRY(launch_kernel(strassen_assemble_kernel<L>, grid, block, 0, s, Mp, ldm, mstride, rh, ch, C, ldc, D, \
+                              ldd, partials, st, dot_out, counter));                                             \
+        SFB_CHECK_LAUNCH();                                                                                      \
+        return SFB_OK;                                                                                           \
+    }
+    SFB_ASSEMBLE(1)
+    SFB_ASSEMBLE(2)
+    SFB_ASSEMBLE(3)
+#undef SFB_ASSEMBLE
+    return arg_error("Strassen assembly: 1 to 3 levels");
 }
 
 int launch_pcg_init_plain(const double* rhs, int ldr, double* R, double* U, int ld, int rows, int cols,

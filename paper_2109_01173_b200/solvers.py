@@ -202,10 +202,11 @@ class KroneckerCSR(sp.csr_matrix):
 
 def set_strassen_min_q(min_q: int) -> int:
     """Grid size from which the inverse-form preconditioner products (the two
-    dense solves of solvers.py:134-143 as DMMA GEMMs) run as one level of
-    Strassen (7 half-size GEMMs each; shapes divisible by 4).  0 disables it.
-    Applies to device preconditioners built afterwards; returns the previous
-    threshold (default 6144, or SYLFEM_B200_STRASSEN_MINQ)."""
+    dense solves of solvers.py:134-143 as DMMA GEMMs) run as up to three
+    Strassen levels (7 half-size products per level; every level's dimensions
+    divisible by 4).  0 disables it.  Applies to device preconditioners built
+    afterwards; returns the previous threshold (default 4096, or
+    SYLFEM_B200_STRASSEN_MINQ)."""
     return int(nat.lib().sfb_set_strassen_min_q(int(min_q)))
 
 

@@ -1,5 +1,6 @@
-"""The inverse-form preconditioner's dense products as one level of Strassen
-around the DMMA GEMM (large shapes divisible by 4; BASELINE cfg5, q = 8192).
+"""The inverse-form preconditioner's dense products as one to three levels of
+Strassen around the DMMA GEMM (large shapes divisible by 4; BASELINE cfg5,
+q = 8192, runs three), and the strided-batch GEMM of their leaf products.
 
 The reference applies P_L^-1 U P_R^-1 by two dense solves
 (solvers.py:134-143).  Strassen changes the summation order of the two
@@ -39,7 +40,7 @@ def test_strassen_product_matches_classic_schedule(Nx, Ny, strassen_from_256):
     d, tau = 20.0, 1.25e-5
     kw = {"d_u": d, "tau": tau, "lumped": True}
     pre_s = pb.make_preconditioner("parabolic_lumped", x, y, mode="inverse", **kw)
-    # leaves of at least 64 (a sixth of the threshold, not below 64): q = 256 takes at most two levels
+    # leaves of at least 64 (an eighth of the threshold, not below 64): q = 256 takes at most two levels
     assert pre_s.uses_strassen() == (strassen_from_256 if min(x.q, y.q) >= 512 else min(strassen_from_256, 2))
     prev = pb.set_strassen_min_q(0)
     try:
@@ -93,31 +94,24 @@ def test_strassen_mo_pcg_iterates_vs_oracle(d, tau, strassen_from_256):
     assert relerr(rep.solution, full["solution"]) <= 1e-9
 
 
-@pytest.mark.parametrize("nb", [7, 49])
+@pytest.mark.parametrize("nb", [1, 7, 49])
 @pytest.mark.parametrize("M,N,K", [(256, 256, 256), (384, 256, 512), (130, 258, 100)])
 def test_batched_gemm_matches_fp64_matmul(M, N, K, nb):
-    """sfb_dgemm_nt_batch: 7 or 49 products in one persistent launch (operands with
-    different leading dimensions, as the Strassen levels pass block views and sums)."""
-    import ctypes as C
-
+    """sfb_dgemm_nt_batch: nb stacked products in one persistent launch (rank-3
+    tensor maps; padded leading dimensions as the Strassen leaves have)."""
     import torch
 
     from paper_2109_01173_b200 import _native as nat
 
     g = torch.Generator(device="cuda").manual_seed(M + N + K)
-    ldc = N + (N % 2)
-    As = [torch.randn(M, K + 2 * (b % 3), dtype=torch.float64, device="cuda", generator=g) for b in range(nb)]
-    Bs = [torch.randn(N, K + 4 * (b % 2), dtype=torch.float64, device="cuda", generator=g) for b in range(nb)]
+    lda, ldb, ldc = K + 2, K + 4, N + (N % 2) + 2
+    A = torch.randn(nb, M, lda, dtype=torch.float64, device="cuda", generator=g)
+    B = torch.randn(nb, N, ldb, dtype=torch.float64, device="cuda", generator=g)
     out = torch.zeros(nb, M, ldc, dtype=torch.float64, device="cuda")
-    pa = (C.c_void_p * nb)(*[a.data_ptr() for a in As])
-    pb_ = (C.c_void_p * nb)(*[b.data_ptr() for b in Bs])
-    la = (C.c_int * nb)(*[a.shape[1] for a in As])
-    lb = (C.c_int * nb)(*[b.shape[1] for b in Bs])
-    nat.check(nat.lib().sfb_dgemm_nt_batch(nb, pa, la, pb_, lb, M, N, K, out.data_ptr(), ldc, M * ldc, nat.stream()),
-              "batched GEMM")
+    nat.check(nat.lib().sfb_dgemm_nt_batch(nb, A.data_ptr(), lda, B.data_ptr(), ldb, M, N, K, out.data_ptr(), ldc,
+                                           M * ldc, nat.stream()), "batched GEMM")
     torch.cuda.synchronize()
     for b in range(nb):
-        ref = As[b][:, :K] @ Bs[b][:, :K].T
+        ref = A[b, :, :K] @ B[b, :, :K].T
         assert float((out[b, :, :N] - ref).norm() / ref.norm()) <= 1e-14
-    if ldc > N:
-        assert float(out[:, :, N:].abs().max()) == 0.0
+    assert float(out[:, :, N:].abs().max()) == 0.0  # nothing stored past the N columns
