@@ -164,17 +164,17 @@ int sfb_pre_create(int qy, int qx, int kind, const double* L,
                    const double* R, const double* lamL_host,
                    const double* lamR_host, sfb_pre** out);
 /* The inverse-form products Z = P_L^-1 (R P_R^-1) of shapes with q_y, q_x >=
- * min_q run as up to three levels of Strassen around the DMMA GEMM (every
- * level's dimensions divisible by 4): one pass forms the 7^L leaf operands of
+ * min_q run as up to three levels of Strassen around the DMMA GEMM (odd
+ * shapes are padded with zeros inside the passes): one pass forms the 7^L leaf operands of
  * the variable factor (those of the constant factors are formed at creation),
  * one strided-batch DMMA launch does the 7^L leaf products, one pass
  * assembles Z (and <Z,R>).  Same value as the two dense solves of
  * Preconditioner.apply_inverse (solvers.py:134-143), other summation order.
  * Applies to preconditioners created afterwards; 0 = never (default:
- * SYLFEM_B200_STRASSEN_MINQ or 4096).  Returns the previous threshold. */
+ * SYLFEM_B200_STRASSEN_MINQ or 2000).  Returns the previous threshold. */
 int sfb_set_strassen_min_q(int min_q);
 /* Most Strassen levels taken (0..3, default SYLFEM_B200_STRASSEN_LEVELS or 3);
- * a level needs dimensions divisible by 4 and halves of at least min_q / 8.
+ * the leaves must be at least min_q / 4 (not below 64).
  * Returns the previous value. */
 int sfb_set_strassen_levels(int levels);
 /* Strassen levels this preconditioner's products use (0: classic GEMMs). */

@@ -129,14 +129,15 @@ int launch_norms(const double* A, int lda, const double* B, int ldb, int rows, i
                  RedSlots* out, cudaStream_t s);
 int vector_grid_blocks();
 // Strassen schedule, `levels` levels flattened (vector.cu): all 7^levels leaf
-// operands of X ((rh 2^levels) x (ch 2^levels); side 0: left operand A, side 1:
-// right operand Bt) at S + l * sstride, and the assembly of C from the leaf
-// products at Mp + l * mstride, with <C,D> when D is set
-int launch_strassen_operands(int levels, int side, const double* X, int ldx, int rh, int ch, double* S, int lds,
-                             size_t sstride, const PcgState* gate, cudaStream_t s);
+// operands (rh x ch each, at S + l * sstride) of X (rows x cols, read as
+// (rh 2^levels) x (ch 2^levels) with zeros past its extents; side 0: left
+// operand A, side 1: right operand Bt), and the assembly of C (rows x cols)
+// from the leaf products at Mp + l * mstride, with <C,D> when D is set
+int launch_strassen_operands(int levels, int side, const double* X, int ldx, int rows, int cols, int rh, int ch,
+                             double* S, int lds, size_t sstride, const PcgState* gate, cudaStream_t s);
 int launch_strassen_assemble(int levels, const double* Mp, int ldm, size_t mstride, int rh, int ch, double* C, int ldc,
-                             const double* D, int ldd, double* partials, PcgState* st, double* dot_out,
-                             unsigned* counter, cudaStream_t s);
+                             int rows, int cols, const double* D, int ldd, double* partials, PcgState* st,
+                             double* dot_out, unsigned* counter, cudaStream_t s);
 int launch_transpose(const double* src, int lds, double* dst, int ldd, int rows, int cols, cudaStream_t s);
 int launch_sh_update(double* U, double* R, const double* Q, const double* W, int ld, int rows, int cols,
                      double alpha, double* partials, RedSlots* out, cudaStream_t s);

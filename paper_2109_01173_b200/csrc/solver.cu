@@ -240,16 +240,17 @@ int op_apply_impl(const sfb_op* op, const double* U, int ldu, double* W, int ldw
 // sfb_pre_create).  Per product: one pass forms the variable operand's 7^L
 // leaf operands, one strided-batch DMMA launch does the 7^L leaf products,
 // one pass assembles the result (and <Z,R>).  Three levels do 343/512 of the
-// flops.  Used for shapes of at least strassen_min_q() with every level's
-// dimensions divisible by 4 and leaves of at least an eighth of the threshold
-// (SYLFEM_B200_STRASSEN_MINQ, default 4096, 0 = never;
-// SYLFEM_B200_STRASSEN_LEVELS, default 3: q = 8192 runs 343 leaves of 1024^3,
-// measured 45.5 ms per preconditioner application against 62.2 ms with one
-// 8192^3 DMMA GEMM per product; q = 4096: 6.3 against 8.0 ms).
+// flops.  Used for shapes of at least strassen_min_q() (any parity: the
+// passes pad odd shapes virtually) with leaves of at least a quarter of the
+// threshold (SYLFEM_B200_STRASSEN_MINQ, default 2000, 0 = never;
+// SYLFEM_B200_STRASSEN_LEVELS, default 3).  Measured per preconditioner
+// application against one DMMA GEMM per product: q = 8192 (343 leaves of
+// 1024^3) 45.5 vs 62.2 ms; q = 4095 (343 of 512^3) 6.58 vs 8.03 ms; q = 2047
+// (49 of 512^3) 1.03 vs 1.10 ms; q = 1024: no gain (0.21 ms either way).
 std::atomic<int>& strassen_min_q_slot() {
     static std::atomic<int> v([] {
         const char* e = std::getenv("SYLFEM_B200_STRASSEN_MINQ");
-        return e ? std::atoi(e) : 4096;
+        return e ? std::atoi(e) : 2000;
     }());
     return v;
 }
@@ -262,23 +263,24 @@ std::atomic<int>& strassen_max_levels_slot() {
     return v;
 }
 
+// leaf dimension of q with L levels: q padded (virtually, with zeros) to a
+// multiple of 2^(L+1), so every leaf has an even dimension (16-byte rows)
+int strassen_leaf(int q, int L) { return (round_up(q, 2 << L)) >> L; }
+
 int strassen_levels_of(int q) {
     const int m = strassen_min_q();
     if (m <= 0 || q < m) return 0;
-    const int leaf = std::max(m / 8, 64);
-    int levels = 0;
-    while (levels < strassen_max_levels_slot().load(std::memory_order_relaxed) && q % 4 == 0 && q / 2 >= leaf) {
-        q /= 2;
-        ++levels;
-    }
-    return levels;
+    const int leaf = std::max(m / 4, 64);
+    for (int L = strassen_max_levels_slot().load(std::memory_order_relaxed); L > 0; --L)
+        if (strassen_leaf(q, L) >= leaf) return L;
+    return 0;
 }
 int strassen_levels(int qy, int qx) { return std::min(strassen_levels_of(qy), strassen_levels_of(qx)); }
 
 // The constant left operand of a product (M x K): its 7^levels leaf operands
-// ((M >> levels) x ldk each, stacked), formed once.
+// (mh x ldk each, stacked), formed once.
 struct StrassenPlan {
-    int levels = 0, M = 0, K = 0, ldk = 0, leaves = 0;
+    int levels = 0, M = 0, K = 0, mh = 0, kh = 0, ldk = 0, leaves = 0;
     double* leaf = nullptr;
 };
 
@@ -295,12 +297,14 @@ int build_strassen_plan(const double* A, int lda, int M, int K, int levels, Stra
     p->K = K;
     p->leaves = 1;
     for (int l = 0; l < levels; ++l) p->leaves *= 7;
-    const int mh = M >> levels, kh = K >> levels;
-    p->ldk = pad_ld(kh);
-    const size_t sa = (size_t)mh * p->ldk;
+    p->mh = strassen_leaf(M, levels);
+    p->kh = strassen_leaf(K, levels);
+    p->ldk = pad_ld(p->kh);
+    const size_t sa = (size_t)p->mh * p->ldk;
     int rc = dalloc(&p->leaf, sa * p->leaves);
     if (rc == SFB_OK && cudaMemset(p->leaf, 0, sa * p->leaves * 8) != cudaSuccess) rc = SFB_ERR_CUDA;
-    if (rc == SFB_OK) rc = launch_strassen_operands(levels, 0, A, lda, mh, kh, p->leaf, p->ldk, sa, nullptr, nullptr);
+    if (rc == SFB_OK)
+        rc = launch_strassen_operands(levels, 0, A, lda, M, K, p->mh, p->kh, p->leaf, p->ldk, sa, nullptr, nullptr);
     if (rc != SFB_OK) {
         free_strassen_plan(p);
         return rc;
@@ -311,7 +315,7 @@ int build_strassen_plan(const double* A, int lda, int M, int K, int levels, Stra
 
 // scratch of a product: the variable operand's leaf operands and the leaf products
 size_t strassen_scratch_doubles(int qy, int qx, int levels) {
-    const int h = std::max(qy, qx) >> levels;
+    const int h = strassen_leaf(std::max(qy, qx), levels);
     size_t leaves = 1;
     for (int l = 0; l < levels; ++l) leaves *= 7;
     return 2 * leaves * (size_t)h * pad_ld(h);
@@ -323,12 +327,12 @@ size_t strassen_scratch_doubles(int qy, int qx, int levels) {
 int strassen_apply(const StrassenPlan* pl, const double* Bt, int ldb, int N, double* scratch, double* C, int ldc,
                    const double* D, int ldd, double* partials, PcgState* pcg, double* dot_out, unsigned* counter,
                    const GemmWs* gw, cudaStream_t s) {
-    const int L = pl->levels, mh = pl->M >> L, nh = N >> L, kh = pl->K >> L;
+    const int L = pl->levels, mh = pl->mh, nh = strassen_leaf(N, L), kh = pl->kh;
     const int ldk = pl->ldk, ldn = pad_ld(nh);
     const size_t sa = (size_t)mh * ldk, sb = (size_t)nh * ldk, sm = (size_t)mh * ldn;
     double* Bl = scratch;
     double* Mp = scratch + (size_t)pl->leaves * sb;
-    SFB_TRY(launch_strassen_operands(L, 1, Bt, ldb, nh, kh, Bl, ldk, sb, pcg, s));
+    SFB_TRY(launch_strassen_operands(L, 1, Bt, ldb, N, pl->K, nh, kh, Bl, ldk, sb, pcg, s));
     GemmEpi e;
     e.mode = EPI_STORE;
     e.ldc = ldn;
@@ -340,7 +344,8 @@ int strassen_apply(const StrassenPlan* pl, const double* Bt, int ldb, int N, dou
         SFB_TRY(launch_dgemm_nt_batch(pl->leaf + (size_t)l0 * sa, ldk, Bl + (size_t)l0 * sb, ldk, nb, mh, nh, kh,
                                       (long long)sm, with_ws(e, gw), s));
     }
-    return launch_strassen_assemble(L, Mp, ldn, sm, mh, nh, C, ldc, D, ldd, partials, pcg, dot_out, counter, s);
+    return launch_strassen_assemble(L, Mp, ldn, sm, mh, nh, C, ldc, pl->M, N, D, ldd, partials, pcg, dot_out, counter,
+                                    s);
 }
 
 // Z = P^-1 R (or the reduced-solve sandwich).  R/Z device buffers with even

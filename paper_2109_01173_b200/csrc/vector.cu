@@ -735,11 +735,13 @@ __host__ __device__ constexpr int quad_col(int idx) {
     return c;
 }
 
-// X: (rh 2^L) x (ch 2^L), ldx; leaf operand l at S + l * sstride (rh x ch, lds)
+// X: rows x cols (ldx), read as (rh 2^L) x (ch 2^L) with zeros past its
+// extents (odd shapes are padded virtually); leaf operand l at S + l * sstride
+// (rh x ch, lds)
 template <int L, int SIDE>
-__global__ void __launch_bounds__(ST) strassen_operands_kernel(const double* __restrict__ X, int ldx, int rh, int ch,
-                                                               double* __restrict__ S, int lds, size_t sstride,
-                                                               const PcgState* gate) {
+__global__ void __launch_bounds__(ST) strassen_operands_kernel(const double* __restrict__ X, int ldx, int rows,
+                                                               int cols, int rh, int ch, double* __restrict__ S,
+                                                               int lds, size_t sstride, const PcgState* gate) {
     SFB_PDL_PROLOGUE();
     if (gate != nullptr && gate->status != SFB_PCG_RUNNING) return;
     constexpr int NQ = pow_int(4, L);
@@ -747,20 +749,24 @@ __global__ void __launch_bounds__(ST) strassen_operands_kernel(const double* __r
         for (int c = threadIdx.x; c < ch; c += ST) {
             double x[NQ];
             #pragma unroll
-            for (int q = 0; q < NQ; ++q)
-                x[q] = X[(size_t)(quad_row<L>(q) * rh + r) * ldx + quad_col<L>(q) * ch + c];
+            for (int q = 0; q < NQ; ++q) {
+                const int row = quad_row<L>(q) * rh + r, col = quad_col<L>(q) * ch + c;
+                x[q] = (row < rows && col < cols) ? X[(size_t)row * ldx + col] : 0.0;
+            }
             const size_t o = (size_t)r * lds + c;
             StrassenDown<L, SIDE>::run(x, 0, [&](int leaf, double v) { S[leaf * sstride + o] = v; });
         }
     }
 }
 
-// leaf product l at Mp + l * mstride (rh x ch, ldm); C: (rh 2^L) x (ch 2^L), ldc
+// leaf product l at Mp + l * mstride (rh x ch, ldm); C: rows x cols (ldc), the
+// leading part of the assembled (rh 2^L) x (ch 2^L)
 template <int L>
 __global__ void __launch_bounds__(ST) strassen_assemble_kernel(const double* __restrict__ Mp, int ldm, size_t mstride,
                                                                int rh, int ch, double* __restrict__ C, int ldc,
-                                                               const double* __restrict__ D, int ldd, double* partials,
-                                                               PcgState* st, double* dot_out, unsigned* counter) {
+                                                               int rows, int cols, const double* __restrict__ D,
+                                                               int ldd, double* partials, PcgState* st, double* dot_out,
+                                                               unsigned* counter) {
     SFB_PDL_PROLOGUE();
     if (st != nullptr && st->status != SFB_PCG_RUNNING) return;
     constexpr int NQ = pow_int(4, L);
@@ -772,10 +778,11 @@ __global__ void __launch_bounds__(ST) strassen_assemble_kernel(const double* __r
             StrassenUp<L>::run(out, 0, [&](int leaf) { return __ldg(Mp + leaf * mstride + o); });
             #pragma unroll
             for (int q = 0; q < NQ; ++q) {
-                const size_t row = (size_t)(quad_row<L>(q) * rh + r);
-                const int col = quad_col<L>(q) * ch + c;
-                C[row * ldc + col] = out[q];
-                if (D != nullptr) dot = fma(out[q], D[row * ldd + col], dot);
+                const int row = quad_row<L>(q) * rh + r, col = quad_col<L>(q) * ch + c;
+                if (row < rows && col < cols) {
+                    C[(size_t)row * ldc + col] = out[q];
+                    if (D != nullptr) dot = fma(out[q], D[(size_t)row * ldd + col], dot);
+                }
             }
         }
     }
@@ -795,13 +802,13 @@ __global__ void __launch_bounds__(ST) strassen_assemble_kernel(const double* __r
 
 int vector_grid_blocks() { return VB; }
 
-int launch_strassen_operands(int levels, int side, const double* X, int ldx, int rh, int ch, double* S, int lds,
-                             size_t sstride, const PcgState* gate, cudaStream_t s) {
+int launch_strassen_operands(int levels, int side, const double* X, int ldx, int rows, int cols, int rh, int ch,
+                             double* S, int lds, size_t sstride, const PcgState* gate, cudaStream_t s) {
     const dim3 grid(std::max(1, std::min(VB, rh))), block(ST);
 #define SFB_OPERANDS(L, SIDE)                                                                                      \
     if (levels == L && side == SIDE) {                                                                             \
-        SFB_TRY(launch_kernel(strassen_operands_kernel<L, SIDE>, grid, block, 0, s, X, ldx, rh, ch, S, lds, sstride, \
-                              gate));                                                                              \
+        SFB_TRY(launch_kernel(strassen_operands_kernel<L, SIDE>, grid, block, 0, s, X, ldx, rows, cols, rh, ch, S, \
+                              lds, sstride, gate));                                                                \
         SFB_CHECK_LAUNCH();                                                                                        \
         return SFB_OK;                                                                                             \
     }
@@ -816,13 +823,13 @@ int launch_strassen_operands(int levels, int side, const double* X, int ldx, int
 }
 
 int launch_strassen_assemble(int levels, const double* Mp, int ldm, size_t mstride, int rh, int ch, double* C, int ldc,
-                             const double* D, int ldd, double* partials, PcgState* st, double* dot_out,
-                             unsigned* counter, cudaStream_t s) {
+                             int rows, int cols, const double* D, int ldd, double* partials, PcgState* st,
+                             double* dot_out, unsigned* counter, cudaStream_t s) {
     const dim3 grid(std::max(1, std::min(VB, rh))), block(ST);
 #define SFB_ASSEMBLE(L)                                                                                          \
     if (levels == L) {                                                                                           \
-        SFB_TRY(launch_kernel(strassen_assemble_kernel<L>, grid, block, 0, s, Mp, ldm, mstride, rh, ch, C, ldc, D, \
-                              ldd, partials, st, dot_out, counter));                                             \
+        SFB_TRY(launch_kernel(strassen_assemble_kernel<L>, grid, block, 0, s, Mp, ldm, mstride, rh, ch, C, ldc, rows, \
+                              cols, D, ldd, partials, st, dot_out, counter));                                    \
         SFB_CHECK_LAUNCH();                                                                                      \
         return SFB_OK;                                                                                           \
     }

@@ -203,9 +203,9 @@ class KroneckerCSR(sp.csr_matrix):
 def set_strassen_min_q(min_q: int) -> int:
     """Grid size from which the inverse-form preconditioner products (the two
     dense solves of solvers.py:134-143 as DMMA GEMMs) run as up to three
-    Strassen levels (7 half-size products per level; every level's dimensions
-    divisible by 4).  0 disables it.  Applies to device preconditioners built
-    afterwards; returns the previous threshold (default 4096, or
+    Strassen levels (7 half-size products per level; odd shapes are padded
+    with zeros inside the passes).  0 disables it.  Applies to device preconditioners built
+    afterwards; returns the previous threshold (default 2000, or
     SYLFEM_B200_STRASSEN_MINQ)."""
     return int(nat.lib().sfb_set_strassen_min_q(int(min_q)))
 

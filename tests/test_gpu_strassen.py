@@ -34,14 +34,15 @@ def _lumped_sets(Nx, Ny):
     return pb.build_direction_sets(pb.SQUARE, 1, (Nx, Ny), pb.BCKind.NEUMANN, lumped=True)
 
 
-@pytest.mark.parametrize("Nx,Ny", [(511, 511), (767, 511), (255, 383)])
+@pytest.mark.parametrize("Nx,Ny", [(511, 511), (767, 511), (255, 383), (512, 510), (300, 277)])
 def test_strassen_product_matches_classic_schedule(Nx, Ny, strassen_from_256):
     x, y = _lumped_sets(Nx, Ny)
     d, tau = 20.0, 1.25e-5
     kw = {"d_u": d, "tau": tau, "lumped": True}
     pre_s = pb.make_preconditioner("parabolic_lumped", x, y, mode="inverse", **kw)
-    # leaves of at least 64 (an eighth of the threshold, not below 64): q = 256 takes at most two levels
-    assert pre_s.uses_strassen() == (strassen_from_256 if min(x.q, y.q) >= 512 else min(strassen_from_256, 2))
+    # leaves of at least 64 (a quarter of the threshold): q < 498 takes at most two levels
+    # (odd shapes are padded to a multiple of 2^(L+1))
+    assert pre_s.uses_strassen() == (strassen_from_256 if min(x.q, y.q) >= 498 else min(strassen_from_256, 2))
     prev = pb.set_strassen_min_q(0)
     try:
         pre_c = pb.make_preconditioner("parabolic_lumped", x, y, mode="inverse", **kw)
@@ -58,10 +59,37 @@ def test_strassen_product_matches_classic_schedule(Nx, Ny, strassen_from_256):
     assert relerr(Zs, opre.inverse(R)) <= 1e-11
 
 
-def test_strassen_shapes_not_divisible_by_4_keep_the_classic_schedule(strassen_from_256):
-    x, y = _lumped_sets(513, 511)  # q_x = 514
+def test_strassen_below_the_threshold_keeps_the_classic_schedule(strassen_from_256):
+    x, y = _lumped_sets(511, 200)  # q_y = 201 < 256
     pre = pb.make_preconditioner("parabolic_lumped", x, y, mode="inverse", d_u=1.0, tau=1e-4, lumped=True)
-    assert not pre.uses_strassen()
+    assert pre.uses_strassen() == 0
+
+
+def test_strassen_odd_shape_five_term_mo_pcg_vs_oracle(strassen_from_256):
+    """cfg3-type system (P2, wave domain, Dirichlet: q = N - 1 is odd, five terms,
+    the elliptic_xnormal preconditioner): the passes pad the odd shape with zeros."""
+    N = 320  # q = N - 1 = 319
+    wave = pb.DomainSpec(pb.DomainKind.XNORMAL, pb.ProfileFn(
+        lambda s: 1.0 + 0.3 * np.sin(2 * np.pi * np.asarray(s, float)),
+        lambda s: 0.6 * np.pi * np.cos(2 * np.pi * np.asarray(s, float)), name="wave"))
+    x, y = pb.build_direction_sets(wave, 2, N, pb.BCKind.DIRICHLET)
+    op, rhs_of = pb.elliptic_operator(x, y, 1.0)
+    a, b, c = orc.seeded_modes(3)
+    s = np.arange(N + 1) / N
+    F = sum(c[m] * np.sin(b[m] * np.pi * s)[:, None] * np.sin(a[m] * np.pi * s)[None, :] for m in range(8))
+    rhs = rhs_of(F)
+    pre = pb.make_preconditioner("elliptic_xnormal", x, y, mode="inverse")
+    assert op.shape == (319, 319) and pre.uses_strassen() == min(strassen_from_256, 2)
+    ox, oy = orc.direction_sets(orc.wave_domain(), 2, N, orc.DIRICHLET)
+    terms, orhs = orc.elliptic_terms(ox, oy, 1.0)
+    opre = orc.LUPrecond(*orc.precond_factors("elliptic_xnormal", ox, oy))
+    K = 10
+    ref = orc.mo_pcg(terms, orhs(F), opre.inverse, ("residual", 1e-300), max_iter=K)
+    rep = pb.mo_pcg(op, rhs, precond=pre, stop=pb.fixed_budget(), max_iter=K)
+    assert rep.iterations == K
+    assert relerr(rep.solution, ref["solution"]) <= 1e-10
+    h = np.asarray(ref["history"])
+    assert np.max(np.abs(rep.residual_history - h) / h) <= 1e-10
 
 
 @pytest.mark.parametrize("d,tau", [(1.0, 5e-4), (20.0, 1.25e-5)])
