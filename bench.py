@@ -294,6 +294,12 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------ GPU pieces ----
+def strassen_leaf(q: int, levels: int) -> int:
+    """Leaf dimension of the Strassen schedule (odd shapes are padded to a multiple of 2^(levels+1))."""
+    unit = 2 << levels
+    return ((q + unit - 1) // unit * unit) >> levels
+
+
 def gemm_roofline(q: int, levels: int = 0):
     """Dominant kernel: the q x q x q DMMA GEMM (C = A Bt^T), live CUDA
     events on the launching stream, against cuBLAS DGEMM 8192^3 measured in
@@ -346,7 +352,7 @@ def gemm_roofline(q: int, levels: int = 0):
     if levels > 0:
         # the dominant kernel of the Strassen schedule: one batched launch of the
         # seven leaf products (its own flops, not the algorithmic 2 q^3)
-        h = q >> levels
+        h = strassen_leaf(q, levels)
         nb = 7 ** levels  # all leaf products of a preconditioner product are one strided-batch launch
         A = torch.randn(nb, h, h, dtype=torch.float64, device="cuda")
         B = torch.randn(nb, h, h, dtype=torch.float64, device="cuda")
@@ -616,7 +622,7 @@ def run_cfg5(args):
     roof = gemm_roofline(qy, levels)
     n_gemm = 2 if args.precond_mode == "inverse" else (4 if args.precond_mode == "spectral" else 0)
     n_launch = n_gemm * roof.get("launches_per_product", 1)  # dominant-kernel launches per iteration
-    tkey = f"q{qy >> levels}x{7 ** levels}" if levels > 0 else f"q{qy}"
+    tkey = f"q{strassen_leaf(qy, levels)}x{7 ** levels}" if levels > 0 else f"q{qy}"
     roof.update({"share_of_iteration": n_launch * roof["launch_ms"] / iter_ms if n_gemm else 0.0,
                  "iteration_ms": iter_ms,
                  "traffic": (profile_json("ncu_dgemm_r02.json").get(tkey) or {}).get("dram_bytes_per_launch")})
@@ -661,7 +667,9 @@ def run_cfg5(args):
         "config": {"workload": cfg5_name(args, qy, qx), "iterations_per_step": 2 * K,
                    "inner": f"InnerSolver(rule='budget', max_iter={K}, precond_mode='{args.precond_mode}') per species",
                    "preconditioner_mode": args.precond_mode,
-                   "gemm_schedule": (f"{levels} Strassen levels over batched DMMA GEMMs ({qy >> levels}^3 leaves)"
+                   "gemm_schedule": (f"{levels} Strassen levels: {7 ** levels} leaf products of "
+                                     f"{strassen_leaf(qy, levels)}^3 per preconditioner product in one strided-batch "
+                                     f"DMMA launch"
                                      if levels > 0 else "classic (one DMMA GEMM per product)"),
                    "l2": "inputs larger than L2 (each q x q state is 537 MB; 2 x (8 solver grids + 2 dense "
                          "inverses) = 10.7 GB resident" +
@@ -708,12 +716,16 @@ def cfg3_block(args, steps=5, K=200):
     e1.record()
     torch.cuda.synchronize()
     el = e0.elapsed_time(e1) / 1e3
+    lv = pre.uses_strassen()
+    sched = (f"2 dense products, each {7 ** lv} leaf products of {strassen_leaf(qy, lv)}^3 ({lv} Strassen levels) in "
+             f"one strided-batch DMMA launch" if lv > 0 else "2 DMMA GEMMs")
     out = {"workload": "cfg3 (BASELINE configs[2]): wave domain, P2, Dirichlet, N=2048, q=2047x2047, 5-term "
-                       "operator, elliptic_xnormal preconditioner (inverse: 2 DMMA GEMMs)",
+                       f"operator, elliptic_xnormal preconditioner (inverse: {sched})",
            "value": qy * qx * its / el, "unit": UNIT, "iterations_per_step": K, "ms_per_step": 1e3 * el / steps}
     out["roofline_hbm"] = hbm_passes(op, pre)
-    out["roofline"] = gemm_roofline(qy)
-    out["roofline"]["traffic"] = (profile_json("ncu_dgemm_r02.json").get(f"q{qy}") or {}).get("dram_bytes_per_launch")
+    out["roofline"] = gemm_roofline(qy, lv)
+    tkey = f"q{strassen_leaf(qy, lv)}x{7 ** lv}" if lv > 0 else f"q{qy}"
+    out["roofline"]["traffic"] = (profile_json("ncu_dgemm_r02.json").get(tkey) or {}).get("dram_bytes_per_launch")
     if not args.no_full:
         pre_b = pb.make_preconditioner("elliptic_xnormal", w.x, w.y, mode="banded")
         pb.mo_pcg(op, rhs, precond=pre_b, stop=stop, max_iter=10)
@@ -817,7 +829,8 @@ def run_cfg3(args):
         dist.barrier()
         dist.destroy_process_group()
         return
-    roof = gemm_roofline(qy) if world == 1 else None
+    lv = pre.uses_strassen() if (world == 1 and args.precond_mode == "inverse") else 0
+    roof = gemm_roofline(qy, lv) if world == 1 else None
     hbm = hbm_passes(op, pre) if world == 1 else None
     cpu = None
     if world == 1 and not args.no_cpu_baseline:

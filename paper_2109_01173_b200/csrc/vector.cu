@@ -745,8 +745,12 @@ __global__ void __launch_bounds__(ST) strassen_operands_kernel(const double* __r
     SFB_PDL_PROLOGUE();
     if (gate != nullptr && gate->status != SFB_PCG_RUNNING) return;
     constexpr int NQ = pow_int(4, L);
-    for (int r = blockIdx.x; r < rh; r += gridDim.x) {
-        for (int c = threadIdx.x; c < ch; c += ST) {
+    // work items: (row, ST-column chunk), round-robin over the CTAs (an even share
+    // for every CTA of the VB-block grid whatever the row count)
+    const int nchunk = (ch + ST - 1) / ST;
+    for (int item = blockIdx.x; item < rh * nchunk; item += gridDim.x) {
+        const int r = item / nchunk, c = (item - r * nchunk) * ST + threadIdx.x;
+        if (c < ch) {
             double x[NQ];
             #pragma unroll
             for (int q = 0; q < NQ; ++q) {
@@ -771,8 +775,10 @@ __global__ void __launch_bounds__(ST) strassen_assemble_kernel(const double* __r
     if (st != nullptr && st->status != SFB_PCG_RUNNING) return;
     constexpr int NQ = pow_int(4, L);
     double dot = 0.0;
-    for (int r = blockIdx.x; r < rh; r += gridDim.x) {
-        for (int c = threadIdx.x; c < ch; c += ST) {
+    const int nchunk = (ch + ST - 1) / ST;
+    for (int item = blockIdx.x; item < rh * nchunk; item += gridDim.x) {
+        const int r = item / nchunk, c = (item - r * nchunk) * ST + threadIdx.x;
+        if (c < ch) {
             const size_t o = (size_t)r * ldm + c;
             double out[NQ];
             StrassenUp<L>::run(out, 0, [&](int leaf) { return __ldg(Mp + leaf * mstride + o); });
@@ -804,7 +810,7 @@ int vector_grid_blocks() { return VB; }
 
 int launch_strassen_operands(int levels, int side, const double* X, int ldx, int rows, int cols, int rh, int ch,
                              double* S, int lds, size_t sstride, const PcgState* gate, cudaStream_t s) {
-    const dim3 grid(std::max(1, std::min(VB, rh))), block(ST);
+    const dim3 grid(std::max(1, std::min(VB, rh * ((ch + ST - 1) / ST)))), block(ST);
 #define SFB_OPERANDS(L, SIDE)                                                                                      \
     if (levels == L && side == SIDE) {                                                                             \
         SFB_TRY(launch_kernel(strassen_operands_kernel<L, SIDE>, grid, block, 0, s, X, ldx, rows, cols, rh, ch, S, \
@@ -825,7 +831,7 @@ int launch_strassen_operands(int levels, int side, const double* X, int ldx, int
 int launch_strassen_assemble(int levels, const double* Mp, int ldm, size_t mstride, int rh, int ch, double* C, int ldc,
                              int rows, int cols, const double* D, int ldd, double* partials, PcgState* st,
                              double* dot_out, unsigned* counter, cudaStream_t s) {
-    const dim3 grid(std::max(1, std::min(VB, rh))), block(ST);
+    const dim3 grid(std::max(1, std::min(VB, rh * ((ch + ST - 1) / ST)))), block(ST);
 #define SFB_ASSEMBLE(L)                                                                                          \
     if (levels == L) {                                                                                           \
         SFB_TRY(launch_kernel(strassen_assemble_kernel<L>, grid, block, 0, s, Mp, ldm, mstride, rh, ch, C, ldc, rows, \

@@ -32,7 +32,10 @@ for q in [int(a) for a in sys.argv[1:]] or [4096, 8192]:
     R = torch.randn(q, q, dtype=torch.float64, device="cuda", generator=g)
     Z = torch.empty_like(R)
     ref = A @ (R @ Bt.T)
+    only = os.environ.get("STRASSEN_PROBE_LEVELS")  # e.g. "3": just that schedule (ncu captures)
     for name, levels in (("classic", 0), ("strassen-1", 1), ("strassen-2", 2), ("strassen-3", 3)):
+        if only is not None and str(levels) not in only.split(","):
+            continue
         h = make(q, A, Bt, levels)
         if L.sfb_pre_uses_strassen(h) != levels:  # leaves below the minimum size
             nat.check(L.sfb_pre_destroy(h), "destroy")
