@@ -27,6 +27,7 @@
 #include "sfb_tma.cuh"
 
 #include <cstdlib>
+#include <string>
 
 namespace sfb {
 
@@ -458,6 +459,17 @@ int tile_mode() {
     return m;
 }
 
+// SYLFEM_B200_BATCH_SCHED=streamk: the strided batch as pure stream-K (tile
+// boundaries, hence epilogue store bursts, spread over time across the CTAs)
+// instead of data-parallel waves + a stream-K tail
+bool batch_stream_k() {
+    static const bool v = [] {
+        const char* e = std::getenv("SYLFEM_B200_BATCH_SCHED");
+        return e != nullptr && std::string(e) == "streamk";
+    }();
+    return v;
+}
+
 int make_map3(CUtensorMap* map, const double* ptr, int rows, int cols, int ld, int box_rows, int nb) {
     if (!tma_aligned(ptr, ld)) return arg_error("DMMA GEMM operands need 16-byte aligned rows (even leading dimension)");
     const cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)rows, (cuuint64_t)nb};
@@ -497,7 +509,7 @@ int launch_tile_batch(const double* A, int lda, const double* Bt, int ldb, int n
         sc.G = tiles;
         sc.waves = 1;  // CTA c: tile c, whole
         sc.U = 0;
-    } else if (tiles > slots && GEMM_HYBRID) {
+    } else if (tiles > slots && GEMM_HYBRID && !(BATCH && batch_stream_k())) {
         sc.G = slots;
         sc.waves = tiles / slots - 1;  // keep one wave + the remainder in the stream-K tail
         sc.U = (long long)(tiles - sc.waves * slots) * sc.KT;
