@@ -137,7 +137,8 @@ int launch_strassen_operands(int levels, int side, const double* X, int ldx, int
                              double* S, int lds, size_t sstride, const PcgState* gate, cudaStream_t s);
 int launch_strassen_assemble(int levels, const double* Mp, int ldm, size_t mstride, int rh, int ch, double* C, int ldc,
                              int rows, int cols, const double* D, int ldd, double* partials, PcgState* st,
-                             double* dot_out, unsigned* counter, cudaStream_t s);
+                             double* dot_out, unsigned* counter, cudaStream_t s, int hmode = EPI_STORE,
+                             const double* sr = nullptr, const double* sc = nullptr);  // hmode: EPI_HADAMARD_* scaling
 int launch_transpose(const double* src, int lds, double* dst, int ldd, int rows, int cols, cudaStream_t s);
 int launch_sh_update(double* U, double* R, const double* Q, const double* W, int ld, int rows, int cols,
                      double alpha, double* partials, RedSlots* out, cudaStream_t s);

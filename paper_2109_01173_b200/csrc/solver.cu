@@ -168,7 +168,8 @@ struct sfb_pre {
     double *sl = nullptr, *sr = nullptr;
     // INVERSE, large shapes divisible by 4: the five Strassen block sums of
     // A1 and B1 (the constant left operands of the two products), formed once
-    sfb::StrassenPlan *planA = nullptr, *planB = nullptr;
+    sfb::StrassenPlan *planA = nullptr, *planB = nullptr;    // of A1, B1
+    sfb::StrassenPlan *planAt = nullptr, *planBt = nullptr;  // of A1t, B1t (spectral sandwich)
     int strassen_levels = 0;
     bool strassen = false;
     // BANDED: factors prepared for the SPIKE solves (spike.cu)
@@ -326,7 +327,8 @@ size_t strassen_scratch_doubles(int qy, int qx, int levels) {
 // (split only when they exceed the stream-K ticket array), one assembly pass.
 int strassen_apply(const StrassenPlan* pl, const double* Bt, int ldb, int N, double* scratch, double* C, int ldc,
                    const double* D, int ldd, double* partials, PcgState* pcg, double* dot_out, unsigned* counter,
-                   const GemmWs* gw, cudaStream_t s) {
+                   const GemmWs* gw, cudaStream_t s, int hmode = EPI_STORE, const double* sr = nullptr,
+                   const double* sc = nullptr) {
     const int L = pl->levels, mh = pl->mh, nh = strassen_leaf(N, L), kh = pl->kh;
     const int ldk = pl->ldk, ldn = pad_ld(nh);
     const size_t sa = (size_t)mh * ldk, sb = (size_t)nh * ldk, sm = (size_t)mh * ldn;
@@ -345,7 +347,7 @@ int strassen_apply(const StrassenPlan* pl, const double* Bt, int ldb, int N, dou
                                       (long long)sm, with_ws(e, gw), s));
     }
     return launch_strassen_assemble(L, Mp, ldn, sm, mh, nh, C, ldc, pl->M, N, D, ldd, partials, pcg, dot_out, counter,
-                                    s);
+                                    s, hmode, sr, sc);
 }
 
 // Z = P^-1 R (or the reduced-solve sandwich).  R/Z device buffers with even
@@ -391,6 +393,20 @@ int pre_apply_impl(const sfb_pre* p, const double* R, int ldr, double* Z, int ld
         }
         case SFB_PRE_SPECTRAL_PROD:
         case SFB_PRE_SPECTRAL_SUM: {
+            if (p->strassen && gw != nullptr && gw->strassen != nullptr) {
+                // the same four products with the constant factor on the left of each:
+                // T1 = V_R^T R^T; T2 = (V_L^T T1^T) o K; T1 = V_R T2^T; Z = V_L T1^T (+ <Z,R>)
+                const int hm = p->kind == SFB_PRE_SPECTRAL_SUM ? EPI_HADAMARD_SUM : EPI_HADAMARD_PROD;
+                SFB_TRY(strassen_apply(p->planBt, R, ldr, qy, gw->strassen, T1, ldt1, nullptr, 0, nullptr, pcg, nullptr,
+                                       nullptr, gw, s));
+                SFB_TRY(strassen_apply(p->planAt, T1, ldt1, qx, gw->strassen, T2, ldt2, nullptr, 0, nullptr, pcg,
+                                       nullptr, nullptr, gw, s, hm, p->sl, p->sr));
+                SFB_TRY(strassen_apply(p->planB, T2, ldt2, qy, gw->strassen, T1, ldt1, nullptr, 0, nullptr, pcg, nullptr,
+                                       nullptr, gw, s));
+                const bool dot = pcg || red;
+                return strassen_apply(p->planA, T1, ldt1, qx, gw->strassen, Z, ldz, dot ? R : nullptr, ldr, partials,
+                                      pcg, red ? &red->v[3] : nullptr, counter, gw, s);
+            }
             GemmEpi e1;  // T1 = (R V_R)^T
             e1.mode = EPI_STORE_T;
             e1.C = T1;
@@ -961,6 +977,16 @@ int sfb_pre_create(int qy, int qx, int kind, const double* L, const double* R, c
         if (rc == SFB_OK) rc = cudaMemset(p->B1t, 0, (size_t)qx * p->ldB * 8) == cudaSuccess ? SFB_OK : SFB_ERR_CUDA;
         if (rc == SFB_OK) rc = launch_transpose(p->B1, p->ldB, p->B1t, p->ldB, qx, qx, nullptr);
         if (rc == SFB_OK && cudaDeviceSynchronize() != cudaSuccess) rc = SFB_ERR_CUDA;
+        const int levels = strassen_levels(qy, qx);
+        if (rc == SFB_OK && levels > 0) {
+            rc = build_strassen_plan(p->A1, p->ldA, qy, qy, levels, &p->planA);
+            if (rc == SFB_OK) rc = build_strassen_plan(p->A1t, p->ldA, qy, qy, levels, &p->planAt);
+            if (rc == SFB_OK) rc = build_strassen_plan(p->B1, p->ldB, qx, qx, levels, &p->planB);
+            if (rc == SFB_OK) rc = build_strassen_plan(p->B1t, p->ldB, qx, qx, levels, &p->planBt);
+            if (rc == SFB_OK && cudaDeviceSynchronize() != cudaSuccess) rc = SFB_ERR_CUDA;
+            p->strassen = rc == SFB_OK;
+            p->strassen_levels = levels;
+        }
         std::vector<double> vl(lamL, lamL + qy), vr(lamR, lamR + qx);
         if (kind == SFB_PRE_SPECTRAL_PROD) {
             for (auto& v : vl) v = 1.0 / v;
@@ -1059,7 +1085,7 @@ int sfb_reduced_destroy(sfb_reduced* r) {
     if (!r) return SFB_OK;
     if (r->exec) cudaGraphExecDestroy(r->exec);
     for (void* p : {(void*)r->B, (void*)r->U, (void*)r->W, (void*)r->T1, (void*)r->T2, (void*)r->parts,
-                    (void*)r->red, (void*)r->gw.ws, (void*)r->gw.flags})
+                    (void*)r->red, (void*)r->gw.ws, (void*)r->gw.flags, (void*)r->gw.strassen})
         cudaFree(p);
     if (r->host) cudaFreeHost(r->host);
     if (r->stream) cudaStreamDestroy(r->stream);
@@ -1090,6 +1116,8 @@ int sfb_reduced_create(const sfb_pre* pre, const sfb_op* op, sfb_reduced** out) 
     if (rc == SFB_OK) rc = dalloc(&r->T2, g);
     if (rc == SFB_OK) rc = dalloc(&r->parts, 4 * nparts);  // launch_norms: 4 partials per block
     if (rc == SFB_OK) rc = dalloc(&r->gw.ws, gemm_workspace_doubles());
+    if (rc == SFB_OK && pre->strassen)
+        rc = dalloc(&r->gw.strassen, strassen_scratch_doubles(r->qy, r->qx, pre->strassen_levels));
     if (rc == SFB_OK && (cudaMalloc(reinterpret_cast<void**>(&r->red), 3 * sizeof(RedSlots)) != cudaSuccess ||
                          cudaMalloc(reinterpret_cast<void**>(&r->gw.flags), gemm_max_tiles() * sizeof(unsigned)) !=
                              cudaSuccess ||
@@ -1214,6 +1242,8 @@ int sfb_pre_destroy(sfb_pre* p) {
     cudaFree(p->sr);
     free_strassen_plan(p->planA);
     free_strassen_plan(p->planB);
+    free_strassen_plan(p->planAt);
+    free_strassen_plan(p->planBt);
     free_spike_factor(p->fl);
     free_spike_factor(p->fr);
     delete p;

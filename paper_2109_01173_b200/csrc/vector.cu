@@ -770,7 +770,8 @@ __global__ void __launch_bounds__(ST) strassen_assemble_kernel(const double* __r
                                                                int rh, int ch, double* __restrict__ C, int ldc,
                                                                int rows, int cols, const double* __restrict__ D,
                                                                int ldd, double* partials, PcgState* st, double* dot_out,
-                                                               unsigned* counter) {
+                                                               unsigned* counter, int hmode, const double* __restrict__ sr,
+                                                               const double* __restrict__ sc) {
     SFB_PDL_PROLOGUE();
     if (st != nullptr && st->status != SFB_PCG_RUNNING) return;
     constexpr int NQ = pow_int(4, L);
@@ -786,8 +787,12 @@ __global__ void __launch_bounds__(ST) strassen_assemble_kernel(const double* __r
             for (int q = 0; q < NQ; ++q) {
                 const int row = quad_row<L>(q) * rh + r, col = quad_col<L>(q) * ch + c;
                 if (row < rows && col < cols) {
-                    C[(size_t)row * ldc + col] = out[q];
-                    if (D != nullptr) dot = fma(out[q], D[(size_t)row * ldd + col], dot);
+                    double v = out[q];
+                    // the spectral sandwich's Hadamard scaling, as in the GEMM epilogues (solvers.py:245-253)
+                    if (hmode == EPI_HADAMARD_SUM) v *= 1.0 / (sr[row] + sc[col]);
+                    else if (hmode == EPI_HADAMARD_PROD) v *= sr[row] * sc[col];
+                    C[(size_t)row * ldc + col] = v;
+                    if (D != nullptr) dot = fma(v, D[(size_t)row * ldd + col], dot);
                 }
             }
         }
@@ -830,12 +835,13 @@ int launch_strassen_operands(int levels, int side, const double* X, int ldx, int
 
 int launch_strassen_assemble(int levels, const double* Mp, int ldm, size_t mstride, int rh, int ch, double* C, int ldc,
                              int rows, int cols, const double* D, int ldd, double* partials, PcgState* st,
-                             double* dot_out, unsigned* counter, cudaStream_t s) {
+                             double* dot_out, unsigned* counter, cudaStream_t s, int hmode, const double* sr,
+                             const double* sc) {
     const dim3 grid(std::max(1, std::min(VB, rh * ((ch + ST - 1) / ST)))), block(ST);
 #define SFB_ASSEMBLE(L)                                                                                          \
     if (levels == L) {                                                                                           \
         SFB_TRY(launch_kernel(strassen_assemble_kernel<L>, grid, block, 0, s, Mp, ldm, mstride, rh, ch, C, ldc, rows, \
-                              cols, D, ldd, partials, st, dot_out, counter));                                    \
+                              cols, D, ldd, partials, st, dot_out, counter, hmode, sr, sc));                     \
         SFB_CHECK_LAUNCH();                                                                                      \
         return SFB_OK;                                                                                           \
     }

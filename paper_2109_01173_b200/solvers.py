@@ -573,6 +573,12 @@ class SpectralCache:
         return h.p
 
 
+    def uses_strassen(self) -> int:
+        """Strassen levels of the four products of the spectral sandwich (0: one
+        DMMA GEMM each; see set_strassen_min_q)."""
+        return int(nat.lib().sfb_pre_uses_strassen(self.native()))
+
+
 def _dense_device(m):
     """Dense fp64 CUDA copy of a factor; band-stored factors are scattered on
     the device from their (row, col, value) triplets (no dense host array)."""

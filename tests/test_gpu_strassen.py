@@ -143,3 +143,60 @@ def test_batched_gemm_matches_fp64_matmul(M, N, K, nb):
         ref = A[b, :, :K] @ B[b, :, :K].T
         assert float((out[b, :, :N] - ref).norm() / ref.norm()) <= 1e-14
     assert float(out[:, :, N:].abs().max()) == 0.0  # nothing stored past the N columns
+
+
+# ---- the spectral sandwich (four products, Hadamard scaling in the second assembly pass) ----
+def test_strassen_spectral_preconditioner_form_matches_classic(strassen_from_256):
+    x, y = _lumped_sets(383, 511)  # q = (512, 384)
+    kw = {"d_u": 20.0, "tau": 1.25e-5, "lumped": True}
+    pre_s = pb.make_preconditioner("parabolic_lumped", x, y, mode="spectral", **kw)
+    assert pre_s.uses_strassen() == min(strassen_from_256, 2)
+    prev = pb.set_strassen_min_q(0)
+    try:
+        pre_c = pb.make_preconditioner("parabolic_lumped", x, y, mode="spectral", **kw)
+        assert pre_c.uses_strassen() == 0
+    finally:
+        pb.set_strassen_min_q(prev)
+    R = np.random.default_rng(3).standard_normal((y.q, x.q))
+    Zs, Zc = pre_s.apply_inverse(R), pre_c.apply_inverse(R)
+    assert relerr(Zs, Zc) <= 1e-12
+    ox, oy = orc.direction_sets(orc.unit_square(), 1, (383, 511), orc.NEUMANN, lumped=True)
+    opre = orc.LUPrecond(*orc.precond_factors("parabolic_lumped", ox, oy, **kw))
+    assert relerr(Zs, opre.inverse(R)) <= 1e-10
+
+
+def test_strassen_reduced_solve_vs_oracle(strassen_from_256):
+    """cfg1-type reduced solve (square, P1, Dirichlet) at q = 511 (odd: padded inside the passes)."""
+    N = 512
+    x, y = pb.build_direction_sets(pb.SQUARE, 1, N, pb.BCKind.DIRICHLET)
+    op, rhs_of = pb.elliptic_operator(x, y, 1.0)
+    a, b, c = orc.seeded_modes(1)
+    s = np.arange(N + 1) / N
+    F = sum(c[m] * np.sin(b[m] * np.pi * s)[:, None] * np.sin(a[m] * np.pi * s)[None, :] for m in range(8))
+    rhs = rhs_of(F)
+    cache = pb.build_spectral_cache(op)
+    assert cache.uses_strassen() == strassen_from_256
+    rep = pb.solve_reduced(op, rhs, cache=cache)
+    ox, oy = orc.direction_sets(orc.unit_square(), 1, N, orc.DIRICHLET)
+    terms, orhs = orc.elliptic_terms(ox, oy, 1.0)
+    U, res, _ = orc.reduced_solve(terms, orhs(F))
+    assert relerr(rep.solution, U) <= 1e-10
+    assert rep.residual_history[-1] <= 1e-10
+
+
+def test_strassen_reduced_solve_swapped_pencil_vs_oracle(strassen_from_256):
+    """cfg2-type reduced solve (Neumann P3 on [0,2]x[0,1], the swapped pencil) at q = 304."""
+    from paper_2109_01173_b200 import workloads as wl
+
+    w = wl.cfg2(N=303)
+    assert w.op.shape == (304, 304)
+    cache = pb.build_spectral_cache(w.op)
+    assert cache.uses_strassen() == min(strassen_from_256, 2)
+    rep = pb.solve_reduced(w.op, w.rhs, cache=cache)
+    ox, oy = orc.direction_sets(orc.rect_domain(), 3, w.N, orc.NEUMANN)
+    terms, orhs = orc.elliptic_terms(ox, oy, 0.5)
+    rhs = orhs(wl.cosine_source_rect(w.N, 2))
+    assert relerr(w.rhs, rhs) <= 1e-13
+    U, res, c = orc.reduced_solve(terms, rhs)
+    assert bool(c["swapped"]) and rep.diagnostics["pencil_swapped"] is True
+    assert relerr(rep.solution, U) <= 1e-10
