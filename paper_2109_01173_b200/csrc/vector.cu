@@ -676,8 +676,6 @@ struct StrassenDown {
         #pragma unroll
         for (int i = 0; i < 7; ++i) {
             double y[NS];
-            constexpr int dummy = 0;
-            (void)dummy;
             const int qa = StrassenIn<SIDE>::qa(i), qb = StrassenIn<SIDE>::qb(i);
             #pragma unroll
             for (int m = 0; m < NS; ++m) {
@@ -696,7 +694,7 @@ struct StrassenUp {
     template <class Load>
     __device__ __forceinline__ static void run(double (&out)[pow_int(4, L)], int prefix, Load&& ld) {
         constexpr int NS = pow_int(4, L - 1);
-        // product i adds into quadrant ca (+) and cb (sign sb; -1: none); the first writer of a quadrant assigns
+        // product i adds into quadrant ca (+) and cb (minus when mb; -1: none); the first writer of a quadrant assigns
         constexpr int ca[7] = {0, 2, 1, 0, 1, 3, 0};     // +C11 +C21 +C12 +C11 +C12 +C22 +C11
         constexpr int cb[7] = {3, 3, 3, 2, 0, -1, -1};   // +C22 -C22 +C22 +C21 -C11
         constexpr bool mb[7] = {false, true, false, false, true, false, false};
