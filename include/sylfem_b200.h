@@ -174,7 +174,7 @@ int sfb_pre_create(int qy, int qx, int kind, const double* L,
  * SYLFEM_B200_STRASSEN_MINQ or 2000).  Returns the previous threshold. */
 int sfb_set_strassen_min_q(int min_q);
 /* Most Strassen levels taken (0..3, default SYLFEM_B200_STRASSEN_LEVELS or 3);
- * the leaves must be at least min_q / 4 (not below 64).
+ * the leaves must be at least min_q / 4 (not below 16).
  * Returns the previous value. */
 int sfb_set_strassen_levels(int levels);
 /* Strassen levels this preconditioner's products use (0: classic GEMMs). */
@@ -340,6 +340,22 @@ int sfb_shard_gemm(sfb_shard* h, const double* A_dev, int lda, const double* Bt_
 int sfb_shard_gemm_scatter(sfb_shard* h, const double* A_dev, int lda, const double* Bt_dev, int ldb,
                            int M, int N, int K, int nseg, const int* seg_host,
                            double* const* dst_host, const int* ldd_host, int col_off, void* stream);
+/* A constant left operand A (M x K) of repeated products C = A Bt^T, Bt of up
+ * to max_n rows -- the full P_L^-1 / P_R^-T of the column-sharded inverse-form
+ * preconditioner (solvers.py:134-143 on shards): prepared once (Strassen leaf
+ * operands and scratch when M, K reach the threshold of sfb_set_strassen_min_q;
+ * sfb_const_levels reports the levels, 0 = plain DMMA GEMM); the products are
+ * gated on the shard state like sfb_shard_gemm / sfb_shard_gemm_scatter.  A
+ * must outlive the handle. */
+typedef struct sfb_const sfb_const;
+int sfb_const_create(const double* A_dev, int lda, int M, int K, int max_n, sfb_const** out);
+int sfb_const_levels(const sfb_const* c);
+int sfb_const_destroy(sfb_const* c);
+int sfb_shard_gemm_const(sfb_shard* h, const sfb_const* c, const double* Bt_dev, int ldb, int N,
+                         double* C_dev, int ldc, void* stream);
+int sfb_shard_gemm_scatter_const(sfb_shard* h, const sfb_const* c, const double* Bt_dev, int ldb, int N,
+                                 int nseg, const int* seg_host, double* const* dst_dev_host,
+                                 const int* ldd_host, int col_off, void* stream);
 int sfb_shard_pre_apply(sfb_shard* h, const sfb_pre* p, const double* R_dev, int ldr, double* Z_dev,
                         int ldz, void* stream);
 /* status, iterations, bad value / iteration; history (iterations + 1) and increments (iterations) */

@@ -41,6 +41,7 @@ EXPORTS = [
     "sfb_shard_create", "sfb_shard_destroy", "sfb_shard_slots", "sfb_shard_dots", "sfb_shard_start",
     "sfb_shard_update", "sfb_shard_control", "sfb_shard_xpby", "sfb_shard_result",
     "sfb_shard_apply", "sfb_shard_gemm", "sfb_shard_gemm_scatter", "sfb_shard_pre_apply",
+    "sfb_const_create", "sfb_const_levels", "sfb_const_destroy", "sfb_shard_gemm_const", "sfb_shard_gemm_scatter_const",
     "sfb_lu_create", "sfb_lu_solve", "sfb_lu_destroy",
 ]
 IMEX_OK, IMEX_BLOWUP, IMEX_NOT_CONVERGED, IMEX_INDEFINITE, IMEX_NONFINITE = range(5)
@@ -123,6 +124,11 @@ _SIGS = {
     "sfb_shard_apply": (_I, [_P, _P, _P, _I, _P, _I, _P]),
     "sfb_shard_gemm": (_I, [_P, _P, _I, _P, _I, _I, _I, _I, _P, _I, _P]),
     "sfb_shard_gemm_scatter": (_I, [_P, _P, _I, _P, _I, _I, _I, _I, _I, _P, _P, _P, _I, _P]),
+    "sfb_const_create": (_I, [_P, _I, _I, _I, _I, C.POINTER(_P)]),
+    "sfb_const_levels": (_I, [_P]),
+    "sfb_const_destroy": (_I, [_P]),
+    "sfb_shard_gemm_const": (_I, [_P, _P, _P, _I, _I, _P, _I, _P]),
+    "sfb_shard_gemm_scatter_const": (_I, [_P, _P, _P, _I, _I, _I, _P, _P, _P, _I, _P]),
     "sfb_shard_pre_apply": (_I, [_P, _P, _P, _I, _P, _I, _P]),
     "sfb_lu_create": (_I, [_I, C.c_longlong, _P, _P, _P, C.c_longlong, _P, _P, _P, _P, _P, C.POINTER(_P)]),
     "sfb_lu_solve": (_I, [_P, _P, _P, _P]),

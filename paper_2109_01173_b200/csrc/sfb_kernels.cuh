@@ -128,6 +128,17 @@ int launch_loop_ctl(PcgState* st, unsigned long long handle, int use_handle, cud
 int launch_norms(const double* A, int lda, const double* B, int ldb, int rows, int cols, double* partials,
                  RedSlots* out, cudaStream_t s);
 int vector_grid_blocks();
+// Row-scatter destinations of an assembled product (the sharded preconditioner's
+// transpose fused into its product, as EPI_SCATTER of the GEMM): row m of C with
+// seg[d] <= m < seg[d+1] goes to dst[d][(m - seg[d]) * ldd[d] + col_off + n]
+struct ScatterArgs {
+    int nseg = 0;
+    int seg[kMaxScatter + 1] = {};
+    double* dst[kMaxScatter] = {};
+    int ldd[kMaxScatter] = {};
+    int col_off = 0;
+};
+
 // Strassen schedule, `levels` levels flattened (vector.cu): all 7^levels leaf
 // operands (rh x ch each, at S + l * sstride) of X (rows x cols, read as
 // (rh 2^levels) x (ch 2^levels) with zeros past its extents; side 0: left
@@ -138,7 +149,8 @@ int launch_strassen_operands(int levels, int side, const double* X, int ldx, int
 int launch_strassen_assemble(int levels, const double* Mp, int ldm, size_t mstride, int rh, int ch, double* C, int ldc,
                              int rows, int cols, const double* D, int ldd, double* partials, PcgState* st,
                              double* dot_out, unsigned* counter, cudaStream_t s, int hmode = EPI_STORE,
-                             const double* sr = nullptr, const double* sc = nullptr);  // hmode: EPI_HADAMARD_* scaling
+                             const double* sr = nullptr, const double* sc = nullptr,  // hmode: EPI_HADAMARD_* scaling
+                             const ScatterArgs* scatter = nullptr);  // set: rows go to the destinations, C unused
 int launch_transpose(const double* src, int lds, double* dst, int ldd, int rows, int cols, cudaStream_t s);
 int launch_sh_update(double* U, double* R, const double* Q, const double* W, int ld, int rows, int cols,
                      double alpha, double* partials, RedSlots* out, cudaStream_t s);

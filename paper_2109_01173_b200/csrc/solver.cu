@@ -271,7 +271,7 @@ int strassen_leaf(int q, int L) { return (round_up(q, 2 << L)) >> L; }
 int strassen_levels_of(int q) {
     const int m = strassen_min_q();
     if (m <= 0 || q < m) return 0;
-    const int leaf = std::max(m / 4, 64);
+    const int leaf = std::max(m / 4, 16);
     for (int L = strassen_max_levels_slot().load(std::memory_order_relaxed); L > 0; --L)
         if (strassen_leaf(q, L) >= leaf) return L;
     return 0;
@@ -328,7 +328,7 @@ size_t strassen_scratch_doubles(int qy, int qx, int levels) {
 int strassen_apply(const StrassenPlan* pl, const double* Bt, int ldb, int N, double* scratch, double* C, int ldc,
                    const double* D, int ldd, double* partials, PcgState* pcg, double* dot_out, unsigned* counter,
                    const GemmWs* gw, cudaStream_t s, int hmode = EPI_STORE, const double* sr = nullptr,
-                   const double* sc = nullptr) {
+                   const double* sc = nullptr, const ScatterArgs* scatter = nullptr) {
     const int L = pl->levels, mh = pl->mh, nh = strassen_leaf(N, L), kh = pl->kh;
     const int ldk = pl->ldk, ldn = pad_ld(nh);
     const size_t sa = (size_t)mh * ldk, sb = (size_t)nh * ldk, sm = (size_t)mh * ldn;
@@ -347,7 +347,7 @@ int strassen_apply(const StrassenPlan* pl, const double* Bt, int ldb, int N, dou
                                       (long long)sm, with_ws(e, gw), s));
     }
     return launch_strassen_assemble(L, Mp, ldn, sm, mh, nh, C, ldc, pl->M, N, D, ldd, partials, pcg, dot_out, counter,
-                                    s, hmode, sr, sc);
+                                    s, hmode, sr, sc, scatter);
 }
 
 // Z = P^-1 R (or the reduced-solve sandwich).  R/Z device buffers with even
@@ -1774,6 +1774,88 @@ int sfb_shard_gemm_scatter(sfb_shard* h, const double* A, int lda, const double*
     e.col_off = col_off;
     e.pcg = h->st;
     return launch_dgemm_nt(A, lda, Bt, ldb, M, N, K, with_ws(e, &h->gw), (cudaStream_t)stream);
+}
+
+// ---- a constant left operand of repeated products (sharded preconditioner) ----
+// The column-sharded inverse-form preconditioner multiplies by the full P_L^-1 and
+// P_R^-T every iteration (C = A Bt^T with Bt a rank's rows / columns): the operand is
+// prepared once -- its Strassen leaf operands and the scratch for right operands of up
+// to max_n rows -- and the products run as in the single-GPU schedule (operands pass,
+// one strided-batch leaf launch, assembly pass; the assembly can scatter its rows to
+// peer GPUs' buffers like the GEMM's EPI_SCATTER epilogue).  Below the Strassen
+// threshold it is the plain DMMA GEMM.
+struct sfb_const {
+    const double* A = nullptr;
+    int lda = 0, M = 0, K = 0, max_n = 0;
+    sfb::StrassenPlan* plan = nullptr;
+    double* scratch = nullptr;
+};
+
+int sfb_const_destroy(sfb_const* c) {
+    if (!c) return SFB_OK;
+    free_strassen_plan(c->plan);
+    cudaFree(c->scratch);
+    delete c;
+    return SFB_OK;
+}
+
+int sfb_const_create(const double* A, int lda, int M, int K, int max_n, sfb_const** out) {
+    if (!A || !out || M <= 0 || K <= 0 || max_n <= 0) return arg_error("constant operand: bad argument");
+    auto* c = new sfb_const;
+    c->A = A;
+    c->lda = lda;
+    c->M = M;
+    c->K = K;
+    c->max_n = max_n;
+    int levels = std::min(strassen_levels_of(M), strassen_levels_of(K));
+    while (levels > 0 && strassen_leaf(max_n, levels) < 16) --levels;  // thin shards: fewer levels
+    if (levels > 0) {
+        int rc = build_strassen_plan(A, lda, M, K, levels, &c->plan);
+        if (rc == SFB_OK) {
+            const int mh = strassen_leaf(M, levels), nh = strassen_leaf(max_n, levels);
+            const size_t n = (size_t)c->plan->leaves * ((size_t)nh * c->plan->ldk + (size_t)mh * pad_ld(nh));
+            rc = dalloc(&c->scratch, n);
+        }
+        if (rc == SFB_OK && cudaDeviceSynchronize() != cudaSuccess) rc = SFB_ERR_CUDA;
+        if (rc != SFB_OK) {
+            sfb_const_destroy(c);
+            return rc;
+        }
+    }
+    *out = c;
+    return SFB_OK;
+}
+
+int sfb_const_levels(const sfb_const* c) { return c != nullptr && c->plan != nullptr ? c->plan->levels : 0; }
+
+int sfb_shard_gemm_const(sfb_shard* h, const sfb_const* c, const double* Bt, int ldb, int N, double* C, int ldc,
+                         void* stream) {
+    if (!h || !c || !Bt || !C) return arg_error("shard GEMM: null argument");
+    if (c->plan == nullptr || N > c->max_n)
+        return sfb_shard_gemm(h, c->A, c->lda, Bt, ldb, c->M, N, c->K, C, ldc, stream);
+    return strassen_apply(c->plan, Bt, ldb, N, c->scratch, C, ldc, nullptr, 0, nullptr, h->st, nullptr, nullptr, &h->gw,
+                          (cudaStream_t)stream);
+}
+
+int sfb_shard_gemm_scatter_const(sfb_shard* h, const sfb_const* c, const double* Bt, int ldb, int N, int nseg,
+                                 const int* seg, double* const* dst, const int* ldd, int col_off, void* stream) {
+    if (!h || !c || !Bt) return arg_error("shard scatter GEMM: null argument");
+    if (c->plan == nullptr || N > c->max_n)
+        return sfb_shard_gemm_scatter(h, c->A, c->lda, Bt, ldb, c->M, N, c->K, nseg, seg, dst, ldd, col_off, stream);
+    if (!seg || !dst || !ldd || nseg < 1 || nseg > kMaxScatter) return arg_error("shard scatter GEMM: bad argument");
+    ScatterArgs sa;
+    sa.nseg = nseg;
+    for (int i = 0; i <= nseg; ++i) sa.seg[i] = seg[i];
+    if (sa.seg[0] != 0 || sa.seg[nseg] != c->M) return arg_error("shard scatter GEMM: segments must cover the M rows");
+    for (int i = 0; i < nseg; ++i) {
+        if (sa.seg[i + 1] < sa.seg[i]) return arg_error("shard scatter GEMM: segments must be increasing");
+        if (!dst[i] && sa.seg[i + 1] > sa.seg[i]) return arg_error("shard scatter GEMM: null destination");
+        sa.dst[i] = dst[i];
+        sa.ldd[i] = ldd[i];
+    }
+    sa.col_off = col_off;
+    return strassen_apply(c->plan, Bt, ldb, N, c->scratch, nullptr, 0, nullptr, 0, nullptr, h->st, nullptr, nullptr,
+                          &h->gw, (cudaStream_t)stream, EPI_STORE, nullptr, nullptr, &sa);
 }
 
 int sfb_shard_pre_apply(sfb_shard* h, const sfb_pre* p, const double* R, int ldr, double* Z, int ldz, void* stream) {

@@ -763,13 +763,14 @@ __global__ void __launch_bounds__(ST) strassen_operands_kernel(const double* __r
 
 // leaf product l at Mp + l * mstride (rh x ch, ldm); C: rows x cols (ldc), the
 // leading part of the assembled (rh 2^L) x (ch 2^L)
-template <int L>
+template <int L, bool SCATTER>
 __global__ void __launch_bounds__(ST) strassen_assemble_kernel(const double* __restrict__ Mp, int ldm, size_t mstride,
                                                                int rh, int ch, double* __restrict__ C, int ldc,
                                                                int rows, int cols, const double* __restrict__ D,
                                                                int ldd, double* partials, PcgState* st, double* dot_out,
                                                                unsigned* counter, int hmode, const double* __restrict__ sr,
-                                                               const double* __restrict__ sc) {
+                                                               const double* __restrict__ sc,
+                                                               const __grid_constant__ ScatterArgs sa) {
     SFB_PDL_PROLOGUE();
     if (st != nullptr && st->status != SFB_PCG_RUNNING) return;
     constexpr int NQ = pow_int(4, L);
@@ -789,7 +790,13 @@ __global__ void __launch_bounds__(ST) strassen_assemble_kernel(const double* __r
                     // the spectral sandwich's Hadamard scaling, as in the GEMM epilogues (solvers.py:245-253)
                     if (hmode == EPI_HADAMARD_SUM) v *= 1.0 / (sr[row] + sc[col]);
                     else if (hmode == EPI_HADAMARD_PROD) v *= sr[row] * sc[col];
-                    C[(size_t)row * ldc + col] = v;
+                    if constexpr (SCATTER) {
+                        int d = 0;
+                        while (d + 1 < sa.nseg && row >= sa.seg[d + 1]) ++d;
+                        sa.dst[d][(size_t)(row - sa.seg[d]) * sa.ldd[d] + sa.col_off + col] = v;
+                    } else {
+                        C[(size_t)row * ldc + col] = v;
+                    }
                     if (D != nullptr) dot = fma(v, D[(size_t)row * ldd + col], dot);
                 }
             }
@@ -834,12 +841,18 @@ int launch_strassen_operands(int levels, int side, const double* X, int ldx, int
 int launch_strassen_assemble(int levels, const double* Mp, int ldm, size_t mstride, int rh, int ch, double* C, int ldc,
                              int rows, int cols, const double* D, int ldd, double* partials, PcgState* st,
                              double* dot_out, unsigned* counter, cudaStream_t s, int hmode, const double* sr,
-                             const double* sc) {
+                             const double* sc, const ScatterArgs* scatter) {
     const dim3 grid(std::max(1, std::min(VB, rh * ((ch + ST - 1) / ST)))), block(ST);
+    const ScatterArgs none;
 #define SFB_ASSEMBLE(L)                                                                                          \
     if (levels == L) {                                                                                           \
-        SFB_TRY(launch_kernel(strassen_assemble_kernel<L>, grid, block, 0, s, Mp, ldm, mstride, rh, ch, C, ldc, rows, \
-                              cols, D, ldd, partials, st, dot_out, counter, hmode, sr, sc));                     \
+        if (scatter != nullptr) {                                                                                \
+            SFB_TRY(launch_kernel(strassen_assemble_kernel<L, true>, grid, block, 0, s, Mp, ldm, mstride, rh, ch, C, \
+                                  ldc, rows, cols, D, ldd, partials, st, dot_out, counter, hmode, sr, sc, *scatter)); \
+        } else {                                                                                                 \
+            SFB_TRY(launch_kernel(strassen_assemble_kernel<L, false>, grid, block, 0, s, Mp, ldm, mstride, rh, ch, C, \
+                                  ldc, rows, cols, D, ldd, partials, st, dot_out, counter, hmode, sr, sc, none)); \
+        }                                                                                                        \
         SFB_CHECK_LAUNCH();                                                                                      \
         return SFB_OK;                                                                                           \
     }

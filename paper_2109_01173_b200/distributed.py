@@ -241,6 +241,7 @@ class PeerTransposes:
         import torch
         import torch.distributed as dist
         self.t, self.dist, self.L, self.group = torch, dist, layout, group
+        self.backend = backend  # its prepared constant operands (right_T_scatter)
         if sync not in ("host", "stream"):
             raise ConfigError(f"unknown peer sync mode '{sync}'")
         self.sync_mode = sync
@@ -336,7 +337,11 @@ class PeerTransposes:
         seg = (nat.C.c_int * (n + 1))(*(list(L.col_offs) + [L.qx]))
         dst = (nat.C.c_void_p * n)(*[p for p, _ in self.peer_colsT])
         ldd = (nat.C.c_int * n)(*[ld for _, ld in self.peer_colsT])
-        if st is not None:
+        const = getattr(self.backend, "_const", {}).get(A.data_ptr()) if st is not None else None
+        if const is not None:  # the prepared P_R^-T: same product, Strassen schedule above the threshold
+            nat.check(nat.lib().sfb_shard_gemm_scatter_const(st.handle.p, const.p, B.data_ptr(), B.stride(0), L.m, n,
+                                                             seg, dst, ldd, L.r0, nat.stream()), "scatter gemm")
+        elif st is not None:
             nat.check(nat.lib().sfb_shard_gemm_scatter(st.handle.p, A.data_ptr(), A.stride(0), B.data_ptr(),
                                                        B.stride(0), L.qx, L.m, L.qx, n, seg, dst, ldd, L.r0,
                                                        nat.stream()), "scatter gemm")
@@ -412,6 +417,15 @@ class CudaBackend:
             # formed on the device and kept there (no host round trip)
             self.Linv = self.from_host(precond._inverse(precond.left, qy, left=True))
             self.RinvT = self.from_host(precond._inverse(precond.right, qx, left=False).T)
+            # the two constant left operands, prepared once for the device-resident
+            # iteration (Strassen leaf operands from the threshold of set_strassen_min_q
+            # on; the right operands are this rank's columns / rows)
+            self._const = {}
+            for A, q, n_max in ((self.Linv, qy, layout.n), (self.RinvT, qx, layout.m)):
+                out = nat.C.c_void_p()
+                nat.check(L.sfb_const_create(A.data_ptr(), A.stride(0), q, q, max(int(n_max), 1), nat.C.byref(out)),
+                          "constant operand")
+                self._const[A.data_ptr()] = nat.Handle(out.value, L.sfb_const_destroy)
 
     # -- helpers ------------------------------------------------------------
     @staticmethod
@@ -461,6 +475,11 @@ class CudaBackend:
             Bs = self._padded(*Bt.shape)
             Bs.copy_(Bt)
         if st is not None:  # gated on the sharded solve's status
+            const = getattr(self, "_const", {}).get(As.data_ptr())
+            if const is not None:  # a prepared constant operand (P_L^-1, P_R^-T)
+                nat.check(nat.lib().sfb_shard_gemm_const(st.handle.p, const.p, Bs.data_ptr(), Bs.stride(0), N,
+                                                         C.data_ptr(), C.stride(0), nat.stream()), "gemm")
+                return C
             nat.check(nat.lib().sfb_shard_gemm(st.handle.p, As.data_ptr(), As.stride(0), Bs.data_ptr(), Bs.stride(0),
                                                M, N, K, C.data_ptr(), C.stride(0), nat.stream()), "gemm")
             return C

@@ -87,8 +87,10 @@ def worker(rank, world, port, N, out_dir, peer=False, mode="inverse"):
             torch.cuda.synchronize()
             dist.barrier()
             pt.close()
+        from paper_2109_01173_b200 import _native as nat
+        levels = [nat.lib().sfb_const_levels(h.p) for h in getattr(be, "_const", {}).values()]
         np.savez(os.path.join(out_dir, f"rank{rank}.npz"), U=rep.solution, iters=rep.iterations,
-                 hist=rep.residual_history)
+                 hist=rep.residual_history, strassen_levels=min(levels) if levels else 0)
     finally:
         dist.destroy_process_group()
 

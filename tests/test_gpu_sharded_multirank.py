@@ -41,6 +41,74 @@ def test_sharded_cuda_backend_multirank_matches_mo_pcg(world, peer, mode):
     assert relerr(U, ref["solution"]) <= 1e-10
 
 
+@pytest.mark.parametrize("world,peer", [(2, True), (3, False)])
+def test_sharded_cuda_backend_multirank_strassen_products(world, peer, monkeypatch):
+    """The shards' products with the full P_L^-1 / P_R^-T as prepared constant operands on the
+    Strassen schedule (threshold lowered through the environment of the spawned ranks; q = 95 is
+    odd: padded inside the passes), incl. the assembly pass that scatters to the peers' buffers."""
+    monkeypatch.setenv("SYLFEM_B200_STRASSEN_MINQ", "64")
+    N = 96
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(worker, args=(world, free_port(), N, d, peer, "inverse"), nprocs=world, join=True)
+        parts = [np.load(os.path.join(d, f"rank{r}.npz")) for r in range(world)]
+    assert all(int(p["strassen_levels"]) >= 1 for p in parts)
+    U = np.concatenate([p["U"] for p in parts], axis=1)
+    iters = {int(p["iters"]) for p in parts}
+    assert len(iters) == 1
+    terms, rhs, pinv = wave_oracle(2, N)
+    ref = orc.mo_pcg(terms, rhs, pinv, ("residual", 1e-12), max_iter=5000)
+    it, lo, hi = orc.iteration_envelope(terms, rhs, pinv, ("residual", 1e-12), max_iter=5000)
+    assert abs(iters.pop() - it) <= hi - lo + 1
+    assert relerr(U, ref["solution"]) <= 1e-10
+
+
+def test_constant_operand_products_match_the_plain_gemm():
+    """sfb_shard_gemm_const / sfb_shard_gemm_scatter_const (prepared constant left operand, Strassen
+    schedule) against the plain product and the scatter layout."""
+    import torch
+
+    from paper_2109_01173_b200 import _native as nat
+    from paper_2109_01173_b200.distributed import Layout, ShardState
+
+    L = nat.lib()
+    rng = np.random.default_rng(4)
+    qx, m, world, off = 302, 77, 3, 5
+    A = torch.from_numpy(rng.standard_normal((qx, qx))).cuda()
+    B = torch.from_numpy(rng.standard_normal((m, qx))).cuda()
+    ref = (A @ B.T).cpu().numpy()
+    prev = pb.set_strassen_min_q(64)
+    try:
+        out = nat.C.c_void_p()
+        nat.check(L.sfb_const_create(A.data_ptr(), qx, qx, qx, m, nat.C.byref(out)), "const")
+        const = nat.Handle(out.value, L.sfb_const_destroy)
+    finally:
+        pb.set_strassen_min_q(prev)
+    assert L.sfb_const_levels(const.p) == 2  # leaves of 76 x 76 (left) and 20 x 76 (right)
+    st = ShardState(10, pb.fixed_budget())
+    C = torch.zeros((qx, m + (m % 2)), dtype=torch.float64, device="cuda")
+    nat.check(L.sfb_shard_gemm_const(st.handle.p, const.p, B.data_ptr(), qx, m, C.data_ptr(), C.stride(0), nat.stream()),
+              "gemm")
+    assert relerr(C[:, :m].cpu().numpy(), ref) <= 1e-13
+    lay = Layout(qy=150, qx=qx, world=world, rank=0)
+    bufs = [torch.full((lay.col_counts[s], 130 + 2 * s), np.nan, dtype=torch.float64, device="cuda")
+            for s in range(world)]
+    seg = (nat.C.c_int * (world + 1))(*(list(lay.col_offs) + [qx]))
+    dst = (nat.C.c_void_p * world)(*[b.data_ptr() for b in bufs])
+    ldd = (nat.C.c_int * world)(*[b.stride(0) for b in bufs])
+    nat.check(L.sfb_shard_gemm_scatter_const(st.handle.p, const.p, B.data_ptr(), qx, m, world, seg, dst, ldd, off,
+                                             nat.stream()), "scatter")
+    torch.cuda.synchronize()
+    for s_ in range(world):
+        got = bufs[s_].cpu().numpy()
+        want = ref[lay.col_offs[s_]:lay.col_offs[s_] + lay.col_counts[s_]]
+        assert relerr(got[:, off:off + m], want) <= 1e-13
+        assert np.isnan(got[:, :off]).all() and np.isnan(got[:, off + m:]).all()  # nothing else touched
+    # a thinner right operand than prepared for, and one too wide (falls back to the plain GEMM)
+    nat.check(L.sfb_shard_gemm_const(st.handle.p, const.p, B.data_ptr(), qx, 40, C.data_ptr(), C.stride(0), nat.stream()),
+              "gemm")
+    assert relerr(C[:, :40].cpu().numpy(), ref[:, :40]) <= 1e-13
+
+
 def test_scatter_gemm_places_rows_like_the_transpose():
     """sfb_dgemm_nt_scatter with three local destinations (stand-ins for the
     ranks' column-shard buffers) against the plain GEMM and the layout."""
