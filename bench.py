@@ -510,7 +510,10 @@ def run_cfg5(args):
             pbuf.copy_(s if isinstance(s, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(s)))
         hstate = tuple(pbuf.numpy() for pbuf in pinned)
         if world == 1:
-            hstate = step(hstate).final  # warm: host result blocks enter the caching host allocator
+            # warm: the page-locked result blocks enter the caching host allocator -- two steps, since a
+            # step's inputs (the previous step's results) are still alive when its own results are allocated
+            for _ in range(2):
+                hstate = step(hstate).final
         barrier()
         e0.record()
         its_e = 0
