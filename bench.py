@@ -631,7 +631,15 @@ def run_cfg5(args):
                  "traffic": (profile_json("ncu_dgemm_r02.json").get(tkey) or {}).get("dram_bytes_per_launch")})
     if levels > 0:
         # the two dense products of one preconditioner application, as a whole
+        h = strassen_leaf(qy, levels)
+        # operand and assembly passes of the two products: (4^L + 7^L) leaf blocks in, out (+ R for <Z,R>)
+        pass_bytes = (2 * 2 * (4 ** levels + 7 ** levels) + 4 ** levels) * h * h * 8.0
+        pass_ms = hbm["preconditioner_ms"] - 2 * roof["launch_ms"]
         roof["preconditioner_application"] = {
+            "passes": {"ms": pass_ms, "algorithmic_bytes": pass_bytes, "achieved": pass_bytes / (pass_ms * 1e-3) / 1e9,
+                       "unit": "GB/s", "frac": pass_bytes / (pass_ms * 1e-3) / 1e9 / hbm["peak"],
+                       "note": "strassen_operands_kernel + strassen_assemble_kernel of both products: the "
+                               "application's time minus its two leaf launches"},
             "ms": hbm["preconditioner_ms"], "algorithmic_flops": 4.0 * qy ** 3,
             "algorithmic_tflops": 4.0 * qy ** 3 / (hbm["preconditioner_ms"] * 1e-3) / 1e12,
             "executed_flops": 4.0 * qy ** 3 * (7.0 / 8.0) ** levels,
