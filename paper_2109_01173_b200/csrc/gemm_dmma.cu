@@ -48,6 +48,9 @@ constexpr int KBOX = 16;  // doubles per 128-byte swizzled TMA box row (one box 
 #ifndef GEMM_SMALL_MINWORK
 #define GEMM_SMALL_MINWORK 4  // k-tiles per CTA at least, 64x64 tiles
 #endif
+#ifndef GEMM_WIDE_STORE
+#define GEMM_WIDE_STORE 1  // plain-store epilogue of whole tiles in 128-byte row segments
+#endif
 #ifndef GEMM_WM
 #define GEMM_WM 32  // rows per warp, 128 x 128 tiles: 32 (128 regs; measured +4 % at q = 2047 over 64 rows / 255 regs)
 #endif
@@ -151,6 +154,34 @@ __device__ __forceinline__ double tile_epilogue(double (&acc)[T::MI][T::NJ][2], 
                                                 int n0, int wm, int wn, int g, int t, size_t coff = 0) {
     constexpr int MI = T::MI, NJ = T::NJ;
     double dot = 0.0;
+#if GEMM_WIDE_STORE
+    // Plain store of a whole tile: lanes of neighbouring quads (g, g ^ 1) swap one of
+    // their two 8 x 8 blocks, so every store instruction writes four rows of 128
+    // contiguous bytes (two blocks side by side) instead of eight rows of 64.
+    if (ep.mode == EPI_STORE && (NJ % 2) == 0 && m0 + T::BM <= M && n0 + T::BN <= N && (ep.ldc % 2) == 0 &&
+        ((reinterpret_cast<uintptr_t>(ep.C) + coff * 8) & 15) == 0) {
+        const int odd = g & 1;
+        #pragma unroll
+        for (int i = 0; i < MI; ++i) {
+            const int me = m0 + wm * T::WM + i * 8 + (g & ~1);  // the pair's even row
+            #pragma unroll
+            for (int jp = 0; jp < NJ / 2; ++jp) {
+                const double a0 = acc[i][2 * jp][0], a1 = acc[i][2 * jp][1];          // row g, columns of block 2jp
+                const double b0 = acc[i][2 * jp + 1][0], b1 = acc[i][2 * jp + 1][1];  // row g, columns of block 2jp + 1
+                // even g sends its right block (it stores the left one of both rows), odd g its left block
+                const double s0 = odd ? a0 : b0, s1 = odd ? a1 : b1;
+                const double r0 = __shfl_xor_sync(0xffffffffu, s0, 4), r1 = __shfl_xor_sync(0xffffffffu, s1, 4);
+                const int n = n0 + wn * T::WN + (2 * jp + odd) * 8 + 2 * t;
+                double* c = ep.C + coff + (size_t)me * ep.ldc + n;
+                // even g: row me <- own left block, row me + 1 <- the neighbour's left block;
+                // odd g:  row me <- the neighbour's right block, row me + 1 <- own right block
+                *reinterpret_cast<double2*>(c) = odd ? make_double2(r0, r1) : make_double2(a0, a1);
+                *reinterpret_cast<double2*>(c + ep.ldc) = odd ? make_double2(b0, b1) : make_double2(r0, r1);
+            }
+        }
+        return 0.0;
+    }
+#endif
     #pragma unroll
     for (int i = 0; i < MI; ++i) {
         const int m = m0 + wm * T::WM + i * 8 + g;
