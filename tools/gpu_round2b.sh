@@ -17,6 +17,6 @@ python tools/batch_gemm_time.py 343 1024 343 512 49 512 > gpurun_out/batch_gemm_
 python tools/strassen_probe.py 2047 4095 8192 > gpurun_out/strassen_probe.log 2>&1
 ncu --set full --import-source on --clock-control none -k regex:"dgemm_nt" -s 3 -c 1 \
   -o gpurun_out/dgemm_batch343_full python tools/batch_gemm_time.py 343 1024 > gpurun_out/ncu_batch343.log 2>&1; echo ncu_full_rc=$?
-ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
-  -k regex:"strassen|dgemm_nt" -c 60 --csv --kernel-name-base demangled --log-file gpurun_out/strassen_passes.csv \
+STRASSEN_PROBE_LEVELS=3 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
+  -k regex:"strassen|dgemm_nt" -c 24 --csv --kernel-name-base demangled --log-file gpurun_out/strassen_passes.csv \
   python tools/strassen_probe.py 8192 > gpurun_out/ncu_strassen_passes.log 2>&1; echo ncu_passes_rc=$?
