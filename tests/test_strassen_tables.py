@@ -80,3 +80,19 @@ def test_quadrant_digits_cover_the_block_grid():
         assert cells == set(itertools.product(range(2 ** L), repeat=2))
     # top-level quadrant = most significant digit: block rows >= 4 of an 8 x 8 grid belong to quadrants 2, 3
     assert all((quad_row(q, 3) >= 4) == (q >> 4 in (2, 3)) for q in range(64))
+
+
+def test_leaf_dimensions_of_the_baseline_shapes():
+    """Odd shapes are padded to a multiple of 2^(L+1) inside the passes (bench.py restates the
+    library's rule for its roofline block): cfg5 q = 8192 runs 1024^3 leaves, cfg4 q = 4095 and
+    cfg3 q = 2047 run 512^3 leaves."""
+    import os
+    import sys
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+
+    assert bench.strassen_leaf(8192, 3) == 1024
+    assert bench.strassen_leaf(4095, 3) == 512
+    assert bench.strassen_leaf(2047, 2) == 512
+    assert bench.strassen_leaf(319, 2) == 80 and bench.strassen_leaf(319, 2) % 2 == 0
