@@ -8,7 +8,8 @@ system of each (cfg3: the elliptic system, K = 10; cfg4: IMEX step 0, rhs
 from u0 and the t = 0 source, warm start u0, K = 3; cfg5: both species'
 step-0 systems of imex_euler_rds, K = 2) runs K MO-PCG iterations with the
 stop rule disabled on the device (reference preconditioner as dense-inverse
-GEMMs and as banded SPIKE solves) and in the oracle; the K-th iterates and
+products -- on the Strassen schedule at these sizes -- and as banded SPIKE
+solves) and in the oracle; the K-th iterates and
 the residual histories must agree to <= 1e-10.  The oracle is the checker
 (dense GEMM apply, LU preconditioner), never the measured path.
 """
@@ -60,6 +61,8 @@ def _fixed_budget(op, kind, kw, x, y, terms, opre, rhs, u0, K):
     assert ref["iterations"] == K
     for mode in ("inverse", "banded"):
         pre = pb.make_preconditioner(kind, x, y, mode=mode, **kw)
+        if mode == "inverse":  # the BASELINE sizes of cfg3-cfg5 run the dense products on the Strassen schedule
+            assert pre.uses_strassen() == (3 if min(op.shape) >= 4000 else 2)
         rep = pb.mo_pcg(op, rhs, precond=pre, stop=pb.fixed_budget(), u0=u0, max_iter=K)
         assert rep.iterations == K and rep.stop_reason == "max_iter", mode
         assert relerr(rep.solution, ref["solution"]) <= 1e-10, mode
